@@ -1,0 +1,245 @@
+/*
+ * gridot_b200.h -- C ABI of the B200-native quantized-Wasserstein hot path.
+ *
+ * One shared library, paper_2506_00976_b200/csrc/libgridot_b200.so, exports
+ * these entry points.  They replace the fine-resolution stages of the
+ * reference Python package `gridot` (paths relative to the reference root
+ * pkg/src/gridot/); INTEGRATION.md shows the ctypes binding the reference
+ * would add to call them.
+ *
+ * Conventions
+ *   - Plain C types only.  Device buffers are caller-owned (allocated by the
+ *     caller, e.g. through PyTorch's caching allocator); `stream` is a
+ *     cudaStream_t passed as void*.  Calls are stream-ordered and reentrant;
+ *     there is no global mutable state.
+ *   - Grids: `ndim` axes (1..GDT_MAX_DIM), fine lengths `dims[ndim]`, flat
+ *     index axis-1-fastest (measures.py:3-6).  Kernels taking `kappa` require
+ *     every dims[a] to be a multiple of kappa (callers pad first with
+ *     gdt_pad_f64, the zero padding of measures.py:236-245).
+ *   - Batched calls process `batch` independent pairs laid out
+ *     [batch, cells] contiguously.
+ *   - Return value: GDT_OK or a negative GDT_ERR_*; per-pair outcomes of the
+ *     iterative stages are reported in an int32 status array (GDT_PAIR_*),
+ *     mapped by the Python layer onto the reference exception classes
+ *     (errors.py).  No C++ exception crosses the ABI.
+ */
+#ifndef GRIDOT_B200_H
+#define GRIDOT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GDT_MAX_DIM 4
+
+enum {
+    GDT_OK = 0,
+    GDT_ERR_ARG = -1,          /* invalid argument (shape, kappa, p, ndim) */
+    GDT_ERR_CUDA = -2,         /* CUDA launch / runtime error */
+    GDT_ERR_NOMEM = -3,        /* host allocation failed */
+    GDT_ERR_UNSUPPORTED = -4   /* valid request this build does not implement */
+};
+
+/* per-pair status codes of the iterative stages */
+enum {
+    GDT_PAIR_OK = 0,
+    GDT_PAIR_ZERO_DENOM_ROW = 1,  /* ZeroDenominatorError, sinkhorn.py:125-128 */
+    GDT_PAIR_ZERO_DENOM_COL = 2,  /* ZeroDenominatorError, sinkhorn.py:131-134 */
+    GDT_PAIR_OVERFLOW = 3         /* NumericOverflowError, sinkhorn.py:88-98    */
+};
+
+/* simplex status codes (_simplex.py:26-28) */
+enum { GDT_LP_OPTIMAL = 0, GDT_LP_PIVOT_LIMIT = 1, GDT_LP_DISCONNECTED = 2 };
+
+/* precision / order modes */
+enum {
+    GDT_MODE_EXACT = 0,  /* fp64, reference summation order (bit-exact) */
+    GDT_MODE_FAST = 1    /* fp32 mode of BASELINE.json: any order, fp32 where safe */
+};
+
+const char *gdt_version(void);
+/* Human-readable text of the last error raised on the calling thread. */
+const char *gdt_last_error(void);
+
+/* ---- layout helpers -------------------------------------------------- */
+
+/* Zero-pad every axis up to a multiple of kappa.  Replaces pad_measure,
+ * measures.py:236-245.  out: [batch, prod(padded dims)]. */
+int gdt_pad_f64(const double *in, double *out, int64_t batch, int ndim,
+                const int64_t *dims, int kappa, void *stream);
+
+/* ---- K1: SumPool ------------------------------------------------------ */
+
+/* Block sums, accumulated in ascending fine flat index (bit-exact with
+ * np.add.at).  Replaces coarsen_measure, measures.py:257-267.
+ * fine: [batch, prod(dims)] -> coarse: [batch, prod(dims)/kappa^ndim]. */
+int gdt_sumpool_f64(const double *fine, double *coarse, int64_t batch, int ndim,
+                    const int64_t *dims, int kappa, void *stream);
+
+/* ---- K2: marginally weighted coarse cost C-bar ------------------------ */
+
+/* C-bar_kl = sum_{x in X_k, y in Y_l} rho(x,y)^p mu_x nu_y / (mu~_k nu~_l);
+ * entries with mu~_k nu~_l == 0 take centre_cost[k,l] and are flagged in
+ * `unused`.  Replaces weighted_cost_matrix, costs.py:128-171.
+ *   mu, nu        [batch, N]   fine masses (padded grid, N = prod(dims))
+ *   mu_c, nu_c    [batch, n]   their SumPool (gdt_sumpool_f64)
+ *   centre_cost   [n, n]       C-tilde (costs.py:121-125), shared by the batch
+ *   cost_table    [max_sq+1]   rho^p of integer squared distance, required
+ *                              when p is neither 1 nor 2 (NULL otherwise)
+ *   out           [batch, n, n], unused [batch, n, n] (uint8)
+ * mode GDT_MODE_EXACT reproduces the reference's rounding order exactly;
+ * GDT_MODE_FAST uses block moments for p == 2 (fp64) and fp32 FFMA tiles
+ * otherwise. */
+int gdt_weighted_cost(const double *mu, const double *nu, const double *mu_c,
+                      const double *nu_c, const double *centre_cost,
+                      const double *cost_table, int64_t max_sq, double *out,
+                      uint8_t *unused, int64_t batch, int ndim, const int64_t *dims,
+                      int kappa, double p, int mode, void *stream);
+
+/* ---- K5/K6: primal upscaling (IPF + pricing + TV) --------------------- */
+
+/* Block-sparse primal upscaling of a coarse plan, refit by IPF to the fine
+ * marginals, priced, plus the weighted-TV inner sums.  Replaces the body of
+ * primal_upscaling_upper_bound, quantized.py:311-363, with ipf_fit,
+ * sinkhorn.py:101-142, over the upscaled coupling of upscale_coupling,
+ * quantized.py:119-159 -- the fine coupling is never materialised.
+ *   mu, nu        [batch, N] fine masses (padded grid)
+ *   arc_off       [batch+1]  pair b owns arcs [arc_off[b], arc_off[b+1])
+ *   row_ptr       [batch, n+1]  per pair CSR over coarse rows (offsets
+ *                 relative to arc_off[b]); arcs sorted by (row, col)
+ *   row_arc_col, row_arc_mass   [total arcs]
+ *   col_ptr       [batch, n+1]  CSC over coarse columns; entries sorted by
+ *                 (col, row); col_arc_row, col_arc_mass [total arcs]
+ *   kernel_w      [m, m] paired kernel weights (m = kappa^ndim; row = source
+ *                 offset, col = target offset, quantized.py:95-103)
+ *   kernel_uniform  non-zero when all kernel_w entries are equal
+ *   xi            per-pair stop threshold; xi < 0 selects the reference
+ *                 default 1e-9 * (|supp mu| + |supp nu|) (quantized.py:319-320)
+ *   max_iter      sweep cap (>= 1)
+ *   cost_table    [max_sq+1] rho^p by integer squared distance for pricing
+ *                 (required when p is neither 1 nor 2, else may be NULL)
+ *   out           [batch, 8]: {transport_p, tv_inner_mu, tv_inner_nu,
+ *                 marginal_gap, iterations, converged, support_count, spare}
+ *                 where transport_p = sum fitted*cost (before ^(1/p)) and
+ *                 tv_inner_* = sum w_i |hat_i - marg_i| (before the root)
+ *   status        [batch] GDT_PAIR_*
+ *   scratch       device workspace of gdt_primal_scratch_bytes() bytes */
+int64_t gdt_primal_scratch_bytes(int64_t batch, int ndim, const int64_t *dims,
+                                 int kappa, int kernel_uniform);
+int gdt_primal_upscale(const double *mu, const double *nu, const int64_t *arc_off,
+                       const int32_t *row_ptr, const int32_t *row_arc_col,
+                       const double *row_arc_mass, const int32_t *col_ptr,
+                       const int32_t *col_arc_row, const double *col_arc_mass,
+                       const double *kernel_w, int kernel_uniform, const double *xi,
+                       int64_t max_iter, double p, int64_t batch, int ndim,
+                       const int64_t *dims, int kappa, const double *cost_table,
+                       int64_t max_sq, double *out, int32_t *status, void *scratch,
+                       void *stream);
+
+/* Generic IPF on an explicit CSR kernel (rows = sources) with its CSC twin;
+ * per-row sums in ascending column, per-column sums in ascending row (the
+ * order of scipy's csr/csc matvec).  Replaces ipf_fit, sinkhorn.py:101-142,
+ * for sparse/dense kernels and the one-ring fallback of quantized.py:335-344.
+ *   out_a [nr], out_b [nc], out_kb [nr], out_kta [nc]
+ *   info  [4]: {iterations, marginal_gap, converged, spare}; status [1]. */
+int gdt_ipf_csr(const int64_t *indptr, const int32_t *indices, const double *data,
+                const int64_t *t_indptr, const int32_t *t_indices, const double *t_data,
+                const double *mu, const double *nu, int64_t nr, int64_t nc, double xi,
+                int64_t max_iter, double *out_a, double *out_b, double *out_kb,
+                double *out_kta, double *info, int32_t *status, void *stream);
+
+/* Pricing of a fitted COO coupling on a grid: sum_e (a[row_e]*mass_e)*b[col_e]
+ * * rho(x_row, x_col)^p.  Replaces quantized.py:346-355 for explicit
+ * couplings.  row/col are fine flat ids of the padded grid; a, b, are the
+ * full-grid scaling vectors.  out [1] = the sum before ^(1/p). */
+int gdt_price_coo(const int64_t *row, const int64_t *col, const double *mass,
+                  int64_t nnz, const double *a, const double *b, const double *cost_table,
+                  int64_t max_sq, double p, int ndim, const int64_t *dims, double *out,
+                  void *stream);
+
+/* Weighted-TV inner sums sum_i w_i |x_i - y_i| (weighted_tv,
+ * measures.py:298-315, before the 1/p root).  `weights` [N] may be NULL, in
+ * which case w_i = rho(centre, x_i)^p of the grid (tv_weights,
+ * measures.py:289-295) is generated on the fly.  x, y [batch, N]; out [batch]. */
+int gdt_weighted_tv_inner(const double *x, const double *y, int64_t batch, int ndim,
+                          const int64_t *dims, double p, const double *weights,
+                          double *out, void *stream);
+
+/* ---- K7-K10: dual upscaling ------------------------------------------ */
+
+/* f_ext_k = min_{l in supp} (C~[k, dst[l]] - g[l]) (quantized.py:504-505).
+ *   g [batch, n] (entries past supp_len[b] ignored), dst [batch, n] int32,
+ *   supp_len [batch], centre_cost [n, n], f_ext [batch, n]. */
+int gdt_coarse_ctransform(const double *g, const int32_t *dst, const int32_t *supp_len,
+                          const double *centre_cost, int64_t n, int64_t batch,
+                          double *f_ext, void *stream);
+
+/* d-linear (method 0) or nearest (method 1) extension of a potential given on
+ * a full coarse lattice to the fine grid `dims` (unpadded; clamped
+ * extrapolation).  `axes` (device) holds the sorted lattice coordinates of
+ * each axis back to back (cdims[0] values, then cdims[1], ...); for the bounds
+ * these are the block centres kappa*b + (kappa+1)/2.  Replaces
+ * interpolate_potential, quantized.py:388-447 (bit-exact, no FMA). */
+int gdt_interpolate(const double *coarse, double *fine, int64_t batch, int ndim,
+                    const int64_t *dims, const int64_t *cdims, const double *axes, int method,
+                    void *stream);
+
+/* Grid c-transform out_j = min_i rho(x_i, x_j)^p - v_i on one grid (the
+ * source and target point sets of dual_upscaling_lower_bound coincide, so the
+ * "target" and "source" directions of c_transform, quantized.py:450-484, are
+ * the same operator).  dtype 0 = fp64, 1 = fp32 arithmetic and `out` type;
+ * in_dtype is the type of `v` (fp64 input with fp32 arithmetic is allowed).
+ * p == 2 uses per-axis separability (O(d N^{d+1})); other p run a tiled
+ * brute-force min-plus with costs rho^p read from `cost_table` (indexed by
+ * the integer squared distance; required for every p != 2).
+ * If `mass` and `dot_out` are non-NULL, also writes dot_out[b] =
+ * sum_j out_j * mass_j in fp64 (the dual value terms, quantized.py:512). */
+int gdt_ctransform_grid(const void *v, void *out, int64_t batch, int ndim,
+                        const int64_t *dims, double p, int dtype, int in_dtype,
+                        const double *cost_table, int64_t max_sq, const double *mass,
+                        double *dot_out, void *scratch, int64_t scratch_bytes, void *stream);
+int64_t gdt_ctransform_scratch_bytes(int64_t batch, int ndim, const int64_t *dims,
+                                     double p, int dtype);
+
+/* c-transform between arbitrary point clouds (CostSpec, costs.py:56-99):
+ * direction 0 ("target"): out_j = min_i C(xs_i, xt_j) - v_i over ns sources;
+ * direction 1 ("source"): out_i = min_j C(xs_i, xt_j) - v_j.  fp64, costs
+ * from the sequential squared distance then ^(p/2) (p=1 sqrt, p=2 as is). */
+int gdt_ctransform_points(const double *xs, const double *xt, int64_t ns, int64_t nt,
+                          int ndim, double p, const double *v, int direction, double *out,
+                          void *stream);
+
+/* sum_i a_i * b_i per row of [batch, n] (fp64 block reduction). */
+int gdt_batched_dot(const double *a, const double *b, int64_t batch, int64_t n,
+                    double *out, void *stream);
+
+/* ---- host coarse LP (stays on the host, _simplex.py) ------------------ */
+
+/* Primal network simplex with the reference's pivot rules (northwest-corner
+ * start, block pricing with Bland fallback, exact subtree relabel,
+ * _simplex.py:31-361).  Host memory.  C row-major [ns, nt]; bi/bj/bf
+ * [ns+nt-1]; u [ns]; v [nt].  block_size/max_pivots <= 0 select the
+ * reference defaults.  Returns GDT_LP_* (>= 0) or GDT_ERR_*. */
+int gdt_transport_simplex(const double *C, const double *sup, const double *dem,
+                          int64_t ns, int64_t nt, int64_t block_size, int64_t max_pivots,
+                          double tol, int64_t *bi, int64_t *bj, double *bf, double *u,
+                          double *v, int64_t *pivots);
+
+/* `count` independent problems solved on `threads` host threads (<=0: all
+ * cores).  Problem q reads C + c_off[q], sup + s_off[q], dem + t_off[q] with
+ * sizes ns[q] x nt[q] and writes bi/bj/bf + b_off[q], u + s_off[q],
+ * v + t_off[q]; status[q], pivots[q].  Releases no locks (pure C). */
+int gdt_transport_simplex_batch(int64_t count, const double *C, const int64_t *c_off,
+                                const double *sup, const double *dem, const int64_t *s_off,
+                                const int64_t *t_off, const int64_t *ns, const int64_t *nt,
+                                const int64_t *b_off, double tol, int64_t *bi, int64_t *bj,
+                                double *bf, double *u, double *v, int32_t *status,
+                                int64_t *pivots, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRIDOT_B200_H */

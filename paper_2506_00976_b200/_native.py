@@ -1,0 +1,99 @@
+"""ctypes binding of libgridot_b200.so (include/gridot_b200.h).
+
+The shared library is built in-tree by ``paper_2506_00976_b200.csrc.build``
+(``__graft_entry__.build()``).  There is no fallback: if the library is
+missing or a CUDA device is required and absent, the calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import GridotError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "csrc", "libgridot_b200.so")
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+I32 = ctypes.c_int
+D = ctypes.c_double
+
+# name -> (restype, argtypes); mirrors include/gridot_b200.h
+_SIGNATURES = {
+    "gdt_version": (ctypes.c_char_p, []),
+    "gdt_last_error": (ctypes.c_char_p, []),
+    "gdt_pad_f64": (I32, [P, P, I64, I32, P, I32, P]),
+    "gdt_sumpool_f64": (I32, [P, P, I64, I32, P, I32, P]),
+    "gdt_weighted_cost": (I32, [P, P, P, P, P, P, I64, P, P, I64, I32, P, I32, D, I32, P]),
+    "gdt_primal_scratch_bytes": (I64, [I64, I32, P, I32, I32]),
+    "gdt_primal_upscale": (I32, [P, P, P, P, P, P, P, P, P, P, I32, P, I64, D, I64, I32, P, I32,
+                                 P, I64, P, P, P, P]),
+    "gdt_ipf_csr": (I32, [P, P, P, P, P, P, P, P, I64, I64, D, I64, P, P, P, P, P, P, P]),
+    "gdt_price_coo": (I32, [P, P, P, I64, P, P, P, I64, D, I32, P, P, P]),
+    "gdt_weighted_tv_inner": (I32, [P, P, I64, I32, P, D, P, P, P]),
+    "gdt_coarse_ctransform": (I32, [P, P, P, P, I64, I64, P, P]),
+    "gdt_interpolate": (I32, [P, P, I64, I32, P, P, P, I32, P]),
+    "gdt_ctransform_grid": (I32, [P, P, I64, I32, P, D, I32, I32, P, I64, P, P, P, I64, P]),
+    "gdt_ctransform_scratch_bytes": (I64, [I64, I32, P, D, I32]),
+    "gdt_ctransform_points": (I32, [P, P, I64, I64, I32, D, P, I32, P, P]),
+    "gdt_batched_dot": (I32, [P, P, I64, I64, P, P]),
+    "gdt_transport_simplex": (I32, [P, P, P, I64, I64, I64, I64, D, P, P, P, P, P, P]),
+    "gdt_transport_simplex_batch": (I32, [I64, P, P, P, P, P, P, P, P, P, D, P, P, P, P, P, P,
+                                          P, I32]),
+}
+
+_lib = None
+
+
+class NativeError(GridotError):
+    """A C-ABI call failed (bad arguments or a CUDA error)."""
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(
+                f"{LIB_PATH} is missing; build it with "
+                "`python -m paper_2506_00976_b200.csrc.build` (there is no CPU fallback)")
+        handle = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGNATURES)
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().gdt_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed with status {rc}: {msg}")
+
+
+def ptr(t) -> int | None:
+    """Raw device/host pointer of a torch tensor or numpy array (None -> NULL)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def i64s(values) -> ctypes.Array:
+    arr = (ctypes.c_int64 * len(values))(*[int(v) for v in values])
+    return arr
+
+
+def stream_handle(device=None) -> int:
+    import torch
+
+    return torch.cuda.current_stream(device).cuda_stream

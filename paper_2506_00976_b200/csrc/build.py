@@ -1,0 +1,80 @@
+"""Build libgridot_b200.so in-tree with nvcc (sm_100a) and g++.
+
+    python -m paper_2506_00976_b200.csrc.build        # incremental
+    python -m paper_2506_00976_b200.csrc.build --force
+
+Object files go to csrc/_obj/; the shared library lands next to this file so
+it travels to the GPU box with the repo snapshot (git-ignored).
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+OBJ = os.path.join(HERE, "_obj")
+LIB = os.path.join(HERE, "libgridot_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = os.environ.get("CXX", "g++")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+           "--expt-relaxed-constexpr"] + ARCH
+# files whose arithmetic restates the reference's rounding order: no FMA
+NO_FMA = {"grid_kernels.cu", "primal.cu", "cbar.cu"}
+CU = ["grid_kernels.cu", "cbar.cu", "primal.cu", "ctransform.cu"]
+CPP = ["simplex.cpp"]
+HEADERS = ["common.cuh", os.path.join("..", "..", "include", "gridot_b200.h")]
+
+
+def _newer(src_list, target):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in src_list)
+
+
+def _run(cmd, log):
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    with open(log, "w") as fh:
+        fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"build failed: {' '.join(cmd)}")
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    hdrs = [os.path.join(HERE, h) for h in HEADERS]
+    objs = []
+    for f in CU:
+        src = os.path.join(HERE, f)
+        obj = os.path.join(OBJ, f + ".o")
+        objs.append(obj)
+        if force or _newer([src] + hdrs + [__file__], obj):
+            flags = NVFLAGS + (["--fmad=false"] if f in NO_FMA else [])
+            _run([NVCC] + flags + ["-c", src, "-o", obj], os.path.join(OBJ, f + ".log"))
+            if verbose:
+                print("built", f)
+    for f in CPP:
+        src = os.path.join(HERE, f)
+        obj = os.path.join(OBJ, f + ".o")
+        objs.append(obj)
+        if force or _newer([src] + hdrs + [__file__], obj):
+            _run([CXX, "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
+                  "-pthread", "-c", src, "-o", obj], os.path.join(OBJ, f + ".log"))
+            if verbose:
+                print("built", f)
+    if force or _newer(objs, LIB):
+        _run([NVCC, "-shared"] + ARCH + ["-o", LIB] + objs + ["-lpthread"],
+             os.path.join(OBJ, "link.log"))
+        if verbose:
+            print("linked", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

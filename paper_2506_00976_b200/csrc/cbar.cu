@@ -1,0 +1,285 @@
+// K2: marginally weighted coarse cost C-bar (costs.py:128-171).
+//
+// Exact mode restates the reference's numpy order bit for bit:
+//   s_{k,c} = sequential over the block's rows r (ascending fine index) of
+//             (C_rc * mu_r) * nu_c                       (costs.py:158-162)
+//   numer_kl = numpy pairwise sum of s_{k,c} over c in Y_l (ascending)
+//   C-bar_kl = numer_kl / (mu~_k * nu~_l), or C-tilde_kl where that is 0.
+// A CTA owns (pair, KT row blocks, LT column blocks); each thread owns
+// column cells, keeps the KT partial sums in registers/shared memory, and the
+// pairwise block sums are formed from shared memory.  Products use
+// __dmul_rn/__dadd_rn so no FMA contraction can change the rounding.
+//
+// Fast mode (the fp32 mode of BASELINE.json): p == 2 uses block moments --
+// sum_{r,c} |x_r - y_c|^2 mu_r nu_c expands into per-block 0th/1st/2nd
+// moments about the block centres, O(N^d + n^2d) instead of O(N^2d) -- and
+// other p use the same tiling as exact mode in fp32 FFMA with an fp64 block
+// sum.
+#include "common.cuh"
+
+namespace gdt {
+
+struct Offsets {  // within-block offset vectors t -> (t_0..t_{d-1})
+    int8_t v[GDT_MAX_DIM];
+};
+
+__device__ __forceinline__ void unravel_block(int64_t id, const Grid &c, int64_t *out) {
+    for (int a = c.nd - 1; a >= 0; --a) {
+        out[a] = id / c.stride[a];
+        id -= out[a] * c.stride[a];
+    }
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(256) cbar_tile_kernel(
+    const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ mu_c,
+    const double *__restrict__ nu_c, const double *__restrict__ Ccentre,
+    const double *__restrict__ table, double *__restrict__ out, uint8_t *__restrict__ unused,
+    Grid f, Grid c, int kappa, int m, double p, int KT, int LT) {
+    extern __shared__ double smem[];
+    using T = typename std::conditional<EXACT, double, float>::type;
+    const int cols = LT * m;
+    T *S = reinterpret_cast<T *>(smem);                       // [KT][cols]
+    double *mus = smem + (KT * cols * sizeof(T) + 7) / 8;     // [KT][m]
+    int *roff = reinterpret_cast<int *>(mus + KT * m);        // [m][nd] offsets
+
+    const int64_t b = blockIdx.z;
+    const int64_t k0 = (int64_t)blockIdx.y * KT, l0 = (int64_t)blockIdx.x * LT;
+    const int64_t n = c.cells;
+    const double *mub = mu + b * f.cells, *nub = nu + b * f.cells;
+
+    for (int t = threadIdx.x; t < m; t += blockDim.x) {
+        int rem = t;
+        for (int a = 0; a < f.nd; ++a) {
+            roff[t * GDT_MAX_DIM + a] = rem % kappa;
+            rem /= kappa;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < KT * m; i += blockDim.x) {
+        const int kk = i / m, t = i - kk * m;
+        const int64_t k = k0 + kk;
+        double v = 0.0;
+        if (k < n) {
+            int64_t kc[GDT_MAX_DIM];
+            unravel_block(k, c, kc);
+            int64_t off = 0;
+            for (int a = 0; a < f.nd; ++a) off += (kc[a] * kappa + roff[t * GDT_MAX_DIM + a]) * f.stride[a];
+            v = mub[off];
+        }
+        mus[i] = v;
+    }
+    __syncthreads();
+
+    for (int cl = threadIdx.x; cl < cols; cl += blockDim.x) {
+        const int64_t l = l0 + cl / m;
+        const int s = cl % m;
+        if (l >= n) {
+            for (int kk = 0; kk < KT; ++kk) S[kk * cols + cl] = (T)0;
+            continue;
+        }
+        int64_t lc[GDT_MAX_DIM], xc[GDT_MAX_DIM];
+        unravel_block(l, c, lc);
+        int64_t coff = 0;
+        for (int a = 0; a < f.nd; ++a) {
+            xc[a] = lc[a] * kappa + roff[s * GDT_MAX_DIM + a];
+            coff += xc[a] * f.stride[a];
+        }
+        const double nuc = nub[coff];
+        for (int kk = 0; kk < KT; ++kk) {
+            const int64_t k = k0 + kk;
+            if (k >= n) {
+                S[kk * cols + cl] = (T)0;
+                continue;
+            }
+            int64_t kc[GDT_MAX_DIM];
+            unravel_block(k, c, kc);
+            int64_t base[GDT_MAX_DIM];
+            for (int a = 0; a < f.nd; ++a) base[a] = kc[a] * kappa - xc[a];
+            if (EXACT) {
+                double acc = 0.0;
+                for (int t = 0; t < m; ++t) {
+                    int64_t sq = 0;
+                    for (int a = 0; a < f.nd; ++a) {
+                        const int64_t dd = base[a] + roff[t * GDT_MAX_DIM + a];
+                        sq += dd * dd;
+                    }
+                    const double cost = cost_from_sq(sq, p, table);
+                    const double term = __dmul_rn(__dmul_rn(cost, mus[kk * m + t]), nuc);
+                    acc = t == 0 ? term : __dadd_rn(acc, term);
+                }
+                S[kk * cols + cl] = (T)acc;
+            } else {
+                float acc = 0.0f;
+                for (int t = 0; t < m; ++t) {
+                    int sq = 0;
+                    for (int a = 0; a < f.nd; ++a) {
+                        const int dd = (int)base[a] + roff[t * GDT_MAX_DIM + a];
+                        sq += dd * dd;
+                    }
+                    const float cost = p == 2.0 ? (float)sq
+                                       : p == 1.0 ? __fsqrt_rn((float)sq)
+                                                  : (float)table[sq];
+                    acc = fmaf(cost, (float)mus[kk * m + t], acc);
+                }
+                S[kk * cols + cl] = (T)(acc * (float)nuc);
+            }
+        }
+    }
+    __syncthreads();
+
+    for (int o = threadIdx.x; o < KT * LT; o += blockDim.x) {
+        const int kk = o / LT, ll = o - kk * LT;
+        const int64_t k = k0 + kk, l = l0 + ll;
+        if (k >= n || l >= n) continue;
+        const T *row = S + kk * cols + ll * m;
+        double numer;
+        if (EXACT) {
+            numer = np_pairwise([&](int64_t i) { return (double)row[i]; }, m);
+        } else {
+            numer = 0.0;
+            for (int i = 0; i < m; ++i) numer += (double)row[i];
+        }
+        const double denom = __dmul_rn(mu_c[b * n + k], nu_c[b * n + l]);
+        const int64_t oi = (b * n + k) * n + l;
+        const bool un = denom == 0.0;
+        out[oi] = un ? Ccentre[k * n + l] : __ddiv_rn(numer, denom);
+        unused[oi] = un ? 1 : 0;
+    }
+}
+
+// ---- fast p == 2: block moments ------------------------------------------
+// mom layout per (pair, block): [M1_0 .. M1_{d-1}, M2] about the block centre.
+__global__ void moments_kernel(const double *__restrict__ fine, double *__restrict__ mom,
+                               int64_t batch, Grid f, Grid c, int kappa) {
+    const int64_t total = batch * c.cells;
+    const int W = f.nd + 1;
+    const double ctr = (kappa - 1) / 2.0;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = idx / c.cells, k = idx - b * c.cells;
+        int64_t kc[GDT_MAX_DIM];
+        unravel_block(k, c, kc);
+        int64_t origin = b * f.cells;
+        for (int a = 0; a < f.nd; ++a) origin += kc[a] * kappa * f.stride[a];
+        double m1[GDT_MAX_DIM] = {0, 0, 0, 0}, m2 = 0.0;
+        const int m = (int)ipow(kappa, f.nd);
+        for (int t = 0; t < m; ++t) {
+            int rem = t;
+            int64_t off = 0;
+            double r2 = 0.0, dl[GDT_MAX_DIM];
+            for (int a = 0; a < f.nd; ++a) {
+                const int o = rem % kappa;
+                rem /= kappa;
+                off += o * f.stride[a];
+                dl[a] = o - ctr;
+                r2 += dl[a] * dl[a];
+            }
+            const double w = fine[origin + off];
+            for (int a = 0; a < f.nd; ++a) m1[a] += w * dl[a];
+            m2 += w * r2;
+        }
+        double *o = mom + idx * W;
+        for (int a = 0; a < f.nd; ++a) o[a] = m1[a];
+        o[f.nd] = m2;
+    }
+}
+
+__global__ void cbar_moments_kernel(const double *__restrict__ mu_c, const double *__restrict__ nu_c,
+                                    const double *__restrict__ mm, const double *__restrict__ nm,
+                                    const double *__restrict__ Ccentre, double *__restrict__ out,
+                                    uint8_t *__restrict__ unused, int64_t batch, Grid c,
+                                    int kappa) {
+    const int64_t n = c.cells;
+    const int64_t total = batch * n * n;
+    const int W = c.nd + 1;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = idx / (n * n);
+        const int64_t kl = idx - b * n * n;
+        const int64_t k = kl / n, l = kl - k * n;
+        const double M0 = mu_c[b * n + k], N0 = nu_c[b * n + l];
+        const double denom = __dmul_rn(M0, N0);
+        if (denom == 0.0) {
+            out[idx] = Ccentre[k * n + l];
+            unused[idx] = 1;
+            continue;
+        }
+        int64_t kc[GDT_MAX_DIM], lc[GDT_MAX_DIM];
+        unravel_block(k, c, kc);
+        unravel_block(l, c, lc);
+        const double *Mk = mm + (b * n + k) * W, *Nl = nm + (b * n + l) * W;
+        double d2 = 0.0, cross = 0.0, m1n1 = 0.0;
+        for (int a = 0; a < c.nd; ++a) {
+            const double D = (double)(kappa * (kc[a] - lc[a]));
+            d2 += D * D;
+            cross += D * (Mk[a] * N0 - M0 * Nl[a]);
+            m1n1 += Mk[a] * Nl[a];
+        }
+        const double numer = denom * d2 + 2.0 * cross + Mk[c.nd] * N0 + M0 * Nl[c.nd] - 2.0 * m1n1;
+        out[idx] = numer / denom;
+        unused[idx] = 0;
+    }
+}
+
+}  // namespace gdt
+
+using namespace gdt;
+
+extern "C" int gdt_weighted_cost(const double *mu, const double *nu, const double *mu_c,
+                                 const double *nu_c, const double *centre_cost,
+                                 const double *cost_table, int64_t max_sq, double *out,
+                                 uint8_t *unused, int64_t batch, int ndim, const int64_t *dims,
+                                 int kappa, double p, int mode, void *stream) {
+    Grid f, c;
+    GDT_CHECK_ARG(make_grid(f, ndim, dims) && make_coarse(c, f, kappa),
+                  "gdt_weighted_cost: dims must be positive multiples of kappa");
+    GDT_CHECK_ARG(p >= 1.0 && batch >= 0, "gdt_weighted_cost: p must be >= 1");
+    GDT_CHECK_ARG(mode == GDT_MODE_EXACT || mode == GDT_MODE_FAST, "gdt_weighted_cost: bad mode");
+    int64_t need_sq = 0;
+    for (int a = 0; a < ndim; ++a) need_sq += (dims[a] - 1) * (dims[a] - 1);
+    GDT_CHECK_ARG(p == 1.0 || p == 2.0 || (cost_table != nullptr && max_sq >= need_sq),
+                  "gdt_weighted_cost: cost_table required for p not in {1, 2}");
+    if (batch == 0) return GDT_OK;
+    cudaStream_t st = as_stream(stream);
+    const int m = (int)ipow(kappa, ndim);
+    const int64_t n = c.cells;
+    if (mode == GDT_MODE_FAST && p == 2.0) {
+        const int W = ndim + 1;
+        double *mom = nullptr;
+        if (cudaMallocAsync(&mom, sizeof(double) * 2 * batch * n * W, st) != cudaSuccess)
+            return cuda_status("gdt_weighted_cost: workspace");
+        moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(mu, mom, batch, f, c, kappa);
+        moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(nu, mom + batch * n * W, batch,
+                                                                   f, c, kappa);
+        cbar_moments_kernel<<<grid_size(batch * n * n, 256), 256, 0, st>>>(
+            mu_c, nu_c, mom, mom + batch * n * W, centre_cost, out, unused, batch, c, kappa);
+        cudaFreeAsync(mom, st);
+        return cuda_status("gdt_weighted_cost(moments)");
+    }
+    // tile shape: ~256 columns per CTA, KT row blocks per CTA
+    int LT = m >= 256 ? 1 : 256 / m;
+    if (LT > n) LT = (int)n;
+    const int KT = 8;
+    const int cols = LT * m;
+    const size_t elem = mode == GDT_MODE_EXACT ? sizeof(double) : sizeof(float);
+    size_t sbytes = ((KT * cols * elem + 7) / 8) * 8 + sizeof(double) * KT * m +
+                    sizeof(int) * m * GDT_MAX_DIM;
+    GDT_CHECK_ARG(sbytes <= 200 * 1024, "gdt_weighted_cost: kappa^d too large for this build");
+    dim3 grid((unsigned)((n + LT - 1) / LT), (unsigned)((n + KT - 1) / KT), (unsigned)batch);
+    if (mode == GDT_MODE_EXACT) {
+        if (sbytes > 48 * 1024)
+            cudaFuncSetAttribute(cbar_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sbytes);
+        cbar_tile_kernel<true><<<grid, 256, sbytes, st>>>(mu, nu, mu_c, nu_c, centre_cost, cost_table,
+                                                          out, unused, f, c, kappa, m, p, KT, LT);
+    } else {
+        if (sbytes > 48 * 1024)
+            cudaFuncSetAttribute(cbar_tile_kernel<false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes);
+        cbar_tile_kernel<false><<<grid, 256, sbytes, st>>>(mu, nu, mu_c, nu_c, centre_cost,
+                                                           cost_table, out, unused, f, c, kappa, m,
+                                                           p, KT, LT);
+    }
+    return cuda_status("gdt_weighted_cost");
+}

@@ -1,0 +1,311 @@
+// Grid primitives: padding, SumPool (K1), potential interpolation (K8),
+// coarse c-transform (K7), weighted-TV inner sums and batched dots (K10).
+// Compiled with --fmad=false: every expression here is rounded exactly as
+// the reference's numpy expression it restates.
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace gdt {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int cuda_status(const char *where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string(where) + ": " + cudaGetErrorString(e));
+        return GDT_ERR_CUDA;
+    }
+    return GDT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// padding (measures.py:236-245)
+// ---------------------------------------------------------------------------
+__global__ void pad_kernel(const double *__restrict__ in, double *__restrict__ out,
+                           int64_t batch, Grid src, Grid dst) {
+    const int64_t total = batch * dst.cells;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = idx / dst.cells;
+        int64_t rem = idx - b * dst.cells;
+        int64_t src_off = 0;
+        bool inside = true;
+        for (int a = dst.nd - 1; a >= 0; --a) {
+            const int64_t x = rem / dst.stride[a];
+            rem -= x * dst.stride[a];
+            if (x >= src.n[a]) inside = false;
+            src_off += x * src.stride[a];
+        }
+        out[idx] = inside ? in[b * src.cells + src_off] : 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1 SumPool: one thread per (pair, block); offsets visited in ascending fine
+// flat order, accumulator starts at 0.0 (np.add.at order, measures.py:266).
+// ---------------------------------------------------------------------------
+__global__ void sumpool_kernel(const double *__restrict__ fine, double *__restrict__ coarse,
+                               int64_t batch, Grid f, Grid c, int kappa) {
+    const int64_t total = batch * c.cells;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = idx / c.cells;
+        int64_t rem = idx - b * c.cells;
+        int64_t origin = 0;
+        for (int a = c.nd - 1; a >= 0; --a) {
+            const int64_t x = rem / c.stride[a];
+            rem -= x * c.stride[a];
+            origin += x * kappa * f.stride[a];
+        }
+        const double *src = fine + b * f.cells + origin;
+        const int K3 = c.nd > 3 ? kappa : 1, K2 = c.nd > 2 ? kappa : 1, K1 = c.nd > 1 ? kappa : 1;
+        double acc = 0.0;
+        for (int o3 = 0; o3 < K3; ++o3)
+            for (int o2 = 0; o2 < K2; ++o2)
+                for (int o1 = 0; o1 < K1; ++o1) {
+                    const double *row = src + o3 * f.stride[3] + o2 * f.stride[2] + o1 * f.stride[1];
+                    for (int o0 = 0; o0 < kappa; ++o0) acc = __dadd_rn(acc, row[o0]);
+                }
+        coarse[idx] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K8 interpolation (quantized.py:388-447).  `axes` holds the sorted coarse
+// axis values (np.unique of the centre columns) of every axis back to back.
+// i0 = clip(searchsorted(ax, q, 'right') - 1, 0, n-2), t = (q - c_i0) / span
+// rounded once and clipped to [0,1]; corners in itertools.product order (last
+// axis fastest), weights multiplied in axis order from 1.0, accumulated from
+// 0.0.  "nearest" = searchsorted(midpoints, q, 'left').
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t upper_count(const double *ax, int64_t n, double q) {
+    int64_t lo = 0, hi = n;  // number of ax[j] <= q
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ax[mid] <= q) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void interpolate_kernel(const double *__restrict__ coarse, double *__restrict__ fine,
+                                   int64_t batch, Grid f, Grid c, const double *__restrict__ axes,
+                                   int method) {
+    const int64_t total = batch * f.cells;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = idx / f.cells;
+        int64_t rem = idx - b * f.cells;
+        double q[GDT_MAX_DIM];
+        for (int a = f.nd - 1; a >= 0; --a) {
+            const int64_t x = rem / f.stride[a];
+            rem -= x * f.stride[a];
+            q[a] = (double)(x + 1);  // 1-based coordinate
+        }
+        const double *T = coarse + b * c.cells;
+        if (method == 1) {
+            int64_t off = 0, a0 = 0;
+            for (int a = 0; a < f.nd; ++a) {
+                const double *ax = axes + a0;
+                const int64_t n = c.n[a];
+                int64_t lo = 0, hi = n - 1;  // midpoints strictly below q
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    const double mp = __ddiv_rn(__dadd_rn(ax[mid], ax[mid + 1]), 2.0);
+                    if (mp < q[a]) lo = mid + 1;
+                    else hi = mid;
+                }
+                off += lo * c.stride[a];
+                a0 += n;
+            }
+            fine[idx] = T[off];
+            continue;
+        }
+        int64_t lo[GDT_MAX_DIM], hi[GDT_MAX_DIM];
+        double t[GDT_MAX_DIM];
+        int64_t a0 = 0;
+        for (int a = 0; a < f.nd; ++a) {
+            const double *ax = axes + a0;
+            const int64_t n = c.n[a];
+            a0 += n;
+            int64_t i0 = upper_count(ax, n, q[a]) - 1;
+            const int64_t top = n - 2 > 0 ? n - 2 : 0;
+            if (i0 < 0) i0 = 0;
+            if (i0 > top) i0 = top;
+            const int64_t i1 = i0 + 1 < n - 1 ? i0 + 1 : n - 1;
+            const double span = __dsub_rn(ax[i1], ax[i0]);
+            double tt = span > 0.0 ? __ddiv_rn(__dsub_rn(q[a], ax[i0]), span) : 0.0;
+            tt = tt < 0.0 ? 0.0 : (tt > 1.0 ? 1.0 : tt);
+            lo[a] = i0;
+            hi[a] = i1;
+            t[a] = tt;
+        }
+        double out = 0.0;
+        const int corners = 1 << f.nd;
+        for (int cidx = 0; cidx < corners; ++cidx) {
+            double w = 1.0;
+            int64_t off = 0;
+            for (int a = 0; a < f.nd; ++a) {
+                const int side = (cidx >> (f.nd - 1 - a)) & 1;  // axis 0 slowest
+                w = __dmul_rn(w, side ? t[a] : __dsub_rn(1.0, t[a]));
+                off += (side ? hi[a] : lo[a]) * c.stride[a];
+            }
+            out = __dadd_rn(out, __dmul_rn(w, T[off]));
+        }
+        fine[idx] = out;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K7 coarse c-transform over the coarse target support (quantized.py:504-505)
+// ---------------------------------------------------------------------------
+__global__ void coarse_ct_kernel(const double *__restrict__ g, const int32_t *__restrict__ dst,
+                                 const int32_t *__restrict__ supp_len,
+                                 const double *__restrict__ C, int64_t n, int64_t batch,
+                                 double *__restrict__ f_ext) {
+    const int64_t total = batch * n;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = idx / n, k = idx - b * n;
+        const int len = supp_len[b];
+        const double *gb = g + b * n;
+        const int32_t *db = dst + b * n;
+        const double *Ck = C + k * n;
+        double best = INFINITY;
+        for (int l = 0; l < len; ++l) best = fmin(best, __dsub_rn(Ck[db[l]], gb[l]));
+        f_ext[idx] = best;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// weighted-TV inner sums (measures.py:289-315, before the 1/p root) and
+// batched dots: block-per-pair fp64 reductions (BLAS-like, any order).
+// ---------------------------------------------------------------------------
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) tv_inner_kernel(const double *__restrict__ x,
+                                                           const double *__restrict__ y,
+                                                           Grid g, double p,
+                                                           const double *__restrict__ wts,
+                                                           double *__restrict__ out) {
+    __shared__ double sh[32];
+    const int64_t b = blockIdx.x;
+    const double *xb = x + b * g.cells, *yb = y + b * g.cells;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < g.cells; i += THREADS) {
+        int64_t rem = i;
+        double sq = -0.0;
+        double parts[GDT_MAX_DIM];
+        for (int a = g.nd - 1; a >= 0; --a) {
+            const int64_t xa = rem / g.stride[a];
+            rem -= xa * g.stride[a];
+            const double ctr = ((double)g.n[a] + 1.0) / 2.0;
+            const double df = __dsub_rn((double)(xa + 1), ctr);
+            parts[a] = __dmul_rn(df, df);
+        }
+        for (int a = 0; a < g.nd; ++a) sq = __dadd_rn(sq, parts[a]);
+        double w;
+        if (wts != nullptr) w = wts[i];
+        else if (p == 2.0) w = sq;
+        else if (p == 1.0) w = __dsqrt_rn(sq);
+        else w = pow(sq, p / 2.0);
+        acc += __dmul_rn(w, fabs(__dsub_rn(xb[i], yb[i])));
+    }
+    acc = block_sum<THREADS>(acc, sh);
+    if (threadIdx.x == 0) out[b] = acc;
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) dot_kernel(const double *__restrict__ a,
+                                                      const double *__restrict__ bv, int64_t n,
+                                                      double *__restrict__ out) {
+    __shared__ double sh[32];
+    const int64_t b = blockIdx.x;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += THREADS) acc += __dmul_rn(a[b * n + i], bv[b * n + i]);
+    acc = block_sum<THREADS>(acc, sh);
+    if (threadIdx.x == 0) out[b] = acc;
+}
+
+}  // namespace gdt
+
+using namespace gdt;
+
+extern "C" {
+
+const char *gdt_version(void) { return "gridot_b200 0.1.0 (sm_100a)"; }
+
+const char *gdt_last_error(void) { return g_last_error.c_str(); }
+
+int gdt_pad_f64(const double *in, double *out, int64_t batch, int ndim, const int64_t *dims,
+                int kappa, void *stream) {
+    Grid s, d;
+    GDT_CHECK_ARG(make_grid(s, ndim, dims) && kappa >= 1 && batch >= 0, "gdt_pad_f64: bad grid");
+    int64_t pd[GDT_MAX_DIM];
+    for (int a = 0; a < ndim; ++a) pd[a] = kappa * ((dims[a] + kappa - 1) / kappa);
+    make_grid(d, ndim, pd);
+    if (batch == 0) return GDT_OK;
+    pad_kernel<<<grid_size(batch * d.cells, 256) > 4096 ? 4096 : grid_size(batch * d.cells, 256), 256, 0,
+                 as_stream(stream)>>>(in, out, batch, s, d);
+    return cuda_status("gdt_pad_f64");
+}
+
+int gdt_sumpool_f64(const double *fine, double *coarse, int64_t batch, int ndim,
+                    const int64_t *dims, int kappa, void *stream) {
+    Grid f, c;
+    GDT_CHECK_ARG(make_grid(f, ndim, dims) && make_coarse(c, f, kappa) && batch >= 0,
+                  "gdt_sumpool_f64: dims must be positive multiples of kappa");
+    if (batch == 0) return GDT_OK;
+    const int64_t work = batch * c.cells;
+    sumpool_kernel<<<grid_size(work, 128), 128, 0, as_stream(stream)>>>(fine, coarse, batch, f, c,
+                                                                        kappa);
+    return cuda_status("gdt_sumpool_f64");
+}
+
+int gdt_interpolate(const double *coarse, double *fine, int64_t batch, int ndim,
+                    const int64_t *dims, const int64_t *cdims, const double *axes, int method,
+                    void *stream) {
+    Grid f, c;
+    GDT_CHECK_ARG(make_grid(f, ndim, dims) && make_grid(c, ndim, cdims) && axes != nullptr,
+                  "gdt_interpolate: bad grid");
+    GDT_CHECK_ARG(method == 0 || method == 1, "gdt_interpolate: method must be 0 or 1");
+    if (batch == 0) return GDT_OK;
+    interpolate_kernel<<<grid_size(batch * f.cells, 256), 256, 0, as_stream(stream)>>>(
+        coarse, fine, batch, f, c, axes, method);
+    return cuda_status("gdt_interpolate");
+}
+
+int gdt_coarse_ctransform(const double *g, const int32_t *dst, const int32_t *supp_len,
+                          const double *centre_cost, int64_t n, int64_t batch, double *f_ext,
+                          void *stream) {
+    GDT_CHECK_ARG(n >= 1 && batch >= 0, "gdt_coarse_ctransform: bad sizes");
+    if (batch == 0) return GDT_OK;
+    coarse_ct_kernel<<<grid_size(batch * n, 128), 128, 0, as_stream(stream)>>>(
+        g, dst, supp_len, centre_cost, n, batch, f_ext);
+    return cuda_status("gdt_coarse_ctransform");
+}
+
+int gdt_weighted_tv_inner(const double *x, const double *y, int64_t batch, int ndim,
+                          const int64_t *dims, double p, const double *weights, double *out,
+                          void *stream) {
+    Grid g;
+    GDT_CHECK_ARG(make_grid(g, ndim, dims) && p >= 1.0, "gdt_weighted_tv_inner: bad args");
+    if (batch == 0) return GDT_OK;
+    tv_inner_kernel<256><<<(unsigned)batch, 256, 0, as_stream(stream)>>>(x, y, g, p, weights,
+                                                                             out);
+    return cuda_status("gdt_weighted_tv_inner");
+}
+
+int gdt_batched_dot(const double *a, const double *b, int64_t batch, int64_t n, double *out,
+                    void *stream) {
+    GDT_CHECK_ARG(batch >= 0 && n >= 0, "gdt_batched_dot: bad sizes");
+    if (batch == 0) return GDT_OK;
+    dot_kernel<256><<<(unsigned)batch, 256, 0, as_stream(stream)>>>(a, b, n, out);
+    return cuda_status("gdt_batched_dot");
+}
+
+}  // extern "C"

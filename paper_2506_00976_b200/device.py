@@ -1,0 +1,58 @@
+"""Device plumbing: CUDA device selection, host<->device moves, stream handle.
+
+PyTorch supplies device memory (caching allocator), streams and
+torch.distributed; every hot-path computation runs in libgridot_b200.so.
+There is no CPU execution path: without a CUDA device these helpers raise.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from ._native import lib, stream_handle
+from .errors import GridotError
+
+_torch = None
+
+
+class NoDeviceError(GridotError):
+    """A CUDA device is required for this operation and none is visible."""
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as _t
+
+        _torch = _t
+    return _torch
+
+
+def device():
+    t = torch()
+    if not t.cuda.is_available():
+        raise NoDeviceError("paper_2506_00976_b200 needs a CUDA device (B200, sm_100a); "
+                            "there is no CPU fallback")
+    lib()  # fail loudly if the native library is missing
+    return t.device("cuda", t.cuda.current_device())
+
+
+def to_dev(a, dtype=None):
+    """numpy / torch -> contiguous CUDA tensor (float64 unless dtype given)."""
+    t = torch()
+    dev = device()
+    if isinstance(a, t.Tensor):
+        out = a.to(dev, non_blocking=True)
+    else:
+        out = t.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=True)
+    if dtype is not None:
+        out = out.to(dtype)
+    return out.contiguous()
+
+
+def to_host(t):
+    return t.detach().cpu().numpy()
+
+
+def stream() -> int:
+    return stream_handle(device())

@@ -1,0 +1,418 @@
+"""Batched quantization-bound engine: B pairs x one (kappa, p) per call.
+
+Unit of work = one pair (mu, nu) at one (kappa, p), producing the four bounds
+of ``QUANT_METHODS`` (reference cli.py:41).  Per batch the device does
+
+    H2D(mu, nu) -> pad -> SumPool (K1) -> C-bar (K2) -> D2H(mu~, nu~, C-bar)
+    host: coarse LPs (C-tilde, C-bar, C-min) on a native thread pool
+    H2D(arcs, duals) -> primal upscaling IPF + pricing + TV (K4-K6)
+                     -> coarse c-transform (K7) -> interpolation (K8)
+                     -> two c-transforms + dual dots (K9, K10)
+    D2H(per-pair scalars)
+
+and the host turns the scalars into ``BoundReport`` objects with exactly the
+reference's final arithmetic (``** (1/p)``, ``signed_root``, clipping).
+
+``prepare_coarse`` + ``gpu_stages`` split the pipeline at the LP boundary so
+the benchmark can time the device stages with coarse plans precomputed
+(SURVEY.md 8(d) "GPU-stage throughput").
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .costs import (centre_cost_cached, cost_table, max_sq_of, min_cost_cached,
+                    weighted_cost_batch)
+from .device import device, stream, to_dev, to_host, torch
+from .errors import DimensionMismatchError, GridotError, NumericOverflowError, \
+    ZeroDenominatorError
+from .exact import build_transport_problem, solve_transport_many
+from .measures import CoarseningSpec, GridSpec, coarsen_grid, pad_batch, sumpool_batch
+from .reports import BoundReport, signed_root
+
+__all__ = ["QUANT_METHODS", "CoarsePlans", "quantized_bounds", "prepare_coarse", "gpu_stages",
+           "PRECISIONS"]
+
+QUANT_METHODS = ("weighted_cost", "min_cost", "primal_upscaling", "dual_upscaling")
+PRECISIONS = ("fp64", "fp32")
+_MODE = {"fp64": 0, "fp32": 1}
+
+
+def _uniform_paired(kappa: int, d: int) -> np.ndarray:
+    m = kappa ** d
+    w = np.full((kappa,) * (2 * d), 1.0 / (kappa ** (2 * d)))
+    w = w / float(w.sum())
+    return w.reshape((m, m), order="F")
+
+
+@dataclass
+class CoarsePlans:
+    """Host-side LP results for a batch (one entry per pair)."""
+
+    n: int
+    ctil_arcs: list = field(default_factory=list)     # (rows, cols, mass) full coarse ids
+    ctil_duals: list = field(default_factory=list)    # (g, dst_index)
+    ctil_error: list = field(default_factory=list)
+    cbar_value: list = field(default_factory=list)    # float or exception
+    cmin_value: list = field(default_factory=list)    # float or exception
+    lp_seconds: float = 0.0
+
+
+class _Batch:
+    """Device state of one batch at one (kappa, p)."""
+
+    def __init__(self, mu, nu, dims, kappa, p, precision):
+        t = torch()
+        self.dims = tuple(int(x) for x in dims)
+        self.d = len(self.dims)
+        self.kappa = int(kappa)
+        self.p = float(p)
+        self.precision = precision
+        self.mode = _MODE[precision]
+        self.mu = mu
+        self.nu = nu
+        self.B = mu.shape[0]
+        self.mu_pad, self.pdims = pad_batch(mu, self.dims, self.kappa)
+        self.nu_pad, _ = pad_batch(nu, self.dims, self.kappa)
+        self.cdims = tuple(n // self.kappa for n in self.pdims)
+        self.n = int(np.prod(self.cdims))
+        self.mu_c = sumpool_batch(mu, self.dims, self.kappa)
+        self.nu_c = sumpool_batch(nu, self.dims, self.kappa)
+        self.ctil = centre_cost_cached(self.pdims, self.kappa, self.p)
+        self.ctil_dev = to_dev(self.ctil)
+        self.table_dev = None
+        if self.p != 2.0:
+            ms = max(max_sq_of(self.pdims), max_sq_of(self.dims))
+            self.max_sq = ms
+            self.table_dev = to_dev(cost_table(ms, self.p))
+        else:
+            self.max_sq = 0
+        self.dev = mu.device
+        self.t = t
+
+
+# ---------------------------------------------------------------------------
+# stage 1: SumPool, C-bar, host LPs
+# ---------------------------------------------------------------------------
+
+
+def _cbar(bt: _Batch):
+    return weighted_cost_batch(bt.mu_pad, bt.nu_pad, bt.mu_c, bt.nu_c, bt.pdims, bt.kappa, bt.p,
+                               bt.mode, bt.ctil_dev, bt.table_dev)
+
+
+def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
+    """SumPool + C-bar on the device, then every coarse LP the methods need."""
+    need_ctil = "primal_upscaling" in methods or "dual_upscaling" in methods
+    need_cbar = "weighted_cost" in methods
+    need_cmin = "min_cost" in methods
+    cbar_host = None
+    if need_cbar:
+        vals, _ = _cbar(bt)
+        cbar_host = to_host(vals)
+    mu_c = to_host(bt.mu_c)
+    nu_c = to_host(bt.nu_c)
+    plans = CoarsePlans(n=bt.n)
+    t0 = time.perf_counter()
+    problems, slots = [], []
+    cmin = min_cost_cached(bt.pdims, bt.kappa, bt.p) if need_cmin else None
+    for b in range(bt.B):
+        for kind, cost in (("ctil", bt.ctil if need_ctil else None),
+                           ("cbar", cbar_host[b] if need_cbar else None),
+                           ("cmin", cmin)):
+            if cost is None:
+                continue
+            try:
+                problems.append(build_transport_problem(mu_c[b], nu_c[b], cost))
+                slots.append((b, kind))
+            except GridotError as exc:
+                slots.append((b, kind, exc))
+    solved = solve_transport_many(problems, threads=lp_threads)
+    res = {}
+    it = iter(zip(problems, solved))
+    for s in slots:
+        if len(s) == 3:
+            res[(s[0], s[1])] = (None, s[2])
+        else:
+            prob, out = next(it)
+            res[(s[0], s[1])] = (prob, out)
+    for b in range(bt.B):
+        if need_ctil:
+            prob, out = res[(b, "ctil")]
+            if isinstance(out, Exception):
+                plans.ctil_arcs.append(None)
+                plans.ctil_duals.append(None)
+                plans.ctil_error.append(out)
+            else:
+                coupling, duals, _ = out
+                plans.ctil_arcs.append((prob.src_index[coupling.row], prob.dst_index[coupling.col],
+                                        coupling.mass))
+                plans.ctil_duals.append((duals.g, prob.dst_index))
+                plans.ctil_error.append(None)
+        if need_cbar:
+            prob, out = res[(b, "cbar")]
+            plans.cbar_value.append(out if isinstance(out, Exception) else out[2])
+        if need_cmin:
+            prob, out = res[(b, "cmin")]
+            plans.cmin_value.append(out if isinstance(out, Exception) else out[2])
+    plans.lp_seconds = time.perf_counter() - t0
+    return plans
+
+
+# ---------------------------------------------------------------------------
+# stage 2: device stages that consume the coarse plans
+# ---------------------------------------------------------------------------
+
+
+def _arc_arrays(bt: _Batch, plans: CoarsePlans):
+    """Per-pair CSR (by coarse row) and CSC (by coarse col) arc lists."""
+    n = bt.n
+    row_ptr = np.zeros((bt.B, n + 1), np.int32)
+    col_ptr = np.zeros((bt.B, n + 1), np.int32)
+    rcol, rmass, crow, cmass = [], [], [], []
+    off = [0]
+    for b in range(bt.B):
+        arcs = plans.ctil_arcs[b]
+        if arcs is None:
+            off.append(off[-1])
+            continue
+        r, c, m = (np.asarray(x) for x in arcs)
+        o = np.lexsort((c, r))
+        rcol.append(c[o].astype(np.int32))
+        rmass.append(m[o])
+        row_ptr[b, 1:] = np.cumsum(np.bincount(r, minlength=n))
+        o = np.lexsort((r, c))
+        crow.append(r[o].astype(np.int32))
+        cmass.append(m[o])
+        col_ptr[b, 1:] = np.cumsum(np.bincount(c, minlength=n))
+        off.append(off[-1] + len(r))
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(1, dt)  # noqa: E731
+    return (np.array(off, np.int64), row_ptr, cat(rcol, np.int32), cat(rmass, np.float64),
+            col_ptr, cat(crow, np.int32), cat(cmass, np.float64))
+
+
+def _primal(bt: _Batch, plans: CoarsePlans, xi, max_iter, paired):
+    t = bt.t
+    arc_off, row_ptr, rcol, rmass, col_ptr, crow, cmass = (to_dev(a) for a in
+                                                           _arc_arrays(bt, plans))
+    uniform = bool(np.all(paired == paired.flat[0]))
+    W = to_dev(np.ascontiguousarray(paired))
+    xi_arr = to_dev(np.full(bt.B, -1.0 if xi is None else float(xi)))
+    nbytes = N.lib().gdt_primal_scratch_bytes(bt.B, bt.d, N.i64s(bt.pdims), bt.kappa,
+                                              int(uniform))
+    scratch = t.empty(max(nbytes // 8, 1), dtype=t.float64, device=bt.dev)
+    out = t.empty((bt.B, 8), dtype=t.float64, device=bt.dev)
+    status = t.empty(bt.B, dtype=t.int32, device=bt.dev)
+    N.check(N.lib().gdt_primal_upscale(
+        N.ptr(bt.mu_pad), N.ptr(bt.nu_pad), N.ptr(arc_off), N.ptr(row_ptr), N.ptr(rcol),
+        N.ptr(rmass), N.ptr(col_ptr), N.ptr(crow), N.ptr(cmass), N.ptr(W), int(uniform),
+        N.ptr(xi_arr), int(max_iter), bt.p, bt.B, bt.d, N.i64s(bt.pdims), bt.kappa,
+        N.ptr(bt.table_dev), bt.max_sq, N.ptr(out), N.ptr(status), N.ptr(scratch), stream()),
+        "gdt_primal_upscale")
+    return out, status
+
+
+def _dual(bt: _Batch, plans: CoarsePlans, method: str):
+    t = bt.t
+    n, B = bt.n, bt.B
+    g = np.zeros((B, n))
+    dst = np.zeros((B, n), np.int32)
+    slen = np.zeros(B, np.int32)
+    for b in range(B):
+        if plans.ctil_duals[b] is None:
+            continue
+        gb, di = plans.ctil_duals[b]
+        g[b, :len(gb)] = gb
+        dst[b, :len(di)] = di
+        slen[b] = len(di)
+    g_d, dst_d, slen_d = to_dev(g), to_dev(dst), to_dev(slen)
+    f_ext = t.empty((B, n), dtype=t.float64, device=bt.dev)
+    N.check(N.lib().gdt_coarse_ctransform(N.ptr(g_d), N.ptr(dst_d), N.ptr(slen_d),
+                                          N.ptr(bt.ctil_dev), n, B, N.ptr(f_ext), stream()),
+            "gdt_coarse_ctransform")
+    centres = coarsen_grid(GridSpec(bt.dims), CoarseningSpec(bt.kappa))
+    axes = to_dev(np.concatenate([np.unique(centres[:, a]) for a in range(bt.d)]))
+    Nf = int(np.prod(bt.dims))
+    f_hat = t.empty((B, Nf), dtype=t.float64, device=bt.dev)
+    N.check(N.lib().gdt_interpolate(N.ptr(f_ext), N.ptr(f_hat), B, bt.d, N.i64s(bt.dims),
+                                    N.i64s(bt.cdims), N.ptr(axes), 1 if method == "nearest" else 0,
+                                    stream()), "gdt_interpolate")
+    return ctransform_pair(f_hat, bt.mu, bt.nu, bt.dims, bt.p, bt.precision, bt.table_dev,
+                           bt.max_sq)
+
+
+def ctransform_pair(f_hat, mu, nu, dims, p, precision, table_dev=None, max_sq=0):
+    """g = T f_hat, f = T g on the fine grid; returns (f, g, dot f.mu, dot g.nu)."""
+    t = torch()
+    B, Nf = f_hat.shape
+    dt = 1 if precision == "fp32" else 0
+    tdt = t.float32 if dt else t.float64
+    if p != 2.0 and table_dev is None:
+        max_sq = max_sq_of(dims)
+        table_dev = to_dev(cost_table(max_sq, float(p)))
+    if dt == 1 and dims[0] % 8 != 0 and p != 2.0:
+        dt, tdt = 0, t.float64  # the fp32 brute kernel tiles axis 0 by 8
+    nbytes = N.lib().gdt_ctransform_scratch_bytes(B, len(dims), N.i64s(dims), float(p), dt)
+    scratch = t.empty(max(nbytes, 8), dtype=t.uint8, device=f_hat.device)
+    g = t.empty((B, Nf), dtype=tdt, device=f_hat.device)
+    f = t.empty((B, Nf), dtype=tdt, device=f_hat.device)
+    dots = t.empty((2, B), dtype=t.float64, device=f_hat.device)
+    N.check(N.lib().gdt_ctransform_grid(N.ptr(f_hat), N.ptr(g), B, len(dims), N.i64s(dims),
+                                        float(p), dt, 0, N.ptr(table_dev), max_sq, N.ptr(nu),
+                                        N.ptr(dots[1]), N.ptr(scratch), nbytes, stream()),
+            "gdt_ctransform_grid(target)")
+    N.check(N.lib().gdt_ctransform_grid(N.ptr(g), N.ptr(f), B, len(dims), N.i64s(dims),
+                                        float(p), dt, dt, N.ptr(table_dev), max_sq, N.ptr(mu),
+                                        N.ptr(dots[0]), N.ptr(scratch), nbytes, stream()),
+            "gdt_ctransform_grid(source)")
+    return f, g, dots
+
+
+def gpu_stages(bt: _Batch, plans: CoarsePlans, methods, xi=None, max_iter=10_000, paired=None,
+               dual_method="multilinear"):
+    """Device work downstream of the LPs; returns host arrays of raw scalars."""
+    res = {}
+    if paired is None:
+        paired = _uniform_paired(bt.kappa, bt.d)
+    if "primal_upscaling" in methods:
+        out, status = _primal(bt, plans, xi, max_iter, paired)
+        res["primal"] = (out, status)
+    if "dual_upscaling" in methods:
+        f, g, dots = _dual(bt, plans, dual_method)
+        res["dual"] = dots
+    return res
+
+
+# ---------------------------------------------------------------------------
+# host finishing (reference arithmetic) and the ring fallback
+# ---------------------------------------------------------------------------
+
+
+def _ring_fallback(bt: _Batch, b: int, plans: CoarsePlans, xi, max_iter):
+    """One-ring respread + generic CSR IPF on the device (quantized.py:335-344)."""
+    from .sinkhorn import ipf_fit_device
+    from .quantized import _one_ring_spread_host
+
+    rows, cols, mass = plans.ctil_arcs[b]
+    fr, fc, fm = _one_ring_spread_host(rows, cols, mass, bt.cdims, bt.pdims, bt.kappa)
+    mu_p = to_host(bt.mu_pad[b])
+    nu_p = to_host(bt.nu_pad[b])
+    return ipf_fit_device(fr, fc, fm, mu_p, nu_p, bt.pdims, bt.p, xi, max_iter, bt.table_dev,
+                          bt.max_sq)
+
+
+def _primal_report(p, price, tmu, tnu, gap, iters, conv, n, wall):
+    transport = float(price) ** (1.0 / p)
+    dmu = 2.0 ** (1.0 - 1.0 / p) * float(tmu) ** (1.0 / p)
+    dnu = 2.0 ** (1.0 - 1.0 / p) * float(tnu) ** (1.0 / p)
+    value = transport + dmu + dnu
+    return BoundReport("primal_upscaling", value, value,
+                       {"transport": transport, "delta_mu": dmu, "delta_nu": dnu,
+                        "marginal_gap": float(gap), "converged": float(conv)},
+                       wall, int(iters), n)
+
+
+def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max_iter=10_000,
+                     kernel=None, methods=QUANT_METHODS, dual_method="multilinear",
+                     lp_threads=0, return_exceptions=True, timings=None):
+    """All requested quantization bounds for a batch of pairs on one grid.
+
+    mus, nus: [B, prod(dims)] float64 (numpy, pinned or device tensors).
+    Returns a list (one per pair) of {method: BoundReport | exception}.
+    """
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}")
+    for m in methods:
+        if m not in QUANT_METHODS:
+            raise ValueError(f"unknown method {m!r}")
+    t_start = time.perf_counter()
+    device()
+    mu = to_dev(mus)
+    nu = to_dev(nus)
+    if mu.dim() == 1:
+        mu, nu = mu[None, :], nu[None, :]
+    if mu.shape != nu.shape or mu.shape[1] != int(np.prod(dims)):
+        raise DimensionMismatchError(f"masses {tuple(mu.shape)} do not match dims {dims}")
+    bt = _Batch(mu, nu, dims, kappa, p, precision)
+    paired = None
+    if kernel is not None:
+        if kernel.kappa != bt.kappa or kernel.ndim != bt.d:
+            raise DimensionMismatchError(
+                f"kernel is ({kernel.kappa}, {kernel.ndim}), expected ({bt.kappa}, {bt.d})")
+        paired = kernel.paired()
+    t0 = time.perf_counter()
+    plans = prepare_coarse(bt, methods, lp_threads)
+    t1 = time.perf_counter()
+    res = gpu_stages(bt, plans, methods, xi, max_iter, paired, dual_method)
+    prim = None
+    if "primal" in res:
+        out, status = res["primal"]
+        prim = (to_host(out), to_host(status))
+    dual = to_host(res["dual"]) if "dual" in res else None
+    t2 = time.perf_counter()
+    if timings is not None:
+        timings.update(prepare=t0 - t_start, coarse=t1 - t0, gpu=t2 - t1)
+    wall = (t2 - t_start) / max(bt.B, 1)
+    reports = []
+    for b in range(bt.B):
+        rep = {}
+        if "weighted_cost" in methods:
+            v = plans.cbar_value[b]
+            if isinstance(v, Exception):
+                rep["weighted_cost"] = v
+            else:
+                val = v ** (1.0 / bt.p)
+                rep["weighted_cost"] = BoundReport("weighted_cost", val, val, {"transport": val},
+                                                   wall, None, bt.n)
+        if "min_cost" in methods:
+            v = plans.cmin_value[b]
+            if isinstance(v, Exception):
+                rep["min_cost"] = v
+            else:
+                raw = signed_root(v, bt.p)
+                rep["min_cost"] = BoundReport("min_cost", max(0.0, raw), raw, {"transport": raw},
+                                              wall, None, bt.n)
+        err = plans.ctil_error[b] if plans.ctil_error else None
+        if "primal_upscaling" in methods:
+            if err is not None:
+                rep["primal_upscaling"] = err
+            else:
+                o, st = prim[0][b], int(prim[1][b])
+                try:
+                    if st in (1, 2):
+                        o = _ring_fallback(bt, b, plans, xi, max_iter)
+                        st = 0
+                    if st == 3:
+                        raise NumericOverflowError("scaling vector left [1e-100, 1e100]")
+                    rep["primal_upscaling"] = _primal_report(bt.p, o[0], o[1], o[2], o[3], o[4],
+                                                             o[5], bt.n, wall)
+                except GridotError as exc:
+                    rep["primal_upscaling"] = exc
+        if "dual_upscaling" in methods:
+            if err is not None:
+                rep["dual_upscaling"] = err
+            else:
+                dv = float(dual[0][b] + dual[1][b])
+                raw = signed_root(dv, bt.p)
+                rep["dual_upscaling"] = BoundReport("dual_upscaling", max(0.0, raw), raw,
+                                                    {"dual_value": dv}, wall, None, bt.n)
+        if not return_exceptions:
+            for v in rep.values():
+                if isinstance(v, Exception):
+                    raise v
+        reports.append(rep)
+    return reports
+
+
+def make_batch(mus, nus, dims, kappa, p, precision="fp64"):
+    """Device-resident batch (for benchmarks and staged use)."""
+    device()
+    return _Batch(to_dev(mus), to_dev(nus), dims, kappa, p, precision)
+
+
+ZeroDenominatorError = ZeroDenominatorError  # re-export for callers of the engine

@@ -1,0 +1,177 @@
+"""Coarse exact transport on the host (reference: exact.py + _simplex.py).
+
+The coarse Kantorovich LP stays on the host, as BASELINE.json's north star
+requires.  It runs the native C++ network simplex in libgridot_b200.so
+(``gdt_transport_simplex``), which follows the reference's pivot rules
+exactly (_simplex.py:31-361), so supports, flows and duals are bit-identical.
+``solve_transport_many`` solves a batch of independent LPs on a host thread
+pool without holding the GIL.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import GridotError, IterationLimitError, UnbalancedError
+
+__all__ = ["TransportProblem", "SparseCoupling", "DualPotentials", "build_transport_problem",
+           "solve_transport", "solve_transport_many", "REBALANCE_TOLERANCE"]
+
+logger = logging.getLogger(__name__)
+
+REBALANCE_TOLERANCE = 1e-12
+
+
+@dataclass(frozen=True, eq=False)
+class TransportProblem:
+    """Balanced instance on the positive supports (exact.py:46-62)."""
+
+    supply: np.ndarray
+    demand: np.ndarray
+    cost: np.ndarray
+    src_index: np.ndarray
+    dst_index: np.ndarray
+
+    @property
+    def shape(self) -> tuple:
+        return self.cost.shape
+
+
+@dataclass(frozen=True, eq=False)
+class SparseCoupling:
+    """(row, col, mass) triples (exact.py:65-87)."""
+
+    row: np.ndarray
+    col: np.ndarray
+    mass: np.ndarray
+    shape: tuple
+
+    def row_marginal(self) -> np.ndarray:
+        return np.bincount(self.row, weights=self.mass, minlength=self.shape[0])
+
+    def col_marginal(self) -> np.ndarray:
+        return np.bincount(self.col, weights=self.mass, minlength=self.shape[1])
+
+    @property
+    def total_mass(self) -> float:
+        return float(np.sum(self.mass))
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros(self.shape)
+        out[self.row, self.col] = self.mass
+        return out
+
+
+@dataclass(frozen=True, eq=False)
+class DualPotentials:
+    """Optimal potentials (f[0] = 0) and min_ij C_ij - f_i - g_j (exact.py:90-100)."""
+
+    f: np.ndarray
+    g: np.ndarray
+    feasibility_slack: float
+
+
+def _rebalance(s: np.ndarray, t: np.ndarray) -> None:
+    drift = float(s.sum() - t.sum())
+    if drift == 0.0:
+        return
+    if abs(drift) > REBALANCE_TOLERANCE:
+        raise UnbalancedError(f"total masses differ by {drift:.3e}, beyond "
+                              f"{REBALANCE_TOLERANCE:.0e}")
+    if drift > 0:
+        t[int(np.argmax(t))] += drift
+    else:
+        s[int(np.argmax(s))] -= drift
+
+
+def build_transport_problem(supply, demand, cost) -> TransportProblem:
+    """Restrict to positive entries and absorb rounding drift (exact.py:103-136)."""
+    supply = np.asarray(supply, dtype=np.float64)
+    demand = np.asarray(demand, dtype=np.float64)
+    si = np.flatnonzero(supply > 0.0)
+    di = np.flatnonzero(demand > 0.0)
+    if si.size == 0 or di.size == 0:
+        raise GridotError("transport needs nonempty supports on both sides")
+    s, t = supply[si].copy(), demand[di].copy()
+    _rebalance(s, t)
+    sub = np.ascontiguousarray(np.asarray(cost)[np.ix_(si, di)], dtype=np.float64)
+    return TransportProblem(s, t, sub, si, di)
+
+
+def _finish(problem: TransportProblem, status: int, bi, bj, bf, u, v, pivots):
+    if status == 1:
+        raise IterationLimitError(f"pivot cap reached after {pivots} pivots")
+    if status != 0:
+        raise GridotError(f"simplex failed with status {status}")
+    keep = bf > 0.0
+    coupling = SparseCoupling(bi[keep].copy(), bj[keep].copy(), bf[keep].copy(), problem.shape)
+    value = float(np.sum(bf * problem.cost[bi, bj]))
+    slack = float(np.min(problem.cost - u[:, None] - v[None, :]))
+    logger.debug("simplex %dx%d: %d pivots, value %.12g, slack %.3g", problem.shape[0],
+                 problem.shape[1], pivots, value, slack)
+    return coupling, DualPotentials(u, v, slack), value
+
+
+def solve_transport(problem: TransportProblem, tol: float = 1e-10,
+                    max_pivots: int | None = None):
+    """Optimal coupling, duals and value (exact.py:156-189) via the native simplex."""
+    ns, nt = problem.shape
+    nb = ns + nt - 1
+    bi, bj = np.empty(nb, np.int64), np.empty(nb, np.int64)
+    bf, u, v = np.empty(nb), np.empty(ns), np.empty(nt)
+    piv = ctypes.c_int64(0)
+    C = np.ascontiguousarray(problem.cost, dtype=np.float64)
+    st = N.lib().gdt_transport_simplex(
+        N.ptr(C), N.ptr(problem.supply), N.ptr(problem.demand), ns, nt, 0,
+        0 if max_pivots is None else int(max_pivots), float(tol), N.ptr(bi), N.ptr(bj),
+        N.ptr(bf), N.ptr(u), N.ptr(v), ctypes.byref(piv))
+    if st < 0:
+        N.check(st, "gdt_transport_simplex")
+    return _finish(problem, st, bi, bj, bf, u, v, int(piv.value))
+
+
+def solve_transport_many(problems, tol: float = 1e-10, threads: int = 0):
+    """Solve independent problems on `threads` host threads (0 = all cores).
+
+    Returns a list of (coupling, duals, value) or the exception each raised."""
+    count = len(problems)
+    if count == 0:
+        return []
+    shapes = [p.shape for p in problems]
+    ns = np.array([s[0] for s in shapes], np.int64)
+    nt = np.array([s[1] for s in shapes], np.int64)
+    c_off = np.concatenate([[0], np.cumsum(ns * nt)[:-1]]).astype(np.int64)
+    s_off = np.concatenate([[0], np.cumsum(ns)[:-1]]).astype(np.int64)
+    t_off = np.concatenate([[0], np.cumsum(nt)[:-1]]).astype(np.int64)
+    nbs = ns + nt - 1
+    b_off = np.concatenate([[0], np.cumsum(nbs)[:-1]]).astype(np.int64)
+    C = np.concatenate([np.ascontiguousarray(p.cost, dtype=np.float64).ravel() for p in problems])
+    sup = np.concatenate([p.supply for p in problems])
+    dem = np.concatenate([p.demand for p in problems])
+    tot_b = int(nbs.sum())
+    bi, bj, bf = np.empty(tot_b, np.int64), np.empty(tot_b, np.int64), np.empty(tot_b)
+    u, v = np.empty(int(ns.sum())), np.empty(int(nt.sum()))
+    status = np.empty(count, np.int32)
+    pivots = np.empty(count, np.int64)
+    N.check(N.lib().gdt_transport_simplex_batch(
+        count, N.ptr(C), N.ptr(c_off), N.ptr(sup), N.ptr(dem), N.ptr(s_off), N.ptr(t_off),
+        N.ptr(ns), N.ptr(nt), N.ptr(b_off), float(tol), N.ptr(bi), N.ptr(bj), N.ptr(bf), N.ptr(u),
+        N.ptr(v), N.ptr(status), N.ptr(pivots), int(threads)), "gdt_transport_simplex_batch")
+    out = []
+    for q, prob in enumerate(problems):
+        b0, b1 = b_off[q], b_off[q] + nbs[q]
+        s0, t0 = s_off[q], t_off[q]
+        st = int(status[q])
+        try:
+            if st < 0:
+                raise GridotError(f"simplex failed with native status {st}")
+            out.append(_finish(prob, st, bi[b0:b1], bj[b0:b1], bf[b0:b1], u[s0:s0 + ns[q]],
+                               v[t0:t0 + nt[q]], int(pivots[q])))
+        except GridotError as exc:
+            out.append(exc)
+    return out

@@ -1,0 +1,74 @@
+"""GPU parity at the five BASELINE.json configurations.
+
+Golden values come from the live reference on pairs of each config
+(tests/golden/configs.npz); full batches are checked through size-independent
+properties (certified bracket lower <= upper on every pair, batch/single
+determinism, fp32 vs fp64 agreement).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import case_ids, rel_close
+from test_oracle_golden import inputs_for
+
+pytestmark = pytest.mark.gpu
+
+G = pytest.importorskip("paper_2506_00976_b200")
+from paper_2506_00976_b200 import synthetic as S  # noqa: E402
+
+CFG = case_ids("configs.npz")
+
+
+@pytest.mark.parametrize("tag", CFG)
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_config_bounds_vs_reference(config_cases, tag, precision):
+    c = next(x for x in config_cases if x["tag"] == tag)
+    mu, nu = inputs_for(c)
+    dims, k, p = c["dims"], c["kappa"], c["p"]
+    xi = None if float(c["xi"]) < 0 else float(c["xi"])
+    reps = G.quantized_bounds(mu[None], nu[None], dims, k, p, xi=xi,
+                              max_iter=int(c["max_iter"]), precision=precision,
+                              return_exceptions=False)[0]
+    tol = 1e-9 if precision == "fp64" else 1e-5
+    assert rel_close(reps["weighted_cost"].value, float(c["wc_value"]), tol)
+    assert reps["min_cost"].raw_value == float(c["mc_raw"])
+    assert rel_close(reps["primal_upscaling"].value, float(c["pu_value"]), tol)
+    assert reps["primal_upscaling"].iterations == int(c["pu_iterations"])
+    assert rel_close(reps["dual_upscaling"].raw_value, float(c["du_multilinear_raw"]), tol)
+    if precision == "fp64":
+        # exact arithmetic order: the C-bar LP value and the primal bound are bit-exact
+        assert reps["weighted_cost"].value == float(c["wc_value"])
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 5])
+def test_full_batch_bracket_and_determinism(cfg):
+    wl = S.WORKLOADS[cfg]
+    B = min(wl.pairs, 16)
+    mus, nus = S.batch(cfg, 0, B)
+    for k, p in wl.combos[:2]:
+        out = G.quantized_bounds(mus, nus, wl.dims, k, p, xi=wl.xi, max_iter=wl.max_iter,
+                                 precision=wl.precision, return_exceptions=False)
+        again = G.quantized_bounds(mus, nus, wl.dims, k, p, xi=wl.xi, max_iter=wl.max_iter,
+                                   precision=wl.precision, return_exceptions=False)
+        for b in range(B):
+            lo = max(out[b]["min_cost"].value, out[b]["dual_upscaling"].value)
+            hi = min(out[b]["weighted_cost"].value, out[b]["primal_upscaling"].value)
+            assert lo <= hi, (cfg, k, p, b)
+            for m in G.QUANT_METHODS:
+                assert out[b][m].raw_value == again[b][m].raw_value
+
+
+def test_fp32_tracks_fp64_on_cfg3_batch():
+    wl = S.WORKLOADS[3]
+    mus, nus = S.batch(3, 0, 8)
+    for k, p in wl.combos:
+        a = G.quantized_bounds(mus, nus, wl.dims, k, p, precision="fp64",
+                               return_exceptions=False)
+        b = G.quantized_bounds(mus, nus, wl.dims, k, p, precision="fp32",
+                               return_exceptions=False)
+        for i in range(8):
+            for m in G.QUANT_METHODS:
+                assert rel_close(a[i][m].raw_value, b[i][m].raw_value, 1e-5), (k, p, m)
