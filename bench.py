@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark: certified W_p bounds for 128x128 image pairs (BASELINE.json config 3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+A STEP = one batch of 45 seeded synthetic 128x128 pairs per GPU, each pair
+evaluated at all four (kappa, p) in {4, 8} x {1, 2} and all four quantization
+bounds (weighted-cost UB, primal-upscaling UB, min-cost LB, dual-upscaling
+LB), fp32 mode.  `value` = pairs/s over all ranks (weak scaling: 45 pairs per
+GPU) for the DEVICE stages with inputs resident in HBM and the coarse LP
+plans precomputed (the LP stays on the host by design and is timed in
+`e2e`).  `e2e` = the same pairs through the public API
+(``quantized_bounds``) from pinned host buffers, host LPs included.
+
+`--impl reference` times the CPU oracle (oracle/port.py, a restatement of
+the reference package, with its C simplex) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+import numpy as np  # noqa: E402
+
+CFG = 3
+METRIC = "image pairs/sec for upper+lower W_p bounds at 128x128 (4 bounds x kappa{4,8} x p{1,2})"
+UNIT = "pairs/s"
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=5)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _oracle_pair(args):
+    """One pair, all four combos, all four bounds -- the reference's own algorithm."""
+    cfg, pair, combos = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import port as P
+    from paper_2506_00976_b200 import synthetic as S
+
+    wl = S.WORKLOADS[cfg]
+    mu, nu = S.measure(cfg, pair, 0), S.measure(cfg, pair, 1)
+    t0 = time.perf_counter()
+    for k, p in combos:
+        P.four_bounds(mu, nu, wl.dims, k, p, xi=wl.xi, max_iter=wl.max_iter)
+    return time.perf_counter() - t0
+
+
+def _pool_ctx():
+    import multiprocessing as mp
+
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"
+    return mp.get_context("fork")
+
+
+def cpu_oracle_sample(cfg, n_pairs, workers, first_pair=0):
+    """Wall time of n_pairs oracle pairs on `workers` processes."""
+    from paper_2506_00976_b200 import synthetic as S
+
+    combos = S.WORKLOADS[cfg].combos
+    ctx = _pool_ctx()
+    with ctx.Pool(workers) as pool:
+        t0 = time.perf_counter()
+        per = pool.map(_oracle_pair, [(cfg, first_pair + i, combos) for i in range(n_pairs)],
+                       chunksize=1)
+        wall = time.perf_counter() - t0
+    return wall, per
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    # W warm-up steps on one small pair per worker (import + first-touch), then
+    # K steps, each one pair per core through all four combos of config 3
+    ctx = _pool_ctx()
+    with ctx.Pool(cores) as pool:
+        for _ in range(args.warmup):
+            pool.map(_oracle_pair, [(1, 0, ((4, 2.0),))] * cores, chunksize=1)
+        times = []
+        for s in range(args.steps):
+            t0 = time.perf_counter()
+            pool.map(_oracle_pair, [(CFG, 1000 + s * cores + i,
+                                     ((4, 1.0), (4, 2.0), (8, 1.0), (8, 2.0)))
+                                    for i in range(cores)], chunksize=1)
+            times.append(time.perf_counter() - t0)
+    ms = 1000.0 * statistics.mean(times)
+    value = cores / (ms / 1000.0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg3: 128x128 smooth random fields, kappa{4,8} x p{1,2}, "
+                               "4 quantization bounds", "pairs_per_step": cores,
+                   "parallelism": f"{cores} host processes"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{cores} cfg3 pairs per step (one per core), all 4 combos"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2506_00976_b200 as G
+    from paper_2506_00976_b200 import _native as N
+    from paper_2506_00976_b200 import engine as E
+    from paper_2506_00976_b200 import synthetic as S
+    from paper_2506_00976_b200.device import stream, to_dev
+
+    wl = S.WORKLOADS[CFG]
+    ppr = args.pairs or wl.pairs
+    lo = rank * ppr
+    mus_h, nus_h = S.batch(CFG, lo, lo + ppr)
+    dims = wl.dims
+    Nf = int(np.prod(dims))
+    mus = to_dev(mus_h)
+    nus = to_dev(nus_h)
+    combos = wl.combos
+
+    # ---- setup (untimed): coarse LP plans for the device-stage benchmark
+    stages = []
+    t_setup = time.perf_counter()
+    for k, p in combos:
+        bt = E.make_batch(mus, nus, dims, k, p, wl.precision)
+        plans = E.prepare_coarse(bt, E.QUANT_METHODS, lp_threads=0)
+        dp = E.DevicePlans(bt, plans, None, wl.xi)
+        stages.append((k, p, bt, dp))
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+
+    cur = torch.cuda.current_stream()
+    names = ("pool", "cbar", "primal", "dual_prep", "ct_target", "ct_source")
+    launches_per_step = 0
+
+    def step(events):
+        nonlocal launches_per_step
+        launches = 0
+        for ci, (k, p, bt, dp) in enumerate(stages):
+            ev = events[ci]
+            ev[0].record(cur)
+            bt.pool()
+            launches += 2 + (0 if bt.pdims == bt.dims else 2)
+            ev[1].record(cur)
+            E._cbar(bt)
+            launches += 3 if (bt.p == 2.0 and bt.mode == 1) else 1
+            ev[2].record(cur)
+            E.launch_primal(bt, dp, wl.max_iter)
+            launches += 1
+            ev[3].record(cur)
+            E.launch_dual_prep(bt, dp)
+            launches += 2
+            ev[4].record(cur)
+            E.launch_ctransform(bt, dp, 0)
+            ev[5].record(cur)
+            E.launch_ctransform(bt, dp, 1)
+            ev[6].record(cur)
+            per_ct = (bt.d + 1) if bt.p == 2.0 else (3 if dp.dt == 1 else 2)
+            launches += 2 * per_ct
+        launches_per_step = launches
+
+    def new_events():
+        return [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in stages]
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    for _ in range(args.warmup):
+        step(new_events())
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    all_events = []
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush (> 126 MB) between timed steps, outside the events
+        ev = new_events()
+        step(ev)
+        all_events.append(ev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+
+    step_ms = [sum(ev[ci][0].elapsed_time(ev[ci][6]) for ci in range(len(stages)))
+               for ev in all_events]
+    stage_ms = {}  # (combo, stage) -> mean ms
+    for ci, (k, p, _, _) in enumerate(stages):
+        for si, nm in enumerate(names):
+            stage_ms[(k, p, nm)] = statistics.mean(
+                ev[ci][si].elapsed_time(ev[ci][si + 1]) for ev in all_events)
+    ms = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ppr * world / (ms / 1000.0)
+
+    # ---- roofline of the dominant kernel --------------------------------
+    sink = torch.empty(1, dtype=torch.float32, device="cuda")
+    iters = 4096
+    blocks = 148 * 8
+    N.check(N.lib().gdt_probe_fp32(blocks, 64, N.ptr(sink), stream()), "probe")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cur)
+    N.check(N.lib().gdt_probe_fp32(blocks, iters, N.ptr(sink), stream()), "probe")
+    e1.record(cur)
+    torch.cuda.synchronize()
+    fp32_peak = 2.0 * blocks * 256 * 8 * iters / (e0.elapsed_time(e1) / 1000.0) / 1e12
+    dom = max(stage_ms.items(), key=lambda kv: kv[1])
+    (dk, dpow, dname), dms = dom
+    n_c = Nf // dk ** len(dims)
+    if dname in ("ct_target", "ct_source") and dpow != 2.0:
+        flops = 2.0 * Nf * Nf * ppr            # sub + min per candidate
+        rl = {"bound": "fp32", "kernel": f"brute_f32_kernel (c-transform, kappa={dk}, p={dpow:g})"}
+    elif dname == "cbar" and dpow != 2.0:
+        flops = 2.0 * Nf * Nf * ppr            # one FMA per (row cell, column cell)
+        rl = {"bound": "fp32", "kernel": f"cbar_tile_kernel<fast> (kappa={dk}, p={dpow:g})"}
+    else:
+        flops = None
+        rl = {"bound": "hbm", "kernel": dname}
+    if flops is not None:
+        achieved = flops / (dms / 1000.0) / 1e12
+        rl.update({"achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                   "frac": achieved / fp32_peak, "traffic": None,
+                   "peak_source": "measured live: FFMA issue-rate probe (gdt_probe_fp32)",
+                   "work": "2 FP32 ops x N^4 candidates per pair (N=128)"})
+    # IPF/TV kernel against HBM (north-star secondary roofline)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(HERE, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    prim_ms = statistics.mean(stage_ms[(k, p, "primal")] for k, p, _, _ in stages)
+    sweeps = statistics.mean(
+        float(np.mean(E.to_host(dp.prim_out)[:, 4])) for _, _, _, dp in stages)
+    ipf_bytes = (48.0 * sweeps + 32.0) * Nf * ppr
+    ipf_roof = {"bound": "hbm", "kernel": "primal_kernel<uniform> (IPF + pricing + TV)",
+                "achieved": ipf_bytes / (prim_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": ipf_bytes / (prim_ms / 1000.0) / 1e9 / hbm, "traffic": None,
+                "sweeps": sweeps,
+                "work": "(48*S + 32) * N^2 bytes per pair (SURVEY.md 8(d)), L2-resident at 45 pairs"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32+f64",
+        "data": "synthetic (seeded smooth random fields, BASELINE.json config 3)",
+        "config": {"workload": "cfg3: 45 pairs/GPU of 128x128 smooth random fields; "
+                               "kappa in {4,8} x p in {1,2}; 4 quantization bounds; fp32 mode",
+                   "pairs_per_gpu": ppr, "global_pairs": ppr * world, "grid": list(dims),
+                   "combos": [list(c) for c in combos],
+                   "parallelism": f"dp{world} (pairs sharded, no data-path collective)",
+                   "l2": "flushed (256 MB write) between timed steps",
+                   "lp": "coarse LP plans precomputed on the host (timed in e2e)",
+                   "setup_s": t_setup,
+                   "stage_ms": {f"k{k}_p{p:g}_{nm}": round(v, 4)
+                                for (k, p, nm), v in sorted(stage_ms.items())}},
+        "roofline": rl, "roofline_ipf": ipf_roof, "clocks": clk,
+        "gpu_launches": launches_per_step * args.steps,
+    }
+
+    # ---- e2e through the public API with host buffers --------------------
+    if not args.no_e2e:
+        pin_mu = torch.from_numpy(mus_h).pin_memory()
+        pin_nu = torch.from_numpy(nus_h).pin_memory()
+        h2d = d2h = 0
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            for k, p in combos:
+                reps = G.quantized_bounds(pin_mu, pin_nu, dims, k, p, precision=wl.precision,
+                                          xi=wl.xi, max_iter=wl.max_iter)
+                h2d += 2 * ppr * Nf * 8
+                n_c = Nf // k ** len(dims)
+                d2h += ppr * (n_c * n_c * 8 + 2 * n_c * 8 + 8 * 8 + 2 * 8)
+                assert all(not isinstance(r[m], Exception) for r in reps for m in r)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        line["e2e"] = {"value": ppr * world / e2e_s, "unit": UNIT,
+                       "h2d_bytes_per_step": h2d // args.e2e_steps,
+                       "d2h_bytes_per_step": d2h // args.e2e_steps,
+                       "s_per_step": e2e_s, "host_cores": os.cpu_count(),
+                       "note": "public API quantized_bounds from pinned host memory; "
+                               "includes 3 host LPs per pair per combo on all host cores"}
+
+    # ---- CPU baseline (rank 0, N=1 only) --------------------------------
+    if world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        wall, per = cpu_oracle_sample(CFG, cores, cores, first_pair=1000)
+        line["cpu_baseline"] = {
+            "value": cores / wall, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{cores} cfg3 pairs (one per core, all 4 combos x 4 bounds); "
+                      f"{statistics.mean(per):.1f} s per pair per core",
+        }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--pairs", type=int, default=0, help="pairs per GPU (default 45)")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -215,6 +215,11 @@ int gdt_ctransform_points(const double *xs, const double *xt, int64_t ns, int64_
 int gdt_batched_dot(const double *a, const double *b, int64_t batch, int64_t n,
                     double *out, void *stream);
 
+/* FP32 FMA issue-rate probe: `blocks` CTAs x 256 threads x 8 independent FFMA
+ * chains x `iters` steps (2 FLOP each).  Used by bench.py as the measured
+ * FP32 CUDA-core peak; `sink` is a 4-byte device buffer. */
+int gdt_probe_fp32(int64_t blocks, int64_t iters, float *sink, void *stream);
+
 /* ---- host coarse LP (stays on the host, _simplex.py) ------------------ */
 
 /* Primal network simplex with the reference's pivot rules (northwest-corner

@@ -380,16 +380,19 @@ __global__ void __launch_bounds__(PT) primal_kernel(
     double tmu = 0.0, tnu = 0.0;
     for (int64_t i = threadIdx.x; i < N; i += PT) {
         const double w = tv_weight(i, f, p);
-        int64_t unit = i;
-        if (UNIFORM) {  // block id of cell i
-            int64_t rem = i, k = 0;
-            for (int a = f.nd - 1; a >= 0; --a) {
-                const int64_t x = rem / f.stride[a];
-                rem -= x * f.stride[a];
-                k += (x / kappa) * c.stride[a];
-            }
-            unit = k;
+        // unit of cell i: its block k (uniform) or the fine row/column (k, t)
+        int64_t rem = i, k = 0, t = 0, tpow = 1;
+        for (int a = f.nd - 1; a >= 0; --a) {
+            const int64_t x = rem / f.stride[a];
+            rem -= x * f.stride[a];
+            k += (x / kappa) * c.stride[a];
         }
+        for (int a = 0; a < f.nd; ++a) {
+            const int64_t x = (i / f.stride[a]) % f.n[a];
+            t += (x % kappa) * tpow;
+            tpow *= kappa;
+        }
+        const int64_t unit = UNIFORM ? k : k * m + t;
         const double mh = P.mu[i] > 0.0 ? __dmul_rn(a_cur[i], P.kb[unit]) : 0.0;
         const double nh = P.nu[i] > 0.0 ? __dmul_rn(P.b[i], P.kta[unit]) : 0.0;
         tmu += w * fabs(__dsub_rn(mh, P.mu[i]));

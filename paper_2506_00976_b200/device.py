@@ -44,7 +44,10 @@ def to_dev(a, dtype=None):
     if isinstance(a, t.Tensor):
         out = a.to(dev, non_blocking=True)
     else:
-        out = t.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=True)
+        arr = np.ascontiguousarray(a)
+        if not arr.flags.writeable:
+            arr = arr.copy()
+        out = t.from_numpy(arr).to(dev, non_blocking=True)
     if dtype is not None:
         out = out.to(dtype)
     return out.contiguous()

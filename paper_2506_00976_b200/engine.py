@@ -35,8 +35,8 @@ from .exact import build_transport_problem, solve_transport_many
 from .measures import CoarseningSpec, GridSpec, coarsen_grid, pad_batch, sumpool_batch
 from .reports import BoundReport, signed_root
 
-__all__ = ["QUANT_METHODS", "CoarsePlans", "quantized_bounds", "prepare_coarse", "gpu_stages",
-           "PRECISIONS"]
+__all__ = ["QUANT_METHODS", "CoarsePlans", "DevicePlans", "quantized_bounds", "prepare_coarse",
+           "gpu_stages", "PRECISIONS", "make_batch"]
 
 QUANT_METHODS = ("weighted_cost", "min_cost", "primal_upscaling", "dual_upscaling")
 PRECISIONS = ("fp64", "fp32")
@@ -68,6 +68,7 @@ class _Batch:
 
     def __init__(self, mu, nu, dims, kappa, p, precision):
         t = torch()
+        self.t = t
         self.dims = tuple(int(x) for x in dims)
         self.d = len(self.dims)
         self.kappa = int(kappa)
@@ -77,23 +78,25 @@ class _Batch:
         self.mu = mu
         self.nu = nu
         self.B = mu.shape[0]
-        self.mu_pad, self.pdims = pad_batch(mu, self.dims, self.kappa)
-        self.nu_pad, _ = pad_batch(nu, self.dims, self.kappa)
+        self.dev = mu.device
+        self.pdims = tuple(-(-n // self.kappa) * self.kappa for n in self.dims)
         self.cdims = tuple(n // self.kappa for n in self.pdims)
         self.n = int(np.prod(self.cdims))
-        self.mu_c = sumpool_batch(mu, self.dims, self.kappa)
-        self.nu_c = sumpool_batch(nu, self.dims, self.kappa)
         self.ctil = centre_cost_cached(self.pdims, self.kappa, self.p)
         self.ctil_dev = to_dev(self.ctil)
         self.table_dev = None
+        self.max_sq = 0
         if self.p != 2.0:
-            ms = max(max_sq_of(self.pdims), max_sq_of(self.dims))
-            self.max_sq = ms
-            self.table_dev = to_dev(cost_table(ms, self.p))
-        else:
-            self.max_sq = 0
-        self.dev = mu.device
-        self.t = t
+            self.max_sq = max(max_sq_of(self.pdims), max_sq_of(self.dims))
+            self.table_dev = to_dev(cost_table(self.max_sq, self.p))
+        self.pool()
+
+    def pool(self):
+        """Zero padding + SumPool (K1) of both sides; re-run per step by the bench."""
+        self.mu_pad, _ = pad_batch(self.mu, self.dims, self.kappa)
+        self.nu_pad, _ = pad_batch(self.nu, self.dims, self.kappa)
+        self.mu_c = sumpool_batch(self.mu_pad, self.pdims, self.kappa)
+        self.nu_c = sumpool_batch(self.nu_pad, self.pdims, self.kappa)
 
 
 # ---------------------------------------------------------------------------
@@ -196,67 +199,95 @@ def _arc_arrays(bt: _Batch, plans: CoarsePlans):
             col_ptr, cat(crow, np.int32), cat(cmass, np.float64))
 
 
-def _primal(bt: _Batch, plans: CoarsePlans, xi, max_iter, paired):
-    t = bt.t
-    arc_off, row_ptr, rcol, rmass, col_ptr, crow, cmass = (to_dev(a) for a in
-                                                           _arc_arrays(bt, plans))
-    uniform = bool(np.all(paired == paired.flat[0]))
-    W = to_dev(np.ascontiguousarray(paired))
-    xi_arr = to_dev(np.full(bt.B, -1.0 if xi is None else float(xi)))
-    nbytes = N.lib().gdt_primal_scratch_bytes(bt.B, bt.d, N.i64s(bt.pdims), bt.kappa,
-                                              int(uniform))
-    scratch = t.empty(max(nbytes // 8, 1), dtype=t.float64, device=bt.dev)
-    out = t.empty((bt.B, 8), dtype=t.float64, device=bt.dev)
-    status = t.empty(bt.B, dtype=t.int32, device=bt.dev)
+class DevicePlans:
+    """Coarse plans uploaded once: arc CSR/CSC lists, duals, lattice axes, scratch."""
+
+    def __init__(self, bt: _Batch, plans: CoarsePlans, paired=None, xi=None):
+        t = bt.t
+        self.plans = plans
+        if paired is None:
+            paired = _uniform_paired(bt.kappa, bt.d)
+        self.uniform = bool(np.all(paired == paired.flat[0]))
+        self.W = to_dev(np.ascontiguousarray(paired))
+        self.xi = to_dev(np.full(bt.B, -1.0 if xi is None else float(xi)))
+        self.has_arcs = bool(plans.ctil_arcs)
+        if self.has_arcs:
+            (self.arc_off, self.row_ptr, self.rcol, self.rmass, self.col_ptr, self.crow,
+             self.cmass) = (to_dev(a) for a in _arc_arrays(bt, plans))
+            n, B = bt.n, bt.B
+            g = np.zeros((B, n))
+            dst = np.zeros((B, n), np.int32)
+            slen = np.zeros(B, np.int32)
+            for b in range(B):
+                if plans.ctil_duals[b] is None:
+                    continue
+                gb, di = plans.ctil_duals[b]
+                g[b, :len(gb)] = gb
+                dst[b, :len(di)] = di
+                slen[b] = len(di)
+            self.g, self.dst, self.slen = to_dev(g), to_dev(dst), to_dev(slen)
+        centres = coarsen_grid(GridSpec(bt.dims), CoarseningSpec(bt.kappa))
+        self.axes = to_dev(np.concatenate([np.unique(centres[:, a]) for a in range(bt.d)]))
+        nbytes = N.lib().gdt_primal_scratch_bytes(bt.B, bt.d, N.i64s(bt.pdims), bt.kappa,
+                                                  int(self.uniform))
+        self.primal_scratch = t.empty(max(nbytes // 8, 1), dtype=t.float64, device=bt.dev)
+        self.dt = 1 if bt.precision == "fp32" else 0
+        if self.dt == 1 and bt.dims[0] % 8 != 0 and bt.p != 2.0:
+            self.dt = 0  # the fp32 brute kernel tiles axis 0 by 8
+        self.ct_bytes = N.lib().gdt_ctransform_scratch_bytes(bt.B, bt.d, N.i64s(bt.dims), bt.p,
+                                                             self.dt)
+        self.ct_scratch = t.empty(max(self.ct_bytes, 8), dtype=t.uint8, device=bt.dev)
+        Nf = int(np.prod(bt.dims))
+        tdt = t.float32 if self.dt else t.float64
+        self.f_ext = t.empty((bt.B, bt.n), dtype=t.float64, device=bt.dev)
+        self.f_hat = t.empty((bt.B, Nf), dtype=t.float64, device=bt.dev)
+        self.gf = t.empty((bt.B, Nf), dtype=tdt, device=bt.dev)
+        self.ff = t.empty((bt.B, Nf), dtype=tdt, device=bt.dev)
+        self.dots = t.empty((2, bt.B), dtype=t.float64, device=bt.dev)
+        self.prim_out = t.empty((bt.B, 8), dtype=t.float64, device=bt.dev)
+        self.prim_status = t.empty(bt.B, dtype=t.int32, device=bt.dev)
+
+
+def launch_primal(bt: _Batch, dp: DevicePlans, max_iter):
     N.check(N.lib().gdt_primal_upscale(
-        N.ptr(bt.mu_pad), N.ptr(bt.nu_pad), N.ptr(arc_off), N.ptr(row_ptr), N.ptr(rcol),
-        N.ptr(rmass), N.ptr(col_ptr), N.ptr(crow), N.ptr(cmass), N.ptr(W), int(uniform),
-        N.ptr(xi_arr), int(max_iter), bt.p, bt.B, bt.d, N.i64s(bt.pdims), bt.kappa,
-        N.ptr(bt.table_dev), bt.max_sq, N.ptr(out), N.ptr(status), N.ptr(scratch), stream()),
-        "gdt_primal_upscale")
-    return out, status
+        N.ptr(bt.mu_pad), N.ptr(bt.nu_pad), N.ptr(dp.arc_off), N.ptr(dp.row_ptr), N.ptr(dp.rcol),
+        N.ptr(dp.rmass), N.ptr(dp.col_ptr), N.ptr(dp.crow), N.ptr(dp.cmass), N.ptr(dp.W),
+        int(dp.uniform), N.ptr(dp.xi), int(max_iter), bt.p, bt.B, bt.d, N.i64s(bt.pdims),
+        bt.kappa, N.ptr(bt.table_dev), bt.max_sq, N.ptr(dp.prim_out), N.ptr(dp.prim_status),
+        N.ptr(dp.primal_scratch), stream()), "gdt_primal_upscale")
+    return dp.prim_out, dp.prim_status
 
 
-def _dual(bt: _Batch, plans: CoarsePlans, method: str):
-    t = bt.t
-    n, B = bt.n, bt.B
-    g = np.zeros((B, n))
-    dst = np.zeros((B, n), np.int32)
-    slen = np.zeros(B, np.int32)
-    for b in range(B):
-        if plans.ctil_duals[b] is None:
-            continue
-        gb, di = plans.ctil_duals[b]
-        g[b, :len(gb)] = gb
-        dst[b, :len(di)] = di
-        slen[b] = len(di)
-    g_d, dst_d, slen_d = to_dev(g), to_dev(dst), to_dev(slen)
-    f_ext = t.empty((B, n), dtype=t.float64, device=bt.dev)
-    N.check(N.lib().gdt_coarse_ctransform(N.ptr(g_d), N.ptr(dst_d), N.ptr(slen_d),
-                                          N.ptr(bt.ctil_dev), n, B, N.ptr(f_ext), stream()),
-            "gdt_coarse_ctransform")
-    centres = coarsen_grid(GridSpec(bt.dims), CoarseningSpec(bt.kappa))
-    axes = to_dev(np.concatenate([np.unique(centres[:, a]) for a in range(bt.d)]))
-    Nf = int(np.prod(bt.dims))
-    f_hat = t.empty((B, Nf), dtype=t.float64, device=bt.dev)
-    N.check(N.lib().gdt_interpolate(N.ptr(f_ext), N.ptr(f_hat), B, bt.d, N.i64s(bt.dims),
-                                    N.i64s(bt.cdims), N.ptr(axes), 1 if method == "nearest" else 0,
-                                    stream()), "gdt_interpolate")
-    return ctransform_pair(f_hat, bt.mu, bt.nu, bt.dims, bt.p, bt.precision, bt.table_dev,
-                           bt.max_sq)
+def launch_dual_prep(bt: _Batch, dp: DevicePlans, method: str = "multilinear"):
+    N.check(N.lib().gdt_coarse_ctransform(N.ptr(dp.g), N.ptr(dp.dst), N.ptr(dp.slen),
+                                          N.ptr(bt.ctil_dev), bt.n, bt.B, N.ptr(dp.f_ext),
+                                          stream()), "gdt_coarse_ctransform")
+    N.check(N.lib().gdt_interpolate(N.ptr(dp.f_ext), N.ptr(dp.f_hat), bt.B, bt.d,
+                                    N.i64s(bt.dims), N.i64s(bt.cdims), N.ptr(dp.axes),
+                                    1 if method == "nearest" else 0, stream()), "gdt_interpolate")
+
+
+def launch_ctransform(bt: _Batch, dp: DevicePlans, which: int):
+    """which = 0: g = T f_hat (dot with nu); 1: f = T g (dot with mu)."""
+    src, dst, mass, dot, in_dt = ((dp.f_hat, dp.gf, bt.nu, dp.dots[1], 0) if which == 0 else
+                                  (dp.gf, dp.ff, bt.mu, dp.dots[0], dp.dt))
+    N.check(N.lib().gdt_ctransform_grid(N.ptr(src), N.ptr(dst), bt.B, bt.d, N.i64s(bt.dims),
+                                        bt.p, dp.dt, in_dt, N.ptr(bt.table_dev), bt.max_sq,
+                                        N.ptr(mass), N.ptr(dot), N.ptr(dp.ct_scratch),
+                                        dp.ct_bytes, stream()), "gdt_ctransform_grid")
 
 
 def ctransform_pair(f_hat, mu, nu, dims, p, precision, table_dev=None, max_sq=0):
-    """g = T f_hat, f = T g on the fine grid; returns (f, g, dot f.mu, dot g.nu)."""
+    """g = T f_hat, f = T g on the fine grid; returns (f, g, dots [f.mu, g.nu])."""
     t = torch()
     B, Nf = f_hat.shape
     dt = 1 if precision == "fp32" else 0
-    tdt = t.float32 if dt else t.float64
     if p != 2.0 and table_dev is None:
         max_sq = max_sq_of(dims)
         table_dev = to_dev(cost_table(max_sq, float(p)))
     if dt == 1 and dims[0] % 8 != 0 and p != 2.0:
-        dt, tdt = 0, t.float64  # the fp32 brute kernel tiles axis 0 by 8
+        dt = 0
+    tdt = t.float32 if dt else t.float64
     nbytes = N.lib().gdt_ctransform_scratch_bytes(B, len(dims), N.i64s(dims), float(p), dt)
     scratch = t.empty(max(nbytes, 8), dtype=t.uint8, device=f_hat.device)
     g = t.empty((B, Nf), dtype=tdt, device=f_hat.device)
@@ -273,18 +304,16 @@ def ctransform_pair(f_hat, mu, nu, dims, p, precision, table_dev=None, max_sq=0)
     return f, g, dots
 
 
-def gpu_stages(bt: _Batch, plans: CoarsePlans, methods, xi=None, max_iter=10_000, paired=None,
-               dual_method="multilinear"):
-    """Device work downstream of the LPs; returns host arrays of raw scalars."""
+def gpu_stages(bt: _Batch, dp: DevicePlans, methods, max_iter=10_000, dual_method="multilinear"):
+    """Device work downstream of the LPs (results stay on the device)."""
     res = {}
-    if paired is None:
-        paired = _uniform_paired(bt.kappa, bt.d)
     if "primal_upscaling" in methods:
-        out, status = _primal(bt, plans, xi, max_iter, paired)
-        res["primal"] = (out, status)
+        res["primal"] = launch_primal(bt, dp, max_iter)
     if "dual_upscaling" in methods:
-        f, g, dots = _dual(bt, plans, dual_method)
-        res["dual"] = dots
+        launch_dual_prep(bt, dp, dual_method)
+        launch_ctransform(bt, dp, 0)
+        launch_ctransform(bt, dp, 1)
+        res["dual"] = dp.dots
     return res
 
 
@@ -348,7 +377,8 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
     t0 = time.perf_counter()
     plans = prepare_coarse(bt, methods, lp_threads)
     t1 = time.perf_counter()
-    res = gpu_stages(bt, plans, methods, xi, max_iter, paired, dual_method)
+    dp = DevicePlans(bt, plans, paired, xi)
+    res = gpu_stages(bt, dp, methods, max_iter, dual_method)
     prim = None
     if "primal" in res:
         out, status = res["primal"]

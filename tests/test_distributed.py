@@ -1,0 +1,105 @@
+"""Multi-process host logic of the data-parallel path (gloo, world_size 2, CPU).
+
+The device compute is per pair and has no collective; what crosses ranks is
+the sharding and the all_gather of fixed-width records.  These tests run two
+gloo ranks on 127.0.0.1 and check that gathering reproduces the single-rank
+table bit for bit, including uneven shards and failed methods.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2506_00976_b200 import distributed as D
+from paper_2506_00976_b200.errors import ZeroDenominatorError
+from paper_2506_00976_b200.reports import BoundReport
+
+
+def _fake_reports(lo, hi):
+    out = []
+    for i in range(lo, hi):
+        rep = {
+            "weighted_cost": BoundReport("weighted_cost", 10.0 + i, 10.0 + i,
+                                         {"transport": 10.0 + i}, 0.5, None, 1024),
+            "min_cost": BoundReport("min_cost", max(0.0, i - 3.0), i - 3.0,
+                                    {"transport": i - 3.0}, 0.5, None, 1024),
+            "dual_upscaling": BoundReport("dual_upscaling", 5.0 + i / 7, 5.0 + i / 7,
+                                          {"dual_value": (5.0 + i / 7) ** 2}, 0.5, None, 1024),
+        }
+        if i % 3 == 2:
+            rep["primal_upscaling"] = ZeroDenominatorError("ring fallback failed")
+        else:
+            rep["primal_upscaling"] = BoundReport(
+                "primal_upscaling", 11.0 + i, 11.0 + i,
+                {"transport": 11.0 + i - 1e-9, "delta_mu": 5e-10, "delta_nu": 5e-10,
+                 "marginal_gap": 1e-16, "converged": 1.0}, 0.5, 1, 1024)
+        out.append(rep)
+    return out
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, total, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = D.shard_range(total, rank, world)
+    local = D.pack_records(_fake_reports(lo, hi), lo)
+    table = D.gather_records(local, total)
+    q.put((rank, table))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total", [8, 7, 1])
+def test_gloo_gather_matches_single_rank(total):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect = D.pack_records(_fake_reports(0, total), 0)
+    for r in range(world):
+        assert got[r].shape == expect.shape
+        assert np.array_equal(got[r], expect, equal_nan=True)
+
+
+def test_shard_range_partitions_exactly():
+    for total in (0, 1, 7, 45, 360):
+        for world in (1, 2, 3, 8):
+            seen = []
+            for r in range(world):
+                lo, hi = D.shard_range(total, r, world)
+                assert hi - lo in (total // world, -(-total // world))
+                seen.extend(range(lo, hi))
+            assert seen == list(range(total))
+
+
+def test_pack_unpack_roundtrip():
+    reps = _fake_reports(0, 6)
+    back = D.unpack_records(D.pack_records(reps, 0))
+    for i, (a, b) in enumerate(zip(reps, back)):
+        assert b["pair"] == i
+        for m in ("weighted_cost", "min_cost", "dual_upscaling"):
+            assert b["reports"][m].raw_value == a[m].raw_value
+            assert b["reports"][m].value == a[m].value
+        if isinstance(a["primal_upscaling"], Exception):
+            assert "primal_upscaling" not in b["reports"] and b["status"] & 4
+        else:
+            assert b["reports"]["primal_upscaling"].components == a["primal_upscaling"].components
