@@ -19,6 +19,11 @@
 
 namespace gdt {
 
+int cbar_fast_toeplitz(const double *mu, const double *nu, const double *mu_c,
+                       const double *nu_c, const double *Ccentre, const double *table,
+                       int64_t max_sq, double *out, uint8_t *unused, int64_t batch, const Grid &f,
+                       const Grid &c, int kappa, cudaStream_t st);
+
 struct Offsets {  // within-block offset vectors t -> (t_0..t_{d-1})
     int8_t v[GDT_MAX_DIM];
 };
@@ -185,41 +190,40 @@ __global__ void moments_kernel(const double *__restrict__ fine, double *__restri
     }
 }
 
-__global__ void cbar_moments_kernel(const double *__restrict__ mu_c, const double *__restrict__ nu_c,
-                                    const double *__restrict__ mm, const double *__restrict__ nm,
-                                    const double *__restrict__ Ccentre, double *__restrict__ out,
-                                    uint8_t *__restrict__ unused, int64_t batch, Grid c,
-                                    int kappa) {
-    const int64_t n = c.cells;
-    const int64_t total = batch * n * n;
-    const int W = c.nd + 1;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = idx / (n * n);
-        const int64_t kl = idx - b * n * n;
-        const int64_t k = kl / n, l = kl - k * n;
-        const double M0 = mu_c[b * n + k], N0 = nu_c[b * n + l];
-        const double denom = __dmul_rn(M0, N0);
-        if (denom == 0.0) {
-            out[idx] = Ccentre[k * n + l];
-            unused[idx] = 1;
-            continue;
-        }
-        int64_t kc[GDT_MAX_DIM], lc[GDT_MAX_DIM];
-        unravel_block(k, c, kc);
-        unravel_block(l, c, lc);
-        const double *Mk = mm + (b * n + k) * W, *Nl = nm + (b * n + l) * W;
-        double d2 = 0.0, cross = 0.0, m1n1 = 0.0;
-        for (int a = 0; a < c.nd; ++a) {
-            const double D = (double)(kappa * (kc[a] - lc[a]));
-            d2 += D * D;
-            cross += D * (Mk[a] * N0 - M0 * Nl[a]);
-            m1n1 += Mk[a] * Nl[a];
-        }
-        const double numer = denom * d2 + 2.0 * cross + Mk[c.nd] * N0 + M0 * Nl[c.nd] - 2.0 * m1n1;
-        out[idx] = numer / denom;
-        unused[idx] = 0;
+__global__ void __launch_bounds__(256) cbar_moments_kernel(
+    const double *__restrict__ mu_c, const double *__restrict__ nu_c, const double *__restrict__ mm,
+    const double *__restrict__ nm, const double *__restrict__ Ccentre, double *__restrict__ out,
+    uint8_t *__restrict__ unused, Grid c, int kappa) {
+    // grid: x = l chunk, y = k, z = pair
+    const int n = (int)c.cells, nd = c.nd, W = nd + 1;
+    const int k = blockIdx.y;
+    const int64_t b = blockIdx.z;
+    const int l = blockIdx.x * 256 + threadIdx.x;
+    if (l >= n) return;
+    const double M0 = mu_c[b * n + k], N0 = nu_c[b * n + l];
+    const double denom = __dmul_rn(M0, N0);
+    const int64_t oi = ((int64_t)b * n + k) * n + l;
+    if (denom == 0.0) {
+        out[oi] = Ccentre[(int64_t)k * n + l];
+        unused[oi] = 1;
+        return;
     }
+    const double *Mk = mm + ((int64_t)b * n + k) * W, *Nl = nm + ((int64_t)b * n + l) * W;
+    double d2 = 0.0, cross = 0.0, m1n1 = 0.0;
+    int kk = k, ll = l;
+    for (int a = nd - 1; a >= 0; --a) {
+        const int st = (int)c.stride[a];
+        const int ka = kk / st, la = ll / st;
+        kk -= ka * st;
+        ll -= la * st;
+        const double D = (double)(kappa * (ka - la));
+        d2 = fma(D, D, d2);
+        cross = fma(D, Mk[a] * N0 - M0 * Nl[a], cross);
+        m1n1 = fma(Mk[a], Nl[a], m1n1);
+    }
+    const double numer = denom * d2 + 2.0 * cross + Mk[nd] * N0 + M0 * Nl[nd] - 2.0 * m1n1;
+    out[oi] = numer / denom;
+    unused[oi] = 0;
 }
 
 }  // namespace gdt
@@ -252,34 +256,31 @@ extern "C" int gdt_weighted_cost(const double *mu, const double *nu, const doubl
         moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(mu, mom, batch, f, c, kappa);
         moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(nu, mom + batch * n * W, batch,
                                                                    f, c, kappa);
-        cbar_moments_kernel<<<grid_size(batch * n * n, 256), 256, 0, st>>>(
-            mu_c, nu_c, mom, mom + batch * n * W, centre_cost, out, unused, batch, c, kappa);
+        dim3 mg((unsigned)((n + 255) / 256), (unsigned)n, (unsigned)batch);
+        cbar_moments_kernel<<<mg, 256, 0, st>>>(mu_c, nu_c, mom, mom + batch * n * W, centre_cost,
+                                                 out, unused, c, kappa);
         cudaFreeAsync(mom, st);
         return cuda_status("gdt_weighted_cost(moments)");
+    }
+    if (mode == GDT_MODE_FAST) {
+        const int rc = cbar_fast_toeplitz(mu, nu, mu_c, nu_c, centre_cost, cost_table, max_sq, out,
+                                          unused, batch, f, c, kappa, st);
+        if (rc == GDT_OK) return cuda_status("gdt_weighted_cost(toeplitz)");
+        // outside the fp32 kernel's envelope: fall through to the exact fp64 kernel
     }
     // tile shape: ~256 columns per CTA, KT row blocks per CTA
     int LT = m >= 256 ? 1 : 256 / m;
     if (LT > n) LT = (int)n;
     const int KT = 8;
     const int cols = LT * m;
-    const size_t elem = mode == GDT_MODE_EXACT ? sizeof(double) : sizeof(float);
-    size_t sbytes = ((KT * cols * elem + 7) / 8) * 8 + sizeof(double) * KT * m +
+    size_t sbytes = ((KT * cols * sizeof(double) + 7) / 8) * 8 + sizeof(double) * KT * m +
                     sizeof(int) * m * GDT_MAX_DIM;
     GDT_CHECK_ARG(sbytes <= 200 * 1024, "gdt_weighted_cost: kappa^d too large for this build");
     dim3 grid((unsigned)((n + LT - 1) / LT), (unsigned)((n + KT - 1) / KT), (unsigned)batch);
-    if (mode == GDT_MODE_EXACT) {
-        if (sbytes > 48 * 1024)
-            cudaFuncSetAttribute(cbar_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sbytes);
-        cbar_tile_kernel<true><<<grid, 256, sbytes, st>>>(mu, nu, mu_c, nu_c, centre_cost, cost_table,
-                                                          out, unused, f, c, kappa, m, p, KT, LT);
-    } else {
-        if (sbytes > 48 * 1024)
-            cudaFuncSetAttribute(cbar_tile_kernel<false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes);
-        cbar_tile_kernel<false><<<grid, 256, sbytes, st>>>(mu, nu, mu_c, nu_c, centre_cost,
-                                                           cost_table, out, unused, f, c, kappa, m,
-                                                           p, KT, LT);
-    }
+    if (sbytes > 48 * 1024)
+        cudaFuncSetAttribute(cbar_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sbytes);
+    cbar_tile_kernel<true><<<grid, 256, sbytes, st>>>(mu, nu, mu_c, nu_c, centre_cost, cost_table,
+                                                      out, unused, f, c, kappa, m, p, KT, LT);
     return cuda_status("gdt_weighted_cost");
 }

@@ -249,6 +249,14 @@ __global__ void points_ct_kernel(const double *__restrict__ xo, const double *__
 
 }  // namespace gdt
 
+namespace gdt {
+int ct_pruned_f32(const float *v, float *out, float *tmax, int64_t batch, const Grid &g, double p,
+                  const float *ftab, cudaStream_t st);
+int ct_pruned_f64(const double *v, double *out, double *tmax, int64_t batch, const Grid &g,
+                  double p, const double *tab, cudaStream_t st);
+int64_t ct_pruned_tiles(const Grid &g);
+}  // namespace gdt
+
 using namespace gdt;
 
 extern "C" int64_t gdt_ctransform_scratch_bytes(int64_t batch, int ndim, const int64_t *dims,
@@ -258,8 +266,8 @@ extern "C" int64_t gdt_ctransform_scratch_bytes(int64_t batch, int ndim, const i
     const int64_t el = dtype == 0 ? 8 : 4;
     int64_t need_sq = 0;
     for (int a = 0; a < ndim; ++a) need_sq += (dims[a] - 1) * (dims[a] - 1);
-    // ping-pong buffer (+ fp32 input copy) + fp32 cost table
-    return batch * g.cells * el * 2 + (need_sq + 1) * 4 + 256;
+    // ping-pong buffer (+ fp32 input copy) + fp32 cost table + pruning tile maxima
+    return batch * g.cells * el * 2 + (need_sq + 1) * 4 + batch * ct_pruned_tiles(g) * 8 + 512;
 }
 
 extern "C" int gdt_ctransform_grid(const void *v, void *out, int64_t batch, int ndim,
@@ -313,9 +321,13 @@ extern "C" int gdt_ctransform_grid(const void *v, void *out, int64_t batch, int 
             (void)el;
         }
     } else if (dtype == 0) {
-        const int64_t tiles = (g.cells + BT - 1) / BT;
-        brute_f64_kernel<<<(unsigned)(batch * tiles), BT, 0, st>>>(
-            (const double *)v, (double *)out, batch, g, p, cost_table);
+        double *tmax = (double *)(scr + total * 8 * 2 + ((need_sq + 1) * 4 + 255) / 256 * 256);
+        if (ct_pruned_f64((const double *)v, (double *)out, tmax, batch, g, p, cost_table, st) !=
+            GDT_OK) {
+            const int64_t tiles = (g.cells + BT - 1) / BT;
+            brute_f64_kernel<<<(unsigned)(batch * tiles), BT, 0, st>>>(
+                (const double *)v, (double *)out, batch, g, p, cost_table);
+        }
     } else {
         GDT_CHECK_ARG(g.n[0] % FR == 0, "gdt_ctransform_grid: fp32 brute needs dims[0] % 8 == 0");
         float *vin = (float *)scr;
@@ -328,13 +340,18 @@ extern "C" int gdt_ctransform_grid(const void *v, void *out, int64_t batch, int 
         }
         table_to_f32_kernel<<<grid_size(need_sq + 1, 256), 256, 0, st>>>(cost_table, ftab,
                                                                              need_sq + 1);
+        float *tmax = (float *)(scr + total * 4 * 2 + ((need_sq + 1) * 4 + 255) / 256 * 256);
+        if (ct_pruned_f32(vsrc, (float *)out, tmax, batch, g, p, ftab, st) == GDT_OK) {
+            vsrc = nullptr;  // done
+        }
         const int64_t per = FT * FR;
         const int64_t ctas = batch * ((g.cells + per - 1) / per);
         const size_t sh = (size_t)FROWS * g.n[0] * 4;
         if (sh > 48 * 1024)
             cudaFuncSetAttribute(brute_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sh);
-        brute_f32_kernel<<<(unsigned)ctas, FT, sh, st>>>(vsrc, (float *)out, batch, g, p, ftab);
+        if (vsrc != nullptr)
+            brute_f32_kernel<<<(unsigned)ctas, FT, sh, st>>>(vsrc, (float *)out, batch, g, p, ftab);
     }
     if (mass != nullptr && dot_out != nullptr) {
         if (dtype == 0)

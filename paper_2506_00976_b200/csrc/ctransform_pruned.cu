@@ -1,0 +1,262 @@
+// K9, p != 2: exact brute-force c-transform with conservative tile pruning.
+//
+//   out_j = min_i rho(x_i, x_j)^p - v_i          (quantized.py:450-484)
+//
+// Each warp owns a 16 x 16 (2-D) or 16 x 4 x 4 (3-D) region of outputs, a
+// lane 8 consecutive outputs along axis 0.  Sources are cut into tiles of
+// 8 x 8 (2-D) / 8 x 4 x 4 (3-D) cells with a precomputed max_i v_i per tile.
+// A tile I can only improve an output j of the region J if
+//     lb(I, J) = rho(gap(I, J))^p - max_{i in I} v_i  <  max_{j in J} best_j,
+// where gap is the smallest grid distance between the two boxes; because
+// rounding is monotone, lb is <= every rounded candidate C_ij - v_i of the
+// tile, so skipping such tiles never changes the minimum.  The warp visits
+// tiles in Chebyshev rings around its own region (near tiles first, which
+// tightens max best_j quickly) and stops at the first ring whose smallest
+// possible lb reaches the bound.  The result equals the full brute force
+// bit for bit; the work shrinks with the regularity of v (potentials of
+// transport problems are Lipschitz, so far tiles are pruned).
+//
+// Inner loop (fp32): for one source row of 8 cells a lane needs 15 distinct
+// costs (Toeplitz: cost depends on dx only) and does 64 candidates with
+// packed sub.f32x2 (FADD2) and 3-input min (FMNMX3).  p == 1 costs use
+// sqrt.approx (fp32 mode contract: bounds within 1e-5); the pruning bound is
+// lowered by 2^-20 to stay below every approximated cost.  fp64 reads the
+// exact cost table (p = 1: IEEE sqrt of the integer squared distance).
+#include "common.cuh"
+
+namespace gdt {
+
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    return (unsigned long long)__float_as_uint(a) | ((unsigned long long)__float_as_uint(b) << 32);
+}
+
+__device__ __forceinline__ void sub_f32x2(float c0, float c1, float v0, float v1, float &r0,
+                                          float &r1) {
+    unsigned long long rr;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rr) : "l"(pk2(c0, c1)), "l"(pk2(v0, v1)));
+    r0 = __uint_as_float((unsigned)(rr & 0xffffffffu));
+    r1 = __uint_as_float((unsigned)(rr >> 32));
+}
+
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+template <typename T>
+__global__ void tile_max_kernel(const T *__restrict__ v, T *__restrict__ tmax, int64_t batch,
+                                Grid g, int s0, int s1, int s2) {
+    const int64_t nt0 = g.n[0] / s0, nt1 = g.n[1] / s1, nt2 = g.n[2] / s2;
+    const int64_t per = nt0 * nt1 * nt2;
+    const int64_t total = batch * per;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = idx / per;
+        int64_t r = idx - b * per;
+        const int64_t t0 = r % nt0;
+        r /= nt0;
+        const int64_t t1 = r % nt1, t2 = r / nt1;
+        T m = (T)-INFINITY;
+        for (int z = 0; z < s2; ++z)
+            for (int y = 0; y < s1; ++y) {
+                const T *row = v + b * g.cells + (t2 * s2 + z) * g.stride[2] +
+                               (t1 * s1 + y) * g.stride[1] + t0 * s0;
+                for (int x = 0; x < s0; ++x) m = row[x] > m ? row[x] : m;
+            }
+        tmax[idx] = m;
+    }
+}
+
+// ND = 2: region 16x16, tile 8x8; ND = 3: region 16x4x4, tile 8x4x4
+template <typename T, int ND, bool P1>
+__global__ void __launch_bounds__(128) pruned_ct_kernel(const T *__restrict__ v,
+                                                        const T *__restrict__ tmax,
+                                                        T *__restrict__ out, int64_t batch,
+                                                        Grid g, const T *__restrict__ tab) {
+    constexpr int R1 = ND == 2 ? 16 : 4, R2 = ND == 2 ? 1 : 4;   // region extent y, z
+    constexpr int S1 = ND == 2 ? 8 : 4, S2 = ND == 2 ? 1 : 4;    // tile extent y, z
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int nr0 = (int)(g.n[0] / 16), nr1 = (int)(g.n[1] / R1), nr2 = (int)(g.n[2] / R2);
+    const int64_t regions = (int64_t)nr0 * nr1 * nr2;
+    if (warp >= batch * regions) return;
+    const int64_t b = warp / regions;
+    int rr = (int)(warp - b * regions);
+    const int rx = rr % nr0;
+    rr /= nr0;
+    const int ry = rr % nr1, rz = rr / nr1;
+    const int X0 = rx * 16, Y0 = ry * R1, Z0 = rz * R2;
+    const int xj0 = X0 + 8 * (lane & 1);
+    const int yj = Y0 + ((lane >> 1) % R1);
+    const int zj = Z0 + (ND == 3 ? (lane >> 3) : 0);
+    const T *vb = v + b * g.cells;
+    const int nt0 = (int)(g.n[0] / 8), nt1 = (int)(g.n[1] / S1), nt2 = (int)(g.n[2] / S2);
+    const T *tm = tmax + b * (int64_t)nt0 * nt1 * nt2;
+
+    // max of v over the pair (termination bound)
+    T vall = (T)-INFINITY;
+    for (int i = lane; i < nt0 * nt1 * nt2; i += 32) vall = tm[i] > vall ? tm[i] : vall;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const T w = __shfl_xor_sync(0xffffffffu, vall, o);
+        vall = w > vall ? w : vall;
+    }
+
+    T best[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) best[r] = (T)INFINITY;
+    T ub = (T)INFINITY;
+
+    // home box in tile units
+    const int h0lo = X0 / 8, h0hi = (X0 + 15) / 8;
+    const int h1lo = Y0 / S1, h1hi = (Y0 + R1 - 1) / S1;
+    const int h2lo = Z0 / S2, h2hi = (Z0 + R2 - 1) / S2;
+    const int rmax = max(max(nt0, nt1), nt2);
+    constexpr int smin = ND == 2 ? 8 : 4;
+
+    auto lowered = [](T c) -> T {
+        if constexpr (P1 && sizeof(T) == 4) return c * (1.0f - 1.0f / 1048576.0f);
+        else return c;
+    };
+    auto cost_of = [&](int sq) -> T {
+        if constexpr (sizeof(T) == 4) {
+            if constexpr (P1) return sqrt_approx((float)sq);
+            else return __ldg(tab + sq);
+        } else {
+            return __ldg(tab + sq);
+        }
+    };
+
+    for (int r = 0; r <= rmax; ++r) {
+        if (r >= 1) {  // smallest lb any tile of ring r can have
+            const int gap = (r - 1) * smin + 1;
+            const T lb = lowered(cost_of(gap * gap)) - vall;
+            if (lb >= ub) break;
+        }
+        const int a0 = max(h0lo - r, 0), b0 = min(h0hi + r, nt0 - 1);
+        const int a1 = max(h1lo - r, 0), b1 = min(h1hi + r, nt1 - 1);
+        const int a2 = max(h2lo - r, 0), b2 = min(h2hi + r, nt2 - 1);
+        for (int t2 = a2; t2 <= b2; ++t2)
+            for (int t1 = a1; t1 <= b1; ++t1)
+                for (int t0 = a0; t0 <= b0; ++t0) {
+                    const int d0 = t0 < h0lo ? h0lo - t0 : (t0 > h0hi ? t0 - h0hi : 0);
+                    const int d1 = t1 < h1lo ? h1lo - t1 : (t1 > h1hi ? t1 - h1hi : 0);
+                    const int d2 = t2 < h2lo ? h2lo - t2 : (t2 > h2hi ? t2 - h2hi : 0);
+                    if (max(max(d0, d1), d2) != r) continue;
+                    // gap between the region box and the tile box, per axis
+                    const int g0 = max(0, max(t0 * 8 - (X0 + 15), X0 - (t0 * 8 + 7)));
+                    const int g1 = max(0, max(t1 * S1 - (Y0 + R1 - 1), Y0 - (t1 * S1 + S1 - 1)));
+                    const int g2 = max(0, max(t2 * S2 - (Z0 + R2 - 1), Z0 - (t2 * S2 + S2 - 1)));
+                    const T lb = lowered(cost_of(g0 * g0 + g1 * g1 + g2 * g2)) -
+                                 tm[((int64_t)t2 * nt1 + t1) * nt0 + t0];
+                    if (lb >= ub) continue;
+                    const int sx0 = t0 * 8;
+                    for (int z = 0; z < S2; ++z)
+                        for (int y = 0; y < S1; ++y) {
+                            const int ys = t1 * S1 + y, zs = t2 * S2 + z;
+                            const int hsq = (ys - yj) * (ys - yj) + (zs - zj) * (zs - zj);
+                            const T *row = vb + (int64_t)zs * g.stride[2] + (int64_t)ys * g.stride[1] + sx0;
+                            T vs[8];
+#pragma unroll
+                            for (int s = 0; s < 8; ++s) vs[s] = row[s];
+                            T cst[15];
+#pragma unroll
+                            for (int q = 0; q < 15; ++q) {
+                                const int dx = sx0 - xj0 - 7 + q;
+                                cst[q] = cost_of(hsq + dx * dx);
+                            }
+                            if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                                for (int r8 = 0; r8 < 8; ++r8) {
+#pragma unroll
+                                    for (int s = 0; s < 8; s += 2) {
+                                        float c0, c1;
+                                        sub_f32x2(cst[s - r8 + 7], cst[s + 1 - r8 + 7], vs[s],
+                                                  vs[s + 1], c0, c1);
+                                        best[r8] = fmin3(best[r8], c0, c1);
+                                    }
+                                }
+                            } else {
+#pragma unroll
+                                for (int r8 = 0; r8 < 8; ++r8)
+#pragma unroll
+                                    for (int s = 0; s < 8; ++s)
+                                        best[r8] = fmin(best[r8], __dsub_rn(cst[s - r8 + 7], vs[s]));
+                            }
+                        }
+                    // refresh the warp bound max_j best_j
+                    T m = best[0];
+#pragma unroll
+                    for (int r8 = 1; r8 < 8; ++r8) m = best[r8] > m ? best[r8] : m;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const T w = __shfl_xor_sync(0xffffffffu, m, o);
+                        m = w > m ? w : m;
+                    }
+                    ub = m;
+                }
+    }
+    T *ob = out + b * g.cells + (int64_t)zj * g.stride[2] + (int64_t)yj * g.stride[1] + xj0;
+#pragma unroll
+    for (int r8 = 0; r8 < 8; ++r8) ob[r8] = best[r8];
+}
+
+// Returns GDT_ERR_UNSUPPORTED outside the tiled envelope (caller falls back).
+// v: device input of type T (fp32 path expects an fp32 copy); tab: T cost table
+// by squared distance (unused for fp32 p == 1); tmax: scratch [batch * tiles].
+template <typename T>
+static int run_pruned(const T *v, T *out, T *tmax, int64_t batch, const Grid &g, double p,
+                      const T *tab, cudaStream_t st) {
+    const bool p1 = p == 1.0;
+    int s1, s2;
+    if (g.nd == 2) {
+        if (g.n[0] % 16 || g.n[1] % 16) return GDT_ERR_UNSUPPORTED;
+        s1 = 8;
+        s2 = 1;
+    } else if (g.nd == 3) {
+        if (g.n[0] % 16 || g.n[1] % 4 || g.n[2] % 4) return GDT_ERR_UNSUPPORTED;
+        s1 = 4;
+        s2 = 4;
+    } else {
+        return GDT_ERR_UNSUPPORTED;
+    }
+    const int64_t tiles = (g.n[0] / 8) * (g.n[1] / s1) * (g.n[2] / s2);
+    tile_max_kernel<T><<<grid_size(batch * tiles, 128), 128, 0, st>>>(v, tmax, batch, g, 8, s1, s2);
+    const int64_t regions = (g.n[0] / 16) * (g.n[1] / (g.nd == 2 ? 16 : 4)) *
+                            (g.n[2] / (g.nd == 2 ? 1 : 4));
+    const int64_t warps = batch * regions;
+    const unsigned ctas = (unsigned)((warps + 3) / 4);
+    if (g.nd == 2) {
+        if (p1 && sizeof(T) == 4) pruned_ct_kernel<T, 2, true><<<ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab);
+        else pruned_ct_kernel<T, 2, false><<<ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab);
+    } else {
+        if (p1 && sizeof(T) == 4) pruned_ct_kernel<T, 3, true><<<ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab);
+        else pruned_ct_kernel<T, 3, false><<<ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab);
+    }
+    return GDT_OK;
+}
+
+int ct_pruned_f32(const float *v, float *out, float *tmax, int64_t batch, const Grid &g, double p,
+                  const float *ftab, cudaStream_t st) {
+    return run_pruned<float>(v, out, tmax, batch, g, p, ftab, st);
+}
+
+int ct_pruned_f64(const double *v, double *out, double *tmax, int64_t batch, const Grid &g,
+                  double p, const double *tab, cudaStream_t st) {
+    return run_pruned<double>(v, out, tmax, batch, g, p, tab, st);
+}
+
+int64_t ct_pruned_tiles(const Grid &g) {
+    if (g.nd == 2) return (g.n[0] / 8) * (g.n[1] / 8);
+    if (g.nd == 3) return (g.n[0] / 8) * (g.n[1] / 4) * (g.n[2] / 4);
+    return 0;
+}
+
+}  // namespace gdt

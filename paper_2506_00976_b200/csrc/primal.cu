@@ -8,49 +8,97 @@
 // ascending fine column, every column sum over ascending fine row.
 //
 // Here the fine coupling is never materialised.  For row block k the sorted
-// columns of the CSR row are the cells of the arcs' target blocks in
-// ascending fine flat index; `walk` enumerates exactly that order from the
-// sorted arc list (lexicographic over (l_{d-1}, s_{d-1}, ..., l_0, s_0)).
-// With the uniform kernel every row of block k has the same term sequence,
-// so one sequential fp64 sum per coarse block replaces kappa^d row sums and
-// the result is bit-identical to scipy's.  Non-uniform kernels get one sum per
-// fine row (W[t,s] differs by row offset t).
+// columns of a CSR row are the cells of the arcs' target blocks in ascending
+// fine flat index; `walk` enumerates exactly that order from the sorted arc
+// list (lexicographic over (l_{d-1}, s_{d-1}, ..., l_0, s_0)).  With the
+// uniform kernel every row of block k has the same term sequence, so one
+// sequential fp64 sum per coarse block replaces kappa^d row sums and the
+// result is bit-identical to scipy's.  Non-uniform kernels get one sum per
+// fine row (W[t,s] depends on the row offset t).
 //
-// One CTA per pair stays resident for all sweeps (persistent over sweeps); a
-// sweep is two barrier-separated phases:
-//   C: per column unit l: kta = sum coef * a_i (ascending rows), then for
-//      its cells b_j = nu_j / kta, gap_nu, range(b), zero-column check;
-//   R: per row unit k:    kb  = sum coef * b_j (ascending columns), then for
-//      its cells gap_mu with the current a, range(a), next a = mu / kb,
-//      zero-row check for the next sweep.
-// followed by one block reduction that applies the reference's checks in its
-// order (sinkhorn.py:125-141).
+// ipf_kernel: one CTA per pair stays resident for all sweeps; a sweep is two
+// barrier-separated phases plus one block reduction:
+//   C: per column unit: kta = sum coef * a_i (ascending rows); for its cells
+//      b_j = nu_j / kta, |nu_j - b_j kta| into the gap, range(b), zero check;
+//   R: per row unit: kb = sum coef * b_j (ascending columns); for its cells
+//      |a_i kb - mu_i| with the current a, range(a), next a = mu_i / kb and
+//      the zero-row check of the next sweep;
+// applying the reference's checks in its order (sinkhorn.py:125-141).
+// Then, grid-parallel and deterministic (no atomics):
+//   moments_tv_kernel: per block, weighted-TV partials and the 0th/1st/2nd
+//     moments of a and b about the block centre;
+//   price_kernel: per arc, sum_{t,s} ((a_t m W_ts) b_s) C_ts -- in closed form
+//     from the moments when p == 2 with the uniform kernel (the cost is a
+//     quadratic), by direct summation with tabulated costs otherwise;
+//   finish_kernel: fixed-order reduction of the per-CTA partials.
 #include "common.cuh"
 
 namespace gdt {
 
-constexpr int PT = 512;  // threads per pair CTA
+constexpr int PT = 512;  // threads of the per-pair IPF CTA
 
-__device__ __forceinline__ int64_t coord_of(int64_t id, const Grid &c, int a) {
+struct G32 {  // int32 grid description (cells < 2^31)
+    int nd;
+    int n[GDT_MAX_DIM];
+    int stride[GDT_MAX_DIM];
+    int cells;
+};
+
+inline G32 to32(const Grid &g) {
+    G32 o;
+    o.nd = g.nd;
+    for (int a = 0; a < GDT_MAX_DIM; ++a) {
+        o.n[a] = (int)g.n[a];
+        o.stride[a] = (int)g.stride[a];
+    }
+    o.cells = (int)g.cells;
+    return o;
+}
+
+__device__ __forceinline__ int coord_of(int id, const G32 &c, int a) {
     return (id / c.stride[a]) % c.n[a];
+}
+
+// fine flat id of the origin cell of block k
+__device__ __forceinline__ int block_origin(int k, const G32 &c, const G32 &f, int kappa) {
+    int off = 0;
+    for (int a = c.nd - 1; a >= 0; --a) {
+        const int ka = k / c.stride[a];
+        k -= ka * c.stride[a];
+        off += ka * kappa * f.stride[a];
+    }
+    return off;
+}
+
+// visit the kappa^d cells of a block in ascending fine order: fn(offset_index, cell)
+template <class F>
+__device__ __forceinline__ void for_block_cells(int origin, const G32 &f, int kappa, F &&fn) {
+    const int K1 = f.nd > 1 ? kappa : 1, K2 = f.nd > 2 ? kappa : 1, K3 = f.nd > 3 ? kappa : 1;
+    int t = 0;
+    for (int o3 = 0; o3 < K3; ++o3)
+        for (int o2 = 0; o2 < K2; ++o2)
+            for (int o1 = 0; o1 < K1; ++o1) {
+                const int row = origin + o3 * f.stride[3] + o2 * f.stride[2] + o1 * f.stride[1];
+                for (int o0 = 0; o0 < kappa; ++o0, ++t) fn(t, row + o0);
+            }
 }
 
 // Visit the cells of the union of coarse blocks ids[lo..hi) (sorted
 // ascending) in ascending fine flat order: fn(q, cell, s) with q the arc index,
 // cell the fine flat id and s the within-block offset (Fortran-flattened).
 template <int LEVEL, class F>
-__device__ __forceinline__ void walk(const int32_t *ids, int lo, int hi, const Grid &c,
-                                     const Grid &f, int kappa, int64_t fbase, int sbase,
-                                     int kpow, F &fn) {
+__device__ __forceinline__ void walk(const int32_t *ids, int lo, int hi, const G32 &c,
+                                     const G32 &f, int kappa, int fbase, int sbase, int kpow,
+                                     F &fn) {
     if constexpr (LEVEL == 0) {
         for (int q = lo; q < hi; ++q) {
-            const int64_t cell = fbase + (int64_t)(ids[q] % c.n[0]) * kappa;
+            const int cell = fbase + (ids[q] % c.n[0]) * kappa;
             for (int s0 = 0; s0 < kappa; ++s0) fn(q, cell + s0, sbase + s0);
         }
     } else {
         int r = lo;
         while (r < hi) {
-            const int64_t cr = coord_of(ids[r], c, LEVEL);
+            const int cr = coord_of(ids[r], c, LEVEL);
             int e = r + 1;
             while (e < hi && coord_of(ids[e], c, LEVEL) == cr) ++e;
             for (int sa = 0; sa < kappa; ++sa)
@@ -62,29 +110,15 @@ __device__ __forceinline__ void walk(const int32_t *ids, int lo, int hi, const G
 }
 
 template <class F>
-__device__ __forceinline__ void walk_blocks(const int32_t *ids, int cnt, const Grid &c,
-                                            const Grid &f, int kappa, F &fn) {
-    const int top = c.nd - 1;
-    const int kpow = (int)ipow(kappa, top);
+__device__ __forceinline__ void walk_blocks(const int32_t *ids, int cnt, const G32 &c,
+                                            const G32 &f, int kappa, F &fn) {
+    const int kpow = (int)ipow(kappa, c.nd - 1);
     switch (c.nd) {
         case 1: walk<0>(ids, 0, cnt, c, f, kappa, 0, 0, kpow, fn); break;
         case 2: walk<1>(ids, 0, cnt, c, f, kappa, 0, 0, kpow, fn); break;
         case 3: walk<2>(ids, 0, cnt, c, f, kappa, 0, 0, kpow, fn); break;
         default: walk<3>(ids, 0, cnt, c, f, kappa, 0, 0, kpow, fn); break;
     }
-}
-
-// fine flat id of (block k, offset t)
-__device__ __forceinline__ int64_t cell_of(int64_t k, int t, const Grid &c, const Grid &f,
-                                           int kappa) {
-    int64_t off = 0;
-    for (int a = 0; a < c.nd; ++a) {
-        const int64_t ka = coord_of(k, c, a);
-        const int ta = t % kappa;
-        t /= kappa;
-        off += (ka * kappa + ta) * f.stride[a];
-    }
-    return off;
 }
 
 struct PairPtrs {
@@ -99,6 +133,10 @@ struct Red {  // per-sweep reduction slots
     int zrow, zcol, nonfinite;
 };
 
+__device__ __forceinline__ Red red_init() {
+    return Red{0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0, 0, 0};
+}
+
 __device__ __forceinline__ void range_acc(double v, double &lo, double &hi, int &nonfinite) {
     if (v > 0.0) {
         lo = fmin(lo, v);
@@ -110,7 +148,6 @@ __device__ __forceinline__ void range_acc(double v, double &lo, double &hi, int 
 }
 
 __device__ void block_reduce_red(Red &r, double *sh) {
-    // sum gap, min amin/bmin, max amax/bmax, or flags; all threads get result
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         r.gap += __shfl_xor_sync(0xffffffffu, r.gap, o);
@@ -126,22 +163,22 @@ __device__ void block_reduce_red(Red &r, double *sh) {
     constexpr int NW = PT / 32;
     __syncthreads();
     if (lane == 0) {
-        sh[w * 8 + 0] = r.gap;
-        sh[w * 8 + 1] = r.amin;
-        sh[w * 8 + 2] = r.amax;
-        sh[w * 8 + 3] = r.bmin;
-        sh[w * 8 + 4] = r.bmax;
-        sh[w * 8 + 5] = (double)(r.zrow | (r.zcol << 1) | (r.nonfinite << 2));
+        sh[w * 6 + 0] = r.gap;
+        sh[w * 6 + 1] = r.amin;
+        sh[w * 6 + 2] = r.amax;
+        sh[w * 6 + 3] = r.bmin;
+        sh[w * 6 + 4] = r.bmax;
+        sh[w * 6 + 5] = (double)(r.zrow | (r.zcol << 1) | (r.nonfinite << 2));
     }
     __syncthreads();
-    Red o{0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0, 0, 0};
+    Red o = red_init();
     for (int i = 0; i < NW; ++i) {
-        o.gap += sh[i * 8 + 0];
-        o.amin = fmin(o.amin, sh[i * 8 + 1]);
-        o.amax = fmax(o.amax, sh[i * 8 + 2]);
-        o.bmin = fmin(o.bmin, sh[i * 8 + 3]);
-        o.bmax = fmax(o.bmax, sh[i * 8 + 4]);
-        const int fl = (int)sh[i * 8 + 5];
+        o.gap += sh[i * 6 + 0];
+        o.amin = fmin(o.amin, sh[i * 6 + 1]);
+        o.amax = fmax(o.amax, sh[i * 6 + 2]);
+        o.bmin = fmin(o.bmin, sh[i * 6 + 3]);
+        o.bmax = fmax(o.bmax, sh[i * 6 + 4]);
+        const int fl = (int)sh[i * 6 + 5];
         o.zrow |= fl & 1;
         o.zcol |= (fl >> 1) & 1;
         o.nonfinite |= (fl >> 2) & 1;
@@ -150,33 +187,30 @@ __device__ void block_reduce_red(Red &r, double *sh) {
     __syncthreads();
 }
 
-// Phase R for one row unit.  UNIFORM: unit = coarse block k (all its rows
-// share the sum); otherwise unit = fine row (k, t).
+// Phase R for one row unit (block k, or fine row (k, t) for non-uniform W).
 template <bool UNIFORM>
-__device__ __forceinline__ void row_unit(int64_t u, const PairPtrs &P, const Grid &c,
-                                         const Grid &f, int kappa, int m, const double *W,
-                                         double Wu, bool init, const double *a_cur,
-                                         double *a_next, Red &r) {
-    const int64_t k = UNIFORM ? u : u / m;
-    const int t = UNIFORM ? 0 : (int)(u % m);
+__device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c, const G32 &f,
+                                         int kappa, int m, const double *W, double Wu, bool init,
+                                         const double *a_cur, double *a_next, Red &r) {
+    const int k = UNIFORM ? u : u / m;
+    const int t = UNIFORM ? 0 : u - k * m;
     const int lo = P.rptr[k], hi = P.rptr[k + 1];
     const int32_t *ids = P.rcol + lo;
     const double *ms = P.rmass + lo;
     double acc = 0.0;
-    auto fn = [&](int q, int64_t cell, int s) {
+    auto fn = [&](int q, int cell, int s) {
         const double coef = __dmul_rn(ms[q], UNIFORM ? Wu : W[t * m + s]);
         acc = __dadd_rn(acc, __dmul_rn(coef, P.b[cell]));
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kb[u] = acc;
-    const int t_lo = UNIFORM ? 0 : t, t_hi = UNIFORM ? m : t + 1;
-    for (int tt = t_lo; tt < t_hi; ++tt) {
-        const int64_t i = cell_of(k, tt, c, f, kappa);
+    const int origin = block_origin(k, c, f, kappa);
+    for_block_cells(origin, f, kappa, [&](int tt, int i) {
+        if (!UNIFORM && tt != t) return;
         const double mui = P.mu[i];
         if (!init) {
             const double ai = a_cur[i];
             range_acc(ai, r.amin, r.amax, r.nonfinite);
-            // reference gap uses support rows only; off-support a = 0, mu = 0
             if (mui > 0.0) r.gap += fabs(__dsub_rn(__dmul_rn(ai, acc), mui));
         }
         double an = 0.0;
@@ -185,28 +219,28 @@ __device__ __forceinline__ void row_unit(int64_t u, const PairPtrs &P, const Gri
             else an = __ddiv_rn(mui, acc);
         }
         a_next[i] = an;
-    }
+    });
 }
 
 template <bool UNIFORM>
-__device__ __forceinline__ void col_unit(int64_t u, const PairPtrs &P, const Grid &c,
-                                         const Grid &f, int kappa, int m, const double *W,
-                                         double Wu, const double *a_cur, Red &r) {
-    const int64_t l = UNIFORM ? u : u / m;
-    const int s = UNIFORM ? 0 : (int)(u % m);
+__device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c, const G32 &f,
+                                         int kappa, int m, const double *W, double Wu,
+                                         const double *a_cur, Red &r) {
+    const int l = UNIFORM ? u : u / m;
+    const int s = UNIFORM ? 0 : u - l * m;
     const int lo = P.cptr[l], hi = P.cptr[l + 1];
     const int32_t *ids = P.crow + lo;
     const double *ms = P.cmass + lo;
     double acc = 0.0;
-    auto fn = [&](int q, int64_t cell, int t) {
+    auto fn = [&](int q, int cell, int t) {
         const double coef = __dmul_rn(ms[q], UNIFORM ? Wu : W[t * m + s]);
         acc = __dadd_rn(acc, __dmul_rn(coef, a_cur[cell]));
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kta[u] = acc;
-    const int s_lo = UNIFORM ? 0 : s, s_hi = UNIFORM ? m : s + 1;
-    for (int ss = s_lo; ss < s_hi; ++ss) {
-        const int64_t j = cell_of(l, ss, c, f, kappa);
+    const int origin = block_origin(l, c, f, kappa);
+    for_block_cells(origin, f, kappa, [&](int ss, int j) {
+        if (!UNIFORM && ss != s) return;
         const double nuj = P.nu[j];
         double bj = 0.0;
         if (nuj > 0.0) {
@@ -216,50 +250,26 @@ __device__ __forceinline__ void col_unit(int64_t u, const PairPtrs &P, const Gri
             r.gap += fabs(__dsub_rn(nuj, __dmul_rn(bj, acc)));
         }
         P.b[j] = bj;
-    }
+    });
 }
 
-__device__ __forceinline__ double grid_cost(int64_t i, int64_t j, const Grid &f, double p,
-                                            const double *table) {
-    int64_t sq = 0;
-    for (int a = f.nd - 1; a >= 0; --a) {
-        const int64_t xi = i / f.stride[a], xj = j / f.stride[a];
-        i -= xi * f.stride[a];
-        j -= xj * f.stride[a];
-        sq += (xi - xj) * (xi - xj);
-    }
-    return cost_from_sq(sq, p, table);
-}
-
-__device__ __forceinline__ double tv_weight(int64_t i, const Grid &f, double p) {
-    double parts[GDT_MAX_DIM];
-    for (int a = f.nd - 1; a >= 0; --a) {
-        const int64_t x = i / f.stride[a];
-        i -= x * f.stride[a];
-        const double df = __dsub_rn((double)(x + 1), ((double)f.n[a] + 1.0) / 2.0);
-        parts[a] = __dmul_rn(df, df);
-    }
-    double sq = -0.0;
-    for (int a = 0; a < f.nd; ++a) sq = __dadd_rn(sq, parts[a]);
-    if (p == 2.0) return sq;
-    if (p == 1.0) return __dsqrt_rn(sq);
-    return pow(sq, p / 2.0);
-}
+// per-pair scalar record written by ipf_kernel / finish_kernel
+// out[b*8 + {0..7}] = {transport_p, tv_mu, tv_nu, gap, iterations, converged, support, 0}
 
 template <bool UNIFORM>
-__global__ void __launch_bounds__(PT) primal_kernel(
+__global__ void __launch_bounds__(PT) ipf_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const int64_t *__restrict__ arc_off,
     const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ row_arc_col,
     const double *__restrict__ row_arc_mass, const int32_t *__restrict__ col_ptr,
     const int32_t *__restrict__ col_arc_row, const double *__restrict__ col_arc_mass,
-    const double *__restrict__ W, const double *__restrict__ xi_in, int64_t max_iter, double p,
-    Grid f, Grid c, int kappa, const double *__restrict__ table, double *__restrict__ out,
-    int32_t *__restrict__ status, double *__restrict__ scratch) {
-    __shared__ double sh[(PT / 32) * 8];
+    const double *__restrict__ W, const double *__restrict__ xi_in, int64_t max_iter, G32 f,
+    G32 c, int kappa, double *__restrict__ out, int32_t *__restrict__ status,
+    double *__restrict__ scratch, int64_t stride_pair) {
+    __shared__ double sh[(PT / 32) * 6];
     const int64_t b = blockIdx.x;
-    const int64_t N = f.cells, n = c.cells;
+    const int N = f.cells, n = c.cells;
     const int m = (int)ipow(kappa, f.nd);
-    const int64_t U = UNIFORM ? n : N;
+    const int U = UNIFORM ? n : N;
     const double Wu = W[0];
 
     PairPtrs P;
@@ -272,7 +282,7 @@ __global__ void __launch_bounds__(PT) primal_kernel(
     P.rmass = row_arc_mass + a0;
     P.crow = col_arc_row + a0;
     P.cmass = col_arc_mass + a0;
-    double *ws = scratch + b * (3 * N + 2 * U);
+    double *ws = scratch + b * stride_pair;
     P.aA = ws;
     P.aB = ws + N;
     P.b = ws + 2 * N;
@@ -281,7 +291,7 @@ __global__ void __launch_bounds__(PT) primal_kernel(
 
     // supports and the reference's default xi (quantized.py:317-320)
     double cnt = 0.0;
-    for (int64_t i = threadIdx.x; i < N; i += PT) {
+    for (int i = threadIdx.x; i < N; i += PT) {
         const double mi = P.mu[i], ni = P.nu[i];
         cnt += (mi > 0.0 ? 1.0 : 0.0) + (ni > 0.0 ? 1.0 : 0.0);
         P.b[i] = ni > 0.0 ? 1.0 : 0.0;  // b = ones over the target support
@@ -291,9 +301,9 @@ __global__ void __launch_bounds__(PT) primal_kernel(
     __syncthreads();
 
     // kb = K b0, a = mu / kb (sinkhorn.py:119-129 before the first sweep)
-    Red r{0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0, 0, 0};
+    Red r = red_init();
     double *a_cur = P.aA, *a_nxt = P.aB;
-    for (int64_t u = threadIdx.x; u < U; u += PT)
+    for (int u = threadIdx.x; u < U; u += PT)
         row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, true, nullptr, a_cur, r);
     block_reduce_red(r, sh);
     int st = r.zrow ? GDT_PAIR_ZERO_DENOM_ROW : GDT_PAIR_OK;
@@ -302,17 +312,14 @@ __global__ void __launch_bounds__(PT) primal_kernel(
     bool converged = false;
     while (st == GDT_PAIR_OK && it < max_iter) {
         ++it;
-        Red rc{0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0, 0, 0};
-        for (int64_t u = threadIdx.x; u < U; u += PT)
+        Red rc = red_init();
+        for (int u = threadIdx.x; u < U; u += PT)
             col_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, a_cur, rc);
-        __syncthreads();
-        // zero-column check must precede anything that reads b
-        int zc = __syncthreads_or(rc.zcol);
-        if (zc) {
+        if (__syncthreads_or(rc.zcol)) {  // before anything reads b
             st = GDT_PAIR_ZERO_DENOM_COL;
             break;
         }
-        for (int64_t u = threadIdx.x; u < U; u += PT)
+        for (int u = threadIdx.x; u < U; u += PT)
             row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, false, a_cur, a_nxt, rc);
         block_reduce_red(rc, sh);
         // _check_scale_range(a), then (b) (sinkhorn.py:137-138)
@@ -330,7 +337,7 @@ __global__ void __launch_bounds__(PT) primal_kernel(
             break;
         }
         if (it >= max_iter) break;
-        if (rc.zrow) {  // checked at the top of the next sweep
+        if (rc.zrow) {  // the check at the top of the next sweep
             st = GDT_PAIR_ZERO_DENOM_ROW;
             break;
         }
@@ -338,79 +345,218 @@ __global__ void __launch_bounds__(PT) primal_kernel(
         a_cur = a_nxt;
         a_nxt = tmp;
     }
-    // on exit a_cur / b / kb / kta are the state of the last completed sweep
-    if (threadIdx.x == 0) status[b] = st;
-    if (st != GDT_PAIR_OK) {
-        if (threadIdx.x == 0) {
-            for (int q = 0; q < 8; ++q) out[b * 8 + q] = 0.0;
-            out[b * 8 + 4] = (double)it;
-        }
-        return;
-    }
-
-    // pricing: sum over fine entries of ((a_i * m W_ts) * b_j) * C_ij
-    // (quantized.py:346-355; order-free like the reference's BLAS dot)
-    double price = 0.0;
-    const int64_t A = P.rptr[n];
-    for (int64_t w = threadIdx.x; w < A * m; w += PT) {
-        const int64_t q = w / m;
-        const int t = (int)(w - q * m);
-        // arc q in row-major order: find its row block by binary search
-        int lo = 0, hi = (int)n;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (P.rptr[mid] <= q) lo = mid;
-            else hi = mid;
-        }
-        const int64_t k = lo, l = P.rcol[q];
-        const double mass = P.rmass[q];
-        const int64_t i = cell_of(k, t, c, f, kappa);
-        const double ai = a_cur[i];
-        if (ai == 0.0) continue;
-        for (int s = 0; s < m; ++s) {
-            const int64_t j = cell_of(l, s, c, f, kappa);
-            const double wts = UNIFORM ? Wu : W[t * m + s];
-            const double fitted = __dmul_rn(__dmul_rn(ai, __dmul_rn(mass, wts)), P.b[j]);
-            price += fitted * grid_cost(i, j, f, p, table);
-        }
-    }
-    price = block_sum<PT>(price, sh);
-
-    // weighted TV inner sums with mu_hat = a * kb, nu_hat = b * kta
-    double tmu = 0.0, tnu = 0.0;
-    for (int64_t i = threadIdx.x; i < N; i += PT) {
-        const double w = tv_weight(i, f, p);
-        // unit of cell i: its block k (uniform) or the fine row/column (k, t)
-        int64_t rem = i, k = 0, t = 0, tpow = 1;
-        for (int a = f.nd - 1; a >= 0; --a) {
-            const int64_t x = rem / f.stride[a];
-            rem -= x * f.stride[a];
-            k += (x / kappa) * c.stride[a];
-        }
-        for (int a = 0; a < f.nd; ++a) {
-            const int64_t x = (i / f.stride[a]) % f.n[a];
-            t += (x % kappa) * tpow;
-            tpow *= kappa;
-        }
-        const int64_t unit = UNIFORM ? k : k * m + t;
-        const double mh = P.mu[i] > 0.0 ? __dmul_rn(a_cur[i], P.kb[unit]) : 0.0;
-        const double nh = P.nu[i] > 0.0 ? __dmul_rn(P.b[i], P.kta[unit]) : 0.0;
-        tmu += w * fabs(__dsub_rn(mh, P.mu[i]));
-        tnu += w * fabs(__dsub_rn(nh, P.nu[i]));
-    }
-    tmu = block_sum<PT>(tmu, sh);
-    tnu = block_sum<PT>(tnu, sh);
+    // publish which buffer holds the final a (aA or aB) for the pricing kernels
     if (threadIdx.x == 0) {
+        status[b] = st;
         double *o = out + b * 8;
-        o[0] = price;
-        o[1] = tmu;
-        o[2] = tnu;
+        o[0] = 0.0;
+        o[1] = 0.0;
+        o[2] = 0.0;
         o[3] = gap;
         o[4] = (double)it;
         o[5] = converged ? 1.0 : 0.0;
         o[6] = cnt;
-        o[7] = 0.0;
+        o[7] = a_cur == P.aA ? 0.0 : 1.0;
     }
+}
+
+__device__ __forceinline__ double tv_weight(int i, const G32 &f, double p) {
+    double parts[GDT_MAX_DIM];
+    for (int a = f.nd - 1; a >= 0; --a) {
+        const int x = i / f.stride[a];
+        i -= x * f.stride[a];
+        const double df = __dsub_rn((double)(x + 1), ((double)f.n[a] + 1.0) / 2.0);
+        parts[a] = __dmul_rn(df, df);
+    }
+    double sq = -0.0;
+    for (int a = 0; a < f.nd; ++a) sq = __dadd_rn(sq, parts[a]);
+    if (p == 2.0) return sq;
+    if (p == 1.0) return __dsqrt_rn(sq);
+    return pow(sq, p / 2.0);
+}
+
+constexpr int MT = 128;  // threads of the moments/price kernels
+
+// Per block: TV partials (per CTA) and moments of a and b about the block
+// centre: mom[(b*n + k)*MW + {A0, A1[d], A2, B0, B1[d], B2}].
+template <bool UNIFORM>
+__global__ void __launch_bounds__(MT) moments_tv_kernel(
+    const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ out,
+    const int32_t *__restrict__ status, double *__restrict__ scratch, int64_t stride_pair,
+    double *__restrict__ mom, double *__restrict__ part, G32 f, G32 c, int kappa, double p,
+    int want_moments) {
+    __shared__ double sh[32];
+    const int64_t b = blockIdx.y;
+    const int N = f.cells, n = c.cells;
+    const int m = (int)ipow(kappa, f.nd);
+    const int U = UNIFORM ? n : N;
+    const int MW = 2 * (f.nd + 2);
+    double tmu = 0.0, tnu = 0.0;
+    if (status[b] == GDT_PAIR_OK) {
+        const double *ws = scratch + b * stride_pair;
+        const double *a = out[b * 8 + 7] == 0.0 ? ws : ws + N;
+        const double *bv = ws + 2 * N, *kb = ws + 3 * N, *kta = ws + 3 * N + U;
+        const double *mub = mu + b * N, *nub = nu + b * N;
+        const double ctr = (kappa - 1) / 2.0;
+        const int k = blockIdx.x * MT + threadIdx.x;
+        if (k < n) {
+            const int origin = block_origin(k, c, f, kappa);
+            double A[2 + GDT_MAX_DIM] = {0, 0, 0, 0, 0, 0}, Bm[2 + GDT_MAX_DIM] = {0, 0, 0, 0, 0, 0};
+            for_block_cells(origin, f, kappa, [&](int t, int i) {
+                const double w = tv_weight(i, f, p);
+                const double kbu = kb[UNIFORM ? k : k * m + t];
+                const double ktu = kta[UNIFORM ? k : k * m + t];
+                const double ai = a[i], bi = bv[i];
+                const double mh = mub[i] > 0.0 ? __dmul_rn(ai, kbu) : 0.0;
+                const double nh = nub[i] > 0.0 ? __dmul_rn(bi, ktu) : 0.0;
+                tmu += w * fabs(__dsub_rn(mh, mub[i]));
+                tnu += w * fabs(__dsub_rn(nh, nub[i]));
+                if (want_moments) {
+                    int rem = t;
+                    double r2 = 0.0;
+                    for (int q = 0; q < f.nd; ++q) {
+                        const double dl = (double)(rem % kappa) - ctr;
+                        rem /= kappa;
+                        A[1 + q] += ai * dl;
+                        Bm[1 + q] += bi * dl;
+                        r2 += dl * dl;
+                    }
+                    A[0] += ai;
+                    Bm[0] += bi;
+                    A[1 + f.nd] += ai * r2;
+                    Bm[1 + f.nd] += bi * r2;
+                }
+            });
+            if (want_moments) {
+                double *o = mom + ((int64_t)b * n + k) * MW;
+                for (int q = 0; q < f.nd + 2; ++q) {
+                    o[q] = A[q];
+                    o[f.nd + 2 + q] = Bm[q];
+                }
+            }
+        }
+    }
+    tmu = block_sum<MT>(tmu, sh);
+    tnu = block_sum<MT>(tnu, sh);
+    if (threadIdx.x == 0) {
+        double *pp = part + ((int64_t)b * gridDim.x + blockIdx.x) * 2;
+        pp[0] = tmu;
+        pp[1] = tnu;
+    }
+}
+
+// Per arc pricing.  p == 2 and uniform W: closed form from the block moments,
+//   sum_{t,s} a_t b_s |D + d_t - e_s|^2 = A0 B0 |D|^2 + 2 D.(A1 B0 - A0 B1)
+//                                          + A2 B0 + A0 B2 - 2 A1.B1,
+// D = kappa (k - l); otherwise direct summation over the kappa^2d entries.
+template <bool UNIFORM>
+__global__ void __launch_bounds__(MT) price_kernel(
+    const int64_t *__restrict__ arc_off, const int32_t *__restrict__ row_ptr,
+    const int32_t *__restrict__ row_arc_col, const double *__restrict__ row_arc_mass,
+    const double *__restrict__ W, const double *__restrict__ out, const int32_t *__restrict__ status,
+    const double *__restrict__ scratch, int64_t stride_pair, const double *__restrict__ mom,
+    double *__restrict__ part, G32 f, G32 c, int kappa, double p, const double *__restrict__ table,
+    int closed_form) {
+    __shared__ double sh[32];
+    const int64_t b = blockIdx.y;
+    const int N = f.cells, n = c.cells;
+    const int m = (int)ipow(kappa, f.nd);
+    const int MW = 2 * (f.nd + 2);
+    const int64_t A = arc_off[b + 1] - arc_off[b];
+    double acc = 0.0;
+    const int64_t item = (int64_t)blockIdx.x * MT + threadIdx.x;
+    const int64_t q = closed_form ? item : item / m;       // arc
+    const int t = closed_form ? 0 : (int)(item - q * m);   // row offset (brute force)
+    if (status[b] == GDT_PAIR_OK && q < A) {
+        const int32_t *rptr = row_ptr + b * (n + 1);
+        int lo = 0, hi = n;  // row block of arc q
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (rptr[mid] <= q) lo = mid;
+            else hi = mid;
+        }
+        const int k = lo, l = row_arc_col[arc_off[b] + q];
+        const double mass = row_arc_mass[arc_off[b] + q];
+        if (closed_form) {
+            const double *Ak = mom + ((int64_t)b * n + k) * MW;
+            const double *Bl = mom + ((int64_t)b * n + l) * MW + (f.nd + 2);
+            double d2 = 0.0, cross = 0.0, ab = 0.0;
+            int kk = k, ll = l;
+            for (int a = c.nd - 1; a >= 0; --a) {
+                const int ka = kk / c.stride[a], la = ll / c.stride[a];
+                kk -= ka * c.stride[a];
+                ll -= la * c.stride[a];
+                const double D = (double)(kappa * (ka - la));
+                d2 += D * D;
+                cross += D * (Ak[1 + a] * Bl[0] - Ak[0] * Bl[1 + a]);
+                ab += Ak[1 + a] * Bl[1 + a];
+            }
+            const double s = Ak[0] * Bl[0] * d2 + 2.0 * cross + Ak[1 + f.nd] * Bl[0] +
+                             Ak[0] * Bl[1 + f.nd] - 2.0 * ab;
+            acc = mass * W[0] * s;
+        } else {
+            const double *ws = scratch + b * stride_pair;
+            const double *a = out[b * 8 + 7] == 0.0 ? ws : ws + N;
+            const double *bv = ws + 2 * N;
+            // coordinates of row cell (k, t) minus the origin of block l
+            int dd[GDT_MAX_DIM] = {0, 0, 0, 0};
+            int i = 0, kk = k, ll = l, tt = t;
+            for (int aa = c.nd - 1; aa >= 0; --aa) {
+                const int ka = kk / c.stride[aa], la = ll / c.stride[aa];
+                kk -= ka * c.stride[aa];
+                ll -= la * c.stride[aa];
+                dd[aa] = (ka - la) * kappa;
+            }
+            for (int aa = 0; aa < f.nd; ++aa) {
+                const int ta = tt % kappa;
+                tt /= kappa;
+                dd[aa] += ta;
+            }
+            i = block_origin(k, c, f, kappa);
+            {
+                int rem = t;
+                for (int aa = 0; aa < f.nd; ++aa) {
+                    i += (rem % kappa) * f.stride[aa];
+                    rem /= kappa;
+                }
+            }
+            const double ai = a[i];
+            if (ai != 0.0) {
+                const double am = __dmul_rn(mass, UNIFORM ? W[0] : 0.0);
+                const int ol = block_origin(l, c, f, kappa);
+                for_block_cells(ol, f, kappa, [&](int s, int j) {
+                    int sq = 0, rem = s;
+                    for (int aa = 0; aa < f.nd; ++aa) {
+                        const int d = dd[aa] - rem % kappa;
+                        rem /= kappa;
+                        sq += d * d;
+                    }
+                    const double coef = UNIFORM ? am : __dmul_rn(mass, W[t * m + s]);
+                    const double fitted = __dmul_rn(__dmul_rn(ai, coef), bv[j]);
+                    acc += fitted * cost_from_sq(sq, p, table);
+                });
+            }
+        }
+    }
+    acc = block_sum<MT>(acc, sh);
+    if (threadIdx.x == 0) part[(int64_t)b * gridDim.x + blockIdx.x] = acc;
+}
+
+__global__ void finish_kernel(const double *__restrict__ tv_part, int tv_ctas,
+                              const double *__restrict__ pr_part, int pr_ctas,
+                              const int32_t *__restrict__ status, double *__restrict__ out,
+                              int64_t batch) {
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= batch || status[b] != GDT_PAIR_OK) return;
+    double tmu = 0.0, tnu = 0.0, pr = 0.0;
+    for (int i = 0; i < tv_ctas; ++i) {
+        tmu += tv_part[(b * tv_ctas + i) * 2];
+        tnu += tv_part[(b * tv_ctas + i) * 2 + 1];
+    }
+    for (int i = 0; i < pr_ctas; ++i) pr += pr_part[b * pr_ctas + i];
+    out[b * 8 + 0] = pr;
+    out[b * 8 + 1] = tmu;
+    out[b * 8 + 2] = tnu;
 }
 
 // ---------------------------------------------------------------------------
@@ -422,9 +568,9 @@ __global__ void __launch_bounds__(PT) csr_ipf_kernel(
     const int32_t *__restrict__ tindices, const double *__restrict__ tdata,
     const double *__restrict__ mu, const double *__restrict__ nu, int64_t nr, int64_t nc,
     double xi, int64_t max_iter, double *__restrict__ a, double *__restrict__ b,
-    double *__restrict__ kb, double *__restrict__ kta, double *__restrict__ a_prev,
-    double *__restrict__ info, int32_t *__restrict__ status) {
-    __shared__ double sh[(PT / 32) * 8];
+    double *__restrict__ kb, double *__restrict__ kta, double *__restrict__ info,
+    int32_t *__restrict__ status) {
+    __shared__ double sh[(PT / 32) * 6];
     for (int64_t j = threadIdx.x; j < nc; j += PT) b[j] = 1.0;
     __syncthreads();
     auto rowpass = [&]() {
@@ -443,7 +589,7 @@ __global__ void __launch_bounds__(PT) csr_ipf_kernel(
     bool conv = false;
     while (it < max_iter) {
         ++it;
-        Red r{0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0, 0, 0};
+        Red r = red_init();
         for (int64_t i = threadIdx.x; i < nr; i += PT) {
             if (kb[i] <= 0.0 && mu[i] > 0.0) r.zrow = 1;
             a[i] = kb[i] > 0.0 ? __ddiv_rn(mu[i], kb[i]) : 0.0;
@@ -475,8 +621,10 @@ __global__ void __launch_bounds__(PT) csr_ipf_kernel(
             r.gap += fabs(__dsub_rn(nu[j], __dmul_rn(b[j], kta[j])));
         }
         block_reduce_red(r, sh);
-        const bool bad_a = r.amin <= r.amax && (r.amin < 1e-100 || r.amax > 1e100 || !isfinite(r.amax));
-        const bool bad_b = r.bmin <= r.bmax && (r.bmin < 1e-100 || r.bmax > 1e100 || !isfinite(r.bmax));
+        const bool bad_a =
+            r.amin <= r.amax && (r.amin < 1e-100 || r.amax > 1e100 || !isfinite(r.amax));
+        const bool bad_b =
+            r.bmin <= r.bmax && (r.bmin < 1e-100 || r.bmax > 1e100 || !isfinite(r.bmax));
         if (bad_a || bad_b || r.nonfinite) {
             st = GDT_PAIR_OVERFLOW;
             break;
@@ -487,7 +635,6 @@ __global__ void __launch_bounds__(PT) csr_ipf_kernel(
             break;
         }
     }
-    (void)a_prev;
     if (threadIdx.x == 0) {
         info[0] = (double)it;
         info[1] = gap;
@@ -497,20 +644,64 @@ __global__ void __launch_bounds__(PT) csr_ipf_kernel(
     }
 }
 
+__device__ __forceinline__ double grid_cost64(int64_t i, int64_t j, const Grid &f, double p,
+                                              const double *table) {
+    int64_t sq = 0;
+    for (int a = f.nd - 1; a >= 0; --a) {
+        const int64_t xi = i / f.stride[a], xj = j / f.stride[a];
+        i -= xi * f.stride[a];
+        j -= xj * f.stride[a];
+        sq += (xi - xj) * (xi - xj);
+    }
+    return cost_from_sq(sq, p, table);
+}
+
 __global__ void price_coo_kernel(const int64_t *__restrict__ row, const int64_t *__restrict__ col,
                                  const double *__restrict__ mass, int64_t nnz,
                                  const double *__restrict__ a, const double *__restrict__ b,
                                  const double *__restrict__ table, double p, Grid f,
-                                 double *__restrict__ out) {
+                                 double *__restrict__ part) {
     __shared__ double sh[32];
     double acc = 0.0;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
          e += (int64_t)gridDim.x * blockDim.x) {
         const double fitted = __dmul_rn(__dmul_rn(a[row[e]], mass[e]), b[col[e]]);
-        acc += fitted * grid_cost(row[e], col[e], f, p, table);
+        acc += fitted * grid_cost64(row[e], col[e], f, p, table);
     }
     acc = block_sum<256>(acc, sh);
-    if (threadIdx.x == 0) atomicAdd(out, acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void sum_parts_kernel(const double *__restrict__ part, int count, double *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < count; ++i) s += part[i];
+        out[0] = s;
+    }
+}
+
+// scratch layout per pair: [aA N][aB N][b N][kb U][kta U]; then, after all
+// pairs: moments [B, n, MW], tv partials [B, tv_ctas, 2], price partials
+// [B, pr_ctas]
+struct PrimalLayout {
+    int64_t stride_pair, mom_off, tv_off, pr_off, total, tv_ctas, pr_ctas;
+};
+
+inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, bool uniform,
+                                  bool p2, int64_t max_arcs) {
+    PrimalLayout L;
+    const int64_t U = uniform ? c.cells : f.cells;
+    L.stride_pair = 3 * f.cells + 2 * U;
+    L.mom_off = batch * L.stride_pair;
+    const int64_t MW = 2 * (f.nd + 2);
+    L.tv_ctas = (c.cells + MT - 1) / MT;
+    // brute-force pricing has one item per (arc, row offset): f.cells / c.cells = kappa^d
+    const int64_t items = (uniform && p2) ? max_arcs : max_arcs * (f.cells / c.cells);
+    L.pr_ctas = (items + MT - 1) / MT;
+    L.tv_off = L.mom_off + batch * c.cells * MW;
+    L.pr_off = L.tv_off + batch * L.tv_ctas * 2;
+    L.total = L.pr_off + batch * L.pr_ctas;
+    return L;
 }
 
 }  // namespace gdt
@@ -521,22 +712,25 @@ extern "C" int64_t gdt_primal_scratch_bytes(int64_t batch, int ndim, const int64
                                             int kappa, int kernel_uniform) {
     Grid f, c;
     if (!make_grid(f, ndim, dims) || !make_coarse(c, f, kappa)) return -1;
-    const int64_t U = kernel_uniform ? c.cells : f.cells;
-    return (int64_t)sizeof(double) * batch * (3 * f.cells + 2 * U);
+    // a basic solution has at most 2n - 1 positive arcs (ns + nt - 1)
+    // sized for the brute-force pricing layout (the larger one)
+    const PrimalLayout L = primal_layout(batch, f, c, kernel_uniform != 0, false, 2 * c.cells);
+    return (int64_t)sizeof(double) * L.total;
 }
 
 extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int64_t *arc_off,
-                                        const int32_t *row_ptr, const int32_t *row_arc_col,
-                                        const double *row_arc_mass, const int32_t *col_ptr,
-                                        const int32_t *col_arc_row, const double *col_arc_mass,
-                                        const double *kernel_w, int kernel_uniform,
-                                        const double *xi, int64_t max_iter, double p,
-                                        int64_t batch, int ndim, const int64_t *dims, int kappa,
-                                        const double *cost_table, int64_t max_sq, double *out,
-                                        int32_t *status, void *scratch, void *stream) {
+                                  const int32_t *row_ptr, const int32_t *row_arc_col,
+                                  const double *row_arc_mass, const int32_t *col_ptr,
+                                  const int32_t *col_arc_row, const double *col_arc_mass,
+                                  const double *kernel_w, int kernel_uniform, const double *xi,
+                                  int64_t max_iter, double p, int64_t batch, int ndim,
+                                  const int64_t *dims, int kappa, const double *cost_table,
+                                  int64_t max_sq, double *out, int32_t *status, void *scratch,
+                                  void *stream) {
     Grid f, c;
     GDT_CHECK_ARG(make_grid(f, ndim, dims) && make_coarse(c, f, kappa),
                   "gdt_primal_upscale: dims must be positive multiples of kappa");
+    GDT_CHECK_ARG(f.cells < (1ll << 31), "gdt_primal_upscale: grid too large for int32 indexing");
     GDT_CHECK_ARG(p >= 1.0 && max_iter >= 1 && batch >= 0, "gdt_primal_upscale: bad p/max_iter");
     int64_t need_sq = 0;
     for (int a = 0; a < ndim; ++a) need_sq += (dims[a] - 1) * (dims[a] - 1);
@@ -544,14 +738,40 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
                   "gdt_primal_upscale: cost_table required for p not in {1, 2}");
     if (batch == 0) return GDT_OK;
     cudaStream_t st = as_stream(stream);
-    if (kernel_uniform)
-        primal_kernel<true><<<(unsigned)batch, PT, 0, st>>>(
-            mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row, col_arc_mass,
-            kernel_w, xi, max_iter, p, f, c, kappa, cost_table, out, status, (double *)scratch);
+    const bool uni = kernel_uniform != 0;
+    const PrimalLayout L = primal_layout(batch, f, c, uni, p == 2.0, 2 * c.cells);
+    double *ws = (double *)scratch;
+    const G32 f32 = to32(f), c32 = to32(c);
+    if (uni)
+        ipf_kernel<true><<<(unsigned)batch, PT, 0, st>>>(
+            mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
+            col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair);
     else
-        primal_kernel<false><<<(unsigned)batch, PT, 0, st>>>(
-            mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row, col_arc_mass,
-            kernel_w, xi, max_iter, p, f, c, kappa, cost_table, out, status, (double *)scratch);
+        ipf_kernel<false><<<(unsigned)batch, PT, 0, st>>>(
+            mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
+            col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair);
+    const int closed = uni && p == 2.0;
+    dim3 gtv((unsigned)L.tv_ctas, (unsigned)batch), gpr((unsigned)L.pr_ctas, (unsigned)batch);
+    if (uni) {
+        moments_tv_kernel<true><<<gtv, MT, 0, st>>>(mu, nu, out, status, ws, L.stride_pair,
+                                                    ws + L.mom_off, ws + L.tv_off, f32, c32,
+                                                    kappa, p, closed);
+        price_kernel<true><<<gpr, MT, 0, st>>>(arc_off, row_ptr, row_arc_col, row_arc_mass,
+                                               kernel_w, out, status, ws, L.stride_pair,
+                                               ws + L.mom_off, ws + L.pr_off, f32, c32, kappa, p,
+                                               cost_table, closed);
+    } else {
+        moments_tv_kernel<false><<<gtv, MT, 0, st>>>(mu, nu, out, status, ws, L.stride_pair,
+                                                     ws + L.mom_off, ws + L.tv_off, f32, c32,
+                                                     kappa, p, 0);
+        price_kernel<false><<<gpr, MT, 0, st>>>(arc_off, row_ptr, row_arc_col, row_arc_mass,
+                                                kernel_w, out, status, ws, L.stride_pair,
+                                                ws + L.mom_off, ws + L.pr_off, f32, c32, kappa, p,
+                                                cost_table, 0);
+    }
+    finish_kernel<<<grid_size(batch, 128), 128, 0, st>>>(ws + L.tv_off, (int)L.tv_ctas,
+                                                         ws + L.pr_off, (int)L.pr_ctas, status,
+                                                         out, batch);
     return cuda_status("gdt_primal_upscale");
 }
 
@@ -563,7 +783,7 @@ extern "C" int gdt_ipf_csr(const int64_t *indptr, const int32_t *indices, const 
     GDT_CHECK_ARG(nr >= 1 && nc >= 1 && max_iter >= 1, "gdt_ipf_csr: bad sizes");
     csr_ipf_kernel<<<1, PT, 0, as_stream(stream)>>>(indptr, indices, data, t_indptr, t_indices,
                                                     t_data, mu, nu, nr, nc, xi, max_iter, out_a,
-                                                    out_b, out_kb, out_kta, nullptr, info, status);
+                                                    out_b, out_kb, out_kta, info, status);
     return cuda_status("gdt_ipf_csr");
 }
 
@@ -575,10 +795,17 @@ extern "C" int gdt_price_coo(const int64_t *row, const int64_t *col, const doubl
     GDT_CHECK_ARG(make_grid(f, ndim, dims) && p >= 1.0, "gdt_price_coo: bad grid");
     (void)max_sq;
     cudaStream_t st = as_stream(stream);
-    cudaMemsetAsync(out, 0, sizeof(double), st);
-    if (nnz == 0) return cuda_status("gdt_price_coo");
+    if (nnz == 0) {
+        cudaMemsetAsync(out, 0, sizeof(double), st);
+        return cuda_status("gdt_price_coo");
+    }
     unsigned g = grid_size(nnz, 256);
     if (g > 1184) g = 1184;
-    price_coo_kernel<<<g, 256, 0, st>>>(row, col, mass, nnz, a, b, cost_table, p, f, out);
+    double *part = nullptr;
+    if (cudaMallocAsync(&part, sizeof(double) * g, st) != cudaSuccess)
+        return cuda_status("gdt_price_coo: workspace");
+    price_coo_kernel<<<g, 256, 0, st>>>(row, col, mass, nnz, a, b, cost_table, p, f, part);
+    sum_parts_kernel<<<1, 32, 0, st>>>(part, (int)g, out);
+    cudaFreeAsync(part, st);
     return cuda_status("gdt_price_coo");
 }

@@ -214,3 +214,42 @@ def test_weighted_tv_and_errors():
         G.weighted_cost_upper_bound(a, G.GridMeasure(G.GridSpec((4, 16)), a.mass), 2, 2.0)
     with pytest.raises(G.DimensionMismatchError):
         G.primal_upscaling_upper_bound(a, b, 2, 1.0, kernel=G.UpscaleKernel.uniform(4, 2))
+
+
+@pytest.mark.parametrize("dims", [(32, 32), (48, 16), (16, 8, 8), (32, 32, 32)])
+@pytest.mark.parametrize("p", [1.0, 1.5])
+def test_pruned_grid_ctransform_exact_fp64(dims, p):
+    """Tile-pruned brute force == oracle brute force, bit for bit (fp64), on
+    smooth and on rough (white-noise) potentials."""
+    from paper_2506_00976_b200.device import to_dev, to_host
+    from paper_2506_00976_b200.engine import ctransform_pair
+
+    rng = np.random.default_rng(sum(dims))
+    n = int(np.prod(dims))
+    X = P.grid_coords(dims)
+    smooth = np.sin(X[:, 0] / 5.0) * 7.0 + np.cos(X[:, 1] / 3.0) * 4.0
+    for v in (smooth, rng.normal(size=n) * 10.0):
+        if n > 4096 and v is not smooth:
+            continue
+        mass = np.full(n, 1.0 / n)
+        f, g, dots = ctransform_pair(to_dev(v[None]), to_dev(mass[None]), to_dev(mass[None]),
+                                     dims, p, "fp64")
+        ref_g = P.ctransform(v, X, X, p, "target")
+        assert _bits(to_host(g)[0], ref_g)
+        ref_f = P.ctransform(ref_g, X, X, p, "source")
+        assert _bits(to_host(f)[0], ref_f)
+
+
+@pytest.mark.parametrize("dims", [(32, 32), (16, 8, 8)])
+def test_pruned_grid_ctransform_fp32_close(dims):
+    from paper_2506_00976_b200.device import to_dev, to_host
+    from paper_2506_00976_b200.engine import ctransform_pair
+
+    n = int(np.prod(dims))
+    X = P.grid_coords(dims)
+    v = np.sin(X[:, 0] / 5.0) * 7.0 + np.cos(X[:, 1] / 3.0) * 4.0
+    mass = np.full(n, 1.0 / n)
+    f, g, dots = ctransform_pair(to_dev(v[None]), to_dev(mass[None]), to_dev(mass[None]), dims,
+                                 1.0, "fp32")
+    ref_g = P.ctransform(v, X, X, 1.0, "target")
+    assert np.max(np.abs(to_host(g)[0] - ref_g)) <= 1e-5 * max(1.0, np.abs(ref_g).max())
