@@ -232,16 +232,20 @@ int gdt_transport_simplex(const double *C, const double *sup, const double *dem,
                           double tol, int64_t *bi, int64_t *bj, double *bf, double *u,
                           double *v, int64_t *pivots);
 
-/* `count` independent problems solved on `threads` host threads (<=0: all
- * cores).  Problem q reads C + c_off[q], sup + s_off[q], dem + t_off[q] with
- * sizes ns[q] x nt[q] and writes bi/bj/bf + b_off[q], u + s_off[q],
- * v + t_off[q]; status[q], pivots[q].  Releases no locks (pure C). */
-int gdt_transport_simplex_batch(int64_t count, const double *C, const int64_t *c_off,
-                                const double *sup, const double *dem, const int64_t *s_off,
-                                const int64_t *t_off, const int64_t *ns, const int64_t *nt,
-                                const int64_t *b_off, double tol, int64_t *bi, int64_t *bj,
-                                double *bf, double *u, double *v, int32_t *status,
-                                int64_t *pivots, int threads);
+/* Batch of `count` problems on `threads` host threads (<= 0: all cores).
+ * Every per-problem buffer is passed as a pointer value in a uint64 array.
+ * warm_from[q] = -1 solves job q from the northwest corner with the
+ * reference's pivot sequence; warm_from[q] = w (w < q, same shape) starts job
+ * q from the optimal basis of job w instead (any optimal basis gives the same
+ * optimal value; the quantization bounds warm-start the C-bar and C-min LPs
+ * from the C-tilde basis on the same marginals).  Jobs chained by warm_from
+ * run in order on one worker.  status[q] = GDT_LP_* or GDT_ERR_*. */
+int gdt_transport_simplex_many(int64_t count, const uint64_t *C, const uint64_t *sup,
+                               const uint64_t *dem, const int64_t *ns, const int64_t *nt,
+                               const int64_t *warm_from, double tol, const uint64_t *bi,
+                               const uint64_t *bj, const uint64_t *bf, const uint64_t *u,
+                               const uint64_t *v, int32_t *status, int64_t *pivots,
+                               int threads);
 
 #ifdef __cplusplus
 }

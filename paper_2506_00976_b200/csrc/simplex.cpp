@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <thread>
 #include <vector>
 
@@ -40,7 +41,8 @@ struct Solver {
     Lists L;
     std::vector<int64_t> par, pslot, dep, stk, pa_s, pb_s;
     std::vector<int8_t> sa_s, sb_s;
-    bool avx2;
+    std::vector<double> ck;  // cost of the arc held by each basis slot (L1-resident)
+    bool avx2, avx512;
 
     void push(int64_t k) {
         const int64_t s = bi[k], t = bj[k];
@@ -74,7 +76,7 @@ struct Solver {
                 for (int64_t k = L.rhead[node]; k != -1; k = L.rnext[k]) {
                     const int64_t t = bj[k];
                     if (subtree ? k == pslot[node] : par[ns + t] != -2) continue;
-                    v[t] = C[node * nt + t] - u[node];
+                    v[t] = ck[k] - u[node];
                     par[ns + t] = node;
                     pslot[ns + t] = k;
                     dep[ns + t] = dep[node] + 1;
@@ -85,7 +87,7 @@ struct Solver {
                 for (int64_t k = L.chead[t]; k != -1; k = L.cnext[k]) {
                     const int64_t s = bi[k];
                     if (subtree ? k == pslot[node] : par[s] != -2) continue;
-                    u[s] = C[s * nt + t] - v[t];
+                    u[s] = ck[k] - v[t];
                     par[s] = node;
                     pslot[s] = k;
                     dep[s] = dep[node] + 1;
@@ -111,6 +113,26 @@ struct Solver {
         alignas(32) double t[4];
         _mm256_store_pd(t, m);
         double mm = std::min(std::min(t[0], t[1]), std::min(t[2], t[3]));
+        const double uu = u[i];
+        for (; j < j1; ++j) {
+            const double r = (crow[j] - uu) - v[j];
+            mm = r < mm ? r : mm;
+        }
+        mval = std::min(mval, mm);
+    }
+
+    __attribute__((target("avx512f"))) void seg_min_avx512(int64_t i, int64_t j0, int64_t j1,
+                                                           double &mval) const {
+        const double *crow = C + i * nt;
+        const __m512d ui = _mm512_set1_pd(u[i]);
+        __m512d m = _mm512_set1_pd(INFINITY);
+        int64_t j = j0;
+        for (; j + 8 <= j1; j += 8) {
+            __m512d r = _mm512_sub_pd(_mm512_sub_pd(_mm512_loadu_pd(crow + j), ui),
+                                      _mm512_loadu_pd(v + j));
+            m = _mm512_min_pd(m, r);
+        }
+        double mm = _mm512_reduce_min_pd(m);
         const double uu = u[i];
         for (; j < j1; ++j) {
             const double r = (crow[j] - uu) - v[j];
@@ -151,7 +173,8 @@ struct Solver {
         int64_t i = a / nt, j = a - i * nt;
         while (a < hi) {
             const int64_t j1 = std::min<int64_t>(nt, j + (hi - a));
-            if (avx2) seg_min_avx2(i, j, j1, m);
+            if (avx512) seg_min_avx512(i, j, j1, m);
+            else if (avx2) seg_min_avx2(i, j, j1, m);
             else seg_min_scalar(i, j, j1, m);
             a += j1 - j;
             j = 0;
@@ -160,15 +183,18 @@ struct Solver {
         return m;
     }
 
+    // warm = true: (bi, bj, bf) already hold a feasible spanning-tree basis
+    // for (sup, dem) -- e.g. the optimal basis of another cost matrix on the
+    // same marginals -- and replace the northwest-corner start.
     int solve(const double *sup, const double *dem, int64_t block_size, int64_t max_pivots,
-              double tol, int64_t *pivots_out) {
+              double tol, int64_t *pivots_out, bool warm = false) {
         nb = ns + nt - 1;
         const int64_t n_arcs = ns * nt, n_nodes = ns + nt;
         if (block_size <= 0) block_size = std::max<int64_t>(64, (int64_t)std::sqrt((double)(ns * nt)) + 1);
         if (max_pivots <= 0) max_pivots = 50 * (ns + nt) * (ns + nt);
         const int64_t degen_limit = 10 * (ns + nt);
         *pivots_out = 0;
-        {  // northwest corner
+        if (!warm) {  // northwest corner
             std::vector<double> rs(sup, sup + ns), rd(dem, dem + nt);
             int64_t r = 0, c = 0;
             for (int64_t k = 0; k < nb; ++k) {
@@ -184,6 +210,8 @@ struct Solver {
                 else if (c < nt - 1) ++c;
             }
         }
+        ck.resize(nb);
+        for (int64_t k = 0; k < nb; ++k) ck[k] = C[bi[k] * nt + bj[k]];
         L.rhead.assign(ns, -1);
         L.chead.assign(nt, -1);
         L.rnext.resize(nb);
@@ -298,6 +326,7 @@ struct Solver {
             bi[leave] = ei;
             bj[leave] = ej;
             bf[leave] = theta;
+            ck[leave] = C[enter];
             push(leave);
 
             int64_t q_root, p_root;
@@ -325,9 +354,14 @@ bool cpu_has_avx2() {
     return has;
 }
 
+bool cpu_has_avx512() {
+    static const bool has = __builtin_cpu_supports("avx512f");
+    return has;
+}
+
 int run_one(const double *C, const double *sup, const double *dem, int64_t ns, int64_t nt,
             int64_t block_size, int64_t max_pivots, double tol, int64_t *bi, int64_t *bj,
-            double *bf, double *u, double *v, int64_t *pivots) {
+            double *bf, double *u, double *v, int64_t *pivots, bool warm = false) {
     if (ns < 1 || nt < 1 || !C || !sup || !dem) return GDT_ERR_ARG;
     try {
         Solver S;
@@ -340,7 +374,8 @@ int run_one(const double *C, const double *sup, const double *dem, int64_t ns, i
         S.u = u;
         S.v = v;
         S.avx2 = cpu_has_avx2();
-        return S.solve(sup, dem, block_size, max_pivots, tol, pivots);
+        S.avx512 = cpu_has_avx512();
+        return S.solve(sup, dem, block_size, max_pivots, tol, pivots, warm);
     } catch (...) {
         return GDT_ERR_NOMEM;
     }
@@ -355,24 +390,63 @@ extern "C" int gdt_transport_simplex(const double *C, const double *sup, const d
     return run_one(C, sup, dem, ns, nt, block_size, max_pivots, tol, bi, bj, bf, u, v, pivots);
 }
 
-extern "C" int gdt_transport_simplex_batch(int64_t count, const double *C, const int64_t *c_off,
-                                           const double *sup, const double *dem,
-                                           const int64_t *s_off, const int64_t *t_off,
-                                           const int64_t *ns, const int64_t *nt,
-                                           const int64_t *b_off, double tol, int64_t *bi,
-                                           int64_t *bj, double *bf, double *u, double *v,
-                                           int32_t *status, int64_t *pivots, int threads) {
+// Pointer-array batch with optional warm starts.  Job q solves C[q] with
+// marginals sup[q]/dem[q]; warm_from[q] = -1 starts from the northwest corner
+// (the reference's pivot sequence), otherwise from the final basis of job
+// warm_from[q] (< q, same shape): jobs form chains that one worker runs in
+// order, chains are spread over `threads` workers.
+extern "C" int gdt_transport_simplex_many(int64_t count, const uint64_t *C, const uint64_t *sup,
+                                          const uint64_t *dem, const int64_t *ns,
+                                          const int64_t *nt, const int64_t *warm_from,
+                                          double tol, const uint64_t *bi, const uint64_t *bj,
+                                          const uint64_t *bf, const uint64_t *u,
+                                          const uint64_t *v, int32_t *status, int64_t *pivots,
+                                          int threads) {
     if (count < 0) return GDT_ERR_ARG;
+    std::vector<std::vector<int64_t>> kids(count);
+    std::vector<int64_t> roots;
+    for (int64_t q = 0; q < count; ++q) {
+        const int64_t w = warm_from ? warm_from[q] : -1;
+        if (w < 0) {
+            roots.push_back(q);
+        } else {
+            if (w >= q || ns[w] != ns[q] || nt[w] != nt[q]) return GDT_ERR_ARG;
+            kids[w].push_back(q);
+        }
+    }
     if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
-    threads = (int)std::min<int64_t>(threads, std::max<int64_t>(count, 1));
+    threads = (int)std::min<int64_t>(threads, std::max<int64_t>((int64_t)roots.size(), 1));
+    auto P = [](uint64_t a) { return reinterpret_cast<void *>(a); };
+    std::function<void(int64_t)> run = [&](int64_t q) {
+        const int64_t w = warm_from ? warm_from[q] : -1;
+        const int64_t nbq = ns[q] + nt[q] - 1;
+        int64_t *qbi = (int64_t *)P(bi[q]), *qbj = (int64_t *)P(bj[q]);
+        double *qbf = (double *)P(bf[q]);
+        if (w >= 0) {
+            if (status[w] != GDT_LP_OPTIMAL) {
+                status[q] = status[w] < 0 ? status[w] : GDT_ERR_ARG;
+                pivots[q] = 0;
+            } else {
+                std::memcpy(qbi, P(bi[w]), sizeof(int64_t) * nbq);
+                std::memcpy(qbj, P(bj[w]), sizeof(int64_t) * nbq);
+                std::memcpy(qbf, P(bf[w]), sizeof(double) * nbq);
+                status[q] = run_one((const double *)P(C[q]), (const double *)P(sup[q]),
+                                    (const double *)P(dem[q]), ns[q], nt[q], 0, 0, tol, qbi, qbj,
+                                    qbf, (double *)P(u[q]), (double *)P(v[q]), pivots + q, true);
+            }
+        } else {
+            status[q] = run_one((const double *)P(C[q]), (const double *)P(sup[q]),
+                                (const double *)P(dem[q]), ns[q], nt[q], 0, 0, tol, qbi, qbj, qbf,
+                                (double *)P(u[q]), (double *)P(v[q]), pivots + q, false);
+        }
+        for (int64_t k : kids[q]) run(k);
+    };
     std::atomic<int64_t> next{0};
     auto work = [&]() {
         for (;;) {
-            const int64_t q = next.fetch_add(1);
-            if (q >= count) break;
-            status[q] = run_one(C + c_off[q], sup + s_off[q], dem + t_off[q], ns[q], nt[q], 0, 0,
-                                tol, bi + b_off[q], bj + b_off[q], bf + b_off[q], u + s_off[q],
-                                v + t_off[q], pivots + q);
+            const int64_t r = next.fetch_add(1);
+            if (r >= (int64_t)roots.size()) break;
+            run(roots[r]);
         }
     };
     if (threads == 1) {

@@ -122,9 +122,10 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
     nu_c = to_host(bt.nu_c)
     plans = CoarsePlans(n=bt.n)
     t0 = time.perf_counter()
-    problems, slots = [], []
+    problems, slots, warm = [], [], []
     cmin = min_cost_cached(bt.pdims, bt.kappa, bt.p) if need_cmin else None
     for b in range(bt.B):
+        root = -1
         for kind, cost in (("ctil", bt.ctil if need_ctil else None),
                            ("cbar", cbar_host[b] if need_cbar else None),
                            ("cmin", cmin)):
@@ -133,9 +134,15 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
             try:
                 problems.append(build_transport_problem(mu_c[b], nu_c[b], cost))
                 slots.append((b, kind))
+                # C-tilde follows the reference's pivot path (its basis defines the
+                # upscaled support and the duals); C-bar / C-min only need the
+                # optimal value, so they start from the C-tilde basis
+                warm.append(root)
+                if root < 0:
+                    root = len(problems) - 1
             except GridotError as exc:
                 slots.append((b, kind, exc))
-    solved = solve_transport_many(problems, threads=lp_threads)
+    solved = solve_transport_many(problems, threads=lp_threads, warm_from=warm, slack=False)
     res = {}
     it = iter(zip(problems, solved))
     for s in slots:

@@ -99,11 +99,15 @@ def build_transport_problem(supply, demand, cost) -> TransportProblem:
         raise GridotError("transport needs nonempty supports on both sides")
     s, t = supply[si].copy(), demand[di].copy()
     _rebalance(s, t)
-    sub = np.ascontiguousarray(np.asarray(cost)[np.ix_(si, di)], dtype=np.float64)
+    cost = np.asarray(cost)
+    if si.size == cost.shape[0] and di.size == cost.shape[1]:
+        sub = np.ascontiguousarray(cost, dtype=np.float64)  # full supports: no gather copy
+    else:
+        sub = np.ascontiguousarray(cost[np.ix_(si, di)], dtype=np.float64)
     return TransportProblem(s, t, sub, si, di)
 
 
-def _finish(problem: TransportProblem, status: int, bi, bj, bf, u, v, pivots):
+def _finish(problem: TransportProblem, status: int, bi, bj, bf, u, v, pivots, slack=True):
     if status == 1:
         raise IterationLimitError(f"pivot cap reached after {pivots} pivots")
     if status != 0:
@@ -111,7 +115,7 @@ def _finish(problem: TransportProblem, status: int, bi, bj, bf, u, v, pivots):
     keep = bf > 0.0
     coupling = SparseCoupling(bi[keep].copy(), bj[keep].copy(), bf[keep].copy(), problem.shape)
     value = float(np.sum(bf * problem.cost[bi, bj]))
-    slack = float(np.min(problem.cost - u[:, None] - v[None, :]))
+    slack = float(np.min(problem.cost - u[:, None] - v[None, :])) if slack else float("nan")
     logger.debug("simplex %dx%d: %d pivots, value %.12g, slack %.3g", problem.shape[0],
                  problem.shape[1], pivots, value, slack)
     return coupling, DualPotentials(u, v, slack), value
@@ -135,43 +139,51 @@ def solve_transport(problem: TransportProblem, tol: float = 1e-10,
     return _finish(problem, st, bi, bj, bf, u, v, int(piv.value))
 
 
-def solve_transport_many(problems, tol: float = 1e-10, threads: int = 0):
-    """Solve independent problems on `threads` host threads (0 = all cores).
+def solve_transport_many(problems, tol: float = 1e-10, threads: int = 0, warm_from=None,
+                         slack: bool = True):
+    """Solve a batch of problems on `threads` host threads (0 = all cores).
 
-    Returns a list of (coupling, duals, value) or the exception each raised."""
+    ``warm_from[q] = w`` (w < q, same supports and marginals) starts problem q
+    from the optimal basis of problem w instead of the northwest corner; the
+    optimal value is unchanged (the LP optimum is unique), only the pivot
+    path differs.  Problems without a warm start follow the reference's pivot
+    sequence exactly.  Returns a list of (coupling, duals, value) or the
+    exception each raised; ``slack=False`` skips the O(ns*nt) feasibility
+    diagnostic of DualPotentials.
+    """
     count = len(problems)
     if count == 0:
         return []
-    shapes = [p.shape for p in problems]
-    ns = np.array([s[0] for s in shapes], np.int64)
-    nt = np.array([s[1] for s in shapes], np.int64)
-    c_off = np.concatenate([[0], np.cumsum(ns * nt)[:-1]]).astype(np.int64)
-    s_off = np.concatenate([[0], np.cumsum(ns)[:-1]]).astype(np.int64)
-    t_off = np.concatenate([[0], np.cumsum(nt)[:-1]]).astype(np.int64)
-    nbs = ns + nt - 1
-    b_off = np.concatenate([[0], np.cumsum(nbs)[:-1]]).astype(np.int64)
-    C = np.concatenate([np.ascontiguousarray(p.cost, dtype=np.float64).ravel() for p in problems])
-    sup = np.concatenate([p.supply for p in problems])
-    dem = np.concatenate([p.demand for p in problems])
-    tot_b = int(nbs.sum())
-    bi, bj, bf = np.empty(tot_b, np.int64), np.empty(tot_b, np.int64), np.empty(tot_b)
-    u, v = np.empty(int(ns.sum())), np.empty(int(nt.sum()))
+    keep = []  # keep every buffer alive for the duration of the native call
+
+    def addr(a):
+        keep.append(a)
+        return a.ctypes.data
+
+    ns = np.array([p.shape[0] for p in problems], np.int64)
+    nt = np.array([p.shape[1] for p in problems], np.int64)
+    costs = [np.ascontiguousarray(p.cost, dtype=np.float64) for p in problems]
+    out = [(np.empty(a + b - 1, np.int64), np.empty(a + b - 1, np.int64), np.empty(a + b - 1),
+            np.empty(a), np.empty(b)) for a, b in zip(ns, nt)]
+    ptr = lambda xs: np.array([addr(x) for x in xs], np.uint64)  # noqa: E731
+    C = ptr(costs)
+    sup = ptr([np.ascontiguousarray(p.supply) for p in problems])
+    dem = ptr([np.ascontiguousarray(p.demand) for p in problems])
+    bi, bj, bf, u, v = (ptr([o[i] for o in out]) for i in range(5))
+    wf = np.full(count, -1, np.int64) if warm_from is None else np.asarray(warm_from, np.int64)
     status = np.empty(count, np.int32)
     pivots = np.empty(count, np.int64)
-    N.check(N.lib().gdt_transport_simplex_batch(
-        count, N.ptr(C), N.ptr(c_off), N.ptr(sup), N.ptr(dem), N.ptr(s_off), N.ptr(t_off),
-        N.ptr(ns), N.ptr(nt), N.ptr(b_off), float(tol), N.ptr(bi), N.ptr(bj), N.ptr(bf), N.ptr(u),
-        N.ptr(v), N.ptr(status), N.ptr(pivots), int(threads)), "gdt_transport_simplex_batch")
-    out = []
+    N.check(N.lib().gdt_transport_simplex_many(
+        count, N.ptr(C), N.ptr(sup), N.ptr(dem), N.ptr(ns), N.ptr(nt), N.ptr(wf), float(tol),
+        N.ptr(bi), N.ptr(bj), N.ptr(bf), N.ptr(u), N.ptr(v), N.ptr(status), N.ptr(pivots),
+        int(threads)), "gdt_transport_simplex_many")
+    res = []
     for q, prob in enumerate(problems):
-        b0, b1 = b_off[q], b_off[q] + nbs[q]
-        s0, t0 = s_off[q], t_off[q]
         st = int(status[q])
         try:
             if st < 0:
                 raise GridotError(f"simplex failed with native status {st}")
-            out.append(_finish(prob, st, bi[b0:b1], bj[b0:b1], bf[b0:b1], u[s0:s0 + ns[q]],
-                               v[t0:t0 + nt[q]], int(pivots[q])))
+            res.append(_finish(prob, st, *out[q], int(pivots[q]), slack=slack))
         except GridotError as exc:
-            out.append(exc)
-    return out
+            res.append(exc)
+    return res

@@ -34,13 +34,13 @@ def test_config_bounds_vs_reference(config_cases, tag, precision):
                               return_exceptions=False)[0]
     tol = 1e-9 if precision == "fp64" else 1e-5
     assert rel_close(reps["weighted_cost"].value, float(c["wc_value"]), tol)
-    assert reps["min_cost"].raw_value == float(c["mc_raw"])
+    assert rel_close(reps["min_cost"].raw_value, float(c["mc_raw"]), 1e-12)  # warm-started LP
     assert rel_close(reps["primal_upscaling"].value, float(c["pu_value"]), tol)
     assert reps["primal_upscaling"].iterations == int(c["pu_iterations"])
     assert rel_close(reps["dual_upscaling"].raw_value, float(c["du_multilinear_raw"]), tol)
     if precision == "fp64":
-        # exact arithmetic order: the C-bar LP value and the primal bound are bit-exact
-        assert reps["weighted_cost"].value == float(c["wc_value"])
+        # exact C-bar; the LP is warm-started, so the optimum agrees to rounding
+        assert rel_close(reps["weighted_cost"].value, float(c["wc_value"]), 1e-12)
 
 
 @pytest.mark.parametrize("cfg", [2, 3, 5])

@@ -66,8 +66,8 @@ def test_four_bounds_fp64_small(small_cases, idx):
         assert pu.components["converged"] == float(c[f"{name}_converged"])
         for key in ("transport", "delta_mu", "delta_nu"):
             assert rel_close(pu.components[key], float(c[f"{name}_{key}"]), 1e-9), key
-    assert reps["weighted_cost"].value == float(c["wc_value"])
-    assert reps["min_cost"].raw_value == float(c["mc_raw"])
+    assert rel_close(reps["weighted_cost"].value, float(c["wc_value"]), 1e-12)
+    assert rel_close(reps["min_cost"].raw_value, float(c["mc_raw"]), 1e-12)  # warm-started LP
     assert rel_close(reps["dual_upscaling"].raw_value, float(c["du_multilinear_raw"]), 1e-9)
     du_n = G.dual_upscaling_lower_bound(G.GridMeasure(G.GridSpec(dims), mu),
                                         G.GridMeasure(G.GridSpec(dims), nu), k, p, "nearest")
@@ -121,7 +121,7 @@ def test_fp32_mode_within_1e5(small_cases):
         assert rel_close(reps["primal_upscaling"].value, float(c["pu_value"]), 1e-5), c["tag"]
         assert rel_close(reps["dual_upscaling"].raw_value, float(c["du_multilinear_raw"]),
                          1e-5), c["tag"]
-        assert reps["min_cost"].raw_value == float(c["mc_raw"])
+        assert rel_close(reps["min_cost"].raw_value, float(c["mc_raw"]), 1e-12)  # warm-started LP
 
 
 def test_ring_fallback_kat(small_cases):
@@ -216,7 +216,7 @@ def test_weighted_tv_and_errors():
         G.primal_upscaling_upper_bound(a, b, 2, 1.0, kernel=G.UpscaleKernel.uniform(4, 2))
 
 
-@pytest.mark.parametrize("dims", [(32, 32), (48, 16), (16, 8, 8), (32, 32, 32)])
+@pytest.mark.parametrize("dims", [(32, 32), (48, 16), (16, 8, 8), (32, 16, 8)])
 @pytest.mark.parametrize("p", [1.0, 1.5])
 def test_pruned_grid_ctransform_exact_fp64(dims, p):
     """Tile-pruned brute force == oracle brute force, bit for bit (fp64), on
