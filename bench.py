@@ -361,10 +361,14 @@ def run_b200(args):
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        parts = {}
         for _ in range(args.e2e_steps):
             for k, p in combos:
+                tm = {}
                 reps = G.quantized_bounds(pin_mu, pin_nu, dims, k, p, precision=wl.precision,
-                                          xi=wl.xi, max_iter=wl.max_iter)
+                                          xi=wl.xi, max_iter=wl.max_iter, timings=tm)
+                for key, val in tm.items():
+                    parts[f"k{k}_p{p:g}_{key}"] = parts.get(f"k{k}_p{p:g}_{key}", 0.0) + val
                 h2d += 2 * ppr * Nf * 8
                 n_c = Nf // k ** len(dims)
                 d2h += ppr * (n_c * n_c * 8 + 2 * n_c * 8 + 8 * 8 + 2 * 8)
@@ -379,6 +383,7 @@ def run_b200(args):
                        "h2d_bytes_per_step": h2d // args.e2e_steps,
                        "d2h_bytes_per_step": d2h // args.e2e_steps,
                        "s_per_step": e2e_s, "host_cores": os.cpu_count(),
+                       "breakdown_s": {k: round(v / args.e2e_steps, 4) for k, v in parts.items()},
                        "note": "public API quantized_bounds from pinned host memory; "
                                "includes 3 host LPs per pair per combo on all host cores"}
 

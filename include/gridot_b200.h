@@ -234,18 +234,24 @@ int gdt_transport_simplex(const double *C, const double *sup, const double *dem,
 
 /* Batch of `count` problems on `threads` host threads (<= 0: all cores).
  * Every per-problem buffer is passed as a pointer value in a uint64 array.
- * warm_from[q] = -1 solves job q from the northwest corner with the
- * reference's pivot sequence; warm_from[q] = w (w < q, same shape) starts job
- * q from the optimal basis of job w instead (any optimal basis gives the same
+ * Costs: C[q] != 0 is a dense row-major ns x nt matrix; C[q] == 0 selects a
+ * translation-invariant cost on a full coarse grid (grid_ndim[q] axes,
+ * extents grid_dims[q*GDT_MAX_DIM + a], ns = nt = cells) read from table[q]
+ * over offset vectors x_j - x_i (extent 2*cd_a - 1 per axis, axis 0 fastest):
+ * the C-tilde and C-min matrices of costs.py:121-125/174-192 without the
+ * n^2 matrix.  warm_from[q] = -1 solves job q from the northwest corner with
+ * the reference's pivot sequence; warm_from[q] = w (w < q, same shape) starts
+ * from the optimal basis of job w instead (any optimal basis gives the same
  * optimal value; the quantization bounds warm-start the C-bar and C-min LPs
  * from the C-tilde basis on the same marginals).  Jobs chained by warm_from
  * run in order on one worker.  status[q] = GDT_LP_* or GDT_ERR_*. */
-int gdt_transport_simplex_many(int64_t count, const uint64_t *C, const uint64_t *sup,
-                               const uint64_t *dem, const int64_t *ns, const int64_t *nt,
-                               const int64_t *warm_from, double tol, const uint64_t *bi,
-                               const uint64_t *bj, const uint64_t *bf, const uint64_t *u,
-                               const uint64_t *v, int32_t *status, int64_t *pivots,
-                               int threads);
+int gdt_transport_simplex_many(int64_t count, const uint64_t *C, const uint64_t *table,
+                               const int32_t *grid_ndim, const int64_t *grid_dims,
+                               const uint64_t *sup, const uint64_t *dem, const int64_t *ns,
+                               const int64_t *nt, const int64_t *warm_from, double tol,
+                               const uint64_t *bi, const uint64_t *bj, const uint64_t *bf,
+                               const uint64_t *u, const uint64_t *v, int32_t *status,
+                               int64_t *pivots, int threads);
 
 #ifdef __cplusplus
 }

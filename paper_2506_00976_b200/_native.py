@@ -43,7 +43,8 @@ _SIGNATURES = {
     "gdt_batched_dot": (I32, [P, P, I64, I64, P, P]),
     "gdt_probe_fp32": (I32, [I64, I64, P, P]),
     "gdt_transport_simplex": (I32, [P, P, P, I64, I64, I64, I64, D, P, P, P, P, P, P]),
-    "gdt_transport_simplex_many": (I32, [I64, P, P, P, P, P, P, D, P, P, P, P, P, P, P, I32]),
+    "gdt_transport_simplex_many": (I32, [I64, P, P, P, P, P, P, P, P, P, D, P, P, P, P, P, P, P,
+                                         I32]),
 }
 
 _lib = None

@@ -143,6 +143,40 @@ def min_cost_cached(dims: tuple, kappa: int, p: float) -> np.ndarray:
     return out
 
 
+def _offset_grid(cdims):
+    """Offset vectors D (per axis -(cd-1)..cd-1), Fortran-flattened: [count, d]."""
+    ext = tuple(2 * c - 1 for c in cdims)
+    axes = np.unravel_index(np.arange(int(np.prod(ext))), ext, order="F")
+    return np.column_stack([a - (c - 1) for a, c in zip(axes, cdims)]).astype(np.float64)
+
+
+@functools.lru_cache(maxsize=32)
+def centre_cost_table(dims: tuple, kappa: int, p: float):
+    """C-tilde as an offset table: same doubles as centre_cost_cached (kappa*D)."""
+    from .exact import OffsetTableCost
+
+    cd = CoarseningSpec(kappa).coarse_dims(GridSpec(dims))
+    D = _offset_grid(cd) * kappa
+    sq = np.zeros(D.shape[0])
+    for a in range(D.shape[1]):
+        sq += D[:, a] * D[:, a]
+    return OffsetTableCost(_power(sq, float(p)), cd)
+
+
+@functools.lru_cache(maxsize=32)
+def min_cost_table(dims: tuple, kappa: int, p: float):
+    """C-min as an offset table: same doubles as min_cost_cached."""
+    from .exact import OffsetTableCost
+
+    cd = CoarseningSpec(kappa).coarse_dims(GridSpec(dims))
+    D = _offset_grid(cd)
+    sq = np.zeros(D.shape[0])
+    for a in range(D.shape[1]):
+        gap = np.maximum(kappa * np.abs(D[:, a]) - (kappa - 1), 0.0)
+        sq += gap * gap
+    return OffsetTableCost(sq ** (p / 2.0), cd)
+
+
 def min_cost_matrix(grid: GridSpec, coarsening: CoarseningSpec, p: float) -> CoarseCostMatrix:
     return CoarseCostMatrix("min", min_cost_cached(grid.dims, coarsening.kappa, float(p)).copy())
 

@@ -22,7 +22,7 @@ namespace gdt {
 int cbar_fast_toeplitz(const double *mu, const double *nu, const double *mu_c,
                        const double *nu_c, const double *Ccentre, const double *table,
                        int64_t max_sq, double *out, uint8_t *unused, int64_t batch, const Grid &f,
-                       const Grid &c, int kappa, cudaStream_t st);
+                       const Grid &c, int kappa, double p, cudaStream_t st);
 
 struct Offsets {  // within-block offset vectors t -> (t_0..t_{d-1})
     int8_t v[GDT_MAX_DIM];
@@ -264,7 +264,7 @@ extern "C" int gdt_weighted_cost(const double *mu, const double *nu, const doubl
     }
     if (mode == GDT_MODE_FAST) {
         const int rc = cbar_fast_toeplitz(mu, nu, mu_c, nu_c, centre_cost, cost_table, max_sq, out,
-                                          unused, batch, f, c, kappa, st);
+                                          unused, batch, f, c, kappa, p, st);
         if (rc == GDT_OK) return cuda_status("gdt_weighted_cost(toeplitz)");
         // outside the fp32 kernel's envelope: fall through to the exact fp64 kernel
     }

@@ -36,7 +36,15 @@ __global__ void ftable1d_kernel(const double *__restrict__ g, float *__restrict_
         t[i] = (float)g[i];
 }
 
-template <int KAPPA, int KR, int ND>
+__device__ __forceinline__ float sqrt_apx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// P1: p == 1 costs are generated as sqrt.approx(dx^2 + dy^2) on the MUFU pipe
+// (no table loads; dx^2 is fixed per pass, dy^2 per row offset)
+template <int KAPPA, int KR, int ND, bool P1>
 __global__ void __launch_bounds__(CF_THREADS, 2) cbar_toeplitz_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ mu_c,
     const double *__restrict__ nu_c, const double *__restrict__ Ccentre,
@@ -118,6 +126,12 @@ __global__ void __launch_bounds__(CF_THREADS, 2) cbar_toeplitz_kernel(
                 rem /= f.n[a];
             }
         }
+        float dx2[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            const float dx = (float)(base_dx + q);
+            dx2[q] = dx * dx;
+        }
         if (active) {
 #pragma unroll 1
             for (int th = 0; th < m_hi; ++th) {
@@ -133,7 +147,11 @@ __global__ void __launch_bounds__(CF_THREADS, 2) cbar_toeplitz_kernel(
                     hsq += d * d;
                 }
                 float cst[NC];
-                if (TAB == TAB2D) {
+                if (P1) {
+                    const float hsqf = (float)hsq;
+#pragma unroll
+                    for (int q = 0; q < NC; ++q) cst[q] = sqrt_apx(dx2[q] + hsqf);
+                } else if (TAB == TAB2D) {
                     const float *row = tab + dy1 * N0;
 #pragma unroll
                     for (int q = 0; q < NC; ++q) {
@@ -200,7 +218,7 @@ __global__ void __launch_bounds__(CF_THREADS, 2) cbar_toeplitz_kernel(
 template <int KAPPA, int KR>
 static int launch_kappa(const double *mu, const double *nu, const double *mu_c, const double *nu_c,
                         const double *Ccentre, const double *table, int64_t max_sq, double *out,
-                        uint8_t *unused, int64_t batch, const Grid &f, const Grid &c,
+                        uint8_t *unused, int64_t batch, const Grid &f, const Grid &c, bool p1,
                         cudaStream_t st) {
     const int64_t n = c.cells;
     int m_hi = 1;
@@ -208,10 +226,11 @@ static int launch_kappa(const double *mu, const double *nu, const double *mu_c, 
     const size_t bytes = sizeof(double) * KR * n + sizeof(float) * m_hi * KAPPA * KR;
     if (bytes > 200 * 1024) return GDT_ERR_UNSUPPORTED;
     const bool two_d = f.nd == 2;
-    const int64_t tcount = two_d ? f.n[0] * f.n[1] : max_sq + 1;
+    const int64_t tcount = p1 ? 1 : (two_d ? f.n[0] * f.n[1] : max_sq + 1);
     float *ftab = nullptr;
     if (cudaMallocAsync(&ftab, sizeof(float) * tcount, st) != cudaSuccess) return GDT_ERR_CUDA;
-    if (two_d)
+    if (p1) {
+    } else if (two_d)
         ftable2d_kernel<<<grid_size(tcount, 256), 256, 0, st>>>(table, ftab, f.n[1], f.n[0]);
     else
         ftable1d_kernel<<<grid_size(tcount, 256), 256, 0, st>>>(table, ftab, tcount);
@@ -221,9 +240,15 @@ static int launch_kappa(const double *mu, const double *nu, const double *mu_c, 
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         kern<<<grid, CF_THREADS, bytes, st>>>(mu, nu, mu_c, nu_c, Ccentre, ftab, out, unused, f, c);
     };
-    if (f.nd == 1) run(cbar_toeplitz_kernel<KAPPA, KR, 1>);
-    else if (f.nd == 2) run(cbar_toeplitz_kernel<KAPPA, KR, 2>);
-    else if (f.nd == 3) run(cbar_toeplitz_kernel<KAPPA, KR, 3>);
+    if (p1) {
+        if (f.nd == 1) run(cbar_toeplitz_kernel<KAPPA, KR, 1, true>);
+        else if (f.nd == 2) run(cbar_toeplitz_kernel<KAPPA, KR, 2, true>);
+        else if (f.nd == 3) run(cbar_toeplitz_kernel<KAPPA, KR, 3, true>);
+    } else {
+        if (f.nd == 1) run(cbar_toeplitz_kernel<KAPPA, KR, 1, false>);
+        else if (f.nd == 2) run(cbar_toeplitz_kernel<KAPPA, KR, 2, false>);
+        else if (f.nd == 3) run(cbar_toeplitz_kernel<KAPPA, KR, 3, false>);
+    }
     cudaFreeAsync(ftab, st);
     return GDT_OK;
 }
@@ -233,17 +258,18 @@ static int launch_kappa(const double *mu, const double *nu, const double *mu_c, 
 int cbar_fast_toeplitz(const double *mu, const double *nu, const double *mu_c,
                        const double *nu_c, const double *Ccentre, const double *table,
                        int64_t max_sq, double *out, uint8_t *unused, int64_t batch, const Grid &f,
-                       const Grid &c, int kappa, cudaStream_t st) {
+                       const Grid &c, int kappa, double p, cudaStream_t st) {
+    const bool p1 = p == 1.0;
     if (table == nullptr || f.n[0] % CF_R != 0 || f.n[0] / CF_R > CF_THREADS)
         return GDT_ERR_UNSUPPORTED;
     if (ipow(kappa, f.nd) > 64 || f.nd > 3) return GDT_ERR_UNSUPPORTED;  // fp32 bound: 64 ulp
     switch (kappa) {
         case 2: return launch_kappa<2, 8>(mu, nu, mu_c, nu_c, Ccentre, table, max_sq, out, unused,
-                                          batch, f, c, st);
+                                          batch, f, c, p1, st);
         case 4: return launch_kappa<4, 4>(mu, nu, mu_c, nu_c, Ccentre, table, max_sq, out, unused,
-                                          batch, f, c, st);
+                                          batch, f, c, p1, st);
         case 8: return launch_kappa<8, 2>(mu, nu, mu_c, nu_c, Ccentre, table, max_sq, out, unused,
-                                          batch, f, c, st);
+                                          batch, f, c, p1, st);
         default: return GDT_ERR_UNSUPPORTED;
     }
 }

@@ -164,22 +164,26 @@ __global__ void interpolate_kernel(const double *__restrict__ coarse, double *__
 // ---------------------------------------------------------------------------
 // K7 coarse c-transform over the coarse target support (quantized.py:504-505)
 // ---------------------------------------------------------------------------
-__global__ void coarse_ct_kernel(const double *__restrict__ g, const int32_t *__restrict__ dst,
-                                 const int32_t *__restrict__ supp_len,
-                                 const double *__restrict__ C, int64_t n, int64_t batch,
-                                 double *__restrict__ f_ext) {
-    const int64_t total = batch * n;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = idx / n, k = idx - b * n;
-        const int len = supp_len[b];
-        const double *gb = g + b * n;
-        const int32_t *db = dst + b * n;
-        const double *Ck = C + k * n;
-        double best = INFINITY;
-        for (int l = 0; l < len; ++l) best = fmin(best, __dsub_rn(Ck[db[l]], gb[l]));
-        f_ext[idx] = best;
-    }
+// one warp per (pair, k): lanes stride over the target support (coalesced
+// reads of the C-tilde row), exact min reduced across the warp
+__global__ void __launch_bounds__(256) coarse_ct_kernel(const double *__restrict__ g,
+                                                        const int32_t *__restrict__ dst,
+                                                        const int32_t *__restrict__ supp_len,
+                                                        const double *__restrict__ C, int64_t n,
+                                                        int64_t batch, double *__restrict__ f_ext) {
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= batch * n) return;
+    const int64_t b = w / n, k = w - b * n;
+    const int len = supp_len[b];
+    const double *gb = g + b * n;
+    const int32_t *db = dst + b * n;
+    const double *Ck = C + k * n;
+    double best = INFINITY;
+    for (int l = lane; l < len; l += 32) best = fmin(best, __dsub_rn(Ck[db[l]], gb[l]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) f_ext[w] = best;
 }
 
 // ---------------------------------------------------------------------------
@@ -284,7 +288,7 @@ int gdt_coarse_ctransform(const double *g, const int32_t *dst, const int32_t *su
                           void *stream) {
     GDT_CHECK_ARG(n >= 1 && batch >= 0, "gdt_coarse_ctransform: bad sizes");
     if (batch == 0) return GDT_OK;
-    coarse_ct_kernel<<<grid_size(batch * n, 128), 128, 0, as_stream(stream)>>>(
+    coarse_ct_kernel<<<grid_size(batch * n * 32, 256), 256, 0, as_stream(stream)>>>(
         g, dst, supp_len, centre_cost, n, batch, f_ext);
     return cuda_status("gdt_coarse_ctransform");
 }

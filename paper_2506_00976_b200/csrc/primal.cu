@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(MT) price_kernel(
                     }
                     const double coef = UNIFORM ? am : __dmul_rn(mass, W[t * m + s]);
                     const double fitted = __dmul_rn(__dmul_rn(ai, coef), bv[j]);
-                    acc += fitted * cost_from_sq(sq, p, table);
+                    acc += fitted * (p == 2.0 ? (double)sq : __ldg(table + sq));
                 });
             }
         }

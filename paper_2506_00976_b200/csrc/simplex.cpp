@@ -10,10 +10,18 @@
 //   has one, lowest index on ties, Bland after 10(ns+nt) degenerate pivots
 //   (:151-191); leaving slot = min flow on the decreasing side, lowest flat arc
 //   index on ties (:193-244); exact subtree relabel (:284-330).
-// Differences are purely mechanical: pricing walks row segments instead of
-// dividing every arc index, and evaluates 4 reduced costs per AVX2 step
-// (min first, then the first index attaining it -- the same arc the scalar
-// strict-< scan picks).  Built with -ffp-contract=off.
+// Potentials depend only on the current tree (each is recomputed from its
+// parent along a tree edge), so any traversal order yields identical values.
+//
+// Mechanical speed-ups that keep every floating-point operation identical:
+//   * pricing evaluates min((C - u) - v) over a block with AVX-512/AVX2 and
+//     only then scans for the first arc attaining it (= the scalar strict-<
+//     scan's choice);
+//   * basis slots cache their arc cost (relabels touch only L1 data);
+//   * translation-invariant costs on a full coarse grid (C-tilde, C-min) are
+//     read from an offset table T[x_j - x_i] instead of an ns x nt matrix,
+//     in contiguous axis-0 runs (the same double values the matrix holds).
+// Built with -ffp-contract=off.
 #include <immintrin.h>
 
 #include <algorithm>
@@ -29,40 +37,147 @@
 
 namespace {
 
-struct Lists {
-    std::vector<int64_t> rhead, chead, rnext, rprev, cnext, cprev;
+bool cpu_has_avx2() {
+    static const bool has = __builtin_cpu_supports("avx2");
+    return has;
+}
+
+bool cpu_has_avx512() {
+    static const bool has = __builtin_cpu_supports("avx512f");
+    return has;
+}
+
+// ---- cost models --------------------------------------------------------
+
+struct DenseCost {
+    const double *C;
+    int64_t nt;
+    double at(int64_t i, int64_t j) const { return C[i * nt + j]; }
+    // visit costs of row i, columns [j0, j1), as contiguous runs fn(ptr, jstart, len)
+    template <class F>
+    void runs(int64_t i, int64_t j0, int64_t j1, F &&fn) const {
+        fn(C + i * nt + j0, j0, j1 - j0);
+    }
 };
 
+// cost(i, j) = T[sum_a (x_j,a - x_i,a + cd_a - 1) * tstride_a] on a full grid
+struct GridCost {
+    int nd;
+    int64_t cd[GDT_MAX_DIM], tstride[GDT_MAX_DIM];
+    const double *T;
+    void coords(int64_t id, int64_t *x) const {
+        for (int a = 0; a < nd; ++a) {
+            x[a] = id % cd[a];
+            id /= cd[a];
+        }
+    }
+    double at(int64_t i, int64_t j) const {
+        int64_t xi[GDT_MAX_DIM], xj[GDT_MAX_DIM];
+        coords(i, xi);
+        coords(j, xj);
+        int64_t off = 0;
+        for (int a = 0; a < nd; ++a) off += (xj[a] - xi[a] + cd[a] - 1) * tstride[a];
+        return T[off];
+    }
+    template <class F>
+    void runs(int64_t i, int64_t j0, int64_t j1, F &&fn) const {
+        int64_t xi[GDT_MAX_DIM], xj[GDT_MAX_DIM];
+        coords(i, xi);
+        coords(j0, xj);
+        int64_t j = j0;
+        while (j < j1) {
+            const int64_t len = std::min<int64_t>(cd[0] - xj[0], j1 - j);
+            int64_t off = 0;
+            for (int a = 0; a < nd; ++a) off += (xj[a] - xi[a] + cd[a] - 1) * tstride[a];
+            fn(T + off, j, len);
+            j += len;
+            // advance xj by len along the flat order (axis 0 fastest)
+            xj[0] += len;
+            for (int a = 0; a < nd - 1 && xj[a] >= cd[a]; ++a) {
+                xj[a] -= cd[a];
+                ++xj[a + 1];
+            }
+        }
+    }
+};
+
+// ---- vectorised reduced-cost minimum of one contiguous run --------------
+
+__attribute__((target("avx512f"))) double run_min_avx512(const double *cs, const double *vs,
+                                                          int64_t len, double ui, double m0) {
+    const __m512d uu = _mm512_set1_pd(ui);
+    __m512d m = _mm512_set1_pd(m0);
+    int64_t t = 0;
+    for (; t + 8 <= len; t += 8)
+        m = _mm512_min_pd(m, _mm512_sub_pd(_mm512_sub_pd(_mm512_loadu_pd(cs + t), uu),
+                                           _mm512_loadu_pd(vs + t)));
+    double mm = _mm512_reduce_min_pd(m);
+    for (; t < len; ++t) {
+        const double r = (cs[t] - ui) - vs[t];
+        mm = r < mm ? r : mm;
+    }
+    return mm;
+}
+
+__attribute__((target("avx2"))) double run_min_avx2(const double *cs, const double *vs,
+                                                    int64_t len, double ui, double m0) {
+    const __m256d uu = _mm256_set1_pd(ui);
+    __m256d m = _mm256_set1_pd(m0);
+    int64_t t = 0;
+    for (; t + 4 <= len; t += 4)
+        m = _mm256_min_pd(m, _mm256_sub_pd(_mm256_sub_pd(_mm256_loadu_pd(cs + t), uu),
+                                           _mm256_loadu_pd(vs + t)));
+    alignas(32) double s[4];
+    _mm256_store_pd(s, m);
+    double mm = std::min(std::min(s[0], s[1]), std::min(s[2], s[3]));
+    for (; t < len; ++t) {
+        const double r = (cs[t] - ui) - vs[t];
+        mm = r < mm ? r : mm;
+    }
+    return mm;
+}
+
+double run_min_scalar(const double *cs, const double *vs, int64_t len, double ui, double mm) {
+    for (int64_t t = 0; t < len; ++t) {
+        const double r = (cs[t] - ui) - vs[t];
+        mm = r < mm ? r : mm;
+    }
+    return mm;
+}
+
+// ---- the solver -----------------------------------------------------------
+
+template <class Cost>
 struct Solver {
-    const double *C;
+    Cost cost;
     int64_t ns, nt, nb;
     int64_t *bi, *bj;
     double *bf, *u, *v;
-    Lists L;
+    std::vector<int64_t> rhead, chead, rnext, rprev, cnext, cprev;
     std::vector<int64_t> par, pslot, dep, stk, pa_s, pb_s;
     std::vector<int8_t> sa_s, sb_s;
-    std::vector<double> ck;  // cost of the arc held by each basis slot (L1-resident)
-    bool avx2, avx512;
+    std::vector<double> ck;  // cost of the arc held by each basis slot
+    int simd;                // 2 = avx512, 1 = avx2, 0 = scalar
 
     void push(int64_t k) {
         const int64_t s = bi[k], t = bj[k];
-        L.rnext[k] = L.rhead[s];
-        L.rprev[k] = -1;
-        if (L.rhead[s] != -1) L.rprev[L.rhead[s]] = k;
-        L.rhead[s] = k;
-        L.cnext[k] = L.chead[t];
-        L.cprev[k] = -1;
-        if (L.chead[t] != -1) L.cprev[L.chead[t]] = k;
-        L.chead[t] = k;
+        rnext[k] = rhead[s];
+        rprev[k] = -1;
+        if (rhead[s] != -1) rprev[rhead[s]] = k;
+        rhead[s] = k;
+        cnext[k] = chead[t];
+        cprev[k] = -1;
+        if (chead[t] != -1) cprev[chead[t]] = k;
+        chead[t] = k;
     }
 
     void unlink(int64_t k) {
-        if (L.rprev[k] != -1) L.rnext[L.rprev[k]] = L.rnext[k];
-        else L.rhead[bi[k]] = L.rnext[k];
-        if (L.rnext[k] != -1) L.rprev[L.rnext[k]] = L.rprev[k];
-        if (L.cprev[k] != -1) L.cnext[L.cprev[k]] = L.cnext[k];
-        else L.chead[bj[k]] = L.cnext[k];
-        if (L.cnext[k] != -1) L.cprev[L.cnext[k]] = L.cprev[k];
+        if (rprev[k] != -1) rnext[rprev[k]] = rnext[k];
+        else rhead[bi[k]] = rnext[k];
+        if (rnext[k] != -1) rprev[rnext[k]] = rprev[k];
+        if (cprev[k] != -1) cnext[cprev[k]] = cnext[k];
+        else chead[bj[k]] = cnext[k];
+        if (cnext[k] != -1) cprev[cnext[k]] = cprev[k];
     }
 
     // DFS labelling below `root`; `subtree` skips the parent slot instead of
@@ -73,10 +188,11 @@ struct Solver {
         while (sp > 0) {
             const int64_t node = stk[--sp];
             if (node < ns) {
-                for (int64_t k = L.rhead[node]; k != -1; k = L.rnext[k]) {
+                const double un = u[node];
+                for (int64_t k = rhead[node]; k != -1; k = rnext[k]) {
                     const int64_t t = bj[k];
                     if (subtree ? k == pslot[node] : par[ns + t] != -2) continue;
-                    v[t] = ck[k] - u[node];
+                    v[t] = ck[k] - un;
                     par[ns + t] = node;
                     pslot[ns + t] = k;
                     dep[ns + t] = dep[node] + 1;
@@ -84,10 +200,11 @@ struct Solver {
                 }
             } else {
                 const int64_t t = node - ns;
-                for (int64_t k = L.chead[t]; k != -1; k = L.cnext[k]) {
+                const double vt = v[t];
+                for (int64_t k = chead[t]; k != -1; k = cnext[k]) {
                     const int64_t s = bi[k];
                     if (subtree ? k == pslot[node] : par[s] != -2) continue;
-                    u[s] = ck[k] - v[t];
+                    u[s] = ck[k] - vt;
                     par[s] = node;
                     pslot[s] = k;
                     dep[s] = dep[node] + 1;
@@ -97,85 +214,22 @@ struct Solver {
         }
     }
 
-    // min over arcs [a, hi) of (C - u_i) - v_j; returns the minimum and the
-    // first arc attaining it (or +inf, -1 for an empty range)
-    __attribute__((target("avx2"))) void seg_min_avx2(int64_t i, int64_t j0, int64_t j1,
-                                                      double &mval) const {
-        const double *crow = C + i * nt;
-        const __m256d ui = _mm256_set1_pd(u[i]);
-        __m256d m = _mm256_set1_pd(INFINITY);
-        int64_t j = j0;
-        for (; j + 4 <= j1; j += 4) {
-            __m256d r = _mm256_sub_pd(_mm256_sub_pd(_mm256_loadu_pd(crow + j), ui),
-                                      _mm256_loadu_pd(v + j));
-            m = _mm256_min_pd(m, r);
-        }
-        alignas(32) double t[4];
-        _mm256_store_pd(t, m);
-        double mm = std::min(std::min(t[0], t[1]), std::min(t[2], t[3]));
-        const double uu = u[i];
-        for (; j < j1; ++j) {
-            const double r = (crow[j] - uu) - v[j];
-            mm = r < mm ? r : mm;
-        }
-        mval = std::min(mval, mm);
+    double run_min(const double *cs, int64_t j, int64_t len, double ui, double m) const {
+        if (simd == 2) return run_min_avx512(cs, v + j, len, ui, m);
+        if (simd == 1) return run_min_avx2(cs, v + j, len, ui, m);
+        return run_min_scalar(cs, v + j, len, ui, m);
     }
 
-    __attribute__((target("avx512f"))) void seg_min_avx512(int64_t i, int64_t j0, int64_t j1,
-                                                           double &mval) const {
-        const double *crow = C + i * nt;
-        const __m512d ui = _mm512_set1_pd(u[i]);
-        __m512d m = _mm512_set1_pd(INFINITY);
-        int64_t j = j0;
-        for (; j + 8 <= j1; j += 8) {
-            __m512d r = _mm512_sub_pd(_mm512_sub_pd(_mm512_loadu_pd(crow + j), ui),
-                                      _mm512_loadu_pd(v + j));
-            m = _mm512_min_pd(m, r);
-        }
-        double mm = _mm512_reduce_min_pd(m);
-        const double uu = u[i];
-        for (; j < j1; ++j) {
-            const double r = (crow[j] - uu) - v[j];
-            mm = r < mm ? r : mm;
-        }
-        mval = std::min(mval, mm);
-    }
-
-    void seg_min_scalar(int64_t i, int64_t j0, int64_t j1, double &mval) const {
-        const double *crow = C + i * nt;
-        const double uu = u[i];
-        double mm = mval;
-        for (int64_t j = j0; j < j1; ++j) {
-            const double r = (crow[j] - uu) - v[j];
-            mm = r < mm ? r : mm;
-        }
-        mval = mm;
-    }
-
-    // scalar strict-< scan of arcs [a, hi), the reference's inner loop
-    void scan_first(int64_t a, int64_t hi, double &best, int64_t &enter) const {
-        int64_t i = a / nt, j = a - i * nt;
-        for (int64_t arc = a; arc < hi; ++arc) {
-            const double r = (C[arc] - u[i]) - v[j];
-            if (r < best) {
-                best = r;
-                enter = arc;
-            }
-            if (++j == nt) {
-                j = 0;
-                ++i;
-            }
-        }
-    }
-
+    // exact min of (C - u) - v over arcs [a, hi)
     double block_min(int64_t a, int64_t hi) const {
         double m = INFINITY;
         int64_t i = a / nt, j = a - i * nt;
         while (a < hi) {
             const int64_t j1 = std::min<int64_t>(nt, j + (hi - a));
-            if (avx512) seg_min_avx512(i, j, j1, m);
-            else if (avx2) seg_min_avx2(i, j, j1, m);
-            else seg_min_scalar(i, j, j1, m);
+            const double ui = u[i];
+            cost.runs(i, j, j1, [&](const double *cs, int64_t js, int64_t len) {
+                m = run_min(cs, js, len, ui, m);
+            });
             a += j1 - j;
             j = 0;
             ++i;
@@ -183,18 +237,59 @@ struct Solver {
         return m;
     }
 
+    // scalar strict-< scan of arcs [a, hi): the reference's inner loop
+    void scan_first(int64_t a, int64_t hi, double &best, int64_t &enter) const {
+        int64_t i = a / nt, j = a - i * nt;
+        while (a < hi) {
+            const int64_t j1 = std::min<int64_t>(nt, j + (hi - a));
+            const double ui = u[i];
+            const int64_t rowbase = i * nt;
+            cost.runs(i, j, j1, [&](const double *cs, int64_t js, int64_t len) {
+                for (int64_t t = 0; t < len; ++t) {
+                    const double r = (cs[t] - ui) - v[js + t];
+                    if (r < best) {
+                        best = r;
+                        enter = rowbase + js + t;
+                    }
+                }
+            });
+            a += j1 - j;
+            j = 0;
+            ++i;
+        }
+    }
+
+    // Bland: first arc (in index order) with reduced cost below -tol
+    int64_t first_below(double tol) const {
+        for (int64_t i = 0; i < ns; ++i) {
+            const double ui = u[i];
+            int64_t found = -1;
+            cost.runs(i, 0, nt, [&](const double *cs, int64_t js, int64_t len) {
+                if (found != -1) return;
+                for (int64_t t = 0; t < len; ++t)
+                    if ((cs[t] - ui) - v[js + t] < -tol) {
+                        found = js + t;
+                        return;
+                    }
+            });
+            if (found != -1) return i * nt + found;
+        }
+        return -1;
+    }
+
     // warm = true: (bi, bj, bf) already hold a feasible spanning-tree basis
     // for (sup, dem) -- e.g. the optimal basis of another cost matrix on the
     // same marginals -- and replace the northwest-corner start.
     int solve(const double *sup, const double *dem, int64_t block_size, int64_t max_pivots,
-              double tol, int64_t *pivots_out, bool warm = false) {
+              double tol, int64_t *pivots_out, bool warm) {
         nb = ns + nt - 1;
         const int64_t n_arcs = ns * nt, n_nodes = ns + nt;
-        if (block_size <= 0) block_size = std::max<int64_t>(64, (int64_t)std::sqrt((double)(ns * nt)) + 1);
+        if (block_size <= 0)
+            block_size = std::max<int64_t>(64, (int64_t)std::sqrt((double)(ns * nt)) + 1);
         if (max_pivots <= 0) max_pivots = 50 * (ns + nt) * (ns + nt);
         const int64_t degen_limit = 10 * (ns + nt);
         *pivots_out = 0;
-        if (!warm) {  // northwest corner
+        if (!warm) {  // northwest corner (_simplex.py:31-54)
             std::vector<double> rs(sup, sup + ns), rd(dem, dem + nt);
             int64_t r = 0, c = 0;
             for (int64_t k = 0; k < nb; ++k) {
@@ -211,13 +306,13 @@ struct Solver {
             }
         }
         ck.resize(nb);
-        for (int64_t k = 0; k < nb; ++k) ck[k] = C[bi[k] * nt + bj[k]];
-        L.rhead.assign(ns, -1);
-        L.chead.assign(nt, -1);
-        L.rnext.resize(nb);
-        L.rprev.resize(nb);
-        L.cnext.resize(nb);
-        L.cprev.resize(nb);
+        for (int64_t k = 0; k < nb; ++k) ck[k] = cost.at(bi[k], bj[k]);
+        rhead.assign(ns, -1);
+        chead.assign(nt, -1);
+        rnext.resize(nb);
+        rprev.resize(nb);
+        cnext.resize(nb);
+        cprev.resize(nb);
         for (int64_t k = 0; k < nb; ++k) push(k);
         par.assign(n_nodes, -2);
         pslot.assign(n_nodes, 0);
@@ -239,25 +334,14 @@ struct Solver {
         int status = GDT_LP_OPTIMAL;
         for (;;) {
             int64_t enter = -1;
-            if (degen_run >= degen_limit) {  // Bland: first arc below -tol
-                int64_t i = 0, j = 0;
-                for (int64_t arc = 0; arc < n_arcs; ++arc) {
-                    if ((C[arc] - u[i]) - v[j] < -tol) {
-                        enter = arc;
-                        break;
-                    }
-                    if (++j == nt) {
-                        j = 0;
-                        ++i;
-                    }
-                }
+            if (degen_run >= degen_limit) {
+                enter = first_below(tol);
             } else {
                 double best = -tol;
                 int64_t scanned = 0, a = next_arc;
                 while (scanned < n_arcs) {
                     const int64_t hi = std::min(a + block_size, n_arcs);
-                    const double m = block_min(a, hi);
-                    if (m < best) scan_first(a, hi, best, enter);
+                    if (block_min(a, hi) < best) scan_first(a, hi, best, enter);
                     scanned += hi - a;
                     a = hi >= n_arcs ? 0 : hi;
                     if (enter != -1) break;
@@ -271,6 +355,7 @@ struct Solver {
             }
             ++pivots;
 
+            // the cycle: tree paths from sink ej (side a) and source ei (side b)
             const int64_t ei = enter / nt, ej = enter - ei * nt;
             int64_t ca = 0, cb = 0, pa = ns + ej, pb = ei;
             while (dep[pa] > dep[pb]) {
@@ -291,6 +376,7 @@ struct Solver {
                 sb_s[cb++] = pb < ns ? -1 : 1;
                 pb = par[pb];
             }
+            // leaving slot: min flow on decreasing arcs, lowest arc index on ties
             double theta = INFINITY;
             int64_t leave = -1, leave_arc = INT64_MAX;
             bool on_a = true;
@@ -326,9 +412,11 @@ struct Solver {
             bi[leave] = ei;
             bj[leave] = ej;
             bf[leave] = theta;
-            ck[leave] = C[enter];
+            ck[leave] = cost.at(ei, ej);
             push(leave);
 
+            // the detached subtree hangs off the entering arc at the endpoint
+            // whose old root path crossed the leaving arc
             int64_t q_root, p_root;
             if (on_a) {
                 q_root = ns + ej;
@@ -340,8 +428,8 @@ struct Solver {
             par[q_root] = p_root;
             pslot[q_root] = leave;
             dep[q_root] = dep[p_root] + 1;
-            if (q_root < ns) u[q_root] = C[q_root * nt + (p_root - ns)] - v[p_root - ns];
-            else v[q_root - ns] = C[p_root * nt + (q_root - ns)] - u[p_root];
+            if (q_root < ns) u[q_root] = ck[leave] - v[p_root - ns];
+            else v[q_root - ns] = ck[leave] - u[p_root];
             label(q_root, true);
         }
         *pivots_out = pivots;
@@ -349,23 +437,15 @@ struct Solver {
     }
 };
 
-bool cpu_has_avx2() {
-    static const bool has = __builtin_cpu_supports("avx2");
-    return has;
-}
+int simd_level() { return cpu_has_avx512() ? 2 : (cpu_has_avx2() ? 1 : 0); }
 
-bool cpu_has_avx512() {
-    static const bool has = __builtin_cpu_supports("avx512f");
-    return has;
-}
-
-int run_one(const double *C, const double *sup, const double *dem, int64_t ns, int64_t nt,
-            int64_t block_size, int64_t max_pivots, double tol, int64_t *bi, int64_t *bj,
-            double *bf, double *u, double *v, int64_t *pivots, bool warm = false) {
-    if (ns < 1 || nt < 1 || !C || !sup || !dem) return GDT_ERR_ARG;
+template <class Cost>
+int run_with(const Cost &cost, const double *sup, const double *dem, int64_t ns, int64_t nt,
+             int64_t block_size, int64_t max_pivots, double tol, int64_t *bi, int64_t *bj,
+             double *bf, double *u, double *v, int64_t *pivots, bool warm) {
     try {
-        Solver S;
-        S.C = C;
+        Solver<Cost> S;
+        S.cost = cost;
         S.ns = ns;
         S.nt = nt;
         S.bi = bi;
@@ -373,12 +453,19 @@ int run_one(const double *C, const double *sup, const double *dem, int64_t ns, i
         S.bf = bf;
         S.u = u;
         S.v = v;
-        S.avx2 = cpu_has_avx2();
-        S.avx512 = cpu_has_avx512();
+        S.simd = simd_level();
         return S.solve(sup, dem, block_size, max_pivots, tol, pivots, warm);
     } catch (...) {
         return GDT_ERR_NOMEM;
     }
+}
+
+int run_one(const double *C, const double *sup, const double *dem, int64_t ns, int64_t nt,
+            int64_t block_size, int64_t max_pivots, double tol, int64_t *bi, int64_t *bj,
+            double *bf, double *u, double *v, int64_t *pivots, bool warm = false) {
+    if (ns < 1 || nt < 1 || !C || !sup || !dem) return GDT_ERR_ARG;
+    return run_with(DenseCost{C, nt}, sup, dem, ns, nt, block_size, max_pivots, tol, bi, bj, bf,
+                    u, v, pivots, warm);
 }
 
 }  // namespace
@@ -390,15 +477,20 @@ extern "C" int gdt_transport_simplex(const double *C, const double *sup, const d
     return run_one(C, sup, dem, ns, nt, block_size, max_pivots, tol, bi, bj, bf, u, v, pivots);
 }
 
-// Pointer-array batch with optional warm starts.  Job q solves C[q] with
-// marginals sup[q]/dem[q]; warm_from[q] = -1 starts from the northwest corner
-// (the reference's pivot sequence), otherwise from the final basis of job
-// warm_from[q] (< q, same shape): jobs form chains that one worker runs in
-// order, chains are spread over `threads` workers.
-extern "C" int gdt_transport_simplex_many(int64_t count, const uint64_t *C, const uint64_t *sup,
-                                          const uint64_t *dem, const int64_t *ns,
-                                          const int64_t *nt, const int64_t *warm_from,
-                                          double tol, const uint64_t *bi, const uint64_t *bj,
+// Pointer-array batch with optional warm starts and offset-table costs.
+// Job q solves cost q with marginals sup[q]/dem[q].  C[q] != 0: dense
+// row-major cost.  C[q] == 0: translation-invariant cost on the full grid
+// grid_dims[q*GDT_MAX_DIM ..] (grid_ndim[q] axes, ns = nt = cells) read from
+// table[q] over offset vectors (extent 2*cd_a - 1 per axis, axis 0 fastest).
+// warm_from[q] = -1 starts from the northwest corner (the reference's pivot
+// sequence), otherwise from the final basis of job warm_from[q] (< q, same
+// shape): chained jobs run in order on one worker.
+extern "C" int gdt_transport_simplex_many(int64_t count, const uint64_t *C, const uint64_t *table,
+                                          const int32_t *grid_ndim, const int64_t *grid_dims,
+                                          const uint64_t *sup, const uint64_t *dem,
+                                          const int64_t *ns, const int64_t *nt,
+                                          const int64_t *warm_from, double tol,
+                                          const uint64_t *bi, const uint64_t *bj,
                                           const uint64_t *bf, const uint64_t *u,
                                           const uint64_t *v, int32_t *status, int64_t *pivots,
                                           int threads) {
@@ -413,31 +505,51 @@ extern "C" int gdt_transport_simplex_many(int64_t count, const uint64_t *C, cons
             if (w >= q || ns[w] != ns[q] || nt[w] != nt[q]) return GDT_ERR_ARG;
             kids[w].push_back(q);
         }
+        if (C[q] == 0) {
+            if (!table || table[q] == 0 || !grid_ndim || !grid_dims) return GDT_ERR_ARG;
+            const int nd = grid_ndim[q];
+            if (nd < 1 || nd > GDT_MAX_DIM) return GDT_ERR_ARG;
+            int64_t cells = 1;
+            for (int a = 0; a < nd; ++a) cells *= grid_dims[q * GDT_MAX_DIM + a];
+            if (cells != ns[q] || cells != nt[q]) return GDT_ERR_ARG;
+        }
     }
     if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
     threads = (int)std::min<int64_t>(threads, std::max<int64_t>((int64_t)roots.size(), 1));
     auto P = [](uint64_t a) { return reinterpret_cast<void *>(a); };
+    auto solve_job = [&](int64_t q, bool warm) {
+        int64_t *qbi = (int64_t *)P(bi[q]), *qbj = (int64_t *)P(bj[q]);
+        double *qbf = (double *)P(bf[q]), *qu = (double *)P(u[q]), *qv = (double *)P(v[q]);
+        const double *qs = (const double *)P(sup[q]), *qd = (const double *)P(dem[q]);
+        if (C[q] != 0)
+            return run_with(DenseCost{(const double *)P(C[q]), nt[q]}, qs, qd, ns[q], nt[q], 0, 0,
+                            tol, qbi, qbj, qbf, qu, qv, pivots + q, warm);
+        GridCost g;
+        g.nd = grid_ndim[q];
+        g.T = (const double *)P(table[q]);
+        int64_t ts = 1;
+        for (int a = 0; a < GDT_MAX_DIM; ++a) {
+            g.cd[a] = a < g.nd ? grid_dims[q * GDT_MAX_DIM + a] : 1;
+            g.tstride[a] = ts;
+            ts *= 2 * g.cd[a] - 1;
+        }
+        return run_with(g, qs, qd, ns[q], nt[q], 0, 0, tol, qbi, qbj, qbf, qu, qv, pivots + q, warm);
+    };
     std::function<void(int64_t)> run = [&](int64_t q) {
         const int64_t w = warm_from ? warm_from[q] : -1;
         const int64_t nbq = ns[q] + nt[q] - 1;
-        int64_t *qbi = (int64_t *)P(bi[q]), *qbj = (int64_t *)P(bj[q]);
-        double *qbf = (double *)P(bf[q]);
         if (w >= 0) {
             if (status[w] != GDT_LP_OPTIMAL) {
                 status[q] = status[w] < 0 ? status[w] : GDT_ERR_ARG;
                 pivots[q] = 0;
             } else {
-                std::memcpy(qbi, P(bi[w]), sizeof(int64_t) * nbq);
-                std::memcpy(qbj, P(bj[w]), sizeof(int64_t) * nbq);
-                std::memcpy(qbf, P(bf[w]), sizeof(double) * nbq);
-                status[q] = run_one((const double *)P(C[q]), (const double *)P(sup[q]),
-                                    (const double *)P(dem[q]), ns[q], nt[q], 0, 0, tol, qbi, qbj,
-                                    qbf, (double *)P(u[q]), (double *)P(v[q]), pivots + q, true);
+                std::memcpy(P(bi[q]), P(bi[w]), sizeof(int64_t) * nbq);
+                std::memcpy(P(bj[q]), P(bj[w]), sizeof(int64_t) * nbq);
+                std::memcpy(P(bf[q]), P(bf[w]), sizeof(double) * nbq);
+                status[q] = solve_job(q, true);
             }
         } else {
-            status[q] = run_one((const double *)P(C[q]), (const double *)P(sup[q]),
-                                (const double *)P(dem[q]), ns[q], nt[q], 0, 0, tol, qbi, qbj, qbf,
-                                (double *)P(u[q]), (double *)P(v[q]), pivots + q, false);
+            status[q] = solve_job(q, false);
         }
         for (int64_t k : kids[q]) run(k);
     };

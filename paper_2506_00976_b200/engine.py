@@ -26,9 +26,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from .costs import (centre_cost_cached, cost_table, max_sq_of, min_cost_cached,
-                    weighted_cost_batch)
-from .device import device, stream, to_dev, to_host, torch
+from .costs import (centre_cost_cached, centre_cost_table, cost_table, max_sq_of,
+                    min_cost_table, weighted_cost_batch)
+from .device import device, stream, to_dev, to_host, to_host_pinned, torch
 from .errors import DimensionMismatchError, GridotError, NumericOverflowError, \
     ZeroDenominatorError
 from .exact import build_transport_problem, solve_transport_many
@@ -117,16 +117,19 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
     cbar_host = None
     if need_cbar:
         vals, _ = _cbar(bt)
-        cbar_host = to_host(vals)
+        cbar_host = to_host_pinned(vals, "cbar")
     mu_c = to_host(bt.mu_c)
     nu_c = to_host(bt.nu_c)
     plans = CoarsePlans(n=bt.n)
     t0 = time.perf_counter()
     problems, slots, warm = [], [], []
-    cmin = min_cost_cached(bt.pdims, bt.kappa, bt.p) if need_cmin else None
+    # C-tilde and C-min are translation-invariant: the host LP reads offset
+    # tables instead of n x n matrices (dense copies only for partial supports)
+    cmin = min_cost_table(bt.pdims, bt.kappa, bt.p) if need_cmin else None
+    ctil = centre_cost_table(bt.pdims, bt.kappa, bt.p) if need_ctil else None
     for b in range(bt.B):
         root = -1
-        for kind, cost in (("ctil", bt.ctil if need_ctil else None),
+        for kind, cost in (("ctil", ctil),
                            ("cbar", cbar_host[b] if need_cbar else None),
                            ("cmin", cmin)):
             if cost is None:
@@ -384,6 +387,8 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
     t0 = time.perf_counter()
     plans = prepare_coarse(bt, methods, lp_threads)
     t1 = time.perf_counter()
+    if timings is not None:
+        timings["lp"] = plans.lp_seconds
     dp = DevicePlans(bt, plans, paired, xi)
     res = gpu_stages(bt, dp, methods, max_iter, dual_method)
     prim = None
@@ -394,6 +399,7 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
     t2 = time.perf_counter()
     if timings is not None:
         timings.update(prepare=t0 - t_start, coarse=t1 - t0, gpu=t2 - t1)
+        timings["finish"] = time.perf_counter() - t2
     wall = (t2 - t_start) / max(bt.B, 1)
     reports = []
     for b in range(bt.B):

@@ -20,7 +20,7 @@ from . import _native as N
 from .errors import GridotError, IterationLimitError, UnbalancedError
 
 __all__ = ["TransportProblem", "SparseCoupling", "DualPotentials", "build_transport_problem",
-           "solve_transport", "solve_transport_many", "REBALANCE_TOLERANCE"]
+           "solve_transport", "solve_transport_many", "OffsetTableCost", "REBALANCE_TOLERANCE"]
 
 logger = logging.getLogger(__name__)
 
@@ -76,6 +76,39 @@ class DualPotentials:
     feasibility_slack: float
 
 
+class OffsetTableCost:
+    """Translation-invariant cost on a full coarse grid, never materialised.
+
+    cost(i, j) = table[x_j - x_i + (cd - 1)] for coarse cells i, j of the grid
+    ``cdims`` (flat order axis 0 fastest); ``table`` is the Fortran-flattened
+    array over offset vectors with extent 2*cd_a - 1 per axis.  The host
+    simplex reads it directly (``gdt_transport_simplex_many``); indexing with
+    (rows, cols) arrays returns the same doubles the dense matrix holds.
+    """
+
+    def __init__(self, table: np.ndarray, cdims: tuple):
+        self.table = np.ascontiguousarray(table, dtype=np.float64).ravel(order="F")
+        self.cdims = tuple(int(x) for x in cdims)
+        n = int(np.prod(self.cdims))
+        self.shape = (n, n)
+        self.ext = tuple(2 * c - 1 for c in self.cdims)
+
+    def _index(self, rows, cols):
+        xi = np.unravel_index(np.asarray(rows), self.cdims, order="F")
+        xj = np.unravel_index(np.asarray(cols), self.cdims, order="F")
+        off = tuple(b - a + (c - 1) for a, b, c in zip(xi, xj, self.cdims))
+        return np.ravel_multi_index(off, self.ext, order="F")
+
+    def __getitem__(self, key):
+        rows, cols = key
+        return self.table[self._index(rows, cols)]
+
+    def dense(self) -> np.ndarray:
+        n = self.shape[0]
+        ids = np.arange(n)
+        return self[ids[:, None], ids[None, :]]
+
+
 def _rebalance(s: np.ndarray, t: np.ndarray) -> None:
     drift = float(s.sum() - t.sum())
     if drift == 0.0:
@@ -99,8 +132,13 @@ def build_transport_problem(supply, demand, cost) -> TransportProblem:
         raise GridotError("transport needs nonempty supports on both sides")
     s, t = supply[si].copy(), demand[di].copy()
     _rebalance(s, t)
+    full = si.size == cost.shape[0] and di.size == cost.shape[1]
+    if isinstance(cost, OffsetTableCost):
+        if full:
+            return TransportProblem(s, t, cost, si, di)
+        cost = cost.dense()
     cost = np.asarray(cost)
-    if si.size == cost.shape[0] and di.size == cost.shape[1]:
+    if full:
         sub = np.ascontiguousarray(cost, dtype=np.float64)  # full supports: no gather copy
     else:
         sub = np.ascontiguousarray(cost[np.ix_(si, di)], dtype=np.float64)
@@ -115,7 +153,11 @@ def _finish(problem: TransportProblem, status: int, bi, bj, bf, u, v, pivots, sl
     keep = bf > 0.0
     coupling = SparseCoupling(bi[keep].copy(), bj[keep].copy(), bf[keep].copy(), problem.shape)
     value = float(np.sum(bf * problem.cost[bi, bj]))
-    slack = float(np.min(problem.cost - u[:, None] - v[None, :])) if slack else float("nan")
+    if slack:
+        dense = problem.cost.dense() if isinstance(problem.cost, OffsetTableCost) else problem.cost
+        slack = float(np.min(dense - u[:, None] - v[None, :]))
+    else:
+        slack = float("nan")
     logger.debug("simplex %dx%d: %d pivots, value %.12g, slack %.3g", problem.shape[0],
                  problem.shape[1], pivots, value, slack)
     return coupling, DualPotentials(u, v, slack), value
@@ -124,6 +166,11 @@ def _finish(problem: TransportProblem, status: int, bi, bj, bf, u, v, pivots, sl
 def solve_transport(problem: TransportProblem, tol: float = 1e-10,
                     max_pivots: int | None = None):
     """Optimal coupling, duals and value (exact.py:156-189) via the native simplex."""
+    if isinstance(problem.cost, OffsetTableCost):
+        return solve_transport_many([problem], tol=tol, threads=1)[0] if max_pivots is None \
+            else solve_transport(TransportProblem(problem.supply, problem.demand,
+                                                  problem.cost.dense(), problem.src_index,
+                                                  problem.dst_index), tol, max_pivots)
     ns, nt = problem.shape
     nb = ns + nt - 1
     bi, bj = np.empty(nb, np.int64), np.empty(nb, np.int64)
@@ -162,11 +209,20 @@ def solve_transport_many(problems, tol: float = 1e-10, threads: int = 0, warm_fr
 
     ns = np.array([p.shape[0] for p in problems], np.int64)
     nt = np.array([p.shape[1] for p in problems], np.int64)
-    costs = [np.ascontiguousarray(p.cost, dtype=np.float64) for p in problems]
     out = [(np.empty(a + b - 1, np.int64), np.empty(a + b - 1, np.int64), np.empty(a + b - 1),
             np.empty(a), np.empty(b)) for a, b in zip(ns, nt)]
     ptr = lambda xs: np.array([addr(x) for x in xs], np.uint64)  # noqa: E731
-    C = ptr(costs)
+    C = np.zeros(count, np.uint64)
+    T = np.zeros(count, np.uint64)
+    gnd = np.zeros(count, np.int32)
+    gdims = np.ones((count, 4), np.int64)
+    for q, prob in enumerate(problems):
+        if isinstance(prob.cost, OffsetTableCost):
+            T[q] = addr(prob.cost.table)
+            gnd[q] = len(prob.cost.cdims)
+            gdims[q, :gnd[q]] = prob.cost.cdims
+        else:
+            C[q] = addr(np.ascontiguousarray(prob.cost, dtype=np.float64))
     sup = ptr([np.ascontiguousarray(p.supply) for p in problems])
     dem = ptr([np.ascontiguousarray(p.demand) for p in problems])
     bi, bj, bf, u, v = (ptr([o[i] for o in out]) for i in range(5))
@@ -174,7 +230,8 @@ def solve_transport_many(problems, tol: float = 1e-10, threads: int = 0, warm_fr
     status = np.empty(count, np.int32)
     pivots = np.empty(count, np.int64)
     N.check(N.lib().gdt_transport_simplex_many(
-        count, N.ptr(C), N.ptr(sup), N.ptr(dem), N.ptr(ns), N.ptr(nt), N.ptr(wf), float(tol),
+        count, N.ptr(C), N.ptr(T), N.ptr(gnd), N.ptr(gdims), N.ptr(sup), N.ptr(dem), N.ptr(ns),
+        N.ptr(nt), N.ptr(wf), float(tol),
         N.ptr(bi), N.ptr(bj), N.ptr(bf), N.ptr(u), N.ptr(v), N.ptr(status), N.ptr(pivots),
         int(threads)), "gdt_transport_simplex_many")
     res = []
