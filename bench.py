@@ -303,10 +303,10 @@ def run_b200(args):
     n_c = Nf // dk ** len(dims)
     if dname in ("ct_target", "ct_source") and dpow != 2.0:
         flops = 2.0 * Nf * Nf * ppr            # sub + min per candidate
-        rl = {"bound": "fp32", "kernel": f"brute_f32_kernel (c-transform, kappa={dk}, p={dpow:g})"}
+        rl = {"bound": "fp32", "kernel": f"pruned_ct_kernel (c-transform, kappa={dk}, p={dpow:g})"}
     elif dname == "cbar" and dpow != 2.0:
         flops = 2.0 * Nf * Nf * ppr            # one FMA per (row cell, column cell)
-        rl = {"bound": "fp32", "kernel": f"cbar_tile_kernel<fast> (kappa={dk}, p={dpow:g})"}
+        rl = {"bound": "fp32", "kernel": f"cbar_toeplitz_kernel (fp32 C-bar, kappa={dk}, p={dpow:g})"}
     else:
         flops = None
         rl = {"bound": "hbm", "kernel": dname}

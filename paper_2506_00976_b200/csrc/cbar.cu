@@ -190,40 +190,78 @@ __global__ void moments_kernel(const double *__restrict__ fine, double *__restri
     }
 }
 
+// grid: x = chunk of 4*256 columns l, y = row block k, z = pair; each thread
+// writes 4 consecutive l (coordinates advanced incrementally, no divisions in
+// the loop)
 __global__ void __launch_bounds__(256) cbar_moments_kernel(
     const double *__restrict__ mu_c, const double *__restrict__ nu_c, const double *__restrict__ mm,
     const double *__restrict__ nm, const double *__restrict__ Ccentre, double *__restrict__ out,
     uint8_t *__restrict__ unused, Grid c, int kappa) {
-    // grid: x = l chunk, y = k, z = pair
     const int n = (int)c.cells, nd = c.nd, W = nd + 1;
     const int k = blockIdx.y;
     const int64_t b = blockIdx.z;
-    const int l = blockIdx.x * 256 + threadIdx.x;
-    if (l >= n) return;
-    const double M0 = mu_c[b * n + k], N0 = nu_c[b * n + l];
-    const double denom = __dmul_rn(M0, N0);
-    const int64_t oi = ((int64_t)b * n + k) * n + l;
-    if (denom == 0.0) {
-        out[oi] = Ccentre[(int64_t)k * n + l];
-        unused[oi] = 1;
-        return;
+    const int l0 = (blockIdx.x * 256 + threadIdx.x) * 4;
+    if (l0 >= n) return;
+    const double M0 = mu_c[b * n + k];
+    const double *Mk = mm + ((int64_t)b * n + k) * W;
+    int kc[GDT_MAX_DIM], lc[GDT_MAX_DIM];
+    {
+        int kk = k, ll = l0;
+        for (int a = nd - 1; a >= 0; --a) {
+            const int st = (int)c.stride[a];
+            kc[a] = kk / st;
+            kk -= kc[a] * st;
+            lc[a] = ll / st;
+            ll -= lc[a] * st;
+        }
     }
-    const double *Mk = mm + ((int64_t)b * n + k) * W, *Nl = nm + ((int64_t)b * n + l) * W;
-    double d2 = 0.0, cross = 0.0, m1n1 = 0.0;
-    int kk = k, ll = l;
-    for (int a = nd - 1; a >= 0; --a) {
-        const int st = (int)c.stride[a];
-        const int ka = kk / st, la = ll / st;
-        kk -= ka * st;
-        ll -= la * st;
-        const double D = (double)(kappa * (ka - la));
-        d2 = fma(D, D, d2);
-        cross = fma(D, Mk[a] * N0 - M0 * Nl[a], cross);
-        m1n1 = fma(Mk[a], Nl[a], m1n1);
+    const int64_t orow = ((int64_t)b * n + k) * n;
+    double vals[4];
+    uint8_t un[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int l = l0 + q;
+        double v = 0.0;
+        uint8_t u = 1;
+        if (l < n) {
+            const double N0 = nu_c[b * n + l];
+            const double denom = __dmul_rn(M0, N0);
+            if (denom == 0.0) {
+                v = Ccentre[(int64_t)k * n + l];
+            } else {
+                const double *Nl = nm + ((int64_t)b * n + l) * W;
+                double d2 = 0.0, cross = 0.0, m1n1 = 0.0;
+                for (int a = 0; a < nd; ++a) {
+                    const double D = (double)(kappa * (kc[a] - lc[a]));
+                    d2 = fma(D, D, d2);
+                    cross = fma(D, Mk[a] * N0 - M0 * Nl[a], cross);
+                    m1n1 = fma(Mk[a], Nl[a], m1n1);
+                }
+                const double numer =
+                    denom * d2 + 2.0 * cross + Mk[nd] * N0 + M0 * Nl[nd] - 2.0 * m1n1;
+                v = numer / denom;
+                u = 0;
+            }
+        }
+        vals[q] = v;
+        un[q] = u;
+        // advance l's coordinates by one (axis 0 fastest)
+        ++lc[0];
+        for (int a = 0; a < nd - 1 && lc[a] >= (int)c.n[a]; ++a) {
+            lc[a] = 0;
+            ++lc[a + 1];
+        }
     }
-    const double numer = denom * d2 + 2.0 * cross + Mk[nd] * N0 + M0 * Nl[nd] - 2.0 * m1n1;
-    out[oi] = numer / denom;
-    unused[oi] = 0;
+    if (l0 + 3 < n && (n & 3) == 0) {
+        reinterpret_cast<double2 *>(out + orow + l0)[0] = make_double2(vals[0], vals[1]);
+        reinterpret_cast<double2 *>(out + orow + l0)[1] = make_double2(vals[2], vals[3]);
+        *reinterpret_cast<uchar4 *>(unused + orow + l0) = make_uchar4(un[0], un[1], un[2], un[3]);
+    } else {
+        for (int q = 0; q < 4 && l0 + q < n; ++q) {
+            out[orow + l0 + q] = vals[q];
+            unused[orow + l0 + q] = un[q];
+        }
+    }
 }
 
 }  // namespace gdt
@@ -256,7 +294,7 @@ extern "C" int gdt_weighted_cost(const double *mu, const double *nu, const doubl
         moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(mu, mom, batch, f, c, kappa);
         moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(nu, mom + batch * n * W, batch,
                                                                    f, c, kappa);
-        dim3 mg((unsigned)((n + 255) / 256), (unsigned)n, (unsigned)batch);
+        dim3 mg((unsigned)((n + 1023) / 1024), (unsigned)n, (unsigned)batch);
         cbar_moments_kernel<<<mg, 256, 0, st>>>(mu_c, nu_c, mom, mom + batch * n * W, centre_cost,
                                                  out, unused, c, kappa);
         cudaFreeAsync(mom, st);

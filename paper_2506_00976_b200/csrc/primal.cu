@@ -35,7 +35,7 @@
 
 namespace gdt {
 
-constexpr int PT = 512;  // threads of the per-pair IPF CTA
+constexpr int PT = 1024;  // threads of the per-pair IPF CTA
 
 struct G32 {  // int32 grid description (cells < 2^31)
     int nd;
@@ -84,17 +84,16 @@ __device__ __forceinline__ void for_block_cells(int origin, const G32 &f, int ka
 }
 
 // Visit the cells of the union of coarse blocks ids[lo..hi) (sorted
-// ascending) in ascending fine flat order: fn(q, cell, s) with q the arc index,
-// cell the fine flat id and s the within-block offset (Fortran-flattened).
+// ascending) in ascending fine flat order, as runs of kappa consecutive cells
+// along axis 0: fn(q, cell, s) with q the arc index, cell the fine flat id of
+// the run's first cell and s its within-block offset (Fortran-flattened).
 template <int LEVEL, class F>
 __device__ __forceinline__ void walk(const int32_t *ids, int lo, int hi, const G32 &c,
                                      const G32 &f, int kappa, int fbase, int sbase, int kpow,
                                      F &fn) {
     if constexpr (LEVEL == 0) {
-        for (int q = lo; q < hi; ++q) {
-            const int cell = fbase + (ids[q] % c.n[0]) * kappa;
-            for (int s0 = 0; s0 < kappa; ++s0) fn(q, cell + s0, sbase + s0);
-        }
+        // one run of kappa consecutive cells per arc: fn(q, first_cell, first_s)
+        for (int q = lo; q < hi; ++q) fn(q, fbase + (ids[q] % c.n[0]) * kappa, sbase);
     } else {
         int r = lo;
         while (r < hi) {
@@ -187,6 +186,26 @@ __device__ void block_reduce_red(Red &r, double *sh) {
     __syncthreads();
 }
 
+// acc += (mass * w_i) * x_i sequentially over a run of `len` cells; the loads
+// are issued first (they do not depend on acc), then the exact-order adds.
+// Non-uniform kernels read w_i = wrow[i * wstride].
+template <bool UNIFORM>
+__device__ __forceinline__ void accumulate_run(double &acc, double mass, double Wu,
+                                               const double *wrow, int wstride,
+                                               const double *x, int len) {
+    for (int o = 0; o < len; o += 4) {
+        double xv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xv[i] = o + i < len ? x[o + i] : 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (o + i >= len) break;
+            const double coef = __dmul_rn(mass, UNIFORM ? Wu : wrow[(o + i) * wstride]);
+            acc = __dadd_rn(acc, __dmul_rn(coef, xv[i]));
+        }
+    }
+}
+
 // Phase R for one row unit (block k, or fine row (k, t) for non-uniform W).
 template <bool UNIFORM>
 __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c, const G32 &f,
@@ -199,8 +218,7 @@ __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c,
     const double *ms = P.rmass + lo;
     double acc = 0.0;
     auto fn = [&](int q, int cell, int s) {
-        const double coef = __dmul_rn(ms[q], UNIFORM ? Wu : W[t * m + s]);
-        acc = __dadd_rn(acc, __dmul_rn(coef, P.b[cell]));
+        accumulate_run<UNIFORM>(acc, ms[q], Wu, W + t * m + s, 1, P.b + cell, kappa);
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kb[u] = acc;
@@ -233,8 +251,7 @@ __device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c,
     const double *ms = P.cmass + lo;
     double acc = 0.0;
     auto fn = [&](int q, int cell, int t) {
-        const double coef = __dmul_rn(ms[q], UNIFORM ? Wu : W[t * m + s]);
-        acc = __dadd_rn(acc, __dmul_rn(coef, a_cur[cell]));
+        accumulate_run<UNIFORM>(acc, ms[q], Wu, W + t * m + s, m, a_cur + cell, kappa);
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kta[u] = acc;
