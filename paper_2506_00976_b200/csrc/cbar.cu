@@ -19,6 +19,10 @@
 
 namespace gdt {
 
+int cbar_fast_diag(const double *mu, const double *nu, const double *mu_c, const double *nu_c,
+                   const double *Ccentre, const double *table, int64_t max_sq, double *out,
+                   uint8_t *unused, int64_t batch, const Grid &f, const Grid &c, int kappa, double p,
+                   cudaStream_t st);
 int cbar_fast_toeplitz(const double *mu, const double *nu, const double *mu_c,
                        const double *nu_c, const double *Ccentre, const double *table,
                        int64_t max_sq, double *out, uint8_t *unused, int64_t batch, const Grid &f,
@@ -190,76 +194,100 @@ __global__ void moments_kernel(const double *__restrict__ fine, double *__restri
     }
 }
 
-// grid: x = chunk of 4*256 columns l, y = row block k, z = pair; each thread
-// writes 4 consecutive l (coordinates advanced incrementally, no divisions in
-// the loop)
+// grid: x = chunk of 4*256 columns l, y = group of MB_K row blocks k, z =
+// pair.  A thread keeps the moments of its 4 consecutive columns in registers
+// and sweeps the MB_K rows, whose moments sit in shared memory; the quotient
+// uses reciprocals (fp32 mode: any order / rounding within ~1e-15).
+constexpr int MB_K = 8;
+
 __global__ void __launch_bounds__(256) cbar_moments_kernel(
     const double *__restrict__ mu_c, const double *__restrict__ nu_c, const double *__restrict__ mm,
     const double *__restrict__ nm, const double *__restrict__ Ccentre, double *__restrict__ out,
     uint8_t *__restrict__ unused, Grid c, int kappa) {
+    __shared__ double sk[MB_K][GDT_MAX_DIM + 3];  // M0, 1/M0, M1[d], M2
+    __shared__ int skc[MB_K][GDT_MAX_DIM];
     const int n = (int)c.cells, nd = c.nd, W = nd + 1;
-    const int k = blockIdx.y;
+    const int k0 = blockIdx.y * MB_K;
     const int64_t b = blockIdx.z;
-    const int l0 = (blockIdx.x * 256 + threadIdx.x) * 4;
-    if (l0 >= n) return;
-    const double M0 = mu_c[b * n + k];
-    const double *Mk = mm + ((int64_t)b * n + k) * W;
-    int kc[GDT_MAX_DIM], lc[GDT_MAX_DIM];
-    {
-        int kk = k, ll = l0;
-        for (int a = nd - 1; a >= 0; --a) {
-            const int st = (int)c.stride[a];
-            kc[a] = kk / st;
-            kk -= kc[a] * st;
-            lc[a] = ll / st;
-            ll -= lc[a] * st;
-        }
-    }
-    const int64_t orow = ((int64_t)b * n + k) * n;
-    double vals[4];
-    uint8_t un[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int l = l0 + q;
-        double v = 0.0;
-        uint8_t u = 1;
-        if (l < n) {
-            const double N0 = nu_c[b * n + l];
-            const double denom = __dmul_rn(M0, N0);
-            if (denom == 0.0) {
-                v = Ccentre[(int64_t)k * n + l];
-            } else {
-                const double *Nl = nm + ((int64_t)b * n + l) * W;
-                double d2 = 0.0, cross = 0.0, m1n1 = 0.0;
-                for (int a = 0; a < nd; ++a) {
-                    const double D = (double)(kappa * (kc[a] - lc[a]));
-                    d2 = fma(D, D, d2);
-                    cross = fma(D, Mk[a] * N0 - M0 * Nl[a], cross);
-                    m1n1 = fma(Mk[a], Nl[a], m1n1);
-                }
-                const double numer =
-                    denom * d2 + 2.0 * cross + Mk[nd] * N0 + M0 * Nl[nd] - 2.0 * m1n1;
-                v = numer / denom;
-                u = 0;
+    if (threadIdx.x < MB_K) {
+        const int k = k0 + threadIdx.x;
+        if (k < n) {
+            const double M0 = mu_c[b * n + k];
+            const double *Mk = mm + ((int64_t)b * n + k) * W;
+            sk[threadIdx.x][0] = M0;
+            sk[threadIdx.x][1] = M0 > 0.0 ? 1.0 / M0 : 0.0;
+            for (int a = 0; a <= nd; ++a) sk[threadIdx.x][2 + a] = Mk[a];
+            int kk = k;
+            for (int a = nd - 1; a >= 0; --a) {
+                skc[threadIdx.x][a] = kk / (int)c.stride[a];
+                kk -= skc[threadIdx.x][a] * (int)c.stride[a];
             }
         }
-        vals[q] = v;
-        un[q] = u;
-        // advance l's coordinates by one (axis 0 fastest)
-        ++lc[0];
-        for (int a = 0; a < nd - 1 && lc[a] >= (int)c.n[a]; ++a) {
-            lc[a] = 0;
-            ++lc[a + 1];
+    }
+    __syncthreads();
+    const int l0 = (blockIdx.x * 256 + threadIdx.x) * 4;
+    if (l0 >= n) return;
+    double N0[4], iN[4], Nm[4][GDT_MAX_DIM + 1];
+    int lc[4][GDT_MAX_DIM];
+    {
+        int cc[GDT_MAX_DIM];
+        int ll = l0;
+        for (int a = nd - 1; a >= 0; --a) {
+            cc[a] = ll / (int)c.stride[a];
+            ll -= cc[a] * (int)c.stride[a];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int l = l0 + q < n ? l0 + q : n - 1;
+            N0[q] = nu_c[b * n + l];
+            iN[q] = N0[q] > 0.0 ? 1.0 / N0[q] : 0.0;
+            const double *Nl = nm + ((int64_t)b * n + l) * W;
+            for (int a = 0; a <= nd; ++a) Nm[q][a] = Nl[a];
+            for (int a = 0; a < nd; ++a) lc[q][a] = cc[a];
+            ++cc[0];
+            for (int a = 0; a < nd - 1 && cc[a] >= (int)c.n[a]; ++a) {
+                cc[a] = 0;
+                ++cc[a + 1];
+            }
         }
     }
-    if (l0 + 3 < n && (n & 3) == 0) {
-        reinterpret_cast<double2 *>(out + orow + l0)[0] = make_double2(vals[0], vals[1]);
-        reinterpret_cast<double2 *>(out + orow + l0)[1] = make_double2(vals[2], vals[3]);
-        *reinterpret_cast<uchar4 *>(unused + orow + l0) = make_uchar4(un[0], un[1], un[2], un[3]);
-    } else {
-        for (int q = 0; q < 4 && l0 + q < n; ++q) {
-            out[orow + l0 + q] = vals[q];
-            unused[orow + l0 + q] = un[q];
+    const bool vec = l0 + 3 < n && (n & 3) == 0;
+    for (int kk = 0; kk < MB_K; ++kk) {
+        const int k = k0 + kk;
+        if (k >= n) break;
+        const double M0 = sk[kk][0], iM = sk[kk][1];
+        const int64_t orow = ((int64_t)b * n + k) * n;
+        double vals[4];
+        uint8_t un[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double denom = __dmul_rn(M0, N0[q]);
+            if (denom == 0.0) {
+                vals[q] = l0 + q < n ? Ccentre[(int64_t)k * n + l0 + q] : 0.0;
+                un[q] = 1;
+                continue;
+            }
+            double d2 = 0.0, cross = 0.0, m1n1 = 0.0;
+            for (int a = 0; a < nd; ++a) {
+                const double D = (double)(kappa * (skc[kk][a] - lc[q][a]));
+                d2 = fma(D, D, d2);
+                cross = fma(D, sk[kk][2 + a] * N0[q] - M0 * Nm[q][a], cross);
+                m1n1 = fma(sk[kk][2 + a], Nm[q][a], m1n1);
+            }
+            const double numer = denom * d2 + 2.0 * cross + sk[kk][2 + nd] * N0[q] +
+                                 M0 * Nm[q][nd] - 2.0 * m1n1;
+            vals[q] = numer * iM * iN[q];
+            un[q] = 0;
+        }
+        if (vec) {
+            reinterpret_cast<double2 *>(out + orow + l0)[0] = make_double2(vals[0], vals[1]);
+            reinterpret_cast<double2 *>(out + orow + l0)[1] = make_double2(vals[2], vals[3]);
+            *reinterpret_cast<uchar4 *>(unused + orow + l0) = make_uchar4(un[0], un[1], un[2], un[3]);
+        } else {
+            for (int q = 0; q < 4 && l0 + q < n; ++q) {
+                out[orow + l0 + q] = vals[q];
+                unused[orow + l0 + q] = un[q];
+            }
         }
     }
 }
@@ -294,13 +322,16 @@ extern "C" int gdt_weighted_cost(const double *mu, const double *nu, const doubl
         moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(mu, mom, batch, f, c, kappa);
         moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(nu, mom + batch * n * W, batch,
                                                                    f, c, kappa);
-        dim3 mg((unsigned)((n + 1023) / 1024), (unsigned)n, (unsigned)batch);
+        dim3 mg((unsigned)((n + 1023) / 1024), (unsigned)((n + MB_K - 1) / MB_K), (unsigned)batch);
         cbar_moments_kernel<<<mg, 256, 0, st>>>(mu_c, nu_c, mom, mom + batch * n * W, centre_cost,
                                                  out, unused, c, kappa);
         cudaFreeAsync(mom, st);
         return cuda_status("gdt_weighted_cost(moments)");
     }
     if (mode == GDT_MODE_FAST) {
+        if (cbar_fast_diag(mu, nu, mu_c, nu_c, centre_cost, cost_table, max_sq, out, unused, batch,
+                           f, c, kappa, p, st) == GDT_OK)
+            return cuda_status("gdt_weighted_cost(diag)");
         const int rc = cbar_fast_toeplitz(mu, nu, mu_c, nu_c, centre_cost, cost_table, max_sq, out,
                                           unused, batch, f, c, kappa, p, st);
         if (rc == GDT_OK) return cuda_status("gdt_weighted_cost(toeplitz)");

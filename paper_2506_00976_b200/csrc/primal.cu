@@ -186,6 +186,21 @@ __device__ void block_reduce_red(Red &r, double *sh) {
     __syncthreads();
 }
 
+// Correctly rounded num / den for many numerators sharing one denominator:
+// y = RN(1/den) once, then q = RN(num*y), r = num - den*q (exact with FMA),
+// q' = RN(q + r*y) -- Markstein's theorem gives q' = RN(num/den) whenever no
+// intermediate leaves the normal range, which the guard checks (otherwise the
+// IEEE division routine runs).  Bit-identical to numpy's `mu / kb`.
+__device__ __forceinline__ double div_shared(double num, double den, double y) {
+    const double an = fabs(num), ad = fabs(den);
+    if (an > 0x1p-900 && an < 0x1p900 && ad > 0x1p-900 && ad < 0x1p900) {
+        const double q = __dmul_rn(num, y);
+        const double r = __fma_rn(-q, den, num);
+        return __fma_rn(r, y, q);
+    }
+    return __ddiv_rn(num, den);
+}
+
 // acc += (mass * w_i) * x_i sequentially over a run of `len` cells; the loads
 // are issued first (they do not depend on acc), then the exact-order adds.
 // Non-uniform kernels read w_i = wrow[i * wstride].
@@ -222,6 +237,7 @@ __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c,
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kb[u] = acc;
+    const double rcp = acc > 0.0 ? __drcp_rn(acc) : 0.0;
     const int origin = block_origin(k, c, f, kappa);
     for_block_cells(origin, f, kappa, [&](int tt, int i) {
         if (!UNIFORM && tt != t) return;
@@ -234,7 +250,7 @@ __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c,
         double an = 0.0;
         if (mui > 0.0) {
             if (acc <= 0.0) r.zrow = 1;
-            else an = __ddiv_rn(mui, acc);
+            else an = div_shared(mui, acc, rcp);
         }
         a_next[i] = an;
     });
@@ -255,6 +271,7 @@ __device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c,
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kta[u] = acc;
+    const double rcp = acc > 0.0 ? __drcp_rn(acc) : 0.0;
     const int origin = block_origin(l, c, f, kappa);
     for_block_cells(origin, f, kappa, [&](int ss, int j) {
         if (!UNIFORM && ss != s) return;
@@ -262,7 +279,7 @@ __device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c,
         double bj = 0.0;
         if (nuj > 0.0) {
             if (acc <= 0.0) r.zcol = 1;
-            else bj = __ddiv_rn(nuj, acc);
+            else bj = div_shared(nuj, acc, rcp);
             range_acc(bj, r.bmin, r.bmax, r.nonfinite);
             r.gap += fabs(__dsub_rn(nuj, __dmul_rn(bj, acc)));
         }
