@@ -10,16 +10,24 @@
 // in the two lanes of sm_100's packed FFMA2 (fma.rn.f32x2), the cost entering
 // as a broadcast scalar operand, so one instruction performs two FMAs.
 // p == 1 costs come from sqrt.approx on the MUFU pipe (dx^2 fixed per thread,
-// dy^2 per row offset); other p read an L1-resident fp32 table.  Column
-// windows start OFF cells left of the grid so every (block, column) pair is
-// covered exactly once; out-of-grid columns are computed and discarded.
-// Accuracy: fp32 FMA chains of kappa^d <= 64 terms (<= 3.8e-6 relative), fp64
-// block sums; fp32 mode contract of BASELINE.json is 1e-5.
+// dy^2 per row offset); other p read an L1-resident fp32 table.
+//
+// Lane mapping: the G = kappa^(d-1) higher-axis rows of one coarse block-row
+// sit in G consecutive lanes (G divides 32), so after the FMA loop a
+// butterfly over those lanes completes numer_kl for every (k+j, l) the group
+// covers; the group leader writes C-bar_kl = numer / (mu~ nu~) straight to
+// global memory.  Every (k, l) is produced by exactly one lane group: no
+// atomics, no shared-memory accumulator, deterministic.
+// Column windows start OFF cells left of the grid so every (block, column)
+// pair is covered exactly once; out-of-grid columns are computed and dropped.
+// Accuracy: fp32 FMA chains of kappa^d <= 64 terms (<= 3.8e-6 relative),
+// fp32 column/row folds of <= 2*kappa^(d-1)... terms, fp64 quotient; fp32
+// mode contract of BASELINE.json is 1e-5 on the bounds.
 #include "common.cuh"
 
 namespace gdt {
 
-constexpr int DG_THREADS = 256;
+constexpr int DG_MAX_THREADS = 288;
 constexpr int DG_R = 8;
 
 __device__ __forceinline__ unsigned long long dg_pack(float a, float b) {
@@ -37,25 +45,23 @@ __device__ __forceinline__ void dg_fma2(unsigned long long &acc, unsigned long l
 }
 
 template <int KAPPA, int KR, int ND, bool P1>
-__global__ void __launch_bounds__(DG_THREADS, 2) cbar_diag_kernel(
+__global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ mu_c,
     const double *__restrict__ nu_c, const double *__restrict__ Ccentre,
     const float *__restrict__ tab, int tab_max, double *__restrict__ out,
-    uint8_t *__restrict__ unused, Grid f, Grid c) {
+    uint8_t *__restrict__ unused, Grid f, Grid c, int nb_per_pass) {
     static_assert(KR % 2 == 0, "blocks are paired in FFMA2 lanes");
-    extern __shared__ double smem[];
+    extern __shared__ unsigned long long mus2[];  // [(th*KP + jp)*KAPPA + tx]
     constexpr int R = DG_R;
-    constexpr int NCD = KAPPA + R - 1;                      // distinct costs per row offset
-    constexpr int OFF = (((KR - 1) * KAPPA + R - 1) / R) * R;  // left extension of the windows
-    constexpr int m_hi = ND == 1 ? 1 : (ND == 2 ? KAPPA : KAPPA * KAPPA);
+    constexpr int NCD = KAPPA + R - 1;
+    constexpr int OFF = (((KR - 1) * KAPPA + R - 1) / R) * R;
+    constexpr int G = ND == 1 ? 1 : (ND == 2 ? KAPPA : KAPPA * KAPPA);  // rows per block-row
     constexpr int KP = KR / 2;
-    constexpr int SPAN = (KR - 1) * KAPPA + R;              // columns touched by one thread
+    constexpr int SPAN = (KR - 1) * KAPPA + R;
+    constexpr int PER = KAPPA < R ? KAPPA : R;  // columns of one block inside a window
     const int n = (int)c.cells, N0 = (int)f.n[0], n0 = (int)c.n[0];
     const int64_t N = f.cells;
-
-    double *numer = smem;                                                  // [KR][n]
-    unsigned long long *mus2 = reinterpret_cast<unsigned long long *>(numer + KR * n);
-    // mus2[(th * KP + jp) * KAPPA + tx] = (mu[k+2jp][t], mu[k+2jp+1][t])
+    const int nthreads = blockDim.x;
 
     const int64_t b = blockIdx.y;
     const int tiles_x = (n0 + KR - 1) / KR;
@@ -74,7 +80,7 @@ __global__ void __launch_bounds__(DG_THREADS, 2) cbar_diag_kernel(
             rem /= (int)c.n[a];
         }
     }
-    for (int i = threadIdx.x; i < m_hi * KP * KAPPA; i += DG_THREADS) {
+    for (int i = threadIdx.x; i < G * KP * KAPPA; i += nthreads) {
         const int th = i / (KP * KAPPA), rest = i - th * KP * KAPPA;
         const int jp = rest / KAPPA, tx = rest - jp * KAPPA;
         int64_t hoff = 0;
@@ -93,13 +99,12 @@ __global__ void __launch_bounds__(DG_THREADS, 2) cbar_diag_kernel(
         }
         mus2[i] = dg_pack(v[0], v[1]);
     }
-    for (int i = threadIdx.x; i < KR * n; i += DG_THREADS) numer[i] = 0.0;
     __syncthreads();
 
     const int segs = (N0 + OFF) / R;
-    const int rows_per_pass = DG_THREADS / segs;
-    const int64_t H = N / N0;
-    const int seg = threadIdx.x % segs, rloc = threadIdx.x / segs;
+    const int rr = threadIdx.x % G;                 // row offset inside the block-row
+    const int seg = (threadIdx.x / G) % segs;
+    const int gblk = threadIdx.x / (G * segs);      // block-row slot of this pass
     const int c0 = seg * R - OFF;
     const int base_dx = kx0 * KAPPA - c0 - (R - 1);
     float dx2[NCD];
@@ -108,17 +113,29 @@ __global__ void __launch_bounds__(DG_THREADS, 2) cbar_diag_kernel(
         const float dx = (float)(base_dx + q);
         dx2[q] = dx * dx;
     }
+    // higher-axis offsets of this lane inside its block-row
+    int roff[GDT_MAX_DIM] = {0, 0, 0, 0};
+    {
+        int rem = rr;
+#pragma unroll
+        for (int a = 1; a < ND; ++a) {
+            roff[a] = rem % KAPPA;
+            rem /= KAPPA;
+        }
+    }
+    const int n_hi = n / n0;  // coarse block-rows
 
-    for (int64_t h0 = 0; h0 < H; h0 += rows_per_pass) {
-        const int64_t hrow = h0 + rloc;
-        if (rloc >= rows_per_pass || hrow >= H) continue;
-        int chc[GDT_MAX_DIM] = {0, 0, 0, 0};
+    for (int lb0 = 0; lb0 < n_hi; lb0 += nb_per_pass) {
+        const int lb = lb0 + gblk;  // coarse block-row (flat over the higher axes)
+        const bool active = lb < n_hi && gblk < nb_per_pass;
+        int chc[GDT_MAX_DIM] = {0, 0, 0, 0};  // fine higher coordinates of this lane's row
         {
-            int64_t rem = hrow;
+            int rem = active ? lb : 0;
 #pragma unroll
             for (int a = 1; a < ND; ++a) {
-                chc[a] = (int)(rem % f.n[a]);
-                rem /= f.n[a];
+                const int la = rem % (int)c.n[a];
+                rem /= (int)c.n[a];
+                chc[a] = la * KAPPA + roff[a];
             }
         }
         unsigned long long acc[KP][R];
@@ -126,93 +143,92 @@ __global__ void __launch_bounds__(DG_THREADS, 2) cbar_diag_kernel(
         for (int jp = 0; jp < KP; ++jp)
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[jp][r] = 0ull;
-
+        if (active) {
 #pragma unroll 1
-        for (int th = 0; th < m_hi; ++th) {
-            int rem = th, hsq = 0, dy1 = 0;
+            for (int th = 0; th < G; ++th) {
+                int rem = th, hsq = 0, dy1 = 0;
 #pragma unroll
-            for (int a = 1; a < ND; ++a) {
-                const int ta = rem % KAPPA;
-                rem /= KAPPA;
-                const int d = khc[a] * KAPPA + ta - chc[a];
-                if (a == 1) dy1 = d < 0 ? -d : d;
-                hsq += d * d;
-            }
-            float cst[NCD];
-            if (P1) {
-                const float hf = (float)hsq;
-#pragma unroll
-                for (int q = 0; q < NCD; ++q) cst[q] = dg_sqrt(dx2[q] + hf);
-            } else if (ND == 2) {
-                const float *row = tab + dy1 * N0;
-#pragma unroll
-                for (int q = 0; q < NCD; ++q) {
-                    int dx = base_dx + q;
-                    dx = dx < 0 ? -dx : dx;
-                    cst[q] = __ldg(row + (dx < N0 ? dx : N0 - 1));  // clamp: masked columns
+                for (int a = 1; a < ND; ++a) {
+                    const int ta = rem % KAPPA;
+                    rem /= KAPPA;
+                    const int d = khc[a] * KAPPA + ta - chc[a];
+                    if (a == 1) dy1 = d < 0 ? -d : d;
+                    hsq += d * d;
                 }
-            } else {
+                float cst[NCD];
+                if (P1) {
+                    const float hf = (float)hsq;
 #pragma unroll
-                for (int q = 0; q < NCD; ++q) {
-                    const int dx = base_dx + q;
-                    const int sq = hsq + dx * dx;
-                    cst[q] = __ldg(tab + (sq < tab_max ? sq : tab_max));
+                    for (int q = 0; q < NCD; ++q) cst[q] = dg_sqrt(dx2[q] + hf);
+                } else if (ND == 2) {
+                    const float *row = tab + dy1 * N0;
+#pragma unroll
+                    for (int q = 0; q < NCD; ++q) {
+                        int dx = base_dx + q;
+                        dx = dx < 0 ? -dx : dx;
+                        cst[q] = __ldg(row + (dx < N0 ? dx : N0 - 1));  // clamp: dropped columns
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NCD; ++q) {
+                        const int dx = base_dx + q;
+                        const int sq = hsq + dx * dx;
+                        cst[q] = __ldg(tab + (sq < tab_max ? sq : tab_max));
+                    }
                 }
-            }
-            const unsigned long long *mrow = mus2 + th * KP * KAPPA;
+                const unsigned long long *mrow = mus2 + th * KP * KAPPA;
 #pragma unroll
-            for (int jp = 0; jp < KP; ++jp) {
+                for (int jp = 0; jp < KP; ++jp) {
 #pragma unroll
-                for (int tx = 0; tx < KAPPA; ++tx) {
-                    const unsigned long long m2 = mrow[jp * KAPPA + tx];
+                    for (int tx = 0; tx < KAPPA; ++tx) {
+                        const unsigned long long m2 = mrow[jp * KAPPA + tx];
 #pragma unroll
-                    for (int r = 0; r < R; ++r) dg_fma2(acc[jp][r], m2, cst[tx - r + R - 1]);
+                        for (int r = 0; r < R; ++r) dg_fma2(acc[jp][r], m2, cst[tx - r + R - 1]);
+                    }
                 }
             }
         }
-        // fold: numer[j][l] += sum over the thread's columns of block l of nu_c * G
-        const int64_t rowbase = hrow * N0;
+        // fold: this lane's row of every (k+j, l) it covers, then the G rows of the
+        // block-row in the lane group; the leader writes C-bar
+        int64_t rowbase = 0;
+#pragma unroll
+        for (int a = 1; a < ND; ++a) rowbase += (int64_t)chc[a] * f.stride[a];
         float nv[SPAN];
 #pragma unroll
         for (int q = 0; q < SPAN; ++q) {
             const int col = c0 + q;
-            nv[q] = (col >= 0 && col < N0) ? (float)nub[rowbase + col] : 0.f;
+            nv[q] = (active && col >= 0 && col < N0) ? (float)nub[rowbase + col] : 0.f;
         }
-        int l_hi = 0;
-#pragma unroll
-        for (int a = ND - 1; a >= 1; --a) l_hi = l_hi * (int)c.n[a] + chc[a] / KAPPA;
-        constexpr int PER = KAPPA < R ? KAPPA : R;
 #pragma unroll
         for (int jp = 0; jp < KP; ++jp) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int j = 2 * jp + h;
-                if (j >= kr_valid) continue;
 #pragma unroll
                 for (int g = 0; g < R / PER; ++g) {
-                    const int cs = c0 + j * KAPPA + g * PER;  // first column of the group
-                    if (cs < 0 || cs >= N0) continue;
                     float s = 0.f;
 #pragma unroll
                     for (int r = g * PER; r < (g + 1) * PER; ++r) {
                         const unsigned long long a2 = acc[jp][r];
-                        const float gv = __uint_as_float((unsigned)(h ? (a2 >> 32) : (a2 & 0xffffffffu)));
+                        const float gv =
+                            __uint_as_float((unsigned)(h ? (a2 >> 32) : (a2 & 0xffffffffu)));
                         s = fmaf(nv[j * KAPPA + r], gv, s);
                     }
-                    atomicAdd(&numer[j * n + l_hi * n0 + cs / KAPPA], (double)s);
+#pragma unroll
+                    for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+                    const int cs = c0 + j * KAPPA + g * PER;
+                    if (rr == 0 && active && j < kr_valid && cs >= 0 && cs < N0) {
+                        const int k = k_hi * n0 + kx0 + j;
+                        const int l = lb * n0 + cs / KAPPA;
+                        const double denom = __dmul_rn(mu_c[b * n + k], nu_c[b * n + l]);
+                        const int64_t oi = ((int64_t)b * n + k) * n + l;
+                        const bool un = denom == 0.0;
+                        out[oi] = un ? Ccentre[(int64_t)k * n + l] : (double)s / denom;
+                        unused[oi] = un ? 1 : 0;
+                    }
                 }
             }
         }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kr_valid * n; i += DG_THREADS) {
-        const int j = i / n, l = i - j * n;
-        const int k = k_hi * n0 + kx0 + j;
-        const double denom = __dmul_rn(mu_c[b * n + k], nu_c[b * n + l]);
-        const int64_t oi = ((int64_t)b * n + k) * n + l;
-        const bool un = denom == 0.0;
-        out[oi] = un ? Ccentre[(int64_t)k * n + l] : numer[i] / denom;
-        unused[oi] = un ? 1 : 0;
     }
 }
 
@@ -237,13 +253,15 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
                      uint8_t *unused, int64_t batch, const Grid &f, const Grid &c, bool p1,
                      cudaStream_t st) {
     constexpr int OFF = (((KR - 1) * KAPPA + DG_R - 1) / DG_R) * DG_R;
-    if (f.n[0] % DG_R || (f.n[0] + OFF) / DG_R > DG_THREADS) return GDT_ERR_UNSUPPORTED;
-    if (f.cells >= (1ll << 31)) return GDT_ERR_UNSUPPORTED;
+    const int Gr = (int)ipow(KAPPA, f.nd - 1);
+    if (Gr > 32 || f.n[0] % DG_R || f.cells >= (1ll << 31)) return GDT_ERR_UNSUPPORTED;
+    const int segs = (int)((f.n[0] + OFF) / DG_R);
+    if (Gr * segs > DG_MAX_THREADS) return GDT_ERR_UNSUPPORTED;
+    const int nb = DG_MAX_THREADS / (Gr * segs);
+    const int threads = ((Gr * segs * nb + 31) / 32) * 32;
+    if (threads > DG_MAX_THREADS) return GDT_ERR_UNSUPPORTED;
     const int64_t n = c.cells;
-    int m_hi = 1;
-    for (int a = 1; a < f.nd; ++a) m_hi *= KAPPA;
-    const size_t bytes = sizeof(double) * KR * n + sizeof(unsigned long long) * m_hi * KR / 2 * KAPPA;
-    if (bytes > 200 * 1024) return GDT_ERR_UNSUPPORTED;
+    const size_t bytes = sizeof(unsigned long long) * Gr * (KR / 2) * KAPPA;
     float *ftab = nullptr;
     int tab_max = 0;
     if (!p1) {
@@ -257,9 +275,8 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
     const int64_t tiles_x = (c.n[0] + KR - 1) / KR;
     dim3 grid((unsigned)(tiles_x * (n / c.n[0])), (unsigned)batch);
     auto run = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        kern<<<grid, DG_THREADS, bytes, st>>>(mu, nu, mu_c, nu_c, Ccentre, ftab, tab_max, out,
-                                              unused, f, c);
+        kern<<<grid, threads, bytes, st>>>(mu, nu, mu_c, nu_c, Ccentre, ftab, tab_max, out, unused,
+                                           f, c, nb);
     };
     switch (f.nd * 2 + (p1 ? 1 : 0)) {
         case 2: run(cbar_diag_kernel<KAPPA, KR, 1, false>); break;

@@ -158,19 +158,39 @@ __global__ void __launch_bounds__(128) pruned_ct_kernel(const T *__restrict__ v,
                                  tm[((int64_t)t2 * nt1 + t1) * nt0 + t0];
                     if (lb >= ub) continue;
                     const int sx0 = t0 * 8;
+                    // dx^2 of the 15 Toeplitz slots, fixed for the whole tile
+                    float dx2[15];
+#pragma unroll
+                    for (int q = 0; q < 15; ++q) {
+                        const float dx = (float)(sx0 - xj0 - 7 + q);
+                        dx2[q] = dx * dx;
+                    }
                     for (int z = 0; z < S2; ++z)
                         for (int y = 0; y < S1; ++y) {
                             const int ys = t1 * S1 + y, zs = t2 * S2 + z;
                             const int hsq = (ys - yj) * (ys - yj) + (zs - zj) * (zs - zj);
                             const T *row = vb + (int64_t)zs * g.stride[2] + (int64_t)ys * g.stride[1] + sx0;
                             T vs[8];
+                            if constexpr (sizeof(T) == 4) {
+                                const float4 v0 = __ldg(reinterpret_cast<const float4 *>(row));
+                                const float4 v1 = __ldg(reinterpret_cast<const float4 *>(row) + 1);
+                                vs[0] = v0.x; vs[1] = v0.y; vs[2] = v0.z; vs[3] = v0.w;
+                                vs[4] = v1.x; vs[5] = v1.y; vs[6] = v1.z; vs[7] = v1.w;
+                            } else {
 #pragma unroll
-                            for (int s = 0; s < 8; ++s) vs[s] = row[s];
+                                for (int s = 0; s < 8; ++s) vs[s] = row[s];
+                            }
                             T cst[15];
+                            if constexpr (sizeof(T) == 4 && P1) {
+                                const float hf = (float)hsq;
 #pragma unroll
-                            for (int q = 0; q < 15; ++q) {
-                                const int dx = sx0 - xj0 - 7 + q;
-                                cst[q] = cost_of(hsq + dx * dx);
+                                for (int q = 0; q < 15; ++q) cst[q] = sqrt_approx(dx2[q] + hf);
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < 15; ++q) {
+                                    const int dx = sx0 - xj0 - 7 + q;
+                                    cst[q] = cost_of(hsq + dx * dx);
+                                }
                             }
                             if constexpr (sizeof(T) == 4) {
 #pragma unroll
