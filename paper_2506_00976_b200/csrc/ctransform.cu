@@ -267,7 +267,7 @@ extern "C" int64_t gdt_ctransform_scratch_bytes(int64_t batch, int ndim, const i
     int64_t need_sq = 0;
     for (int a = 0; a < ndim; ++a) need_sq += (dims[a] - 1) * (dims[a] - 1);
     // ping-pong buffer (+ fp32 input copy) + fp32 cost table + pruning tile maxima
-    return batch * g.cells * el * 2 + (need_sq + 1) * 4 + batch * ct_pruned_tiles(g) * 8 + 512;
+    return batch * g.cells * el * 2 + (need_sq + 1) * 4 + batch * ct_pruned_tiles(g) * 8 + 1024;
 }
 
 extern "C" int gdt_ctransform_grid(const void *v, void *out, int64_t batch, int ndim,

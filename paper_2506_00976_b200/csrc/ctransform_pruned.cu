@@ -79,14 +79,20 @@ template <typename T, int ND, bool P1>
 __global__ void __launch_bounds__(128) pruned_ct_kernel(const T *__restrict__ v,
                                                         const T *__restrict__ tmax,
                                                         T *__restrict__ out, int64_t batch,
-                                                        Grid g, const T *__restrict__ tab) {
+                                                        Grid g, const T *__restrict__ tab,
+                                                        unsigned long long *__restrict__ counter) {
     constexpr int R1 = ND == 2 ? 16 : 4, R2 = ND == 2 ? 1 : 4;   // region extent y, z
     constexpr int S1 = ND == 2 ? 8 : 4, S2 = ND == 2 ? 1 : 4;    // tile extent y, z
     const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int nr0 = (int)(g.n[0] / 16), nr1 = (int)(g.n[1] / R1), nr2 = (int)(g.n[2] / R2);
     const int64_t regions = (int64_t)nr0 * nr1 * nr2;
-    if (warp >= batch * regions) return;
+    const int64_t total = batch * regions;
+    // persistent warps: regions are handed out dynamically (pruning makes the
+    // work per region uneven)
+    unsigned long long item = lane == 0 ? atomicAdd(counter, 1ull) : 0ull;
+    item = __shfl_sync(0xffffffffu, item, 0);
+    for (; item < (unsigned long long)total;) {
+    const int64_t warp = (int64_t)item;
     const int64_t b = warp / regions;
     int rr = (int)(warp - b * regions);
     const int rx = rr % nr0;
@@ -226,6 +232,9 @@ __global__ void __launch_bounds__(128) pruned_ct_kernel(const T *__restrict__ v,
     T *ob = out + b * g.cells + (int64_t)zj * g.stride[2] + (int64_t)yj * g.stride[1] + xj0;
 #pragma unroll
     for (int r8 = 0; r8 < 8; ++r8) ob[r8] = best[r8];
+    item = lane == 0 ? atomicAdd(counter, 1ull) : 0ull;
+    item = __shfl_sync(0xffffffffu, item, 0);
+    }
 }
 
 // Returns GDT_ERR_UNSUPPORTED outside the tiled envelope (caller falls back).
@@ -252,13 +261,20 @@ static int run_pruned(const T *v, T *out, T *tmax, int64_t batch, const Grid &g,
     const int64_t regions = (g.n[0] / 16) * (g.n[1] / (g.nd == 2 ? 16 : 4)) *
                             (g.n[2] / (g.nd == 2 ? 1 : 4));
     const int64_t warps = batch * regions;
-    const unsigned ctas = (unsigned)((warps + 3) / 4);
+    unsigned long long *counter =
+        reinterpret_cast<unsigned long long *>(tmax + ((batch * tiles + 1) & ~1ll));
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t ctas = (warps + 3) / 4;
+    if (ctas > (int64_t)sms * 5) ctas = (int64_t)sms * 5;  // ~5 resident CTAs per SM
     if (g.nd == 2) {
-        if (p1 && sizeof(T) == 4) pruned_ct_kernel<T, 2, true><<<ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab);
-        else pruned_ct_kernel<T, 2, false><<<ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab);
+        if (p1 && sizeof(T) == 4) pruned_ct_kernel<T, 2, true><<<(unsigned)ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab, counter);
+        else pruned_ct_kernel<T, 2, false><<<(unsigned)ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab, counter);
     } else {
-        if (p1 && sizeof(T) == 4) pruned_ct_kernel<T, 3, true><<<ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab);
-        else pruned_ct_kernel<T, 3, false><<<ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab);
+        if (p1 && sizeof(T) == 4) pruned_ct_kernel<T, 3, true><<<(unsigned)ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab, counter);
+        else pruned_ct_kernel<T, 3, false><<<(unsigned)ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab, counter);
     }
     return GDT_OK;
 }

@@ -83,25 +83,27 @@ __device__ __forceinline__ void for_block_cells(int origin, const G32 &f, int ka
             }
 }
 
-// Visit the cells of the union of coarse blocks ids[lo..hi) (sorted
-// ascending) in ascending fine flat order, as runs of kappa consecutive cells
+// Visit the cells of the union of coarse blocks of arcs [lo, hi) (sorted by
+// coarse id) in ascending fine flat order, as runs of kappa consecutive cells
 // along axis 0: fn(q, cell, s) with q the arc index, cell the fine flat id of
 // the run's first cell and s its within-block offset (Fortran-flattened).
+// pc[q] packs the arc's coarse coordinates, 16 bits per axis (axis 0 lowest).
+__device__ __forceinline__ int pc_coord(int64_t w, int a) { return (int)((w >> (16 * a)) & 0xffff); }
+
 template <int LEVEL, class F>
-__device__ __forceinline__ void walk(const int32_t *ids, int lo, int hi, const G32 &c,
-                                     const G32 &f, int kappa, int fbase, int sbase, int kpow,
-                                     F &fn) {
+__device__ __forceinline__ void walk(const int64_t *pc, int lo, int hi, const G32 &f, int kappa,
+                                     int fbase, int sbase, int kpow, F &fn) {
     if constexpr (LEVEL == 0) {
         // one run of kappa consecutive cells per arc: fn(q, first_cell, first_s)
-        for (int q = lo; q < hi; ++q) fn(q, fbase + (ids[q] % c.n[0]) * kappa, sbase);
+        for (int q = lo; q < hi; ++q) fn(q, fbase + pc_coord(pc[q], 0) * kappa, sbase);
     } else {
         int r = lo;
         while (r < hi) {
-            const int cr = coord_of(ids[r], c, LEVEL);
+            const int cr = pc_coord(pc[r], LEVEL);
             int e = r + 1;
-            while (e < hi && coord_of(ids[e], c, LEVEL) == cr) ++e;
+            while (e < hi && pc_coord(pc[e], LEVEL) == cr) ++e;
             for (int sa = 0; sa < kappa; ++sa)
-                walk<LEVEL - 1>(ids, r, e, c, f, kappa, fbase + (cr * kappa + sa) * f.stride[LEVEL],
+                walk<LEVEL - 1>(pc, r, e, f, kappa, fbase + (cr * kappa + sa) * f.stride[LEVEL],
                                 sbase + sa * kpow, kpow / kappa, fn);
             r = e;
         }
@@ -109,20 +111,42 @@ __device__ __forceinline__ void walk(const int32_t *ids, int lo, int hi, const G
 }
 
 template <class F>
-__device__ __forceinline__ void walk_blocks(const int32_t *ids, int cnt, const G32 &c,
+__device__ __forceinline__ void walk_blocks(const int64_t *pc, int cnt, const G32 &c,
                                             const G32 &f, int kappa, F &fn) {
     const int kpow = (int)ipow(kappa, c.nd - 1);
     switch (c.nd) {
-        case 1: walk<0>(ids, 0, cnt, c, f, kappa, 0, 0, kpow, fn); break;
-        case 2: walk<1>(ids, 0, cnt, c, f, kappa, 0, 0, kpow, fn); break;
-        case 3: walk<2>(ids, 0, cnt, c, f, kappa, 0, 0, kpow, fn); break;
-        default: walk<3>(ids, 0, cnt, c, f, kappa, 0, 0, kpow, fn); break;
+        case 1: walk<0>(pc, 0, cnt, f, kappa, 0, 0, kpow, fn); break;
+        case 2: walk<1>(pc, 0, cnt, f, kappa, 0, 0, kpow, fn); break;
+        case 3: walk<2>(pc, 0, cnt, f, kappa, 0, 0, kpow, fn); break;
+        default: walk<3>(pc, 0, cnt, f, kappa, 0, 0, kpow, fn); break;
+    }
+}
+
+// packed coarse coordinates of every arc endpoint (row lists: targets, column
+// lists: sources), built once per launch
+__global__ void pack_coords_kernel(const int32_t *__restrict__ ids, const int64_t *__restrict__ arc_off,
+                                   int64_t per_pair, int64_t batch, G32 c,
+                                   int64_t *__restrict__ pc) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < batch * per_pair;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / per_pair, q = t - b * per_pair;
+        if (q >= arc_off[b + 1] - arc_off[b]) continue;
+        const int64_t i = arc_off[b] + q;
+        int id = ids[i];
+        int64_t w = 0;
+        for (int a = c.nd - 1; a >= 0; --a) {
+            const int x = id / c.stride[a];
+            id -= x * c.stride[a];
+            w |= (int64_t)x << (16 * a);
+        }
+        pc[i] = w;
     }
 }
 
 struct PairPtrs {
     const double *mu, *nu;
     const int32_t *rptr, *rcol, *cptr, *crow;
+    const int64_t *rpc, *cpc;
     const double *rmass, *cmass;
     double *aA, *aB, *b, *kb, *kta;
 };
@@ -208,6 +232,22 @@ template <bool UNIFORM>
 __device__ __forceinline__ void accumulate_run(double &acc, double mass, double Wu,
                                                const double *wrow, int wstride,
                                                const double *x, int len) {
+    if (UNIFORM && (len & 1) == 0) {
+        // 16-byte loads (kappa even), issued ahead of the exact-order adds
+        const double coef = __dmul_rn(mass, Wu);
+        for (int o = 0; o < len; o += 4) {
+            const double2 x0 = reinterpret_cast<const double2 *>(x + o)[0];
+            const double2 x1 = o + 2 < len ? reinterpret_cast<const double2 *>(x + o)[1]
+                                           : make_double2(0.0, 0.0);
+            acc = __dadd_rn(acc, __dmul_rn(coef, x0.x));
+            acc = __dadd_rn(acc, __dmul_rn(coef, x0.y));
+            if (o + 2 < len) {
+                acc = __dadd_rn(acc, __dmul_rn(coef, x1.x));
+                acc = __dadd_rn(acc, __dmul_rn(coef, x1.y));
+            }
+        }
+        return;
+    }
     for (int o = 0; o < len; o += 4) {
         double xv[4];
 #pragma unroll
@@ -229,7 +269,7 @@ __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c,
     const int k = UNIFORM ? u : u / m;
     const int t = UNIFORM ? 0 : u - k * m;
     const int lo = P.rptr[k], hi = P.rptr[k + 1];
-    const int32_t *ids = P.rcol + lo;
+    const int64_t *ids = P.rpc + lo;
     const double *ms = P.rmass + lo;
     double acc = 0.0;
     auto fn = [&](int q, int cell, int s) {
@@ -263,7 +303,7 @@ __device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c,
     const int l = UNIFORM ? u : u / m;
     const int s = UNIFORM ? 0 : u - l * m;
     const int lo = P.cptr[l], hi = P.cptr[l + 1];
-    const int32_t *ids = P.crow + lo;
+    const int64_t *ids = P.cpc + lo;
     const double *ms = P.cmass + lo;
     double acc = 0.0;
     auto fn = [&](int q, int cell, int t) {
@@ -298,7 +338,8 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     const int32_t *__restrict__ col_arc_row, const double *__restrict__ col_arc_mass,
     const double *__restrict__ W, const double *__restrict__ xi_in, int64_t max_iter, G32 f,
     G32 c, int kappa, double *__restrict__ out, int32_t *__restrict__ status,
-    double *__restrict__ scratch, int64_t stride_pair) {
+    double *__restrict__ scratch, int64_t stride_pair, const int64_t *__restrict__ rpc,
+    const int64_t *__restrict__ cpc) {
     __shared__ double sh[(PT / 32) * 6];
     const int64_t b = blockIdx.x;
     const int N = f.cells, n = c.cells;
@@ -316,6 +357,8 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     P.rmass = row_arc_mass + a0;
     P.crow = col_arc_row + a0;
     P.cmass = col_arc_mass + a0;
+    P.rpc = rpc + a0;
+    P.cpc = cpc + a0;
     double *ws = scratch + b * stride_pair;
     P.aA = ws;
     P.aB = ws + N;
@@ -718,7 +761,7 @@ __global__ void sum_parts_kernel(const double *__restrict__ part, int count, dou
 // pairs: moments [B, n, MW], tv partials [B, tv_ctas, 2], price partials
 // [B, pr_ctas]
 struct PrimalLayout {
-    int64_t stride_pair, mom_off, tv_off, pr_off, total, tv_ctas, pr_ctas;
+    int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, total, tv_ctas, pr_ctas;
 };
 
 inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, bool uniform,
@@ -734,7 +777,8 @@ inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, b
     L.pr_ctas = (items + MT - 1) / MT;
     L.tv_off = L.mom_off + batch * c.cells * MW;
     L.pr_off = L.tv_off + batch * L.tv_ctas * 2;
-    L.total = L.pr_off + batch * L.pr_ctas;
+    L.pc_off = L.pr_off + batch * L.pr_ctas;       // packed arc coordinates (int64)
+    L.total = L.pc_off + 2 * batch * max_arcs;
     return L;
 }
 
@@ -776,14 +820,25 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
     const PrimalLayout L = primal_layout(batch, f, c, uni, p == 2.0, 2 * c.cells);
     double *ws = (double *)scratch;
     const G32 f32 = to32(f), c32 = to32(c);
+    GDT_CHECK_ARG(c.n[0] < 65536 && c.n[1] < 65536 && c.n[2] < 65536 && c.n[3] < 65536,
+                  "gdt_primal_upscale: coarse axes must be < 65536");
+    int64_t *rpc = reinterpret_cast<int64_t *>(ws + L.pc_off);
+    int64_t *cpc = rpc + batch * 2 * c.cells;
+    const int64_t per_pair = 2 * c.cells;
+    pack_coords_kernel<<<grid_size(batch * per_pair, 256), 256, 0, st>>>(row_arc_col, arc_off,
+                                                                         per_pair, batch, c32, rpc);
+    pack_coords_kernel<<<grid_size(batch * per_pair, 256), 256, 0, st>>>(col_arc_row, arc_off,
+                                                                         per_pair, batch, c32, cpc);
     if (uni)
         ipf_kernel<true><<<(unsigned)batch, PT, 0, st>>>(
             mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
-            col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair);
+            col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair,
+            rpc, cpc);
     else
         ipf_kernel<false><<<(unsigned)batch, PT, 0, st>>>(
             mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
-            col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair);
+            col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair,
+            rpc, cpc);
     const int closed = uni && p == 2.0;
     dim3 gtv((unsigned)L.tv_ctas, (unsigned)batch), gpr((unsigned)L.pr_ctas, (unsigned)batch);
     if (uni) {
