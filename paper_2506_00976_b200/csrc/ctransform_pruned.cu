@@ -150,11 +150,16 @@ __global__ void __launch_bounds__(128) pruned_ct_kernel(const T *__restrict__ v,
         const int a1 = max(h1lo - r, 0), b1 = min(h1hi + r, nt1 - 1);
         const int a2 = max(h2lo - r, 0), b2 = min(h2hi + r, nt2 - 1);
         for (int t2 = a2; t2 <= b2; ++t2)
-            for (int t1 = a1; t1 <= b1; ++t1)
-                for (int t0 = a0; t0 <= b0; ++t0) {
+            for (int t1 = a1; t1 <= b1; ++t1) {
+                const int d1 = t1 < h1lo ? h1lo - t1 : (t1 > h1hi ? t1 - h1hi : 0);
+                const int d2 = t2 < h2lo ? h2lo - t2 : (t2 > h2hi ? t2 - h2hi : 0);
+                // only ring tiles: a full t0 sweep on the ring's t1/t2 faces, else
+                // just the two t0 ends at distance r
+                const bool face = max(d1, d2) == r;
+                const int step = face ? 1 : (h0hi + r) - (h0lo - r);
+                for (int t0 = face ? a0 : h0lo - r; t0 <= b0; t0 += step > 0 ? step : 1) {
+                    if (t0 < a0) continue;
                     const int d0 = t0 < h0lo ? h0lo - t0 : (t0 > h0hi ? t0 - h0hi : 0);
-                    const int d1 = t1 < h1lo ? h1lo - t1 : (t1 > h1hi ? t1 - h1hi : 0);
-                    const int d2 = t2 < h2lo ? h2lo - t2 : (t2 > h2hi ? t2 - h2hi : 0);
                     if (max(max(d0, d1), d2) != r) continue;
                     // gap between the region box and the tile box, per axis
                     const int g0 = max(0, max(t0 * 8 - (X0 + 15), X0 - (t0 * 8 + 7)));
@@ -228,6 +233,7 @@ __global__ void __launch_bounds__(128) pruned_ct_kernel(const T *__restrict__ v,
                     }
                     ub = m;
                 }
+            }
     }
     T *ob = out + b * g.cells + (int64_t)zj * g.stride[2] + (int64_t)yj * g.stride[1] + xj0;
 #pragma unroll
