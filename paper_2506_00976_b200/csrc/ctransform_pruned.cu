@@ -76,7 +76,7 @@ __global__ void tile_max_kernel(const T *__restrict__ v, T *__restrict__ tmax, i
 
 // ND = 2: region 16x16, tile 8x8; ND = 3: region 16x4x4, tile 8x4x4
 template <typename T, int ND, bool P1>
-__global__ void __launch_bounds__(128) pruned_ct_kernel(const T *__restrict__ v,
+__global__ void __launch_bounds__(64) pruned_ct_kernel(const T *__restrict__ v,
                                                         const T *__restrict__ tmax,
                                                         T *__restrict__ out, int64_t batch,
                                                         Grid g, const T *__restrict__ tab,
@@ -87,12 +87,15 @@ __global__ void __launch_bounds__(128) pruned_ct_kernel(const T *__restrict__ v,
     const int nr0 = (int)(g.n[0] / 16), nr1 = (int)(g.n[1] / R1), nr2 = (int)(g.n[2] / R2);
     const int64_t regions = (int64_t)nr0 * nr1 * nr2;
     const int64_t total = batch * regions;
-    // persistent warps: regions are handed out dynamically (pruning makes the
-    // work per region uneven)
-    unsigned long long item = lane == 0 ? atomicAdd(counter, 1ull) : 0ull;
-    item = __shfl_sync(0xffffffffu, item, 0);
-    for (; item < (unsigned long long)total;) {
-    const int64_t warp = (int64_t)item;
+    // one region per 2-warp CTA; warp `half` takes every other tile of each
+    // ring (with its own bound), the two results are merged at the end.  Many
+    // small CTAs let the hardware scheduler balance the uneven pruned work.
+    (void)counter;
+    const int half = threadIdx.x >> 5;
+    const int64_t warp = blockIdx.x;
+    if (warp >= total) return;
+    __shared__ T other[32][8];
+    int parity = 0;
     const int64_t b = warp / regions;
     int rr = (int)(warp - b * regions);
     const int rx = rr % nr0;
@@ -167,6 +170,7 @@ __global__ void __launch_bounds__(128) pruned_ct_kernel(const T *__restrict__ v,
                     const int g2 = max(0, max(t2 * S2 - (Z0 + R2 - 1), Z0 - (t2 * S2 + S2 - 1)));
                     const T lb = lowered(cost_of(g0 * g0 + g1 * g1 + g2 * g2)) -
                                  tm[((int64_t)t2 * nt1 + t1) * nt0 + t0];
+                    if (((parity++) & 1) != half) continue;
                     if (lb >= ub) continue;
                     const int sx0 = t0 * 8;
                     // dx^2 of the 15 Toeplitz slots, fixed for the whole tile
@@ -235,11 +239,18 @@ __global__ void __launch_bounds__(128) pruned_ct_kernel(const T *__restrict__ v,
                 }
             }
     }
-    T *ob = out + b * g.cells + (int64_t)zj * g.stride[2] + (int64_t)yj * g.stride[1] + xj0;
+    if (half == 1) {
 #pragma unroll
-    for (int r8 = 0; r8 < 8; ++r8) ob[r8] = best[r8];
-    item = lane == 0 ? atomicAdd(counter, 1ull) : 0ull;
-    item = __shfl_sync(0xffffffffu, item, 0);
+        for (int r8 = 0; r8 < 8; ++r8) other[lane][r8] = best[r8];
+    }
+    __syncthreads();
+    if (half == 0) {
+        T *ob = out + b * g.cells + (int64_t)zj * g.stride[2] + (int64_t)yj * g.stride[1] + xj0;
+#pragma unroll
+        for (int r8 = 0; r8 < 8; ++r8) {
+            const T o = other[lane][r8];
+            ob[r8] = o < best[r8] ? o : best[r8];
+        }
     }
 }
 
@@ -273,14 +284,14 @@ static int run_pruned(const T *v, T *out, T *tmax, int64_t batch, const Grid &g,
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int64_t ctas = (warps + 3) / 4;
-    if (ctas > (int64_t)sms * 5) ctas = (int64_t)sms * 5;  // ~5 resident CTAs per SM
+    (void)sms;
+    const unsigned ctas = (unsigned)warps;  // one region per 2-warp CTA
     if (g.nd == 2) {
-        if (p1 && sizeof(T) == 4) pruned_ct_kernel<T, 2, true><<<(unsigned)ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab, counter);
-        else pruned_ct_kernel<T, 2, false><<<(unsigned)ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab, counter);
+        if (p1 && sizeof(T) == 4) pruned_ct_kernel<T, 2, true><<<ctas, 64, 0, st>>>(v, tmax, out, batch, g, tab, counter);
+        else pruned_ct_kernel<T, 2, false><<<ctas, 64, 0, st>>>(v, tmax, out, batch, g, tab, counter);
     } else {
-        if (p1 && sizeof(T) == 4) pruned_ct_kernel<T, 3, true><<<(unsigned)ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab, counter);
-        else pruned_ct_kernel<T, 3, false><<<(unsigned)ctas, 128, 0, st>>>(v, tmax, out, batch, g, tab, counter);
+        if (p1 && sizeof(T) == 4) pruned_ct_kernel<T, 3, true><<<ctas, 64, 0, st>>>(v, tmax, out, batch, g, tab, counter);
+        else pruned_ct_kernel<T, 3, false><<<ctas, 64, 0, st>>>(v, tmax, out, batch, g, tab, counter);
     }
     return GDT_OK;
 }

@@ -265,7 +265,8 @@ __device__ __forceinline__ void accumulate_run(double &acc, double mass, double 
 template <bool UNIFORM>
 __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c, const G32 &f,
                                          int kappa, int m, const double *W, double Wu, bool init,
-                                         const double *a_cur, double *a_next, Red &r) {
+                                         const double *a_cur, double *a_next, Red &r,
+                                         const double *bsrc) {
     const int k = UNIFORM ? u : u / m;
     const int t = UNIFORM ? 0 : u - k * m;
     const int lo = P.rptr[k], hi = P.rptr[k + 1];
@@ -273,7 +274,7 @@ __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c,
     const double *ms = P.rmass + lo;
     double acc = 0.0;
     auto fn = [&](int q, int cell, int s) {
-        accumulate_run<UNIFORM>(acc, ms[q], Wu, W + t * m + s, 1, P.b + cell, kappa);
+        accumulate_run<UNIFORM>(acc, ms[q], Wu, W + t * m + s, 1, bsrc + cell, kappa);
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kb[u] = acc;
@@ -299,7 +300,7 @@ __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c,
 template <bool UNIFORM>
 __device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c, const G32 &f,
                                          int kappa, int m, const double *W, double Wu,
-                                         const double *a_cur, Red &r) {
+                                         const double *a_cur, Red &r, const double *asrc) {
     const int l = UNIFORM ? u : u / m;
     const int s = UNIFORM ? 0 : u - l * m;
     const int lo = P.cptr[l], hi = P.cptr[l + 1];
@@ -307,7 +308,7 @@ __device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c,
     const double *ms = P.cmass + lo;
     double acc = 0.0;
     auto fn = [&](int q, int cell, int t) {
-        accumulate_run<UNIFORM>(acc, ms[q], Wu, W + t * m + s, m, a_cur + cell, kappa);
+        accumulate_run<UNIFORM>(acc, ms[q], Wu, W + t * m + s, m, asrc + cell, kappa);
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kta[u] = acc;
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     const double *__restrict__ W, const double *__restrict__ xi_in, int64_t max_iter, G32 f,
     G32 c, int kappa, double *__restrict__ out, int32_t *__restrict__ status,
     double *__restrict__ scratch, int64_t stride_pair, const int64_t *__restrict__ rpc,
-    const int64_t *__restrict__ cpc) {
+    const int64_t *__restrict__ cpc, int use_smem) {
     __shared__ double sh[(PT / 32) * 6];
     const int64_t b = blockIdx.x;
     const int N = f.cells, n = c.cells;
@@ -377,11 +378,23 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     const double xi = xi_in[b] < 0.0 ? 1e-9 * cnt : xi_in[b];
     __syncthreads();
 
+    // The sequential exact-order sums of the long units are load-latency
+    // bound; when the grid fits, the vector they gather from (b for row
+    // units, a for column units) is staged in shared memory first.
+    extern __shared__ double sx[];
+    auto stage = [&](const double *src) -> const double * {
+        if (!use_smem) return src;
+        for (int i = threadIdx.x; i < N; i += PT) sx[i] = src[i];
+        __syncthreads();
+        return sx;
+    };
+
     // kb = K b0, a = mu / kb (sinkhorn.py:119-129 before the first sweep)
     Red r = red_init();
     double *a_cur = P.aA, *a_nxt = P.aB;
+    const double *bs = stage(P.b);
     for (int u = threadIdx.x; u < U; u += PT)
-        row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, true, nullptr, a_cur, r);
+        row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, true, nullptr, a_cur, r, bs);
     block_reduce_red(r, sh);
     int st = r.zrow ? GDT_PAIR_ZERO_DENOM_ROW : GDT_PAIR_OK;
     int64_t it = 0;
@@ -390,14 +403,16 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     while (st == GDT_PAIR_OK && it < max_iter) {
         ++it;
         Red rc = red_init();
+        const double *as = stage(a_cur);
         for (int u = threadIdx.x; u < U; u += PT)
-            col_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, a_cur, rc);
+            col_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, a_cur, rc, as);
         if (__syncthreads_or(rc.zcol)) {  // before anything reads b
             st = GDT_PAIR_ZERO_DENOM_COL;
             break;
         }
+        const double *bsw = stage(P.b);
         for (int u = threadIdx.x; u < U; u += PT)
-            row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, false, a_cur, a_nxt, rc);
+            row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, false, a_cur, a_nxt, rc, bsw);
         block_reduce_red(rc, sh);
         // _check_scale_range(a), then (b) (sinkhorn.py:137-138)
         const bool bad_a = rc.amin <= rc.amax &&
@@ -829,16 +844,26 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
                                                                          per_pair, batch, c32, rpc);
     pack_coords_kernel<<<grid_size(batch * per_pair, 256), 256, 0, st>>>(col_arc_row, arc_off,
                                                                          per_pair, batch, c32, cpc);
-    if (uni)
-        ipf_kernel<true><<<(unsigned)batch, PT, 0, st>>>(
+    const size_t sxb = sizeof(double) * f.cells;
+    const int use_smem = sxb <= 160 * 1024;
+    const size_t dyn = use_smem ? sxb : 0;
+    if (uni) {
+        if (dyn > 48 * 1024)
+            cudaFuncSetAttribute(ipf_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)dyn);
+        ipf_kernel<true><<<(unsigned)batch, PT, dyn, st>>>(
             mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
             col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair,
-            rpc, cpc);
-    else
-        ipf_kernel<false><<<(unsigned)batch, PT, 0, st>>>(
+            rpc, cpc, use_smem);
+    } else {
+        if (dyn > 48 * 1024)
+            cudaFuncSetAttribute(ipf_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)dyn);
+        ipf_kernel<false><<<(unsigned)batch, PT, dyn, st>>>(
             mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
             col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair,
-            rpc, cpc);
+            rpc, cpc, use_smem);
+    }
     const int closed = uni && p == 2.0;
     dim3 gtv((unsigned)L.tv_ctas, (unsigned)batch), gpr((unsigned)L.pr_ctas, (unsigned)batch);
     if (uni) {
