@@ -120,6 +120,9 @@ int gdt_weighted_cost(const double *mu, const double *nu, const double *mu_c,
  *   max_iter      sweep cap (>= 1)
  *   cost_table    [max_sq+1] rho^p by integer squared distance for pricing
  *                 (required when p is neither 1 nor 2, else may be NULL)
+ *   mode          GDT_MODE_EXACT: IPF in the reference's order, fp64 pricing
+ *                 costs; GDT_MODE_FAST: same IPF, p = 1 pricing costs from
+ *                 fp32 sqrt (transport term within ~1e-7)
  *   out           [batch, 8]: {transport_p, tv_inner_mu, tv_inner_nu,
  *                 marginal_gap, iterations, converged, support_count, spare}
  *                 where transport_p = sum fitted*cost (before ^(1/p)) and
@@ -135,7 +138,7 @@ int gdt_primal_upscale(const double *mu, const double *nu, const int64_t *arc_of
                        const double *kernel_w, int kernel_uniform, const double *xi,
                        int64_t max_iter, double p, int64_t batch, int ndim,
                        const int64_t *dims, int kappa, const double *cost_table,
-                       int64_t max_sq, double *out, int32_t *status, void *scratch,
+                       int64_t max_sq, int mode, double *out, int32_t *status, void *scratch,
                        void *stream);
 
 /* Generic IPF on an explicit CSR kernel (rows = sources) with its CSC twin;

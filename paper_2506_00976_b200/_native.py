@@ -31,7 +31,7 @@ _SIGNATURES = {
     "gdt_weighted_cost": (I32, [P, P, P, P, P, P, I64, P, P, I64, I32, P, I32, D, I32, P]),
     "gdt_primal_scratch_bytes": (I64, [I64, I32, P, I32, I32]),
     "gdt_primal_upscale": (I32, [P, P, P, P, P, P, P, P, P, P, I32, P, I64, D, I64, I32, P, I32,
-                                 P, I64, P, P, P, P]),
+                                 P, I64, I32, P, P, P, P]),
     "gdt_ipf_csr": (I32, [P, P, P, P, P, P, P, P, I64, I64, D, I64, P, P, P, P, P, P, P]),
     "gdt_price_coo": (I32, [P, P, P, I64, P, P, P, I64, D, I32, P, P, P]),
     "gdt_weighted_tv_inner": (I32, [P, P, I64, I32, P, D, P, P, P]),

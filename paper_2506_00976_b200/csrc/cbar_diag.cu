@@ -57,7 +57,6 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
     constexpr int OFF = (((KR - 1) * KAPPA + R - 1) / R) * R;
     constexpr int G = ND == 1 ? 1 : (ND == 2 ? KAPPA : KAPPA * KAPPA);  // rows per block-row
     constexpr int KP = KR / 2;
-    constexpr int SPAN = (KR - 1) * KAPPA + R;
     constexpr int PER = KAPPA < R ? KAPPA : R;  // columns of one block inside a window
     const int n = (int)c.cells, N0 = (int)f.n[0], n0 = (int)c.n[0];
     const int64_t N = f.cells;
@@ -193,12 +192,7 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
         int64_t rowbase = 0;
 #pragma unroll
         for (int a = 1; a < ND; ++a) rowbase += (int64_t)chc[a] * f.stride[a];
-        float nv[SPAN];
-#pragma unroll
-        for (int q = 0; q < SPAN; ++q) {
-            const int col = c0 + q;
-            nv[q] = (active && col >= 0 && col < N0) ? (float)nub[rowbase + col] : 0.f;
-        }
+        const double *nrow = nub + rowbase;
 #pragma unroll
         for (int jp = 0; jp < KP; ++jp) {
 #pragma unroll
@@ -206,18 +200,20 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
                 const int j = 2 * jp + h;
 #pragma unroll
                 for (int g = 0; g < R / PER; ++g) {
+                    const int cs = c0 + j * KAPPA + g * PER;
+                    const bool colok = active && cs >= 0 && cs < N0;
                     float s = 0.f;
 #pragma unroll
                     for (int r = g * PER; r < (g + 1) * PER; ++r) {
                         const unsigned long long a2 = acc[jp][r];
                         const float gv =
                             __uint_as_float((unsigned)(h ? (a2 >> 32) : (a2 & 0xffffffffu)));
-                        s = fmaf(nv[j * KAPPA + r], gv, s);
+                        const float nvv = colok ? (float)__ldg(nrow + cs + (r - g * PER)) : 0.f;
+                        s = fmaf(nvv, gv, s);
                     }
 #pragma unroll
                     for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
-                    const int cs = c0 + j * KAPPA + g * PER;
-                    if (rr == 0 && active && j < kr_valid && cs >= 0 && cs < N0) {
+                    if (rr == 0 && colok && j < kr_valid) {
                         const int k = k_hi * n0 + kx0 + j;
                         const int l = lb * n0 + cs / KAPPA;
                         const double denom = __dmul_rn(mu_c[b * n + k], nu_c[b * n + l]);

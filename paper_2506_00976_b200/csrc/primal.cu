@@ -452,6 +452,12 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     }
 }
 
+__device__ __forceinline__ float sqrt_apx32(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ double tv_weight(int i, const G32 &f, double p) {
     double parts[GDT_MAX_DIM];
     for (int a = f.nd - 1; a >= 0; --a) {
@@ -548,7 +554,7 @@ __global__ void __launch_bounds__(MT) price_kernel(
     const double *__restrict__ W, const double *__restrict__ out, const int32_t *__restrict__ status,
     const double *__restrict__ scratch, int64_t stride_pair, const double *__restrict__ mom,
     double *__restrict__ part, G32 f, G32 c, int kappa, double p, const double *__restrict__ table,
-    int closed_form) {
+    int closed_form, int fast) {
     __shared__ double sh[32];
     const int64_t b = blockIdx.y;
     const int N = f.cells, n = c.cells;
@@ -625,7 +631,11 @@ __global__ void __launch_bounds__(MT) price_kernel(
                     }
                     const double coef = UNIFORM ? am : __dmul_rn(mass, W[t * m + s]);
                     const double fitted = __dmul_rn(__dmul_rn(ai, coef), bv[j]);
-                    acc += fitted * (p == 2.0 ? (double)sq : __ldg(table + sq));
+                    double cost;
+                    if (p == 2.0) cost = (double)sq;
+                    else if (fast && p == 1.0) cost = (double)sqrt_apx32((float)sq);
+                    else cost = __ldg(table + sq);
+                    acc += fitted * cost;
                 });
             }
         }
@@ -818,8 +828,8 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
                                   const double *kernel_w, int kernel_uniform, const double *xi,
                                   int64_t max_iter, double p, int64_t batch, int ndim,
                                   const int64_t *dims, int kappa, const double *cost_table,
-                                  int64_t max_sq, double *out, int32_t *status, void *scratch,
-                                  void *stream) {
+                                  int64_t max_sq, int mode, double *out, int32_t *status,
+                                  void *scratch, void *stream) {
     Grid f, c;
     GDT_CHECK_ARG(make_grid(f, ndim, dims) && make_coarse(c, f, kappa),
                   "gdt_primal_upscale: dims must be positive multiples of kappa");
@@ -873,7 +883,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         price_kernel<true><<<gpr, MT, 0, st>>>(arc_off, row_ptr, row_arc_col, row_arc_mass,
                                                kernel_w, out, status, ws, L.stride_pair,
                                                ws + L.mom_off, ws + L.pr_off, f32, c32, kappa, p,
-                                               cost_table, closed);
+                                               cost_table, closed, mode == GDT_MODE_FAST);
     } else {
         moments_tv_kernel<false><<<gtv, MT, 0, st>>>(mu, nu, out, status, ws, L.stride_pair,
                                                      ws + L.mom_off, ws + L.tv_off, f32, c32,
@@ -881,7 +891,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         price_kernel<false><<<gpr, MT, 0, st>>>(arc_off, row_ptr, row_arc_col, row_arc_mass,
                                                 kernel_w, out, status, ws, L.stride_pair,
                                                 ws + L.mom_off, ws + L.pr_off, f32, c32, kappa, p,
-                                                cost_table, 0);
+                                                cost_table, 0, mode == GDT_MODE_FAST);
     }
     finish_kernel<<<grid_size(batch, 128), 128, 0, st>>>(ws + L.tv_off, (int)L.tv_ctas,
                                                          ws + L.pr_off, (int)L.pr_ctas, status,

@@ -263,7 +263,8 @@ def launch_primal(bt: _Batch, dp: DevicePlans, max_iter):
         N.ptr(bt.mu_pad), N.ptr(bt.nu_pad), N.ptr(dp.arc_off), N.ptr(dp.row_ptr), N.ptr(dp.rcol),
         N.ptr(dp.rmass), N.ptr(dp.col_ptr), N.ptr(dp.crow), N.ptr(dp.cmass), N.ptr(dp.W),
         int(dp.uniform), N.ptr(dp.xi), int(max_iter), bt.p, bt.B, bt.d, N.i64s(bt.pdims),
-        bt.kappa, N.ptr(bt.table_dev), bt.max_sq, N.ptr(dp.prim_out), N.ptr(dp.prim_status),
+        bt.kappa, N.ptr(bt.table_dev), bt.max_sq, bt.mode, N.ptr(dp.prim_out),
+        N.ptr(dp.prim_status),
         N.ptr(dp.primal_scratch), stream()), "gdt_primal_upscale")
     return dp.prim_out, dp.prim_status
 
@@ -390,6 +391,7 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
     if timings is not None:
         timings["lp"] = plans.lp_seconds
     dp = DevicePlans(bt, plans, paired, xi)
+    t_dp = time.perf_counter()
     res = gpu_stages(bt, dp, methods, max_iter, dual_method)
     prim = None
     if "primal" in res:
@@ -398,8 +400,7 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
     dual = to_host(res["dual"]) if "dual" in res else None
     t2 = time.perf_counter()
     if timings is not None:
-        timings.update(prepare=t0 - t_start, coarse=t1 - t0, gpu=t2 - t1)
-        timings["finish"] = time.perf_counter() - t2
+        timings.update(prepare=t0 - t_start, coarse=t1 - t0, upload=t_dp - t1, gpu=t2 - t_dp)
     wall = (t2 - t_start) / max(bt.B, 1)
     reports = []
     for b in range(bt.B):
@@ -428,6 +429,8 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
                 o, st = prim[0][b], int(prim[1][b])
                 try:
                     if st in (1, 2):
+                        if timings is not None:
+                            timings["ring_fallbacks"] = timings.get("ring_fallbacks", 0) + 1
                         o = _ring_fallback(bt, b, plans, xi, max_iter)
                         st = 0
                     if st == 3:
@@ -444,7 +447,9 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
                 raw = signed_root(dv, bt.p)
                 rep["dual_upscaling"] = BoundReport("dual_upscaling", max(0.0, raw), raw,
                                                     {"dual_value": dv}, wall, None, bt.n)
-        if not return_exceptions:
+        if timings is not None:
+        timings["finish"] = time.perf_counter() - t2
+    if not return_exceptions:
             for v in rep.values():
                 if isinstance(v, Exception):
                     raise v
