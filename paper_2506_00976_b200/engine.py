@@ -447,13 +447,13 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
                 raw = signed_root(dv, bt.p)
                 rep["dual_upscaling"] = BoundReport("dual_upscaling", max(0.0, raw), raw,
                                                     {"dual_value": dv}, wall, None, bt.n)
-        if timings is not None:
-        timings["finish"] = time.perf_counter() - t2
-    if not return_exceptions:
+        if not return_exceptions:
             for v in rep.values():
                 if isinstance(v, Exception):
                     raise v
         reports.append(rep)
+    if timings is not None:
+        timings["finish"] = time.perf_counter() - t2
     return reports
 
 
