@@ -196,8 +196,10 @@ def run_b200(args):
     from paper_2506_00976_b200 import synthetic as S
     from paper_2506_00976_b200.device import stream, to_dev
 
+    global CFG
+    CFG = args.config
     wl = S.WORKLOADS[CFG]
-    ppr = args.pairs or wl.pairs
+    ppr = args.pairs or (45 if CFG == 4 else wl.pairs)  # cfg4: 360 pairs = 45 per GPU x 8
     lo = rank * ppr
     mus_h, nus_h = S.batch(CFG, lo, lo + ppr)
     dims = wl.dims
@@ -309,7 +311,7 @@ def run_b200(args):
         rl = {"bound": "fp32", "kernel": f"cbar_toeplitz_kernel (fp32 C-bar, kappa={dk}, p={dpow:g})"}
     else:
         flops = None
-        rl = {"bound": "hbm", "kernel": dname}
+        rl = None
     if flops is not None:
         achieved = flops / (dms / 1000.0) / 1e12
         rl.update({"achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
@@ -333,13 +335,37 @@ def run_b200(args):
                 "sweeps": sweeps,
                 "work": "(48*S + 32) * N^2 bytes per pair (SURVEY.md 8(d)), L2-resident at 45 pairs"}
 
+    ct_roofs = {}
+    for (k, p_, nm), v in stage_ms.items():
+        if nm in ("ct_target", "ct_source") and p_ != 2.0:
+            eff = 2.0 * Nf * Nf * ppr / (v / 1000.0) / 1e12
+            ct_roofs[f"k{k}_p{p_:g}_{nm}"] = round(eff, 3)
+    ct_roof = None
+    if ct_roofs:
+        best = max(ct_roofs.values())
+        ct_roof = {"bound": "fp32", "kernel": "pruned_ct_kernel (fp32, p != 2)",
+                   "achieved": best, "peak": fp32_peak, "unit": "TFLOP/s",
+                   "frac": best / fp32_peak, "traffic": None, "per_launch": ct_roofs,
+                   "work": "brute-force count 2*N^4 per transform per pair (the reference's "
+                           "algorithm); tile pruning evaluates a subset exactly, so this is an "
+                           "effective rate"}
+    if rl is None:
+        rl = dict(ipf_roof) if dname == "primal" else {"bound": "hbm", "kernel": dname,
+                                                         "achieved": None, "peak": hbm,
+                                                         "unit": "GB/s", "frac": None,
+                                                         "traffic": None}
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC if CFG == 3 else
+        f"pairs/sec for the four quantization bounds, BASELINE config {CFG} "
+        f"({'x'.join(map(str, dims))}, combos {list(combos)})",
+        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32+f64",
         "data": "synthetic (seeded smooth random fields, BASELINE.json config 3)",
-        "config": {"workload": "cfg3: 45 pairs/GPU of 128x128 smooth random fields; "
-                               "kappa in {4,8} x p in {1,2}; 4 quantization bounds; fp32 mode",
+        "config": {"workload": ("cfg3: 45 pairs/GPU of 128x128 smooth random fields; "
+                                "kappa in {4,8} x p in {1,2}; 4 quantization bounds; fp32 mode")
+                   if CFG == 3 else f"cfg{CFG}: {ppr} pairs/GPU of {wl.kind} on "
+                   f"{'x'.join(map(str, dims))}; {wl.precision} mode; max_iter {wl.max_iter}",
                    "pairs_per_gpu": ppr, "global_pairs": ppr * world, "grid": list(dims),
                    "combos": [list(c) for c in combos],
                    "parallelism": f"dp{world} (pairs sharded, no data-path collective)",
@@ -348,7 +374,7 @@ def run_b200(args):
                    "setup_s": t_setup,
                    "stage_ms": {f"k{k}_p{p:g}_{nm}": round(v, 4)
                                 for (k, p, nm), v in sorted(stage_ms.items())}},
-        "roofline": rl, "roofline_ipf": ipf_roof, "clocks": clk,
+        "roofline": rl, "roofline_ipf": ipf_roof, "roofline_ctransform": ct_roof, "clocks": clk,
         "gpu_launches": launches_per_step * args.steps,
     }
 
@@ -412,7 +438,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    ap.add_argument("--pairs", type=int, default=0, help="pairs per GPU (default 45)")
+    ap.add_argument("--pairs", type=int, default=0, help="pairs per GPU (default: the config's)")
+    ap.add_argument("--config", type=int, default=3, choices=(1, 2, 3, 4, 5),
+                    help="BASELINE.json config (3 = the headline 128x128 workload)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
     const float *__restrict__ tab, int tab_max, double *__restrict__ out,
     uint8_t *__restrict__ unused, Grid f, Grid c, int nb_per_pass) {
     static_assert(KR % 2 == 0, "blocks are paired in FFMA2 lanes");
-    extern __shared__ unsigned long long mus2[];  // [(th*KP + jp)*KAPPA + tx]
+    extern __shared__ unsigned long long mus2[];  // [(th*KP + jp)*KAPPA + tx], then numer
     constexpr int R = DG_R;
     constexpr int NCD = KAPPA + R - 1;
     constexpr int OFF = (((KR - 1) * KAPPA + R - 1) / R) * R;
@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
     const int n = (int)c.cells, N0 = (int)f.n[0], n0 = (int)c.n[0];
     const int64_t N = f.cells;
     const int nthreads = blockDim.x;
+    float *snum = reinterpret_cast<float *>(mus2 + G * KP * KAPPA);  // [KR][n] block numerators
 
     const int64_t b = blockIdx.y;
     const int tiles_x = (n0 + KR - 1) / KR;
@@ -213,18 +214,22 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
                     }
 #pragma unroll
                     for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
-                    if (rr == 0 && colok && j < kr_valid) {
-                        const int k = k_hi * n0 + kx0 + j;
-                        const int l = lb * n0 + cs / KAPPA;
-                        const double denom = __dmul_rn(mu_c[b * n + k], nu_c[b * n + l]);
-                        const int64_t oi = ((int64_t)b * n + k) * n + l;
-                        const bool un = denom == 0.0;
-                        out[oi] = un ? Ccentre[(int64_t)k * n + l] : (double)s / denom;
-                        unused[oi] = un ? 1 : 0;
-                    }
+                    if (rr == 0 && colok && j < kr_valid)
+                        snum[j * n + lb * n0 + cs / KAPPA] = s;  // unique writer per entry
                 }
             }
         }
+    }
+    __syncthreads();
+    // coalesced row writes of C-bar = numer / (mu~ nu~) (centre cost where 0)
+    for (int i = threadIdx.x; i < kr_valid * n; i += nthreads) {
+        const int j = i / n, l = i - j * n;
+        const int k = k_hi * n0 + kx0 + j;
+        const double denom = __dmul_rn(mu_c[b * n + k], nu_c[b * n + l]);
+        const int64_t oi = ((int64_t)b * n + k) * n + l;
+        const bool un = denom == 0.0;
+        out[oi] = un ? Ccentre[(int64_t)k * n + l] : (double)snum[i] / denom;
+        unused[oi] = un ? 1 : 0;
     }
 }
 
@@ -257,7 +262,9 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
     const int threads = ((Gr * segs * nb + 31) / 32) * 32;
     if (threads > DG_MAX_THREADS) return GDT_ERR_UNSUPPORTED;
     const int64_t n = c.cells;
-    const size_t bytes = sizeof(unsigned long long) * Gr * (KR / 2) * KAPPA;
+    const size_t bytes = sizeof(unsigned long long) * Gr * (KR / 2) * KAPPA +
+                         sizeof(float) * KR * n;
+    if (bytes > 100 * 1024) return GDT_ERR_UNSUPPORTED;
     float *ftab = nullptr;
     int tab_max = 0;
     if (!p1) {
@@ -271,6 +278,8 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
     const int64_t tiles_x = (c.n[0] + KR - 1) / KR;
     dim3 grid((unsigned)(tiles_x * (n / c.n[0])), (unsigned)batch);
     auto run = [&](auto kern) {
+        if (bytes > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         kern<<<grid, threads, bytes, st>>>(mu, nu, mu_c, nu_c, Ccentre, ftab, tab_max, out, unused,
                                            f, c, nb);
     };

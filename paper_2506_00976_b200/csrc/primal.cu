@@ -278,6 +278,7 @@ __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c,
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kb[u] = acc;
+    if (UNIFORM) return;  // cells handled by cell_pass_row (all threads, all cells)
     const double rcp = acc > 0.0 ? __drcp_rn(acc) : 0.0;
     const int origin = block_origin(k, c, f, kappa);
     for_block_cells(origin, f, kappa, [&](int tt, int i) {
@@ -312,6 +313,7 @@ __device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c,
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kta[u] = acc;
+    if (UNIFORM) return;  // cells handled by cell_pass_col
     const double rcp = acc > 0.0 ? __drcp_rn(acc) : 0.0;
     const int origin = block_origin(l, c, f, kappa);
     for_block_cells(origin, f, kappa, [&](int ss, int j) {
@@ -326,6 +328,60 @@ __device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c,
         }
         P.b[j] = bj;
     });
+}
+
+// coarse block of fine cell i
+__device__ __forceinline__ int block_of(int i, const G32 &f, const G32 &c, int kappa) {
+    int k = 0;
+    for (int a = f.nd - 1; a >= 0; --a) {
+        const int x = i / f.stride[a];
+        i -= x * f.stride[a];
+        k += (x / kappa) * c.stride[a];
+    }
+    return k;
+}
+
+// Uniform kernel, phase R cell work spread over every thread: with the
+// block sums kb[] complete, a_next = mu / kb, the gap / range terms of the
+// current a and the zero-row check (same arithmetic as row_unit's cell loop).
+__device__ __forceinline__ void cell_pass_row(const PairPtrs &P, const G32 &c, const G32 &f,
+                                              int kappa, bool init, const double *a_cur,
+                                              double *a_next, Red &r, const double *kbs,
+                                              const double *rcps) {
+    for (int i = threadIdx.x; i < f.cells; i += PT) {
+        const int k = block_of(i, f, c, kappa);
+        const double acc = kbs[k];
+        const double mui = P.mu[i];
+        if (!init) {
+            const double ai = a_cur[i];
+            range_acc(ai, r.amin, r.amax, r.nonfinite);
+            if (mui > 0.0) r.gap += fabs(__dsub_rn(__dmul_rn(ai, acc), mui));
+        }
+        double an = 0.0;
+        if (mui > 0.0) {
+            if (acc <= 0.0) r.zrow = 1;
+            else an = div_shared(mui, acc, rcps[k]);
+        }
+        a_next[i] = an;
+    }
+}
+
+__device__ __forceinline__ void cell_pass_col(const PairPtrs &P, const G32 &c, const G32 &f,
+                                              int kappa, Red &r, const double *ktas,
+                                              const double *rcps) {
+    for (int j = threadIdx.x; j < f.cells; j += PT) {
+        const int l = block_of(j, f, c, kappa);
+        const double acc = ktas[l];
+        const double nuj = P.nu[j];
+        double bj = 0.0;
+        if (nuj > 0.0) {
+            if (acc <= 0.0) r.zcol = 1;
+            else bj = div_shared(nuj, acc, rcps[l]);
+            range_acc(bj, r.bmin, r.bmax, r.nonfinite);
+            r.gap += fabs(__dsub_rn(nuj, __dmul_rn(bj, acc)));
+        }
+        P.b[j] = bj;
+    }
 }
 
 // per-pair scalar record written by ipf_kernel / finish_kernel
@@ -392,9 +448,24 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     // kb = K b0, a = mu / kb (sinkhorn.py:119-129 before the first sweep)
     Red r = red_init();
     double *a_cur = P.aA, *a_nxt = P.aB;
+    // uniform kernel: block sums, then per-block reciprocals, then the cell
+    // work of the pass spread over all threads
+    auto finish_units = [&](const double *sums, double *rcps) {
+        __syncthreads();
+        for (int u = threadIdx.x; u < U; u += PT) {
+            const double v = sums[u];
+            rcps[u] = v > 0.0 ? __drcp_rn(v) : 0.0;
+        }
+        __syncthreads();
+    };
+    double *rcp_buf = P.kta + U;  // scratch after kta (U doubles, see primal_layout)
     const double *bs = stage(P.b);
     for (int u = threadIdx.x; u < U; u += PT)
         row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, true, nullptr, a_cur, r, bs);
+    if (UNIFORM) {
+        finish_units(P.kb, rcp_buf);
+        cell_pass_row(P, c, f, kappa, true, nullptr, a_cur, r, P.kb, rcp_buf);
+    }
     block_reduce_red(r, sh);
     int st = r.zrow ? GDT_PAIR_ZERO_DENOM_ROW : GDT_PAIR_OK;
     int64_t it = 0;
@@ -406,6 +477,10 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
         const double *as = stage(a_cur);
         for (int u = threadIdx.x; u < U; u += PT)
             col_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, a_cur, rc, as);
+        if (UNIFORM) {
+            finish_units(P.kta, rcp_buf);
+            cell_pass_col(P, c, f, kappa, rc, P.kta, rcp_buf);
+        }
         if (__syncthreads_or(rc.zcol)) {  // before anything reads b
             st = GDT_PAIR_ZERO_DENOM_COL;
             break;
@@ -413,6 +488,10 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
         const double *bsw = stage(P.b);
         for (int u = threadIdx.x; u < U; u += PT)
             row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, false, a_cur, a_nxt, rc, bsw);
+        if (UNIFORM) {
+            finish_units(P.kb, rcp_buf);
+            cell_pass_row(P, c, f, kappa, false, a_cur, a_nxt, rc, P.kb, rcp_buf);
+        }
         block_reduce_red(rc, sh);
         // _check_scale_range(a), then (b) (sinkhorn.py:137-138)
         const bool bad_a = rc.amin <= rc.amax &&
@@ -793,7 +872,7 @@ inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, b
                                   bool p2, int64_t max_arcs) {
     PrimalLayout L;
     const int64_t U = uniform ? c.cells : f.cells;
-    L.stride_pair = 3 * f.cells + 2 * U;
+    L.stride_pair = 3 * f.cells + 3 * U;  // aA, aB, b, kb, kta, reciprocals
     L.mom_off = batch * L.stride_pair;
     const int64_t MW = 2 * (f.nd + 2);
     L.tv_ctas = (c.cells + MT - 1) / MT;
