@@ -44,6 +44,33 @@ __device__ __forceinline__ void dg_fma2(unsigned long long &acc, unsigned long l
     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(m2), "l"(dg_pack(c, c)));
 }
 
+// staged nu row length: N0 + 2 OFF, rounded to 4 (mod 32) floats against bank conflicts
+__host__ __device__ __forceinline__ int dg_row_len(int n0, int off) {
+    const int l = n0 + 2 * off;
+    return ((l + 31) / 32) * 32 + 4;
+}
+
+// PER consecutive floats from shared memory, vectorised (cs is a multiple of PER)
+template <int PER>
+__device__ __forceinline__ void dg_load(float *v, const float *src) {
+    if constexpr (PER % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < PER / 4; ++q) {
+            const float4 t = reinterpret_cast<const float4 *>(src)[q];
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+        }
+    } else if constexpr (PER % 2 == 0) {
+#pragma unroll
+        for (int q = 0; q < PER / 2; ++q) {
+            const float2 t = reinterpret_cast<const float2 *>(src)[q];
+            v[2 * q] = t.x; v[2 * q + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) v[q] = src[q];
+    }
+}
+
 template <int KAPPA, int KR, int ND, bool P1>
 __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ mu_c,
@@ -62,6 +89,9 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
     const int64_t N = f.cells;
     const int nthreads = blockDim.x;
     float *snum = reinterpret_cast<float *>(mus2 + G * KP * KAPPA);  // [KR][n] block numerators
+    // nu rows of the current pass, fp32, OFF zero cells either side: [nb][G][NL]
+    const int NL = dg_row_len(N0, OFF);
+    float *nbuf = snum + ((KR * n + 3) & ~3);  // 16-byte aligned
 
     const int64_t b = blockIdx.y;
     const int tiles_x = (n0 + KR - 1) / KR;
@@ -125,7 +155,32 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
     }
     const int n_hi = n / n0;  // coarse block-rows
 
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = nthreads / 32;
     for (int lb0 = 0; lb0 < n_hi; lb0 += nb_per_pass) {
+        // stage this pass's nu rows (one warp per row, coalesced)
+        __syncthreads();
+        for (int row = warp; row < nb_per_pass * G; row += nwarps) {
+            const int slot = row / G, rq = row - slot * G, lbq = lb0 + slot;
+            float *dst = nbuf + row * NL;
+            if (lbq >= n_hi) {
+                for (int x = lane; x < NL; x += 32) dst[x] = 0.f;
+                continue;
+            }
+            int64_t rb = 0;
+            int remb = lbq, remr = rq;
+#pragma unroll
+            for (int a = 1; a < ND; ++a) {
+                const int la = remb % (int)c.n[a], ta = remr % KAPPA;
+                remb /= (int)c.n[a];
+                remr /= KAPPA;
+                rb += (int64_t)(la * KAPPA + ta) * f.stride[a];
+            }
+            for (int x = lane; x < NL; x += 32) {
+                const int cx = x - OFF;
+                dst[x] = cx >= 0 && cx < N0 ? (float)nub[rb + cx] : 0.f;
+            }
+        }
+        __syncthreads();
         const int lb = lb0 + gblk;  // coarse block-row (flat over the higher axes)
         const bool active = lb < n_hi && gblk < nb_per_pass;
         int chc[GDT_MAX_DIM] = {0, 0, 0, 0};  // fine higher coordinates of this lane's row
@@ -190,10 +245,7 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
         }
         // fold: this lane's row of every (k+j, l) it covers, then the G rows of the
         // block-row in the lane group; the leader writes C-bar
-        int64_t rowbase = 0;
-#pragma unroll
-        for (int a = 1; a < ND; ++a) rowbase += (int64_t)chc[a] * f.stride[a];
-        const double *nrow = nub + rowbase;
+        const float *nrow = nbuf + (gblk * G + rr) * NL + OFF;  // zero outside the grid
 #pragma unroll
         for (int jp = 0; jp < KP; ++jp) {
 #pragma unroll
@@ -203,14 +255,18 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
                 for (int g = 0; g < R / PER; ++g) {
                     const int cs = c0 + j * KAPPA + g * PER;
                     const bool colok = active && cs >= 0 && cs < N0;
+                    float nv[PER];
+                    if (active) dg_load<PER>(nv, nrow + cs);
+                    else
+#pragma unroll
+                        for (int r = 0; r < PER; ++r) nv[r] = 0.f;
                     float s = 0.f;
 #pragma unroll
                     for (int r = g * PER; r < (g + 1) * PER; ++r) {
                         const unsigned long long a2 = acc[jp][r];
                         const float gv =
                             __uint_as_float((unsigned)(h ? (a2 >> 32) : (a2 & 0xffffffffu)));
-                        const float nvv = colok ? (float)__ldg(nrow + cs + (r - g * PER)) : 0.f;
-                        s = fmaf(nvv, gv, s);
+                        s = fmaf(nv[r - g * PER], gv, s);
                     }
 #pragma unroll
                     for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
@@ -263,7 +319,8 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
     if (threads > DG_MAX_THREADS) return GDT_ERR_UNSUPPORTED;
     const int64_t n = c.cells;
     const size_t bytes = sizeof(unsigned long long) * Gr * (KR / 2) * KAPPA +
-                         sizeof(float) * KR * n;
+                         sizeof(float) * ((KR * n + 3) & ~3) +
+                         sizeof(float) * nb * Gr * dg_row_len((int)f.n[0], OFF);
     if (bytes > 100 * 1024) return GDT_ERR_UNSUPPORTED;
     float *ftab = nullptr;
     int tab_max = 0;

@@ -341,15 +341,20 @@ __device__ __forceinline__ int block_of(int i, const G32 &f, const G32 &c, int k
     return k;
 }
 
+__global__ void block_map_kernel(G32 f, G32 c, int kappa, int32_t *__restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < f.cells; i += gridDim.x * blockDim.x)
+        out[i] = block_of(i, f, c, kappa);
+}
+
 // Uniform kernel, phase R cell work spread over every thread: with the
 // block sums kb[] complete, a_next = mu / kb, the gap / range terms of the
 // current a and the zero-row check (same arithmetic as row_unit's cell loop).
-__device__ __forceinline__ void cell_pass_row(const PairPtrs &P, const G32 &c, const G32 &f,
-                                              int kappa, bool init, const double *a_cur,
+__device__ __forceinline__ void cell_pass_row(const PairPtrs &P, const G32 &f,
+                                              const int32_t *__restrict__ bmap, bool init, const double *a_cur,
                                               double *a_next, Red &r, const double *kbs,
                                               const double *rcps) {
     for (int i = threadIdx.x; i < f.cells; i += PT) {
-        const int k = block_of(i, f, c, kappa);
+        const int k = bmap[i];
         const double acc = kbs[k];
         const double mui = P.mu[i];
         if (!init) {
@@ -366,11 +371,11 @@ __device__ __forceinline__ void cell_pass_row(const PairPtrs &P, const G32 &c, c
     }
 }
 
-__device__ __forceinline__ void cell_pass_col(const PairPtrs &P, const G32 &c, const G32 &f,
-                                              int kappa, Red &r, const double *ktas,
+__device__ __forceinline__ void cell_pass_col(const PairPtrs &P, const G32 &f,
+                                              const int32_t *__restrict__ bmap, Red &r, const double *ktas,
                                               const double *rcps) {
     for (int j = threadIdx.x; j < f.cells; j += PT) {
-        const int l = block_of(j, f, c, kappa);
+        const int l = bmap[j];
         const double acc = ktas[l];
         const double nuj = P.nu[j];
         double bj = 0.0;
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     const double *__restrict__ W, const double *__restrict__ xi_in, int64_t max_iter, G32 f,
     G32 c, int kappa, double *__restrict__ out, int32_t *__restrict__ status,
     double *__restrict__ scratch, int64_t stride_pair, const int64_t *__restrict__ rpc,
-    const int64_t *__restrict__ cpc, int use_smem) {
+    const int64_t *__restrict__ cpc, int use_smem, const int32_t *__restrict__ bmap) {
     __shared__ double sh[(PT / 32) * 6];
     const int64_t b = blockIdx.x;
     const int N = f.cells, n = c.cells;
@@ -464,7 +469,7 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
         row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, true, nullptr, a_cur, r, bs);
     if (UNIFORM) {
         finish_units(P.kb, rcp_buf);
-        cell_pass_row(P, c, f, kappa, true, nullptr, a_cur, r, P.kb, rcp_buf);
+        cell_pass_row(P, f, bmap, true, nullptr, a_cur, r, P.kb, rcp_buf);
     }
     block_reduce_red(r, sh);
     int st = r.zrow ? GDT_PAIR_ZERO_DENOM_ROW : GDT_PAIR_OK;
@@ -479,7 +484,7 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
             col_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, a_cur, rc, as);
         if (UNIFORM) {
             finish_units(P.kta, rcp_buf);
-            cell_pass_col(P, c, f, kappa, rc, P.kta, rcp_buf);
+            cell_pass_col(P, f, bmap, rc, P.kta, rcp_buf);
         }
         if (__syncthreads_or(rc.zcol)) {  // before anything reads b
             st = GDT_PAIR_ZERO_DENOM_COL;
@@ -490,7 +495,7 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
             row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, false, a_cur, a_nxt, rc, bsw);
         if (UNIFORM) {
             finish_units(P.kb, rcp_buf);
-            cell_pass_row(P, c, f, kappa, false, a_cur, a_nxt, rc, P.kb, rcp_buf);
+            cell_pass_row(P, f, bmap, false, a_cur, a_nxt, rc, P.kb, rcp_buf);
         }
         block_reduce_red(rc, sh);
         // _check_scale_range(a), then (b) (sinkhorn.py:137-138)
@@ -865,7 +870,7 @@ __global__ void sum_parts_kernel(const double *__restrict__ part, int count, dou
 // pairs: moments [B, n, MW], tv partials [B, tv_ctas, 2], price partials
 // [B, pr_ctas]
 struct PrimalLayout {
-    int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, total, tv_ctas, pr_ctas;
+    int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, bm_off, total, tv_ctas, pr_ctas;
 };
 
 inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, bool uniform,
@@ -882,7 +887,8 @@ inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, b
     L.tv_off = L.mom_off + batch * c.cells * MW;
     L.pr_off = L.tv_off + batch * L.tv_ctas * 2;
     L.pc_off = L.pr_off + batch * L.pr_ctas;       // packed arc coordinates (int64)
-    L.total = L.pc_off + 2 * batch * max_arcs;
+    L.bm_off = L.pc_off + 2 * batch * max_arcs;    // fine cell -> coarse block (int32)
+    L.total = L.bm_off + (f.cells + 1) / 2;
     return L;
 }
 
@@ -933,6 +939,8 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
                                                                          per_pair, batch, c32, rpc);
     pack_coords_kernel<<<grid_size(batch * per_pair, 256), 256, 0, st>>>(col_arc_row, arc_off,
                                                                          per_pair, batch, c32, cpc);
+    int32_t *bmap = reinterpret_cast<int32_t *>(ws + L.bm_off);
+    if (uni) block_map_kernel<<<grid_size(f.cells, 256), 256, 0, st>>>(f32, c32, kappa, bmap);
     const size_t sxb = sizeof(double) * f.cells;
     const int use_smem = sxb <= 160 * 1024;
     const size_t dyn = use_smem ? sxb : 0;
@@ -943,7 +951,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         ipf_kernel<true><<<(unsigned)batch, PT, dyn, st>>>(
             mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
             col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair,
-            rpc, cpc, use_smem);
+            rpc, cpc, use_smem, bmap);
     } else {
         if (dyn > 48 * 1024)
             cudaFuncSetAttribute(ipf_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -951,7 +959,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         ipf_kernel<false><<<(unsigned)batch, PT, dyn, st>>>(
             mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
             col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair,
-            rpc, cpc, use_smem);
+            rpc, cpc, use_smem, nullptr);
     }
     const int closed = uni && p == 2.0;
     dim3 gtv((unsigned)L.tv_ctas, (unsigned)batch), gpr((unsigned)L.pr_ctas, (unsigned)batch);
