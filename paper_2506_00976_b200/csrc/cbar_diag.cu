@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ mu_c,
     const double *__restrict__ nu_c, const double *__restrict__ Ccentre,
     const float *__restrict__ tab, int tab_max, double *__restrict__ out,
-    uint8_t *__restrict__ unused, Grid f, Grid c, int nb_per_pass) {
+    uint8_t *__restrict__ unused, Grid f, Grid c, int nb_per_pass, int stage_all) {
     static_assert(KR % 2 == 0, "blocks are paired in FFMA2 lanes");
     extern __shared__ unsigned long long mus2[];  // [(th*KP + jp)*KAPPA + tx], then numer
     constexpr int R = DG_R;
@@ -156,10 +156,10 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
     const int n_hi = n / n0;  // coarse block-rows
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = nthreads / 32;
-    for (int lb0 = 0; lb0 < n_hi; lb0 += nb_per_pass) {
-        // stage this pass's nu rows (one warp per row, coalesced)
-        __syncthreads();
-        for (int row = warp; row < nb_per_pass * G; row += nwarps) {
+    // nu rows (fp32, one warp per row, coalesced): all of them once when they
+    // fit (stage_all), else the rows of each pass
+    auto stage_rows = [&](int lb0, int nrows) {
+        for (int row = warp; row < nrows * G; row += nwarps) {
             const int slot = row / G, rq = row - slot * G, lbq = lb0 + slot;
             float *dst = nbuf + row * NL;
             if (lbq >= n_hi) {
@@ -180,7 +180,17 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
                 dst[x] = cx >= 0 && cx < N0 ? (float)nub[rb + cx] : 0.f;
             }
         }
+    };
+    if (stage_all) {
+        stage_rows(0, n_hi);
         __syncthreads();
+    }
+    for (int lb0 = 0; lb0 < n_hi; lb0 += nb_per_pass) {
+        if (!stage_all) {
+            __syncthreads();
+            stage_rows(lb0, nb_per_pass);
+            __syncthreads();
+        }
         const int lb = lb0 + gblk;  // coarse block-row (flat over the higher axes)
         const bool active = lb < n_hi && gblk < nb_per_pass;
         int chc[GDT_MAX_DIM] = {0, 0, 0, 0};  // fine higher coordinates of this lane's row
@@ -245,33 +255,37 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
         }
         // fold: this lane's row of every (k+j, l) it covers, then the G rows of the
         // block-row in the lane group; the leader writes C-bar
-        const float *nrow = nbuf + (gblk * G + rr) * NL + OFF;  // zero outside the grid
+        const float *nrow = nbuf + ((stage_all ? lb : gblk) * G + rr) * NL + OFF;  // zero outside the grid
 #pragma unroll
         for (int jp = 0; jp < KP; ++jp) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int j = 2 * jp + h;
+            for (int g = 0; g < R / PER; ++g) {
+                // blocks 2jp, 2jp+1 share the FFMA2 lanes: s2 = sum_r acc * (nu_A, nu_B)
+                const int csA = c0 + 2 * jp * KAPPA + g * PER, csB = csA + KAPPA;
+                float nvA[PER], nvB[PER];
+                if (active) {
+                    dg_load<PER>(nvA, nrow + csA);
+                    dg_load<PER>(nvB, nrow + csB);
+                } else {
 #pragma unroll
-                for (int g = 0; g < R / PER; ++g) {
-                    const int cs = c0 + j * KAPPA + g * PER;
-                    const bool colok = active && cs >= 0 && cs < N0;
-                    float nv[PER];
-                    if (active) dg_load<PER>(nv, nrow + cs);
-                    else
+                    for (int r = 0; r < PER; ++r) nvA[r] = nvB[r] = 0.f;
+                }
+                unsigned long long s2 = 0ull;
 #pragma unroll
-                        for (int r = 0; r < PER; ++r) nv[r] = 0.f;
-                    float s = 0.f;
+                for (int r = g * PER; r < (g + 1) * PER; ++r)
+                    asm("fma.rn.f32x2 %0, %1, %2, %0;"
+                        : "+l"(s2)
+                        : "l"(acc[jp][r]), "l"(dg_pack(nvA[r - g * PER], nvB[r - g * PER])));
+                float sv[2] = {__uint_as_float((unsigned)(s2 & 0xffffffffu)),
+                               __uint_as_float((unsigned)(s2 >> 32))};
 #pragma unroll
-                    for (int r = g * PER; r < (g + 1) * PER; ++r) {
-                        const unsigned long long a2 = acc[jp][r];
-                        const float gv =
-                            __uint_as_float((unsigned)(h ? (a2 >> 32) : (a2 & 0xffffffffu)));
-                        s = fmaf(nv[r - g * PER], gv, s);
-                    }
+                for (int h = 0; h < 2; ++h) {
+                    const int j = 2 * jp + h, cs = h ? csB : csA;
+                    float sh = sv[h];
 #pragma unroll
-                    for (int o = 1; o < G; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
-                    if (rr == 0 && colok && j < kr_valid)
-                        snum[j * n + lb * n0 + cs / KAPPA] = s;  // unique writer per entry
+                    for (int o = 1; o < G; o <<= 1) sh += __shfl_xor_sync(0xffffffffu, sh, o, G);
+                    if (rr == 0 && active && cs >= 0 && cs < N0 && j < kr_valid)
+                        snum[j * n + lb * n0 + cs / KAPPA] = sh;  // unique writer per entry
                 }
             }
         }
@@ -318,9 +332,12 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
     const int threads = ((Gr * segs * nb + 31) / 32) * 32;
     if (threads > DG_MAX_THREADS) return GDT_ERR_UNSUPPORTED;
     const int64_t n = c.cells;
-    const size_t bytes = sizeof(unsigned long long) * Gr * (KR / 2) * KAPPA +
-                         sizeof(float) * ((KR * n + 3) & ~3) +
-                         sizeof(float) * nb * Gr * dg_row_len((int)f.n[0], OFF);
+    const size_t fixed = sizeof(unsigned long long) * Gr * (KR / 2) * KAPPA +
+                         sizeof(float) * ((KR * n + 3) & ~3);
+    const size_t row_bytes = sizeof(float) * dg_row_len((int)f.n[0], OFF);
+    const int64_t n_hi = n / c.n[0];
+    const int stage_all = fixed + row_bytes * Gr * n_hi <= 100 * 1024;
+    const size_t bytes = fixed + row_bytes * Gr * (stage_all ? n_hi : nb);
     if (bytes > 100 * 1024) return GDT_ERR_UNSUPPORTED;
     float *ftab = nullptr;
     int tab_max = 0;
@@ -338,7 +355,7 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
         if (bytes > 48 * 1024)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         kern<<<grid, threads, bytes, st>>>(mu, nu, mu_c, nu_c, Ccentre, ftab, tab_max, out, unused,
-                                           f, c, nb);
+                                           f, c, nb, stage_all);
     };
     switch (f.nd * 2 + (p1 ? 1 : 0)) {
         case 2: run(cbar_diag_kernel<KAPPA, KR, 1, false>); break;

@@ -145,7 +145,49 @@ double run_min_scalar(const double *cs, const double *vs, int64_t len, double ui
     return mm;
 }
 
+// ---- first index attaining a known block minimum --------------------------
+// The reference's strict-< scan over a block ends on the FIRST arc whose
+// reduced cost equals the block minimum; given that minimum (computed with the
+// same arithmetic), an equality search finds the same arc.
+
+__attribute__((target("avx512f"))) int64_t run_find_avx512(const double *cs, const double *vs,
+                                                           int64_t len, double ui, double m) {
+    const __m512d uu = _mm512_set1_pd(ui), mm = _mm512_set1_pd(m);
+    int64_t t = 0;
+    for (; t + 8 <= len; t += 8) {
+        const __m512d r = _mm512_sub_pd(_mm512_sub_pd(_mm512_loadu_pd(cs + t), uu),
+                                        _mm512_loadu_pd(vs + t));
+        const __mmask8 hit = _mm512_cmp_pd_mask(r, mm, _CMP_EQ_OQ);
+        if (hit) return t + __builtin_ctz((unsigned)hit);
+    }
+    for (; t < len; ++t)
+        if ((cs[t] - ui) - vs[t] == m) return t;
+    return -1;
+}
+
+int64_t run_find_scalar(const double *cs, const double *vs, int64_t len, double ui, double m) {
+    for (int64_t t = 0; t < len; ++t)
+        if ((cs[t] - ui) - vs[t] == m) return t;
+    return -1;
+}
+
 // ---- the solver -----------------------------------------------------------
+//
+// Tree storage is compact (int32 links, one 24-byte record per basis slot,
+// one 16-byte record per node, potentials u|v in one array) so the subtree
+// relabel after each pivot -- half of the pivot cost -- stays in L1/L2.
+// Per-node adjacency lists are singly linked (rows through `rn`, columns
+// through `cn`); unlinking walks the short list from its head.
+
+struct Slot {
+    int32_t i, j;    // source, sink
+    int32_t rn, cn;  // next slot in the source's / sink's list
+    double ck;       // cost of the arc
+};
+
+struct Node {
+    int32_t par, pslot, dep, head;
+};
 
 template <class Cost>
 struct Solver {
@@ -153,71 +195,82 @@ struct Solver {
     int64_t ns, nt, nb;
     int64_t *bi, *bj;
     double *bf, *u, *v;
-    std::vector<int64_t> rhead, chead, rnext, rprev, cnext, cprev;
-    std::vector<int64_t> par, pslot, dep, stk, pa_s, pb_s;
+    std::vector<Slot> sl;
+    std::vector<Node> nd;
+    std::vector<double> pot;  // u[0, ns) then v[0, nt)
+    std::vector<int32_t> stk, pa_s, pb_s;
     std::vector<int8_t> sa_s, sb_s;
-    std::vector<double> ck;  // cost of the arc held by each basis slot
-    int simd;                // 2 = avx512, 1 = avx2, 0 = scalar
+    int simd;  // 2 = avx512, 1 = avx2, 0 = scalar
 
-    void push(int64_t k) {
-        const int64_t s = bi[k], t = bj[k];
-        rnext[k] = rhead[s];
-        rprev[k] = -1;
-        if (rhead[s] != -1) rprev[rhead[s]] = k;
-        rhead[s] = k;
-        cnext[k] = chead[t];
-        cprev[k] = -1;
-        if (chead[t] != -1) cprev[chead[t]] = k;
-        chead[t] = k;
+    void push(int32_t k) {
+        Slot &e = sl[k];
+        Node &a = nd[e.i], &b = nd[ns + e.j];
+        e.rn = a.head;
+        a.head = k;
+        e.cn = b.head;
+        b.head = k;
     }
 
-    void unlink(int64_t k) {
-        if (rprev[k] != -1) rnext[rprev[k]] = rnext[k];
-        else rhead[bi[k]] = rnext[k];
-        if (rnext[k] != -1) rprev[rnext[k]] = rprev[k];
-        if (cprev[k] != -1) cnext[cprev[k]] = cnext[k];
-        else chead[bj[k]] = cnext[k];
-        if (cnext[k] != -1) cprev[cnext[k]] = cprev[k];
+    void unlink(int32_t k) {
+        const Slot &e = sl[k];
+        int32_t *pp = &nd[e.i].head;
+        while (*pp != k) pp = &sl[*pp].rn;
+        *pp = e.rn;
+        pp = &nd[ns + e.j].head;
+        while (*pp != k) pp = &sl[*pp].cn;
+        *pp = e.cn;
     }
 
-    // DFS labelling below `root`; `subtree` skips the parent slot instead of
+    // Labelling below `root`; `subtree` skips the parent slot instead of
     // testing for unlabelled nodes (full relabel vs. pivot relabel).
-    void label(int64_t root, bool subtree) {
-        int64_t sp = 0;
+    // u[s] = C - v[t] and v[t] = C - u[s] along tree edges (_simplex.py:105-144,
+    // 284-330): every potential is recomputed from its parent.
+    void label(int32_t root, bool subtree) {
+        // breadth-first: the next node's record was written long before it is
+        // processed, so consecutive nodes' loads overlap (a LIFO stack would
+        // serialise on the record just written)
+        int64_t qh = 0, sp = 0;
         stk[sp++] = root;
-        while (sp > 0) {
-            const int64_t node = stk[--sp];
+        double *P = pot.data();
+        while (qh < sp) {
+            const int32_t node = stk[qh++];
+            const Node me = nd[node];
+            const double pn = P[node];
             if (node < ns) {
-                const double un = u[node];
-                for (int64_t k = rhead[node]; k != -1; k = rnext[k]) {
-                    const int64_t t = bj[k];
-                    if (subtree ? k == pslot[node] : par[ns + t] != -2) continue;
-                    v[t] = ck[k] - un;
-                    par[ns + t] = node;
-                    pslot[ns + t] = k;
-                    dep[ns + t] = dep[node] + 1;
-                    stk[sp++] = ns + t;
+                for (int32_t k = me.head; k != -1;) {
+                    const Slot &e = sl[k];
+                    const int32_t w = (int32_t)ns + e.j;
+                    if (subtree ? k != me.pslot : nd[w].par == -2) {
+                        P[w] = e.ck - pn;
+                        nd[w].par = node;
+                        nd[w].pslot = k;
+                        nd[w].dep = me.dep + 1;
+                        stk[sp++] = w;
+                    }
+                    k = e.rn;
                 }
             } else {
-                const int64_t t = node - ns;
-                const double vt = v[t];
-                for (int64_t k = chead[t]; k != -1; k = cnext[k]) {
-                    const int64_t s = bi[k];
-                    if (subtree ? k == pslot[node] : par[s] != -2) continue;
-                    u[s] = ck[k] - vt;
-                    par[s] = node;
-                    pslot[s] = k;
-                    dep[s] = dep[node] + 1;
-                    stk[sp++] = s;
+                for (int32_t k = me.head; k != -1;) {
+                    const Slot &e = sl[k];
+                    const int32_t w = e.i;
+                    if (subtree ? k != me.pslot : nd[w].par == -2) {
+                        P[w] = e.ck - pn;
+                        nd[w].par = node;
+                        nd[w].pslot = k;
+                        nd[w].dep = me.dep + 1;
+                        stk[sp++] = w;
+                    }
+                    k = e.cn;
                 }
             }
         }
     }
 
     double run_min(const double *cs, int64_t j, int64_t len, double ui, double m) const {
-        if (simd == 2) return run_min_avx512(cs, v + j, len, ui, m);
-        if (simd == 1) return run_min_avx2(cs, v + j, len, ui, m);
-        return run_min_scalar(cs, v + j, len, ui, m);
+        const double *v_ = pot.data() + ns;
+        if (simd == 2) return run_min_avx512(cs, v_ + j, len, ui, m);
+        if (simd == 1) return run_min_avx2(cs, v_ + j, len, ui, m);
+        return run_min_scalar(cs, v_ + j, len, ui, m);
     }
 
     // exact min of (C - u) - v over arcs [a, hi)
@@ -226,7 +279,7 @@ struct Solver {
         int64_t i = a / nt, j = a - i * nt;
         while (a < hi) {
             const int64_t j1 = std::min<int64_t>(nt, j + (hi - a));
-            const double ui = u[i];
+            const double ui = pot[i];
             cost.runs(i, j, j1, [&](const double *cs, int64_t js, int64_t len) {
                 m = run_min(cs, js, len, ui, m);
             });
@@ -237,37 +290,38 @@ struct Solver {
         return m;
     }
 
-    // scalar strict-< scan of arcs [a, hi): the reference's inner loop
-    void scan_first(int64_t a, int64_t hi, double &best, int64_t &enter) const {
-        int64_t i = a / nt, j = a - i * nt;
-        while (a < hi) {
+    // first arc of [a, hi) whose reduced cost equals m (the block minimum):
+    // the arc the reference's strict-< scan ends on
+    int64_t find_first(int64_t a, int64_t hi, double m) const {
+        const double *v_ = pot.data() + ns;
+        int64_t i = a / nt, j = a - i * nt, found = -1;
+        while (a < hi && found < 0) {
             const int64_t j1 = std::min<int64_t>(nt, j + (hi - a));
-            const double ui = u[i];
+            const double ui = pot[i];
             const int64_t rowbase = i * nt;
             cost.runs(i, j, j1, [&](const double *cs, int64_t js, int64_t len) {
-                for (int64_t t = 0; t < len; ++t) {
-                    const double r = (cs[t] - ui) - v[js + t];
-                    if (r < best) {
-                        best = r;
-                        enter = rowbase + js + t;
-                    }
-                }
+                if (found >= 0) return;
+                const int64_t t = simd == 2 ? run_find_avx512(cs, v_ + js, len, ui, m)
+                                            : run_find_scalar(cs, v_ + js, len, ui, m);
+                if (t >= 0) found = rowbase + js + t;
             });
             a += j1 - j;
             j = 0;
             ++i;
         }
+        return found;
     }
 
     // Bland: first arc (in index order) with reduced cost below -tol
     int64_t first_below(double tol) const {
+        const double *v_ = pot.data() + ns;
         for (int64_t i = 0; i < ns; ++i) {
-            const double ui = u[i];
+            const double ui = pot[i];
             int64_t found = -1;
             cost.runs(i, 0, nt, [&](const double *cs, int64_t js, int64_t len) {
                 if (found != -1) return;
                 for (int64_t t = 0; t < len; ++t)
-                    if ((cs[t] - ui) - v[js + t] < -tol) {
+                    if ((cs[t] - ui) - v_[js + t] < -tol) {
                         found = js + t;
                         return;
                     }
@@ -284,6 +338,7 @@ struct Solver {
               double tol, int64_t *pivots_out, bool warm) {
         nb = ns + nt - 1;
         const int64_t n_arcs = ns * nt, n_nodes = ns + nt;
+        if (n_nodes >= (int64_t)INT32_MAX) return GDT_ERR_ARG;
         if (block_size <= 0)
             block_size = std::max<int64_t>(64, (int64_t)std::sqrt((double)(ns * nt)) + 1);
         if (max_pivots <= 0) max_pivots = 50 * (ns + nt) * (ns + nt);
@@ -305,30 +360,28 @@ struct Solver {
                 else if (c < nt - 1) ++c;
             }
         }
-        ck.resize(nb);
-        for (int64_t k = 0; k < nb; ++k) ck[k] = cost.at(bi[k], bj[k]);
-        rhead.assign(ns, -1);
-        chead.assign(nt, -1);
-        rnext.resize(nb);
-        rprev.resize(nb);
-        cnext.resize(nb);
-        cprev.resize(nb);
-        for (int64_t k = 0; k < nb; ++k) push(k);
-        par.assign(n_nodes, -2);
-        pslot.assign(n_nodes, 0);
-        dep.assign(n_nodes, 0);
+        sl.resize(nb);
+        nd.assign(n_nodes, Node{-2, 0, 0, -1});
+        pot.assign(n_nodes, 0.0);
+        for (int64_t k = 0; k < nb; ++k) {
+            sl[k].i = (int32_t)bi[k];
+            sl[k].j = (int32_t)bj[k];
+            sl[k].ck = cost.at(bi[k], bj[k]);
+        }
+        // head-inserted in slot order (_simplex.py:70-89)
+        for (int64_t k = 0; k < nb; ++k) push((int32_t)k);
         stk.resize(n_nodes);
         pa_s.resize(n_nodes);
         pb_s.resize(n_nodes);
         sa_s.resize(n_nodes);
         sb_s.resize(n_nodes);
-        par[0] = -1;
-        pslot[0] = -1;
-        dep[0] = 0;
-        u[0] = 0.0;
+        nd[0].par = -1;
+        nd[0].pslot = -1;
+        nd[0].dep = 0;
+        pot[0] = 0.0;
         label(0, false);
         for (int64_t w = 0; w < n_nodes; ++w)
-            if (par[w] == -2) return GDT_LP_DISCONNECTED;
+            if (nd[w].par == -2) return GDT_LP_DISCONNECTED;
 
         int64_t next_arc = 0, degen_run = 0, pivots = 0;
         int status = GDT_LP_OPTIMAL;
@@ -337,14 +390,16 @@ struct Solver {
             if (degen_run >= degen_limit) {
                 enter = first_below(tol);
             } else {
-                double best = -tol;
                 int64_t scanned = 0, a = next_arc;
                 while (scanned < n_arcs) {
                     const int64_t hi = std::min(a + block_size, n_arcs);
-                    if (block_min(a, hi) < best) scan_first(a, hi, best, enter);
+                    const double m = block_min(a, hi);
+                    if (m < -tol) {
+                        enter = find_first(a, hi, m);
+                        break;
+                    }
                     scanned += hi - a;
                     a = hi >= n_arcs ? 0 : hi;
-                    if (enter != -1) break;
                 }
                 if (enter != -1) next_arc = enter + 1 >= n_arcs ? 0 : enter + 1;
             }
@@ -356,35 +411,37 @@ struct Solver {
             ++pivots;
 
             // the cycle: tree paths from sink ej (side a) and source ei (side b)
-            const int64_t ei = enter / nt, ej = enter - ei * nt;
-            int64_t ca = 0, cb = 0, pa = ns + ej, pb = ei;
-            while (dep[pa] > dep[pb]) {
-                pa_s[ca] = pslot[pa];
+            const int32_t ei = (int32_t)(enter / nt), ej = (int32_t)(enter - (int64_t)ei * nt);
+            int64_t ca = 0, cb = 0;
+            int32_t pa = (int32_t)ns + ej, pb = ei;
+            while (nd[pa].dep > nd[pb].dep) {
+                pa_s[ca] = nd[pa].pslot;
                 sa_s[ca++] = pa >= ns ? -1 : 1;
-                pa = par[pa];
+                pa = nd[pa].par;
             }
-            while (dep[pb] > dep[pa]) {
-                pb_s[cb] = pslot[pb];
+            while (nd[pb].dep > nd[pa].dep) {
+                pb_s[cb] = nd[pb].pslot;
                 sb_s[cb++] = pb < ns ? -1 : 1;
-                pb = par[pb];
+                pb = nd[pb].par;
             }
             while (pa != pb) {
-                pa_s[ca] = pslot[pa];
+                pa_s[ca] = nd[pa].pslot;
                 sa_s[ca++] = pa >= ns ? -1 : 1;
-                pa = par[pa];
-                pb_s[cb] = pslot[pb];
+                pa = nd[pa].par;
+                pb_s[cb] = nd[pb].pslot;
                 sb_s[cb++] = pb < ns ? -1 : 1;
-                pb = par[pb];
+                pb = nd[pb].par;
             }
             // leaving slot: min flow on decreasing arcs, lowest arc index on ties
             double theta = INFINITY;
-            int64_t leave = -1, leave_arc = INT64_MAX;
+            int32_t leave = -1;
+            int64_t leave_arc = INT64_MAX;
             bool on_a = true;
             for (int64_t q = 0; q < ca; ++q) {
                 if (sa_s[q] > 0) continue;
-                const int64_t k = pa_s[q];
+                const int32_t k = pa_s[q];
                 const double fl = bf[k];
-                const int64_t ak = bi[k] * nt + bj[k];
+                const int64_t ak = (int64_t)sl[k].i * nt + sl[k].j;
                 if (fl < theta || (fl == theta && ak < leave_arc)) {
                     theta = fl;
                     leave = k;
@@ -394,9 +451,9 @@ struct Solver {
             }
             for (int64_t q = 0; q < cb; ++q) {
                 if (sb_s[q] > 0) continue;
-                const int64_t k = pb_s[q];
+                const int32_t k = pb_s[q];
                 const double fl = bf[k];
-                const int64_t ak = bi[k] * nt + bj[k];
+                const int64_t ak = (int64_t)sl[k].i * nt + sl[k].j;
                 if (fl < theta || (fl == theta && ak < leave_arc)) {
                     theta = fl;
                     leave = k;
@@ -409,29 +466,34 @@ struct Solver {
             for (int64_t q = 0; q < cb; ++q) bf[pb_s[q]] += sb_s[q] < 0 ? -theta : theta;
 
             unlink(leave);
-            bi[leave] = ei;
-            bj[leave] = ej;
+            sl[leave].i = ei;
+            sl[leave].j = ej;
+            sl[leave].ck = cost.at(ei, ej);
             bf[leave] = theta;
-            ck[leave] = cost.at(ei, ej);
             push(leave);
 
             // the detached subtree hangs off the entering arc at the endpoint
             // whose old root path crossed the leaving arc
-            int64_t q_root, p_root;
+            int32_t q_root, p_root;
             if (on_a) {
-                q_root = ns + ej;
+                q_root = (int32_t)ns + ej;
                 p_root = ei;
             } else {
                 q_root = ei;
-                p_root = ns + ej;
+                p_root = (int32_t)ns + ej;
             }
-            par[q_root] = p_root;
-            pslot[q_root] = leave;
-            dep[q_root] = dep[p_root] + 1;
-            if (q_root < ns) u[q_root] = ck[leave] - v[p_root - ns];
-            else v[q_root - ns] = ck[leave] - u[p_root];
+            nd[q_root].par = p_root;
+            nd[q_root].pslot = leave;
+            nd[q_root].dep = nd[p_root].dep + 1;
+            pot[q_root] = sl[leave].ck - pot[p_root];
             label(q_root, true);
         }
+        for (int64_t k = 0; k < nb; ++k) {
+            bi[k] = sl[k].i;
+            bj[k] = sl[k].j;
+        }
+        std::memcpy(u, pot.data(), sizeof(double) * ns);
+        std::memcpy(v, pot.data() + ns, sizeof(double) * nt);
         *pivots_out = pivots;
         return status;
     }

@@ -128,7 +128,7 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
     cmin = min_cost_table(bt.pdims, bt.kappa, bt.p) if need_cmin else None
     ctil = centre_cost_table(bt.pdims, bt.kappa, bt.p) if need_ctil else None
     for b in range(bt.B):
-        root = -1
+        prev = -1
         for kind, cost in (("ctil", ctil),
                            ("cbar", cbar_host[b] if need_cbar else None),
                            ("cmin", cmin)):
@@ -139,10 +139,10 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
                 slots.append((b, kind))
                 # C-tilde follows the reference's pivot path (its basis defines the
                 # upscaled support and the duals); C-bar / C-min only need the
-                # optimal value, so they start from the C-tilde basis
-                warm.append(root)
-                if root < 0:
-                    root = len(problems) - 1
+                # optimal value, so each starts from the previous optimal basis of
+                # the chain C-tilde -> C-bar -> C-min (same marginals)
+                warm.append(prev)
+                prev = len(problems) - 1
             except GridotError as exc:
                 slots.append((b, kind, exc))
     solved = solve_transport_many(problems, threads=lp_threads, warm_from=warm, slack=False)
