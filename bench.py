@@ -233,10 +233,12 @@ def run_b200(args):
             launches += 2 + (0 if bt.pdims == bt.dims else 2)
             ev[1].record(cur)
             E._cbar(bt)
-            launches += 3 if (bt.p == 2.0 and bt.mode == 1) else 1
+            launches += 3 if bt.p == 2.0 else 1  # moments x2 + C-bar, or one C-bar kernel
             ev[2].record(cur)
             E.launch_primal(bt, dp, wl.max_iter)
-            launches += 1
+            # ipf_fast + TV/moments + pricing + finish (fp32 mode); the exact
+            # path adds two arc-coordinate packs and the block map
+            launches += 4 if bt.mode == 1 else 7
             ev[3].record(cur)
             E.launch_dual_prep(bt, dp)
             launches += 2
@@ -328,12 +330,21 @@ def run_b200(args):
     prim_ms = statistics.mean(stage_ms[(k, p, "primal")] for k, p, _, _ in stages)
     sweeps = statistics.mean(
         float(np.mean(E.to_host(dp.prim_out)[:, 4])) for _, _, _, dp in stages)
-    ipf_bytes = (48.0 * sweeps + 32.0) * Nf * ppr
-    ipf_roof = {"bound": "hbm", "kernel": "primal_kernel<uniform> (IPF + pricing + TV)",
+    # fp32 mode (ipf_fast_kernel): per sweep read mu, a, write a; read nu,
+    # write b = 40 B/cell; init 24 B/cell and the closing gap pass 24 B/cell;
+    # moments/TV pass 32 B/cell.  fp64 mode (ipf_kernel): SURVEY 8(d) model.
+    if wl.precision == "fp32":
+        ipf_bytes = (40.0 * sweeps + 48.0 + 32.0) * Nf * ppr
+        bytes_model = "(40*S + 48 + 32) * N^d bytes per pair: IPF sweeps + init/closing pass + TV"
+    else:
+        ipf_bytes = (48.0 * sweeps + 32.0) * Nf * ppr
+        bytes_model = "(48*S + 32) * N^d bytes per pair (SURVEY.md 8(d))"
+    ipf_roof = {"bound": "hbm", "kernel": ("ipf_fast_kernel" if wl.precision == "fp32" else
+                                           "ipf_kernel") + " + moments_tv + price (primal stage)",
                 "achieved": ipf_bytes / (prim_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
                 "frac": ipf_bytes / (prim_ms / 1000.0) / 1e9 / hbm, "traffic": None,
                 "sweeps": sweeps,
-                "work": "(48*S + 32) * N^2 bytes per pair (SURVEY.md 8(d)), L2-resident at 45 pairs"}
+                "work": bytes_model + "; stage time includes pricing"}
 
     ct_roofs = {}
     for (k, p_, nm), v in stage_ms.items():

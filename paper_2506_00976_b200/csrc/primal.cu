@@ -536,6 +536,248 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     }
 }
 
+// ---------------------------------------------------------------------------
+// ipf_fast_kernel (fp32 mode, uniform kernel): the same sweep as ipf_kernel
+// -- a = mu / K b, b = nu / K^T a, the reference's checks in its order
+// (sinkhorn.py:119-141) -- with the block-sparse mat-vecs regrouped by the
+// plan's block structure: with W_ts = W for every cell pair of an arc,
+//   (K^T a)_s = sum_{k -> l(s)} m_kl W S_k,  S_k = sum_{t in X_k} a_t,
+//   (K b)_t   = sum_{l <- k(t)} m_kl W B_l,  B_l = sum_{s in Y_l} b_s,
+// so a sweep is two coalesced streaming passes over the fine cells (per
+// coarse block: one thread, its kappa^d cells, the block sum in a register)
+// and two O(arcs) passes over the coarse plan.  The summation order differs
+// from scipy's CSR/CSC order (fp64 throughout, rounding-level differences;
+// the fp32-mode contract is 1e-5 on the bounds), which removes the
+// sequential per-unit chains whose length (up to m_kl * kappa^d terms) bounds
+// ipf_kernel.  One thread-block cluster per pair (<= 8 CTAs), two cluster
+// barriers per sweep; cross-CTA sums combine per-CTA partials in rank order
+// (deterministic).
+// Per sweep and fine cell: read mu, a, write a; read nu, write b = 40 bytes.
+constexpr int FT = 128;  // threads per CTA of ipf_fast_kernel
+constexpr int FCS_MAX = 8;
+
+struct FastPart {
+    double gap, lo, hi, flags;  // flags: 1 = zero denominator, 2 = non-finite
+};
+
+__device__ __forceinline__ void fp_range(double v, FastPart &q) {
+    if (v > 0.0) {
+        q.lo = fmin(q.lo, v);
+        q.hi = fmax(q.hi, v);
+        if (!isfinite(v)) q.flags = (double)((int)q.flags | 2);
+    } else if (isnan(v)) {
+        q.flags = (double)((int)q.flags | 2);
+    }
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+                 ::: "memory");
+}
+
+__device__ __forceinline__ unsigned cluster_rank_id() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ unsigned cluster_size() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+
+// CTA-reduce q, thread 0 stores it in slot[rank]
+__device__ __forceinline__ void fp_publish(FastPart q, FastPart *slot, unsigned rank, FastPart *sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        q.gap += __shfl_xor_sync(0xffffffffu, q.gap, o);
+        q.lo = fmin(q.lo, __shfl_xor_sync(0xffffffffu, q.lo, o));
+        q.hi = fmax(q.hi, __shfl_xor_sync(0xffffffffu, q.hi, o));
+        q.flags = (double)((int)q.flags | (int)__shfl_xor_sync(0xffffffffu, q.flags, o));
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) sh[w] = q;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        FastPart t = sh[0];
+        for (int i = 1; i < FT / 32; ++i) {
+            t.gap += sh[i].gap;
+            t.lo = fmin(t.lo, sh[i].lo);
+            t.hi = fmax(t.hi, sh[i].hi);
+            t.flags = (double)((int)t.flags | (int)sh[i].flags);
+        }
+        slot[rank] = t;
+    }
+    __syncthreads();
+}
+
+// after a cluster barrier: every thread combines the cluster's partials in rank order
+__device__ __forceinline__ FastPart fp_combine(const FastPart *slot, unsigned cs) {
+    FastPart t{0.0, INFINITY, -INFINITY, 0.0};
+    for (unsigned r = 0; r < cs; ++r) {
+        const double g = __ldcg(&slot[r].gap), lo = __ldcg(&slot[r].lo),
+                     hi = __ldcg(&slot[r].hi), fl = __ldcg(&slot[r].flags);
+        t.gap += g;
+        t.lo = fmin(t.lo, lo);
+        t.hi = fmax(t.hi, hi);
+        t.flags = (double)((int)t.flags | (int)fl);
+    }
+    return t;
+}
+
+__device__ __forceinline__ bool fp_bad(double lo, double hi) {
+    return lo <= hi && (lo < 1e-100 || hi > 1e100 || !isfinite(hi));
+}
+
+__global__ void __launch_bounds__(FT) ipf_fast_kernel(
+    const double *__restrict__ mu, const double *__restrict__ nu, const int64_t *__restrict__ arc_off,
+    const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ row_arc_col,
+    const double *__restrict__ row_arc_mass, const int32_t *__restrict__ col_ptr,
+    const int32_t *__restrict__ col_arc_row, const double *__restrict__ col_arc_mass,
+    const double *__restrict__ W, const double *__restrict__ xi_in, int64_t max_iter, G32 f,
+    G32 c, int kappa, double *__restrict__ out, int32_t *__restrict__ status,
+    double *__restrict__ scratch, int64_t stride_pair, FastPart *__restrict__ parts) {
+    __shared__ FastPart sh[FT / 32];
+    const unsigned cs = cluster_size(), rank = cluster_rank_id();
+    const int64_t b = blockIdx.x / cs;
+    const int N = f.cells, n = c.cells;
+    const double Wu = W[0];
+    const double *mub = mu + b * N, *nub = nu + b * N;
+    const int64_t a0 = arc_off[b];
+    const int32_t *rptr = row_ptr + b * (n + 1), *cptr = col_ptr + b * (n + 1);
+    const int32_t *rcol = row_arc_col + a0, *crow = col_arc_row + a0;
+    const double *rmass = row_arc_mass + a0, *cmass = col_arc_mass + a0;
+    double *ws = scratch + b * stride_pair;
+    double *aA = ws, *aB = ws + N, *bv = ws + 2 * N, *kbv = ws + 3 * N, *ktv = ws + 3 * N + n;
+    double *S = ws + 3 * N + 2 * n, *Bs = ws + 3 * N + 3 * n;  // block sums of a and b
+    FastPart *pp = parts + b * 5 * FCS_MAX;  // slots: init, AC[2], B[2]
+    const int g0 = (int)rank * FT + threadIdx.x, gstep = (int)cs * FT;
+
+    // b = 1 on the target support (sinkhorn.py:119 on the restricted matrix),
+    // B_l = its count, support count for the default xi
+    {
+        FastPart q{0.0, INFINITY, -INFINITY, 0.0};
+        for (int l = g0; l < n; l += gstep) {
+            double sb = 0.0;
+            for_block_cells(block_origin(l, c, f, kappa), f, kappa, [&](int, int j) {
+                const double nj = nub[j], mj = mub[j];
+                q.gap += (mj > 0.0 ? 1.0 : 0.0) + (nj > 0.0 ? 1.0 : 0.0);
+                const double bj = nj > 0.0 ? 1.0 : 0.0;
+                bv[j] = bj;
+                sb += bj;
+            });
+            Bs[l] = sb;
+        }
+        fp_publish(q, pp, rank, sh);
+    }
+    cluster_sync_all();
+    const double cnt = fp_combine(pp, cs).gap;
+    const double xi = xi_in[b] < 0.0 ? 1e-9 * cnt : xi_in[b];
+
+    double *a_cur = aA, *a_nxt = aB;
+    int st = GDT_PAIR_OK;
+    int64_t it = 0;
+    bool converged = false;
+    double gap = INFINITY;
+    FastPart ra{0.0, INFINITY, -INFINITY, 0.0}, rb = ra;  // a and b of sweep `it`
+    for (;;) {
+        // kb = K b (coarse), then the row pass: |a kb - mu| of sweep it, the
+        // zero-row check and a of sweep it+1, and its block sums
+        FastPart q{0.0, INFINITY, -INFINITY, 0.0};
+        for (int k = g0; k < n; k += gstep) {
+            double kb = 0.0;
+            for (int e = rptr[k]; e < rptr[k + 1]; ++e)
+                kb += __dmul_rn(rmass[e], Wu) * __ldcg(Bs + rcol[e]);
+            kbv[k] = kb;
+            const double rcp = kb > 0.0 ? __drcp_rn(kb) : 0.0;
+            double sa = 0.0;
+            for_block_cells(block_origin(k, c, f, kappa), f, kappa, [&](int, int i) {
+                const double mi = mub[i];
+                if (it >= 1 && mi > 0.0) q.gap += fabs(__dsub_rn(__dmul_rn(a_cur[i], kb), mi));
+                double an = 0.0;
+                if (mi > 0.0) {
+                    if (kb <= 0.0) q.flags = (double)((int)q.flags | 1);
+                    else an = div_shared(mi, kb, rcp);
+                }
+                fp_range(an, q);
+                a_nxt[i] = an;
+                sa += an;
+            });
+            S[k] = sa;
+        }
+        FastPart *slot_ac = pp + (1 + (int)((it + 1) & 1)) * FCS_MAX;
+        fp_publish(q, slot_ac, rank, sh);
+        cluster_sync_all();
+        const FastPart ac = fp_combine(slot_ac, cs);
+        if (it >= 1) {  // end of sweep `it`: range checks, then the gap
+            if (fp_bad(ra.lo, ra.hi) || fp_bad(rb.lo, rb.hi) || (((int)ra.flags | (int)rb.flags) & 2)) {
+                st = GDT_PAIR_OVERFLOW;
+                break;
+            }
+            gap = ac.gap + rb.gap;
+            if (gap < xi) {
+                converged = true;
+                break;
+            }
+            if (it >= max_iter) break;
+        }
+        if ((int)ac.flags & 1) {  // top of sweep it+1
+            st = GDT_PAIR_ZERO_DENOM_ROW;
+            break;
+        }
+        ++it;
+        double *tmp = a_cur;
+        a_cur = a_nxt;
+        a_nxt = tmp;
+        ra = ac;
+        // kta = K^T a (coarse), then the column pass: zero-column check, b,
+        // |nu - b kta|, range(b), block sums of b
+        FastPart qb{0.0, INFINITY, -INFINITY, 0.0};
+        for (int l = g0; l < n; l += gstep) {
+            double kt = 0.0;
+            for (int e = cptr[l]; e < cptr[l + 1]; ++e)
+                kt += __dmul_rn(cmass[e], Wu) * __ldcg(S + crow[e]);
+            ktv[l] = kt;
+            const double rcp = kt > 0.0 ? __drcp_rn(kt) : 0.0;
+            double sb = 0.0;
+            for_block_cells(block_origin(l, c, f, kappa), f, kappa, [&](int, int j) {
+                const double nj = nub[j];
+                double bj = 0.0;
+                if (nj > 0.0) {
+                    if (kt <= 0.0) qb.flags = (double)((int)qb.flags | 1);
+                    else bj = div_shared(nj, kt, rcp);
+                    fp_range(bj, qb);
+                    qb.gap += fabs(__dsub_rn(nj, __dmul_rn(bj, kt)));
+                }
+                bv[j] = bj;
+                sb += bj;
+            });
+            Bs[l] = sb;
+        }
+        FastPart *slot_b = pp + (3 + (int)(it & 1)) * FCS_MAX;
+        fp_publish(qb, slot_b, rank, sh);
+        cluster_sync_all();
+        rb = fp_combine(slot_b, cs);
+        if ((int)rb.flags & 1) {
+            st = GDT_PAIR_ZERO_DENOM_COL;
+            break;
+        }
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+        status[b] = st;
+        double *o = out + b * 8;
+        o[0] = 0.0;
+        o[1] = 0.0;
+        o[2] = 0.0;
+        o[3] = gap;
+        o[4] = (double)it;
+        o[5] = converged ? 1.0 : 0.0;
+        o[6] = cnt;
+        o[7] = a_cur == aA ? 0.0 : 1.0;
+    }
+}
+
 __device__ __forceinline__ float sqrt_apx32(float x) {
     float r;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -870,14 +1112,14 @@ __global__ void sum_parts_kernel(const double *__restrict__ part, int count, dou
 // pairs: moments [B, n, MW], tv partials [B, tv_ctas, 2], price partials
 // [B, pr_ctas]
 struct PrimalLayout {
-    int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, bm_off, total, tv_ctas, pr_ctas;
+    int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, bm_off, fp_off, total, tv_ctas, pr_ctas;
 };
 
 inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, bool uniform,
                                   bool p2, int64_t max_arcs) {
     PrimalLayout L;
     const int64_t U = uniform ? c.cells : f.cells;
-    L.stride_pair = 3 * f.cells + 3 * U;  // aA, aB, b, kb, kta, reciprocals
+    L.stride_pair = 3 * f.cells + 4 * U;  // aA, aB, b, kb, kta, reciprocals / S, B
     L.mom_off = batch * L.stride_pair;
     const int64_t MW = 2 * (f.nd + 2);
     L.tv_ctas = (c.cells + MT - 1) / MT;
@@ -888,7 +1130,8 @@ inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, b
     L.pr_off = L.tv_off + batch * L.tv_ctas * 2;
     L.pc_off = L.pr_off + batch * L.pr_ctas;       // packed arc coordinates (int64)
     L.bm_off = L.pc_off + 2 * batch * max_arcs;    // fine cell -> coarse block (int32)
-    L.total = L.bm_off + (f.cells + 1) / 2;
+    L.fp_off = L.bm_off + (f.cells + 1) / 2;        // ipf_fast_kernel partials
+    L.total = L.fp_off + batch * 5 * FCS_MAX * 4;
     return L;
 }
 
@@ -932,19 +1175,45 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
     const G32 f32 = to32(f), c32 = to32(c);
     GDT_CHECK_ARG(c.n[0] < 65536 && c.n[1] < 65536 && c.n[2] < 65536 && c.n[3] < 65536,
                   "gdt_primal_upscale: coarse axes must be < 65536");
+    const bool fast_ipf = uni && mode == GDT_MODE_FAST;
     int64_t *rpc = reinterpret_cast<int64_t *>(ws + L.pc_off);
     int64_t *cpc = rpc + batch * 2 * c.cells;
     const int64_t per_pair = 2 * c.cells;
-    pack_coords_kernel<<<grid_size(batch * per_pair, 256), 256, 0, st>>>(row_arc_col, arc_off,
-                                                                         per_pair, batch, c32, rpc);
-    pack_coords_kernel<<<grid_size(batch * per_pair, 256), 256, 0, st>>>(col_arc_row, arc_off,
-                                                                         per_pair, batch, c32, cpc);
     int32_t *bmap = reinterpret_cast<int32_t *>(ws + L.bm_off);
-    if (uni) block_map_kernel<<<grid_size(f.cells, 256), 256, 0, st>>>(f32, c32, kappa, bmap);
+    if (!fast_ipf) {  // packed arc coordinates and the block map of ipf_kernel
+        pack_coords_kernel<<<grid_size(batch * per_pair, 256), 256, 0, st>>>(
+            row_arc_col, arc_off, per_pair, batch, c32, rpc);
+        pack_coords_kernel<<<grid_size(batch * per_pair, 256), 256, 0, st>>>(
+            col_arc_row, arc_off, per_pair, batch, c32, cpc);
+        if (uni) block_map_kernel<<<grid_size(f.cells, 256), 256, 0, st>>>(f32, c32, kappa, bmap);
+    }
     const size_t sxb = sizeof(double) * f.cells;
     const int use_smem = sxb <= 160 * 1024;
     const size_t dyn = use_smem ? sxb : 0;
-    if (uni) {
+    if (fast_ipf) {
+        // one cluster of ceil(n / FT) <= 8 CTAs per pair
+        const unsigned csz = (unsigned)std::min<int64_t>(FCS_MAX, (c.cells + FT - 1) / FT);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(batch * csz));
+        cfg.blockDim = dim3(FT);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = csz;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        FastPart *fparts = reinterpret_cast<FastPart *>(ws + L.fp_off);
+        const cudaError_t e = cudaLaunchKernelEx(
+            &cfg, ipf_fast_kernel, mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr,
+            col_arc_row, col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws,
+            L.stride_pair, fparts);
+        if (e != cudaSuccess) {
+            set_error(std::string("gdt_primal_upscale: ipf_fast_kernel: ") + cudaGetErrorString(e));
+            return GDT_ERR_CUDA;
+        }
+    } else if (uni) {
         if (dyn > 48 * 1024)
             cudaFuncSetAttribute(ipf_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)dyn);

@@ -105,8 +105,13 @@ class _Batch:
 
 
 def _cbar(bt: _Batch):
+    # p == 2: C-bar from fp64 block moments in both precisions (the quadratic
+    # cost factorises; <= ~1e-14 relative per entry against the reference's
+    # summation, far inside fp64 mode's 1e-9 bound contract); p != 2: the
+    # reference-order fp64 kernel (fp64 mode) or the fp32 FFMA2 kernel
+    mode = 1 if bt.p == 2.0 else bt.mode
     return weighted_cost_batch(bt.mu_pad, bt.nu_pad, bt.mu_c, bt.nu_c, bt.pdims, bt.kappa, bt.p,
-                               bt.mode, bt.ctil_dev, bt.table_dev)
+                               mode, bt.ctil_dev, bt.table_dev)
 
 
 def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:

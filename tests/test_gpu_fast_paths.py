@@ -21,6 +21,7 @@ from paper_2506_00976_b200.costs import (centre_cost_cached, cost_table, max_sq_
                                          weighted_cost_batch)
 from paper_2506_00976_b200.device import to_dev, to_host  # noqa: E402
 from paper_2506_00976_b200.measures import sumpool_batch  # noqa: E402
+from test_oracle_golden import inputs_for  # noqa: E402
 
 
 def _pairs(dims, B, seed, holes=False):
@@ -69,3 +70,42 @@ def test_fp32_pruned_ctransform_tracks_fp64(dims):
     assert np.max(np.abs(g64 - g32)) <= 1e-5 * max(1.0, np.abs(g64).max())
     d64, d32 = to_host(f64[2]), to_host(f32[2])
     assert np.allclose(d64, d32, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("cfg,k,max_iter", [(2, 4, 40), (3, 8, 10), (4, 8, 12)])
+def test_fast_ipf_tracks_exact_ipf(cfg, k, max_iter):
+    """fp32-mode IPF (block-regrouped mat-vecs, ipf_fast_kernel) vs the exact
+    scipy-order kernel: p = 2 prices in closed form in both modes, so the
+    primal bound differs only by the IPF summation order (fp64 both)."""
+    from paper_2506_00976_b200 import synthetic as S
+
+    wl = S.WORKLOADS[cfg]
+    B = 6
+    mus, nus = S.batch(cfg, 0, B)
+    kw = dict(xi=0.0, max_iter=max_iter, methods=("primal_upscaling",), return_exceptions=False)
+    ex = G.quantized_bounds(mus, nus, wl.dims, k, 2.0, precision="fp64", **kw)
+    fa = G.quantized_bounds(mus, nus, wl.dims, k, 2.0, precision="fp32", **kw)
+    for b in range(B):
+        e, f = ex[b]["primal_upscaling"], fa[b]["primal_upscaling"]
+        assert e.iterations == f.iterations == max_iter
+        assert abs(e.value - f.value) <= 1e-12 * abs(e.value), (b, e.value, f.value)
+        for key in ("transport", "delta_mu", "delta_nu"):
+            assert abs(e.components[key] - f.components[key]) <= 1e-10 * max(1.0, e.value)
+
+
+def test_fast_ipf_default_xi_and_statuses(small_cases):
+    """Default xi: both IPF kernels stop on the same sweep; zero-denominator
+    pairs fail the same way (ring fallback)."""
+    for c in small_cases:
+        if "kernel" in c:
+            continue
+        mu, nu = inputs_for(c)
+        dims, k, p = c["dims"], c["kappa"], c["p"]
+        kw = dict(methods=("primal_upscaling",), return_exceptions=True)
+        e = G.quantized_bounds(mu[None], nu[None], dims, k, p, precision="fp64", **kw)[0]
+        f = G.quantized_bounds(mu[None], nu[None], dims, k, p, precision="fp32", **kw)[0]
+        e, f = e["primal_upscaling"], f["primal_upscaling"]
+        assert type(e) is type(f), c["tag"]
+        if not isinstance(e, Exception):
+            assert e.iterations == f.iterations, c["tag"]
+            assert abs(e.value - f.value) <= 1e-6 * abs(e.value), c["tag"]
