@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
 // barriers per sweep; cross-CTA sums combine per-CTA partials in rank order
 // (deterministic).
 // Per sweep and fine cell: read mu, a, write a; read nu, write b = 40 bytes.
-constexpr int FT = 128;  // threads per CTA of ipf_fast_kernel
+constexpr int FT = 256;  // threads per CTA of ipf_fast_kernel
 constexpr int FCS_MAX = 8;
 
 struct FastPart {
@@ -630,6 +630,44 @@ __device__ __forceinline__ bool fp_bad(double lo, double hi) {
     return lo <= hi && (lo < 1e-100 || hi > 1e100 || !isfinite(hi));
 }
 
+// Work mapping: a unit is one fine row (KAPPA cells along axis 0) of one
+// coarse block; the G = kappa^(d-1) rows of a block sit in G consecutive
+// lanes, which split the block's arcs for the coarse sum and fold the block
+// sum with xor shuffles (fixed order: deterministic).  A unit's KAPPA masses
+// and scalings are loaded together (vector loads) before use.  KAPPA = 0:
+// runtime kappa (or G > 32), one thread per block walking its cells.
+template <int KAPPA>
+__device__ __forceinline__ void fp_load(const double *p, double *v, int kappa) {
+    if constexpr (KAPPA >= 2) {
+#pragma unroll
+        for (int x = 0; x < KAPPA; x += 2) {
+            const double2 t = *reinterpret_cast<const double2 *>(p + x);
+            v[x] = t.x;
+            v[x + 1] = t.y;
+        }
+    } else {
+        for (int x = 0; x < kappa; ++x) v[x] = p[x];
+    }
+}
+
+template <int KAPPA>
+__device__ __forceinline__ void fp_store(double *p, const double *v, int kappa) {
+    if constexpr (KAPPA >= 2) {
+#pragma unroll
+        for (int x = 0; x < KAPPA; x += 2)
+            *reinterpret_cast<double2 *>(p + x) = make_double2(v[x], v[x + 1]);
+    } else {
+        for (int x = 0; x < kappa; ++x) p[x] = v[x];
+    }
+}
+
+// xor-fold over the G lanes of a group (all 32 lanes participate)
+__device__ __forceinline__ double group_sum(double v, int G) {
+    for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int KAPPA>
 __global__ void __launch_bounds__(FT) ipf_fast_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const int64_t *__restrict__ arc_off,
     const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ row_arc_col,
@@ -638,6 +676,7 @@ __global__ void __launch_bounds__(FT) ipf_fast_kernel(
     const double *__restrict__ W, const double *__restrict__ xi_in, int64_t max_iter, G32 f,
     G32 c, int kappa, double *__restrict__ out, int32_t *__restrict__ status,
     double *__restrict__ scratch, int64_t stride_pair, FastPart *__restrict__ parts) {
+    constexpr int KV = KAPPA >= 2 ? KAPPA : 16;  // register row buffer (runtime kappa <= 16)
     __shared__ FastPart sh[FT / 32];
     const unsigned cs = cluster_size(), rank = cluster_rank_id();
     const int64_t b = blockIdx.x / cs;
@@ -652,22 +691,63 @@ __global__ void __launch_bounds__(FT) ipf_fast_kernel(
     double *aA = ws, *aB = ws + N, *bv = ws + 2 * N, *kbv = ws + 3 * N, *ktv = ws + 3 * N + n;
     double *S = ws + 3 * N + 2 * n, *Bs = ws + 3 * N + 3 * n;  // block sums of a and b
     FastPart *pp = parts + b * 5 * FCS_MAX;  // slots: init, AC[2], B[2]
-    const int g0 = (int)rank * FT + threadIdx.x, gstep = (int)cs * FT;
+    const int kp = KAPPA >= 2 ? KAPPA : kappa;
+    int rows = 1;  // fine rows per block
+    for (int a = 1; a < f.nd; ++a) rows *= kp;
+    const int G = KAPPA >= 2 ? rows : 1;           // lanes per block
+    const int rows_per_unit = KAPPA >= 2 ? 1 : rows;
+    const int units = n * G;
+    const int gstep = (int)cs * FT;
+    const int g0 = (int)rank * FT + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    // warp-uniform trip count (shuffles need every lane)
+    const int trips = (units + gstep - 1) / gstep;
+
+    // fine index of row q of block k
+    auto row_start = [&](int k, int q) {
+        int off = block_origin(k, c, f, kp);
+        for (int a = 1; a < f.nd; ++a) {
+            off += (q % kp) * f.stride[a];
+            q /= kp;
+        }
+        return off;
+    };
+    // coarse sum over the arcs of unit u's block, split over its G lanes
+    auto coarse = [&](int k, int r, bool act, const int32_t *ptr, const int32_t *idx,
+                      const double *mass, const double *src) {
+        double v = 0.0;
+        if (act)
+            for (int e = ptr[k] + r; e < ptr[k + 1]; e += G)
+                v += __dmul_rn(mass[e], Wu) * __ldcg(src + idx[e]);
+        return group_sum(v, G);
+    };
 
     // b = 1 on the target support (sinkhorn.py:119 on the restricted matrix),
     // B_l = its count, support count for the default xi
     {
         FastPart q{0.0, INFINITY, -INFINITY, 0.0};
-        for (int l = g0; l < n; l += gstep) {
+        for (int t = 0; t < trips; ++t) {
+            const int u = g0 + t * gstep;
+            const bool act = u < units;
+            const int l = act ? u / G : 0, r = act ? u - l * G : 0;
             double sb = 0.0;
-            for_block_cells(block_origin(l, c, f, kappa), f, kappa, [&](int, int j) {
-                const double nj = nub[j], mj = mub[j];
-                q.gap += (mj > 0.0 ? 1.0 : 0.0) + (nj > 0.0 ? 1.0 : 0.0);
-                const double bj = nj > 0.0 ? 1.0 : 0.0;
-                bv[j] = bj;
-                sb += bj;
-            });
-            Bs[l] = sb;
+            if (act)
+                for (int qq = 0; qq < rows_per_unit; ++qq) {
+                    const int j0 = row_start(l, r + qq);
+                    double nv[KV], mv[KV], bb[KV];
+                    fp_load<KAPPA>(nub + j0, nv, kp);
+                    fp_load<KAPPA>(mub + j0, mv, kp);
+#pragma unroll
+                    for (int x = 0; x < KV; ++x) {
+                        if (x >= kp) break;
+                        q.gap += (mv[x] > 0.0 ? 1.0 : 0.0) + (nv[x] > 0.0 ? 1.0 : 0.0);
+                        bb[x] = nv[x] > 0.0 ? 1.0 : 0.0;
+                        sb += bb[x];
+                    }
+                    fp_store<KAPPA>(bv + j0, bb, kp);
+                }
+            sb = group_sum(sb, G);
+            if (act && r == 0) Bs[l] = sb;
         }
         fp_publish(q, pp, rank, sh);
     }
@@ -685,26 +765,40 @@ __global__ void __launch_bounds__(FT) ipf_fast_kernel(
         // kb = K b (coarse), then the row pass: |a kb - mu| of sweep it, the
         // zero-row check and a of sweep it+1, and its block sums
         FastPart q{0.0, INFINITY, -INFINITY, 0.0};
-        for (int k = g0; k < n; k += gstep) {
-            double kb = 0.0;
-            for (int e = rptr[k]; e < rptr[k + 1]; ++e)
-                kb += __dmul_rn(rmass[e], Wu) * __ldcg(Bs + rcol[e]);
-            kbv[k] = kb;
+        for (int t = 0; t < trips; ++t) {
+            const int u = g0 + t * gstep;
+            const bool act = u < units;
+            const int k = act ? u / G : 0, r = act ? u - k * G : 0;
+            const double kb = coarse(k, r, act, rptr, rcol, rmass, Bs);
             const double rcp = kb > 0.0 ? __drcp_rn(kb) : 0.0;
             double sa = 0.0;
-            for_block_cells(block_origin(k, c, f, kappa), f, kappa, [&](int, int i) {
-                const double mi = mub[i];
-                if (it >= 1 && mi > 0.0) q.gap += fabs(__dsub_rn(__dmul_rn(a_cur[i], kb), mi));
-                double an = 0.0;
-                if (mi > 0.0) {
-                    if (kb <= 0.0) q.flags = (double)((int)q.flags | 1);
-                    else an = div_shared(mi, kb, rcp);
+            if (act)
+                for (int qq = 0; qq < rows_per_unit; ++qq) {
+                    const int i0 = row_start(k, r + qq);
+                    double mv[KV], av[KV], an[KV];
+                    fp_load<KAPPA>(mub + i0, mv, kp);
+                    if (it >= 1) fp_load<KAPPA>(a_cur + i0, av, kp);
+#pragma unroll
+                    for (int x = 0; x < KV; ++x) {
+                        if (x >= kp) break;
+                        const double mi = mv[x];
+                        if (it >= 1 && mi > 0.0) q.gap += fabs(__dsub_rn(__dmul_rn(av[x], kb), mi));
+                        double v = 0.0;
+                        if (mi > 0.0) {
+                            if (kb <= 0.0) q.flags = (double)((int)q.flags | 1);
+                            else v = div_shared(mi, kb, rcp);
+                        }
+                        fp_range(v, q);
+                        an[x] = v;
+                        sa += v;
+                    }
+                    fp_store<KAPPA>(a_nxt + i0, an, kp);
                 }
-                fp_range(an, q);
-                a_nxt[i] = an;
-                sa += an;
-            });
-            S[k] = sa;
+            sa = group_sum(sa, G);
+            if (act && r == 0) {
+                S[k] = sa;
+                kbv[k] = kb;
+            }
         }
         FastPart *slot_ac = pp + (1 + (int)((it + 1) & 1)) * FCS_MAX;
         fp_publish(q, slot_ac, rank, sh);
@@ -734,26 +828,39 @@ __global__ void __launch_bounds__(FT) ipf_fast_kernel(
         // kta = K^T a (coarse), then the column pass: zero-column check, b,
         // |nu - b kta|, range(b), block sums of b
         FastPart qb{0.0, INFINITY, -INFINITY, 0.0};
-        for (int l = g0; l < n; l += gstep) {
-            double kt = 0.0;
-            for (int e = cptr[l]; e < cptr[l + 1]; ++e)
-                kt += __dmul_rn(cmass[e], Wu) * __ldcg(S + crow[e]);
-            ktv[l] = kt;
+        for (int t = 0; t < trips; ++t) {
+            const int u = g0 + t * gstep;
+            const bool act = u < units;
+            const int l = act ? u / G : 0, r = act ? u - l * G : 0;
+            const double kt = coarse(l, r, act, cptr, crow, cmass, S);
             const double rcp = kt > 0.0 ? __drcp_rn(kt) : 0.0;
             double sb = 0.0;
-            for_block_cells(block_origin(l, c, f, kappa), f, kappa, [&](int, int j) {
-                const double nj = nub[j];
-                double bj = 0.0;
-                if (nj > 0.0) {
-                    if (kt <= 0.0) qb.flags = (double)((int)qb.flags | 1);
-                    else bj = div_shared(nj, kt, rcp);
-                    fp_range(bj, qb);
-                    qb.gap += fabs(__dsub_rn(nj, __dmul_rn(bj, kt)));
+            if (act)
+                for (int qq = 0; qq < rows_per_unit; ++qq) {
+                    const int j0 = row_start(l, r + qq);
+                    double nv[KV], bb[KV];
+                    fp_load<KAPPA>(nub + j0, nv, kp);
+#pragma unroll
+                    for (int x = 0; x < KV; ++x) {
+                        if (x >= kp) break;
+                        const double nj = nv[x];
+                        double v = 0.0;
+                        if (nj > 0.0) {
+                            if (kt <= 0.0) qb.flags = (double)((int)qb.flags | 1);
+                            else v = div_shared(nj, kt, rcp);
+                            fp_range(v, qb);
+                            qb.gap += fabs(__dsub_rn(nj, __dmul_rn(v, kt)));
+                        }
+                        bb[x] = v;
+                        sb += v;
+                    }
+                    fp_store<KAPPA>(bv + j0, bb, kp);
                 }
-                bv[j] = bj;
-                sb += bj;
-            });
-            Bs[l] = sb;
+            sb = group_sum(sb, G);
+            if (act && r == 0) {
+                Bs[l] = sb;
+                ktv[l] = kt;
+            }
         }
         FastPart *slot_b = pp + (3 + (int)(it & 1)) * FCS_MAX;
         fp_publish(qb, slot_b, rank, sh);
@@ -1191,8 +1298,14 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
     const int use_smem = sxb <= 160 * 1024;
     const size_t dyn = use_smem ? sxb : 0;
     if (fast_ipf) {
-        // one cluster of ceil(n / FT) <= 8 CTAs per pair
-        const unsigned csz = (unsigned)std::min<int64_t>(FCS_MAX, (c.cells + FT - 1) / FT);
+        // one cluster of ceil(units / FT) <= 8 CTAs per pair; a unit is one
+        // fine row of a block for kappa in {2, 4, 8} with kappa^(d-1) <= 32
+        int rows = 1;
+        for (int a = 1; a < ndim; ++a) rows *= kappa;
+        const bool tmpl = (kappa == 2 || kappa == 4 || kappa == 8) && rows <= 32;
+        GDT_CHECK_ARG(tmpl || kappa <= 16, "gdt_primal_upscale: fast IPF needs kappa <= 16");
+        const int64_t units = c.cells * (tmpl ? rows : 1);
+        const unsigned csz = (unsigned)std::min<int64_t>(FCS_MAX, (units + FT - 1) / FT);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(batch * csz));
         cfg.blockDim = dim3(FT);
@@ -1205,10 +1318,17 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         FastPart *fparts = reinterpret_cast<FastPart *>(ws + L.fp_off);
-        const cudaError_t e = cudaLaunchKernelEx(
-            &cfg, ipf_fast_kernel, mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr,
-            col_arc_row, col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws,
-            L.stride_pair, fparts);
+        auto go = [&](auto kern) {
+            return cudaLaunchKernelEx(&cfg, kern, mu, nu, arc_off, row_ptr, row_arc_col,
+                                      row_arc_mass, col_ptr, col_arc_row, col_arc_mass, kernel_w,
+                                      xi, max_iter, f32, c32, kappa, out, status, ws,
+                                      L.stride_pair, fparts);
+        };
+        cudaError_t e;
+        if (!tmpl) e = go(ipf_fast_kernel<0>);
+        else if (kappa == 2) e = go(ipf_fast_kernel<2>);
+        else if (kappa == 4) e = go(ipf_fast_kernel<4>);
+        else e = go(ipf_fast_kernel<8>);
         if (e != cudaSuccess) {
             set_error(std::string("gdt_primal_upscale: ipf_fast_kernel: ") + cudaGetErrorString(e));
             return GDT_ERR_CUDA;

@@ -76,7 +76,7 @@ def test_fp32_pruned_ctransform_tracks_fp64(dims):
 def test_fast_ipf_tracks_exact_ipf(cfg, k, max_iter):
     """fp32-mode IPF (block-regrouped mat-vecs, ipf_fast_kernel) vs the exact
     scipy-order kernel: p = 2 prices in closed form in both modes, so the
-    primal bound differs only by the IPF summation order (fp64 both)."""
+    bounds differ only through the IPF summation order (fp64 both)."""
     from paper_2506_00976_b200 import synthetic as S
 
     wl = S.WORKLOADS[cfg]
@@ -88,9 +88,14 @@ def test_fast_ipf_tracks_exact_ipf(cfg, k, max_iter):
     for b in range(B):
         e, f = ex[b]["primal_upscaling"], fa[b]["primal_upscaling"]
         assert e.iterations == f.iterations == max_iter
-        assert abs(e.value - f.value) <= 1e-12 * abs(e.value), (b, e.value, f.value)
-        for key in ("transport", "delta_mu", "delta_nu"):
-            assert abs(e.components[key] - f.components[key]) <= 1e-10 * max(1.0, e.value)
+        # the transport cost sees only the summation-order rounding; the TV
+        # terms are 2^(1-1/p) tv^(1/p) of rounding-level marginal errors, so
+        # their noise is amplified by the root (both ~1e-8 here)
+        assert abs(e.components["transport"] - f.components["transport"]) <= \
+            1e-12 * e.components["transport"]
+        for key in ("delta_mu", "delta_nu"):
+            assert abs(e.components[key] - f.components[key]) <= 1e-7
+        assert abs(e.value - f.value) <= 1e-7 * abs(e.value), (b, e.value, f.value)
 
 
 def test_fast_ipf_default_xi_and_statuses(small_cases):
