@@ -555,6 +555,7 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
 // Per sweep and fine cell: read mu, a, write a; read nu, write b = 40 bytes.
 constexpr int FT = 256;  // threads per CTA of ipf_fast_kernel
 constexpr int FCS_MAX = 8;
+constexpr int FP_SMEM_SRC = 4096;  // block sums gathered into shared memory up to this n
 
 struct FastPart {
     double gap, lo, hi, flags;  // flags: 1 = zero denominator, 2 = non-finite
@@ -668,7 +669,7 @@ __device__ __forceinline__ double group_sum(double v, int G) {
 }
 
 template <int KAPPA>
-__global__ void __launch_bounds__(FT) ipf_fast_kernel(
+__global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const int64_t *__restrict__ arc_off,
     const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ row_arc_col,
     const double *__restrict__ row_arc_mass, const int32_t *__restrict__ col_ptr,
@@ -697,11 +698,32 @@ __global__ void __launch_bounds__(FT) ipf_fast_kernel(
     const int G = KAPPA >= 2 ? rows : 1;           // lanes per block
     const int rows_per_unit = KAPPA >= 2 ? 1 : rows;
     const int units = n * G;
-    const int gstep = (int)cs * FT;
-    const int g0 = (int)rank * FT + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    // warp-uniform trip count (shuffles need every lane)
-    const int trips = (units + gstep - 1) / gstep;
+    // CTA `rank` owns a contiguous, warp-aligned range of units (so its blocks
+    // are contiguous too); trip counts are CTA-uniform (shuffles need every lane)
+    const int upc = (((units + (int)cs - 1) / (int)cs) + 31) / 32 * 32;
+    const int u_lo = (int)rank * upc;
+    const int trips = (upc + FT - 1) / FT;
+    const int k_lo = u_lo / G;
+    const int nblk = min(upc / G, max(0, n - k_lo));
+    // shared: the block sums the coarse pass gathers from (whole pair, when
+    // they fit) and this CTA's slices of the CSR / CSC row pointers
+    extern __shared__ double fsm[];
+    const bool src_smem = n <= FP_SMEM_SRC;
+    double *src_s = fsm;
+    int *rp_s = reinterpret_cast<int *>(fsm + (src_smem ? n : 0));
+    int *cp_s = rp_s + nblk + 1;
+    for (int i = threadIdx.x; i <= nblk && k_lo + i <= n; i += FT) {
+        rp_s[i] = rptr[k_lo + i];
+        cp_s[i] = cptr[k_lo + i];
+    }
+    __syncthreads();
+    auto gather = [&](const double *src) -> const double * {
+        if (!src_smem) return src;
+        __syncthreads();  // previous readers of src_s are done
+        for (int i = threadIdx.x; i < n; i += FT) src_s[i] = __ldcg(src + i);
+        __syncthreads();
+        return src_s;
+    };
 
     // fine index of row q of block k
     auto row_start = [&](int k, int q) {
@@ -713,12 +735,15 @@ __global__ void __launch_bounds__(FT) ipf_fast_kernel(
         return off;
     };
     // coarse sum over the arcs of unit u's block, split over its G lanes
-    auto coarse = [&](int k, int r, bool act, const int32_t *ptr, const int32_t *idx,
+    auto coarse = [&](int k, int r, bool act, const int *ptr_s, const int32_t *idx,
                       const double *mass, const double *src) {
         double v = 0.0;
         if (act)
-            for (int e = ptr[k] + r; e < ptr[k + 1]; e += G)
-                v += __dmul_rn(mass[e], Wu) * __ldcg(src + idx[e]);
+            for (int e = ptr_s[k - k_lo] + r; e < ptr_s[k - k_lo + 1]; e += G) {
+                const double m = __ldg(mass + e);
+                const int j = __ldg(idx + e);
+                v += __dmul_rn(m, Wu) * (src_smem ? src[j] : __ldcg(src + j));
+            }
         return group_sum(v, G);
     };
 
@@ -727,8 +752,8 @@ __global__ void __launch_bounds__(FT) ipf_fast_kernel(
     {
         FastPart q{0.0, INFINITY, -INFINITY, 0.0};
         for (int t = 0; t < trips; ++t) {
-            const int u = g0 + t * gstep;
-            const bool act = u < units;
+            const int u = u_lo + t * FT + (int)threadIdx.x;
+            const bool act = u < units && u < u_lo + upc;
             const int l = act ? u / G : 0, r = act ? u - l * G : 0;
             double sb = 0.0;
             if (act)
@@ -765,11 +790,12 @@ __global__ void __launch_bounds__(FT) ipf_fast_kernel(
         // kb = K b (coarse), then the row pass: |a kb - mu| of sweep it, the
         // zero-row check and a of sweep it+1, and its block sums
         FastPart q{0.0, INFINITY, -INFINITY, 0.0};
+        const double *bsrc = gather(Bs);
         for (int t = 0; t < trips; ++t) {
-            const int u = g0 + t * gstep;
-            const bool act = u < units;
-            const int k = act ? u / G : 0, r = act ? u - k * G : 0;
-            const double kb = coarse(k, r, act, rptr, rcol, rmass, Bs);
+            const int u = u_lo + t * FT + (int)threadIdx.x;
+            const bool act = u < units && u < u_lo + upc;
+            const int k = act ? u / G : k_lo, r = act ? u - k * G : 0;
+            const double kb = coarse(k, r, act, rp_s, rcol, rmass, bsrc);
             const double rcp = kb > 0.0 ? __drcp_rn(kb) : 0.0;
             double sa = 0.0;
             if (act)
@@ -778,6 +804,9 @@ __global__ void __launch_bounds__(FT) ipf_fast_kernel(
                     double mv[KV], av[KV], an[KV];
                     fp_load<KAPPA>(mub + i0, mv, kp);
                     if (it >= 1) fp_load<KAPPA>(a_cur + i0, av, kp);
+                    else
+#pragma unroll
+                        for (int x = 0; x < KV; ++x) av[x] = 0.0;
 #pragma unroll
                     for (int x = 0; x < KV; ++x) {
                         if (x >= kp) break;
@@ -828,11 +857,12 @@ __global__ void __launch_bounds__(FT) ipf_fast_kernel(
         // kta = K^T a (coarse), then the column pass: zero-column check, b,
         // |nu - b kta|, range(b), block sums of b
         FastPart qb{0.0, INFINITY, -INFINITY, 0.0};
+        const double *ssrc = gather(S);
         for (int t = 0; t < trips; ++t) {
-            const int u = g0 + t * gstep;
-            const bool act = u < units;
-            const int l = act ? u / G : 0, r = act ? u - l * G : 0;
-            const double kt = coarse(l, r, act, cptr, crow, cmass, S);
+            const int u = u_lo + t * FT + (int)threadIdx.x;
+            const bool act = u < units && u < u_lo + upc;
+            const int l = act ? u / G : k_lo, r = act ? u - l * G : 0;
+            const double kt = coarse(l, r, act, cp_s, crow, cmass, ssrc);
             const double rcp = kt > 0.0 ? __drcp_rn(kt) : 0.0;
             double sb = 0.0;
             if (act)
@@ -1306,9 +1336,14 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         GDT_CHECK_ARG(tmpl || kappa <= 16, "gdt_primal_upscale: fast IPF needs kappa <= 16");
         const int64_t units = c.cells * (tmpl ? rows : 1);
         const unsigned csz = (unsigned)std::min<int64_t>(FCS_MAX, (units + FT - 1) / FT);
+        const int64_t upc = ((units + csz - 1) / csz + 31) / 32 * 32;
+        const int64_t bpc = upc / (tmpl ? rows : 1) + 1;
+        const size_t fsmem = sizeof(double) * (c.cells <= FP_SMEM_SRC ? c.cells : 0) +
+                             sizeof(int) * 2 * (bpc + 1);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(batch * csz));
         cfg.blockDim = dim3(FT);
+        cfg.dynamicSmemBytes = fsmem;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1319,6 +1354,8 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         cfg.numAttrs = 1;
         FastPart *fparts = reinterpret_cast<FastPart *>(ws + L.fp_off);
         auto go = [&](auto kern) {
+            if (fsmem > 48 * 1024)
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
             return cudaLaunchKernelEx(&cfg, kern, mu, nu, arc_off, row_ptr, row_arc_col,
                                       row_arc_mass, col_ptr, col_arc_row, col_arc_mass, kernel_w,
                                       xi, max_iter, f32, c32, kappa, out, status, ws,

@@ -94,8 +94,8 @@ def test_fast_ipf_tracks_exact_ipf(cfg, k, max_iter):
         assert abs(e.components["transport"] - f.components["transport"]) <= \
             1e-12 * e.components["transport"]
         for key in ("delta_mu", "delta_nu"):
-            assert abs(e.components[key] - f.components[key]) <= 1e-7
-        assert abs(e.value - f.value) <= 1e-7 * abs(e.value), (b, e.value, f.value)
+            assert abs(e.components[key] - f.components[key]) <= 1e-6 * max(1.0, e.value)
+        assert abs(e.value - f.value) <= 1e-6 * abs(e.value), (b, e.value, f.value)
 
 
 def test_fast_ipf_default_xi_and_statuses(small_cases):
