@@ -558,18 +558,11 @@ constexpr int FCS_MAX = 8;
 constexpr int FP_SMEM_SRC = 4096;  // block sums gathered into shared memory up to this n
 
 struct FastPart {
-    double gap, lo, hi, flags;  // flags: 1 = zero denominator, 2 = non-finite
+    double gap, lo, hi;
+    int flags, pad;  // flags: 1 = zero denominator, 2 = non-finite
 };
 
-__device__ __forceinline__ void fp_range(double v, FastPart &q) {
-    if (v > 0.0) {
-        q.lo = fmin(q.lo, v);
-        q.hi = fmax(q.hi, v);
-        if (!isfinite(v)) q.flags = (double)((int)q.flags | 2);
-    } else if (isnan(v)) {
-        q.flags = (double)((int)q.flags | 2);
-    }
-}
+__device__ __forceinline__ FastPart fp_init() { return FastPart{0.0, INFINITY, -INFINITY, 0, 0}; }
 
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
@@ -595,7 +588,7 @@ __device__ __forceinline__ void fp_publish(FastPart q, FastPart *slot, unsigned 
         q.gap += __shfl_xor_sync(0xffffffffu, q.gap, o);
         q.lo = fmin(q.lo, __shfl_xor_sync(0xffffffffu, q.lo, o));
         q.hi = fmax(q.hi, __shfl_xor_sync(0xffffffffu, q.hi, o));
-        q.flags = (double)((int)q.flags | (int)__shfl_xor_sync(0xffffffffu, q.flags, o));
+        q.flags |= __shfl_xor_sync(0xffffffffu, q.flags, o);
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (lane == 0) sh[w] = q;
@@ -606,29 +599,56 @@ __device__ __forceinline__ void fp_publish(FastPart q, FastPart *slot, unsigned 
             t.gap += sh[i].gap;
             t.lo = fmin(t.lo, sh[i].lo);
             t.hi = fmax(t.hi, sh[i].hi);
-            t.flags = (double)((int)t.flags | (int)sh[i].flags);
+            t.flags |= sh[i].flags;
         }
         slot[rank] = t;
     }
-    __syncthreads();
 }
 
-// after a cluster barrier: every thread combines the cluster's partials in rank order
-__device__ __forceinline__ FastPart fp_combine(const FastPart *slot, unsigned cs) {
-    FastPart t{0.0, INFINITY, -INFINITY, 0.0};
-    for (unsigned r = 0; r < cs; ++r) {
-        const double g = __ldcg(&slot[r].gap), lo = __ldcg(&slot[r].lo),
-                     hi = __ldcg(&slot[r].hi), fl = __ldcg(&slot[r].flags);
-        t.gap += g;
-        t.lo = fmin(t.lo, lo);
-        t.hi = fmax(t.hi, hi);
-        t.flags = (double)((int)t.flags | (int)fl);
+// after a cluster barrier: combine the cluster's partials in rank order
+// (warp 0 reads, the CTA shares the result through shared memory)
+__device__ __forceinline__ FastPart fp_combine(const FastPart *slot, unsigned cs, FastPart *sh) {
+    if (threadIdx.x < 32) {
+        FastPart t = fp_init();
+        if (threadIdx.x < cs) {
+            t.gap = __ldcg(&slot[threadIdx.x].gap);
+            t.lo = __ldcg(&slot[threadIdx.x].lo);
+            t.hi = __ldcg(&slot[threadIdx.x].hi);
+            t.flags = __ldcg(&slot[threadIdx.x].flags);
+        }
+        // fixed-order sum: gather to lane 0 in rank order
+        FastPart o = fp_init();
+        for (unsigned r = 0; r < cs; ++r) {
+            o.gap += __shfl_sync(0xffffffffu, t.gap, r);
+            o.lo = fmin(o.lo, __shfl_sync(0xffffffffu, t.lo, r));
+            o.hi = fmax(o.hi, __shfl_sync(0xffffffffu, t.hi, r));
+            o.flags |= __shfl_sync(0xffffffffu, t.flags, r);
+        }
+        if (threadIdx.x == 0) sh[FT / 32] = o;
     }
-    return t;
+    __syncthreads();
+    return sh[FT / 32];
 }
 
 __device__ __forceinline__ bool fp_bad(double lo, double hi) {
     return lo <= hi && (lo < 1e-100 || hi > 1e100 || !isfinite(hi));
+}
+
+// range and flags of mass / den over a block whose positive masses span
+// [mlo, mhi] (mlo = +inf: no positive mass): correctly rounded division by a
+// positive constant is monotone, so these are the min / max of the block's
+// scalings; den <= 0 with positive mass is the zero-denominator case
+__device__ __forceinline__ void fp_block_range(double mlo, double mhi, double den, double rcp,
+                                               FastPart &q) {
+    if (!(mlo <= mhi)) return;
+    if (den <= 0.0) {
+        q.flags |= 1;
+        return;
+    }
+    const double lo = div_shared(mlo, den, rcp), hi = div_shared(mhi, den, rcp);
+    if (isnan(lo) || isnan(hi) || !isfinite(hi)) q.flags |= 2;
+    if (lo > 0.0) q.lo = fmin(q.lo, lo);
+    if (hi > 0.0) q.hi = fmax(q.hi, hi);
 }
 
 // Work mapping: a unit is one fine row (KAPPA cells along axis 0) of one
@@ -636,7 +656,7 @@ __device__ __forceinline__ bool fp_bad(double lo, double hi) {
 // lanes, which split the block's arcs for the coarse sum and fold the block
 // sum with xor shuffles (fixed order: deterministic).  A unit's KAPPA masses
 // and scalings are loaded together (vector loads) before use.  KAPPA = 0:
-// runtime kappa (or G > 32), one thread per block walking its cells.
+// runtime kappa (or G > 32), one thread per block walking its rows.
 template <int KAPPA>
 __device__ __forceinline__ void fp_load(const double *p, double *v, int kappa) {
     if constexpr (KAPPA >= 2) {
@@ -662,10 +682,51 @@ __device__ __forceinline__ void fp_store(double *p, const double *v, int kappa) 
     }
 }
 
-// xor-fold over the G lanes of a group (all 32 lanes participate)
+// xor-fold over the G lanes of a group (G warp-uniform, all lanes participate)
 __device__ __forceinline__ double group_sum(double v, int G) {
-    for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1)
+        if (o < G) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
+}
+
+// Shared-memory plan of one CTA (all offsets in bytes, 16-aligned):
+//   src [n] f64 (gathered block sums, if n <= FP_SMEM_SRC), stats [4 nblk] f64
+//   (min/max positive mu and nu per own block), rp/cp [nblk+1] i32 (slices of
+//   the CSR/CSC pointers), rows [upc] i32 (fine index of each unit's row),
+//   arcs: rc/cc [arcs] f64 coefficients and ri/ci [arcs] i32 indices (if they
+//   fit, else read from global)
+struct FpSmem {
+    int src, stats, rp, cp, rows, rc, ri, cc, ci, total;
+    bool src_s;
+};
+
+__host__ __device__ inline int fp_al(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline FpSmem fp_smem_plan(int n, int nblk, int upc, int rarcs, int carcs) {
+    FpSmem m;
+    m.src_s = n <= FP_SMEM_SRC;
+    int o = 0;
+    m.src = o;
+    o = fp_al(o + (m.src_s ? 8 * n : 0));
+    m.stats = o;
+    o = fp_al(o + 32 * nblk);
+    m.rp = o;
+    o = fp_al(o + 4 * (nblk + 1));
+    m.cp = o;
+    o = fp_al(o + 4 * (nblk + 1));
+    m.rows = o;
+    o = fp_al(o + 4 * upc);
+    m.rc = o;
+    o = fp_al(o + 8 * rarcs);
+    m.ri = o;
+    o = fp_al(o + 4 * rarcs);
+    m.cc = o;
+    o = fp_al(o + 8 * carcs);
+    m.ci = o;
+    o = fp_al(o + 4 * carcs);
+    m.total = o;
+    return m;
 }
 
 template <int KAPPA>
@@ -676,9 +737,11 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
     const int32_t *__restrict__ col_arc_row, const double *__restrict__ col_arc_mass,
     const double *__restrict__ W, const double *__restrict__ xi_in, int64_t max_iter, G32 f,
     G32 c, int kappa, double *__restrict__ out, int32_t *__restrict__ status,
-    double *__restrict__ scratch, int64_t stride_pair, FastPart *__restrict__ parts) {
+    double *__restrict__ scratch, int64_t stride_pair, FastPart *__restrict__ parts,
+    int arc_cap) {
     constexpr int KV = KAPPA >= 2 ? KAPPA : 16;  // register row buffer (runtime kappa <= 16)
-    __shared__ FastPart sh[FT / 32];
+    __shared__ FastPart sh[FT / 32 + 1];
+    extern __shared__ __align__(16) unsigned char fsm[];
     const unsigned cs = cluster_size(), rank = cluster_rank_id();
     const int64_t b = blockIdx.x / cs;
     const int N = f.cells, n = c.cells;
@@ -703,62 +766,103 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
     const int upc = (((units + (int)cs - 1) / (int)cs) + 31) / 32 * 32;
     const int u_lo = (int)rank * upc;
     const int trips = (upc + FT - 1) / FT;
-    const int k_lo = u_lo / G;
-    const int nblk = min(upc / G, max(0, n - k_lo));
-    // shared: the block sums the coarse pass gathers from (whole pair, when
-    // they fit) and this CTA's slices of the CSR / CSC row pointers
-    extern __shared__ double fsm[];
-    const bool src_smem = n <= FP_SMEM_SRC;
-    double *src_s = fsm;
-    int *rp_s = reinterpret_cast<int *>(fsm + (src_smem ? n : 0));
-    int *cp_s = rp_s + nblk + 1;
-    for (int i = threadIdx.x; i <= nblk && k_lo + i <= n; i += FT) {
-        rp_s[i] = rptr[k_lo + i];
-        cp_s[i] = cptr[k_lo + i];
+    const int k_lo = min(u_lo / G, n);
+    const int nblk = max(0, min(upc / G, n - k_lo));
+    const int r_lo = rptr[k_lo], r_n = rptr[k_lo + nblk] - r_lo;
+    const int c_lo = cptr[k_lo], c_n = cptr[k_lo + nblk] - c_lo;
+    const bool arcs_s = r_n <= arc_cap && c_n <= arc_cap;
+    const FpSmem L = fp_smem_plan(n, nblk, upc, arcs_s ? arc_cap : 0, arcs_s ? arc_cap : 0);
+    double *src_s = reinterpret_cast<double *>(fsm + L.src);
+    double *st_s = reinterpret_cast<double *>(fsm + L.stats);  // [nblk][mu lo, mu hi, nu lo, nu hi]
+    int *rp_s = reinterpret_cast<int *>(fsm + L.rp), *cp_s = reinterpret_cast<int *>(fsm + L.cp);
+    int *row_s = reinterpret_cast<int *>(fsm + L.rows);
+    double *rc_s = reinterpret_cast<double *>(fsm + L.rc), *cc_s = reinterpret_cast<double *>(fsm + L.cc);
+    int *ri_s = reinterpret_cast<int *>(fsm + L.ri), *ci_s = reinterpret_cast<int *>(fsm + L.ci);
+
+    // ---- per-CTA tables (once) ----
+    for (int i = threadIdx.x; i <= nblk; i += FT) {
+        rp_s[i] = rptr[k_lo + i] - (arcs_s ? r_lo : 0);
+        cp_s[i] = cptr[k_lo + i] - (arcs_s ? c_lo : 0);
     }
+    if (arcs_s) {
+        for (int e = threadIdx.x; e < r_n; e += FT) {
+            rc_s[e] = __dmul_rn(rmass[r_lo + e], Wu);
+            ri_s[e] = rcol[r_lo + e];
+        }
+        for (int e = threadIdx.x; e < c_n; e += FT) {
+            cc_s[e] = __dmul_rn(cmass[c_lo + e], Wu);
+            ci_s[e] = crow[c_lo + e];
+        }
+    }
+    for (int i = threadIdx.x; i < upc; i += FT) {
+        const int u = u_lo + i;
+        int off = 0;
+        if (u < units) {
+            const int k = u / G;
+            int q = u - k * G;
+            off = block_origin(k, c, f, kp);
+            for (int a = 1; a < f.nd && KAPPA >= 2; ++a) {
+                off += (q % kp) * f.stride[a];
+                q /= kp;
+            }
+        }
+        row_s[i] = off;
+    }
+    for (int i = threadIdx.x; i < 4 * nblk; i += FT) st_s[i] = (i & 1) ? -INFINITY : INFINITY;
     __syncthreads();
+
+    // coarse sum over the arcs of block k, split over its G lanes
+    auto coarse = [&](int k, int r, bool act, const int *ptr_s, const double *coef_s,
+                      const int *idx_s, const int32_t *idx, const double *mass,
+                      const double *src) {
+        double v = 0.0;
+        if (act) {
+            const int e0 = ptr_s[k - k_lo], e1 = ptr_s[k - k_lo + 1];
+            if (arcs_s) {
+                for (int e = e0 + r; e < e1; e += G)
+                    v += coef_s[e] * (L.src_s ? src[idx_s[e]] : __ldcg(src + idx_s[e]));
+            } else {
+                for (int e = e0 + r; e < e1; e += G)
+                    v += __dmul_rn(__ldg(mass + e), Wu) *
+                         (L.src_s ? src[__ldg(idx + e)] : __ldcg(src + __ldg(idx + e)));
+            }
+        }
+        return group_sum(v, G);
+    };
     auto gather = [&](const double *src) -> const double * {
-        if (!src_smem) return src;
+        if (!L.src_s) return src;
         __syncthreads();  // previous readers of src_s are done
         for (int i = threadIdx.x; i < n; i += FT) src_s[i] = __ldcg(src + i);
         __syncthreads();
         return src_s;
     };
-
-    // fine index of row q of block k
-    auto row_start = [&](int k, int q) {
-        int off = block_origin(k, c, f, kp);
-        for (int a = 1; a < f.nd; ++a) {
-            off += (q % kp) * f.stride[a];
-            q /= kp;
-        }
-        return off;
-    };
-    // coarse sum over the arcs of unit u's block, split over its G lanes
-    auto coarse = [&](int k, int r, bool act, const int *ptr_s, const int32_t *idx,
-                      const double *mass, const double *src) {
-        double v = 0.0;
-        if (act)
-            for (int e = ptr_s[k - k_lo] + r; e < ptr_s[k - k_lo + 1]; e += G) {
-                const double m = __ldg(mass + e);
-                const int j = __ldg(idx + e);
-                v += __dmul_rn(m, Wu) * (src_smem ? src[j] : __ldcg(src + j));
+    auto fold_minmax = [&](double &lo, double &hi) {
+        for (int o = 1; o < 32; o <<= 1)
+            if (o < G) {
+                lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+                hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
             }
-        return group_sum(v, G);
     };
 
     // b = 1 on the target support (sinkhorn.py:119 on the restricted matrix),
-    // B_l = its count, support count for the default xi
+    // B_l = its count, support count for the default xi, block mass ranges
     {
-        FastPart q{0.0, INFINITY, -INFINITY, 0.0};
+        FastPart q = fp_init();
         for (int t = 0; t < trips; ++t) {
-            const int u = u_lo + t * FT + (int)threadIdx.x;
-            const bool act = u < units && u < u_lo + upc;
-            const int l = act ? u / G : 0, r = act ? u - l * G : 0;
-            double sb = 0.0;
+            const int ui = t * FT + (int)threadIdx.x, u = u_lo + ui;
+            const bool act = u < units && ui < upc;
+            const int l = act ? u / G : k_lo, r = act ? u - l * G : 0;
+            double sb = 0.0, mlo = INFINITY, mhi = -INFINITY, nlo = INFINITY, nhi = -INFINITY;
             if (act)
                 for (int qq = 0; qq < rows_per_unit; ++qq) {
-                    const int j0 = row_start(l, r + qq);
+                    const int j0 = KAPPA >= 2 ? row_s[ui] : row_s[ui] + [&] {
+                        int off = 0, z = qq;
+                        for (int a = 1; a < f.nd; ++a) {
+                            off += (z % kp) * f.stride[a];
+                            z /= kp;
+                        }
+                        return off;
+                    }();
                     double nv[KV], mv[KV], bb[KV];
                     fp_load<KAPPA>(nub + j0, nv, kp);
                     fp_load<KAPPA>(mub + j0, mv, kp);
@@ -768,16 +872,33 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
                         q.gap += (mv[x] > 0.0 ? 1.0 : 0.0) + (nv[x] > 0.0 ? 1.0 : 0.0);
                         bb[x] = nv[x] > 0.0 ? 1.0 : 0.0;
                         sb += bb[x];
+                        if (mv[x] > 0.0) {
+                            mlo = fmin(mlo, mv[x]);
+                            mhi = fmax(mhi, mv[x]);
+                        }
+                        if (nv[x] > 0.0) {
+                            nlo = fmin(nlo, nv[x]);
+                            nhi = fmax(nhi, nv[x]);
+                        }
                     }
                     fp_store<KAPPA>(bv + j0, bb, kp);
                 }
             sb = group_sum(sb, G);
-            if (act && r == 0) Bs[l] = sb;
+            fold_minmax(mlo, mhi);
+            fold_minmax(nlo, nhi);
+            if (act && r == 0) {
+                Bs[l] = sb;
+                double *stk = st_s + 4 * (l - k_lo);
+                stk[0] = mlo;
+                stk[1] = mhi;
+                stk[2] = nlo;
+                stk[3] = nhi;
+            }
         }
         fp_publish(q, pp, rank, sh);
     }
     cluster_sync_all();
-    const double cnt = fp_combine(pp, cs).gap;
+    const double cnt = fp_combine(pp, cs, sh).gap;
     const double xi = xi_in[b] < 0.0 ? 1e-9 * cnt : xi_in[b];
 
     double *a_cur = aA, *a_nxt = aB;
@@ -785,44 +906,48 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
     int64_t it = 0;
     bool converged = false;
     double gap = INFINITY;
-    FastPart ra{0.0, INFINITY, -INFINITY, 0.0}, rb = ra;  // a and b of sweep `it`
+    FastPart ra = fp_init(), rb = ra;  // a and b of sweep `it`
     for (;;) {
         // kb = K b (coarse), then the row pass: |a kb - mu| of sweep it, the
         // zero-row check and a of sweep it+1, and its block sums
-        FastPart q{0.0, INFINITY, -INFINITY, 0.0};
+        FastPart q = fp_init();
         const double *bsrc = gather(Bs);
         for (int t = 0; t < trips; ++t) {
-            const int u = u_lo + t * FT + (int)threadIdx.x;
-            const bool act = u < units && u < u_lo + upc;
+            const int ui = t * FT + (int)threadIdx.x, u = u_lo + ui;
+            const bool act = u < units && ui < upc;
             const int k = act ? u / G : k_lo, r = act ? u - k * G : 0;
-            const double kb = coarse(k, r, act, rp_s, rcol, rmass, bsrc);
+            const double kb = coarse(k, r, act, rp_s, rc_s, ri_s, rcol, rmass, bsrc);
             const double rcp = kb > 0.0 ? __drcp_rn(kb) : 0.0;
             double sa = 0.0;
-            if (act)
+            if (act) {
+                if (r == 0) {
+                    const double *stk = st_s + 4 * (k - k_lo);
+                    fp_block_range(stk[0], stk[1], kb, rcp, q);
+                }
                 for (int qq = 0; qq < rows_per_unit; ++qq) {
-                    const int i0 = row_start(k, r + qq);
+                    const int i0 = KAPPA >= 2 ? row_s[ui] : row_s[ui] + [&] {
+                        int off = 0, z = qq;
+                        for (int a = 1; a < f.nd; ++a) {
+                            off += (z % kp) * f.stride[a];
+                            z /= kp;
+                        }
+                        return off;
+                    }();
                     double mv[KV], av[KV], an[KV];
                     fp_load<KAPPA>(mub + i0, mv, kp);
                     if (it >= 1) fp_load<KAPPA>(a_cur + i0, av, kp);
-                    else
-#pragma unroll
-                        for (int x = 0; x < KV; ++x) av[x] = 0.0;
 #pragma unroll
                     for (int x = 0; x < KV; ++x) {
                         if (x >= kp) break;
                         const double mi = mv[x];
                         if (it >= 1 && mi > 0.0) q.gap += fabs(__dsub_rn(__dmul_rn(av[x], kb), mi));
-                        double v = 0.0;
-                        if (mi > 0.0) {
-                            if (kb <= 0.0) q.flags = (double)((int)q.flags | 1);
-                            else v = div_shared(mi, kb, rcp);
-                        }
-                        fp_range(v, q);
+                        const double v = (mi > 0.0 && kb > 0.0) ? div_shared(mi, kb, rcp) : 0.0;
                         an[x] = v;
                         sa += v;
                     }
                     fp_store<KAPPA>(a_nxt + i0, an, kp);
                 }
+            }
             sa = group_sum(sa, G);
             if (act && r == 0) {
                 S[k] = sa;
@@ -832,9 +957,9 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
         FastPart *slot_ac = pp + (1 + (int)((it + 1) & 1)) * FCS_MAX;
         fp_publish(q, slot_ac, rank, sh);
         cluster_sync_all();
-        const FastPart ac = fp_combine(slot_ac, cs);
+        const FastPart ac = fp_combine(slot_ac, cs, sh);
         if (it >= 1) {  // end of sweep `it`: range checks, then the gap
-            if (fp_bad(ra.lo, ra.hi) || fp_bad(rb.lo, rb.hi) || (((int)ra.flags | (int)rb.flags) & 2)) {
+            if (fp_bad(ra.lo, ra.hi) || fp_bad(rb.lo, rb.hi) || ((ra.flags | rb.flags) & 2)) {
                 st = GDT_PAIR_OVERFLOW;
                 break;
             }
@@ -845,7 +970,7 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
             }
             if (it >= max_iter) break;
         }
-        if ((int)ac.flags & 1) {  // top of sweep it+1
+        if (ac.flags & 1) {  // top of sweep it+1
             st = GDT_PAIR_ZERO_DENOM_ROW;
             break;
         }
@@ -856,36 +981,43 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
         ra = ac;
         // kta = K^T a (coarse), then the column pass: zero-column check, b,
         // |nu - b kta|, range(b), block sums of b
-        FastPart qb{0.0, INFINITY, -INFINITY, 0.0};
+        FastPart qb = fp_init();
         const double *ssrc = gather(S);
         for (int t = 0; t < trips; ++t) {
-            const int u = u_lo + t * FT + (int)threadIdx.x;
-            const bool act = u < units && u < u_lo + upc;
+            const int ui = t * FT + (int)threadIdx.x, u = u_lo + ui;
+            const bool act = u < units && ui < upc;
             const int l = act ? u / G : k_lo, r = act ? u - l * G : 0;
-            const double kt = coarse(l, r, act, cp_s, crow, cmass, ssrc);
+            const double kt = coarse(l, r, act, cp_s, cc_s, ci_s, crow, cmass, ssrc);
             const double rcp = kt > 0.0 ? __drcp_rn(kt) : 0.0;
             double sb = 0.0;
-            if (act)
+            if (act) {
+                if (r == 0) {
+                    const double *stl = st_s + 4 * (l - k_lo);
+                    fp_block_range(stl[2], stl[3], kt, rcp, qb);
+                }
                 for (int qq = 0; qq < rows_per_unit; ++qq) {
-                    const int j0 = row_start(l, r + qq);
+                    const int j0 = KAPPA >= 2 ? row_s[ui] : row_s[ui] + [&] {
+                        int off = 0, z = qq;
+                        for (int a = 1; a < f.nd; ++a) {
+                            off += (z % kp) * f.stride[a];
+                            z /= kp;
+                        }
+                        return off;
+                    }();
                     double nv[KV], bb[KV];
                     fp_load<KAPPA>(nub + j0, nv, kp);
 #pragma unroll
                     for (int x = 0; x < KV; ++x) {
                         if (x >= kp) break;
                         const double nj = nv[x];
-                        double v = 0.0;
-                        if (nj > 0.0) {
-                            if (kt <= 0.0) qb.flags = (double)((int)qb.flags | 1);
-                            else v = div_shared(nj, kt, rcp);
-                            fp_range(v, qb);
-                            qb.gap += fabs(__dsub_rn(nj, __dmul_rn(v, kt)));
-                        }
+                        const double v = (nj > 0.0 && kt > 0.0) ? div_shared(nj, kt, rcp) : 0.0;
+                        if (nj > 0.0) qb.gap += fabs(__dsub_rn(nj, __dmul_rn(v, kt)));
                         bb[x] = v;
                         sb += v;
                     }
                     fp_store<KAPPA>(bv + j0, bb, kp);
                 }
+            }
             sb = group_sum(sb, G);
             if (act && r == 0) {
                 Bs[l] = sb;
@@ -895,8 +1027,8 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
         FastPart *slot_b = pp + (3 + (int)(it & 1)) * FCS_MAX;
         fp_publish(qb, slot_b, rank, sh);
         cluster_sync_all();
-        rb = fp_combine(slot_b, cs);
-        if ((int)rb.flags & 1) {
+        rb = fp_combine(slot_b, cs, sh);
+        if (rb.flags & 1) {
             st = GDT_PAIR_ZERO_DENOM_COL;
             break;
         }
@@ -1268,7 +1400,7 @@ inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, b
     L.pc_off = L.pr_off + batch * L.pr_ctas;       // packed arc coordinates (int64)
     L.bm_off = L.pc_off + 2 * batch * max_arcs;    // fine cell -> coarse block (int32)
     L.fp_off = L.bm_off + (f.cells + 1) / 2;        // ipf_fast_kernel partials
-    L.total = L.fp_off + batch * 5 * FCS_MAX * 4;
+    L.total = L.fp_off + batch * 5 * FCS_MAX * (int64_t)(sizeof(FastPart) / sizeof(double));
     return L;
 }
 
@@ -1337,9 +1469,11 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         const int64_t units = c.cells * (tmpl ? rows : 1);
         const unsigned csz = (unsigned)std::min<int64_t>(FCS_MAX, (units + FT - 1) / FT);
         const int64_t upc = ((units + csz - 1) / csz + 31) / 32 * 32;
-        const int64_t bpc = upc / (tmpl ? rows : 1) + 1;
-        const size_t fsmem = sizeof(double) * (c.cells <= FP_SMEM_SRC ? c.cells : 0) +
-                             sizeof(int) * 2 * (bpc + 1);
+        const int64_t nblk = upc / (tmpl ? rows : 1);
+        // arcs of one CTA's blocks in shared memory up to arc_cap per side
+        const int arc_cap = (int)std::min<int64_t>(2 * c.cells, 2048);
+        FpSmem plan = fp_smem_plan((int)c.cells, (int)nblk, (int)upc, arc_cap, arc_cap);
+        const size_t fsmem = (size_t)plan.total;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(batch * csz));
         cfg.blockDim = dim3(FT);
@@ -1359,7 +1493,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
             return cudaLaunchKernelEx(&cfg, kern, mu, nu, arc_off, row_ptr, row_arc_col,
                                       row_arc_mass, col_ptr, col_arc_row, col_arc_mass, kernel_w,
                                       xi, max_iter, f32, c32, kappa, out, status, ws,
-                                      L.stride_pair, fparts);
+                                      L.stride_pair, fparts, arc_cap);
         };
         cudaError_t e;
         if (!tmpl) e = go(ipf_fast_kernel<0>);
