@@ -330,15 +330,13 @@ def run_b200(args):
     prim_ms = statistics.mean(stage_ms[(k, p, "primal")] for k, p, _, _ in stages)
     sweeps = statistics.mean(
         float(np.mean(E.to_host(dp.prim_out)[:, 4])) for _, _, _, dp in stages)
-    # fp32 mode (ipf_fast_kernel): per sweep read mu, a, write a; read nu,
-    # write b = 40 B/cell; init 24 B/cell and the closing gap pass 24 B/cell;
-    # moments/TV pass 32 B/cell.  fp64 mode (ipf_kernel): SURVEY 8(d) model.
-    if wl.precision == "fp32":
-        ipf_bytes = (40.0 * sweeps + 48.0 + 32.0) * Nf * ppr
-        bytes_model = "(40*S + 48 + 32) * N^d bytes per pair: IPF sweeps + init/closing pass + TV"
-    else:
-        ipf_bytes = (48.0 * sweeps + 32.0) * Nf * ppr
-        bytes_model = "(48*S + 32) * N^d bytes per pair (SURVEY.md 8(d))"
+    # algorithmic bytes: 48 B per cell and executed sweep
+    # (read b, mu, write a; read a, nu, write b) + 32 B per cell for TV and
+    # pricing.  ipf_fast_kernel (fp32 mode) moves fewer: it recomputes a and
+    # b from mu, nu and the per-block denominators instead of storing them
+    # every sweep (16 B per cell and sweep; the ncu DRAM traffic is in profiles/).
+    ipf_bytes = (48.0 * sweeps + 32.0) * Nf * ppr
+    bytes_model = "(48*S + 32) * N^d bytes per pair (SURVEY.md 8(d))"
     ipf_roof = {"bound": "hbm", "kernel": ("ipf_fast_kernel" if wl.precision == "fp32" else
                                            "ipf_kernel") + " + moments_tv + price (primal stage)",
                 "achieved": ipf_bytes / (prim_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",

@@ -555,7 +555,6 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
 // Per sweep and fine cell: read mu, a, write a; read nu, write b = 40 bytes.
 constexpr int FT = 256;  // threads per CTA of ipf_fast_kernel
 constexpr int FCS_MAX = 8;
-constexpr int FP_SMEM_SRC = 4096;  // block sums gathered into shared memory up to this n
 
 struct FastPart {
     double gap, lo, hi;
@@ -581,8 +580,17 @@ __device__ __forceinline__ unsigned cluster_size() {
     return r;
 }
 
-// CTA-reduce q, thread 0 stores it in slot[rank]
-__device__ __forceinline__ void fp_publish(FastPart q, FastPart *slot, unsigned rank, FastPart *sh) {
+// address of the same shared variable in CTA `rank` of the cluster (DSMEM)
+template <class T>
+__device__ __forceinline__ T *dsmem(T *p, unsigned rank) {
+    uint64_t out;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+    return reinterpret_cast<T *>(out);
+}
+
+// CTA-reduce q into *mine (this CTA's shared slot, read by the cluster after
+// the next cluster barrier)
+__device__ __forceinline__ void fp_publish(FastPart q, FastPart *mine, FastPart *sh) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         q.gap += __shfl_xor_sync(0xffffffffu, q.gap, o);
@@ -601,22 +609,16 @@ __device__ __forceinline__ void fp_publish(FastPart q, FastPart *slot, unsigned 
             t.hi = fmax(t.hi, sh[i].hi);
             t.flags |= sh[i].flags;
         }
-        slot[rank] = t;
+        *mine = t;
     }
 }
 
-// after a cluster barrier: combine the cluster's partials in rank order
-// (warp 0 reads, the CTA shares the result through shared memory)
-__device__ __forceinline__ FastPart fp_combine(const FastPart *slot, unsigned cs, FastPart *sh) {
+// after a cluster barrier: combine the cluster's slots in rank order (thread
+// 0 reads them over DSMEM, the CTA shares the result through shared memory)
+__device__ __forceinline__ FastPart fp_combine(FastPart *mine, unsigned cs, FastPart *sh) {
     if (threadIdx.x < 32) {
-        FastPart t = fp_init();
-        if (threadIdx.x < cs) {
-            t.gap = __ldcg(&slot[threadIdx.x].gap);
-            t.lo = __ldcg(&slot[threadIdx.x].lo);
-            t.hi = __ldcg(&slot[threadIdx.x].hi);
-            t.flags = __ldcg(&slot[threadIdx.x].flags);
-        }
-        // fixed-order sum: gather to lane 0 in rank order
+        // lane r reads CTA r's slot; lane 0 combines them in rank order
+        const FastPart t = threadIdx.x < cs ? *dsmem(mine, threadIdx.x) : fp_init();
         FastPart o = fp_init();
         for (unsigned r = 0; r < cs; ++r) {
             o.gap += __shfl_sync(0xffffffffu, t.gap, r);
@@ -651,23 +653,29 @@ __device__ __forceinline__ void fp_block_range(double mlo, double mhi, double de
     if (hi > 0.0) q.hi = fmax(q.hi, hi);
 }
 
+// scaling of one cell: mass / den on the support, 0 elsewhere or when den <= 0
+__device__ __forceinline__ double fp_scale(double m, double den, double rcp) {
+    return (m > 0.0 && den > 0.0) ? div_shared(m, den, rcp) : 0.0;
+}
+
+__device__ __forceinline__ double fp_rcp(double den) { return den > 0.0 ? __drcp_rn(den) : 0.0; }
+
 // Work mapping: a unit is one fine row (KAPPA cells along axis 0) of one
 // coarse block; the G = kappa^(d-1) rows of a block sit in G consecutive
-// lanes, which split the block's arcs for the coarse sum and fold the block
-// sum with xor shuffles (fixed order: deterministic).  A unit's KAPPA masses
-// and scalings are loaded together (vector loads) before use.  KAPPA = 0:
-// runtime kappa (or G > 32), one thread per block walking its rows.
+// lanes, which fold the block sum with xor shuffles (fixed order:
+// deterministic).  KAPPA = 0: runtime kappa (or G > 32), one thread per
+// block walking its rows.
 template <int KAPPA>
 __device__ __forceinline__ void fp_load(const double *p, double *v, int kappa) {
     if constexpr (KAPPA >= 2) {
 #pragma unroll
         for (int x = 0; x < KAPPA; x += 2) {
-            const double2 t = *reinterpret_cast<const double2 *>(p + x);
+            const double2 t = __ldg(reinterpret_cast<const double2 *>(p + x));
             v[x] = t.x;
             v[x + 1] = t.y;
         }
     } else {
-        for (int x = 0; x < kappa; ++x) v[x] = p[x];
+        for (int x = 0; x < kappa; ++x) v[x] = __ldg(p + x);
     }
 }
 
@@ -690,27 +698,32 @@ __device__ __forceinline__ double group_sum(double v, int G) {
     return v;
 }
 
-// Shared-memory plan of one CTA (all offsets in bytes, 16-aligned):
-//   src [n] f64 (gathered block sums, if n <= FP_SMEM_SRC), stats [4 nblk] f64
-//   (min/max positive mu and nu per own block), rp/cp [nblk+1] i32 (slices of
-//   the CSR/CSC pointers), rows [upc] i32 (fine index of each unit's row),
-//   arcs: rc/cc [arcs] f64 coefficients and ri/ci [arcs] i32 indices (if they
-//   fit, else read from global)
+// Shared-memory plan of one CTA (byte offsets, 16-aligned):
+//   src [n] f64      block sums of the whole pair gathered over DSMEM
+//   own [2 nblk] f64 this CTA's block sums of a (S) and b (B), read remotely
+//   blk [5 nblk] f64 per own block: min/max positive mu, min/max positive nu,
+//                    and kb of the previous sweep (to recompute a)
+//   kv  [2 nblk] f64 per own block: current kb and kta
+//   rp/cp [nblk+1] i32 CSR / CSC pointer slices, rows [upc] i32 row starts
+//   rc/cc [cap] f64 arc coefficients m W, ri/ci [cap] i32 arc endpoints,
+//   prod [cap] f64 per-arc products of the current coarse pass
 struct FpSmem {
-    int src, stats, rp, cp, rows, rc, ri, cc, ci, total;
-    bool src_s;
+    int src, own, blk, kv, rp, cp, rows, rc, ri, cc, ci, prod, total;
 };
 
 __host__ __device__ inline int fp_al(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline FpSmem fp_smem_plan(int n, int nblk, int upc, int rarcs, int carcs) {
+__host__ __device__ inline FpSmem fp_smem_plan(int n, int nblk, int upc, int cap) {
     FpSmem m;
-    m.src_s = n <= FP_SMEM_SRC;
     int o = 0;
     m.src = o;
-    o = fp_al(o + (m.src_s ? 8 * n : 0));
-    m.stats = o;
-    o = fp_al(o + 32 * nblk);
+    o = fp_al(o + 8 * n);
+    m.own = o;
+    o = fp_al(o + 16 * nblk);
+    m.blk = o;
+    o = fp_al(o + 40 * nblk);
+    m.kv = o;
+    o = fp_al(o + 16 * nblk);
     m.rp = o;
     o = fp_al(o + 4 * (nblk + 1));
     m.cp = o;
@@ -718,13 +731,15 @@ __host__ __device__ inline FpSmem fp_smem_plan(int n, int nblk, int upc, int rar
     m.rows = o;
     o = fp_al(o + 4 * upc);
     m.rc = o;
-    o = fp_al(o + 8 * rarcs);
+    o = fp_al(o + 8 * cap);
     m.ri = o;
-    o = fp_al(o + 4 * rarcs);
+    o = fp_al(o + 4 * cap);
     m.cc = o;
-    o = fp_al(o + 8 * carcs);
+    o = fp_al(o + 8 * cap);
     m.ci = o;
-    o = fp_al(o + 4 * carcs);
+    o = fp_al(o + 4 * cap);
+    m.prod = o;
+    o = fp_al(o + 8 * cap);
     m.total = o;
     return m;
 }
@@ -737,10 +752,10 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
     const int32_t *__restrict__ col_arc_row, const double *__restrict__ col_arc_mass,
     const double *__restrict__ W, const double *__restrict__ xi_in, int64_t max_iter, G32 f,
     G32 c, int kappa, double *__restrict__ out, int32_t *__restrict__ status,
-    double *__restrict__ scratch, int64_t stride_pair, FastPart *__restrict__ parts,
-    int arc_cap) {
+    double *__restrict__ scratch, int64_t stride_pair, int cap) {
     constexpr int KV = KAPPA >= 2 ? KAPPA : 16;  // register row buffer (runtime kappa <= 16)
     __shared__ FastPart sh[FT / 32 + 1];
+    __shared__ FastPart slot[3];  // this CTA's partials: init, row pass, column pass
     extern __shared__ __align__(16) unsigned char fsm[];
     const unsigned cs = cluster_size(), rank = cluster_rank_id();
     const int64_t b = blockIdx.x / cs;
@@ -752,9 +767,7 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
     const int32_t *rcol = row_arc_col + a0, *crow = col_arc_row + a0;
     const double *rmass = row_arc_mass + a0, *cmass = col_arc_mass + a0;
     double *ws = scratch + b * stride_pair;
-    double *aA = ws, *aB = ws + N, *bv = ws + 2 * N, *kbv = ws + 3 * N, *ktv = ws + 3 * N + n;
-    double *S = ws + 3 * N + 2 * n, *Bs = ws + 3 * N + 3 * n;  // block sums of a and b
-    FastPart *pp = parts + b * 5 * FCS_MAX;  // slots: init, AC[2], B[2]
+    double *aA = ws, *bv = ws + 2 * N, *kbv = ws + 3 * N, *ktv = ws + 3 * N + n;
     const int kp = KAPPA >= 2 ? KAPPA : kappa;
     int rows = 1;  // fine rows per block
     for (int a = 1; a < f.nd; ++a) rows *= kp;
@@ -764,25 +777,29 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
     // CTA `rank` owns a contiguous, warp-aligned range of units (so its blocks
     // are contiguous too); trip counts are CTA-uniform (shuffles need every lane)
     const int upc = (((units + (int)cs - 1) / (int)cs) + 31) / 32 * 32;
+    const int bpc = upc / G;  // blocks per CTA (owner of block k: k / bpc)
     const int u_lo = (int)rank * upc;
     const int trips = (upc + FT - 1) / FT;
-    const int k_lo = min(u_lo / G, n);
-    const int nblk = max(0, min(upc / G, n - k_lo));
+    const int k_lo = min((int)rank * bpc, n);
+    const int nblk = max(0, min(bpc, n - k_lo));
     const int r_lo = rptr[k_lo], r_n = rptr[k_lo + nblk] - r_lo;
     const int c_lo = cptr[k_lo], c_n = cptr[k_lo + nblk] - c_lo;
-    const bool arcs_s = r_n <= arc_cap && c_n <= arc_cap;
-    const FpSmem L = fp_smem_plan(n, nblk, upc, arcs_s ? arc_cap : 0, arcs_s ? arc_cap : 0);
+    const bool arcs_s = r_n <= cap && c_n <= cap;
+    const FpSmem L = fp_smem_plan(n, bpc, upc, cap);
     double *src_s = reinterpret_cast<double *>(fsm + L.src);
-    double *st_s = reinterpret_cast<double *>(fsm + L.stats);  // [nblk][mu lo, mu hi, nu lo, nu hi]
+    double *ownS = reinterpret_cast<double *>(fsm + L.own), *ownB = ownS + bpc;
+    double *blk_s = reinterpret_cast<double *>(fsm + L.blk);  // [bpc][5]
+    double *kb_s = reinterpret_cast<double *>(fsm + L.kv), *kt_s = kb_s + bpc;
     int *rp_s = reinterpret_cast<int *>(fsm + L.rp), *cp_s = reinterpret_cast<int *>(fsm + L.cp);
     int *row_s = reinterpret_cast<int *>(fsm + L.rows);
     double *rc_s = reinterpret_cast<double *>(fsm + L.rc), *cc_s = reinterpret_cast<double *>(fsm + L.cc);
     int *ri_s = reinterpret_cast<int *>(fsm + L.ri), *ci_s = reinterpret_cast<int *>(fsm + L.ci);
+    double *prod_s = reinterpret_cast<double *>(fsm + L.prod);
 
     // ---- per-CTA tables (once) ----
     for (int i = threadIdx.x; i <= nblk; i += FT) {
-        rp_s[i] = rptr[k_lo + i] - (arcs_s ? r_lo : 0);
-        cp_s[i] = cptr[k_lo + i] - (arcs_s ? c_lo : 0);
+        rp_s[i] = rptr[k_lo + i] - r_lo;
+        cp_s[i] = cptr[k_lo + i] - c_lo;
     }
     if (arcs_s) {
         for (int e = threadIdx.x; e < r_n; e += FT) {
@@ -808,40 +825,52 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
         }
         row_s[i] = off;
     }
-    for (int i = threadIdx.x; i < 4 * nblk; i += FT) st_s[i] = (i & 1) ? -INFINITY : INFINITY;
+    for (int i = threadIdx.x; i < 5 * bpc; i += FT) {
+        const int w = i % 5;
+        blk_s[i] = w == 4 ? 0.0 : ((w & 1) ? -INFINITY : INFINITY);
+    }
     __syncthreads();
 
-    // coarse sum over the arcs of block k, split over its G lanes
-    auto coarse = [&](int k, int r, bool act, const int *ptr_s, const double *coef_s,
-                      const int *idx_s, const int32_t *idx, const double *mass,
-                      const double *src) {
+    auto row_index = [&](int ui, int qq) {
+        if constexpr (KAPPA >= 2) {
+            return row_s[ui];
+        } else {
+            int off = 0, z = qq;
+            for (int a = 1; a < f.nd; ++a) {
+                off += (z % kp) * f.stride[a];
+                z /= kp;
+            }
+            return row_s[ui] + off;
+        }
+    };
+    // the pair's block sums (a: own = ownS, b: own = ownB) into src_s over DSMEM
+    auto gather = [&](double *own) {
+        for (int i = threadIdx.x; i < n; i += FT) {
+            const unsigned r = (unsigned)(i / bpc);
+            src_s[i] = *dsmem(own + (i - (int)r * bpc), r);
+        }
+        __syncthreads();
+    };
+    // per-arc products coef * src[endpoint] of this CTA's arcs, then each
+    // block's G lanes add its arcs (fixed order)
+    auto products = [&](const double *coef_s, const int *idx_s, int count) {
+        if (arcs_s)
+            for (int e = threadIdx.x; e < count; e += FT) prod_s[e] = coef_s[e] * src_s[idx_s[e]];
+        __syncthreads();
+    };
+    auto coarse = [&](int k, int r, bool act, const int *ptr_s, int e_base, const int32_t *idx,
+                      const double *mass) {
         double v = 0.0;
         if (act) {
             const int e0 = ptr_s[k - k_lo], e1 = ptr_s[k - k_lo + 1];
             if (arcs_s) {
-                for (int e = e0 + r; e < e1; e += G)
-                    v += coef_s[e] * (L.src_s ? src[idx_s[e]] : __ldcg(src + idx_s[e]));
+                for (int e = e0 + r; e < e1; e += G) v += prod_s[e];
             } else {
                 for (int e = e0 + r; e < e1; e += G)
-                    v += __dmul_rn(__ldg(mass + e), Wu) *
-                         (L.src_s ? src[__ldg(idx + e)] : __ldcg(src + __ldg(idx + e)));
+                    v += __dmul_rn(__ldg(mass + e_base + e), Wu) * src_s[__ldg(idx + e_base + e)];
             }
         }
         return group_sum(v, G);
-    };
-    auto gather = [&](const double *src) -> const double * {
-        if (!L.src_s) return src;
-        __syncthreads();  // previous readers of src_s are done
-        for (int i = threadIdx.x; i < n; i += FT) src_s[i] = __ldcg(src + i);
-        __syncthreads();
-        return src_s;
-    };
-    auto fold_minmax = [&](double &lo, double &hi) {
-        for (int o = 1; o < 32; o <<= 1)
-            if (o < G) {
-                lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-                hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-            }
     };
 
     // b = 1 on the target support (sinkhorn.py:119 on the restricted matrix),
@@ -855,23 +884,15 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
             double sb = 0.0, mlo = INFINITY, mhi = -INFINITY, nlo = INFINITY, nhi = -INFINITY;
             if (act)
                 for (int qq = 0; qq < rows_per_unit; ++qq) {
-                    const int j0 = KAPPA >= 2 ? row_s[ui] : row_s[ui] + [&] {
-                        int off = 0, z = qq;
-                        for (int a = 1; a < f.nd; ++a) {
-                            off += (z % kp) * f.stride[a];
-                            z /= kp;
-                        }
-                        return off;
-                    }();
-                    double nv[KV], mv[KV], bb[KV];
+                    const int j0 = row_index(ui, qq);
+                    double nv[KV], mv[KV];
                     fp_load<KAPPA>(nub + j0, nv, kp);
                     fp_load<KAPPA>(mub + j0, mv, kp);
 #pragma unroll
                     for (int x = 0; x < KV; ++x) {
                         if (x >= kp) break;
                         q.gap += (mv[x] > 0.0 ? 1.0 : 0.0) + (nv[x] > 0.0 ? 1.0 : 0.0);
-                        bb[x] = nv[x] > 0.0 ? 1.0 : 0.0;
-                        sb += bb[x];
+                        sb += nv[x] > 0.0 ? 1.0 : 0.0;
                         if (mv[x] > 0.0) {
                             mlo = fmin(mlo, mv[x]);
                             mhi = fmax(mhi, mv[x]);
@@ -881,83 +902,77 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
                             nhi = fmax(nhi, nv[x]);
                         }
                     }
-                    fp_store<KAPPA>(bv + j0, bb, kp);
                 }
             sb = group_sum(sb, G);
-            fold_minmax(mlo, mhi);
-            fold_minmax(nlo, nhi);
+            for (int o = 1; o < 32; o <<= 1)
+                if (o < G) {
+                    mlo = fmin(mlo, __shfl_xor_sync(0xffffffffu, mlo, o));
+                    mhi = fmax(mhi, __shfl_xor_sync(0xffffffffu, mhi, o));
+                    nlo = fmin(nlo, __shfl_xor_sync(0xffffffffu, nlo, o));
+                    nhi = fmax(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
+                }
             if (act && r == 0) {
-                Bs[l] = sb;
-                double *stk = st_s + 4 * (l - k_lo);
-                stk[0] = mlo;
-                stk[1] = mhi;
-                stk[2] = nlo;
-                stk[3] = nhi;
+                ownB[l - k_lo] = sb;
+                double *bk = blk_s + 5 * (l - k_lo);
+                bk[0] = mlo;
+                bk[1] = mhi;
+                bk[2] = nlo;
+                bk[3] = nhi;
             }
         }
-        fp_publish(q, pp, rank, sh);
+        fp_publish(q, &slot[0], sh);
     }
     cluster_sync_all();
-    const double cnt = fp_combine(pp, cs, sh).gap;
+    const double cnt = fp_combine(&slot[0], cs, sh).gap;
     const double xi = xi_in[b] < 0.0 ? 1e-9 * cnt : xi_in[b];
 
-    double *a_cur = aA, *a_nxt = aB;
     int st = GDT_PAIR_OK;
     int64_t it = 0;
     bool converged = false;
     double gap = INFINITY;
     FastPart ra = fp_init(), rb = ra;  // a and b of sweep `it`
     for (;;) {
-        // kb = K b (coarse), then the row pass: |a kb - mu| of sweep it, the
-        // zero-row check and a of sweep it+1, and its block sums
+        // kb = K b (coarse); row pass: a of sweep it recomputed from its kb
+        // (blk[4]) for |a kb - mu|, the zero-row check, a of sweep it+1 and
+        // its block sums.  a is not stored: the closing pass writes the final one.
         FastPart q = fp_init();
-        const double *bsrc = gather(Bs);
+        gather(ownB);
+        products(rc_s, ri_s, r_n);
         for (int t = 0; t < trips; ++t) {
             const int ui = t * FT + (int)threadIdx.x, u = u_lo + ui;
             const bool act = u < units && ui < upc;
             const int k = act ? u / G : k_lo, r = act ? u - k * G : 0;
-            const double kb = coarse(k, r, act, rp_s, rc_s, ri_s, rcol, rmass, bsrc);
-            const double rcp = kb > 0.0 ? __drcp_rn(kb) : 0.0;
+            const double kb = coarse(k, r, act, rp_s, r_lo, rcol, rmass);
+            const double rcp = fp_rcp(kb);
+            double *bk = blk_s + 5 * (k - k_lo);
+            const double kbo = act ? bk[4] : 0.0, rcpo = fp_rcp(kbo);
             double sa = 0.0;
             if (act) {
-                if (r == 0) {
-                    const double *stk = st_s + 4 * (k - k_lo);
-                    fp_block_range(stk[0], stk[1], kb, rcp, q);
-                }
+                if (r == 0) fp_block_range(bk[0], bk[1], kb, rcp, q);
                 for (int qq = 0; qq < rows_per_unit; ++qq) {
-                    const int i0 = KAPPA >= 2 ? row_s[ui] : row_s[ui] + [&] {
-                        int off = 0, z = qq;
-                        for (int a = 1; a < f.nd; ++a) {
-                            off += (z % kp) * f.stride[a];
-                            z /= kp;
-                        }
-                        return off;
-                    }();
-                    double mv[KV], av[KV], an[KV];
-                    fp_load<KAPPA>(mub + i0, mv, kp);
-                    if (it >= 1) fp_load<KAPPA>(a_cur + i0, av, kp);
+                    double mv[KV];
+                    fp_load<KAPPA>(mub + row_index(ui, qq), mv, kp);
 #pragma unroll
                     for (int x = 0; x < KV; ++x) {
                         if (x >= kp) break;
                         const double mi = mv[x];
-                        if (it >= 1 && mi > 0.0) q.gap += fabs(__dsub_rn(__dmul_rn(av[x], kb), mi));
-                        const double v = (mi > 0.0 && kb > 0.0) ? div_shared(mi, kb, rcp) : 0.0;
-                        an[x] = v;
-                        sa += v;
+                        if (it >= 1 && mi > 0.0) {
+                            const double ao = fp_scale(mi, kbo, rcpo);
+                            q.gap += fabs(__dsub_rn(__dmul_rn(ao, kb), mi));
+                        }
+                        sa += fp_scale(mi, kb, rcp);
                     }
-                    fp_store<KAPPA>(a_nxt + i0, an, kp);
                 }
             }
             sa = group_sum(sa, G);
             if (act && r == 0) {
-                S[k] = sa;
-                kbv[k] = kb;
+                ownS[k - k_lo] = sa;
+                kb_s[k - k_lo] = kb;
             }
         }
-        FastPart *slot_ac = pp + (1 + (int)((it + 1) & 1)) * FCS_MAX;
-        fp_publish(q, slot_ac, rank, sh);
+        fp_publish(q, &slot[1], sh);
         cluster_sync_all();
-        const FastPart ac = fp_combine(slot_ac, cs, sh);
+        const FastPart ac = fp_combine(&slot[1], cs, sh);
         if (it >= 1) {  // end of sweep `it`: range checks, then the gap
             if (fp_bad(ra.lo, ra.hi) || fp_bad(rb.lo, rb.hi) || ((ra.flags | rb.flags) & 2)) {
                 st = GDT_PAIR_OVERFLOW;
@@ -975,64 +990,84 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
             break;
         }
         ++it;
-        double *tmp = a_cur;
-        a_cur = a_nxt;
-        a_nxt = tmp;
         ra = ac;
-        // kta = K^T a (coarse), then the column pass: zero-column check, b,
-        // |nu - b kta|, range(b), block sums of b
+        // the kb that defines a of sweep `it` (kept for the recompute)
+        for (int i = threadIdx.x; i < nblk; i += FT) blk_s[5 * i + 4] = kb_s[i];
+        // kta = K^T a (coarse); column pass: zero-column check, b, |nu - b kta|,
+        // range(b), block sums of b (b is not stored either)
         FastPart qb = fp_init();
-        const double *ssrc = gather(S);
+        gather(ownS);
+        products(cc_s, ci_s, c_n);
         for (int t = 0; t < trips; ++t) {
             const int ui = t * FT + (int)threadIdx.x, u = u_lo + ui;
             const bool act = u < units && ui < upc;
             const int l = act ? u / G : k_lo, r = act ? u - l * G : 0;
-            const double kt = coarse(l, r, act, cp_s, cc_s, ci_s, crow, cmass, ssrc);
-            const double rcp = kt > 0.0 ? __drcp_rn(kt) : 0.0;
+            const double kt = coarse(l, r, act, cp_s, c_lo, crow, cmass);
+            const double rcp = fp_rcp(kt);
             double sb = 0.0;
             if (act) {
                 if (r == 0) {
-                    const double *stl = st_s + 4 * (l - k_lo);
-                    fp_block_range(stl[2], stl[3], kt, rcp, qb);
+                    const double *bl = blk_s + 5 * (l - k_lo);
+                    fp_block_range(bl[2], bl[3], kt, rcp, qb);
                 }
                 for (int qq = 0; qq < rows_per_unit; ++qq) {
-                    const int j0 = KAPPA >= 2 ? row_s[ui] : row_s[ui] + [&] {
-                        int off = 0, z = qq;
-                        for (int a = 1; a < f.nd; ++a) {
-                            off += (z % kp) * f.stride[a];
-                            z /= kp;
-                        }
-                        return off;
-                    }();
-                    double nv[KV], bb[KV];
-                    fp_load<KAPPA>(nub + j0, nv, kp);
+                    double nv[KV];
+                    fp_load<KAPPA>(nub + row_index(ui, qq), nv, kp);
 #pragma unroll
                     for (int x = 0; x < KV; ++x) {
                         if (x >= kp) break;
                         const double nj = nv[x];
-                        const double v = (nj > 0.0 && kt > 0.0) ? div_shared(nj, kt, rcp) : 0.0;
+                        const double v = fp_scale(nj, kt, rcp);
                         if (nj > 0.0) qb.gap += fabs(__dsub_rn(nj, __dmul_rn(v, kt)));
-                        bb[x] = v;
                         sb += v;
                     }
-                    fp_store<KAPPA>(bv + j0, bb, kp);
                 }
             }
             sb = group_sum(sb, G);
             if (act && r == 0) {
-                Bs[l] = sb;
-                ktv[l] = kt;
+                ownB[l - k_lo] = sb;
+                kt_s[l - k_lo] = kt;
             }
         }
-        FastPart *slot_b = pp + (3 + (int)(it & 1)) * FCS_MAX;
-        fp_publish(qb, slot_b, rank, sh);
+        fp_publish(qb, &slot[2], sh);
         cluster_sync_all();
-        rb = fp_combine(slot_b, cs, sh);
+        rb = fp_combine(&slot[2], cs, sh);
         if (rb.flags & 1) {
             st = GDT_PAIR_ZERO_DENOM_COL;
             break;
         }
     }
+    // closing pass: the final a (from its kb, blk[4]) and b (from kta of the
+    // same sweep) for pricing and TV, with kb = K b and kta = K^T a
+    if (st == GDT_PAIR_OK && it >= 1) {
+        __syncthreads();
+        for (int t = 0; t < trips; ++t) {
+            const int ui = t * FT + (int)threadIdx.x, u = u_lo + ui;
+            if (u >= units || ui >= upc) continue;
+            const int k = u / G, r = u - k * G;
+            const double kbo = blk_s[5 * (k - k_lo) + 4], rcpo = fp_rcp(kbo);
+            const double kt = kt_s[k - k_lo], rcpt = fp_rcp(kt);
+            for (int qq = 0; qq < rows_per_unit; ++qq) {
+                const int i0 = row_index(ui, qq);
+                double mv[KV], nv[KV];
+                fp_load<KAPPA>(mub + i0, mv, kp);
+                fp_load<KAPPA>(nub + i0, nv, kp);
+#pragma unroll
+                for (int x = 0; x < KV; ++x) {
+                    if (x >= kp) break;
+                    mv[x] = fp_scale(mv[x], kbo, rcpo);
+                    nv[x] = fp_scale(nv[x], kt, rcpt);
+                }
+                fp_store<KAPPA>(aA + i0, mv, kp);
+                fp_store<KAPPA>(bv + i0, nv, kp);
+            }
+            if (r == 0) {
+                kbv[k] = kb_s[k - k_lo];
+                ktv[k] = kt;
+            }
+        }
+    }
+    cluster_sync_all();  // no CTA leaves while its shared memory may be read
     if (rank == 0 && threadIdx.x == 0) {
         status[b] = st;
         double *o = out + b * 8;
@@ -1043,7 +1078,7 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
         o[4] = (double)it;
         o[5] = converged ? 1.0 : 0.0;
         o[6] = cnt;
-        o[7] = a_cur == aA ? 0.0 : 1.0;
+        o[7] = 0.0;  // final a in the first buffer
     }
 }
 
@@ -1469,10 +1504,11 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         const int64_t units = c.cells * (tmpl ? rows : 1);
         const unsigned csz = (unsigned)std::min<int64_t>(FCS_MAX, (units + FT - 1) / FT);
         const int64_t upc = ((units + csz - 1) / csz + 31) / 32 * 32;
-        const int64_t nblk = upc / (tmpl ? rows : 1);
-        // arcs of one CTA's blocks in shared memory up to arc_cap per side
-        const int arc_cap = (int)std::min<int64_t>(2 * c.cells, 2048);
-        FpSmem plan = fp_smem_plan((int)c.cells, (int)nblk, (int)upc, arc_cap, arc_cap);
+        const int64_t bpc = upc / (tmpl ? rows : 1);
+        // arcs of one CTA's blocks in shared memory up to `cap` per side
+        const int cap = (int)std::min<int64_t>(2 * c.cells, 1024);
+        const FpSmem plan = fp_smem_plan((int)c.cells, (int)bpc, (int)upc, cap);
+        GDT_CHECK_ARG(plan.total <= 200 * 1024, "gdt_primal_upscale: coarse grid too large for the fast IPF");
         const size_t fsmem = (size_t)plan.total;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(batch * csz));
@@ -1486,14 +1522,13 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        FastPart *fparts = reinterpret_cast<FastPart *>(ws + L.fp_off);
         auto go = [&](auto kern) {
             if (fsmem > 48 * 1024)
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
             return cudaLaunchKernelEx(&cfg, kern, mu, nu, arc_off, row_ptr, row_arc_col,
                                       row_arc_mass, col_ptr, col_arc_row, col_arc_mass, kernel_w,
                                       xi, max_iter, f32, c32, kappa, out, status, ws,
-                                      L.stride_pair, fparts, arc_cap);
+                                      L.stride_pair, cap);
         };
         cudaError_t e;
         if (!tmpl) e = go(ipf_fast_kernel<0>);
@@ -1580,3 +1615,4 @@ extern "C" int gdt_price_coo(const int64_t *row, const int64_t *col, const doubl
     cudaFreeAsync(part, st);
     return cuda_status("gdt_price_coo");
 }
+
