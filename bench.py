@@ -450,7 +450,7 @@ def main():
     ap.add_argument("--pairs", type=int, default=0, help="pairs per GPU (default: the config's)")
     ap.add_argument("--config", type=int, default=3, choices=(1, 2, 3, 4, 5),
                     help="BASELINE.json config (3 = the headline 128x128 workload)")
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

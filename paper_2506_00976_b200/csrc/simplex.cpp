@@ -145,6 +145,24 @@ double run_min_scalar(const double *cs, const double *vs, int64_t len, double ui
     return mm;
 }
 
+// Vector accumulator form (no horizontal reduction per run): acc = min(acc,
+// (C - u) - v) lane-wise, the run tail through a lane mask.
+__attribute__((target("avx512f"))) inline __m512d run_acc_avx512(__m512d acc, const double *cs,
+                                                                const double *vs, int64_t len,
+                                                                __m512d uu) {
+    int64_t t = 0;
+    for (; t + 8 <= len; t += 8)
+        acc = _mm512_min_pd(acc, _mm512_sub_pd(_mm512_sub_pd(_mm512_loadu_pd(cs + t), uu),
+                                               _mm512_loadu_pd(vs + t)));
+    if (t < len) {
+        const __mmask8 m = (__mmask8)((1u << (len - t)) - 1u);
+        const __m512d r = _mm512_sub_pd(_mm512_sub_pd(_mm512_maskz_loadu_pd(m, cs + t), uu),
+                                        _mm512_maskz_loadu_pd(m, vs + t));
+        acc = _mm512_mask_min_pd(acc, m, acc, r);
+    }
+    return acc;
+}
+
 // ---- first index attaining a known block minimum --------------------------
 // The reference's strict-< scan over a block ends on the FIRST arc whose
 // reduced cost equals the block minimum; given that minimum (computed with the
@@ -199,6 +217,10 @@ struct Solver {
     std::vector<Node> nd;
     std::vector<double> pot;  // u[0, ns) then v[0, nt)
     std::vector<int32_t> stk, pa_s, pb_s;
+    // preorder of the spanning tree as an array: the subtree of w is
+    // pre[pos[w] .. pos[w] + sz[w]); maintained across pivots so the subtree
+    // relabel is a branch-free sweep over a contiguous range
+    std::vector<int32_t> pre, pos, sz, tmp, stem, stem_slot, stem_sz, stem_pos;
     std::vector<int8_t> sa_s, sb_s;
     int simd;  // 2 = avx512, 1 = avx2, 0 = scalar
 
@@ -226,14 +248,12 @@ struct Solver {
     // u[s] = C - v[t] and v[t] = C - u[s] along tree edges (_simplex.py:105-144,
     // 284-330): every potential is recomputed from its parent.
     void label(int32_t root, bool subtree) {
-        // breadth-first: the next node's record was written long before it is
-        // processed, so consecutive nodes' loads overlap (a LIFO stack would
-        // serialise on the record just written)
-        int64_t qh = 0, sp = 0;
+        int64_t sp = 0, np = 0;
         stk[sp++] = root;
         double *P = pot.data();
-        while (qh < sp) {
-            const int32_t node = stk[qh++];
+        while (sp > 0) {
+            const int32_t node = stk[--sp];
+            pre[np++] = node;  // depth-first pop order = a preorder
             const Node me = nd[node];
             const double pn = P[node];
             if (node < ns) {
@@ -274,7 +294,25 @@ struct Solver {
     }
 
     // exact min of (C - u) - v over arcs [a, hi)
+    __attribute__((target("avx512f"))) double block_min_avx512(int64_t a, int64_t hi) const {
+        __m512d acc = _mm512_set1_pd(INFINITY);
+        const double *v_ = pot.data() + ns;
+        int64_t i = a / nt, j = a - i * nt;
+        while (a < hi) {
+            const int64_t j1 = std::min<int64_t>(nt, j + (hi - a));
+            const __m512d uu = _mm512_set1_pd(pot[i]);
+            cost.runs(i, j, j1, [&](const double *cs, int64_t js, int64_t len) {
+                acc = run_acc_avx512(acc, cs, v_ + js, len, uu);
+            });
+            a += j1 - j;
+            j = 0;
+            ++i;
+        }
+        return _mm512_reduce_min_pd(acc);
+    }
+
     double block_min(int64_t a, int64_t hi) const {
+        if (simd == 2) return block_min_avx512(a, hi);
         double m = INFINITY;
         int64_t i = a / nt, j = a - i * nt;
         while (a < hi) {
@@ -331,6 +369,71 @@ struct Solver {
         return -1;
     }
 
+    // Re-root T = subtree(u_out) at q_root (the stem q_root .. u_out reverses),
+    // hang it under p_root through slot `in_slot`, keep the preorder array and
+    // subtree sizes consistent, then relabel T: every potential recomputed
+    // from its (new) parent along its tree arc, parents before children
+    // (_simplex.py:284-330; the values do not depend on the visiting order).
+    void rehang(int32_t q_root, int32_t p_root, int32_t u_out, int32_t in_slot, int32_t join) {
+        // stem s_0 = q_root, ..., s_k = u_out with their old links / sizes / positions
+        int k = 0;
+        for (int32_t w = q_root;; w = nd[w].par) {
+            stem[k] = w;
+            stem_slot[k] = nd[w].pslot;
+            stem_sz[k] = sz[w];
+            stem_pos[k] = pos[w];
+            ++k;
+            if (w == u_out) break;
+        }
+        const int32_t S = sz[u_out], a = pos[u_out];
+        // sizes between the two cycle sides and the join
+        for (int32_t w = nd[u_out].par; w != join; w = nd[w].par) sz[w] -= S;
+        for (int32_t w = p_root; w != join; w = nd[w].par) sz[w] += S;
+        // T's new preorder: subtree(s_0), then for each s_i its old subtree
+        // minus subtree(s_{i-1}) (s_i first), which is two contiguous pieces
+        int32_t *t = tmp.data();
+        int32_t m = 0;
+        for (int32_t i = stem_pos[0]; i < stem_pos[0] + stem_sz[0]; ++i) t[m++] = pre[i];
+        for (int i = 1; i < k; ++i) {
+            for (int32_t x = stem_pos[i]; x < stem_pos[i - 1]; ++x) t[m++] = pre[x];
+            for (int32_t x = stem_pos[i - 1] + stem_sz[i - 1]; x < stem_pos[i] + stem_sz[i]; ++x)
+                t[m++] = pre[x];
+        }
+        // move T right after p_root in the array (p_root is outside T)
+        const int32_t pv = pos[p_root];
+        int32_t start, lo, hi;
+        if (pv < a) {
+            std::memmove(&pre[pv + 1 + S], &pre[pv + 1], sizeof(int32_t) * (a - pv - 1));
+            start = pv + 1;
+            lo = pv + 1;
+            hi = a + S;
+        } else {
+            std::memmove(&pre[a], &pre[a + S], sizeof(int32_t) * (pv + 1 - a - S));
+            start = pv + 1 - S;
+            lo = a;
+            hi = pv + 1;
+        }
+        std::memcpy(&pre[start], t, sizeof(int32_t) * S);
+        for (int32_t i = lo; i < hi; ++i) pos[pre[i]] = i;
+        // reverse the stem
+        for (int i = k - 1; i >= 1; --i) {
+            nd[stem[i]].par = stem[i - 1];
+            nd[stem[i]].pslot = stem_slot[i - 1];
+            sz[stem[i]] = S - stem_sz[i - 1];
+        }
+        nd[q_root].par = p_root;
+        nd[q_root].pslot = in_slot;
+        sz[q_root] = S;
+        // relabel T in preorder
+        double *P = pot.data();
+        for (int32_t i = start; i < start + S; ++i) {
+            const int32_t w = pre[i];
+            Node &e = nd[w];
+            P[w] = sl[e.pslot].ck - P[e.par];
+            e.dep = nd[e.par].dep + 1;
+        }
+    }
+
     // warm = true: (bi, bj, bf) already hold a feasible spanning-tree basis
     // for (sup, dem) -- e.g. the optimal basis of another cost matrix on the
     // same marginals -- and replace the northwest-corner start.
@@ -379,9 +482,19 @@ struct Solver {
         nd[0].pslot = -1;
         nd[0].dep = 0;
         pot[0] = 0.0;
+        pre.assign(n_nodes, 0);
+        pos.resize(n_nodes);
+        sz.assign(n_nodes, 1);
+        tmp.resize(n_nodes);
+        stem.resize(n_nodes);
+        stem_slot.resize(n_nodes);
+        stem_sz.resize(n_nodes);
+        stem_pos.resize(n_nodes);
         label(0, false);
         for (int64_t w = 0; w < n_nodes; ++w)
             if (nd[w].par == -2) return GDT_LP_DISCONNECTED;
+        for (int64_t i = 0; i < n_nodes; ++i) pos[pre[i]] = (int32_t)i;
+        for (int64_t i = n_nodes - 1; i > 0; --i) sz[nd[pre[i]].par] += sz[pre[i]];
 
         int64_t next_arc = 0, degen_run = 0, pivots = 0;
         int status = GDT_LP_OPTIMAL;
@@ -465,15 +578,9 @@ struct Solver {
             for (int64_t q = 0; q < ca; ++q) bf[pa_s[q]] += sa_s[q] < 0 ? -theta : theta;
             for (int64_t q = 0; q < cb; ++q) bf[pb_s[q]] += sb_s[q] < 0 ? -theta : theta;
 
-            unlink(leave);
-            sl[leave].i = ei;
-            sl[leave].j = ej;
-            sl[leave].ck = cost.at(ei, ej);
-            bf[leave] = theta;
-            push(leave);
-
-            // the detached subtree hangs off the entering arc at the endpoint
-            // whose old root path crossed the leaving arc
+            // the detached subtree T (below the leaving arc, rooted at u_out)
+            // hangs off the entering arc at the endpoint q_root whose old root
+            // path crossed the leaving arc
             int32_t q_root, p_root;
             if (on_a) {
                 q_root = (int32_t)ns + ej;
@@ -482,11 +589,13 @@ struct Solver {
                 q_root = ei;
                 p_root = (int32_t)ns + ej;
             }
-            nd[q_root].par = p_root;
-            nd[q_root].pslot = leave;
-            nd[q_root].dep = nd[p_root].dep + 1;
-            pot[q_root] = sl[leave].ck - pot[p_root];
-            label(q_root, true);
+            const int32_t lx = sl[leave].i, ly = (int32_t)ns + sl[leave].j;
+            const int32_t u_out = nd[lx].pslot == leave ? lx : ly;
+            sl[leave].i = ei;
+            sl[leave].j = ej;
+            sl[leave].ck = cost.at(ei, ej);
+            bf[leave] = theta;
+            rehang(q_root, p_root, u_out, leave, pa);
         }
         for (int64_t k = 0; k < nb; ++k) {
             bi[k] = sl[k].i;

@@ -61,6 +61,10 @@ class CoarsePlans:
     cbar_value: list = field(default_factory=list)    # float or exception
     cmin_value: list = field(default_factory=list)    # float or exception
     lp_seconds: float = 0.0
+    cbar_seconds: float = 0.0    # C-bar kernel + D2H
+    table_seconds: float = 0.0   # offset tables
+    build_seconds: float = 0.0   # problem construction
+    solve_seconds: float = 0.0   # the native LP batch
 
 
 class _Batch:
@@ -120,6 +124,7 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
     need_cbar = "weighted_cost" in methods
     need_cmin = "min_cost" in methods
     cbar_host = None
+    tc = time.perf_counter()
     if need_cbar:
         vals, _ = _cbar(bt)
         cbar_host = to_host_pinned(vals, "cbar")
@@ -127,11 +132,13 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
     nu_c = to_host(bt.nu_c)
     plans = CoarsePlans(n=bt.n)
     t0 = time.perf_counter()
+    plans.cbar_seconds = t0 - tc
     problems, slots, warm = [], [], []
     # C-tilde and C-min are translation-invariant: the host LP reads offset
     # tables instead of n x n matrices (dense copies only for partial supports)
     cmin = min_cost_table(bt.pdims, bt.kappa, bt.p) if need_cmin else None
     ctil = centre_cost_table(bt.pdims, bt.kappa, bt.p) if need_ctil else None
+    plans.table_seconds = time.perf_counter() - t0
     for b in range(bt.B):
         prev = -1
         for kind, cost in (("ctil", ctil),
@@ -150,7 +157,10 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
                 prev = len(problems) - 1
             except GridotError as exc:
                 slots.append((b, kind, exc))
+    t_lp = time.perf_counter()
+    plans.build_seconds = t_lp - t0 - plans.table_seconds
     solved = solve_transport_many(problems, threads=lp_threads, warm_from=warm, slack=False)
+    plans.solve_seconds = time.perf_counter() - t_lp
     res = {}
     it = iter(zip(problems, solved))
     for s in slots:
@@ -395,6 +405,8 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
     t1 = time.perf_counter()
     if timings is not None:
         timings["lp"] = plans.lp_seconds
+        for key in ("cbar", "table", "build", "solve"):
+            timings["lp_" + key] = getattr(plans, key + "_seconds", 0.0)
     dp = DevicePlans(bt, plans, paired, xi)
     t_dp = time.perf_counter()
     res = gpu_stages(bt, dp, methods, max_iter, dual_method)
