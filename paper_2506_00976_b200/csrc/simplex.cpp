@@ -84,17 +84,18 @@ struct GridCost {
         int64_t xi[GDT_MAX_DIM], xj[GDT_MAX_DIM];
         coords(i, xi);
         coords(j0, xj);
-        int64_t j = j0;
+        int64_t j = j0, off = 0;
+        for (int a = 0; a < nd; ++a) off += (xj[a] - xi[a] + cd[a] - 1) * tstride[a];
         while (j < j1) {
             const int64_t len = std::min<int64_t>(cd[0] - xj[0], j1 - j);
-            int64_t off = 0;
-            for (int a = 0; a < nd; ++a) off += (xj[a] - xi[a] + cd[a] - 1) * tstride[a];
             fn(T + off, j, len);
             j += len;
-            // advance xj by len along the flat order (axis 0 fastest)
+            // advance xj (and the table offset) by len along the flat order
             xj[0] += len;
+            off += len;
             for (int a = 0; a < nd - 1 && xj[a] >= cd[a]; ++a) {
                 xj[a] -= cd[a];
+                off += tstride[a + 1] - cd[a] * tstride[a];
                 ++xj[a + 1];
             }
         }
