@@ -317,7 +317,7 @@ extern "C" int gdt_weighted_cost(const double *mu, const double *nu, const doubl
     if (mode == GDT_MODE_FAST && p == 2.0) {
         const int W = ndim + 1;
         double *mom = nullptr;
-        if (cudaMallocAsync(&mom, sizeof(double) * 2 * batch * n * W, st) != cudaSuccess)
+        if (malloc_async(reinterpret_cast<void **>(&mom), sizeof(double) * 2 * batch * n * W, st) != cudaSuccess)
             return cuda_status("gdt_weighted_cost: workspace");
         moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(mu, mom, batch, f, c, kappa);
         moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(nu, mom + batch * n * W, batch,

@@ -344,7 +344,7 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
     if (!p1) {
         const bool two_d = f.nd == 2;
         const int64_t cnt = two_d ? f.n[0] * f.n[1] : max_sq + 1;
-        if (cudaMallocAsync(&ftab, sizeof(float) * cnt, st) != cudaSuccess) return GDT_ERR_CUDA;
+        if (malloc_async(reinterpret_cast<void **>(&ftab), sizeof(float) * cnt, st) != cudaSuccess) return GDT_ERR_CUDA;
         if (two_d) dg_table2d_kernel<<<grid_size(cnt, 256), 256, 0, st>>>(table, ftab, f.n[1], f.n[0]);
         else dg_table1d_kernel<<<grid_size(cnt, 256), 256, 0, st>>>(table, ftab, cnt);
         tab_max = (int)max_sq;

@@ -228,7 +228,7 @@ static int launch_kappa(const double *mu, const double *nu, const double *mu_c, 
     const bool two_d = f.nd == 2;
     const int64_t tcount = p1 ? 1 : (two_d ? f.n[0] * f.n[1] : max_sq + 1);
     float *ftab = nullptr;
-    if (cudaMallocAsync(&ftab, sizeof(float) * tcount, st) != cudaSuccess) return GDT_ERR_CUDA;
+    if (malloc_async(reinterpret_cast<void **>(&ftab), sizeof(float) * tcount, st) != cudaSuccess) return GDT_ERR_CUDA;
     if (p1) {
     } else if (two_d)
         ftable2d_kernel<<<grid_size(tcount, 256), 256, 0, st>>>(table, ftab, f.n[1], f.n[0]);

@@ -13,6 +13,7 @@ namespace gdt {
 // Error text of the last failing call on this host thread (gdt_last_error).
 void set_error(const std::string &msg);
 int cuda_status(const char *where);  // GDT_OK or GDT_ERR_CUDA after a launch
+cudaError_t malloc_async(void **p, size_t bytes, cudaStream_t st);  // pooled workspace
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 

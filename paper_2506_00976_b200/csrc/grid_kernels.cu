@@ -14,6 +14,23 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
+// Stream-ordered workspaces come from the device's default memory pool; keep
+// freed blocks cached in the pool (release threshold = max) so repeated calls
+// do not map and unmap device memory at every synchronisation.
+cudaError_t malloc_async(void **p, size_t bytes, cudaStream_t st) {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev != done_dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        done_dev = dev;
+    }
+    return cudaMallocAsync(p, bytes, st);
+}
+
 int cuda_status(const char *where) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

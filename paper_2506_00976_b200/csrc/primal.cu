@@ -653,9 +653,15 @@ __device__ __forceinline__ void fp_block_range(double mlo, double mhi, double de
     if (hi > 0.0) q.hi = fmax(q.hi, hi);
 }
 
-// scaling of one cell: mass / den on the support, 0 elsewhere or when den <= 0
+// scaling of one cell: mass / den on the support, 0 elsewhere or when den <= 0.
+// Markstein quotient without div_shared's range guards: correctly rounded
+// whenever mass, den and the quotient stay inside the normal range, which the
+// scale-range checks (1e-100 .. 1e100, evaluated with the guarded division on
+// the block extremes) require of every accepted sweep anyway.
 __device__ __forceinline__ double fp_scale(double m, double den, double rcp) {
-    return (m > 0.0 && den > 0.0) ? div_shared(m, den, rcp) : 0.0;
+    const double q = __dmul_rn(m, rcp);
+    const double r = __fma_rn(-q, den, m);
+    return (m > 0.0 && den > 0.0) ? __fma_rn(r, rcp, q) : 0.0;
 }
 
 __device__ __forceinline__ double fp_rcp(double den) { return den > 0.0 ? __drcp_rn(den) : 0.0; }
@@ -1608,7 +1614,7 @@ extern "C" int gdt_price_coo(const int64_t *row, const int64_t *col, const doubl
     unsigned g = grid_size(nnz, 256);
     if (g > 1184) g = 1184;
     double *part = nullptr;
-    if (cudaMallocAsync(&part, sizeof(double) * g, st) != cudaSuccess)
+    if (malloc_async(reinterpret_cast<void **>(&part), sizeof(double) * g, st) != cudaSuccess)
         return cuda_status("gdt_price_coo: workspace");
     price_coo_kernel<<<g, 256, 0, st>>>(row, col, mass, nnz, a, b, cost_table, p, f, part);
     sum_parts_kernel<<<1, 32, 0, st>>>(part, (int)g, out);
