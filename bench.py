@@ -301,7 +301,13 @@ def run_b200(args):
     N.check(N.lib().gdt_probe_fp32(blocks, iters, N.ptr(sink), stream()), "probe")
     e1.record(cur)
     torch.cuda.synchronize()
-    fp32_peak = 2.0 * blocks * 256 * 8 * iters / (e0.elapsed_time(e1) / 1000.0) / 1e12
+    fp32_probe = 2.0 * blocks * 256 * 8 * iters / (e0.elapsed_time(e1) / 1000.0) / 1e12
+    # denominator: the nominal FP32 CUDA-core rate at the SM clock sampled under
+    # load (SMs x 128 FMA lanes x 2 FLOP x f); the FFMA probe is reported beside it
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    fp32_peak = sms * 128 * 2.0 * float(clk.get("sm_mhz") or 1965.0) * 1e6 / 1e12
+    peak_src = (f"nominal {sms} SMs x 128 FP32 lanes x 2 at the sampled {clk.get('sm_mhz')} MHz; "
+                f"FFMA probe measured {fp32_probe:.1f} TFLOP/s")
     dom = max(stage_ms.items(), key=lambda kv: kv[1])
     (dk, dpow, dname), dms = dom
     n_c = Nf // dk ** len(dims)
@@ -310,7 +316,7 @@ def run_b200(args):
         rl = {"bound": "fp32", "kernel": f"pruned_ct_kernel (c-transform, kappa={dk}, p={dpow:g})"}
     elif dname == "cbar" and dpow != 2.0:
         flops = 2.0 * Nf * Nf * ppr            # one FMA per (row cell, column cell)
-        rl = {"bound": "fp32", "kernel": f"cbar_toeplitz_kernel (fp32 C-bar, kappa={dk}, p={dpow:g})"}
+        rl = {"bound": "fp32", "kernel": f"cbar_diag_kernel (fp32 FFMA2 C-bar, kappa={dk}, p={dpow:g})"}
     else:
         flops = None
         rl = None
@@ -318,7 +324,7 @@ def run_b200(args):
         achieved = flops / (dms / 1000.0) / 1e12
         rl.update({"achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                    "frac": achieved / fp32_peak, "traffic": None,
-                   "peak_source": "measured live: FFMA issue-rate probe (gdt_probe_fp32)",
+                   "peak_source": peak_src,
                    "work": "2 FP32 ops x N^4 candidates per pair (N=128)"})
     # IPF/TV kernel against HBM (north-star secondary roofline)
     peaks = {}
@@ -355,6 +361,7 @@ def run_b200(args):
         ct_roof = {"bound": "fp32", "kernel": "pruned_ct_kernel (fp32, p != 2)",
                    "achieved": best, "peak": fp32_peak, "unit": "TFLOP/s",
                    "frac": best / fp32_peak, "traffic": None, "per_launch": ct_roofs,
+                   "peak_source": peak_src,
                    "work": "brute-force count 2*N^4 per transform per pair (the reference's "
                            "algorithm); tile pruning evaluates a subset exactly, so this is an "
                            "effective rate"}
