@@ -396,12 +396,14 @@ def run_b200(args):
 
     # ---- e2e through the public API with host buffers --------------------
     if not args.no_e2e:
+        # each rank gets its own slice of the host cores for its LPs
+        lp_threads = max(1, (os.cpu_count() or 1) // world)
         pin_mu = torch.from_numpy(mus_h).pin_memory()
         pin_nu = torch.from_numpy(nus_h).pin_memory()
         h2d = d2h = 0
         for k, p in combos:  # untimed warm-up pass through the public API
             G.quantized_bounds(pin_mu, pin_nu, dims, k, p, precision=wl.precision, xi=wl.xi,
-                               max_iter=wl.max_iter)
+                               max_iter=wl.max_iter, lp_threads=lp_threads)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -411,7 +413,8 @@ def run_b200(args):
             for k, p in combos:
                 tm = {}
                 reps = G.quantized_bounds(pin_mu, pin_nu, dims, k, p, precision=wl.precision,
-                                          xi=wl.xi, max_iter=wl.max_iter, timings=tm)
+                                          xi=wl.xi, max_iter=wl.max_iter, timings=tm,
+                                          lp_threads=lp_threads)
                 for key, val in tm.items():
                     parts[f"k{k}_p{p:g}_{key}"] = parts.get(f"k{k}_p{p:g}_{key}", 0.0) + val
                 h2d += 2 * ppr * Nf * 8
@@ -428,6 +431,7 @@ def run_b200(args):
                        "h2d_bytes_per_step": h2d // args.e2e_steps,
                        "d2h_bytes_per_step": d2h // args.e2e_steps,
                        "s_per_step": e2e_s, "host_cores": os.cpu_count(),
+                       "lp_threads_per_rank": lp_threads,
                        "breakdown_s": {k: round(v / args.e2e_steps, 4) for k, v in parts.items()},
                        "note": "public API quantized_bounds from pinned host memory; "
                                "includes 3 host LPs per pair per combo on all host cores"}

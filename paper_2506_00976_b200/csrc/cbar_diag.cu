@@ -72,7 +72,7 @@ __device__ __forceinline__ void dg_load(float *v, const float *src) {
 }
 
 template <int KAPPA, int KR, int ND, bool P1>
-__global__ void __launch_bounds__(DG_MAX_THREADS, 2) cbar_diag_kernel(
+__global__ void __launch_bounds__(DG_MAX_THREADS, 3) cbar_diag_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ mu_c,
     const double *__restrict__ nu_c, const double *__restrict__ Ccentre,
     const float *__restrict__ tab, int tab_max, double *__restrict__ out,
@@ -336,7 +336,7 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
                          sizeof(float) * ((KR * n + 3) & ~3);
     const size_t row_bytes = sizeof(float) * dg_row_len((int)f.n[0], OFF);
     const int64_t n_hi = n / c.n[0];
-    const int stage_all = fixed + row_bytes * Gr * n_hi <= 100 * 1024;
+    const int stage_all = fixed + row_bytes * Gr * n_hi <= 72 * 1024;  // 3 CTAs per SM
     const size_t bytes = fixed + row_bytes * Gr * (stage_all ? n_hi : nb);
     if (bytes > 100 * 1024) return GDT_ERR_UNSUPPORTED;
     float *ftab = nullptr;

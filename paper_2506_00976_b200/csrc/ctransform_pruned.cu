@@ -254,6 +254,164 @@ __global__ void __launch_bounds__(64) pruned_ct_kernel(const T *__restrict__ v,
     }
 }
 
+// ---- fp32, p = 1, 2-D grids up to 128 x 128: shared-memory cost table -----
+//
+// Same regions, tiles, ring order and pruning rule as pruned_ct_kernel, but the
+// 15 Toeplitz costs of a (lane, source row) pair come from a per-CTA table of
+// correctly rounded sqrt(dx^2 + dy^2) instead of 15 MUFU sqrt.approx (the MUFU
+// pipe bounded the kernel).  Row |dy| of the table holds T[i] = cost(|i - 7|, dy)
+// for i in [0, 135]: for a lane whose 8 outputs start at xj0 and a tile row
+// starting at sx0, off = sx0 - xj0 is a multiple of 8 and the lane's costs are
+// T[off + q] (off >= 0) or T[-off + 14 - q] (off < 0), q = 0..14 -- 16 aligned
+// floats, four LDS.128.  Row stride 140 floats (12 mod 32 banks) makes the
+// 16-byte reads of 8 lanes on 8 different rows conflict-free.  Eight regions
+// (16 warps) per CTA amortise the table; the pruning bound of a tile uses the
+// same table values, so no lowering is needed.
+constexpr int CT_TAB_W = 140;      // row stride (floats)
+constexpr int CT_TAB_ROWS = 128;   // |dy| <= 127
+constexpr int CT_TAB_REG = 8;      // regions per CTA (2 warps each)
+
+__device__ __forceinline__ void pair_sync(int id) {
+    asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+
+__global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
+    const float *__restrict__ v, const float *__restrict__ tmax, float *__restrict__ out,
+    int64_t batch, Grid g, unsigned long long *__restrict__ counter) {
+    extern __shared__ __align__(16) float ct_tab[];  // [CT_TAB_ROWS][CT_TAB_W]
+    __shared__ float other[CT_TAB_REG][32][8];
+    __shared__ long long next_region[CT_TAB_REG];
+    const int lane = threadIdx.x & 31;
+    const int warp_in_cta = threadIdx.x >> 5;
+    const int half = warp_in_cta & 1;
+    const int slot = warp_in_cta >> 1;
+    const int bar_id = 1 + slot;  // named barrier of this warp pair
+    const int N0 = (int)g.n[0], N1 = (int)g.n[1];
+    // table: row dy, column i -> sqrt((i - 7)^2 + dy^2), correctly rounded
+    for (int e = threadIdx.x; e < CT_TAB_ROWS * CT_TAB_W; e += blockDim.x) {
+        const int dy = e / CT_TAB_W, i = e - dy * CT_TAB_W;
+        const int dx = i - 7;
+        ct_tab[e] = sqrtf((float)(dx * dx + dy * dy));
+    }
+    __syncthreads();
+
+    const int nr0 = N0 / 16, nr1 = N1 / 16;
+    const int64_t regions = (int64_t)nr0 * nr1;
+    const int64_t total = batch * regions;
+    const int nt0 = N0 / 8, nt1 = N1 / 8;
+    // persistent warp pairs: each pair takes the next region from a global
+    // counter (pruned work per region is uneven)
+    for (;;) {
+        if (half == 0 && lane == 0)
+            next_region[slot] = (long long)atomicAdd(counter, 1ull);
+        pair_sync(bar_id);
+        const int64_t region = next_region[slot];
+        if (region >= total) break;
+        float best[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) best[r] = INFINITY;
+        const int64_t b = region / regions;
+        const int rr = (int)(region - b * regions);
+        const int rx = rr % nr0, ry = rr / nr0;
+        const int X0 = rx * 16, Y0 = ry * 16;
+        const int xj0 = X0 + 8 * (lane & 1);
+        const int yj = Y0 + (lane >> 1);
+        const float *vb = v + b * g.cells;
+        const float *tm = tmax + b * (int64_t)nt0 * nt1;
+        float vall = -INFINITY;
+        for (int i = lane; i < nt0 * nt1; i += 32) vall = fmaxf(vall, tm[i]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) vall = fmaxf(vall, __shfl_xor_sync(0xffffffffu, vall, o));
+        float ub = INFINITY;
+        const int h0lo = X0 / 8, h0hi = h0lo + 1, h1lo = Y0 / 8, h1hi = h1lo + 1;
+        const int rmax = max(nt0, nt1);
+        int parity = 0;
+        for (int r = 0; r <= rmax; ++r) {
+            if (r >= 1) {  // smallest cost any tile of ring r can reach
+                const int gap = (r - 1) * 8 + 1;
+                const float cmin = gap + 7 < CT_TAB_W ? ct_tab[gap + 7] : sqrtf((float)gap * gap);
+                if (cmin - vall >= ub) break;
+            }
+            const int a0 = max(h0lo - r, 0), b0 = min(h0hi + r, nt0 - 1);
+            const int a1 = max(h1lo - r, 0), b1 = min(h1hi + r, nt1 - 1);
+            for (int t1 = a1; t1 <= b1; ++t1) {
+                const int d1 = t1 < h1lo ? h1lo - t1 : (t1 > h1hi ? t1 - h1hi : 0);
+                const bool face = d1 == r;
+                const int step = face ? 1 : (h0hi + r) - (h0lo - r);
+                for (int t0 = face ? a0 : h0lo - r; t0 <= b0; t0 += step > 0 ? step : 1) {
+                    if (t0 < a0) continue;
+                    const int d0 = t0 < h0lo ? h0lo - t0 : (t0 > h0hi ? t0 - h0hi : 0);
+                    if (max(d0, d1) != r) continue;
+                    if (((parity++) & 1) != half) continue;
+                    const int g0 = max(0, max(t0 * 8 - (X0 + 15), X0 - (t0 * 8 + 7)));
+                    const int g1 = max(0, max(t1 * 8 - (Y0 + 15), Y0 - (t1 * 8 + 7)));
+                    const float lb = ct_tab[g1 * CT_TAB_W + g0 + 7] - tm[t1 * nt0 + t0];
+                    if (lb >= ub) continue;
+                    const int sx0 = t0 * 8, off = sx0 - xj0;
+                    const int base = off >= 0 ? off : -off;
+                    for (int y = 0; y < 8; ++y) {
+                        const int ys = t1 * 8 + y;
+                        const int dy = ys > yj ? ys - yj : yj - ys;
+                        const float4 *trow = reinterpret_cast<const float4 *>(
+                            ct_tab + dy * CT_TAB_W + base);
+                        float L[16];
+#pragma unroll
+                        for (int c4 = 0; c4 < 4; ++c4) {
+                            const float4 t = trow[c4];
+                            L[4 * c4] = t.x;
+                            L[4 * c4 + 1] = t.y;
+                            L[4 * c4 + 2] = t.z;
+                            L[4 * c4 + 3] = t.w;
+                        }
+                        float cst[15];
+                        if (off >= 0) {
+#pragma unroll
+                            for (int q = 0; q < 15; ++q) cst[q] = L[q];
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 15; ++q) cst[q] = L[14 - q];
+                        }
+                        const float *row = vb + (int64_t)ys * N0 + sx0;
+                        const float4 v0 = __ldg(reinterpret_cast<const float4 *>(row));
+                        const float4 v1 = __ldg(reinterpret_cast<const float4 *>(row) + 1);
+                        const float vs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                        for (int r8 = 0; r8 < 8; ++r8) {
+#pragma unroll
+                            for (int s2 = 0; s2 < 8; s2 += 2) {
+                                float c0, c1;
+                                sub_f32x2(cst[s2 - r8 + 7], cst[s2 + 1 - r8 + 7], vs[s2],
+                                          vs[s2 + 1], c0, c1);
+                                best[r8] = fmin3(best[r8], c0, c1);
+                            }
+                        }
+                    }
+                    float m = best[0];
+#pragma unroll
+                    for (int r8 = 1; r8 < 8; ++r8) m = fmaxf(m, best[r8]);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                    ub = m;
+                }
+            }
+        }
+        // merge the two warps' minima
+        if (half == 1) {
+#pragma unroll
+            for (int r8 = 0; r8 < 8; ++r8) other[slot][lane][r8] = best[r8];
+        }
+        pair_sync(bar_id);
+        if (half == 0) {
+            float *ob = out + b * g.cells + (int64_t)yj * N0 + xj0;
+#pragma unroll
+            for (int r8 = 0; r8 < 8; ++r8) {
+                const float o = other[slot][lane][r8];
+                ob[r8] = o < best[r8] ? o : best[r8];
+            }
+        }
+    }
+}
+
 // Returns GDT_ERR_UNSUPPORTED outside the tiled envelope (caller falls back).
 // v: device input of type T (fp32 path expects an fp32 copy); tab: T cost table
 // by squared distance (unused for fp32 p == 1); tmax: scratch [batch * tiles].
@@ -286,6 +444,22 @@ static int run_pruned(const T *v, T *out, T *tmax, int64_t batch, const Grid &g,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     (void)sms;
     const unsigned ctas = (unsigned)warps;  // one region per 2-warp CTA
+    if constexpr (sizeof(T) == 4) {
+        if (g.nd == 2 && p1 && g.n[0] <= CT_TAB_ROWS && g.n[1] <= CT_TAB_ROWS) {
+            const size_t tb = sizeof(float) * CT_TAB_ROWS * CT_TAB_W;
+            cudaFuncSetAttribute(pruned_ct_tab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tb);
+            int dev2 = 0, nsm = 148;
+            cudaGetDevice(&dev2);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev2);
+            const int64_t need = (warps + CT_TAB_REG - 1) / CT_TAB_REG;
+            const unsigned tctas = (unsigned)std::min<int64_t>(need, 2 * nsm);  // persistent
+            pruned_ct_tab_kernel<<<tctas, 64 * CT_TAB_REG, tb, st>>>(
+                reinterpret_cast<const float *>(v), reinterpret_cast<const float *>(tmax),
+                reinterpret_cast<float *>(out), batch, g, counter);
+            return GDT_OK;
+        }
+    }
     if (g.nd == 2) {
         if (p1 && sizeof(T) == 4) pruned_ct_kernel<T, 2, true><<<ctas, 64, 0, st>>>(v, tmax, out, batch, g, tab, counter);
         else pruned_ct_kernel<T, 2, false><<<ctas, 64, 0, st>>>(v, tmax, out, batch, g, tab, counter);

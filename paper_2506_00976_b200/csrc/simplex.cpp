@@ -151,6 +151,15 @@ double run_min_scalar(const double *cs, const double *vs, int64_t len, double ui
 __attribute__((target("avx512f"))) inline __m512d run_acc_avx512(__m512d acc, const double *cs,
                                                                 const double *vs, int64_t len,
                                                                 __m512d uu) {
+    if (len == 32) {  // the common coarse-grid row (32 cells): fully unrolled, two chains
+        __m512d a1 = _mm512_sub_pd(_mm512_sub_pd(_mm512_loadu_pd(cs + 8), uu), _mm512_loadu_pd(vs + 8));
+        acc = _mm512_min_pd(acc, _mm512_sub_pd(_mm512_sub_pd(_mm512_loadu_pd(cs), uu), _mm512_loadu_pd(vs)));
+        a1 = _mm512_min_pd(a1, _mm512_sub_pd(_mm512_sub_pd(_mm512_loadu_pd(cs + 24), uu),
+                                             _mm512_loadu_pd(vs + 24)));
+        acc = _mm512_min_pd(acc, _mm512_sub_pd(_mm512_sub_pd(_mm512_loadu_pd(cs + 16), uu),
+                                               _mm512_loadu_pd(vs + 16)));
+        return _mm512_min_pd(acc, a1);
+    }
     int64_t t = 0;
     for (; t + 8 <= len; t += 8)
         acc = _mm512_min_pd(acc, _mm512_sub_pd(_mm512_sub_pd(_mm512_loadu_pd(cs + t), uu),
