@@ -72,7 +72,7 @@ __device__ __forceinline__ void dg_load(float *v, const float *src) {
 }
 
 template <int KAPPA, int KR, int ND, bool P1>
-__global__ void __launch_bounds__(DG_MAX_THREADS, 3) cbar_diag_kernel(
+__global__ void __launch_bounds__(DG_MAX_THREADS, 4) cbar_diag_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ mu_c,
     const double *__restrict__ nu_c, const double *__restrict__ Ccentre,
     const float *__restrict__ tab, int tab_max, double *__restrict__ out,
