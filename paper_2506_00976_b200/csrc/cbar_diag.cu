@@ -56,18 +56,18 @@ __device__ __forceinline__ void dg_load(float *v, const float *src) {
     if constexpr (PER % 4 == 0) {
 #pragma unroll
         for (int q = 0; q < PER / 4; ++q) {
-            const float4 t = reinterpret_cast<const float4 *>(src)[q];
+            const float4 t = __ldg(reinterpret_cast<const float4 *>(src) + q);
             v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
         }
     } else if constexpr (PER % 2 == 0) {
 #pragma unroll
         for (int q = 0; q < PER / 2; ++q) {
-            const float2 t = reinterpret_cast<const float2 *>(src)[q];
+            const float2 t = __ldg(reinterpret_cast<const float2 *>(src) + q);
             v[2 * q] = t.x; v[2 * q + 1] = t.y;
         }
     } else {
 #pragma unroll
-        for (int q = 0; q < PER; ++q) v[q] = src[q];
+        for (int q = 0; q < PER; ++q) v[q] = __ldg(src + q);
     }
 }
 
@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 4) cbar_diag_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ mu_c,
     const double *__restrict__ nu_c, const double *__restrict__ Ccentre,
     const float *__restrict__ tab, int tab_max, double *__restrict__ out,
-    uint8_t *__restrict__ unused, Grid f, Grid c, int nb_per_pass, int stage_all) {
+    uint8_t *__restrict__ unused, Grid f, Grid c, int nb_per_pass,
+    const float *__restrict__ nup, const double *__restrict__ rmu, const double *__restrict__ rnu) {
     static_assert(KR % 2 == 0, "blocks are paired in FFMA2 lanes");
     extern __shared__ unsigned long long mus2[];  // [(th*KP + jp)*KAPPA + tx], then numer
     constexpr int R = DG_R;
@@ -89,9 +90,10 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 4) cbar_diag_kernel(
     const int64_t N = f.cells;
     const int nthreads = blockDim.x;
     float *snum = reinterpret_cast<float *>(mus2 + G * KP * KAPPA);  // [KR][n] block numerators
-    // nu rows of the current pass, fp32, OFF zero cells either side: [nb][G][NL]
+    // nu rows in fp32 with OFF zero cells either side, prepared once per call
+    // by dg_nu_pad_kernel: [B][fine rows][NL]
     const int NL = dg_row_len(N0, OFF);
-    float *nbuf = snum + ((KR * n + 3) & ~3);  // 16-byte aligned
+    const int frows = (int)(N / N0);
 
     const int64_t b = blockIdx.y;
     const int tiles_x = (n0 + KR - 1) / KR;
@@ -155,42 +157,7 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 4) cbar_diag_kernel(
     }
     const int n_hi = n / n0;  // coarse block-rows
 
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = nthreads / 32;
-    // nu rows (fp32, one warp per row, coalesced): all of them once when they
-    // fit (stage_all), else the rows of each pass
-    auto stage_rows = [&](int lb0, int nrows) {
-        for (int row = warp; row < nrows * G; row += nwarps) {
-            const int slot = row / G, rq = row - slot * G, lbq = lb0 + slot;
-            float *dst = nbuf + row * NL;
-            if (lbq >= n_hi) {
-                for (int x = lane; x < NL; x += 32) dst[x] = 0.f;
-                continue;
-            }
-            int64_t rb = 0;
-            int remb = lbq, remr = rq;
-#pragma unroll
-            for (int a = 1; a < ND; ++a) {
-                const int la = remb % (int)c.n[a], ta = remr % KAPPA;
-                remb /= (int)c.n[a];
-                remr /= KAPPA;
-                rb += (int64_t)(la * KAPPA + ta) * f.stride[a];
-            }
-            for (int x = lane; x < NL; x += 32) {
-                const int cx = x - OFF;
-                dst[x] = cx >= 0 && cx < N0 ? (float)nub[rb + cx] : 0.f;
-            }
-        }
-    };
-    if (stage_all) {
-        stage_rows(0, n_hi);
-        __syncthreads();
-    }
     for (int lb0 = 0; lb0 < n_hi; lb0 += nb_per_pass) {
-        if (!stage_all) {
-            __syncthreads();
-            stage_rows(lb0, nb_per_pass);
-            __syncthreads();
-        }
         const int lb = lb0 + gblk;  // coarse block-row (flat over the higher axes)
         const bool active = lb < n_hi && gblk < nb_per_pass;
         int chc[GDT_MAX_DIM] = {0, 0, 0, 0};  // fine higher coordinates of this lane's row
@@ -255,7 +222,10 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 4) cbar_diag_kernel(
         }
         // fold: this lane's row of every (k+j, l) it covers, then the G rows of the
         // block-row in the lane group; the leader writes C-bar
-        const float *nrow = nbuf + ((stage_all ? lb : gblk) * G + rr) * NL + OFF;  // zero outside the grid
+        int rowid = 0;  // fine row (flat over the higher axes) of this lane
+#pragma unroll
+        for (int a = 1; a < ND; ++a) rowid += chc[a] * (int)(f.stride[a] / N0);
+        const float *nrow = nup + ((int64_t)b * frows + (active ? rowid : 0)) * NL + OFF;
 #pragma unroll
         for (int jp = 0; jp < KP; ++jp) {
 #pragma unroll
@@ -298,9 +268,29 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 4) cbar_diag_kernel(
         const double denom = __dmul_rn(mu_c[b * n + k], nu_c[b * n + l]);
         const int64_t oi = ((int64_t)b * n + k) * n + l;
         const bool un = denom == 0.0;
-        out[oi] = un ? Ccentre[(int64_t)k * n + l] : (double)snum[i] / denom;
+        // fp32-mode quotient through precomputed reciprocals (~2 ulp of fp64)
+        out[oi] = un ? Ccentre[(int64_t)k * n + l] : (double)snum[i] * rmu[b * n + k] * rnu[b * n + l];
         unused[oi] = un ? 1 : 0;
     }
+}
+
+// nu as padded fp32 rows [B][rows][NL] (OFF zeros either side) and the
+// reciprocals of the coarse masses (0 where the mass is 0)
+__global__ void dg_nu_pad_kernel(const double *__restrict__ nu, float *__restrict__ nup,
+                                 int64_t batch, int64_t rows, int N0, int NL, int OFF) {
+    const int64_t total = batch * rows * NL;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / NL;
+        const int x = (int)(i - r * NL) - OFF;
+        nup[i] = x >= 0 && x < N0 ? (float)nu[r * N0 + x] : 0.f;
+    }
+}
+
+__global__ void dg_recip_kernel(const double *__restrict__ a, double *__restrict__ r, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        r[i] = a[i] > 0.0 ? 1.0 / a[i] : 0.0;
 }
 
 __global__ void dg_table2d_kernel(const double *__restrict__ g, float *__restrict__ t, int64_t ny,
@@ -332,13 +322,9 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
     const int threads = ((Gr * segs * nb + 31) / 32) * 32;
     if (threads > DG_MAX_THREADS) return GDT_ERR_UNSUPPORTED;
     const int64_t n = c.cells;
-    const size_t fixed = sizeof(unsigned long long) * Gr * (KR / 2) * KAPPA +
+    const size_t bytes = sizeof(unsigned long long) * Gr * (KR / 2) * KAPPA +
                          sizeof(float) * ((KR * n + 3) & ~3);
-    const size_t row_bytes = sizeof(float) * dg_row_len((int)f.n[0], OFF);
-    const int64_t n_hi = n / c.n[0];
-    const int stage_all = fixed + row_bytes * Gr * n_hi <= 72 * 1024;  // 3 CTAs per SM
-    const size_t bytes = fixed + row_bytes * Gr * (stage_all ? n_hi : nb);
-    if (bytes > 100 * 1024) return GDT_ERR_UNSUPPORTED;
+    if (bytes > 56 * 1024) return GDT_ERR_UNSUPPORTED;
     float *ftab = nullptr;
     int tab_max = 0;
     if (!p1) {
@@ -349,13 +335,29 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
         else dg_table1d_kernel<<<grid_size(cnt, 256), 256, 0, st>>>(table, ftab, cnt);
         tab_max = (int)max_sq;
     }
+    const int NL = dg_row_len((int)f.n[0], OFF);
+    const int64_t frows = f.cells / f.n[0];
+    float *nup = nullptr;
+    double *rmu = nullptr, *rnu = nullptr;
+    if (malloc_async(reinterpret_cast<void **>(&nup), sizeof(float) * batch * frows * NL, st) !=
+            cudaSuccess ||
+        malloc_async(reinterpret_cast<void **>(&rmu), sizeof(double) * 2 * batch * n, st) !=
+            cudaSuccess) {
+        if (ftab) cudaFreeAsync(ftab, st);
+        return GDT_ERR_CUDA;
+    }
+    rnu = rmu + batch * n;
+    dg_nu_pad_kernel<<<grid_size(batch * frows * NL, 256), 256, 0, st>>>(nu, nup, batch, frows,
+                                                                         (int)f.n[0], NL, OFF);
+    dg_recip_kernel<<<grid_size(batch * n, 256), 256, 0, st>>>(mu_c, rmu, batch * n);
+    dg_recip_kernel<<<grid_size(batch * n, 256), 256, 0, st>>>(nu_c, rnu, batch * n);
     const int64_t tiles_x = (c.n[0] + KR - 1) / KR;
     dim3 grid((unsigned)(tiles_x * (n / c.n[0])), (unsigned)batch);
     auto run = [&](auto kern) {
         if (bytes > 48 * 1024)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         kern<<<grid, threads, bytes, st>>>(mu, nu, mu_c, nu_c, Ccentre, ftab, tab_max, out, unused,
-                                           f, c, nb, stage_all);
+                                           f, c, nb, nup, rmu, rnu);
     };
     switch (f.nd * 2 + (p1 ? 1 : 0)) {
         case 2: run(cbar_diag_kernel<KAPPA, KR, 1, false>); break;
@@ -367,6 +369,8 @@ static int dg_launch(const double *mu, const double *nu, const double *mu_c, con
         default: break;
     }
     if (ftab) cudaFreeAsync(ftab, st);
+    cudaFreeAsync(nup, st);
+    cudaFreeAsync(rmu, st);
     return GDT_OK;
 }
 
