@@ -71,8 +71,14 @@ __device__ __forceinline__ void dg_load(float *v, const float *src) {
     }
 }
 
+// occupancy target: 4 CTAs/SM for 2 block pairs per thread, 2 for 4 pairs
+template <int KR>
+struct DgMinBlocks {
+    static constexpr int value = KR <= 4 ? 4 : 2;
+};
+
 template <int KAPPA, int KR, int ND, bool P1>
-__global__ void __launch_bounds__(DG_MAX_THREADS, 4) cbar_diag_kernel(
+__global__ void __launch_bounds__(DG_MAX_THREADS, DgMinBlocks<KR>::value) cbar_diag_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ mu_c,
     const double *__restrict__ nu_c, const double *__restrict__ Ccentre,
     const float *__restrict__ tab, int tab_max, double *__restrict__ out,
