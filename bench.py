@@ -238,7 +238,7 @@ def run_b200(args):
             E.launch_primal(bt, dp, wl.max_iter)
             # ipf_fast + TV/moments + pricing + finish (fp32 mode); the exact
             # path adds two arc-coordinate packs and the block map
-            launches += 4 if bt.mode == 1 else 7
+            launches += (4 if bt.mode == 1 else 7) + (0 if bt.p == 2.0 else 1)  # + arc rows
             ev[3].record(cur)
             E.launch_dual_prep(bt, dp)
             launches += 2

@@ -1190,7 +1190,7 @@ __global__ void __launch_bounds__(MT) price_kernel(
     const double *__restrict__ W, const double *__restrict__ out, const int32_t *__restrict__ status,
     const double *__restrict__ scratch, int64_t stride_pair, const double *__restrict__ mom,
     double *__restrict__ part, G32 f, G32 c, int kappa, double p, const double *__restrict__ table,
-    int closed_form, int fast) {
+    int closed_form, int fast, const int32_t *__restrict__ arc_row) {
     __shared__ double sh[32];
     const int64_t b = blockIdx.y;
     const int N = f.cells, n = c.cells;
@@ -1202,14 +1202,20 @@ __global__ void __launch_bounds__(MT) price_kernel(
     const int64_t q = closed_form ? item : item / m;       // arc
     const int t = closed_form ? 0 : (int)(item - q * m);   // row offset (brute force)
     if (status[b] == GDT_PAIR_OK && q < A) {
-        const int32_t *rptr = row_ptr + b * (n + 1);
-        int lo = 0, hi = n;  // row block of arc q
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (rptr[mid] <= q) lo = mid;
-            else hi = mid;
+        int k;  // row block of arc q
+        if (arc_row) {
+            k = arc_row[arc_off[b] + q];
+        } else {
+            const int32_t *rptr = row_ptr + b * (n + 1);
+            int lo = 0, hi = n;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (rptr[mid] <= q) lo = mid;
+                else hi = mid;
+            }
+            k = lo;
         }
-        const int k = lo, l = row_arc_col[arc_off[b] + q];
+        const int l = row_arc_col[arc_off[b] + q];
         const double mass = row_arc_mass[arc_off[b] + q];
         if (closed_form) {
             const double *Ak = mom + ((int64_t)b * n + k) * MW;
@@ -1258,26 +1264,49 @@ __global__ void __launch_bounds__(MT) price_kernel(
             if (ai != 0.0) {
                 const double am = __dmul_rn(mass, UNIFORM ? W[0] : 0.0);
                 const int ol = block_origin(l, c, f, kappa);
-                for_block_cells(ol, f, kappa, [&](int s, int j) {
-                    int sq = 0, rem = s;
-                    for (int aa = 0; aa < f.nd; ++aa) {
-                        const int d = dd[aa] - rem % kappa;
-                        rem /= kappa;
-                        sq += d * d;
+                // target cells of block l in ascending order with their squared
+                // offsets kept incrementally (no per-cell division)
+                const int K1 = f.nd > 1 ? kappa : 1, K2 = f.nd > 2 ? kappa : 1;
+                int s = 0;
+                for (int o2 = 0; o2 < K2; ++o2) {
+                    const int e2 = f.nd > 2 ? dd[2] - o2 : 0;
+                    for (int o1 = 0; o1 < K1; ++o1) {
+                        const int e1 = f.nd > 1 ? dd[1] - o1 : 0;
+                        const int hsq = e1 * e1 + e2 * e2;
+                        const int row = ol + o2 * (f.nd > 2 ? f.stride[2] : 0) +
+                                        o1 * (f.nd > 1 ? f.stride[1] : 0);
+                        for (int o0 = 0; o0 < kappa; ++o0, ++s) {
+                            const int e0 = dd[0] - o0;
+                            const int sq = hsq + e0 * e0;
+                            const double coef = UNIFORM ? am : __dmul_rn(mass, W[t * m + s]);
+                            const double fitted = __dmul_rn(__dmul_rn(ai, coef), bv[row + o0]);
+                            double cost;
+                            if (p == 2.0) cost = (double)sq;
+                            else if (fast && p == 1.0) cost = (double)sqrt_apx32((float)sq);
+                            else cost = __ldg(table + sq);
+                            acc += fitted * cost;
+                        }
                     }
-                    const double coef = UNIFORM ? am : __dmul_rn(mass, W[t * m + s]);
-                    const double fitted = __dmul_rn(__dmul_rn(ai, coef), bv[j]);
-                    double cost;
-                    if (p == 2.0) cost = (double)sq;
-                    else if (fast && p == 1.0) cost = (double)sqrt_apx32((float)sq);
-                    else cost = __ldg(table + sq);
-                    acc += fitted * cost;
-                });
+                }
             }
         }
     }
     acc = block_sum<MT>(acc, sh);
     if (threadIdx.x == 0) part[(int64_t)b * gridDim.x + blockIdx.x] = acc;
+}
+
+// row block of every arc (CSR order), for the pricing kernel
+__global__ void arc_rows_kernel(const int64_t *__restrict__ arc_off,
+                                const int32_t *__restrict__ row_ptr, int64_t batch, int n,
+                                int32_t *__restrict__ arc_row) {
+    const int64_t total = batch * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / n;
+        const int k = (int)(i - b * n);
+        const int32_t *rp = row_ptr + b * (n + 1);
+        for (int e = rp[k]; e < rp[k + 1]; ++e) arc_row[arc_off[b] + e] = k;
+    }
 }
 
 __global__ void finish_kernel(const double *__restrict__ tv_part, int tv_ctas,
@@ -1422,7 +1451,8 @@ __global__ void sum_parts_kernel(const double *__restrict__ part, int count, dou
 // pairs: moments [B, n, MW], tv partials [B, tv_ctas, 2], price partials
 // [B, pr_ctas]
 struct PrimalLayout {
-    int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, bm_off, fp_off, total, tv_ctas, pr_ctas;
+    int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, bm_off, fp_off, ar_off, total, tv_ctas,
+        pr_ctas;
 };
 
 inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, bool uniform,
@@ -1441,7 +1471,8 @@ inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, b
     L.pc_off = L.pr_off + batch * L.pr_ctas;       // packed arc coordinates (int64)
     L.bm_off = L.pc_off + 2 * batch * max_arcs;    // fine cell -> coarse block (int32)
     L.fp_off = L.bm_off + (f.cells + 1) / 2;        // ipf_fast_kernel partials
-    L.total = L.fp_off + batch * 5 * FCS_MAX * (int64_t)(sizeof(FastPart) / sizeof(double));
+    L.ar_off = L.fp_off + batch * 5 * FCS_MAX * (int64_t)(sizeof(FastPart) / sizeof(double));
+    L.total = L.ar_off + (batch * max_arcs + 1) / 2;  // arc -> row block (int32)
     return L;
 }
 
@@ -1563,6 +1594,10 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
             rpc, cpc, use_smem, nullptr);
     }
     const int closed = uni && p == 2.0;
+    int32_t *arc_row = reinterpret_cast<int32_t *>(ws + L.ar_off);
+    if (!closed)
+        arc_rows_kernel<<<grid_size(batch * c.cells, 256), 256, 0, st>>>(arc_off, row_ptr, batch,
+                                                                         (int)c.cells, arc_row);
     dim3 gtv((unsigned)L.tv_ctas, (unsigned)batch), gpr((unsigned)L.pr_ctas, (unsigned)batch);
     if (uni) {
         moments_tv_kernel<true><<<gtv, MT, 0, st>>>(mu, nu, out, status, ws, L.stride_pair,
@@ -1571,7 +1606,8 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         price_kernel<true><<<gpr, MT, 0, st>>>(arc_off, row_ptr, row_arc_col, row_arc_mass,
                                                kernel_w, out, status, ws, L.stride_pair,
                                                ws + L.mom_off, ws + L.pr_off, f32, c32, kappa, p,
-                                               cost_table, closed, mode == GDT_MODE_FAST);
+                                               cost_table, closed, mode == GDT_MODE_FAST,
+                                               closed ? nullptr : arc_row);
     } else {
         moments_tv_kernel<false><<<gtv, MT, 0, st>>>(mu, nu, out, status, ws, L.stride_pair,
                                                      ws + L.mom_off, ws + L.tv_off, f32, c32,
@@ -1579,7 +1615,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         price_kernel<false><<<gpr, MT, 0, st>>>(arc_off, row_ptr, row_arc_col, row_arc_mass,
                                                 kernel_w, out, status, ws, L.stride_pair,
                                                 ws + L.mom_off, ws + L.pr_off, f32, c32, kappa, p,
-                                                cost_table, 0, mode == GDT_MODE_FAST);
+                                                cost_table, 0, mode == GDT_MODE_FAST, arc_row);
     }
     finish_kernel<<<grid_size(batch, 128), 128, 0, st>>>(ws + L.tv_off, (int)L.tv_ctas,
                                                          ws + L.pr_off, (int)L.pr_ctas, status,
