@@ -275,17 +275,25 @@ __device__ __forceinline__ void pair_sync(int id) {
     asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
 
+constexpr int CT_TAB_TILES = 256;  // (128 / 8)^2 source tiles at most
+
 __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
     const float *__restrict__ v, const float *__restrict__ tmax, float *__restrict__ out,
     int64_t batch, Grid g, unsigned long long *__restrict__ counter) {
     extern __shared__ __align__(16) float ct_tab[];  // [CT_TAB_ROWS][CT_TAB_W]
     __shared__ float other[CT_TAB_REG][32][8];
     __shared__ long long next_region[CT_TAB_REG];
+    // per warp pair: the region's tiles in Chebyshev-ring order, packed
+    // (ring << 16) | tile, and the cursor both warps take tiles from
+    __shared__ unsigned tiles_s[CT_TAB_REG][CT_TAB_TILES];
+    __shared__ int ring_cnt[CT_TAB_REG][17];
+    __shared__ int cursor[CT_TAB_REG];
     const int lane = threadIdx.x & 31;
     const int warp_in_cta = threadIdx.x >> 5;
     const int half = warp_in_cta & 1;
     const int slot = warp_in_cta >> 1;
-    const int bar_id = 1 + slot;  // named barrier of this warp pair
+    const int pt = threadIdx.x & 63;  // thread index inside the pair
+    const int bar_id = 1 + slot;      // named barrier of this warp pair
     const int N0 = (int)g.n[0], N1 = (int)g.n[1];
     // table: row dy, column i -> sqrt((i - 7)^2 + dy^2), correctly rounded
     for (int e = threadIdx.x; e < CT_TAB_ROWS * CT_TAB_W; e += blockDim.x) {
@@ -298,102 +306,131 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
     const int nr0 = N0 / 16, nr1 = N1 / 16;
     const int64_t regions = (int64_t)nr0 * nr1;
     const int64_t total = batch * regions;
-    const int nt0 = N0 / 8, nt1 = N1 / 8;
+    const int nt0 = N0 / 8, nt1 = N1 / 8, ntiles = nt0 * nt1;
     // persistent warp pairs: each pair takes the next region from a global
-    // counter (pruned work per region is uneven)
+    // counter (pruned work per region is uneven); inside a region the two
+    // warps take ring-ordered tiles from a shared cursor
     for (;;) {
-        if (half == 0 && lane == 0)
-            next_region[slot] = (long long)atomicAdd(counter, 1ull);
+        if (pt == 0) next_region[slot] = (long long)atomicAdd(counter, 1ull);
+        if (pt < 17) ring_cnt[slot][pt] = 0;
         pair_sync(bar_id);
         const int64_t region = next_region[slot];
         if (region >= total) break;
-        float best[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) best[r] = INFINITY;
         const int64_t b = region / regions;
         const int rr = (int)(region - b * regions);
         const int rx = rr % nr0, ry = rr / nr0;
         const int X0 = rx * 16, Y0 = ry * 16;
+        const int h0lo = X0 / 8, h0hi = h0lo + 1, h1lo = Y0 / 8, h1hi = h1lo + 1;
+        // ring of every tile, counting sort into ring order
+        int my_ring[CT_TAB_TILES / 64];
+#pragma unroll
+        for (int q = 0; q < CT_TAB_TILES / 64; ++q) {
+            const int t = pt + 64 * q;
+            my_ring[q] = -1;
+            if (t < ntiles) {
+                const int t0 = t % nt0, t1 = t / nt0;
+                const int d0 = t0 < h0lo ? h0lo - t0 : (t0 > h0hi ? t0 - h0hi : 0);
+                const int d1 = t1 < h1lo ? h1lo - t1 : (t1 > h1hi ? t1 - h1hi : 0);
+                my_ring[q] = max(d0, d1);
+                atomicAdd(&ring_cnt[slot][my_ring[q]], 1);
+            }
+        }
+        pair_sync(bar_id);
+        if (pt == 0) {
+            int acc = 0;
+            for (int r = 0; r < 17; ++r) {
+                const int c = ring_cnt[slot][r];
+                ring_cnt[slot][r] = acc;
+                acc += c;
+            }
+            cursor[slot] = 0;
+        }
+        pair_sync(bar_id);
+#pragma unroll
+        for (int q = 0; q < CT_TAB_TILES / 64; ++q) {
+            const int t = pt + 64 * q;
+            if (my_ring[q] >= 0) {
+                const int pos = atomicAdd(&ring_cnt[slot][my_ring[q]], 1);
+                tiles_s[slot][pos] = ((unsigned)my_ring[q] << 16) | (unsigned)t;
+            }
+        }
+        pair_sync(bar_id);
+
+        float best[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) best[r] = INFINITY;
         const int xj0 = X0 + 8 * (lane & 1);
         const int yj = Y0 + (lane >> 1);
         const float *vb = v + b * g.cells;
-        const float *tm = tmax + b * (int64_t)nt0 * nt1;
+        const float *tm = tmax + b * (int64_t)ntiles;
         float vall = -INFINITY;
-        for (int i = lane; i < nt0 * nt1; i += 32) vall = fmaxf(vall, tm[i]);
+        for (int i = lane; i < ntiles; i += 32) vall = fmaxf(vall, tm[i]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) vall = fmaxf(vall, __shfl_xor_sync(0xffffffffu, vall, o));
         float ub = INFINITY;
-        const int h0lo = X0 / 8, h0hi = h0lo + 1, h1lo = Y0 / 8, h1hi = h1lo + 1;
-        const int rmax = max(nt0, nt1);
-        int parity = 0;
-        for (int r = 0; r <= rmax; ++r) {
-            if (r >= 1) {  // smallest cost any tile of ring r can reach
+        int cur_ring = 0;
+        for (;;) {
+            int idx = 0;
+            if (lane == 0) idx = atomicAdd(&cursor[slot], 1);
+            idx = __shfl_sync(0xffffffffu, idx, 0);
+            if (idx >= ntiles) break;
+            const unsigned e = tiles_s[slot][idx];
+            const int r = (int)(e >> 16), t = (int)(e & 0xffffu);
+            if (r != cur_ring) {  // entering ring r: the ring bound may end this warp
+                cur_ring = r;
                 const int gap = (r - 1) * 8 + 1;
                 const float cmin = gap + 7 < CT_TAB_W ? ct_tab[gap + 7] : sqrtf((float)gap * gap);
                 if (cmin - vall >= ub) break;
             }
-            const int a0 = max(h0lo - r, 0), b0 = min(h0hi + r, nt0 - 1);
-            const int a1 = max(h1lo - r, 0), b1 = min(h1hi + r, nt1 - 1);
-            for (int t1 = a1; t1 <= b1; ++t1) {
-                const int d1 = t1 < h1lo ? h1lo - t1 : (t1 > h1hi ? t1 - h1hi : 0);
-                const bool face = d1 == r;
-                const int step = face ? 1 : (h0hi + r) - (h0lo - r);
-                for (int t0 = face ? a0 : h0lo - r; t0 <= b0; t0 += step > 0 ? step : 1) {
-                    if (t0 < a0) continue;
-                    const int d0 = t0 < h0lo ? h0lo - t0 : (t0 > h0hi ? t0 - h0hi : 0);
-                    if (max(d0, d1) != r) continue;
-                    if (((parity++) & 1) != half) continue;
-                    const int g0 = max(0, max(t0 * 8 - (X0 + 15), X0 - (t0 * 8 + 7)));
-                    const int g1 = max(0, max(t1 * 8 - (Y0 + 15), Y0 - (t1 * 8 + 7)));
-                    const float lb = ct_tab[g1 * CT_TAB_W + g0 + 7] - tm[t1 * nt0 + t0];
-                    if (lb >= ub) continue;
-                    const int sx0 = t0 * 8, off = sx0 - xj0;
-                    const int base = off >= 0 ? off : -off;
-                    for (int y = 0; y < 8; ++y) {
-                        const int ys = t1 * 8 + y;
-                        const int dy = ys > yj ? ys - yj : yj - ys;
-                        const float4 *trow = reinterpret_cast<const float4 *>(
-                            ct_tab + dy * CT_TAB_W + base);
-                        float L[16];
+            const int t0 = t % nt0, t1 = t / nt0;
+            const int g0 = max(0, max(t0 * 8 - (X0 + 15), X0 - (t0 * 8 + 7)));
+            const int g1 = max(0, max(t1 * 8 - (Y0 + 15), Y0 - (t1 * 8 + 7)));
+            const float lb = ct_tab[g1 * CT_TAB_W + g0 + 7] - tm[t];
+            if (lb >= ub) continue;
+            const int sx0 = t0 * 8, off = sx0 - xj0;
+            const int base = off >= 0 ? off : -off;
+            const float *vrow = vb + (int64_t)(t1 * 8) * N0 + sx0;
+            for (int y = 0; y < 8; ++y) {
+                const int ys = t1 * 8 + y;
+                const int dy = ys > yj ? ys - yj : yj - ys;
+                const float4 *trow = reinterpret_cast<const float4 *>(ct_tab + dy * CT_TAB_W + base);
+                float L[16];
 #pragma unroll
-                        for (int c4 = 0; c4 < 4; ++c4) {
-                            const float4 t = trow[c4];
-                            L[4 * c4] = t.x;
-                            L[4 * c4 + 1] = t.y;
-                            L[4 * c4 + 2] = t.z;
-                            L[4 * c4 + 3] = t.w;
-                        }
-                        float cst[15];
-                        if (off >= 0) {
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    const float4 tt = trow[c4];
+                    L[4 * c4] = tt.x;
+                    L[4 * c4 + 1] = tt.y;
+                    L[4 * c4 + 2] = tt.z;
+                    L[4 * c4 + 3] = tt.w;
+                }
+                float cst[15];
+                if (off >= 0) {
 #pragma unroll
-                            for (int q = 0; q < 15; ++q) cst[q] = L[q];
-                        } else {
+                    for (int q = 0; q < 15; ++q) cst[q] = L[q];
+                } else {
 #pragma unroll
-                            for (int q = 0; q < 15; ++q) cst[q] = L[14 - q];
-                        }
-                        const float *row = vb + (int64_t)ys * N0 + sx0;
-                        const float4 v0 = __ldg(reinterpret_cast<const float4 *>(row));
-                        const float4 v1 = __ldg(reinterpret_cast<const float4 *>(row) + 1);
-                        const float vs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                    for (int q = 0; q < 15; ++q) cst[q] = L[14 - q];
+                }
+                const float4 v0 = __ldg(reinterpret_cast<const float4 *>(vrow + y * N0));
+                const float4 v1 = __ldg(reinterpret_cast<const float4 *>(vrow + y * N0) + 1);
+                const float vs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-                        for (int r8 = 0; r8 < 8; ++r8) {
+                for (int r8 = 0; r8 < 8; ++r8) {
 #pragma unroll
-                            for (int s2 = 0; s2 < 8; s2 += 2) {
-                                float c0, c1;
-                                sub_f32x2(cst[s2 - r8 + 7], cst[s2 + 1 - r8 + 7], vs[s2],
-                                          vs[s2 + 1], c0, c1);
-                                best[r8] = fmin3(best[r8], c0, c1);
-                            }
-                        }
+                    for (int s2 = 0; s2 < 8; s2 += 2) {
+                        float c0, c1;
+                        sub_f32x2(cst[s2 - r8 + 7], cst[s2 + 1 - r8 + 7], vs[s2], vs[s2 + 1], c0,
+                                  c1);
+                        best[r8] = fmin3(best[r8], c0, c1);
                     }
-                    float m = best[0];
-#pragma unroll
-                    for (int r8 = 1; r8 < 8; ++r8) m = fmaxf(m, best[r8]);
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-                    ub = m;
                 }
             }
+            float m = best[0];
+#pragma unroll
+            for (int r8 = 1; r8 < 8; ++r8) m = fmaxf(m, best[r8]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            ub = m;
         }
         // merge the two warps' minima
         if (half == 1) {
@@ -409,6 +446,7 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
                 ob[r8] = o < best[r8] ? o : best[r8];
             }
         }
+        pair_sync(bar_id);  // the pair's shared lists are reused by the next region
     }
 }
 
