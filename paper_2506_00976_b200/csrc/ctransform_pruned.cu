@@ -351,7 +351,8 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
             const int t = pt + 64 * q;
             if (my_ring[q] >= 0) {
                 const int pos = atomicAdd(&ring_cnt[slot][my_ring[q]], 1);
-                tiles_s[slot][pos] = ((unsigned)my_ring[q] << 16) | (unsigned)t;
+                tiles_s[slot][pos] = ((unsigned)my_ring[q] << 16) |
+                                     ((unsigned)(t / nt0) << 8) | (unsigned)(t % nt0);
             }
         }
         pair_sync(bar_id);
@@ -359,8 +360,11 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
         float best[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) best[r] = INFINITY;
-        const int xj0 = X0 + 8 * (lane & 1);
-        const int yj = Y0 + (lane >> 1);
+        // lanes 0-15: rows Y0.., left 8 columns; lanes 16-31: right 8 columns
+        // (the 8 lanes of a quarter warp read 8 different table rows: with a
+        // row stride of 12 mod 32 banks their 16-byte reads do not conflict)
+        const int xj0 = X0 + 8 * (lane >> 4);
+        const int yj = Y0 + (lane & 15);
         const float *vb = v + b * g.cells;
         const float *tm = tmax + b * (int64_t)ntiles;
         float vall = -INFINITY;
@@ -375,14 +379,14 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
             idx = __shfl_sync(0xffffffffu, idx, 0);
             if (idx >= ntiles) break;
             const unsigned e = tiles_s[slot][idx];
-            const int r = (int)(e >> 16), t = (int)(e & 0xffffu);
+            const int r = (int)(e >> 16), t1 = (int)((e >> 8) & 0xffu), t0 = (int)(e & 0xffu);
+            const int t = t1 * nt0 + t0;
             if (r != cur_ring) {  // entering ring r: the ring bound may end this warp
                 cur_ring = r;
                 const int gap = (r - 1) * 8 + 1;
                 const float cmin = gap + 7 < CT_TAB_W ? ct_tab[gap + 7] : sqrtf((float)gap * gap);
                 if (cmin - vall >= ub) break;
             }
-            const int t0 = t % nt0, t1 = t / nt0;
             const int g0 = max(0, max(t0 * 8 - (X0 + 15), X0 - (t0 * 8 + 7)));
             const int g1 = max(0, max(t1 * 8 - (Y0 + 15), Y0 - (t1 * 8 + 7)));
             const float lb = ct_tab[g1 * CT_TAB_W + g0 + 7] - tm[t];
