@@ -24,6 +24,104 @@ namespace gdt {
 // separable p == 2: one pass along axis `ax`
 //   out[.., j, ..] = min_i (i - j)^2 + sign * in[.., i, ..]
 // ---------------------------------------------------------------------------
+// Register-tiled 1-D min-plus pass (the same arithmetic as sep_pass_kernel:
+// cand = (TO)(d*d) + line[i], exact min): a thread owns 8 consecutive outputs
+// of one line and sweeps the sources 8 at a time; the 15 squared offsets of a
+// chunk come from a shared table (aligned 16-byte reads) and fp32 candidates
+// use packed add.f32x2 + 3-input min.  Lines of the CTA are interleaved so
+// strided-axis loads and stores coalesce.
+__device__ __forceinline__ void add_f32x2(float c0, float c1, float v0, float v1, float &r0,
+                                          float &r1) {
+    unsigned long long rr;
+    asm("add.rn.f32x2 %0, %1, %2;"
+        : "=l"(rr)
+        : "l"((unsigned long long)__float_as_uint(c0) | ((unsigned long long)__float_as_uint(c1) << 32)),
+          "l"((unsigned long long)__float_as_uint(v0) | ((unsigned long long)__float_as_uint(v1) << 32)));
+    r0 = __uint_as_float((unsigned)(rr & 0xffffffffu));
+    r1 = __uint_as_float((unsigned)(rr >> 32));
+}
+
+__device__ __forceinline__ float fmin3f(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+constexpr int SEPT = 256;  // threads per CTA of sep_tile_kernel
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ in,
+                                                        TO *__restrict__ out, int64_t batch,
+                                                        int64_t cells, int L, int64_t S,
+                                                        bool negate, int lpc) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tpl = L / 8;
+    TO *sq = reinterpret_cast<TO *>(smem_raw);          // [2L + 16]: sq[k] = (k - L - 7)^2
+    TO *lines = sq + ((2 * L + 16 + 3) & ~3);            // [lpc][L]
+    const int64_t lines_per_pair = cells / L;
+    const int64_t total_lines = batch * lines_per_pair;
+    const int64_t line0 = (int64_t)blockIdx.x * lpc;
+    for (int k = threadIdx.x; k < 2 * L + 16; k += blockDim.x) {
+        const int d = k - L - 7;
+        sq[k] = (TO)(d * d);
+    }
+    // load: consecutive threads -> consecutive lines (coalesced when S > 1)
+    for (int e = threadIdx.x; e < lpc * L; e += blockDim.x) {
+        const int li = e % lpc, i = e / lpc;
+        const int64_t lid = line0 + li;
+        TO v = (TO)0;
+        if (lid < total_lines) {
+            const int64_t b = lid / lines_per_pair, r = lid - b * lines_per_pair;
+            const int64_t low = r % S, high = r / S;
+            v = (TO)in[b * cells + high * S * L + low + (int64_t)i * S];
+            if (negate) v = -v;
+        }
+        lines[li * L + i] = v;
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    const int li = t % lpc, tl = t / lpc;
+    if (tl >= tpl) return;
+    const int64_t lid = line0 + li;
+    const TO *line = lines + li * L;
+    const int j0 = 8 * tl;
+    TO best[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) best[r] = (TO)INFINITY;
+    for (int i0 = 0; i0 < L; i0 += 8) {
+        TO vs[8], cst[16];
+        const TO *cp = sq + (i0 - j0 + L);  // squares of d = i0 - j0 - 7 + q
+#pragma unroll
+        for (int q = 0; q < 8; ++q) vs[q] = line[i0 + q];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) cst[q] = cp[q];
+        if constexpr (sizeof(TO) == 4) {
+#pragma unroll
+            for (int r8 = 0; r8 < 8; ++r8)
+#pragma unroll
+                for (int s2 = 0; s2 < 8; s2 += 2) {
+                    float c0, c1;
+                    add_f32x2(cst[s2 - r8 + 7], cst[s2 + 1 - r8 + 7], vs[s2], vs[s2 + 1], c0, c1);
+                    best[r8] = fmin3f(best[r8], c0, c1);
+                }
+        } else {
+#pragma unroll
+            for (int r8 = 0; r8 < 8; ++r8)
+#pragma unroll
+                for (int s = 0; s < 8; ++s) {
+                    const TO cand = cst[s - r8 + 7] + vs[s];
+                    best[r8] = cand < best[r8] ? cand : best[r8];
+                }
+        }
+    }
+    if (lid >= total_lines) return;
+    const int64_t b = lid / lines_per_pair, r = lid - b * lines_per_pair;
+    const int64_t low = r % S, high = r / S;
+    TO *o = out + b * cells + high * S * L + low;
+#pragma unroll
+    for (int r8 = 0; r8 < 8; ++r8) o[(int64_t)(j0 + r8) * S] = best[r8];
+}
+
 template <typename TI, typename TO>
 __global__ void sep_pass_kernel(const TI *__restrict__ in, TO *__restrict__ out, int64_t batch,
                                 Grid g, int ax, bool negate) {
@@ -302,10 +400,36 @@ extern "C" int gdt_ctransform_grid(const void *v, void *out, int64_t batch, int 
         int src_dtype = in_dtype;
         for (int ax = 0; ax < ndim; ++ax) {
             const int64_t L = g.n[ax];
+            void *o = bufs[dst];
+            if (L % 8 == 0 && L / 8 <= SEPT) {
+                // lines per CTA: fill the CTA, but keep >= 2 CTAs per SM
+                const int tpl = (int)(L / 8);
+                int dev = 0, nsm = 148;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                const int64_t lines = total / L;
+                int lpc = SEPT / tpl;
+                while (lpc > 1 && (lines + lpc - 1) / lpc < 2 * nsm) lpc >>= 1;
+                const int thr = ((lpc * tpl + 31) / 32) * 32;
+                const unsigned ctas = (unsigned)((lines + lpc - 1) / lpc);
+                const size_t sh = el * (((2 * L + 16 + 3) & ~3) + (size_t)lpc * L);
+                if (dtype == 0)
+                    sep_tile_kernel<double, double><<<ctas, thr, sh, st>>>(
+                        (const double *)src, (double *)o, batch, g.cells, (int)L, g.stride[ax], ax == 0, lpc);
+                else if (src_dtype == 0)
+                    sep_tile_kernel<double, float><<<ctas, thr, sh, st>>>(
+                        (const double *)src, (float *)o, batch, g.cells, (int)L, g.stride[ax], ax == 0, lpc);
+                else
+                    sep_tile_kernel<float, float><<<ctas, thr, sh, st>>>(
+                        (const float *)src, (float *)o, batch, g.cells, (int)L, g.stride[ax], ax == 0, lpc);
+                src = o;
+                src_dtype = dtype;
+                dst ^= 1;
+                continue;
+            }
             const unsigned ctas = (unsigned)(total / L);
             const int thr = L >= 256 ? 256 : (int)((L + 31) / 32 * 32);
             const size_t sh = L * el;
-            void *o = bufs[dst];
             if (dtype == 0)
                 sep_pass_kernel<double, double><<<ctas, thr, sh, st>>>(
                     (const double *)src, (double *)o, batch, g, ax, ax == 0);
