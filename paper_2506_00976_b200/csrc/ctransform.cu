@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ i
     }
     // load: consecutive threads -> consecutive lines (coalesced when S > 1)
     for (int e = threadIdx.x; e < lpc * L; e += blockDim.x) {
-        const int li = e % lpc, i = e / lpc;
+        // contiguous axis: i fastest; strided axis: consecutive lines fastest
+        const int li = S == 1 ? e / L : e % lpc, i = S == 1 ? e % L : e / lpc;
         const int64_t lid = line0 + li;
         TO v = (TO)0;
         if (lid < total_lines) {
@@ -299,14 +300,25 @@ __global__ void __launch_bounds__(FT) brute_f32_kernel(const float *__restrict__
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) dot_mass_kernel(const T *__restrict__ x,
-                                                       const double *__restrict__ m, int64_t n,
-                                                       double *__restrict__ out) {
+__global__ void __launch_bounds__(1024) dot_mass_kernel(const T *__restrict__ x,
+                                                        const double *__restrict__ m, int64_t n,
+                                                        double *__restrict__ out) {
     __shared__ double sh[32];
     const int64_t b = blockIdx.x;
-    double acc = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += 256) acc += (double)x[b * n + i] * m[b * n + i];
-    acc = block_sum<256>(acc, sh);
+    const T *xb = x + b * n;
+    const double *mb = m + b * n;
+    // four independent partial sums per thread (loads in flight), fixed order
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t i = threadIdx.x;
+    for (; i + 3 * 1024 < n; i += 4 * 1024) {
+        a0 += (double)xb[i] * mb[i];
+        a1 += (double)xb[i + 1024] * mb[i + 1024];
+        a2 += (double)xb[i + 2048] * mb[i + 2048];
+        a3 += (double)xb[i + 3072] * mb[i + 3072];
+    }
+    for (; i < n; i += 1024) a0 += (double)xb[i] * mb[i];
+    double acc = (a0 + a1) + (a2 + a3);
+    acc = block_sum<1024>(acc, sh);
     if (threadIdx.x == 0) out[b] = acc;
 }
 
@@ -479,10 +491,10 @@ extern "C" int gdt_ctransform_grid(const void *v, void *out, int64_t batch, int 
     }
     if (mass != nullptr && dot_out != nullptr) {
         if (dtype == 0)
-            dot_mass_kernel<double><<<(unsigned)batch, 256, 0, st>>>((const double *)out, mass,
+            dot_mass_kernel<double><<<(unsigned)batch, 1024, 0, st>>>((const double *)out, mass,
                                                                     g.cells, dot_out);
         else
-            dot_mass_kernel<float><<<(unsigned)batch, 256, 0, st>>>((const float *)out, mass,
+            dot_mass_kernel<float><<<(unsigned)batch, 1024, 0, st>>>((const float *)out, mass,
                                                                    g.cells, dot_out);
     }
     return cuda_status("gdt_ctransform_grid");

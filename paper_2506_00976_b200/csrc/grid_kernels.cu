@@ -6,6 +6,8 @@
 #include <mutex>
 #include <string>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace gdt {
@@ -110,6 +112,84 @@ __device__ __forceinline__ int64_t upper_count(const double *ax, int64_t n, doub
     return lo;
 }
 
+// Multilinear interpolation with the per-axis bracket (lo, hi, t) of every
+// fine coordinate precomputed once per CTA in shared memory (the same
+// arithmetic as interpolate_kernel, which recomputes it per cell).
+constexpr int IP_MAX_AX = 2048;  // sum of fine axis lengths handled by the table kernel
+
+__global__ void __launch_bounds__(256) interpolate_tab_kernel(
+    const double *__restrict__ coarse, double *__restrict__ fine, int64_t batch, Grid f, Grid c,
+    const double *__restrict__ axes) {
+    __shared__ double tt_s[IP_MAX_AX];
+    __shared__ int lo_s[IP_MAX_AX], hi_s[IP_MAX_AX];
+    int base[GDT_MAX_DIM], cb[GDT_MAX_DIM];
+    {
+        int o = 0, co = 0;
+        for (int a = 0; a < f.nd; ++a) {
+            base[a] = o;
+            cb[a] = co;
+            o += (int)f.n[a];
+            co += (int)c.n[a];
+        }
+        for (int e = threadIdx.x; e < o; e += blockDim.x) {
+            int a = 0;
+            while (a + 1 < f.nd && e >= base[a + 1]) ++a;
+            const double q = (double)(e - base[a] + 1);  // 1-based coordinate
+            const double *ax = axes + cb[a];
+            const int64_t n = c.n[a];
+            int64_t i0 = upper_count(ax, n, q) - 1;
+            const int64_t top = n - 2 > 0 ? n - 2 : 0;
+            if (i0 < 0) i0 = 0;
+            if (i0 > top) i0 = top;
+            const int64_t i1 = i0 + 1 < n - 1 ? i0 + 1 : n - 1;
+            const double span = __dsub_rn(ax[i1], ax[i0]);
+            double t = span > 0.0 ? __ddiv_rn(__dsub_rn(q, ax[i0]), span) : 0.0;
+            t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+            lo_s[e] = (int)i0;
+            hi_s[e] = (int)i1;
+            tt_s[e] = t;
+        }
+    }
+    __syncthreads();
+    const int64_t total = batch * f.cells;
+    const int nd = f.nd, corners = 1 << nd;
+    int fs[GDT_MAX_DIM], cs[GDT_MAX_DIM];
+#pragma unroll
+    for (int a = 0; a < GDT_MAX_DIM; ++a) {
+        fs[a] = (int)f.stride[a];
+        cs[a] = (int)c.stride[a];
+    }
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = idx / f.cells;
+        int rem = (int)(idx - b * f.cells);
+        int e[GDT_MAX_DIM] = {0, 0, 0, 0};
+#pragma unroll
+        for (int a = GDT_MAX_DIM - 1; a >= 0; --a)
+            if (a < nd) {
+                const int x = rem / fs[a];
+                rem -= x * fs[a];
+                e[a] = base[a] + x;
+            }
+        const double *T = coarse + b * c.cells;
+        double out = 0.0;
+        for (int cidx = 0; cidx < corners; ++cidx) {
+            double w = 1.0;
+            int off = 0;
+#pragma unroll
+            for (int a = 0; a < GDT_MAX_DIM; ++a)
+                if (a < nd) {
+                    const int side = (cidx >> (nd - 1 - a)) & 1;  // axis 0 slowest
+                    const double t = tt_s[e[a]];
+                    w = __dmul_rn(w, side ? t : __dsub_rn(1.0, t));
+                    off += (side ? hi_s[e[a]] : lo_s[e[a]]) * cs[a];
+                }
+            out = __dadd_rn(out, __dmul_rn(w, T[off]));
+        }
+        fine[idx] = out;
+    }
+}
+
 __global__ void interpolate_kernel(const double *__restrict__ coarse, double *__restrict__ fine,
                                    int64_t batch, Grid f, Grid c, const double *__restrict__ axes,
                                    int method) {
@@ -197,7 +277,18 @@ __global__ void __launch_bounds__(256) coarse_ct_kernel(const double *__restrict
     const int32_t *db = dst + b * n;
     const double *Ck = C + k * n;
     double best = INFINITY;
-    for (int l = lane; l < len; l += 32) best = fmin(best, __dsub_rn(Ck[db[l]], gb[l]));
+    if (len == n) {  // full target support: dst is the identity, the row is contiguous
+        int l = lane;
+        double b1 = INFINITY;
+        for (; l + 32 < len; l += 64) {
+            best = fmin(best, __dsub_rn(__ldg(Ck + l), __ldg(gb + l)));
+            b1 = fmin(b1, __dsub_rn(__ldg(Ck + l + 32), __ldg(gb + l + 32)));
+        }
+        for (; l < len; l += 32) best = fmin(best, __dsub_rn(__ldg(Ck + l), __ldg(gb + l)));
+        best = fmin(best, b1);
+    } else {
+        for (int l = lane; l < len; l += 32) best = fmin(best, __dsub_rn(Ck[db[l]], gb[l]));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
     if (lane == 0) f_ext[w] = best;
@@ -295,8 +386,17 @@ int gdt_interpolate(const double *coarse, double *fine, int64_t batch, int ndim,
                   "gdt_interpolate: bad grid");
     GDT_CHECK_ARG(method == 0 || method == 1, "gdt_interpolate: method must be 0 or 1");
     if (batch == 0) return GDT_OK;
-    interpolate_kernel<<<grid_size(batch * f.cells, 256), 256, 0, as_stream(stream)>>>(
-        coarse, fine, batch, f, c, axes, method);
+    int64_t axsum = 0;
+    for (int a = 0; a < ndim; ++a) axsum += dims[a];
+    if (method == 0 && axsum <= IP_MAX_AX && f.cells < (1ll << 31)) {
+        const int64_t want = (batch * f.cells + 255) / 256;
+        const unsigned ctas = (unsigned)std::min<int64_t>(want, 148 * 8);  // amortise the tables
+        interpolate_tab_kernel<<<ctas, 256, 0, as_stream(stream)>>>(coarse, fine, batch, f, c,
+                                                                    axes);
+    } else {
+        interpolate_kernel<<<grid_size(batch * f.cells, 256), 256, 0, as_stream(stream)>>>(
+            coarse, fine, batch, f, c, axes, method);
+    }
     return cuda_status("gdt_interpolate");
 }
 
