@@ -114,3 +114,69 @@ def test_fast_ipf_default_xi_and_statuses(small_cases):
         if not isinstance(e, Exception):
             assert e.iterations == f.iterations, c["tag"]
             assert abs(e.value - f.value) <= 1e-6 * abs(e.value), c["tag"]
+
+
+def _f32_brute_ct(v32, dims, p):
+    """fp32 emulation of the table-driven p=1 / brute-force c-transform:
+    min_i (RN32(cost_ij) - v_i) with correctly rounded fp32 costs."""
+    from oracle import port as P
+
+    X = P.grid_coords(dims)
+    sq = ((X[:, None, :] - X[None, :, :]) ** 2).sum(-1).astype(np.float32)
+    cost = np.sqrt(sq) if p == 1.0 else sq
+    return np.min(cost - v32[:, None], axis=0)
+
+
+@pytest.mark.parametrize("dims", [(32, 32), (64, 48), (48, 128), (128, 16)])
+def test_fp32_p1_table_ctransform_bit_exact_emulation(dims):
+    """The shared-memory-table p=1 kernel computes exactly the fp32 brute
+    force with correctly rounded costs (numpy float32 emulation), on smooth
+    and rough potentials; the second transform too."""
+    from oracle import port as P
+    from paper_2506_00976_b200.engine import ctransform_pair
+
+    rng = np.random.default_rng(dims[0] * 7 + dims[1])
+    n = int(np.prod(dims))
+    X = P.grid_coords(dims)
+    smooth = np.sin(X[:, 0] / 5.0) * 7.0 + np.cos(X[:, 1] / 3.0) * 4.0
+    for v in (smooth, rng.normal(size=n) * 10.0):
+        mass = np.full(n, 1.0 / n)
+        f, g, _ = ctransform_pair(to_dev(v[None]), to_dev(mass[None]), to_dev(mass[None]), dims,
+                                  1.0, "fp32")
+        g32 = to_host(g)[0]
+        ref_g = _f32_brute_ct(v.astype(np.float32), dims, 1.0)
+        assert np.array_equal(g32, ref_g)
+        ref_f = _f32_brute_ct(ref_g, dims, 1.0)
+        assert np.array_equal(to_host(f)[0], ref_f)
+
+
+def _f32_separable_ct(v32, dims, negate_first=True):
+    """fp32 emulation of the separable p=2 passes: along each axis (axis 0 =
+    fastest, first pass negates), cand = RN32(d^2) + line_i, exact min."""
+    a = v32.reshape(tuple(reversed(dims)))  # C-order view: last index = axis 0
+    nd = len(dims)
+    for ax in range(nd):
+        arr_ax = nd - 1 - ax
+        a = np.moveaxis(a, arr_ax, -1)
+        L = a.shape[-1]
+        d2 = ((np.arange(L)[:, None] - np.arange(L)[None, :]) ** 2).astype(np.float32)
+        line = -a if (ax == 0 and negate_first) else a
+        a = np.min(line[..., :, None] + d2, axis=-2)
+        a = np.moveaxis(a.astype(np.float32), -1, arr_ax)
+    return a.reshape(-1)
+
+
+@pytest.mark.parametrize("dims", [(128, 128), (64, 32), (20, 12), (16, 8, 24)])
+def test_fp32_separable_ctransform_bit_exact_emulation(dims):
+    """Register-tiled (and, for lengths not divisible by 8, the plain) p=2
+    passes equal the fp32 separable emulation bit for bit."""
+    from paper_2506_00976_b200.engine import ctransform_pair
+
+    rng = np.random.default_rng(len(dims) + dims[0])
+    n = int(np.prod(dims))
+    v = rng.normal(size=n) * 50.0
+    mass = np.full(n, 1.0 / n)
+    f, g, _ = ctransform_pair(to_dev(v[None]), to_dev(mass[None]), to_dev(mass[None]), dims, 2.0,
+                              "fp32")
+    ref_g = _f32_separable_ct(v.astype(np.float32), dims)
+    assert np.array_equal(to_host(g)[0], ref_g)
