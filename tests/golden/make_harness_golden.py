@@ -1,0 +1,50 @@
+"""Golden CSV of the reference's bench matrix (build container only).
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_harness_golden.py
+
+Runs the LIVE reference ``gridot.cli.bench_run`` on a small matrix (all three
+generator classes, exact + the four quantization bounds) and writes
+``tests/golden/harness_bench.csv`` plus the generated measures of every pair
+(``tests/golden/harness_measures.npz``), so ``paper_2506_00976_b200.harness``
+can be checked for the same measures (CPU) and the same rows (GPU).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.environ.get("GRIDOT_REF", "/root/reference/pkg/src"))
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+from gridot import cli  # noqa: E402
+
+CFG = dict(classes=("gaussians", "shapes", "noise"), n=8, d=2, p_values=(1.0, 2.0),
+           kappas=(2, 4), seed=7, n_pairs=2,
+           methods=("exact", "weighted_cost", "min_cost", "primal_upscaling", "dual_upscaling"))
+
+
+def main():
+    cfg = cli.BenchConfig(**CFG)
+    rows = cli.bench_run(cfg)
+    with open(os.path.join(HERE, "harness_bench.csv"), "w", newline="") as fh:
+        cli.write_csv(rows, fh)
+    meas = {}
+    for ci, cls in enumerate(cfg.classes):
+        for pi in range(cfg.n_pairs):
+            for side in (0, 1):
+                m = cli.gen_synthetic(cls, cfg.n, cfg.d, seed=[cfg.seed, ci, pi, side])
+                meas[f"{cls}_{pi}_{side}"] = m.mass
+    # a 3-D case for the generator only
+    for cls in cfg.classes:
+        meas[f"{cls}_3d"] = cli.gen_synthetic(cls, 6, 3, seed=[11, 2]).mass
+    np.savez_compressed(os.path.join(HERE, "harness_measures.npz"), **meas)
+    print(len(rows), "rows")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,86 @@
+"""Bench-matrix harness (reference cli.py bench): generators, config checks,
+CSV schema and the exact baseline on CPU; the full device matrix against the
+reference's own CSV on the GPU (tests/golden/make_harness_golden.py)."""
+
+from __future__ import annotations
+
+import csv
+import io
+import os
+
+import numpy as np
+import pytest
+
+from paper_2506_00976_b200 import harness as H
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+CFG = dict(classes=("gaussians", "shapes", "noise"), n=8, d=2, p_values=(1.0, 2.0),
+           kappas=(2, 4), seed=7, n_pairs=2,
+           methods=("exact", "weighted_cost", "min_cost", "primal_upscaling", "dual_upscaling"))
+
+
+def _golden_rows():
+    with open(os.path.join(GOLD, "harness_bench.csv")) as fh:
+        return list(csv.DictReader(fh))
+
+
+def test_generators_match_reference_bit_for_bit():
+    z = np.load(os.path.join(GOLD, "harness_measures.npz"))
+    for ci, cls in enumerate(CFG["classes"]):
+        for pi in range(CFG["n_pairs"]):
+            for side in (0, 1):
+                m = H.gen_synthetic(cls, 8, 2, seed=[7, ci, pi, side])
+                assert np.array_equal(m.mass, z[f"{cls}_{pi}_{side}"]), (cls, pi, side)
+        assert np.array_equal(H.gen_synthetic(cls, 6, 3, seed=[11, 2]).mass, z[f"{cls}_3d"])
+
+
+def test_config_validation_and_schema():
+    H.BenchConfig(**CFG).validate()
+    for bad in (dict(n=3), dict(d=0), dict(n=300), dict(p_values=(0.5,)), dict(kappas=(0,)),
+                dict(xi=0.0), dict(n_pairs=0), dict(methods=()), dict(methods=("reg_lower",)),
+                dict(methods=("nope",)), dict(max_iter=0), dict(precision="bf16"),
+                dict(classes=("blobs",))):
+        with pytest.raises(H.CliValidationError):
+            H.BenchConfig(**{**CFG, **bad}).validate()
+    with pytest.raises(H.CliValidationError):
+        H.gen_synthetic("gaussians", 3, 2, 0)
+    row = H.ReportRow("x-000", "min_cost", 2.0, "4", bound=1.0 / 3.0, exact=None)
+    assert row.as_record() == ["x-000", "min_cost", "2", "4", "0.33333333333333331", "", "",
+                               "", "", ""]
+    text = H.rows_to_csv([row])
+    assert text.splitlines()[0] == ",".join(H.CSV_COLUMNS)
+    assert H._relative_error("min_cost", 1.0, 2.0) == 0.5
+    assert H._relative_error("weighted_cost", 3.0, 2.0) == 0.5
+    assert H.main(["bench", "--methods", "reg_upper"]) == 1
+
+
+def test_exact_baseline_matches_reference():
+    gold = {(r["pair"], float(r["p"])): float(r["exact"]) for r in _golden_rows()
+            if r["method"] == "exact"}
+    for ci, cls in enumerate(CFG["classes"]):
+        mus = [H.gen_synthetic(cls, 8, 2, seed=[7, ci, i, 0]).mass for i in range(2)]
+        nus = [H.gen_synthetic(cls, 8, 2, seed=[7, ci, i, 1]).mass for i in range(2)]
+        for p in CFG["p_values"]:
+            out = H.exact_distances(mus, nus, 8, 2, p, threads=1)
+            for i, (value, wall, err) in enumerate(out):
+                assert err == ""
+                ref = gold[(f"{cls}-{i:03d}", p)]
+                assert abs(value - ref) <= 1e-15 * ref, (cls, i, p, value, ref)
+
+
+@pytest.mark.gpu
+def test_device_bench_matrix_matches_reference_csv():
+    rows = H.bench_run(H.BenchConfig(**CFG))
+    gold = _golden_rows()
+    assert len(rows) == len(gold)
+    got = list(csv.DictReader(io.StringIO(H.rows_to_csv(rows))))
+    for g, r in zip(gold, got):
+        assert (g["pair"], g["method"], g["p"], g["param"]) == \
+            (r["pair"], r["method"], r["p"], r["param"])
+        assert bool(g["error"]) == bool(r["error"]), (g, r)
+        if g["error"]:
+            assert g["error"].split(":")[0] == r["error"].split(":")[0]
+            continue
+        for key in ("bound", "exact", "rel_error"):
+            a, b = float(g[key]), float(r[key])
+            assert abs(a - b) <= 1e-9 * max(1.0, abs(a)), (g["pair"], g["method"], key, a, b)
