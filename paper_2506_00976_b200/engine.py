@@ -118,8 +118,20 @@ def _cbar(bt: _Batch):
                                mode, bt.ctil_dev, bt.table_dev)
 
 
-def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
-    """SumPool + C-bar on the device, then every coarse LP the methods need."""
+@dataclass
+class _LPJob:
+    """The coarse LPs of one batch at one (kappa, p), before solving."""
+
+    plans: CoarsePlans
+    problems: list
+    slots: list
+    warm: list
+    need: tuple
+    cbar_host: object = None  # keeps the pinned C-bar alive until the solve
+
+
+def coarse_problems(bt: _Batch, methods, pin_slot: str = "cbar") -> _LPJob:
+    """SumPool + C-bar on the device and every coarse LP the methods need."""
     need_ctil = "primal_upscaling" in methods or "dual_upscaling" in methods
     need_cbar = "weighted_cost" in methods
     need_cmin = "min_cost" in methods
@@ -127,7 +139,7 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
     tc = time.perf_counter()
     if need_cbar:
         vals, _ = _cbar(bt)
-        cbar_host = to_host_pinned(vals, "cbar")
+        cbar_host = to_host_pinned(vals, pin_slot)
     mu_c = to_host(bt.mu_c)
     nu_c = to_host(bt.nu_c)
     plans = CoarsePlans(n=bt.n)
@@ -157,13 +169,17 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
                 prev = len(problems) - 1
             except GridotError as exc:
                 slots.append((b, kind, exc))
-    t_lp = time.perf_counter()
-    plans.build_seconds = t_lp - t0 - plans.table_seconds
-    solved = solve_transport_many(problems, threads=lp_threads, warm_from=warm, slack=False)
-    plans.solve_seconds = time.perf_counter() - t_lp
+    plans.build_seconds = time.perf_counter() - t0 - plans.table_seconds
+    return _LPJob(plans, problems, slots, warm, (need_ctil, need_cbar, need_cmin), cbar_host)
+
+
+def assemble_plans(bt: _Batch, job: _LPJob, solved) -> CoarsePlans:
+    """Per-pair plans / values from the solved LPs of one job."""
+    need_ctil, need_cbar, need_cmin = job.need
+    plans = job.plans
     res = {}
-    it = iter(zip(problems, solved))
-    for s in slots:
+    it = iter(zip(job.problems, solved))
+    for s in job.slots:
         if len(s) == 3:
             res[(s[0], s[1])] = (None, s[2])
         else:
@@ -188,7 +204,36 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
         if need_cmin:
             prob, out = res[(b, "cmin")]
             plans.cmin_value.append(out if isinstance(out, Exception) else out[2])
-    plans.lp_seconds = time.perf_counter() - t0
+    job.cbar_host = None
+    return plans
+
+
+def solve_jobs(jobs, lp_threads: int = 0):
+    """Solve the LPs of several jobs as ONE host batch (one thread pool, warm
+    chains kept inside each job); returns the plans of every job."""
+    problems, warm, spans = [], [], []
+    for job in jobs:
+        base = len(problems)
+        problems.extend(job.problems)
+        warm.extend(w if w < 0 else w + base for w in job.warm)
+        spans.append((base, len(problems)))
+    t = time.perf_counter()
+    solved = solve_transport_many(problems, threads=lp_threads, warm_from=warm, slack=False)
+    dt = time.perf_counter() - t
+    out = []
+    for job, (lo, hi) in zip(jobs, spans):
+        job.plans.solve_seconds = dt
+        out.append(solved[lo:hi])
+    return out
+
+
+def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
+    """SumPool + C-bar on the device, then every coarse LP the methods need."""
+    t0 = time.perf_counter()
+    job = coarse_problems(bt, methods)
+    solved = solve_jobs([job], lp_threads)[0]
+    plans = assemble_plans(bt, job, solved)
+    plans.lp_seconds = time.perf_counter() - t0 - plans.cbar_seconds
     return plans
 
 
@@ -372,20 +417,15 @@ def _primal_report(p, price, tmu, tnu, gap, iters, conv, n, wall):
                        wall, int(iters), n)
 
 
-def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max_iter=10_000,
-                     kernel=None, methods=QUANT_METHODS, dual_method="multilinear",
-                     lp_threads=0, return_exceptions=True, timings=None):
-    """All requested quantization bounds for a batch of pairs on one grid.
-
-    mus, nus: [B, prod(dims)] float64 (numpy, pinned or device tensors).
-    Returns a list (one per pair) of {method: BoundReport | exception}.
-    """
+def _check_args(precision, methods):
     if precision not in PRECISIONS:
         raise ValueError(f"precision must be one of {PRECISIONS}")
     for m in methods:
         if m not in QUANT_METHODS:
             raise ValueError(f"unknown method {m!r}")
-    t_start = time.perf_counter()
+
+
+def _device_masses(mus, nus, dims):
     device()
     mu = to_dev(mus)
     nu = to_dev(nus)
@@ -393,20 +433,19 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
         mu, nu = mu[None, :], nu[None, :]
     if mu.shape != nu.shape or mu.shape[1] != int(np.prod(dims)):
         raise DimensionMismatchError(f"masses {tuple(mu.shape)} do not match dims {dims}")
-    bt = _Batch(mu, nu, dims, kappa, p, precision)
-    paired = None
-    if kernel is not None:
-        if kernel.kappa != bt.kappa or kernel.ndim != bt.d:
-            raise DimensionMismatchError(
-                f"kernel is ({kernel.kappa}, {kernel.ndim}), expected ({bt.kappa}, {bt.d})")
-        paired = kernel.paired()
-    t0 = time.perf_counter()
-    plans = prepare_coarse(bt, methods, lp_threads)
-    t1 = time.perf_counter()
-    if timings is not None:
-        timings["lp"] = plans.lp_seconds
-        for key in ("cbar", "table", "build", "solve"):
-            timings["lp_" + key] = getattr(plans, key + "_seconds", 0.0)
+    return mu, nu
+
+
+def _kernel_pairs(bt: _Batch, kernel):
+    if kernel is None:
+        return None
+    if kernel.kappa != bt.kappa or kernel.ndim != bt.d:
+        raise DimensionMismatchError(
+            f"kernel is ({kernel.kappa}, {kernel.ndim}), expected ({bt.kappa}, {bt.d})")
+    return kernel.paired()
+
+
+def _run_device(bt: _Batch, plans: CoarsePlans, paired, xi, max_iter, methods, dual_method):
     dp = DevicePlans(bt, plans, paired, xi)
     t_dp = time.perf_counter()
     res = gpu_stages(bt, dp, methods, max_iter, dual_method)
@@ -415,10 +454,11 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
         out, status = res["primal"]
         prim = (to_host(out), to_host(status))
     dual = to_host(res["dual"]) if "dual" in res else None
-    t2 = time.perf_counter()
-    if timings is not None:
-        timings.update(prepare=t0 - t_start, coarse=t1 - t0, upload=t_dp - t1, gpu=t2 - t_dp)
-    wall = (t2 - t_start) / max(bt.B, 1)
+    return prim, dual, t_dp
+
+
+def _reports(bt: _Batch, plans: CoarsePlans, prim, dual, methods, xi, max_iter, wall,
+             return_exceptions, timings):
     reports = []
     for b in range(bt.B):
         rep = {}
@@ -469,9 +509,82 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
                 if isinstance(v, Exception):
                     raise v
         reports.append(rep)
+    return reports
+
+
+def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max_iter=10_000,
+                     kernel=None, methods=QUANT_METHODS, dual_method="multilinear",
+                     lp_threads=0, return_exceptions=True, timings=None):
+    """All requested quantization bounds for a batch of pairs on one grid.
+
+    mus, nus: [B, prod(dims)] float64 (numpy, pinned or device tensors).
+    Returns a list (one per pair) of {method: BoundReport | exception}.
+    """
+    _check_args(precision, methods)
+    t_start = time.perf_counter()
+    mu, nu = _device_masses(mus, nus, dims)
+    bt = _Batch(mu, nu, dims, kappa, p, precision)
+    paired = _kernel_pairs(bt, kernel)
+    t0 = time.perf_counter()
+    plans = prepare_coarse(bt, methods, lp_threads)
+    t1 = time.perf_counter()
+    if timings is not None:
+        timings["lp"] = plans.lp_seconds
+        for key in ("cbar", "table", "build", "solve"):
+            timings["lp_" + key] = getattr(plans, key + "_seconds", 0.0)
+    prim, dual, t_dp = _run_device(bt, plans, paired, xi, max_iter, methods, dual_method)
+    t2 = time.perf_counter()
+    if timings is not None:
+        timings.update(prepare=t0 - t_start, coarse=t1 - t0, upload=t_dp - t1, gpu=t2 - t_dp)
+    wall = (t2 - t_start) / max(bt.B, 1)
+    reports = _reports(bt, plans, prim, dual, methods, xi, max_iter, wall, return_exceptions,
+                       timings)
     if timings is not None:
         timings["finish"] = time.perf_counter() - t2
     return reports
+
+
+def quantized_bounds_many(mus, nus, dims, combos, *, precision="fp64", xi=None,
+                          max_iter=10_000, methods=QUANT_METHODS, dual_method="multilinear",
+                          lp_threads=0, return_exceptions=True, timings=None):
+    """:func:`quantized_bounds` for several (kappa, p) combinations of the same
+    batch at once: the masses are uploaded once, and the coarse LPs of ALL
+    combinations run as one host batch on one thread pool (the expensive
+    combinations' LPs first), which keeps every core busy where one batch per
+    combination leaves the tail of each wave idle.  Results and their values
+    are those of one ``quantized_bounds`` call per combination (the same LPs,
+    pivot paths and device kernels); ``BoundReport.wall_time`` is the whole
+    call's wall time per pair and combination.
+
+    Returns {(kappa, p): [per-pair {method: BoundReport | exception}]}.
+    """
+    _check_args(precision, methods)
+    t_start = time.perf_counter()
+    mu, nu = _device_masses(mus, nus, dims)
+    combos = [(int(k), float(p)) for k, p in combos]
+    batches = [_Batch(mu, nu, dims, k, p, precision) for k, p in combos]
+    # expensive (fine coarse grids, i.e. small kappa) LP batches first
+    order = sorted(range(len(combos)), key=lambda i: -batches[i].n)
+    t0 = time.perf_counter()
+    jobs = {i: coarse_problems(batches[i], methods, pin_slot=f"cbar{i}") for i in order}
+    t1 = time.perf_counter()
+    solved = solve_jobs([jobs[i] for i in order], lp_threads)
+    t2 = time.perf_counter()
+    plans = {i: assemble_plans(batches[i], jobs[i], sv) for i, sv in zip(order, solved)}
+    dev = {i: _run_device(batches[i], plans[i], None, xi, max_iter, methods, dual_method)
+           for i in range(len(combos))}
+    t3 = time.perf_counter()
+    nb = max(batches[0].B, 1) if batches else 1
+    wall = (t3 - t_start) / nb / max(len(combos), 1)
+    out = {}
+    for i, key in enumerate(combos):
+        prim, dual, _ = dev[i]
+        out[key] = _reports(batches[i], plans[i], prim, dual, methods, xi, max_iter, wall,
+                            return_exceptions, timings)
+    if timings is not None:
+        timings.update(prepare=t0 - t_start, lp_build=t1 - t0, lp_solve=t2 - t1,
+                       gpu=t3 - t2, finish=time.perf_counter() - t3)
+    return out
 
 
 def make_batch(mus, nus, dims, kappa, p, precision="fp64"):

@@ -72,3 +72,18 @@ def test_fp32_tracks_fp64_on_cfg3_batch():
         for i in range(8):
             for m in G.QUANT_METHODS:
                 assert rel_close(a[i][m].raw_value, b[i][m].raw_value, 1e-5), (k, p, m)
+
+
+def test_many_combos_equal_single_calls():
+    """quantized_bounds_many (one LP batch for all combinations) returns the
+    same values as one quantized_bounds call per combination."""
+    wl = S.WORKLOADS[3]
+    mus, nus = S.batch(3, 0, 6)
+    many = G.quantized_bounds_many(mus, nus, wl.dims, wl.combos, precision="fp32",
+                                   return_exceptions=False)
+    for k, p in wl.combos:
+        one = G.quantized_bounds(mus, nus, wl.dims, k, p, precision="fp32",
+                                 return_exceptions=False)
+        for b in range(6):
+            for m in G.QUANT_METHODS:
+                assert many[(k, p)][b][m].raw_value == one[b][m].raw_value, (k, p, b, m)
