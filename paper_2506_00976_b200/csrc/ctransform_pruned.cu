@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(64) pruned_ct_kernel(const T *__restrict__ v,
 // same table values, so no lowering is needed.
 constexpr int CT_TAB_W = 140;      // row stride (floats)
 constexpr int CT_TAB_ROWS = 128;   // |dy| <= 127
-constexpr int CT_TAB_REG = 6;      // regions per CTA (2 warps each)
+constexpr int CT_TAB_REG = 8;      // regions per CTA (2 warps each)
 
 __device__ __forceinline__ void pair_sync(int id) {
     asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
