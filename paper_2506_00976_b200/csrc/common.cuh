@@ -141,6 +141,59 @@ __device__ double block_sum(double v, double *sh) {
     return r;
 }
 
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    return (unsigned long long)__float_as_uint(a) | ((unsigned long long)__float_as_uint(b) << 32);
+}
+
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// One source row of a lane's 8 x 8 candidate block from the 16 table floats
+// L: the cost of offset index q is L[q] (off >= 0) or L[14 - q] (off < 0).
+// Each add.f32x2 pairs the candidates of ONE source s for two adjacent
+// outputs r8, r8 + 1: their costs cst[q] and cst[q - 1] (q = s - r8 + 7) are
+// an aligned register pair of L (straight or swapped) and the potential vs[s]
+// is the broadcast scalar operand -- no register shuffling.  Per source the
+// aligned output pairs are (0,1),(2,3),(4,5),(6,7) or (1,2),(3,4),(5,6) plus
+// two scalar adds, depending on the parity of s (and on the direction).
+template <bool REV, bool SUB>
+__device__ __forceinline__ void minplus_row8(const float (&L)[16], const float (&vs)[8],
+                                             float (&best)[8]) {
+    float cand[8][8];  // [r8][s], consumed by the min folds below
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        // pairs (r8, r8+1) whose cost pair is aligned: straight L pair
+        // (L[q-1], L[q]) needs q - 1 even; swapped pair (L[14-q], L[15-q])
+        // needs 14 - q even
+        const int first = REV ? ((s % 2 == 0) ? 1 : 0) : ((s % 2 == 0) ? 0 : 1);
+#pragma unroll
+        for (int r8 = first; r8 + 1 < 8; r8 += 2) {
+            const int q = s - r8 + 7;
+            unsigned long long c;
+            if (!REV) c = pk2(L[q], L[q - 1]);        // (cst[q], cst[q-1])
+            else c = pk2(L[14 - q], L[15 - q]);       // (cst[q], cst[q-1])
+            unsigned long long rr;
+            const unsigned long long vv = pk2(vs[s], vs[s]);
+            if (SUB) asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rr) : "l"(c), "l"(vv));
+            else asm("add.rn.f32x2 %0, %1, %2;" : "=l"(rr) : "l"(c), "l"(vv));
+            cand[r8][s] = __uint_as_float((unsigned)(rr & 0xffffffffu));
+            cand[r8 + 1][s] = __uint_as_float((unsigned)(rr >> 32));
+        }
+        if (first == 1) {  // r8 = 0 and r8 = 7 left over for this s
+            const float c0 = REV ? L[7 - s] : L[s + 7], c7 = REV ? L[14 - s] : L[s];
+            cand[0][s] = SUB ? c0 - vs[s] : c0 + vs[s];
+            cand[7][s] = SUB ? c7 - vs[s] : c7 + vs[s];
+        }
+    }
+#pragma unroll
+    for (int r8 = 0; r8 < 8; ++r8)
+#pragma unroll
+        for (int s = 0; s < 8; s += 2) best[r8] = fmin3(best[r8], cand[r8][s], cand[r8][s + 1]);
+}
+
 }  // namespace gdt
 
 #define GDT_CHECK_ARG(cond, msg)              \

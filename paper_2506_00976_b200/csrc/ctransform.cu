@@ -90,22 +90,25 @@ __global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ i
 #pragma unroll
     for (int r = 0; r < 8; ++r) best[r] = (TO)INFINITY;
     for (int i0 = 0; i0 < L; i0 += 8) {
-        TO vs[8], cst[16];
-        const TO *cp = sq + (i0 - j0 + L);  // squares of d = i0 - j0 - 7 + q
-#pragma unroll
-        for (int q = 0; q < 8; ++q) vs[q] = line[i0 + q];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) cst[q] = cp[q];
+        const TO *cp = sq + (i0 - j0 + L);  // squares of d = i0 - j0 - 7 + q, 16-byte aligned
         if constexpr (sizeof(TO) == 4) {
+            float vs[8], Lq[16];
+            const float4 a0 = reinterpret_cast<const float4 *>(line + i0)[0];
+            const float4 a1 = reinterpret_cast<const float4 *>(line + i0)[1];
+            vs[0] = a0.x; vs[1] = a0.y; vs[2] = a0.z; vs[3] = a0.w;
+            vs[4] = a1.x; vs[5] = a1.y; vs[6] = a1.z; vs[7] = a1.w;
 #pragma unroll
-            for (int r8 = 0; r8 < 8; ++r8)
-#pragma unroll
-                for (int s2 = 0; s2 < 8; s2 += 2) {
-                    float c0, c1;
-                    add_f32x2(cst[s2 - r8 + 7], cst[s2 + 1 - r8 + 7], vs[s2], vs[s2 + 1], c0, c1);
-                    best[r8] = fmin3f(best[r8], c0, c1);
-                }
+            for (int c4 = 0; c4 < 4; ++c4) {
+                const float4 t = reinterpret_cast<const float4 *>(cp)[c4];
+                Lq[4 * c4] = t.x; Lq[4 * c4 + 1] = t.y; Lq[4 * c4 + 2] = t.z; Lq[4 * c4 + 3] = t.w;
+            }
+            minplus_row8<false, false>(Lq, vs, best);
         } else {
+            TO vs[8], cst[16];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) vs[q] = line[i0 + q];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) cst[q] = cp[q];
 #pragma unroll
             for (int r8 = 0; r8 < 8; ++r8)
 #pragma unroll

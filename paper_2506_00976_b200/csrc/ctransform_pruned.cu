@@ -26,22 +26,12 @@
 
 namespace gdt {
 
-__device__ __forceinline__ unsigned long long pk2(float a, float b) {
-    return (unsigned long long)__float_as_uint(a) | ((unsigned long long)__float_as_uint(b) << 32);
-}
-
 __device__ __forceinline__ void sub_f32x2(float c0, float c1, float v0, float v1, float &r0,
                                           float &r1) {
     unsigned long long rr;
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rr) : "l"(pk2(c0, c1)), "l"(pk2(v0, v1)));
     r0 = __uint_as_float((unsigned)(rr & 0xffffffffu));
     r1 = __uint_as_float((unsigned)(rr >> 32));
-}
-
-__device__ __forceinline__ float fmin3(float a, float b, float c) {
-    float r;
-    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-    return r;
 }
 
 __device__ __forceinline__ float sqrt_approx(float x) {
@@ -275,46 +265,6 @@ __device__ __forceinline__ void pair_sync(int id) {
     asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
 
-// One source row of a lane's 8 x 8 candidate block from the 16 table floats
-// L: the cost of offset index q is L[q] (off >= 0) or L[14 - q] (off < 0).
-// Each add.f32x2 pairs the candidates of ONE source s for two adjacent
-// outputs r8, r8 + 1: their costs cst[q] and cst[q - 1] (q = s - r8 + 7) are
-// an aligned register pair of L (straight or swapped) and the potential vs[s]
-// is the broadcast scalar operand -- no register shuffling.  Per source the
-// aligned output pairs are (0,1),(2,3),(4,5),(6,7) or (1,2),(3,4),(5,6) plus
-// two scalar adds, depending on the parity of s (and on the direction).
-template <bool REV>
-__device__ __forceinline__ void ct_row(const float (&L)[16], const float (&vs)[8],
-                                       float (&best)[8]) {
-    float cand[8][8];  // [r8][s], consumed by the min folds below
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-        // pairs (r8, r8+1) whose cost pair is aligned: straight L pair
-        // (L[q-1], L[q]) needs q - 1 even; swapped pair (L[14-q], L[15-q])
-        // needs 14 - q even
-        const int first = REV ? ((s % 2 == 0) ? 1 : 0) : ((s % 2 == 0) ? 0 : 1);
-#pragma unroll
-        for (int r8 = first; r8 + 1 < 8; r8 += 2) {
-            const int q = s - r8 + 7;
-            unsigned long long c;
-            if (!REV) c = pk2(L[q], L[q - 1]);        // (cst[q], cst[q-1])
-            else c = pk2(L[14 - q], L[15 - q]);       // (cst[q], cst[q-1])
-            unsigned long long rr;
-            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rr) : "l"(c), "l"(pk2(vs[s], vs[s])));
-            cand[r8][s] = __uint_as_float((unsigned)(rr & 0xffffffffu));
-            cand[r8 + 1][s] = __uint_as_float((unsigned)(rr >> 32));
-        }
-        if (first == 1) {  // r8 = 0 and r8 = 7 left over for this s
-            cand[0][s] = (REV ? L[7 - s] : L[s + 7]) - vs[s];
-            cand[7][s] = (REV ? L[14 - s] : L[s]) - vs[s];
-        }
-    }
-#pragma unroll
-    for (int r8 = 0; r8 < 8; ++r8)
-#pragma unroll
-        for (int s = 0; s < 8; s += 2) best[r8] = fmin3(best[r8], cand[r8][s], cand[r8][s + 1]);
-}
-
 constexpr int CT_TAB_TILES = 256;  // (128 / 8)^2 source tiles at most
 
 __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
@@ -450,8 +400,8 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
                 const float4 v0 = __ldg(reinterpret_cast<const float4 *>(vrow + y * N0));
                 const float4 v1 = __ldg(reinterpret_cast<const float4 *>(vrow + y * N0) + 1);
                 const float vs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                if (off >= 0) ct_row<false>(L, vs, best);
-                else ct_row<true>(L, vs, best);
+                if (off >= 0) minplus_row8<false, true>(L, vs, best);
+                else minplus_row8<true, true>(L, vs, best);
             }
             float m = best[0];
 #pragma unroll
