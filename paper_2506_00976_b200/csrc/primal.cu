@@ -760,6 +760,9 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
     G32 c, int kappa, double *__restrict__ out, int32_t *__restrict__ status,
     double *__restrict__ scratch, int64_t stride_pair, int cap) {
     constexpr int KV = KAPPA >= 2 ? KAPPA : 16;  // register row buffer (runtime kappa <= 16)
+    // request a unit's masses before its coarse sum (kappa <= 4: the row
+    // buffer fits the register budget next to the rest)
+    constexpr bool EARLY = KAPPA >= 2 && KAPPA <= 4;
     __shared__ FastPart sh[FT / 32 + 1];
     __shared__ FastPart slot[3];  // this CTA's partials: init, row pass, column pass
     extern __shared__ __align__(16) unsigned char fsm[];
@@ -948,6 +951,10 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
             const int ui = t * FT + (int)threadIdx.x, u = u_lo + ui;
             const bool act = u < units && ui < upc;
             const int k = act ? u / G : k_lo, r = act ? u - k * G : 0;
+            // the unit's masses are requested first: their latency overlaps
+            // the coarse sum and the reciprocals
+            double mv0[KV];
+            if (EARLY && act) fp_load<KAPPA>(mub + row_s[ui], mv0, kp);
             const double kb = coarse(k, r, act, rp_s, r_lo, rcol, rmass);
             const double rcp = fp_rcp(kb);
             double *bk = blk_s + 5 * (k - k_lo);
@@ -957,7 +964,12 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
                 if (r == 0) fp_block_range(bk[0], bk[1], kb, rcp, q);
                 for (int qq = 0; qq < rows_per_unit; ++qq) {
                     double mv[KV];
-                    fp_load<KAPPA>(mub + row_index(ui, qq), mv, kp);
+                    if constexpr (EARLY) {
+#pragma unroll
+                        for (int x = 0; x < KV; ++x) mv[x] = mv0[x];
+                    } else {
+                        fp_load<KAPPA>(mub + row_index(ui, qq), mv, kp);
+                    }
 #pragma unroll
                     for (int x = 0; x < KV; ++x) {
                         if (x >= kp) break;
@@ -1008,6 +1020,8 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
             const int ui = t * FT + (int)threadIdx.x, u = u_lo + ui;
             const bool act = u < units && ui < upc;
             const int l = act ? u / G : k_lo, r = act ? u - l * G : 0;
+            double nv0[KV];
+            if (EARLY && act) fp_load<KAPPA>(nub + row_s[ui], nv0, kp);
             const double kt = coarse(l, r, act, cp_s, c_lo, crow, cmass);
             const double rcp = fp_rcp(kt);
             double sb = 0.0;
@@ -1018,7 +1032,12 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
                 }
                 for (int qq = 0; qq < rows_per_unit; ++qq) {
                     double nv[KV];
-                    fp_load<KAPPA>(nub + row_index(ui, qq), nv, kp);
+                    if constexpr (EARLY) {
+#pragma unroll
+                        for (int x = 0; x < KV; ++x) nv[x] = nv0[x];
+                    } else {
+                        fp_load<KAPPA>(nub + row_index(ui, qq), nv, kp);
+                    }
 #pragma unroll
                     for (int x = 0; x < KV; ++x) {
                         if (x >= kp) break;
