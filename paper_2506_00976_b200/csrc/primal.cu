@@ -666,6 +666,22 @@ __device__ __forceinline__ double fp_scale(double m, double den, double rcp) {
 
 __device__ __forceinline__ double fp_rcp(double den) { return den > 0.0 ? __drcp_rn(den) : 0.0; }
 
+#ifdef GDT_IPF_TRACE
+__device__ unsigned long long g_ipf_trace[128];
+#define FP_TRACE(slot_)                                                                    \
+    do {                                                                                   \
+        if (blockIdx.x < 8 && threadIdx.x == 0 && it == 10) {                              \
+            unsigned long long t_;                                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+            g_ipf_trace[blockIdx.x * 16 + (slot_)] = t_;                                   \
+        }                                                                                  \
+    } while (0)
+#else
+#define FP_TRACE(slot_) \
+    do {                \
+    } while (0)
+#endif
+
 // Work mapping: a unit is one fine row (KAPPA cells along axis 0) of one
 // coarse block; the G = kappa^(d-1) rows of a block sit in G consecutive
 // lanes, which fold the block sum with xor shuffles (fixed order:
@@ -945,8 +961,11 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
         // (blk[4]) for |a kb - mu|, the zero-row check, a of sweep it+1 and
         // its block sums.  a is not stored: the closing pass writes the final one.
         FastPart q = fp_init();
+        FP_TRACE(0);
         gather(ownB);
+        FP_TRACE(1);
         products(rc_s, ri_s, r_n);
+        FP_TRACE(2);
         for (int t = 0; t < trips; ++t) {
             const int ui = t * FT + (int)threadIdx.x, u = u_lo + ui;
             const bool act = u < units && ui < upc;
@@ -988,9 +1007,13 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
                 kb_s[k - k_lo] = kb;
             }
         }
+        FP_TRACE(3);
         fp_publish(q, &slot[1], sh);
+        FP_TRACE(4);
         cluster_sync_all();
+        FP_TRACE(5);
         const FastPart ac = fp_combine(&slot[1], cs, sh);
+        FP_TRACE(6);
         if (it >= 1) {  // end of sweep `it`: range checks, then the gap
             if (fp_bad(ra.lo, ra.hi) || fp_bad(rb.lo, rb.hi) || ((ra.flags | rb.flags) & 2)) {
                 st = GDT_PAIR_OVERFLOW;
@@ -1015,7 +1038,9 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
         // range(b), block sums of b (b is not stored either)
         FastPart qb = fp_init();
         gather(ownS);
+        FP_TRACE(7);
         products(cc_s, ci_s, c_n);
+        FP_TRACE(8);
         for (int t = 0; t < trips; ++t) {
             const int ui = t * FT + (int)threadIdx.x, u = u_lo + ui;
             const bool act = u < units && ui < upc;
@@ -1054,9 +1079,13 @@ __global__ void __launch_bounds__(FT, 3) ipf_fast_kernel(
                 kt_s[l - k_lo] = kt;
             }
         }
+        FP_TRACE(9);
         fp_publish(qb, &slot[2], sh);
+        FP_TRACE(10);
         cluster_sync_all();
+        FP_TRACE(11);
         rb = fp_combine(&slot[2], cs, sh);
+        FP_TRACE(12);
         if (rb.flags & 1) {
             st = GDT_PAIR_ZERO_DENOM_COL;
             break;
@@ -1677,3 +1706,12 @@ extern "C" int gdt_price_coo(const int64_t *row, const int64_t *col, const doubl
     return cuda_status("gdt_price_coo");
 }
 
+
+#ifdef GDT_IPF_TRACE
+extern "C" int gdt_debug_ipf_trace(unsigned long long *host) {
+    return cudaMemcpyFromSymbol(host, gdt::g_ipf_trace, sizeof(unsigned long long) * 128) ==
+                   cudaSuccess
+               ? 0
+               : -1;
+}
+#endif
