@@ -214,7 +214,14 @@ struct Slot {
 };
 
 struct Node {
-    int32_t par, pslot, dep, head;
+    int32_t pslot, head;
+};
+
+// per-node tree data the pivot loop touches together: parent-arc cost,
+// parent, position in the preorder array
+struct Hot {
+    double ck;
+    int32_t par, pos;
 };
 
 template <class Cost>
@@ -226,11 +233,12 @@ struct Solver {
     std::vector<Slot> sl;
     std::vector<Node> nd;
     std::vector<double> pot;  // u[0, ns) then v[0, nt)
+    std::vector<Hot> hv;
     std::vector<int32_t> stk, pa_s, pb_s;
     // preorder of the spanning tree as an array: the subtree of w is
-    // pre[pos[w] .. pos[w] + sz[w]); maintained across pivots so the subtree
+    // pre[hv[w].pos .. hv[w].pos + sz[w]); maintained across pivots so the subtree
     // relabel is a branch-free sweep over a contiguous range
-    std::vector<int32_t> pre, pos, sz, tmp, stem, stem_slot, stem_sz, stem_pos;
+    std::vector<int32_t> pre, sz, tmp, stem, stem_slot, stem_sz, stem_pos;
     std::vector<int8_t> sa_s, sb_s;
     int simd;  // 2 = avx512, 1 = avx2, 0 = scalar
 
@@ -270,11 +278,11 @@ struct Solver {
                 for (int32_t k = me.head; k != -1;) {
                     const Slot &e = sl[k];
                     const int32_t w = (int32_t)ns + e.j;
-                    if (subtree ? k != me.pslot : nd[w].par == -2) {
+                    if (subtree ? k != me.pslot : hv[w].par == -2) {
                         P[w] = e.ck - pn;
-                        nd[w].par = node;
+                        hv[w].ck = e.ck;
+                        hv[w].par = node;
                         nd[w].pslot = k;
-                        nd[w].dep = me.dep + 1;
                         stk[sp++] = w;
                     }
                     k = e.rn;
@@ -283,11 +291,11 @@ struct Solver {
                 for (int32_t k = me.head; k != -1;) {
                     const Slot &e = sl[k];
                     const int32_t w = e.i;
-                    if (subtree ? k != me.pslot : nd[w].par == -2) {
+                    if (subtree ? k != me.pslot : hv[w].par == -2) {
                         P[w] = e.ck - pn;
-                        nd[w].par = node;
+                        hv[w].ck = e.ck;
+                        hv[w].par = node;
                         nd[w].pslot = k;
-                        nd[w].dep = me.dep + 1;
                         stk[sp++] = w;
                     }
                     k = e.cn;
@@ -387,18 +395,19 @@ struct Solver {
     void rehang(int32_t q_root, int32_t p_root, int32_t u_out, int32_t in_slot, int32_t join) {
         // stem s_0 = q_root, ..., s_k = u_out with their old links / sizes / positions
         int k = 0;
-        for (int32_t w = q_root;; w = nd[w].par) {
+        for (int32_t w = q_root;; w = hv[w].par) {
             stem[k] = w;
             stem_slot[k] = nd[w].pslot;
             stem_sz[k] = sz[w];
-            stem_pos[k] = pos[w];
+            stem_pos[k] = hv[w].pos;
             ++k;
             if (w == u_out) break;
         }
-        const int32_t S = sz[u_out], a = pos[u_out];
+        const int32_t S = sz[u_out], a = hv[u_out].pos;
+        const int32_t pv = hv[p_root].pos, pend = pv + sz[p_root];  // p_root's old subtree [pv, pend)
         // sizes between the two cycle sides and the join
-        for (int32_t w = nd[u_out].par; w != join; w = nd[w].par) sz[w] -= S;
-        for (int32_t w = p_root; w != join; w = nd[w].par) sz[w] += S;
+        for (int32_t w = hv[u_out].par; w != join; w = hv[w].par) sz[w] -= S;
+        for (int32_t w = p_root; w != join; w = hv[w].par) sz[w] += S;
         // T's new preorder: subtree(s_0), then for each s_i its old subtree
         // minus subtree(s_{i-1}) (s_i first), which is two contiguous pieces
         int32_t *t = tmp.data();
@@ -409,38 +418,45 @@ struct Solver {
             for (int32_t x = stem_pos[i - 1] + stem_sz[i - 1]; x < stem_pos[i] + stem_sz[i]; ++x)
                 t[m++] = pre[x];
         }
-        // move T right after p_root in the array (p_root is outside T)
-        const int32_t pv = pos[p_root];
-        int32_t start, lo, hi;
-        if (pv < a) {
-            std::memmove(&pre[pv + 1 + S], &pre[pv + 1], sizeof(int32_t) * (a - pv - 1));
-            start = pv + 1;
-            lo = pv + 1;
-            hi = a + S;
-        } else {
-            std::memmove(&pre[a], &pre[a + S], sizeof(int32_t) * (pv + 1 - a - S));
-            start = pv + 1 - S;
-            lo = a;
-            hi = pv + 1;
+        // T becomes a child subtree of p_root: its block goes right after p_root
+        // or right after p_root's subtree, whichever moves fewer entries (the
+        // order of siblings in the preorder is free)
+        int32_t x;  // insertion point in old coordinates, outside (a, a + S)
+        if (a < pv) x = pv + 1;
+        else if (a >= pend) x = pend;
+        else x = (a - pv - 1) <= (pend - a - S) ? pv + 1 : pend;
+        int32_t start;
+        if (x >= a + S) {  // [a + S, x) moves left by S
+            std::memmove(&pre[a], &pre[a + S], sizeof(int32_t) * (x - a - S));
+            for (int32_t i = a; i < x - S; ++i) hv[pre[i]].pos = i;
+            start = x - S;
+        } else {  // [x, a) moves right by S
+            std::memmove(&pre[x + S], &pre[x], sizeof(int32_t) * (a - x));
+            for (int32_t i = x + S; i < a + S; ++i) hv[pre[i]].pos = i;
+            start = x;
         }
-        std::memcpy(&pre[start], t, sizeof(int32_t) * S);
-        for (int32_t i = lo; i < hi; ++i) pos[pre[i]] = i;
         // reverse the stem
         for (int i = k - 1; i >= 1; --i) {
-            nd[stem[i]].par = stem[i - 1];
+            hv[stem[i]].par = stem[i - 1];
             nd[stem[i]].pslot = stem_slot[i - 1];
+            hv[stem[i]].ck = sl[stem_slot[i - 1]].ck;
             sz[stem[i]] = S - stem_sz[i - 1];
         }
-        nd[q_root].par = p_root;
+        hv[q_root].par = p_root;
         nd[q_root].pslot = in_slot;
+        hv[q_root].ck = sl[in_slot].ck;
         sz[q_root] = S;
-        // relabel T in preorder
+        // place and relabel T in preorder: every potential recomputed from its
+        // (new) parent along its tree arc
         double *P = pot.data();
-        for (int32_t i = start; i < start + S; ++i) {
-            const int32_t w = pre[i];
-            Node &e = nd[w];
-            P[w] = sl[e.pslot].ck - P[e.par];
-            e.dep = nd[e.par].dep + 1;
+        Hot *H = hv.data();
+        int32_t *pre_ = pre.data() + start;
+        for (int32_t i = 0; i < S; ++i) {
+            const int32_t w = t[i];
+            Hot &h = H[w];
+            pre_[i] = w;
+            h.pos = start + i;
+            P[w] = h.ck - P[h.par];
         }
     }
 
@@ -474,7 +490,8 @@ struct Solver {
             }
         }
         sl.resize(nb);
-        nd.assign(n_nodes, Node{-2, 0, 0, -1});
+        nd.assign(n_nodes, Node{0, -1});
+        hv.assign(n_nodes, Hot{0.0, -2, 0});
         pot.assign(n_nodes, 0.0);
         for (int64_t k = 0; k < nb; ++k) {
             sl[k].i = (int32_t)bi[k];
@@ -488,12 +505,10 @@ struct Solver {
         pb_s.resize(n_nodes);
         sa_s.resize(n_nodes);
         sb_s.resize(n_nodes);
-        nd[0].par = -1;
+        hv[0].par = -1;
         nd[0].pslot = -1;
-        nd[0].dep = 0;
         pot[0] = 0.0;
         pre.assign(n_nodes, 0);
-        pos.resize(n_nodes);
         sz.assign(n_nodes, 1);
         tmp.resize(n_nodes);
         stem.resize(n_nodes);
@@ -502,9 +517,9 @@ struct Solver {
         stem_pos.resize(n_nodes);
         label(0, false);
         for (int64_t w = 0; w < n_nodes; ++w)
-            if (nd[w].par == -2) return GDT_LP_DISCONNECTED;
-        for (int64_t i = 0; i < n_nodes; ++i) pos[pre[i]] = (int32_t)i;
-        for (int64_t i = n_nodes - 1; i > 0; --i) sz[nd[pre[i]].par] += sz[pre[i]];
+            if (hv[w].par == -2) return GDT_LP_DISCONNECTED;
+        for (int64_t i = 0; i < n_nodes; ++i) hv[pre[i]].pos = (int32_t)i;
+        for (int64_t i = n_nodes - 1; i > 0; --i) sz[hv[pre[i]].par] += sz[pre[i]];
 
         int64_t next_arc = 0, degen_run = 0, pivots = 0;
         int status = GDT_LP_OPTIMAL;
@@ -537,23 +552,19 @@ struct Solver {
             const int32_t ei = (int32_t)(enter / nt), ej = (int32_t)(enter - (int64_t)ei * nt);
             int64_t ca = 0, cb = 0;
             int32_t pa = (int32_t)ns + ej, pb = ei;
-            while (nd[pa].dep > nd[pb].dep) {
+            // a is an ancestor of b (or b itself) iff hv[b].pos - hv[a].pos in [0, sz[a])
+            auto anc = [&](int32_t x, int32_t y) {
+                return (uint32_t)(hv[y].pos - hv[x].pos) < (uint32_t)sz[x];
+            };
+            while (!anc(pa, pb)) {
                 pa_s[ca] = nd[pa].pslot;
                 sa_s[ca++] = pa >= ns ? -1 : 1;
-                pa = nd[pa].par;
+                pa = hv[pa].par;
             }
-            while (nd[pb].dep > nd[pa].dep) {
+            while (pb != pa) {
                 pb_s[cb] = nd[pb].pslot;
                 sb_s[cb++] = pb < ns ? -1 : 1;
-                pb = nd[pb].par;
-            }
-            while (pa != pb) {
-                pa_s[ca] = nd[pa].pslot;
-                sa_s[ca++] = pa >= ns ? -1 : 1;
-                pa = nd[pa].par;
-                pb_s[cb] = nd[pb].pslot;
-                sb_s[cb++] = pb < ns ? -1 : 1;
-                pb = nd[pb].par;
+                pb = hv[pb].par;
             }
             // leaving slot: min flow on decreasing arcs, lowest arc index on ties
             double theta = INFINITY;
