@@ -675,7 +675,8 @@ extern "C" int gdt_transport_simplex(const double *C, const double *sup, const d
 // grid_dims[q*GDT_MAX_DIM ..] (grid_ndim[q] axes, ns = nt = cells) read from
 // table[q] over offset vectors (extent 2*cd_a - 1 per axis, axis 0 fastest).
 // warm_from[q] = -1 starts from the northwest corner (the reference's pivot
-// sequence), otherwise from the final basis of job warm_from[q] (< q, same
+// sequence), warm_from[q] = q from the basis the caller left in job q's own
+// (bi, bj, bf), otherwise from the final basis of job warm_from[q] (< q, same
 // shape): chained jobs run in order on one worker.
 extern "C" int gdt_transport_simplex_many(int64_t count, const uint64_t *C, const uint64_t *table,
                                           const int32_t *grid_ndim, const int64_t *grid_dims,
@@ -691,7 +692,7 @@ extern "C" int gdt_transport_simplex_many(int64_t count, const uint64_t *C, cons
     std::vector<int64_t> roots;
     for (int64_t q = 0; q < count; ++q) {
         const int64_t w = warm_from ? warm_from[q] : -1;
-        if (w < 0) {
+        if (w < 0 || w == q) {
             roots.push_back(q);
         } else {
             if (w >= q || ns[w] != ns[q] || nt[w] != nt[q]) return GDT_ERR_ARG;
@@ -730,7 +731,9 @@ extern "C" int gdt_transport_simplex_many(int64_t count, const uint64_t *C, cons
     std::function<void(int64_t)> run = [&](int64_t q) {
         const int64_t w = warm_from ? warm_from[q] : -1;
         const int64_t nbq = ns[q] + nt[q] - 1;
-        if (w >= 0) {
+        if (w == q) {
+            status[q] = solve_job(q, true);
+        } else if (w >= 0) {
             if (status[w] != GDT_LP_OPTIMAL) {
                 status[q] = status[w] < 0 ? status[w] : GDT_ERR_ARG;
                 pivots[q] = 0;

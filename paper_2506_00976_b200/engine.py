@@ -20,6 +20,7 @@ the benchmark can time the device stages with coarse plans precomputed
 
 from __future__ import annotations
 
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -235,6 +236,136 @@ def prepare_coarse(bt: _Batch, methods, lp_threads: int = 0) -> CoarsePlans:
     plans = assemble_plans(bt, job, solved)
     plans.lp_seconds = time.perf_counter() - t0 - plans.cbar_seconds
     return plans
+
+
+class _Worker(threading.Thread):
+    """Runs one native LP batch off the main thread (the ctypes call releases
+    the GIL), so the device work of the orchestrator overlaps it."""
+
+    def __init__(self, fn, *args, **kw):
+        super().__init__(daemon=True)
+        self.fn, self.args, self.kw = fn, args, kw
+        self.result, self.error = None, None
+
+    def run(self):
+        try:
+            self.result = self.fn(*self.args, **self.kw)
+        except BaseException as exc:  # re-raised on the main thread
+            self.error = exc
+
+    def get(self):
+        self.join()
+        if self.error is not None:
+            raise self.error
+        return self.result
+
+
+def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
+    """Coarse LPs of several batches overlapped with their device work.
+
+    Phase A: the C-tilde LPs of every batch (the reference's pivot path; they
+    need only the coarse masses) run on the host pool while the device
+    computes C-bar and copies it to pinned host memory.  Phase B: the C-bar /
+    C-min LPs, warm-started from each pair's C-tilde basis, run on the pool
+    while ``device_fn(i, plans_i)`` runs the stages that need only the C-tilde
+    plans (upscaling, IPF, c-transforms).  Values, supports and duals are those
+    of the serial order (same LPs, same starts).  Returns (plans, device
+    results) per batch.
+    """
+    need_ctil = "primal_upscaling" in methods or "dual_upscaling" in methods
+    need_cbar = "weighted_cost" in methods
+    need_cmin = "min_cost" in methods
+    order = sorted(range(len(batches)), key=lambda i: -batches[i].n)  # big LPs first
+    t0 = time.perf_counter()
+    masses = {i: (to_host(batches[i].mu_c), to_host(batches[i].nu_c)) for i in order}
+    plans = {i: CoarsePlans(n=batches[i].n) for i in order}
+
+    def build(i, b, cost):
+        try:
+            return build_transport_problem(masses[i][0][b], masses[i][1][b], cost)
+        except GridotError as exc:
+            return exc
+
+    # phase A
+    ctil_slots, ctil_probs = [], []
+    if need_ctil:
+        for i in order:
+            tab = centre_cost_table(batches[i].pdims, batches[i].kappa, batches[i].p)
+            for b in range(batches[i].B):
+                ctil_slots.append((i, b, build(i, b, tab)))
+        ctil_probs = [pr for _, _, pr in ctil_slots if not isinstance(pr, Exception)]
+    worker = _Worker(solve_transport_many, ctil_probs, threads=lp_threads, slack=False,
+                     return_basis=True)
+    worker.start()
+    t1 = time.perf_counter()
+    pinned, vb_slots, vb_probs = {}, [], []
+    for i in order:
+        bt = batches[i]
+        if need_cbar:
+            vals, _ = _cbar(bt)
+            pinned[i] = to_host_pinned(vals, f"cbar{i}")
+        cmin = min_cost_table(bt.pdims, bt.kappa, bt.p) if need_cmin else None
+        for b in range(bt.B):
+            if need_cbar:
+                vb_slots.append((i, b, "cbar", build(i, b, pinned[i][b])))
+            if need_cmin:
+                vb_slots.append((i, b, "cmin", build(i, b, cmin)))
+    t2 = time.perf_counter()
+    solved, bases = worker.get()
+    t3 = time.perf_counter()
+    basis_of = {}
+    it = iter(zip(solved, bases))
+    for i, b, pr in ctil_slots:
+        pl = plans[i]
+        out, basis = (pr, None) if isinstance(pr, Exception) else next(it)
+        if isinstance(out, Exception):
+            pl.ctil_arcs.append(None)
+            pl.ctil_duals.append(None)
+            pl.ctil_error.append(out)
+        else:
+            coupling, duals, _ = out
+            pl.ctil_arcs.append((pr.src_index[coupling.row], pr.dst_index[coupling.col],
+                                 coupling.mass))
+            pl.ctil_duals.append((duals.g, pr.dst_index))
+            pl.ctil_error.append(None)
+            basis_of[(i, b)] = basis
+    # phase B: each pair's chain C-tilde -> C-bar -> C-min (same marginals)
+    probs, warm_from, warm_basis, live = [], [], [], []
+    prev = {}
+    for i, b, kind, pr in vb_slots:
+        if isinstance(pr, Exception):
+            continue
+        q = len(probs)
+        probs.append(pr)
+        live.append((i, b, kind))
+        if (i, b) in prev:
+            warm_from.append(prev[(i, b)])
+            warm_basis.append(None)
+        else:
+            warm_from.append(-1)
+            warm_basis.append(basis_of.get((i, b)))
+        prev[(i, b)] = q
+    worker = _Worker(solve_transport_many, probs, threads=lp_threads, slack=False,
+                     warm_from=warm_from, warm_basis=warm_basis)
+    worker.start()
+    t4 = time.perf_counter()
+    dev = {i: device_fn(i, plans[i]) for i in order}
+    t5 = time.perf_counter()
+    values = {key: out for key, out in zip(live, worker.get())}
+    t6 = time.perf_counter()
+    for i, b, kind, pr in vb_slots:
+        v = pr if isinstance(pr, Exception) else values[(i, b, kind)]
+        v = v if isinstance(v, Exception) else v[2]
+        (plans[i].cbar_value if kind == "cbar" else plans[i].cmin_value).append(v)
+    pinned.clear()
+    for i in order:
+        plans[i].lp_seconds = (t3 - t0) + (t6 - t4)
+        plans[i].solve_seconds = (t3 - t1) + (t6 - t4)
+        plans[i].cbar_seconds = t2 - t1
+    if timings is not None:
+        timings.update(lp_ctil_build=t1 - t0, cbar_and_build=t2 - t1, lp_ctil_wait=t3 - t2,
+                       device=t5 - t4, lp_cbar_wait=t6 - t5)
+    return plans, dev
 
 
 # ---------------------------------------------------------------------------
@@ -526,16 +657,14 @@ def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max
     bt = _Batch(mu, nu, dims, kappa, p, precision)
     paired = _kernel_pairs(bt, kernel)
     t0 = time.perf_counter()
-    plans = prepare_coarse(bt, methods, lp_threads)
-    t1 = time.perf_counter()
-    if timings is not None:
-        timings["lp"] = plans.lp_seconds
-        for key in ("cbar", "table", "build", "solve"):
-            timings["lp_" + key] = getattr(plans, key + "_seconds", 0.0)
-    prim, dual, t_dp = _run_device(bt, plans, paired, xi, max_iter, methods, dual_method)
+    plans, dev = _pipeline([bt], methods, lp_threads,
+                           lambda i, pl: _run_device(bt, pl, paired, xi, max_iter, methods,
+                                                     dual_method), timings)
+    plans = plans[0]
+    prim, dual, _ = dev[0]
     t2 = time.perf_counter()
     if timings is not None:
-        timings.update(prepare=t0 - t_start, coarse=t1 - t0, upload=t_dp - t1, gpu=t2 - t_dp)
+        timings.update(prepare=t0 - t_start, coarse_and_gpu=t2 - t0)
     wall = (t2 - t_start) / max(bt.B, 1)
     reports = _reports(bt, plans, prim, dual, methods, xi, max_iter, wall, return_exceptions,
                        timings)
@@ -563,16 +692,10 @@ def quantized_bounds_many(mus, nus, dims, combos, *, precision="fp64", xi=None,
     mu, nu = _device_masses(mus, nus, dims)
     combos = [(int(k), float(p)) for k, p in combos]
     batches = [_Batch(mu, nu, dims, k, p, precision) for k, p in combos]
-    # expensive (fine coarse grids, i.e. small kappa) LP batches first
-    order = sorted(range(len(combos)), key=lambda i: -batches[i].n)
     t0 = time.perf_counter()
-    jobs = {i: coarse_problems(batches[i], methods, pin_slot=f"cbar{i}") for i in order}
-    t1 = time.perf_counter()
-    solved = solve_jobs([jobs[i] for i in order], lp_threads)
-    t2 = time.perf_counter()
-    plans = {i: assemble_plans(batches[i], jobs[i], sv) for i, sv in zip(order, solved)}
-    dev = {i: _run_device(batches[i], plans[i], None, xi, max_iter, methods, dual_method)
-           for i in range(len(combos))}
+    plans, dev = _pipeline(batches, methods, lp_threads,
+                           lambda i, pl: _run_device(batches[i], pl, None, xi, max_iter, methods,
+                                                     dual_method), timings)
     t3 = time.perf_counter()
     nb = max(batches[0].B, 1) if batches else 1
     wall = (t3 - t_start) / nb / max(len(combos), 1)
@@ -582,8 +705,8 @@ def quantized_bounds_many(mus, nus, dims, combos, *, precision="fp64", xi=None,
         out[key] = _reports(batches[i], plans[i], prim, dual, methods, xi, max_iter, wall,
                             return_exceptions, timings)
     if timings is not None:
-        timings.update(prepare=t0 - t_start, lp_build=t1 - t0, lp_solve=t2 - t1,
-                       gpu=t3 - t2, finish=time.perf_counter() - t3)
+        timings.update(prepare=t0 - t_start, coarse_and_gpu=t3 - t0,
+                       finish=time.perf_counter() - t3)
     return out
 
 

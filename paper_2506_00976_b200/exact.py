@@ -187,20 +187,24 @@ def solve_transport(problem: TransportProblem, tol: float = 1e-10,
 
 
 def solve_transport_many(problems, tol: float = 1e-10, threads: int = 0, warm_from=None,
-                         slack: bool = True):
+                         slack: bool = True, warm_basis=None, return_basis: bool = False):
     """Solve a batch of problems on `threads` host threads (0 = all cores).
 
     ``warm_from[q] = w`` (w < q, same supports and marginals) starts problem q
-    from the optimal basis of problem w instead of the northwest corner; the
-    optimal value is unchanged (the LP optimum is unique), only the pivot
-    path differs.  Problems without a warm start follow the reference's pivot
-    sequence exactly.  Returns a list of (coupling, duals, value) or the
-    exception each raised; ``slack=False`` skips the O(ns*nt) feasibility
-    diagnostic of DualPotentials.
+    from the optimal basis of problem w instead of the northwest corner;
+    ``warm_basis[q] = (bi, bj, bf)`` (a feasible spanning-tree basis of q's
+    marginals, e.g. the final basis of an earlier solve on the same supports)
+    starts it from that basis.  The optimal value is unchanged (the LP optimum
+    is unique), only the pivot path differs.  Problems without a warm start
+    follow the reference's pivot sequence exactly.  Returns a list of
+    (coupling, duals, value) or the exception each raised -- and, with
+    ``return_basis``, also the list of final bases (bi, bj, bf) (None where the
+    solve failed); ``slack=False`` skips the O(ns*nt) feasibility diagnostic
+    of DualPotentials.
     """
     count = len(problems)
     if count == 0:
-        return []
+        return ([], []) if return_basis else []
     keep = []  # keep every buffer alive for the duration of the native call
 
     def addr(a):
@@ -226,7 +230,16 @@ def solve_transport_many(problems, tol: float = 1e-10, threads: int = 0, warm_fr
     sup = ptr([np.ascontiguousarray(p.supply) for p in problems])
     dem = ptr([np.ascontiguousarray(p.demand) for p in problems])
     bi, bj, bf, u, v = (ptr([o[i] for o in out]) for i in range(5))
-    wf = np.full(count, -1, np.int64) if warm_from is None else np.asarray(warm_from, np.int64)
+    wf = np.full(count, -1, np.int64) if warm_from is None else np.array(warm_from, np.int64)
+    if warm_basis is not None:
+        for q, wb in enumerate(warm_basis):
+            if wb is None:
+                continue
+            if wf[q] >= 0 or len(wb[0]) != len(out[q][0]):
+                raise ValueError("warm_basis: one start per problem, sized ns + nt - 1")
+            for dst, src in zip(out[q][:3], wb):
+                dst[:] = src
+            wf[q] = q
     status = np.empty(count, np.int32)
     pivots = np.empty(count, np.int64)
     N.check(N.lib().gdt_transport_simplex_many(
@@ -234,13 +247,15 @@ def solve_transport_many(problems, tol: float = 1e-10, threads: int = 0, warm_fr
         N.ptr(nt), N.ptr(wf), float(tol),
         N.ptr(bi), N.ptr(bj), N.ptr(bf), N.ptr(u), N.ptr(v), N.ptr(status), N.ptr(pivots),
         int(threads)), "gdt_transport_simplex_many")
-    res = []
+    res, bases = [], []
     for q, prob in enumerate(problems):
         st = int(status[q])
         try:
             if st < 0:
                 raise GridotError(f"simplex failed with native status {st}")
             res.append(_finish(prob, st, *out[q], int(pivots[q]), slack=slack))
+            bases.append(out[q][:3])
         except GridotError as exc:
             res.append(exc)
-    return res
+            bases.append(None)
+    return (res, bases) if return_basis else res
