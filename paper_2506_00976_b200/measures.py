@@ -1,8 +1,9 @@
 """Grid measures and their coarsening (reference: pkg/src/gridot/measures.py).
 
 Host side: the frozen data model (``GridSpec``, ``GridMeasure``,
-``CoarseningSpec``), index/coordinate helpers and the closed-form TV
-weights.  Device side (libgridot_b200.so): SumPool (``coarsen_measure``,
+``CoarseningSpec``), the GRID text format (``load_grid_measure`` /
+``dump_grid_measure``, measures.py:138-220), index/coordinate helpers and the
+closed-form TV weights.  Device side (libgridot_b200.so): SumPool (``coarsen_measure``,
 K1, bit-exact with the reference's ``np.add.at`` order), zero padding and
 the weighted-TV reduction.
 
@@ -18,12 +19,12 @@ import numpy as np
 
 from . import _native as N
 from .device import device, stream, to_dev, to_host, torch
-from .errors import (DimensionMismatchError, GridMismatchError, NegativeMassError,
-                     ZeroTotalMassError)
+from .errors import (DimensionMismatchError, GridFormatError, GridMismatchError,
+                     NegativeMassError, ZeroTotalMassError)
 
 __all__ = ["GridSpec", "GridMeasure", "CoarseningSpec", "normalize", "pad_measure",
            "coarsen_measure", "coarsen_grid", "block_index_map", "tv_weights", "weighted_tv",
-           "pad_batch", "sumpool_batch"]
+           "pad_batch", "sumpool_batch", "load_grid_measure", "dump_grid_measure"]
 
 
 @dataclass(frozen=True)
@@ -83,6 +84,87 @@ class GridMeasure:
     @property
     def support(self) -> np.ndarray:
         return np.flatnonzero(self.mass > 0.0)
+
+
+# ---------------------------------------------------------------------------
+# GRID text format (measures.py:138-220)
+# ---------------------------------------------------------------------------
+
+
+def _grid_text(source) -> str:
+    if isinstance(source, bytes):
+        return source.decode("ascii", errors="replace")
+    if isinstance(source, str):
+        return source
+    if hasattr(source, "read"):
+        raw = source.read()
+        return raw.decode("ascii", errors="replace") if isinstance(raw, bytes) else raw
+    raise TypeError(f"cannot read GRID data from {type(source).__name__}")
+
+
+def load_grid_measure(source) -> GridMeasure:
+    """Parse GRID text: '#' comment and blank lines, a header ``d N1 .. Nd``,
+    then exactly N1*..*Nd whitespace-separated masses in flat order (axis 1
+    fastest).  Accepts str, bytes or a file object (measures.py:138-204).
+
+    Failures raise GridFormatError with the 1-based line of the header (or
+    of the first body line for count errors) and the 0-based index of a bad
+    mass token, or NegativeMassError with the flat index of the first
+    negative entry -- the reference's checks, in its order.
+    """
+    lines = _grid_text(source).split("\n")
+    hno = next((no for no, ln in enumerate(lines, start=1)
+                if ln.strip() and not ln.strip().startswith("#")), None)
+    if hno is None:
+        raise GridFormatError("no header line found")
+    header = lines[hno - 1].strip()
+    head = header.split()
+    try:
+        d = int(head[0])
+    except ValueError:
+        raise GridFormatError(f"dimension count {head[0]!r} is not an integer", line=hno)
+    if d < 1:
+        raise GridFormatError(f"dimension count must be >= 1, got {d}", line=hno)
+    if len(head) != d + 1:
+        raise GridFormatError(f"header needs {d + 1} integers for d={d}, got {len(head)}",
+                              line=hno)
+    try:
+        dims = tuple(int(tok) for tok in head[1:])
+    except ValueError:
+        raise GridFormatError(f"bad axis length in header {header!r}", line=hno)
+    if min(dims) < 1:
+        raise GridFormatError(f"axis lengths must be positive, got {dims}", line=hno)
+    grid = GridSpec(dims)
+    tokens = "\n".join(lines[hno:]).split()
+    if len(tokens) != grid.cell_count:
+        raise GridFormatError(f"expected {grid.cell_count} mass entries, got {len(tokens)}",
+                              line=hno + 1)
+    try:  # Python's float() grammar, as the reference parses each token
+        mass = np.fromiter(map(float, tokens), dtype=np.float64, count=len(tokens))
+    except ValueError:
+        for i, tok in enumerate(tokens):
+            try:
+                float(tok)
+            except ValueError:
+                raise GridFormatError(f"bad mass entry {tok!r}", token=i) from None
+        raise
+    bad = np.flatnonzero(~np.isfinite(mass))
+    if bad.size:
+        raise GridFormatError(f"non-finite mass entry {tokens[bad[0]]!r}", token=int(bad[0]))
+    neg = np.flatnonzero(mass < 0.0)
+    if neg.size:
+        raise NegativeMassError(int(neg[0]), float(mass[neg[0]]))
+    return GridMeasure(grid, mass)
+
+
+def dump_grid_measure(measure: GridMeasure) -> str:
+    """GRID text with round-tripping float reprs, one axis-1 run per line
+    (measures.py:207-216)."""
+    dims = measure.grid.dims
+    n1 = dims[0]
+    m = measure.mass
+    rows = (" ".join(map(repr, m[i:i + n1].tolist())) for i in range(0, m.size, n1))
+    return f"{len(dims)} " + " ".join(map(str, dims)) + "\n" + "\n".join(rows) + "\n"
 
 
 @dataclass(frozen=True)
