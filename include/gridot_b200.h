@@ -256,6 +256,39 @@ int gdt_transport_simplex_many(int64_t count, const uint64_t *C, const uint64_t 
                                const uint64_t *u, const uint64_t *v, int32_t *status,
                                int64_t *pivots, int threads);
 
+/* ---- entropic bounds (sinkhorn.py:150-299) ------------------------------ */
+
+/* Device scratch for gdt_entropic_fit / gdt_entropic_plan: the dense
+ * support-restricted kernel [ns][nt] fp64 plus sweep vectors and partials. */
+int64_t gdt_entropic_scratch_bytes(int64_t ns, int64_t nt);
+
+/* Alternating scaling on the Gibbs kernel K = exp(-C / eps) of the cost
+ * C_ij = |xs_i - xt_j|^p (ipf_fit, sinkhorn.py:101-142), restarted in the log
+ * domain (sinkhorn.py:150-178) when a denominator vanishes or a scaling vector
+ * leaves [1e-100, 1e100] (_run_scaling, sinkhorn.py:181-195).  Replaces
+ * _run_scaling for reg_lower_bound / reg_upper_bound.
+ *   xs [ns, d], xt [nt, d]   support coordinates (row-major fp64, device)
+ *   mu [ns], nu [nt]         positive support masses
+ *   xi, max_iter             stop threshold on the L1 marginal gap, sweep cap
+ *   f [ns], g [nt]           out: eps*log(a), eps*log(b) (or the log-domain
+ *                            potentials)
+ *   info [4]                 out: {iterations, marginal_gap, converged,
+ *                            log_domain}
+ *   status [1]               out: GDT_PAIR_OK, or GDT_PAIR_OVERFLOW when the
+ *                            log-domain potentials are not finite
+ * Synchronises `stream` every few sweeps to test for convergence. */
+int gdt_entropic_fit(const double *xs, const double *xt, int64_t ns, int64_t nt, int d,
+                     double p, double eps, const double *mu, const double *nu, double xi,
+                     int64_t max_iter, double *f, double *g, double *info, int32_t *status,
+                     void *scratch, void *stream);
+
+/* Pricing of the fitted plan P_ij = exp((f_i + g_j - C_ij) / eps)
+ * (sinkhorn.py:268-276): mu_hat [ns] = row sums, nu_hat [nt] = column sums,
+ * transport [1] = sum_ij P_ij C_ij (before the 1/p root). */
+int gdt_entropic_plan(const double *xs, const double *xt, int64_t ns, int64_t nt, int d,
+                      double p, double eps, const double *f, const double *g, double *mu_hat,
+                      double *nu_hat, double *transport, void *scratch, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -606,3 +606,83 @@ def four_bounds(mu, nu, dims, kappa, p, xi=None, max_iter=10_000, share_lp=False
                                            max_iter=max_iter, coarse=coarse)
     out["dual_upscaling"] = dual_bound(mu, nu, dims, kappa, p, coarse=coarse)
     return out
+
+
+# ---------------------------------------------------------------------------
+# entropic bounds (sinkhorn.py:150-299): dense Gibbs kernel, log-domain restart
+# ---------------------------------------------------------------------------
+
+
+def _logsumexp(x, axis):
+    """The reference calls scipy.special.logsumexp (scipy 1.18.1 here, the
+    version the fixtures were made with); the oracle calls the same function
+    so the log-domain iterates match it bit for bit."""
+    from scipy.special import logsumexp
+
+    return logsumexp(x, axis=axis)
+
+
+def log_domain_scaling(cost, mu, nu, eps, xi, max_iter):
+    """sinkhorn.py:150-178: the scaling iteration on potentials."""
+    log_mu, log_nu = np.log(mu), np.log(nu)
+    g = np.zeros_like(nu)
+    lkb = _logsumexp((g[None, :] - cost) / eps, axis=1)
+    f = np.zeros_like(mu)
+    gap, conv, iters = np.inf, False, max_iter
+    for it in range(1, max_iter + 1):
+        f = eps * (log_mu - lkb)
+        lkta = _logsumexp((f[:, None] - cost) / eps, axis=0)
+        g = eps * (log_nu - lkta)
+        lkb = _logsumexp((g[None, :] - cost) / eps, axis=1)
+        mu_hat = np.exp(f / eps + lkb)
+        nu_hat = np.exp(g / eps + lkta)
+        gap = float(np.abs(mu_hat - mu).sum() + np.abs(nu - nu_hat).sum())
+        if gap < xi:
+            conv, iters = True, it
+            break
+    if not (np.all(np.isfinite(f)) and np.all(np.isfinite(g))):
+        raise Overflow("log-domain potentials are not finite")
+    return f, g, iters, gap, conv
+
+
+def run_scaling(cost, mu, nu, eps, xi, max_iter):
+    """sinkhorn.py:181-195: plain scaling on exp(-C/eps), log-domain restart on
+    a zero denominator or scale overflow.  Returns (f, g, iterations, gap,
+    converged, log_domain)."""
+    try:
+        K = np.exp(-cost / eps)
+        a, b, it, gap, conv, _, _ = ipf(K, mu, nu, xi, max_iter)
+        return eps * np.log(a), eps * np.log(b), it, gap, conv, False
+    except (ZeroDenominator, Overflow):
+        return (*log_domain_scaling(cost, mu, nu, eps, xi, max_iter), True)
+
+
+def reg_bounds(mu, nu, dims, p, eps, xi=None, max_iter=10_000):
+    """reg_lower_bound and reg_upper_bound (sinkhorn.py:226-299) of one grid
+    pair with the grid cost rho^p; returns {"lower": {...}, "upper": {...},
+    "log_domain": bool}."""
+    mu = np.asarray(mu, dtype=np.float64)
+    nu = np.asarray(nu, dtype=np.float64)
+    X = grid_coords(dims)
+    src, dst = np.flatnonzero(mu > 0.0), np.flatnonzero(nu > 0.0)
+    mu_s, nu_s = mu[src], nu[dst]
+    cost = costs(X[src], X[dst], p)
+    if xi is None:
+        xi = 1e-9 * (src.size + dst.size)
+    f, g, it, gap, conv, logd = run_scaling(cost, mu_s, nu_s, eps, xi, max_iter)
+    dv = float(f @ mu_s + g @ nu_s)
+    raw = signed_root(dv, p)
+    lower = {"value": max(0.0, raw), "raw_value": raw, "dual_value": dv, "marginal_gap": gap,
+             "converged": float(conv), "iterations": it}
+    plan = np.exp((f[:, None] + g[None, :] - cost) / eps)
+    transport = float(np.sum(plan * cost)) ** (1.0 / p)
+    n = cell_count(dims)
+    mu_hat, nu_hat = np.zeros(n), np.zeros(n)
+    mu_hat[src] = plan.sum(axis=1)
+    nu_hat[dst] = plan.sum(axis=0)
+    w = tv_weights(dims, p)
+    dmu, dnu = weighted_tv(mu_hat, mu, w, p), weighted_tv(nu_hat, nu, w, p)
+    value = transport + dmu + dnu
+    upper = {"value": value, "raw_value": value, "transport": transport, "delta_mu": dmu,
+             "delta_nu": dnu, "marginal_gap": gap, "converged": float(conv), "iterations": it}
+    return {"lower": lower, "upper": upper, "log_domain": logd}

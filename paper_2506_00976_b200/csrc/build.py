@@ -24,9 +24,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
            "--expt-relaxed-constexpr"] + ARCH
 # files whose arithmetic restates the reference's rounding order: no FMA
-NO_FMA = {"grid_kernels.cu", "primal.cu", "cbar.cu"}
+NO_FMA = {"grid_kernels.cu", "primal.cu", "cbar.cu", "entropic.cu"}
 CU = ["grid_kernels.cu", "cbar.cu", "cbar_fast.cu", "cbar_diag.cu", "primal.cu", "ctransform.cu",
-      "ctransform_pruned.cu"]
+      "ctransform_pruned.cu", "entropic.cu"]
 CPP = ["simplex.cpp"]
 HEADERS = ["common.cuh", os.path.join("..", "..", "include", "gridot_b200.h")]
 
