@@ -72,6 +72,44 @@ def test_fp32_pruned_ctransform_tracks_fp64(dims):
     assert np.allclose(d64, d32, rtol=1e-5, atol=1e-6)
 
 
+@pytest.mark.parametrize("noise", [0.1, 3.0])
+def test_fp32_p1_ctransform_is_exact_brute_force(noise):
+    """The fp32 p = 1 c-transform (lane-pruned table kernel on 2-D grids) equals
+    the fp32 brute force min_i fl(fl(sqrt(d2)) - v_i) bit for bit: pruning only
+    skips rows whose rounded lower bound cannot lower any best value."""
+    import torch
+
+    from paper_2506_00976_b200.engine import ctransform_pair
+
+    dims = (128, 128)
+    n = dims[0] * dims[1]
+    rng = np.random.default_rng(int(noise * 10))
+    X = np.column_stack(np.unravel_index(np.arange(n), dims, order="F")).astype(float)
+    vs = []
+    for b in range(2):
+        v = 9 * np.sin(X[:, 0] / (7.0 + b)) + 5 * np.cos(X[:, 1] / 11.0) + \
+            rng.normal(size=n) * noise
+        vs.append(v)
+    v64 = np.stack(vs)
+    mass = np.full((2, n), 1.0 / n)
+    f, g, _ = ctransform_pair(to_dev(v64), to_dev(mass), to_dev(mass), dims, 1.0, "fp32")
+    Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
+
+    def brute(v32):
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+        for j0 in range(0, n, 2048):
+            d = Xd[j0:j0 + 2048, None, :] - Xd[None, :, :]
+            c = torch.sqrt((d * d).sum(-1))
+            out[j0:j0 + 2048] = (c - v32[None, :]).min(dim=1).values
+        return out
+
+    for b in range(2):
+        v32 = torch.tensor(v64[b], dtype=torch.float32, device="cuda")
+        g_ref = brute(v32)
+        assert torch.equal(g[b], g_ref)
+        assert torch.equal(f[b], brute(g[b]))
+
+
 @pytest.mark.parametrize("cfg,k,max_iter", [(2, 4, 40), (3, 8, 10), (4, 8, 12)])
 def test_fast_ipf_tracks_exact_ipf(cfg, k, max_iter):
     """fp32-mode IPF (block-regrouped mat-vecs, ipf_fast_kernel) vs the exact
