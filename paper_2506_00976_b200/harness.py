@@ -12,8 +12,10 @@ Differences, all deliberate:
 * the exact baseline is the host network simplex (same pivot rules as
   ``_simplex.py``) on the fine grid with an offset-table cost, all pairs of a
   class in one multi-threaded batch;
-* the entropic methods (``reg_lower``, ``reg_upper``, sinkhorn.py:150-299) are
-  outside this build's scope and rejected by ``validate``.
+* the entropic methods (``reg_lower``, ``reg_upper``, sinkhorn.py:150-299) run
+  per pair on the device (``sinkhorn.reg_lower_bound`` / ``reg_upper_bound``)
+  with epsilon = multiplier * n^p (cli.py:224-232), one row per ``--eps``
+  multiplier.
 """
 
 from __future__ import annotations
@@ -28,11 +30,12 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .costs import centre_cost_table
+from .costs import CostSpec, centre_cost_table
 from .engine import QUANT_METHODS, quantized_bounds
 from .errors import GridotError
 from .exact import build_transport_problem, solve_transport_many
 from .measures import GridMeasure, GridSpec, normalize
+from .sinkhorn import RegularizationParams, reg_lower_bound, reg_upper_bound
 
 logger = logging.getLogger(__name__)
 
@@ -40,7 +43,7 @@ GENERATOR_CLASSES = ("gaussians", "shapes", "noise")
 REG_METHODS = ("reg_lower", "reg_upper")
 LOWER_METHODS = frozenset({"min_cost", "dual_upscaling", "reg_lower"})
 ALL_METHODS = ("exact",) + QUANT_METHODS + REG_METHODS
-SUPPORTED_METHODS = ("exact",) + QUANT_METHODS
+SUPPORTED_METHODS = ALL_METHODS
 MAX_EXACT_CELLS = 2 ** 16  # the reference's bench limit (sinkhorn.MAX_KERNEL_CELLS)
 
 CSV_COLUMNS = (
@@ -121,6 +124,7 @@ class BenchConfig:
     out: str | None = None
     max_iter: int = 10_000
     precision: str = "fp64"
+    eps_multipliers: tuple = (0.001, 0.004)
 
     def validate(self) -> None:
         for cls in self.classes:
@@ -146,10 +150,10 @@ class BenchConfig:
             raise CliValidationError(f"pairs must be >= 1, got {self.n_pairs}")
         if not self.methods:
             raise CliValidationError("no methods selected")
+        for m in self.eps_multipliers:
+            if m <= 0.0:
+                raise CliValidationError(f"eps multiplier must be > 0, got {m}")
         for m in self.methods:
-            if m in REG_METHODS:
-                raise CliValidationError(
-                    f"method {m!r} (entropic bounds) is not part of this build")
             if m not in ALL_METHODS:
                 raise CliValidationError(
                     f"unknown method {m!r}; choose from {', '.join(SUPPORTED_METHODS)}")
@@ -278,6 +282,27 @@ def _class_rows(cls: str, class_index: int, cfg: BenchConfig) -> list:
                         if ex_wall:
                             row.rel_time = wall / ex_wall
                     rows.append(row)
+        reg = [m for m in cfg.methods if m in REG_METHODS]
+        coords = GridSpec(dims).coordinates()
+        for i, pid in enumerate(ids):
+            ex_value, ex_wall, _ = exact[i]
+            for m in reg:
+                fn = reg_lower_bound if m == "reg_lower" else reg_upper_bound
+                for mult in cfg.eps_multipliers:
+                    row = ReportRow(pid, m, p, param=format(mult, "g"), exact=ex_value)
+                    try:
+                        params = RegularizationParams(epsilon=mult * max(dims) ** p, xi=cfg.xi,
+                                                      max_iter=cfg.max_iter)
+                        rep = fn(mus[i], nus[i], CostSpec(coords, coords, p), params)
+                        row.bound, row.wall_time = rep.value, rep.wall_time
+                        row.rel_error = _relative_error(m, rep.value, ex_value)
+                        if ex_wall:
+                            row.rel_time = rep.wall_time / ex_wall
+                    except GridotError as exc:
+                        row.error = f"{type(exc).__name__}: {exc}"
+                        logger.warning("%s failed on %s (p=%g, param=%s): %s", m, pid, p,
+                                       row.param, exc)
+                    rows.append(row)
     return rows
 
 
@@ -338,6 +363,7 @@ def _parser() -> _Parser:
     b.add_argument("--methods", default="all")
     b.add_argument("--max-iter", type=int, default=10_000)
     b.add_argument("--precision", default="fp64")
+    b.add_argument("--eps", default="0.001,0.004")
     b.add_argument("--out", default=None)
     return ap
 
@@ -352,7 +378,8 @@ def main(argv=None) -> int:
         cfg = BenchConfig(classes=_split(args.classes, str), n=args.n, d=args.d,
                           p_values=_split(args.p, float), kappas=_split(args.kappa, int),
                           xi=args.xi, seed=args.seed, n_pairs=args.pairs, methods=methods,
-                          out=args.out, max_iter=args.max_iter, precision=args.precision)
+                          out=args.out, max_iter=args.max_iter, precision=args.precision,
+                          eps_multipliers=_split(args.eps, float))
         rows = bench_run(cfg)
         if cfg.out is None:
             write_csv(rows, sys.stdout)

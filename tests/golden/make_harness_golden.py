@@ -4,8 +4,9 @@
         python tests/golden/make_harness_golden.py
 
 Runs the LIVE reference ``gridot.cli.bench_run`` on a small matrix (all three
-generator classes, exact + the four quantization bounds) and writes
-``tests/golden/harness_bench.csv`` plus the generated measures of every pair
+generator classes, exact + the four quantization bounds; exact + the two
+entropic bounds) and writes ``tests/golden/harness_bench.csv``,
+``tests/golden/harness_bench_reg.csv`` plus the generated measures of every pair
 (``tests/golden/harness_measures.npz``), so ``paper_2506_00976_b200.harness``
 can be checked for the same measures (CPU) and the same rows (GPU).
 """
@@ -44,6 +45,13 @@ def main():
         meas[f"{cls}_3d"] = cli.gen_synthetic(cls, 6, 3, seed=[11, 2]).mass
     np.savez_compressed(os.path.join(HERE, "harness_measures.npz"), **meas)
     print(len(rows), "rows")
+    # the entropic methods at the reference's default eps multipliers
+    rcfg = cli.BenchConfig(**{**CFG, "n_pairs": 1,
+                              "methods": ("exact", "reg_lower", "reg_upper")})
+    rrows = cli.bench_run(rcfg)
+    with open(os.path.join(HERE, "harness_bench_reg.csv"), "w", newline="") as fh:
+        cli.write_csv(rrows, fh)
+    print(len(rrows), "entropic rows")
 
 
 if __name__ == "__main__":

@@ -37,7 +37,7 @@ def test_generators_match_reference_bit_for_bit():
 def test_config_validation_and_schema():
     H.BenchConfig(**CFG).validate()
     for bad in (dict(n=3), dict(d=0), dict(n=300), dict(p_values=(0.5,)), dict(kappas=(0,)),
-                dict(xi=0.0), dict(n_pairs=0), dict(methods=()), dict(methods=("reg_lower",)),
+                dict(xi=0.0), dict(n_pairs=0), dict(methods=()), dict(eps_multipliers=(0.0,)),
                 dict(methods=("nope",)), dict(max_iter=0), dict(precision="bf16"),
                 dict(classes=("blobs",))):
         with pytest.raises(H.CliValidationError):
@@ -51,7 +51,8 @@ def test_config_validation_and_schema():
     assert text.splitlines()[0] == ",".join(H.CSV_COLUMNS)
     assert H._relative_error("min_cost", 1.0, 2.0) == 0.5
     assert H._relative_error("weighted_cost", 3.0, 2.0) == 0.5
-    assert H.main(["bench", "--methods", "reg_upper"]) == 1
+    assert H.main(["bench", "--methods", "reg_upper", "--eps", "0"]) == 1
+    H.BenchConfig(**{**CFG, "methods": ("reg_lower", "reg_upper")}).validate()
 
 
 def test_exact_baseline_matches_reference():
@@ -84,3 +85,25 @@ def test_device_bench_matrix_matches_reference_csv():
         for key in ("bound", "exact", "rel_error"):
             a, b = float(g[key]), float(r[key])
             assert abs(a - b) <= 1e-9 * max(1.0, abs(a)), (g["pair"], g["method"], key, a, b)
+
+
+@pytest.mark.gpu
+def test_device_entropic_rows_match_reference_csv():
+    """reg_lower / reg_upper rows at the reference's default eps multipliers
+    (cli.py:123, epsilon = multiplier * n^p).  The lower bound is a dual value
+    (1e-9); the upper bound carries weighted-TV corrections whose rounding
+    noise the 1/p root amplifies (tests/test_entropic.py), hence 1e-7."""
+    with open(os.path.join(GOLD, "harness_bench_reg.csv")) as fh:
+        gold = list(csv.DictReader(fh))
+    cfg = H.BenchConfig(**{**CFG, "n_pairs": 1, "methods": ("exact", "reg_lower", "reg_upper")})
+    got = list(csv.DictReader(io.StringIO(H.rows_to_csv(H.bench_run(cfg)))))
+    assert len(got) == len(gold)
+    for g, r in zip(gold, got):
+        assert (g["pair"], g["method"], g["p"], g["param"]) == \
+            (r["pair"], r["method"], r["p"], r["param"])
+        assert bool(g["error"]) == bool(r["error"]), (g, r)
+        if g["error"]:
+            continue
+        tol = 1e-7 if g["method"] == "reg_upper" else 1e-9
+        a, b = float(g["bound"]), float(r["bound"])
+        assert abs(a - b) <= tol * max(1.0, abs(a)), (g["pair"], g["method"], g["param"], a, b)
