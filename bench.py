@@ -326,6 +326,23 @@ def run_b200(args):
                    "frac": achieved / fp32_peak, "traffic": None,
                    "peak_source": peak_src,
                    "work": "2 FP32 ops x N^4 candidates per pair (N=128)"})
+    # DRAM traffic per launch of the named kernels, from the committed ncu
+    # full-set capture of this config (scripts/ncu_traffic.py); None if absent
+    tfile = os.path.join(HERE, "profiles", f"ncu_traffic_cfg{CFG}.json")
+    try:
+        traffic_tab = json.load(open(tfile))
+    except (OSError, ValueError):
+        traffic_tab = {}
+
+    def traffic(prefix):
+        vals = [v["bytes_per_launch"] for k, v in traffic_tab.items() if k.startswith(prefix)]
+        return sum(vals) / len(vals) if vals else None
+
+    tsrc = f"profiles/ncu_traffic_cfg{CFG}.json (dram read+write per launch, ncu --set full)"
+    if rl is not None:
+        kname = (f"cbar_diag_kernel<{dk}," if dname == "cbar" else "pruned_ct_tab_kernel")
+        rl["traffic"] = traffic(kname)
+        rl["traffic_source"] = tsrc
     # IPF/TV kernel against HBM (north-star secondary roofline)
     peaks = {}
     try:
@@ -346,8 +363,9 @@ def run_b200(args):
     ipf_roof = {"bound": "hbm", "kernel": ("ipf_fast_kernel" if wl.precision == "fp32" else
                                            "ipf_kernel") + " + moments_tv + price (primal stage)",
                 "achieved": ipf_bytes / (prim_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
-                "frac": ipf_bytes / (prim_ms / 1000.0) / 1e9 / hbm, "traffic": None,
-                "sweeps": sweeps,
+                "frac": ipf_bytes / (prim_ms / 1000.0) / 1e9 / hbm,
+                "traffic": traffic("ipf_fast_kernel") if wl.precision == "fp32" else None,
+                "traffic_source": tsrc, "sweeps": sweeps,
                 "work": bytes_model + "; stage time includes pricing"}
 
     ct_roofs = {}
@@ -360,7 +378,8 @@ def run_b200(args):
         best = max(ct_roofs.values())
         ct_roof = {"bound": "fp32", "kernel": "pruned_ct_kernel (fp32, p != 2)",
                    "achieved": best, "peak": fp32_peak, "unit": "TFLOP/s",
-                   "frac": best / fp32_peak, "traffic": None, "per_launch": ct_roofs,
+                   "frac": best / fp32_peak, "traffic": traffic("pruned_ct_tab_kernel"),
+                   "traffic_source": tsrc, "per_launch": ct_roofs,
                    "peak_source": peak_src,
                    "work": "brute-force count 2*N^4 per transform per pair (the reference's "
                            "algorithm); tile pruning evaluates a subset exactly, so this is an "

@@ -10,6 +10,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 echo "launches exit $?"
 $CMD > gpurun_out/prof_plain2.json 2> gpurun_out/prof_plain2.err && \
 ncu --set full --clock-control none --import-source on \
-    -k regex:"cbar_diag|pruned_ct|ipf_kernel|price_kernel|cbar_moments|sep_pass" -c 8 \
+    -k regex:"cbar_diag|pruned_ct|ipf_fast|price_kernel|cbar_moments|sep_tile|moments_tv" -c 12 \
     -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full exit $?"

@@ -48,6 +48,7 @@ RAW = {
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm%",
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue%",
     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma%",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_cyc%",
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu%",
     "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu%",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64%",
