@@ -197,16 +197,22 @@ __global__ void moments_kernel(const double *__restrict__ fine, double *__restri
 // grid: x = chunk of 4*256 columns l, y = group of MB_K row blocks k, z =
 // pair.  A thread keeps the moments of its 4 consecutive columns in registers
 // and sweeps the MB_K rows, whose moments sit in shared memory; the quotient
-// uses reciprocals (fp32 mode: any order / rounding within ~1e-15).
-constexpr int MB_K = 8;
+// uses reciprocals (fp32 mode: any order / rounding within ~1e-15).  ND is a
+// template parameter so the per-axis loops unroll; per output the expansion
+//   numer = denom |D|^2 + 2 D.(M1_k N0_l - M0_k N1_l) + M2_k N0_l + M0_k N2_l
+//           - 2 M1_k.N1_l,   D = kappa (k - l) in block units,
+// is ~4 ND + 6 FP64 operations against 9 bytes written: HBM-bound.
+constexpr int MB_K = 16;
 
+template <int ND>
 __global__ void __launch_bounds__(256) cbar_moments_kernel(
     const double *__restrict__ mu_c, const double *__restrict__ nu_c, const double *__restrict__ mm,
     const double *__restrict__ nm, const double *__restrict__ Ccentre, double *__restrict__ out,
     uint8_t *__restrict__ unused, Grid c, int kappa) {
-    __shared__ double sk[MB_K][GDT_MAX_DIM + 3];  // M0, 1/M0, M1[d], M2
-    __shared__ int skc[MB_K][GDT_MAX_DIM];
-    const int n = (int)c.cells, nd = c.nd, W = nd + 1;
+    constexpr int W = ND + 1;
+    __shared__ double sk[MB_K][ND + 3];  // M0, 1/M0, M1[ND], M2
+    __shared__ double skd[MB_K][ND];     // kappa * k coordinates
+    const int n = (int)c.cells;
     const int k0 = blockIdx.y * MB_K;
     const int64_t b = blockIdx.z;
     if (threadIdx.x < MB_K) {
@@ -216,25 +222,28 @@ __global__ void __launch_bounds__(256) cbar_moments_kernel(
             const double *Mk = mm + ((int64_t)b * n + k) * W;
             sk[threadIdx.x][0] = M0;
             sk[threadIdx.x][1] = M0 > 0.0 ? 1.0 / M0 : 0.0;
-            for (int a = 0; a <= nd; ++a) sk[threadIdx.x][2 + a] = Mk[a];
+#pragma unroll
+            for (int a = 0; a <= ND; ++a) sk[threadIdx.x][2 + a] = Mk[a];
             int kk = k;
-            for (int a = nd - 1; a >= 0; --a) {
-                skc[threadIdx.x][a] = kk / (int)c.stride[a];
-                kk -= skc[threadIdx.x][a] * (int)c.stride[a];
+#pragma unroll
+            for (int a = 0; a < ND; ++a) {
+                const int ca = kk % (int)c.n[a];
+                kk /= (int)c.n[a];
+                skd[threadIdx.x][a] = (double)(kappa * ca);
             }
         }
     }
     __syncthreads();
     const int l0 = (blockIdx.x * 256 + threadIdx.x) * 4;
     if (l0 >= n) return;
-    double N0[4], iN[4], Nm[4][GDT_MAX_DIM + 1];
-    int lc[4][GDT_MAX_DIM];
+    double N0[4], iN[4], N1[4][ND], N2[4], ld[4][ND];
     {
-        int cc[GDT_MAX_DIM];
+        int cc[ND];
         int ll = l0;
-        for (int a = nd - 1; a >= 0; --a) {
-            cc[a] = ll / (int)c.stride[a];
-            ll -= cc[a] * (int)c.stride[a];
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+            cc[a] = ll % (int)c.n[a];
+            ll /= (int)c.n[a];
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -242,43 +251,48 @@ __global__ void __launch_bounds__(256) cbar_moments_kernel(
             N0[q] = nu_c[b * n + l];
             iN[q] = N0[q] > 0.0 ? 1.0 / N0[q] : 0.0;
             const double *Nl = nm + ((int64_t)b * n + l) * W;
-            for (int a = 0; a <= nd; ++a) Nm[q][a] = Nl[a];
-            for (int a = 0; a < nd; ++a) lc[q][a] = cc[a];
-            ++cc[0];
-            for (int a = 0; a < nd - 1 && cc[a] >= (int)c.n[a]; ++a) {
-                cc[a] = 0;
-                ++cc[a + 1];
+#pragma unroll
+            for (int a = 0; a < ND; ++a) {
+                N1[q][a] = Nl[a];
+                ld[q][a] = (double)(kappa * cc[a]);
             }
+            N2[q] = Nl[ND];
+            ++cc[0];
+#pragma unroll
+            for (int a = 0; a < ND - 1; ++a)
+                if (cc[a] >= (int)c.n[a]) {
+                    cc[a] = 0;
+                    ++cc[a + 1];
+                }
         }
     }
     const bool vec = l0 + 3 < n && (n & 3) == 0;
-    for (int kk = 0; kk < MB_K; ++kk) {
+    const int kend = min(MB_K, n - k0);
+    for (int kk = 0; kk < kend; ++kk) {
         const int k = k0 + kk;
-        if (k >= n) break;
-        const double M0 = sk[kk][0], iM = sk[kk][1];
+        const double M0 = sk[kk][0], iM = sk[kk][1], M2 = sk[kk][2 + ND];
         const int64_t orow = ((int64_t)b * n + k) * n;
         double vals[4];
         uint8_t un[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const double denom = __dmul_rn(M0, N0[q]);
-            if (denom == 0.0) {
-                vals[q] = l0 + q < n ? Ccentre[(int64_t)k * n + l0 + q] : 0.0;
-                un[q] = 1;
-                continue;
-            }
             double d2 = 0.0, cross = 0.0, m1n1 = 0.0;
-            for (int a = 0; a < nd; ++a) {
-                const double D = (double)(kappa * (skc[kk][a] - lc[q][a]));
+#pragma unroll
+            for (int a = 0; a < ND; ++a) {
+                const double D = skd[kk][a] - ld[q][a];
+                const double M1 = sk[kk][2 + a];
                 d2 = fma(D, D, d2);
-                cross = fma(D, sk[kk][2 + a] * N0[q] - M0 * Nm[q][a], cross);
-                m1n1 = fma(sk[kk][2 + a], Nm[q][a], m1n1);
+                cross = fma(D, M1 * N0[q] - M0 * N1[q][a], cross);
+                m1n1 = fma(M1, N1[q][a], m1n1);
             }
-            const double numer = denom * d2 + 2.0 * cross + sk[kk][2 + nd] * N0[q] +
-                                 M0 * Nm[q][nd] - 2.0 * m1n1;
+            const double numer = denom * d2 + 2.0 * cross + M2 * N0[q] + M0 * N2[q] - 2.0 * m1n1;
+            un[q] = denom == 0.0;
             vals[q] = numer * iM * iN[q];
-            un[q] = 0;
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (un[q]) vals[q] = l0 + q < n ? Ccentre[(int64_t)k * n + l0 + q] : 0.0;
         if (vec) {
             reinterpret_cast<double2 *>(out + orow + l0)[0] = make_double2(vals[0], vals[1]);
             reinterpret_cast<double2 *>(out + orow + l0)[1] = make_double2(vals[2], vals[3]);
@@ -323,8 +337,14 @@ extern "C" int gdt_weighted_cost(const double *mu, const double *nu, const doubl
         moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(nu, mom + batch * n * W, batch,
                                                                    f, c, kappa);
         dim3 mg((unsigned)((n + 1023) / 1024), (unsigned)((n + MB_K - 1) / MB_K), (unsigned)batch);
-        cbar_moments_kernel<<<mg, 256, 0, st>>>(mu_c, nu_c, mom, mom + batch * n * W, centre_cost,
-                                                 out, unused, c, kappa);
+        auto launch = [&](auto kern) {
+            kern<<<mg, 256, 0, st>>>(mu_c, nu_c, mom, mom + batch * n * W, centre_cost, out, unused,
+                                     c, kappa);
+        };
+        if (ndim == 1) launch(cbar_moments_kernel<1>);
+        else if (ndim == 2) launch(cbar_moments_kernel<2>);
+        else if (ndim == 3) launch(cbar_moments_kernel<3>);
+        else launch(cbar_moments_kernel<4>);
         cudaFreeAsync(mom, st);
         return cuda_status("gdt_weighted_cost(moments)");
     }
