@@ -256,6 +256,19 @@ int gdt_transport_simplex_many(int64_t count, const uint64_t *C, const uint64_t 
                                const uint64_t *u, const uint64_t *v, int32_t *status,
                                int64_t *pivots, int threads);
 
+/* gdt_transport_simplex_many with hand-off flags (both nullable): job q waits
+ * until ready[q] != 0 (the caller sets it from another thread once the job's
+ * cost data is in host memory) and done[q] is set to 1 when its outputs and
+ * status are final, so finished jobs can be consumed while the batch runs. */
+int gdt_transport_simplex_many_flags(int64_t count, const uint64_t *C, const uint64_t *table,
+                                     const int32_t *grid_ndim, const int64_t *grid_dims,
+                                     const uint64_t *sup, const uint64_t *dem, const int64_t *ns,
+                                     const int64_t *nt, const int64_t *warm_from, double tol,
+                                     const uint64_t *bi, const uint64_t *bj, const uint64_t *bf,
+                                     const uint64_t *u, const uint64_t *v, int32_t *status,
+                                     int64_t *pivots, int threads, const int32_t *ready,
+                                     int32_t *done);
+
 /* ---- entropic bounds (sinkhorn.py:150-299) ------------------------------ */
 
 /* Device scratch for gdt_entropic_fit / gdt_entropic_plan: the dense

@@ -48,6 +48,8 @@ _SIGNATURES = {
     "gdt_transport_simplex": (I32, [P, P, P, I64, I64, I64, I64, D, P, P, P, P, P, P]),
     "gdt_transport_simplex_many": (I32, [I64, P, P, P, P, P, P, P, P, P, D, P, P, P, P, P, P, P,
                                          I32]),
+    "gdt_transport_simplex_many_flags": (I32, [I64, P, P, P, P, P, P, P, P, P, D, P, P, P, P, P,
+                                               P, P, I32, P, P]),
 }
 
 _lib = None

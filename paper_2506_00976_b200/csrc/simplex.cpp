@@ -678,6 +678,17 @@ extern "C" int gdt_transport_simplex(const double *C, const double *sup, const d
 // sequence), warm_from[q] = q from the basis the caller left in job q's own
 // (bi, bj, bf), otherwise from the final basis of job warm_from[q] (< q, same
 // shape): chained jobs run in order on one worker.
+// ready / done (nullable): job q starts only once ready[q] != 0 (set by the
+// caller from another thread, e.g. after copying its cost matrix to host
+// memory), and done[q] is set to 1 once status[q] and q's outputs are final,
+// so the caller can consume finished jobs while the batch runs.
+extern "C" int gdt_transport_simplex_many_flags(
+    int64_t count, const uint64_t *C, const uint64_t *table, const int32_t *grid_ndim,
+    const int64_t *grid_dims, const uint64_t *sup, const uint64_t *dem, const int64_t *ns,
+    const int64_t *nt, const int64_t *warm_from, double tol, const uint64_t *bi,
+    const uint64_t *bj, const uint64_t *bf, const uint64_t *u, const uint64_t *v,
+    int32_t *status, int64_t *pivots, int threads, const int32_t *ready, int32_t *done);
+
 extern "C" int gdt_transport_simplex_many(int64_t count, const uint64_t *C, const uint64_t *table,
                                           const int32_t *grid_ndim, const int64_t *grid_dims,
                                           const uint64_t *sup, const uint64_t *dem,
@@ -687,6 +698,17 @@ extern "C" int gdt_transport_simplex_many(int64_t count, const uint64_t *C, cons
                                           const uint64_t *bf, const uint64_t *u,
                                           const uint64_t *v, int32_t *status, int64_t *pivots,
                                           int threads) {
+    return gdt_transport_simplex_many_flags(count, C, table, grid_ndim, grid_dims, sup, dem, ns, nt,
+                                            warm_from, tol, bi, bj, bf, u, v, status, pivots,
+                                            threads, nullptr, nullptr);
+}
+
+extern "C" int gdt_transport_simplex_many_flags(
+    int64_t count, const uint64_t *C, const uint64_t *table, const int32_t *grid_ndim,
+    const int64_t *grid_dims, const uint64_t *sup, const uint64_t *dem, const int64_t *ns,
+    const int64_t *nt, const int64_t *warm_from, double tol, const uint64_t *bi,
+    const uint64_t *bj, const uint64_t *bf, const uint64_t *u, const uint64_t *v,
+    int32_t *status, int64_t *pivots, int threads, const int32_t *ready, int32_t *done) {
     if (count < 0) return GDT_ERR_ARG;
     std::vector<std::vector<int64_t>> kids(count);
     std::vector<int64_t> roots;
@@ -729,6 +751,8 @@ extern "C" int gdt_transport_simplex_many(int64_t count, const uint64_t *C, cons
         return run_with(g, qs, qd, ns[q], nt[q], 0, 0, tol, qbi, qbj, qbf, qu, qv, pivots + q, warm);
     };
     std::function<void(int64_t)> run = [&](int64_t q) {
+        if (ready)  // wait for the caller's go (its data may still be in flight)
+            while (__atomic_load_n(ready + q, __ATOMIC_ACQUIRE) == 0) std::this_thread::yield();
         const int64_t w = warm_from ? warm_from[q] : -1;
         const int64_t nbq = ns[q] + nt[q] - 1;
         if (w == q) {
@@ -746,6 +770,7 @@ extern "C" int gdt_transport_simplex_many(int64_t count, const uint64_t *C, cons
         } else {
             status[q] = solve_job(q, false);
         }
+        if (done) __atomic_store_n(done + q, 1, __ATOMIC_RELEASE);
         for (int64_t k : kids[q]) run(k);
     };
     std::atomic<int64_t> next{0};

@@ -60,6 +60,20 @@ def to_host(t):
 _PINNED = {}
 
 
+def pinned_empty(shape, slot: str, dtype=None):
+    """A page-locked host buffer of `shape` (float64 by default), reused per
+    `slot`; returns (torch view, numpy view) aliasing it."""
+    tt = torch()
+    dtype = dtype or tt.float64
+    n = int(np.prod(shape))
+    buf = _PINNED.get(slot)
+    if buf is None or buf.numel() < n or buf.dtype != dtype:
+        buf = tt.empty(n, dtype=dtype, pin_memory=True)
+        _PINNED[slot] = buf
+    view = buf[:n].view(tuple(shape))
+    return view, view.numpy()
+
+
 def to_host_pinned(t, slot: str = "default"):
     """D2H through a reused page-locked buffer (full PCIe/NVLink-C2C rate).
 

@@ -29,10 +29,10 @@ import numpy as np
 from . import _native as N
 from .costs import (centre_cost_cached, centre_cost_table, cost_table, max_sq_of,
                     min_cost_table, weighted_cost_batch)
-from .device import device, stream, to_dev, to_host, to_host_pinned, torch
+from .device import device, pinned_empty, stream, to_dev, to_host, to_host_pinned, torch
 from .errors import DimensionMismatchError, GridotError, NumericOverflowError, \
     ZeroDenominatorError
-from .exact import build_transport_problem, solve_transport_many
+from .exact import LPBatch, build_transport_problem, solve_transport_many
 from .measures import CoarseningSpec, GridSpec, coarsen_grid, pad_batch, sumpool_batch
 from .reports import BoundReport, signed_root
 
@@ -263,14 +263,17 @@ class _Worker(threading.Thread):
 def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
     """Coarse LPs of several batches overlapped with their device work.
 
-    Phase A: the C-tilde LPs of every batch (the reference's pivot path; they
-    need only the coarse masses) run on the host pool while the device
-    computes C-bar and copies it to pinned host memory.  Phase B: the C-bar /
-    C-min LPs, warm-started from each pair's C-tilde basis, run on the pool
-    while ``device_fn(i, plans_i)`` runs the stages that need only the C-tilde
-    plans (upscaling, IPF, c-transforms).  Values, supports and duals are those
-    of the serial order (same LPs, same starts).  Returns (plans, device
-    results) per batch.
+    All LPs run as ONE native batch on the host pool, one chain per pair:
+    C-tilde (the reference's pivot path; needs only the coarse masses), then
+    C-bar and C-min warm-started from the previous optimal basis of the chain.
+    The C-bar jobs are held until the device has computed C-bar and copied it
+    into their page-locked cost buffers; meanwhile the C-tilde jobs already
+    run.  As soon as every C-tilde job of a (kappa, p) batch has finished,
+    ``device_fn(i, plans_i)`` runs that batch's device stages (upscaling, IPF,
+    c-transforms) while the pool works on the remaining chains.  Values,
+    supports and duals are those of the serial order (same LPs, same starts).
+    Pairs whose coarse supports are partial get their C-bar LP from a dense
+    sub-matrix, built after the batch.  Returns (plans, device results).
     """
     need_ctil = "primal_upscaling" in methods or "dual_upscaling" in methods
     need_cbar = "weighted_cost" in methods
@@ -279,6 +282,7 @@ def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
     t0 = time.perf_counter()
     masses = {i: (to_host(batches[i].mu_c), to_host(batches[i].nu_c)) for i in order}
     plans = {i: CoarsePlans(n=batches[i].n) for i in order}
+    pinned = {}
 
     def build(i, b, cost):
         try:
@@ -286,85 +290,136 @@ def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
         except GridotError as exc:
             return exc
 
-    # phase A
-    ctil_slots, ctil_probs = [], []
-    if need_ctil:
-        for i in order:
-            tab = centre_cost_table(batches[i].pdims, batches[i].kappa, batches[i].p)
-            for b in range(batches[i].B):
-                ctil_slots.append((i, b, build(i, b, tab)))
-        ctil_probs = [pr for _, _, pr in ctil_slots if not isinstance(pr, Exception)]
-    worker = _Worker(solve_transport_many, ctil_probs, threads=lp_threads, slack=False,
-                     return_basis=True)
-    worker.start()
-    t1 = time.perf_counter()
-    pinned, vb_slots, vb_probs = {}, [], []
+    probs, warm, hold, slot = [], [], [], {}  # slot[(i, b, kind)] = job index or exception
+    late = []  # (i, b): C-bar LPs that need the C-bar values to build (partial supports)
     for i in order:
         bt = batches[i]
-        if need_cbar:
-            vals, _ = _cbar(bt)
-            pinned[i] = to_host_pinned(vals, f"cbar{i}")
+        ctil = centre_cost_table(bt.pdims, bt.kappa, bt.p) if need_ctil else None
         cmin = min_cost_table(bt.pdims, bt.kappa, bt.p) if need_cmin else None
+        if need_cbar:
+            pinned[i] = pinned_empty((bt.B, bt.n, bt.n), f"cbar{i}")
         for b in range(bt.B):
-            if need_cbar:
-                vb_slots.append((i, b, "cbar", build(i, b, pinned[i][b])))
-            if need_cmin:
-                vb_slots.append((i, b, "cmin", build(i, b, cmin)))
-    t2 = time.perf_counter()
-    solved, bases = worker.get()
-    t3 = time.perf_counter()
-    basis_of = {}
-    it = iter(zip(solved, bases))
-    for i, b, pr in ctil_slots:
-        pl = plans[i]
-        out, basis = (pr, None) if isinstance(pr, Exception) else next(it)
-        if isinstance(out, Exception):
-            pl.ctil_arcs.append(None)
-            pl.ctil_duals.append(None)
-            pl.ctil_error.append(out)
-        else:
-            coupling, duals, _ = out
-            pl.ctil_arcs.append((pr.src_index[coupling.row], pr.dst_index[coupling.col],
-                                 coupling.mass))
-            pl.ctil_duals.append((duals.g, pr.dst_index))
-            pl.ctil_error.append(None)
-            basis_of[(i, b)] = basis
-    # phase B: each pair's chain C-tilde -> C-bar -> C-min (same marginals)
-    probs, warm_from, warm_basis, live = [], [], [], []
-    prev = {}
-    for i, b, kind, pr in vb_slots:
-        if isinstance(pr, Exception):
-            continue
-        q = len(probs)
-        probs.append(pr)
-        live.append((i, b, kind))
-        if (i, b) in prev:
-            warm_from.append(prev[(i, b)])
-            warm_basis.append(None)
-        else:
-            warm_from.append(-1)
-            warm_basis.append(basis_of.get((i, b)))
-        prev[(i, b)] = q
-    worker = _Worker(solve_transport_many, probs, threads=lp_threads, slack=False,
-                     warm_from=warm_from, warm_basis=warm_basis)
+            full = bool((masses[i][0][b] > 0).all() and (masses[i][1][b] > 0).all())
+            prev = -1
+            for kind in ("ctil", "cbar", "cmin"):
+                if kind == "ctil" and not need_ctil or kind == "cmin" and not need_cmin:
+                    continue
+                if kind == "cbar":
+                    if not need_cbar:
+                        continue
+                    if not full:
+                        late.append((i, b))
+                        continue
+                    pr = build(i, b, pinned[i][1][b])  # values arrive before release
+                else:
+                    pr = build(i, b, ctil if kind == "ctil" else cmin)
+                if isinstance(pr, Exception):
+                    slot[(i, b, kind)] = pr
+                    continue
+                q = len(probs)
+                probs.append(pr)
+                warm.append(prev)
+                if kind == "cbar":
+                    hold.append(q)
+                slot[(i, b, kind)] = q
+                prev = q
+    batch = LPBatch(probs, warm_from=warm, hold=hold)
+    worker = _Worker(batch.run, lp_threads)
     worker.start()
+    t1 = time.perf_counter()
+    # C-bar on the device, into the page-locked cost buffers, then release
+    try:
+        for i in order:
+            if not need_cbar:
+                break
+            vals, _ = _cbar(batches[i])
+            pinned[i][0].copy_(vals, non_blocking=True)
+            torch().cuda.current_stream(vals.device).synchronize()
+            qs = [slot[(i, b, "cbar")] for b in range(batches[i].B)
+                  if isinstance(slot.get((i, b, "cbar")), int)]
+            batch.release(qs)
+    except BaseException:
+        batch.release(hold)  # never leave the pool waiting; the error propagates
+        worker.join()
+        raise
+    t2 = time.perf_counter()
+
+    def ctil_jobs(i):
+        return [slot[(i, b, "ctil")] for b in range(batches[i].B)
+                if isinstance(slot.get((i, b, "ctil")), int)]
+
+    def assemble_ctil(i):
+        pl = plans[i]
+        for b in range(batches[i].B):
+            q = slot.get((i, b, "ctil"))
+            out = q if isinstance(q, Exception) else batch.result(q)
+            if isinstance(out, Exception):
+                pl.ctil_arcs.append(None)
+                pl.ctil_duals.append(None)
+                pl.ctil_error.append(out)
+            else:
+                pr = probs[q]
+                coupling, duals, _ = out
+                pl.ctil_arcs.append((pr.src_index[coupling.row], pr.dst_index[coupling.col],
+                                     coupling.mass))
+                pl.ctil_duals.append((duals.g, pr.dst_index))
+                pl.ctil_error.append(None)
+
+    # device stages of each batch as soon as its C-tilde LPs are done
+    dev, pending, t_dev = {}, list(order), 0.0
+    while pending:
+        ready_i = [i for i in pending if all(batch.finished(q) for q in ctil_jobs(i))]
+        if not ready_i:
+            if not worker.is_alive():
+                worker.get()  # surfaces a native failure
+                ready_i = list(pending)
+            else:
+                time.sleep(0.0005)
+                continue
+        for i in ready_i:
+            pending.remove(i)
+            if need_ctil:
+                assemble_ctil(i)
+            td = time.perf_counter()
+            dev[i] = device_fn(i, plans[i])
+            t_dev += time.perf_counter() - td
+    t3 = time.perf_counter()
+    worker.get()
     t4 = time.perf_counter()
-    dev = {i: device_fn(i, plans[i]) for i in order}
-    t5 = time.perf_counter()
-    values = {key: out for key, out in zip(live, worker.get())}
-    t6 = time.perf_counter()
-    for i, b, kind, pr in vb_slots:
-        v = pr if isinstance(pr, Exception) else values[(i, b, kind)]
-        v = v if isinstance(v, Exception) else v[2]
-        (plans[i].cbar_value if kind == "cbar" else plans[i].cmin_value).append(v)
-    pinned.clear()
+    # partial-support C-bar LPs (dense sub-matrices of the copied C-bar)
+    if late:
+        lp_probs, lp_keys = [], []
+        for i, b in late:
+            pr = build(i, b, pinned[i][1][b])
+            if isinstance(pr, Exception):
+                slot[(i, b, "cbar")] = pr
+            else:
+                lp_keys.append((i, b))
+                lp_probs.append(pr)
+        for (i, b), out in zip(lp_keys, solve_transport_many(lp_probs, threads=lp_threads,
+                                                             slack=False)):
+            slot[(i, b, "cbar")] = out if isinstance(out, Exception) else ("late", out)
     for i in order:
-        plans[i].lp_seconds = (t3 - t0) + (t6 - t4)
-        plans[i].solve_seconds = (t3 - t1) + (t6 - t4)
+        for kind, dst in (("cbar", plans[i].cbar_value), ("cmin", plans[i].cmin_value)):
+            if kind == "cbar" and not need_cbar or kind == "cmin" and not need_cmin:
+                continue
+            for b in range(batches[i].B):
+                q = slot[(i, b, kind)]
+                if isinstance(q, tuple):
+                    v = q[1]
+                elif isinstance(q, Exception):
+                    v = q
+                else:
+                    v = batch.result(q)
+                dst.append(v if isinstance(v, Exception) else v[2])
+    t5 = time.perf_counter()
+    for i in order:
+        plans[i].lp_seconds = t4 - t0
+        plans[i].solve_seconds = t4 - t1
         plans[i].cbar_seconds = t2 - t1
     if timings is not None:
-        timings.update(lp_ctil_build=t1 - t0, cbar_and_build=t2 - t1, lp_ctil_wait=t3 - t2,
-                       device=t5 - t4, lp_cbar_wait=t6 - t5)
+        timings.update(lp_build=t1 - t0, cbar=t2 - t1, device_overlapped=t_dev,
+                       lp_tail_wait=t4 - t3, lp_late_and_values=t5 - t4)
     return plans, dev
 
 

@@ -20,7 +20,8 @@ from . import _native as N
 from .errors import GridotError, IterationLimitError, UnbalancedError
 
 __all__ = ["TransportProblem", "SparseCoupling", "DualPotentials", "build_transport_problem",
-           "solve_transport", "solve_transport_many", "OffsetTableCost", "REBALANCE_TOLERANCE"]
+           "solve_transport", "solve_transport_many", "OffsetTableCost", "REBALANCE_TOLERANCE",
+           "LPBatch"]
 
 logger = logging.getLogger(__name__)
 
@@ -186,6 +187,102 @@ def solve_transport(problem: TransportProblem, tol: float = 1e-10,
     return _finish(problem, st, bi, bj, bf, u, v, int(piv.value))
 
 
+class LPBatch:
+    """A batch of LPs for one native call (``gdt_transport_simplex_many_flags``).
+
+    Jobs may be held back until their cost data exists (``hold`` then
+    ``release(q)``, callable from another thread while :meth:`run` blocks in
+    native code) and consumed as soon as they finish (``finished(q)``,
+    ``result(q)``, ``basis(q)``).  ``warm_from`` / ``warm_basis`` as in
+    :func:`solve_transport_many`.
+    """
+
+    def __init__(self, problems, tol: float = 1e-10, warm_from=None, warm_basis=None,
+                 hold=None):
+        self.problems = list(problems)
+        count = len(self.problems)
+        self.tol = float(tol)
+        self._keep = []  # every buffer the native call reads stays alive with the batch
+
+        def addr(a):
+            self._keep.append(a)
+            return a.ctypes.data
+
+        self.ns = np.array([p.shape[0] for p in self.problems], np.int64)
+        self.nt = np.array([p.shape[1] for p in self.problems], np.int64)
+        self.out = [(np.empty(a + b - 1, np.int64), np.empty(a + b - 1, np.int64),
+                     np.empty(a + b - 1), np.empty(a), np.empty(b))
+                    for a, b in zip(self.ns, self.nt)]
+        ptr = lambda xs: np.array([addr(x) for x in xs], np.uint64)  # noqa: E731
+        self.C = np.zeros(count, np.uint64)
+        self.T = np.zeros(count, np.uint64)
+        self.gnd = np.zeros(count, np.int32)
+        self.gdims = np.ones((count, 4), np.int64)
+        for q, prob in enumerate(self.problems):
+            if isinstance(prob.cost, OffsetTableCost):
+                self.T[q] = addr(prob.cost.table)
+                self.gnd[q] = len(prob.cost.cdims)
+                self.gdims[q, :self.gnd[q]] = prob.cost.cdims
+            else:
+                cost = prob.cost
+                if not (isinstance(cost, np.ndarray) and cost.dtype == np.float64
+                        and cost.flags.c_contiguous):
+                    cost = np.ascontiguousarray(cost, dtype=np.float64)
+                self.C[q] = addr(cost)
+        self.sup = ptr([np.ascontiguousarray(p.supply) for p in self.problems])
+        self.dem = ptr([np.ascontiguousarray(p.demand) for p in self.problems])
+        self.bi, self.bj, self.bf, self.u, self.v = (ptr([o[i] for o in self.out])
+                                                     for i in range(5))
+        self.wf = (np.full(count, -1, np.int64) if warm_from is None
+                   else np.array(warm_from, np.int64))
+        if warm_basis is not None:
+            for q, wb in enumerate(warm_basis):
+                if wb is None:
+                    continue
+                if self.wf[q] >= 0 or len(wb[0]) != len(self.out[q][0]):
+                    raise ValueError("warm_basis: one start per problem, sized ns + nt - 1")
+                for dst, src in zip(self.out[q][:3], wb):
+                    dst[:] = src
+                self.wf[q] = q
+        self.ready = np.ones(count, np.int32)
+        if hold is not None:
+            self.ready[np.asarray(hold, dtype=np.int64)] = 0
+        self.done = np.zeros(count, np.int32)
+        self.status = np.full(count, -999, np.int32)
+        self.pivots = np.zeros(count, np.int64)
+
+    def release(self, q) -> None:
+        """Let held job(s) q start (their cost data is now in place)."""
+        self.ready[q] = 1
+
+    def run(self, threads: int = 0) -> None:
+        if len(self.problems) == 0:
+            return
+        N.check(N.lib().gdt_transport_simplex_many_flags(
+            len(self.problems), N.ptr(self.C), N.ptr(self.T), N.ptr(self.gnd),
+            N.ptr(self.gdims), N.ptr(self.sup), N.ptr(self.dem), N.ptr(self.ns), N.ptr(self.nt),
+            N.ptr(self.wf), self.tol, N.ptr(self.bi), N.ptr(self.bj), N.ptr(self.bf),
+            N.ptr(self.u), N.ptr(self.v), N.ptr(self.status), N.ptr(self.pivots), int(threads),
+            N.ptr(self.ready), N.ptr(self.done)), "gdt_transport_simplex_many_flags")
+
+    def finished(self, q) -> bool:
+        return bool(self.done[q])
+
+    def result(self, q, slack: bool = False):
+        """(coupling, duals, value) of job q, or the exception it raised."""
+        st = int(self.status[q])
+        try:
+            if st < 0:
+                raise GridotError(f"simplex failed with native status {st}")
+            return _finish(self.problems[q], st, *self.out[q], int(self.pivots[q]), slack=slack)
+        except GridotError as exc:
+            return exc
+
+    def basis(self, q):
+        """Final basis (bi, bj, bf) of job q, None if it failed."""
+        return self.out[q][:3] if int(self.status[q]) in (0,) else None
+
+
 def solve_transport_many(problems, tol: float = 1e-10, threads: int = 0, warm_from=None,
                          slack: bool = True, warm_basis=None, return_basis: bool = False):
     """Solve a batch of problems on `threads` host threads (0 = all cores).
@@ -205,57 +302,10 @@ def solve_transport_many(problems, tol: float = 1e-10, threads: int = 0, warm_fr
     count = len(problems)
     if count == 0:
         return ([], []) if return_basis else []
-    keep = []  # keep every buffer alive for the duration of the native call
-
-    def addr(a):
-        keep.append(a)
-        return a.ctypes.data
-
-    ns = np.array([p.shape[0] for p in problems], np.int64)
-    nt = np.array([p.shape[1] for p in problems], np.int64)
-    out = [(np.empty(a + b - 1, np.int64), np.empty(a + b - 1, np.int64), np.empty(a + b - 1),
-            np.empty(a), np.empty(b)) for a, b in zip(ns, nt)]
-    ptr = lambda xs: np.array([addr(x) for x in xs], np.uint64)  # noqa: E731
-    C = np.zeros(count, np.uint64)
-    T = np.zeros(count, np.uint64)
-    gnd = np.zeros(count, np.int32)
-    gdims = np.ones((count, 4), np.int64)
-    for q, prob in enumerate(problems):
-        if isinstance(prob.cost, OffsetTableCost):
-            T[q] = addr(prob.cost.table)
-            gnd[q] = len(prob.cost.cdims)
-            gdims[q, :gnd[q]] = prob.cost.cdims
-        else:
-            C[q] = addr(np.ascontiguousarray(prob.cost, dtype=np.float64))
-    sup = ptr([np.ascontiguousarray(p.supply) for p in problems])
-    dem = ptr([np.ascontiguousarray(p.demand) for p in problems])
-    bi, bj, bf, u, v = (ptr([o[i] for o in out]) for i in range(5))
-    wf = np.full(count, -1, np.int64) if warm_from is None else np.array(warm_from, np.int64)
-    if warm_basis is not None:
-        for q, wb in enumerate(warm_basis):
-            if wb is None:
-                continue
-            if wf[q] >= 0 or len(wb[0]) != len(out[q][0]):
-                raise ValueError("warm_basis: one start per problem, sized ns + nt - 1")
-            for dst, src in zip(out[q][:3], wb):
-                dst[:] = src
-            wf[q] = q
-    status = np.empty(count, np.int32)
-    pivots = np.empty(count, np.int64)
-    N.check(N.lib().gdt_transport_simplex_many(
-        count, N.ptr(C), N.ptr(T), N.ptr(gnd), N.ptr(gdims), N.ptr(sup), N.ptr(dem), N.ptr(ns),
-        N.ptr(nt), N.ptr(wf), float(tol),
-        N.ptr(bi), N.ptr(bj), N.ptr(bf), N.ptr(u), N.ptr(v), N.ptr(status), N.ptr(pivots),
-        int(threads)), "gdt_transport_simplex_many")
-    res, bases = [], []
-    for q, prob in enumerate(problems):
-        st = int(status[q])
-        try:
-            if st < 0:
-                raise GridotError(f"simplex failed with native status {st}")
-            res.append(_finish(prob, st, *out[q], int(pivots[q]), slack=slack))
-            bases.append(out[q][:3])
-        except GridotError as exc:
-            res.append(exc)
-            bases.append(None)
-    return (res, bases) if return_basis else res
+    batch = LPBatch(problems, tol=tol, warm_from=warm_from, warm_basis=warm_basis)
+    batch.run(threads)
+    res = [batch.result(q, slack=slack) for q in range(count)]
+    if return_basis:
+        return res, [None if isinstance(r, Exception) else batch.out[q][:3]
+                     for q, r in enumerate(res)]
+    return res
