@@ -1166,55 +1166,70 @@ __global__ void __launch_bounds__(MT) moments_tv_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ out,
     const int32_t *__restrict__ status, double *__restrict__ scratch, int64_t stride_pair,
     double *__restrict__ mom, double *__restrict__ part, G32 f, G32 c, int kappa, double p,
-    int want_moments) {
+    int want_moments, int lb) {
+    // one group of `lb` consecutive lanes per coarse block (tv_lanes: a power
+    // of two dividing kappa^d): lane j of the group takes the block's cells
+    // j, j + lb, ...; moments fold over the group by shuffles, TV partials
+    // over the CTA (fixed order: deterministic)
     __shared__ double sh[32];
     const int64_t b = blockIdx.y;
     const int N = f.cells, n = c.cells;
     const int m = (int)ipow(kappa, f.nd);
     const int U = UNIFORM ? n : N;
     const int MW = 2 * (f.nd + 2);
+    const int gid = blockIdx.x * MT + threadIdx.x;
+    const int k = gid / lb, j = gid - k * lb;
     double tmu = 0.0, tnu = 0.0;
-    if (status[b] == GDT_PAIR_OK) {
+    double A[2 + GDT_MAX_DIM] = {0, 0, 0, 0, 0, 0}, Bm[2 + GDT_MAX_DIM] = {0, 0, 0, 0, 0, 0};
+    const bool live = status[b] == GDT_PAIR_OK && k < n;
+    if (live) {
         const double *ws = scratch + b * stride_pair;
         const double *a = out[b * 8 + 7] == 0.0 ? ws : ws + N;
         const double *bv = ws + 2 * N, *kb = ws + 3 * N, *kta = ws + 3 * N + U;
         const double *mub = mu + b * N, *nub = nu + b * N;
         const double ctr = (kappa - 1) / 2.0;
-        const int k = blockIdx.x * MT + threadIdx.x;
-        if (k < n) {
-            const int origin = block_origin(k, c, f, kappa);
-            double A[2 + GDT_MAX_DIM] = {0, 0, 0, 0, 0, 0}, Bm[2 + GDT_MAX_DIM] = {0, 0, 0, 0, 0, 0};
-            for_block_cells(origin, f, kappa, [&](int t, int i) {
-                const double w = tv_weight(i, f, p);
-                const double kbu = kb[UNIFORM ? k : k * m + t];
-                const double ktu = kta[UNIFORM ? k : k * m + t];
-                const double ai = a[i], bi = bv[i];
-                const double mh = mub[i] > 0.0 ? __dmul_rn(ai, kbu) : 0.0;
-                const double nh = nub[i] > 0.0 ? __dmul_rn(bi, ktu) : 0.0;
-                tmu += w * fabs(__dsub_rn(mh, mub[i]));
-                tnu += w * fabs(__dsub_rn(nh, nub[i]));
-                if (want_moments) {
-                    int rem = t;
-                    double r2 = 0.0;
-                    for (int q = 0; q < f.nd; ++q) {
-                        const double dl = (double)(rem % kappa) - ctr;
-                        rem /= kappa;
-                        A[1 + q] += ai * dl;
-                        Bm[1 + q] += bi * dl;
-                        r2 += dl * dl;
-                    }
-                    A[0] += ai;
-                    Bm[0] += bi;
-                    A[1 + f.nd] += ai * r2;
-                    Bm[1 + f.nd] += bi * r2;
-                }
-            });
+        const int origin = block_origin(k, c, f, kappa);
+        for (int t = j; t < m; t += lb) {
+            int i = origin, rem = t;
+            double dl[GDT_MAX_DIM], r2 = 0.0;
+            for (int q = 0; q < f.nd; ++q) {
+                const int o = rem % kappa;
+                rem /= kappa;
+                i += o * f.stride[q];
+                dl[q] = (double)o - ctr;
+                r2 += dl[q] * dl[q];
+            }
+            const double w = tv_weight(i, f, p);
+            const double kbu = kb[UNIFORM ? k : k * m + t];
+            const double ktu = kta[UNIFORM ? k : k * m + t];
+            const double ai = a[i], bi = bv[i];
+            const double mh = mub[i] > 0.0 ? __dmul_rn(ai, kbu) : 0.0;
+            const double nh = nub[i] > 0.0 ? __dmul_rn(bi, ktu) : 0.0;
+            tmu += w * fabs(__dsub_rn(mh, mub[i]));
+            tnu += w * fabs(__dsub_rn(nh, nub[i]));
             if (want_moments) {
-                double *o = mom + ((int64_t)b * n + k) * MW;
-                for (int q = 0; q < f.nd + 2; ++q) {
-                    o[q] = A[q];
-                    o[f.nd + 2 + q] = Bm[q];
+                for (int q = 0; q < f.nd; ++q) {
+                    A[1 + q] += ai * dl[q];
+                    Bm[1 + q] += bi * dl[q];
                 }
+                A[0] += ai;
+                Bm[0] += bi;
+                A[1 + f.nd] += ai * r2;
+                Bm[1 + f.nd] += bi * r2;
+            }
+        }
+    }
+    if (want_moments) {  // uniform across the CTA: every lane takes part in the shuffles
+        for (int q = 0; q < f.nd + 2; ++q)
+            for (int o = 1; o < lb; o <<= 1) {
+                A[q] += __shfl_xor_sync(0xffffffffu, A[q], o, lb);
+                Bm[q] += __shfl_xor_sync(0xffffffffu, Bm[q], o, lb);
+            }
+        if (live && j == 0) {
+            double *o = mom + ((int64_t)b * n + k) * MW;
+            for (int q = 0; q < f.nd + 2; ++q) {
+                o[q] = A[q];
+                o[f.nd + 2 + q] = Bm[q];
             }
         }
     }
@@ -1357,21 +1372,31 @@ __global__ void arc_rows_kernel(const int64_t *__restrict__ arc_off,
     }
 }
 
+// one warp per pair: lanes stride over the CTA partials, fixed-order butterfly
 __global__ void finish_kernel(const double *__restrict__ tv_part, int tv_ctas,
                               const double *__restrict__ pr_part, int pr_ctas,
                               const int32_t *__restrict__ status, double *__restrict__ out,
                               int64_t batch) {
-    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (b >= batch || status[b] != GDT_PAIR_OK) return;
+    const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (b >= batch || status[b] != GDT_PAIR_OK) return;  // warp-uniform
     double tmu = 0.0, tnu = 0.0, pr = 0.0;
-    for (int i = 0; i < tv_ctas; ++i) {
+    for (int i = lane; i < tv_ctas; i += 32) {
         tmu += tv_part[(b * tv_ctas + i) * 2];
         tnu += tv_part[(b * tv_ctas + i) * 2 + 1];
     }
-    for (int i = 0; i < pr_ctas; ++i) pr += pr_part[b * pr_ctas + i];
-    out[b * 8 + 0] = pr;
-    out[b * 8 + 1] = tmu;
-    out[b * 8 + 2] = tnu;
+    for (int i = lane; i < pr_ctas; i += 32) pr += pr_part[b * pr_ctas + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        tmu += __shfl_xor_sync(0xffffffffu, tmu, o);
+        tnu += __shfl_xor_sync(0xffffffffu, tnu, o);
+        pr += __shfl_xor_sync(0xffffffffu, pr, o);
+    }
+    if (lane == 0) {
+        out[b * 8 + 0] = pr;
+        out[b * 8 + 1] = tmu;
+        out[b * 8 + 2] = tnu;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1498,6 +1523,15 @@ __global__ void sum_parts_kernel(const double *__restrict__ part, int count, dou
 // scratch layout per pair: [aA N][aB N][b N][kb U][kta U]; then, after all
 // pairs: moments [B, n, MW], tv partials [B, tv_ctas, 2], price partials
 // [B, pr_ctas]
+// lanes per coarse block in moments_tv_kernel: a power of two dividing
+// kappa^d with >= 4 cells per lane (the group fold costs shuffles), <= 32
+inline int tv_lanes(const Grid &f, const Grid &c) {
+    const int64_t m = f.cells / c.cells;
+    int lb = 1;
+    while (lb < 32 && lb * 8 <= m && m % (lb * 2) == 0) lb *= 2;
+    return lb;
+}
+
 struct PrimalLayout {
     int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, bm_off, fp_off, ar_off, total, tv_ctas,
         pr_ctas;
@@ -1510,7 +1544,7 @@ inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, b
     L.stride_pair = 3 * f.cells + 4 * U;  // aA, aB, b, kb, kta, reciprocals / S, B
     L.mom_off = batch * L.stride_pair;
     const int64_t MW = 2 * (f.nd + 2);
-    L.tv_ctas = (c.cells + MT - 1) / MT;
+    L.tv_ctas = (c.cells * tv_lanes(f, c) + MT - 1) / MT;
     // brute-force pricing has one item per (arc, row offset): f.cells / c.cells = kappa^d
     const int64_t items = (uniform && p2) ? max_arcs : max_arcs * (f.cells / c.cells);
     L.pr_ctas = (items + MT - 1) / MT;
@@ -1650,7 +1684,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
     if (uni) {
         moments_tv_kernel<true><<<gtv, MT, 0, st>>>(mu, nu, out, status, ws, L.stride_pair,
                                                     ws + L.mom_off, ws + L.tv_off, f32, c32,
-                                                    kappa, p, closed);
+                                                    kappa, p, closed, tv_lanes(f, c));
         price_kernel<true><<<gpr, MT, 0, st>>>(arc_off, row_ptr, row_arc_col, row_arc_mass,
                                                kernel_w, out, status, ws, L.stride_pair,
                                                ws + L.mom_off, ws + L.pr_off, f32, c32, kappa, p,
@@ -1659,13 +1693,13 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
     } else {
         moments_tv_kernel<false><<<gtv, MT, 0, st>>>(mu, nu, out, status, ws, L.stride_pair,
                                                      ws + L.mom_off, ws + L.tv_off, f32, c32,
-                                                     kappa, p, 0);
+                                                     kappa, p, 0, tv_lanes(f, c));
         price_kernel<false><<<gpr, MT, 0, st>>>(arc_off, row_ptr, row_arc_col, row_arc_mass,
                                                 kernel_w, out, status, ws, L.stride_pair,
                                                 ws + L.mom_off, ws + L.pr_off, f32, c32, kappa, p,
                                                 cost_table, 0, mode == GDT_MODE_FAST, arc_row);
     }
-    finish_kernel<<<grid_size(batch, 128), 128, 0, st>>>(ws + L.tv_off, (int)L.tv_ctas,
+    finish_kernel<<<grid_size(batch * 32, 128), 128, 0, st>>>(ws + L.tv_off, (int)L.tv_ctas,
                                                          ws + L.pr_off, (int)L.pr_ctas, status,
                                                          out, batch);
     return cuda_status("gdt_primal_upscale");
