@@ -31,7 +31,6 @@
 // fp32 folds, fp64 quotient; the fp32-mode contract of BASELINE.json is 1e-5
 // on the bounds.
 #include <algorithm>
-#include <cstdlib>
 
 #include "common.cuh"
 
@@ -458,27 +457,17 @@ int cbar_fast_diag(const double *mu, const double *nu, const double *mu_c, const
                    cudaStream_t st) {
     const bool p1 = p == 1.0;
     if ((!p1 && table == nullptr) || f.nd > 3 || ipow(kappa, f.nd) > 64) return GDT_ERR_UNSUPPORTED;
-    // tile shape per kappa: (KR row blocks, TR target rows, R columns) per thread;
-    // GDT_DG_VARIANT (tuning only) picks an alternative
-    static const int variant = [] {
-        const char *e = getenv("GDT_DG_VARIANT");
-        return e ? atoi(e) : 0;
-    }();
+    // tile shape per kappa: (KR row blocks, TR target rows, R columns) per
+    // thread, the fastest of the shapes measured on B200 (KR x TR x R with
+    // 64 accumulator floats and no spills at 128 registers)
 #define DG_ARGS mu, nu, mu_c, nu_c, Ccentre, table, max_sq, out, unused, batch, f, c, p1, st
     switch (kappa) {
         case 2: return dg_launch<2, 8, 1, 8>(DG_ARGS);
-        case 4:
-            if (variant == 1) return dg_launch<4, 4, 1, 8>(DG_ARGS);
-            if (variant == 2) return dg_launch<4, 2, 2, 8>(DG_ARGS);
-            if (variant == 3) return dg_launch<4, 2, 4, 8>(DG_ARGS);
-            return dg_launch<4, 4, 2, 8>(DG_ARGS);
-        case 8:
-            if (variant == 1) return dg_launch<8, 2, 1, 8>(DG_ARGS);
-            if (variant == 2) return dg_launch<8, 2, 2, 16>(DG_ARGS);
-            if (variant == 3) return dg_launch<8, 4, 1, 8>(DG_ARGS);
-            return dg_launch<8, 2, 2, 8>(DG_ARGS);
+        case 4: return dg_launch<4, 4, 2, 8>(DG_ARGS);
+        case 8: return dg_launch<8, 2, 2, 8>(DG_ARGS);
         default: return GDT_ERR_UNSUPPORTED;
     }
+#undef DG_ARGS
 }
 
 }  // namespace gdt
