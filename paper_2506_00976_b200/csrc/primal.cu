@@ -149,7 +149,59 @@ struct PairPtrs {
     const int64_t *rpc, *cpc;
     const double *rmass, *cmass;
     double *aA, *aB, *b, *kb, *kta;
+    // uniform kernel: the walk of every unit precomputed once per launch as
+    // runs (first cell, coefficient mass * W), arc q owning runs
+    // [q * K1, (q + 1) * K1), K1 = kappa^(d-1) (run_list_kernel)
+    const int32_t *rrc, *crc;
+    const double *rrf, *crf;
 };
+
+// Exact-order run sum of one unit from its precomputed run list: runs are
+// consumed in order, the next run's loads issued before the current run's
+// adds (they do not depend on acc), every term rounded as accumulate_run does.
+template <int KAP>
+__device__ __forceinline__ double run_list_sum(const int32_t *cells, const double *coefs, int nr,
+                                               const double *x) {
+    double acc = 0.0;
+    if (nr <= 0) return acc;
+    double xc[KAP], cc = coefs[0];
+    {
+        const double *p0 = x + cells[0];
+#pragma unroll
+        for (int i = 0; i < KAP; ++i) xc[i] = p0[i];
+    }
+    for (int r = 0; r < nr; ++r) {
+        double xn[KAP], cn = 0.0;
+        if (r + 1 < nr) {
+            const double *pn = x + cells[r + 1];
+            cn = coefs[r + 1];
+#pragma unroll
+            for (int i = 0; i < KAP; ++i) xn[i] = pn[i];
+        }
+#pragma unroll
+        for (int i = 0; i < KAP; ++i) acc = __dadd_rn(acc, __dmul_rn(cc, xc[i]));
+#pragma unroll
+        for (int i = 0; i < KAP; ++i) xc[i] = xn[i];
+        cc = cn;
+    }
+    return acc;
+}
+
+__device__ __forceinline__ double run_list_sum_any(const int32_t *cells, const double *coefs,
+                                                   int nr, const double *x, int kappa) {
+    switch (kappa) {
+        case 2: return run_list_sum<2>(cells, coefs, nr, x);
+        case 4: return run_list_sum<4>(cells, coefs, nr, x);
+        default: {
+            double acc = 0.0;
+            for (int r = 0; r < nr; ++r) {
+                const double cf = coefs[r], *p = x + cells[r];
+                for (int i = 0; i < kappa; ++i) acc = __dadd_rn(acc, __dmul_rn(cf, p[i]));
+            }
+            return acc;
+        }
+    }
+}
 
 struct Red {  // per-sweep reduction slots
     double gap, amin, amax, bmin, bmax;
@@ -171,19 +223,25 @@ __device__ __forceinline__ void range_acc(double v, double &lo, double &hi, int 
 }
 
 __device__ void block_reduce_red(Red &r, double *sh) {
+    // warp butterflies, then warp 0 folds the per-warp records the same way
+    // and publishes the result (sh holds (PT / 32 + 1) * 6 doubles)
+    auto warp_fold = [](Red &x) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        r.gap += __shfl_xor_sync(0xffffffffu, r.gap, o);
-        r.amin = fmin(r.amin, __shfl_xor_sync(0xffffffffu, r.amin, o));
-        r.bmin = fmin(r.bmin, __shfl_xor_sync(0xffffffffu, r.bmin, o));
-        r.amax = fmax(r.amax, __shfl_xor_sync(0xffffffffu, r.amax, o));
-        r.bmax = fmax(r.bmax, __shfl_xor_sync(0xffffffffu, r.bmax, o));
-        r.zrow |= __shfl_xor_sync(0xffffffffu, r.zrow, o);
-        r.zcol |= __shfl_xor_sync(0xffffffffu, r.zcol, o);
-        r.nonfinite |= __shfl_xor_sync(0xffffffffu, r.nonfinite, o);
-    }
+        for (int o = 16; o > 0; o >>= 1) {
+            x.gap += __shfl_xor_sync(0xffffffffu, x.gap, o);
+            x.amin = fmin(x.amin, __shfl_xor_sync(0xffffffffu, x.amin, o));
+            x.bmin = fmin(x.bmin, __shfl_xor_sync(0xffffffffu, x.bmin, o));
+            x.amax = fmax(x.amax, __shfl_xor_sync(0xffffffffu, x.amax, o));
+            x.bmax = fmax(x.bmax, __shfl_xor_sync(0xffffffffu, x.bmax, o));
+            x.zrow |= __shfl_xor_sync(0xffffffffu, x.zrow, o);
+            x.zcol |= __shfl_xor_sync(0xffffffffu, x.zcol, o);
+            x.nonfinite |= __shfl_xor_sync(0xffffffffu, x.nonfinite, o);
+        }
+    };
+    warp_fold(r);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     constexpr int NW = PT / 32;
+    static_assert(NW <= 32, "one warp folds the per-warp records");
     __syncthreads();
     if (lane == 0) {
         sh[w * 6 + 0] = r.gap;
@@ -194,19 +252,41 @@ __device__ void block_reduce_red(Red &r, double *sh) {
         sh[w * 6 + 5] = (double)(r.zrow | (r.zcol << 1) | (r.nonfinite << 2));
     }
     __syncthreads();
-    Red o = red_init();
-    for (int i = 0; i < NW; ++i) {
-        o.gap += sh[i * 6 + 0];
-        o.amin = fmin(o.amin, sh[i * 6 + 1]);
-        o.amax = fmax(o.amax, sh[i * 6 + 2]);
-        o.bmin = fmin(o.bmin, sh[i * 6 + 3]);
-        o.bmax = fmax(o.bmax, sh[i * 6 + 4]);
-        const int fl = (int)sh[i * 6 + 5];
-        o.zrow |= fl & 1;
-        o.zcol |= (fl >> 1) & 1;
-        o.nonfinite |= (fl >> 2) & 1;
+    if (w == 0) {
+        Red o = red_init();
+        if (lane < NW) {
+            o.gap = sh[lane * 6 + 0];
+            o.amin = sh[lane * 6 + 1];
+            o.amax = sh[lane * 6 + 2];
+            o.bmin = sh[lane * 6 + 3];
+            o.bmax = sh[lane * 6 + 4];
+            const int fl = (int)sh[lane * 6 + 5];
+            o.zrow = fl & 1;
+            o.zcol = (fl >> 1) & 1;
+            o.nonfinite = (fl >> 2) & 1;
+        }
+        warp_fold(o);
+        if (lane == 0) {
+            double *res = sh + NW * 6;
+            res[0] = o.gap;
+            res[1] = o.amin;
+            res[2] = o.amax;
+            res[3] = o.bmin;
+            res[4] = o.bmax;
+            res[5] = (double)(o.zrow | (o.zcol << 1) | (o.nonfinite << 2));
+        }
     }
-    r = o;
+    __syncthreads();
+    const double *res = sh + NW * 6;
+    r.gap = res[0];
+    r.amin = res[1];
+    r.amax = res[2];
+    r.bmin = res[3];
+    r.bmax = res[4];
+    const int fl = (int)res[5];
+    r.zrow = fl & 1;
+    r.zcol = (fl >> 1) & 1;
+    r.nonfinite = (fl >> 2) & 1;
     __syncthreads();
 }
 
@@ -270,6 +350,11 @@ __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c,
     const int k = UNIFORM ? u : u / m;
     const int t = UNIFORM ? 0 : u - k * m;
     const int lo = P.rptr[k], hi = P.rptr[k + 1];
+    if (UNIFORM && kappa <= 8) {  // cells handled by cell_pass_row (all threads, all cells)
+        const int K1 = m / kappa;
+        P.kb[u] = run_list_sum_any(P.rrc + lo * K1, P.rrf + lo * K1, (hi - lo) * K1, bsrc, kappa);
+        return;
+    }
     const int64_t *ids = P.rpc + lo;
     const double *ms = P.rmass + lo;
     double acc = 0.0;
@@ -278,7 +363,7 @@ __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c,
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kb[u] = acc;
-    if (UNIFORM) return;  // cells handled by cell_pass_row (all threads, all cells)
+    if (UNIFORM) return;
     const double rcp = acc > 0.0 ? __drcp_rn(acc) : 0.0;
     const int origin = block_origin(k, c, f, kappa);
     for_block_cells(origin, f, kappa, [&](int tt, int i) {
@@ -305,6 +390,11 @@ __device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c,
     const int l = UNIFORM ? u : u / m;
     const int s = UNIFORM ? 0 : u - l * m;
     const int lo = P.cptr[l], hi = P.cptr[l + 1];
+    if (UNIFORM && kappa <= 8) {  // cells handled by cell_pass_col
+        const int K1 = m / kappa;
+        P.kta[u] = run_list_sum_any(P.crc + lo * K1, P.crf + lo * K1, (hi - lo) * K1, asrc, kappa);
+        return;
+    }
     const int64_t *ids = P.cpc + lo;
     const double *ms = P.cmass + lo;
     double acc = 0.0;
@@ -313,7 +403,7 @@ __device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c,
     };
     walk_blocks(ids, hi - lo, c, f, kappa, fn);
     P.kta[u] = acc;
-    if (UNIFORM) return;  // cells handled by cell_pass_col
+    if (UNIFORM) return;
     const double rcp = acc > 0.0 ? __drcp_rn(acc) : 0.0;
     const int origin = block_origin(l, c, f, kappa);
     for_block_cells(origin, f, kappa, [&](int ss, int j) {
@@ -389,6 +479,37 @@ __device__ __forceinline__ void cell_pass_col(const PairPtrs &P, const G32 &f,
     }
 }
 
+// The uniform kernel's walk of every row / column unit, once per launch:
+// run r of arc q (CSR order) -> first fine cell and coefficient mass * W.
+// One thread per (pair, unit); dir 0 = row units, 1 = column units.
+__global__ void run_list_kernel(const int64_t *__restrict__ arc_off,
+                                const int32_t *__restrict__ ptr, const int64_t *__restrict__ pc,
+                                const double *__restrict__ mass, const double *__restrict__ W,
+                                int64_t batch, G32 f, G32 c, int kappa,
+                                int32_t *__restrict__ cells, double *__restrict__ coefs) {
+    const int n = c.cells;
+    const int K1 = (int)ipow(kappa, f.nd - 1);
+    const double Wu = W[0];
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < batch * n;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = g / n;
+        const int u = (int)(g - b * n);
+        const int64_t a0 = arc_off[b];
+        const int32_t *pp = ptr + b * (n + 1);
+        const int lo = pp[u], hi = pp[u + 1];
+        int32_t *oc = cells + (a0 + lo) * K1;
+        double *of = coefs + (a0 + lo) * K1;
+        const double *ms = mass + a0 + lo;
+        int r = 0;
+        auto fn = [&](int q, int cell, int) {
+            oc[r] = cell;
+            of[r] = __dmul_rn(ms[q], Wu);
+            ++r;
+        };
+        walk_blocks(pc + a0 + lo, hi - lo, c, f, kappa, fn);
+    }
+}
+
 // per-pair scalar record written by ipf_kernel / finish_kernel
 // out[b*8 + {0..7}] = {transport_p, tv_mu, tv_nu, gap, iterations, converged, support, 0}
 
@@ -401,8 +522,10 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     const double *__restrict__ W, const double *__restrict__ xi_in, int64_t max_iter, G32 f,
     G32 c, int kappa, double *__restrict__ out, int32_t *__restrict__ status,
     double *__restrict__ scratch, int64_t stride_pair, const int64_t *__restrict__ rpc,
-    const int64_t *__restrict__ cpc, int use_smem, const int32_t *__restrict__ bmap) {
-    __shared__ double sh[(PT / 32) * 6];
+    const int64_t *__restrict__ cpc, int use_smem, const int32_t *__restrict__ bmap,
+    const int32_t *__restrict__ rl_cells, const double *__restrict__ rl_coef,
+    const int32_t *__restrict__ cl_cells, const double *__restrict__ cl_coef) {
+    __shared__ double sh[(PT / 32 + 1) * 6];
     const int64_t b = blockIdx.x;
     const int N = f.cells, n = c.cells;
     const int m = (int)ipow(kappa, f.nd);
@@ -421,6 +544,13 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     P.cmass = col_arc_mass + a0;
     P.rpc = rpc + a0;
     P.cpc = cpc + a0;
+    {
+        const int64_t K1 = ipow(kappa, f.nd - 1);
+        P.rrc = rl_cells ? rl_cells + a0 * K1 : nullptr;
+        P.rrf = rl_coef ? rl_coef + a0 * K1 : nullptr;
+        P.crc = cl_cells ? cl_cells + a0 * K1 : nullptr;
+        P.crf = cl_coef ? cl_coef + a0 * K1 : nullptr;
+    }
     double *ws = scratch + b * stride_pair;
     P.aA = ws;
     P.aB = ws + N;
@@ -1410,7 +1540,7 @@ __global__ void __launch_bounds__(PT) csr_ipf_kernel(
     double xi, int64_t max_iter, double *__restrict__ a, double *__restrict__ b,
     double *__restrict__ kb, double *__restrict__ kta, double *__restrict__ info,
     int32_t *__restrict__ status) {
-    __shared__ double sh[(PT / 32) * 6];
+    __shared__ double sh[(PT / 32 + 1) * 6];
     for (int64_t j = threadIdx.x; j < nc; j += PT) b[j] = 1.0;
     __syncthreads();
     auto rowpass = [&]() {
@@ -1533,8 +1663,8 @@ inline int tv_lanes(const Grid &f, const Grid &c) {
 }
 
 struct PrimalLayout {
-    int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, bm_off, fp_off, ar_off, total, tv_ctas,
-        pr_ctas;
+    int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, bm_off, fp_off, ar_off, rl_off, total,
+        tv_ctas, pr_ctas, runs;
 };
 
 inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, bool uniform,
@@ -1554,7 +1684,11 @@ inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, b
     L.bm_off = L.pc_off + 2 * batch * max_arcs;    // fine cell -> coarse block (int32)
     L.fp_off = L.bm_off + (f.cells + 1) / 2;        // ipf_fast_kernel partials
     L.ar_off = L.fp_off + batch * 5 * FCS_MAX * (int64_t)(sizeof(FastPart) / sizeof(double));
-    L.total = L.ar_off + (batch * max_arcs + 1) / 2;  // arc -> row block (int32)
+    L.rl_off = L.ar_off + (batch * max_arcs + 1) / 2;  // arc -> row block (int32)
+    // uniform exact IPF: run lists per direction, coefficients (f64) then cells (int32)
+    const int64_t kap = f.n[0] / c.n[0];
+    L.runs = uniform ? batch * max_arcs * (f.cells / c.cells / kap) : 0;
+    L.total = L.rl_off + 2 * L.runs + L.runs;
     return L;
 }
 
@@ -1659,13 +1793,19 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
             return GDT_ERR_CUDA;
         }
     } else if (uni) {
+        double *rl_coef = ws + L.rl_off, *cl_coef = rl_coef + L.runs;
+        int32_t *rl_cells = reinterpret_cast<int32_t *>(cl_coef + L.runs), *cl_cells = rl_cells + L.runs;
+        run_list_kernel<<<grid_size(batch * c.cells, 128), 128, 0, st>>>(
+            arc_off, row_ptr, rpc, row_arc_mass, kernel_w, batch, f32, c32, kappa, rl_cells, rl_coef);
+        run_list_kernel<<<grid_size(batch * c.cells, 128), 128, 0, st>>>(
+            arc_off, col_ptr, cpc, col_arc_mass, kernel_w, batch, f32, c32, kappa, cl_cells, cl_coef);
         if (dyn > 48 * 1024)
             cudaFuncSetAttribute(ipf_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)dyn);
         ipf_kernel<true><<<(unsigned)batch, PT, dyn, st>>>(
             mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
             col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair,
-            rpc, cpc, use_smem, bmap);
+            rpc, cpc, use_smem, bmap, rl_cells, rl_coef, cl_cells, cl_coef);
     } else {
         if (dyn > 48 * 1024)
             cudaFuncSetAttribute(ipf_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1673,7 +1813,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
         ipf_kernel<false><<<(unsigned)batch, PT, dyn, st>>>(
             mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
             col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair,
-            rpc, cpc, use_smem, nullptr);
+            rpc, cpc, use_smem, nullptr, nullptr, nullptr, nullptr, nullptr);
     }
     const int closed = uni && p == 2.0;
     int32_t *arc_row = reinterpret_cast<int32_t *>(ws + L.ar_off);
