@@ -119,6 +119,39 @@ def test_warm_basis_matches_chained_and_cold():
         G.solve_transport_many([pb], warm_basis=[(basis[0][:3], basis[1][:3], basis[2][:3])])
 
 
+def test_lp_batch_hold_release_and_done_flags():
+    """LPBatch: held jobs wait for release (issued from another thread while the
+    native batch runs), chained jobs follow their parent, `finished` flags
+    turn on as jobs complete, and results equal a plain batch's."""
+    import threading
+    import time
+
+    rng = np.random.default_rng(11)
+    n = 40
+    s, t = rng.random(n), rng.random(n)
+    s, t = s / s.sum(), t / t.sum()
+    t[np.argmax(t)] += s.sum() - t.sum()
+    C1 = rng.random((n, n))
+    C2 = np.zeros((n, n))  # filled only after the batch has started
+    probs = [G.build_transport_problem(s, t, C1), G.build_transport_problem(s, t, C2),
+             G.build_transport_problem(s, t, C1)]
+    batch = G.LPBatch(probs, warm_from=[-1, 0, 1], hold=[1])
+    worker = threading.Thread(target=batch.run, kwargs={"threads": 2})
+    worker.start()
+    deadline = time.time() + 30
+    while not batch.finished(0) and time.time() < deadline:
+        time.sleep(0.001)
+    assert batch.finished(0) and not batch.finished(1)
+    C2[:] = rng.random((n, n))  # the held job's cost data arrives
+    batch.release([1])
+    worker.join(30)
+    assert not worker.is_alive() and all(batch.finished(q) for q in range(3))
+    ref = G.solve_transport_many([probs[0], G.build_transport_problem(s, t, C2.copy())],
+                                 threads=1, warm_from=[-1, 0])
+    assert batch.result(0)[2] == ref[0][2] and batch.result(1)[2] == ref[1][2]
+    assert abs(batch.result(2)[2] - ref[0][2]) <= 1e-12 * abs(ref[0][2])
+
+
 def test_lp_error_mapping():
     with pytest.raises(G.UnbalancedError):
         G.build_transport_problem(np.array([0.5, 0.5]), np.array([0.9]), np.ones((2, 1)))
