@@ -365,24 +365,29 @@ def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
                 pl.ctil_duals.append((duals.g, pr.dst_index))
                 pl.ctil_error.append(None)
 
-    # device stages of each batch as soon as its C-tilde LPs are done
+    # device stages of each batch as soon as its C-tilde LPs are done; on an
+    # error the native batch is drained first (it reads the pinned buffers)
     dev, pending, t_dev = {}, list(order), 0.0
-    while pending:
-        ready_i = [i for i in pending if all(batch.finished(q) for q in ctil_jobs(i))]
-        if not ready_i:
-            if not worker.is_alive():
-                worker.get()  # surfaces a native failure
-                ready_i = list(pending)
-            else:
-                time.sleep(0.0005)
-                continue
-        for i in ready_i:
-            pending.remove(i)
-            if need_ctil:
-                assemble_ctil(i)
-            td = time.perf_counter()
-            dev[i] = device_fn(i, plans[i])
-            t_dev += time.perf_counter() - td
+    try:
+        while pending:
+            ready_i = [i for i in pending if all(batch.finished(q) for q in ctil_jobs(i))]
+            if not ready_i:
+                if not worker.is_alive():
+                    worker.get()  # surfaces a native failure
+                    ready_i = list(pending)
+                else:
+                    time.sleep(0.0005)
+                    continue
+            for i in ready_i:
+                pending.remove(i)
+                if need_ctil:
+                    assemble_ctil(i)
+                td = time.perf_counter()
+                dev[i] = device_fn(i, plans[i])
+                t_dev += time.perf_counter() - td
+    except BaseException:
+        worker.join()
+        raise
     t3 = time.perf_counter()
     worker.get()
     t4 = time.perf_counter()
