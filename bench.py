@@ -277,6 +277,21 @@ def run_b200(args):
         dist.barrier()
     clk = clocks.stop()
 
+    # kernels of one step, counted exactly by the CUDA activity profiler on an
+    # extra (untimed) step; the hand count of step() is the fallback
+    try:
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step(new_events())
+            torch.cuda.synchronize()
+        counted = sum(1 for e in prof.events()
+                      if e.device_type.name == "CUDA" and "gdt::" in e.name)
+        if counted > 0:
+            launches_per_step = counted
+    except Exception as exc:  # profiler unavailable: keep the hand count
+        print(f"launch count: profiler unavailable ({exc}); using the hand count",
+              file=sys.stderr)
     step_ms = [sum(ev[ci][0].elapsed_time(ev[ci][6]) for ci in range(len(stages)))
                for ev in all_events]
     stage_ms = {}  # (combo, stage) -> mean ms
