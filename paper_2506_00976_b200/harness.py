@@ -3,7 +3,9 @@
 Mirrors the reference's reporting contract so its CSV consumers carry over:
 ``CSV_COLUMNS`` / ``ReportRow`` (cli.py:46-49, 170-193), ``gen_synthetic``
 (cli.py:60-103), ``BenchConfig`` (cli.py:116-167), ``bench_run`` /
-``write_csv`` (cli.py:282-310) and the ``bench`` sub-command (cli.py:335-356).
+``write_csv`` (cli.py:282-310), the ``bench`` sub-command (cli.py:335-356) and
+the ``dist`` sub-command (cli.py:358-445: two GRID files, one method, one CSV
+record on stdout).
 
 Differences, all deliberate:
 * the quantization bounds of all pairs of one class run as ONE batched device
@@ -34,7 +36,7 @@ from .costs import CostSpec, centre_cost_table
 from .engine import QUANT_METHODS, quantized_bounds
 from .errors import GridotError
 from .exact import build_transport_problem, solve_transport_many
-from .measures import GridMeasure, GridSpec, normalize
+from .measures import GridMeasure, GridSpec, load_grid_measure, normalize
 from .sinkhorn import RegularizationParams, reg_lower_bound, reg_upper_bound
 
 logger = logging.getLogger(__name__)
@@ -329,6 +331,59 @@ def rows_to_csv(rows) -> str:
     return buf.getvalue()
 
 
+def _exact_one(mu: GridMeasure, nu: GridMeasure, p: float):
+    """W_p on the fine grid by the host simplex (exact.py:139-189); (value, s)."""
+    table = centre_cost_table(mu.grid.dims, 1, float(p))  # kappa = 1: the fine costs
+    t0 = time.perf_counter()
+    (res,) = solve_transport_many([build_transport_problem(mu.mass, nu.mass, table)],
+                                  threads=1, slack=False)
+    if isinstance(res, Exception):
+        raise res
+    return res[2] ** (1.0 / p), time.perf_counter() - t0
+
+
+def dist_run(mu_path: str, nu_path: str, method: str, p: float = 2.0, kappa: int = 2,
+             eps: float = 0.001, xi=None, max_iter: int = 10_000,
+             precision: str = "fp64") -> ReportRow:
+    """One bound between two GRID files (cli.py:398-445); GridotError raised by
+    the method is recorded in the row's ``error``."""
+    if method not in ALL_METHODS:
+        raise CliValidationError(
+            f"unknown method {method!r}; choose from {', '.join(ALL_METHODS)}")
+    if p < 1.0:
+        raise CliValidationError(f"p must be >= 1, got {p}")
+    with open(mu_path) as fh:
+        mu = normalize(load_grid_measure(fh))
+    with open(nu_path) as fh:
+        nu = normalize(load_grid_measure(fh))
+    if mu.grid != nu.grid:
+        raise CliValidationError(
+            f"measures live on different grids: {mu.grid.dims} vs {nu.grid.dims}")
+    param = "" if method == "exact" else (format(eps, "g") if method in REG_METHODS
+                                          else str(kappa))
+    row = ReportRow(pair="dist", method=method, p=p, param=param)
+    try:
+        if method == "exact":
+            value, wall = _exact_one(mu, nu, p)
+            row.exact, row.rel_error, row.rel_time = value, 0.0, 1.0
+        elif method in REG_METHODS:
+            fn = reg_lower_bound if method == "reg_lower" else reg_upper_bound
+            coords = mu.grid.coordinates()
+            rep = fn(mu, nu, CostSpec(coords, coords, p),
+                     RegularizationParams(epsilon=eps * max(mu.grid.dims) ** p, xi=xi,
+                                          max_iter=max_iter))
+            value, wall = rep.value, rep.wall_time
+        else:
+            reps = quantized_bounds(mu.mass[None], nu.mass[None], mu.grid.dims, int(kappa),
+                                    float(p), precision=precision, xi=xi, max_iter=max_iter,
+                                    methods=(method,), return_exceptions=False)
+            value, wall = reps[0][method].value, reps[0][method].wall_time
+        row.bound, row.wall_time = value, wall
+    except GridotError as exc:
+        row.error = f"{type(exc).__name__}: {exc}"
+    return row
+
+
 # ---------------------------------------------------------------------------
 # command line: python -m paper_2506_00976_b200.harness bench ...
 # ---------------------------------------------------------------------------
@@ -365,6 +420,16 @@ def _parser() -> _Parser:
     b.add_argument("--precision", default="fp64")
     b.add_argument("--eps", default="0.001,0.004")
     b.add_argument("--out", default=None)
+    d = sub.add_parser("dist", help="bound the distance between two GRID files")
+    d.add_argument("--mu", required=True)
+    d.add_argument("--nu", required=True)
+    d.add_argument("--method", required=True)
+    d.add_argument("--p", type=float, default=2.0)
+    d.add_argument("--kappa", type=int, default=2)
+    d.add_argument("--eps", type=float, default=0.001)
+    d.add_argument("--xi", type=float, default=None)
+    d.add_argument("--max-iter", type=int, default=10_000)
+    d.add_argument("--precision", default="fp64")
     return ap
 
 
@@ -373,6 +438,14 @@ def main(argv=None) -> int:
         args = _parser().parse_args(argv)
         level = (logging.WARNING, logging.INFO, logging.DEBUG)[min(args.verbose, 2)]
         logging.basicConfig(level=level, format="%(levelname)s %(name)s: %(message)s")
+        if args.command == "dist":
+            row = dist_run(args.mu, args.nu, args.method, args.p, args.kappa, args.eps, args.xi,
+                           args.max_iter, args.precision)
+            print(",".join(row.as_record()))
+            if row.error:
+                print(f"gridot-b200: {row.error}", file=sys.stderr)
+                return 2
+            return 0
         methods = (SUPPORTED_METHODS if args.methods.strip() == "all"
                    else _split(args.methods, str))
         cfg = BenchConfig(classes=_split(args.classes, str), n=args.n, d=args.d,

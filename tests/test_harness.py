@@ -6,6 +6,7 @@ from __future__ import annotations
 
 import csv
 import io
+import json
 import os
 
 import numpy as np
@@ -107,3 +108,53 @@ def test_device_entropic_rows_match_reference_csv():
         tol = 1e-7 if g["method"] == "reg_upper" else 1e-9
         a, b = float(g["bound"]), float(r["bound"])
         assert abs(a - b) <= tol * max(1.0, abs(a)), (g["pair"], g["method"], g["param"], a, b)
+
+
+DIST = json.load(open(os.path.join(GOLD, "harness_dist.json")))
+
+
+def _dist_cases(gpu: bool):
+    out = []
+    for c in DIST["cases"]:
+        needs_gpu = c["method"] not in ("exact", "nope")
+        if needs_gpu == gpu:
+            out.append(c)
+    return out
+
+
+def _run_dist(tmp_path, c, capsys):
+    paths = {}
+    for key, text in DIST["grids"].items():
+        paths[key] = tmp_path / f"{key}.grid"
+        paths[key].write_text(text)
+    rc = H.main(["dist", "--mu", str(paths[c["mu"]]), "--nu", str(paths[c["nu"]]),
+                 "--method", c["method"], "--p", c["p"]] + c["extra"])
+    return rc, capsys.readouterr().out
+
+
+def _same_record(got: str, want: str, tol: float):
+    g, w = got.strip().split(","), want.strip().split(",")
+    assert len(g) == len(w) == len(H.CSV_COLUMNS)
+    assert g[:4] == w[:4] and g[9] == w[9]
+    for i in (4, 5, 6):  # bound, exact, rel_error
+        assert (g[i] == "") == (w[i] == "")
+        if w[i]:
+            assert abs(float(g[i]) - float(w[i])) <= tol * max(1.0, abs(float(w[i]))), (i, g, w)
+
+
+@pytest.mark.parametrize("c", _dist_cases(False), ids=lambda c: f"{c['method']}-{c['nu']}")
+def test_dist_host_methods_match_reference(tmp_path, capsys, c):
+    """`dist` (cli.py:358-445) with the host methods: the exact LP value bit for
+    bit, and the reference's exit codes for bad arguments / mismatched grids."""
+    rc, out = _run_dist(tmp_path, c, capsys)
+    assert rc == c["rc"]
+    if c["rc"] == 0:
+        _same_record(out, c["stdout"], 0.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c", _dist_cases(True), ids=lambda c: f"{c['method']}-p{c['p']}")
+def test_dist_device_methods_match_reference(tmp_path, capsys, c):
+    rc, out = _run_dist(tmp_path, c, capsys)
+    assert rc == c["rc"]
+    _same_record(out, c["stdout"], 1e-7 if c["method"] == "reg_upper" else 1e-9)
