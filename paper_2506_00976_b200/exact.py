@@ -21,7 +21,7 @@ from .errors import GridotError, IterationLimitError, UnbalancedError
 
 __all__ = ["TransportProblem", "SparseCoupling", "DualPotentials", "build_transport_problem",
            "solve_transport", "solve_transport_many", "OffsetTableCost", "REBALANCE_TOLERANCE",
-           "LPBatch"]
+           "LPBatch", "grid_transport_problem", "hungarian_oracle", "wasserstein_1d"]
 
 logger = logging.getLogger(__name__)
 
@@ -309,3 +309,69 @@ def solve_transport_many(problems, tol: float = 1e-10, threads: int = 0, warm_fr
         return res, [None if isinstance(r, Exception) else batch.out[q][:3]
                      for q, r in enumerate(res)]
     return res
+
+
+# ---------------------------------------------------------------------------
+# fine-grid instances and the validation oracles (exact.py:139-153, 197-253)
+# ---------------------------------------------------------------------------
+
+
+def grid_transport_problem(mu, nu, p: float, metric: str = "l2") -> TransportProblem:
+    """Fine-scale instance between two grid measures under rho^p costs
+    (exact.py:139-153): supports, rebalanced masses, dense support cost."""
+    from .costs import pairwise_costs
+
+    if metric != "l2":
+        raise ValueError(f"unsupported metric {metric!r}")
+    mu_idx, nu_idx = mu.support, nu.support
+    if mu_idx.size == 0 or nu_idx.size == 0:
+        raise GridotError("transport needs nonempty supports on both sides")
+    sup, dem = mu.mass[mu_idx].copy(), nu.mass[nu_idx].copy()
+    _rebalance(sup, dem)
+    cost = pairwise_costs(mu.grid.coordinates()[mu_idx], nu.grid.coordinates()[nu_idx], p)
+    return TransportProblem(sup, dem, np.ascontiguousarray(cost), mu_idx, nu_idx)
+
+
+def hungarian_oracle(problem: TransportProblem, denom: int) -> float:
+    """Exact value by unit splitting and an assignment solve (exact.py:197-224);
+    every mass must be a multiple of 1/denom.  Small instances only."""
+    from scipy.optimize import linear_sum_assignment
+
+    from .errors import QuantizationResidualError
+
+    ks_f, kd_f = problem.supply * denom, problem.demand * denom
+    res = max(float(np.abs(ks_f - np.round(ks_f)).max()), float(np.abs(kd_f - np.round(kd_f)).max()))
+    if res > 1e-9:
+        raise QuantizationResidualError(f"masses are not multiples of 1/{denom} "
+                                        f"(residual {res:.3e})")
+    ks, kd = np.round(ks_f).astype(np.int64), np.round(kd_f).astype(np.int64)
+    if ks.sum() != kd.sum():
+        raise UnbalancedError(f"unit counts differ: {int(ks.sum())} vs {int(kd.sum())}")
+    cost = problem.cost.dense() if isinstance(problem.cost, OffsetTableCost) else problem.cost
+    unit = np.asarray(cost)[np.ix_(np.repeat(np.arange(ks.size), ks),
+                                   np.repeat(np.arange(kd.size), kd))]
+    rows, cols = linear_sum_assignment(unit)
+    return float(unit[rows, cols].sum()) / denom
+
+
+def wasserstein_1d(mu, nu, p: float) -> float:
+    """Closed-form W_p on a 1-D grid (exact.py:227-253): |F_mu - F_nu| summed
+    for p = 1, quantile slivers swept in lockstep otherwise."""
+    from .errors import DimensionMismatchError, GridMismatchError
+
+    if mu.grid.ndim != 1 or nu.grid.ndim != 1:
+        raise DimensionMismatchError("wasserstein_1d needs 1-dimensional grids")
+    if mu.grid != nu.grid:
+        raise GridMismatchError(f"grids differ: {mu.grid.dims} vs {nu.grid.dims}")
+    if abs(mu.total_mass - nu.total_mass) > 1e-9:
+        raise UnbalancedError(f"total masses differ: {mu.total_mass!r} vs {nu.total_mass!r}")
+    cm, cn = np.cumsum(mu.mass), np.cumsum(nu.mass)
+    if p == 1.0:
+        return float(np.sum(np.abs(cm - cn)))
+    n = mu.grid.cell_count
+    pos = np.arange(1, n + 1, dtype=np.float64)
+    levels = np.union1d(cm, cn)
+    dq = np.diff(np.concatenate(([0.0], levels)))
+    iu = np.minimum(np.searchsorted(cm, levels, side="left"), n - 1)
+    iv = np.minimum(np.searchsorted(cn, levels, side="left"), n - 1)
+    return float(np.sum(dq * np.abs(pos[iu] - pos[iv]) ** p)) ** (1.0 / p)

@@ -248,3 +248,26 @@ def test_device_paths_fail_loudly_without_gpu():
         G.weighted_cost_upper_bound(mu, mu, 2, 2.0)
     with pytest.raises(NoDeviceError):
         G.quantized_bounds(mu.mass[None], mu.mass[None], (4, 4), 2, 2.0)
+
+
+def test_exact_module_helpers():
+    """grid_transport_problem / wasserstein_1d / hungarian_oracle (reference
+    exact.py:139-253): the closed form and the assignment oracle agree with the
+    host simplex on the same instances."""
+    rng = np.random.default_rng(21)
+    for n, p in ((12, 1.0), (12, 2.0), (9, 1.5)):
+        a, b = rng.random(n), rng.random(n)
+        ga = G.GridMeasure(G.GridSpec((n,)), a / a.sum())
+        gb = G.GridMeasure(G.GridSpec((n,)), b / b.sum())
+        lp = G.solve_transport(G.grid_transport_problem(ga, gb, p))[2] ** (1.0 / p)
+        assert abs(G.wasserstein_1d(ga, gb, p) - lp) <= 1e-12 * lp
+    k, l = np.array([2, 1, 3, 0, 2.0]), np.array([1, 1, 2, 3, 1.0])
+    grid = G.GridSpec((5,))
+    prob = G.grid_transport_problem(G.GridMeasure(grid, k / 8), G.GridMeasure(grid, l / 8), 2.0)
+    assert G.hungarian_oracle(prob, 8) == 0.625
+    assert abs(G.solve_transport(prob)[2] - 0.625) <= 1e-15
+    with pytest.raises(G.QuantizationResidualError):
+        G.hungarian_oracle(prob, 3)
+    with pytest.raises(G.DimensionMismatchError):
+        m2 = G.GridMeasure(G.GridSpec((2, 2)), np.full(4, 0.25))
+        G.wasserstein_1d(m2, m2, 1.0)
