@@ -61,20 +61,33 @@ __global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ i
     const int64_t lines_per_pair = cells / L;
     const int64_t total_lines = batch * lines_per_pair;
     const int64_t line0 = (int64_t)blockIdx.x * lpc;
+    // element offset of each of the CTA's lines (the 64-bit index arithmetic
+    // once per line, not per element); -1 past the last line
+    int64_t *lbase = reinterpret_cast<int64_t *>(lines + lpc * L);
     for (int k = threadIdx.x; k < 2 * L + 16; k += blockDim.x) {
         const int d = k - L - 7;
         sq[k] = (TO)(d * d);
     }
-    // load: consecutive threads -> consecutive lines (coalesced when S > 1)
-    for (int e = threadIdx.x; e < lpc * L; e += blockDim.x) {
-        // contiguous axis: i fastest; strided axis: consecutive lines fastest
-        const int li = S == 1 ? e / L : e % lpc, i = S == 1 ? e % L : e / lpc;
+    for (int li = threadIdx.x; li < lpc; li += blockDim.x) {
         const int64_t lid = line0 + li;
-        TO v = (TO)0;
+        int64_t off = -1;
         if (lid < total_lines) {
             const int64_t b = lid / lines_per_pair, r = lid - b * lines_per_pair;
             const int64_t low = r % S, high = r / S;
-            v = (TO)in[b * cells + high * S * L + low + (int64_t)i * S];
+            off = b * cells + high * S * L + low;
+        }
+        lbase[li] = off;
+    }
+    __syncthreads();
+    // load: consecutive threads -> consecutive lines (coalesced when S > 1);
+    // contiguous axis: i fastest; strided axis: consecutive lines fastest
+    for (int e = threadIdx.x; e < lpc * L; e += blockDim.x) {
+        const int li = S == 1 ? e / L : e % lpc;  // 32-bit: e < lpc * L
+        const int i = S == 1 ? e - li * L : e / lpc;
+        const int64_t off = lbase[li];
+        TO v = (TO)0;
+        if (off >= 0) {
+            v = (TO)in[off + (int64_t)i * S];
             if (negate) v = -v;
         }
         lines[li * L + i] = v;
@@ -119,9 +132,7 @@ __global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ i
         }
     }
     if (lid >= total_lines) return;
-    const int64_t b = lid / lines_per_pair, r = lid - b * lines_per_pair;
-    const int64_t low = r % S, high = r / S;
-    TO *o = out + b * cells + high * S * L + low;
+    TO *o = out + lbase[li];
 #pragma unroll
     for (int r8 = 0; r8 < 8; ++r8) o[(int64_t)(j0 + r8) * S] = best[r8];
 }
@@ -427,7 +438,8 @@ extern "C" int gdt_ctransform_grid(const void *v, void *out, int64_t batch, int 
                 while (lpc > 1 && (lines + lpc - 1) / lpc < 2 * nsm) lpc >>= 1;
                 const int thr = ((lpc * tpl + 31) / 32) * 32;
                 const unsigned ctas = (unsigned)((lines + lpc - 1) / lpc);
-                const size_t sh = el * (((2 * L + 16 + 3) & ~3) + (size_t)lpc * L);
+                const size_t sh = el * (((2 * L + 16 + 3) & ~3) + (size_t)lpc * L) +
+                                  sizeof(int64_t) * lpc;  // + line offsets
                 if (dtype == 0)
                     sep_tile_kernel<double, double><<<ctas, thr, sh, st>>>(
                         (const double *)src, (double *)o, batch, g.cells, (int)L, g.stride[ax], ax == 0, lpc);
