@@ -389,7 +389,25 @@ def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
         worker.join()
         raise
     t3 = time.perf_counter()
+    # C-bar / C-min values as their jobs finish, while the pool runs the rest
+    values = {}
+    waiting = [(key, q) for key, q in slot.items()
+               if key[2] in ("cbar", "cmin") and isinstance(q, int)]
+    while waiting:
+        still = []
+        for key, q in waiting:
+            if batch.finished(q):
+                values[key] = batch.value(q)
+            else:
+                still.append((key, q))
+        waiting = still
+        if waiting:
+            if not worker.is_alive():
+                break
+            time.sleep(0.0005)
     worker.get()
+    for key, q in waiting:  # finished as the worker exited
+        values[key] = batch.value(q)
     t4 = time.perf_counter()
     # partial-support C-bar LPs (dense sub-matrices of the copied C-bar)
     if late:
@@ -412,11 +430,12 @@ def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
                 q = slot[(i, b, kind)]
                 if isinstance(q, tuple):
                     v = q[1]
+                    v = v if isinstance(v, Exception) else v[2]
                 elif isinstance(q, Exception):
                     v = q
                 else:
-                    v = batch.result(q)
-                dst.append(v if isinstance(v, Exception) else v[2])
+                    v = values[(i, b, kind)]
+                dst.append(v)
     t5 = time.perf_counter()
     for i in order:
         plans[i].lp_seconds = t4 - t0

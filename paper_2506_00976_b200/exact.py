@@ -278,6 +278,16 @@ class LPBatch:
         except GridotError as exc:
             return exc
 
+    def value(self, q):
+        """Optimal value of job q only (no coupling / duals), or its exception."""
+        st = int(self.status[q])
+        if st == 1:
+            return IterationLimitError(f"pivot cap reached after {int(self.pivots[q])} pivots")
+        if st != 0:
+            return GridotError(f"simplex failed with status {st}")
+        bi, bj, bf = self.out[q][:3]
+        return float(np.sum(bf * self.problems[q].cost[bi, bj]))
+
     def basis(self, q):
         """Final basis (bi, bj, bf) of job q, None if it failed."""
         return self.out[q][:3] if int(self.status[q]) in (0,) else None
