@@ -32,7 +32,7 @@ from .costs import (centre_cost_cached, centre_cost_table, cost_table, max_sq_of
 from .device import device, pinned_empty, stream, to_dev, to_host, to_host_pinned, torch
 from .errors import DimensionMismatchError, GridotError, NumericOverflowError, \
     ZeroDenominatorError
-from .exact import LPBatch, build_transport_problem, solve_transport_many
+from .exact import LPBatch, TransportProblem, build_transport_problem, solve_transport_many
 from .measures import CoarseningSpec, GridSpec, coarsen_grid, pad_batch, sumpool_batch
 from .reports import BoundReport, signed_root
 
@@ -301,6 +301,7 @@ def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
         for b in range(bt.B):
             full = bool((masses[i][0][b] > 0).all() and (masses[i][1][b] > 0).all())
             prev = -1
+            first = None  # full supports: the chain's problems share masses and supports
             for kind in ("ctil", "cbar", "cmin"):
                 if kind == "ctil" and not need_ctil or kind == "cmin" and not need_cmin:
                     continue
@@ -310,9 +311,16 @@ def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
                     if not full:
                         late.append((i, b))
                         continue
-                    pr = build(i, b, pinned[i][1][b])  # values arrive before release
+                    cost = pinned[i][1][b]  # values arrive before release
                 else:
-                    pr = build(i, b, ctil if kind == "ctil" else cmin)
+                    cost = ctil if kind == "ctil" else cmin
+                if full and first is not None:
+                    pr = TransportProblem(first.supply, first.demand, cost, first.src_index,
+                                          first.dst_index)
+                else:
+                    pr = build(i, b, cost)
+                    if full and not isinstance(pr, Exception):
+                        first = pr
                 if isinstance(pr, Exception):
                     slot[(i, b, kind)] = pr
                     continue
