@@ -48,6 +48,7 @@ __device__ __forceinline__ float fmin3f(float a, float b, float c) {
 }
 
 constexpr int SEPT = 256;  // threads per CTA of sep_tile_kernel
+constexpr int SEP_SPLIT = 2;  // lanes sharing one (line, 8 outputs) tile (2: measured best)
 
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ in,
@@ -93,16 +94,22 @@ __global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ i
         lines[li * L + i] = v;
     }
     __syncthreads();
-    const int t = threadIdx.x;
+    // SEP_SPLIT consecutive lanes split the source range of a (line, 8
+    // outputs) tile: more warps for latency hiding; the parts meet in a
+    // shuffle min
+    const int part = threadIdx.x % SEP_SPLIT, t = threadIdx.x / SEP_SPLIT;
     const int li = t % lpc, tl = t / lpc;
-    if (tl >= tpl) return;
+    const bool live = tl < tpl;
     const int64_t lid = line0 + li;
     const TO *line = lines + li * L;
-    const int j0 = 8 * tl;
+    const int j0 = 8 * (live ? tl : 0);
     TO best[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) best[r] = (TO)INFINITY;
-    for (int i0 = 0; i0 < L; i0 += 8) {
+    const int nch = L / 8;  // chunks of 8 sources, split evenly over the parts
+    const int ib = live ? 8 * (part * nch / SEP_SPLIT) : L;
+    const int ie = live ? 8 * ((part + 1) * nch / SEP_SPLIT) : L;
+    for (int i0 = ib; i0 < ie; i0 += 8) {
         const TO *cp = sq + (i0 - j0 + L);  // squares of d = i0 - j0 - 7 + q, 16-byte aligned
         if constexpr (sizeof(TO) == 4) {
             float vs[8], Lq[16];
@@ -131,7 +138,14 @@ __global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ i
                 }
         }
     }
-    if (lid >= total_lines) return;
+#pragma unroll
+    for (int sh = 1; sh < SEP_SPLIT; sh <<= 1)
+#pragma unroll
+        for (int r8 = 0; r8 < 8; ++r8) {
+            const TO o = __shfl_xor_sync(0xffffffffu, best[r8], sh);
+            best[r8] = o < best[r8] ? o : best[r8];
+        }
+    if (!live || part || lid >= total_lines) return;
     TO *o = out + lbase[li];
 #pragma unroll
     for (int r8 = 0; r8 < 8; ++r8) o[(int64_t)(j0 + r8) * S] = best[r8];
@@ -427,16 +441,16 @@ extern "C" int gdt_ctransform_grid(const void *v, void *out, int64_t batch, int 
         for (int ax = 0; ax < ndim; ++ax) {
             const int64_t L = g.n[ax];
             void *o = bufs[dst];
-            if (L % 8 == 0 && L / 8 <= SEPT) {
+            if (L % 8 == 0 && L / 8 <= SEPT / SEP_SPLIT) {
                 // lines per CTA: fill the CTA, but keep >= 2 CTAs per SM
                 const int tpl = (int)(L / 8);
                 int dev = 0, nsm = 148;
                 cudaGetDevice(&dev);
                 cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
                 const int64_t lines = total / L;
-                int lpc = SEPT / tpl;
+                int lpc = SEPT / (SEP_SPLIT * tpl);  // SEP_SPLIT threads per (line, 8 outputs)
                 while (lpc > 1 && (lines + lpc - 1) / lpc < 2 * nsm) lpc >>= 1;
-                const int thr = ((lpc * tpl + 31) / 32) * 32;
+                const int thr = ((SEP_SPLIT * lpc * tpl + 31) / 32) * 32;
                 const unsigned ctas = (unsigned)((lines + lpc - 1) / lpc);
                 const size_t sh = el * (((2 * L + 16 + 3) & ~3) + (size_t)lpc * L) +
                                   sizeof(int64_t) * lpc;  // + line offsets
