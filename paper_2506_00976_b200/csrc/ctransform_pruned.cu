@@ -384,6 +384,9 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
             const int sx0 = t0 * 8, off = sx0 - xj0;
             const int base = off >= 0 ? off : -off;
             const float *vrow = vb + (int64_t)(t1 * 8) * N0 + sx0;
+            // the next row's potentials are loaded before this row's min-plus
+            float4 v0 = __ldg(reinterpret_cast<const float4 *>(vrow));
+            float4 v1 = __ldg(reinterpret_cast<const float4 *>(vrow) + 1);
             for (int y = 0; y < 8; ++y) {
                 const int ys = t1 * 8 + y;
                 const int dy = ys > yj ? ys - yj : yj - ys;
@@ -397,9 +400,11 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
                     L[4 * c4 + 2] = tt.z;
                     L[4 * c4 + 3] = tt.w;
                 }
-                const float4 v0 = __ldg(reinterpret_cast<const float4 *>(vrow + y * N0));
-                const float4 v1 = __ldg(reinterpret_cast<const float4 *>(vrow + y * N0) + 1);
                 const float vs[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                if (y + 1 < 8) {
+                    v0 = __ldg(reinterpret_cast<const float4 *>(vrow + (y + 1) * N0));
+                    v1 = __ldg(reinterpret_cast<const float4 *>(vrow + (y + 1) * N0) + 1);
+                }
                 if (off >= 0) minplus_row8<false, true>(L, vs, best);
                 else minplus_row8<true, true>(L, vs, best);
             }
