@@ -47,11 +47,16 @@ def fit_seconds(xs, xt, mu, nu, ns, nt, sweeps, scratch, f, g, info, st, p, eps)
 
 
 def main():
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sides", default="64,128,256")
+    args = ap.parse_args()
     t = torch()
     from paper_2506_00976_b200.device import device
 
     device()
-    for side in (64, 128, 256):
+    for side in (int(x) for x in args.sides.split(",")):
         dims = (side, side)
         grid = G.GridSpec(dims)
         n = grid.cell_count
