@@ -112,8 +112,17 @@ __global__ void __launch_bounds__(EN_T) en_row_kernel(const double *__restrict__
     for (int64_t i = (int64_t)blockIdx.x * (EN_T / 32) + wib; i < ns;
          i += (int64_t)gridDim.x * (EN_T / 32)) {
         const double *row = K + i * nt;
-        double s = 0.0;
-        for (int64_t j = lane; j < nt; j += 32) s += row[j] * b[j];
+        // four independent partial sums per lane keep four loads in flight
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int64_t j = lane;
+        for (; j + 96 < nt; j += 128) {
+            s0 += row[j] * b[j];
+            s1 += row[j + 32] * b[j + 32];
+            s2 += row[j + 64] * b[j + 64];
+            s3 += row[j + 96] * b[j + 96];
+        }
+        for (; j < nt; j += 32) s0 += row[j] * b[j];
+        double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) {
