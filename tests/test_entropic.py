@@ -164,3 +164,24 @@ def test_device_full_size_brackets_quantization_bounds():
     qhi = min(q["weighted_cost"].value, q["primal_upscaling"].value)
     assert lo.value <= up.value
     assert lo.value <= qhi * (1 + 1e-9) and qlo <= up.value * (1 + 1e-9)
+
+
+@pytest.mark.gpu
+def test_device_kernel_cap_size():
+    """The reference's cap (2^16 cells, a 34 GB fp64 kernel) on one B200:
+    256 x 256, p = 2.  No CPU oracle at this size; the bounds must bracket
+    the quantization bracket's overlap."""
+    from paper_2506_00976_b200 import synthetic as S
+
+    dims = (256, 256)
+    mu, nu = S.measure(4, 0, 0), S.measure(4, 0, 1)
+    grid = G.GridSpec(dims)
+    a, b = G.GridMeasure(grid, mu), G.GridMeasure(grid, nu)
+    params = G.RegularizationParams(0.02 * 256 ** 2, max_iter=200)
+    lo = G.reg_lower_bound(a, b, _grid_cost(grid, 2.0), params)
+    up = G.reg_upper_bound(a, b, _grid_cost(grid, 2.0), params)
+    q = G.quantized_bounds(mu[None], nu[None], dims, 8, 2.0)[0]
+    qlo = max(q["min_cost"].value, q["dual_upscaling"].value)
+    qhi = min(q["weighted_cost"].value, q["primal_upscaling"].value)
+    assert 0.0 <= lo.value <= up.value
+    assert lo.value <= qhi * (1 + 1e-9) and qlo <= up.value * (1 + 1e-9)
