@@ -223,36 +223,62 @@ def run_b200(args):
     names = ("pool", "cbar", "primal", "dual_prep", "ct_target", "ct_source")
     launches_per_step = 0
 
-    def step(events):
+    # the (kappa, p) combinations are independent: each runs on its own
+    # stream, forked from and joined back into the current one, so the
+    # latency-bound small kernels of one overlap the big ones of another
+    streams = [torch.cuda.Stream() for _ in stages]
+
+    def step(events, concurrent=True):
         nonlocal launches_per_step
         launches = 0
+        events[-1][0].record(cur)  # step start
         for ci, (k, p, bt, dp) in enumerate(stages):
             ev = events[ci]
-            ev[0].record(cur)
+            if not concurrent:  # stage timing pass: everything on one stream
+                launches += combo(ci, k, p, bt, dp, ev, cur)
+                continue
+            sc = streams[ci]
+            sc.wait_stream(cur)
+            with torch.cuda.stream(sc):
+                launches += combo(ci, k, p, bt, dp, ev, sc)
+        for sc in streams if concurrent else ():
+            cur.wait_stream(sc)
+        events[-1][1].record(cur)  # step end
+        launches_per_step = launches
+
+    def combo(ci, k, p, bt, dp, ev, sc):
+        launches = 0
+        if True:
+            ev[0].record(sc)
             bt.pool()
             launches += 2 + (0 if bt.pdims == bt.dims else 2)
-            ev[1].record(cur)
+            ev[1].record(sc)
             E._cbar(bt)
-            launches += 3 if bt.p == 2.0 else 1  # moments x2 + C-bar, or one C-bar kernel
-            ev[2].record(cur)
+            # moments x2 + C-bar (p = 2); fp32 diag C-bar: nu pad, 2 reciprocals + C-bar
+            launches += 3 if bt.p == 2.0 else (4 if bt.mode == 1 else 1)
+            ev[2].record(sc)
             E.launch_primal(bt, dp, wl.max_iter)
             # ipf_fast + TV/moments + pricing + finish (fp32 mode); the exact
             # path adds two arc-coordinate packs and the block map
             launches += (4 if bt.mode == 1 else 7) + (0 if bt.p == 2.0 else 1)  # + arc rows
-            ev[3].record(cur)
+            ev[3].record(sc)
             E.launch_dual_prep(bt, dp)
             launches += 2
-            ev[4].record(cur)
+            ev[4].record(sc)
             E.launch_ctransform(bt, dp, 0)
-            ev[5].record(cur)
+            ev[5].record(sc)
             E.launch_ctransform(bt, dp, 1)
-            ev[6].record(cur)
-            per_ct = (bt.d + 1) if bt.p == 2.0 else (3 if dp.dt == 1 else 2)
-            launches += 2 * per_ct
-        launches_per_step = launches
+            ev[6].record(sc)
+            # separable passes + dot (p = 2); fp32 pruned: cost table, tile max,
+            # pruned kernel, dot, plus one f64->f32 conversion of f_hat
+            per_ct = (bt.d + 1) if bt.p == 2.0 else (4 if dp.dt == 1 else 2)
+            launches += 2 * per_ct + (1 if bt.p != 2.0 and dp.dt == 1 else 0)
+        return launches
 
     def new_events():
-        return [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in stages]
+        # per combo: 7 stage boundaries on its stream; last entry: step start / end
+        return [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in stages] + \
+            [[torch.cuda.Event(enable_timing=True) for _ in range(2)]]
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -277,6 +303,23 @@ def run_b200(args):
         dist.barrier()
     clk = clocks.stop()
 
+    # per-kernel stage times come from an untimed serial pass (one stream, the
+    # same flushed-L2 steps): under the concurrent schedule a stage's events
+    # would include the kernels of the other combinations running beside it
+    conc_out = [(dp.prim_out.clone(), dp.dots.clone()) for _, _, _, dp in stages]
+    step(new_events(), concurrent=False)  # warm the current stream's allocator pool
+    serial_events = []
+    for _ in range(args.steps):
+        flush.zero_()
+        ev = new_events()
+        step(ev, concurrent=False)
+        serial_events.append(ev)
+    torch.cuda.synchronize()
+    serial_ms = statistics.mean(ev[-1][0].elapsed_time(ev[-1][1]) for ev in serial_events)
+    # the concurrent schedule must not change a single bit of the outputs
+    streams_match = all(torch.equal(a, dp.prim_out) and torch.equal(b, dp.dots)
+                        for (a, b), (_, _, _, dp) in zip(conc_out, stages))
+
     # kernels of one step, counted exactly by the CUDA activity profiler on an
     # extra (untimed) step; the hand count of step() is the fallback
     try:
@@ -287,18 +330,23 @@ def run_b200(args):
             torch.cuda.synchronize()
         counted = sum(1 for e in prof.events()
                       if e.device_type.name == "CUDA" and "gdt::" in e.name)
+        if os.environ.get("GDT_BENCH_LAUNCHES"):
+            import collections
+            cnt = collections.Counter(e.name for e in prof.events()
+                                      if e.device_type.name == "CUDA" and "gdt::" in e.name)
+            print(f"launches: hand {launches_per_step} profiler {counted}: {dict(cnt)}",
+                  file=sys.stderr)
         if counted > 0:
             launches_per_step = counted
     except Exception as exc:  # profiler unavailable: keep the hand count
         print(f"launch count: profiler unavailable ({exc}); using the hand count",
               file=sys.stderr)
-    step_ms = [sum(ev[ci][0].elapsed_time(ev[ci][6]) for ci in range(len(stages)))
-               for ev in all_events]
+    step_ms = [ev[-1][0].elapsed_time(ev[-1][1]) for ev in all_events]
     stage_ms = {}  # (combo, stage) -> mean ms
     for ci, (k, p, _, _) in enumerate(stages):
         for si, nm in enumerate(names):
             stage_ms[(k, p, nm)] = statistics.mean(
-                ev[ci][si].elapsed_time(ev[ci][si + 1]) for ev in all_events)
+                ev[ci][si].elapsed_time(ev[ci][si + 1]) for ev in serial_events)
     ms = statistics.mean(step_ms)
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -422,6 +470,10 @@ def run_b200(args):
                    "l2": "flushed (256 MB write) between timed steps",
                    "lp": "coarse LP plans precomputed on the host (timed in e2e)",
                    "setup_s": t_setup,
+                   "streams": "one CUDA stream per (kappa, p) combination, forked from and "
+                              "joined into the timed stream; stage_ms from a serial pass",
+                   "serial_ms_per_step": round(serial_ms, 4),
+                   "streams_match_serial": streams_match,
                    "stage_ms": {f"k{k}_p{p:g}_{nm}": round(v, 4)
                                 for (k, p, nm), v in sorted(stage_ms.items())}},
         "roofline": rl, "roofline_ipf": ipf_roof, "roofline_ctransform": ct_roof, "clocks": clk,
