@@ -228,7 +228,7 @@ def run_b200(args):
     # latency-bound small kernels of one overlap the big ones of another
     streams = [torch.cuda.Stream() for _ in stages]
 
-    def step(events, concurrent=True):
+    def step(events, concurrent=len(stages) > 1):  # one combination: nothing to overlap
         nonlocal launches_per_step
         launches = 0
         events[-1][0].record(cur)  # step start
@@ -470,8 +470,9 @@ def run_b200(args):
                    "l2": "flushed (256 MB write) between timed steps",
                    "lp": "coarse LP plans precomputed on the host (timed in e2e)",
                    "setup_s": t_setup,
-                   "streams": "one CUDA stream per (kappa, p) combination, forked from and "
-                              "joined into the timed stream; stage_ms from a serial pass",
+                   "streams": ("one CUDA stream per (kappa, p) combination, forked from and "
+                               "joined into the timed stream; stage_ms from a serial pass")
+                              if len(stages) > 1 else "one stream",
                    "serial_ms_per_step": round(serial_ms, 4),
                    "streams_match_serial": streams_match,
                    "stage_ms": {f"k{k}_p{p:g}_{nm}": round(v, 4)

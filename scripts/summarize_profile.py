@@ -82,8 +82,9 @@ def main():
     bench = json.load(open(sys.argv[4])) if len(sys.argv) > 4 else None
     agg = launches(lpath)
     tot = sum(v[0] for v in agg.values())
-    lines = ["# ncu evidence", "", f"Launch list: `{lpath}` (one warm-up + one timed step of "
-             "`bench.py`, cold and serialised under ncu: compare shares).", "",
+    lines = ["# ncu evidence", "", f"Launch list: `{lpath}` (every step of `bench.py "
+             "--steps 1 --warmup 1`: warm-up, timed, the serial stage-timing pass and the "
+             "launch-count step; cold and serialised under ncu: compare shares).", "",
              "| kernel | launches | total us | avg us | share |", "|---|---|---|---|---|"]
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:25]:
         lines.append(f"| `{k}` | {v[1]} | {v[0] / 1e3:.1f} | {v[0] / 1e3 / v[1]:.1f} | "
