@@ -231,20 +231,27 @@ def run_b200(args):
     def step(events, concurrent=len(stages) > 1):  # one combination: nothing to overlap
         nonlocal launches_per_step
         launches = 0
-        events[-1][0].record(cur)  # step start
+        base = torch.cuda.current_stream()  # the capture stream under graph capture
+        events[-1][0].record(base)  # step start
         for ci, (k, p, bt, dp) in enumerate(stages):
             ev = events[ci]
             if not concurrent:  # stage timing pass: everything on one stream
-                launches += combo(ci, k, p, bt, dp, ev, cur)
+                launches += combo(ci, k, p, bt, dp, ev, base)
                 continue
             sc = streams[ci]
-            sc.wait_stream(cur)
+            sc.wait_stream(base)
             with torch.cuda.stream(sc):
                 launches += combo(ci, k, p, bt, dp, ev, sc)
         for sc in streams if concurrent else ():
-            cur.wait_stream(sc)
-        events[-1][1].record(cur)  # step end
+            base.wait_stream(sc)
+        events[-1][1].record(base)  # step end
         launches_per_step = launches
+
+    class _NoEvent:
+        def record(self, stream=None):
+            pass
+
+    no_events = [[_NoEvent()] * 7 for _ in stages] + [[_NoEvent()] * 2]
 
     def combo(ci, k, p, bt, dp, ev, sc):
         launches = 0
@@ -286,6 +293,31 @@ def run_b200(args):
         step(new_events())
     torch.cuda.synchronize()
 
+    # the whole step (all combinations, fork and join included) as one CUDA
+    # graph: replays the same launches on the same buffers without the
+    # per-launch host cost (ctypes argument marshalling + cudaLaunchKernel)
+    graph, graph_note = None, "off (--no-graph)"
+    if not args.no_graph:
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step(no_events)
+            g.replay()
+            torch.cuda.synchronize()
+            graph, graph_note = g, "one CUDA graph per step (captured after warm-up)"
+        except Exception as exc:  # capture unsupported: time the eager launches
+            graph_note = f"capture failed, eager launches ({type(exc).__name__}: {exc})"[:200]
+            print(f"bench: {graph_note}", file=sys.stderr)
+            torch.cuda.synchronize()
+
+    def timed_step(ev):
+        if graph is None:
+            step(ev)
+            return
+        ev[-1][0].record(cur)
+        graph.replay()
+        ev[-1][1].record(cur)
+
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
@@ -296,7 +328,7 @@ def run_b200(args):
     for _ in range(args.steps):
         flush.zero_()  # L2 flush (> 126 MB) between timed steps, outside the events
         ev = new_events()
-        step(ev)
+        timed_step(ev)
         all_events.append(ev)
     torch.cuda.synchronize()
     if world > 1:
@@ -473,6 +505,7 @@ def run_b200(args):
                    "streams": ("one CUDA stream per (kappa, p) combination, forked from and "
                                "joined into the timed stream; stage_ms from a serial pass")
                               if len(stages) > 1 else "one stream",
+                   "graph": graph_note,
                    "serial_ms_per_step": round(serial_ms, 4),
                    "streams_match_serial": streams_match,
                    "stage_ms": {f"k{k}_p{p:g}_{nm}": round(v, 4)
@@ -555,6 +588,7 @@ def main():
                     help="BASELINE.json config (3 = the headline 128x128 workload)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches, no CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
