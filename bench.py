@@ -14,8 +14,9 @@ plans precomputed (the LP stays on the host by design and is timed in
 `e2e`).  `e2e` = the same pairs through the public API
 (``quantized_bounds``) from pinned host buffers, host LPs included.
 
-`--impl reference` times the CPU oracle (oracle/port.py, a restatement of
-the reference package, with its C simplex) on all host cores.
+`--impl reference` times the stock reference package (gridot's own four bound
+functions and numba simplex, staged byte-identical and sha256-verified in
+oracle/_ref/ by build()) on all host cores, on the same seeded pairs.
 """
 
 from __future__ import annotations
@@ -101,9 +102,16 @@ class ClockSampler:
 
 
 def _oracle_pair(args):
-    """One pair, all four combos, all four bounds -- the reference's own algorithm."""
-    cfg, pair, combos = args
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    """One pair, all its combos, all four bounds -- the reference's own algorithm.
+
+    kind "reference": the stock reference package (oracle/_ref/gridot, staged
+    byte-identical by build(), sha256-verified, numba simplex); kind "port":
+    the oracle's numpy restatement (used only if the staged copy is absent)."""
+    cfg, pair, combos, kind = args
+    if kind == "reference":
+        from oracle import ref_stock
+
+        return ref_stock.pair_bounds(cfg, pair, combos)[0]
     from oracle import port as P
     from paper_2506_00976_b200 import synthetic as S
 
@@ -123,18 +131,56 @@ def _pool_ctx():
     return mp.get_context("fork")
 
 
-def cpu_oracle_sample(cfg, n_pairs, workers, first_pair=0):
-    """Wall time of n_pairs oracle pairs on `workers` processes."""
+def cpu_kind():
+    """("reference", note) when the staged stock reference verifies, else ("port", why)."""
+    from oracle import ref_stock
+
+    try:
+        ref_stock.verify()
+    except ref_stock.ReferenceUnavailable as exc:
+        return "port", str(exc)
+    # JIT the numba simplex once in the parent (fork inherits it), untimed
+    return "reference", f"stock gridot (sha256-pinned copy), numba warm-up {ref_stock.warm_up():.1f} s"
+
+
+def cpu_sample(cfg, pairs, workers, kind):
+    """Wall time of the given pairs (all combos each) on `workers` processes."""
     from paper_2506_00976_b200 import synthetic as S
 
     combos = S.WORKLOADS[cfg].combos
     ctx = _pool_ctx()
     with ctx.Pool(workers) as pool:
         t0 = time.perf_counter()
-        per = pool.map(_oracle_pair, [(cfg, first_pair + i, combos) for i in range(n_pairs)],
-                       chunksize=1)
+        per = pool.map(_oracle_pair, [(cfg, i, combos, kind) for i in pairs], chunksize=1)
         wall = time.perf_counter() - t0
     return wall, per
+
+
+def measure_peaks(torch, N, stream, cur):
+    """FP32 / FP64 CUDA-core peaks measured live (csrc/probes.cu): 148 x 8
+    CTAs of 8 independent FMA chains per thread; best of 3 launches each."""
+    sink = torch.empty(1, dtype=torch.float32, device="cuda")
+    blocks, out = 148 * 8, {}
+    for name, kind, iters in (("ffma", 0, 256), ("ffma2", 1, 128), ("dfma", 2, 256)):
+        N.check(N.lib().gdt_probe_peak(kind, blocks, 8, N.ptr(sink), stream()), "probe")
+        best = None
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cur)
+            N.check(N.lib().gdt_probe_peak(kind, blocks, iters, N.ptr(sink), stream()), "probe")
+            e1.record(cur)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        out[f"{name}_tflops"] = N.lib().gdt_probe_flops(kind, blocks, iters) / (best / 1e3) / 1e12
+    out["fp32_tflops"] = max(out["ffma_tflops"], out["ffma2_tflops"])
+    out["fp64_tflops"] = out["dfma_tflops"]
+    return out
+
+
+def _ref_pairs(step, cores, total):
+    """Pairs of CPU step `step`: the GPU arm's own seeds (pairs 0..total-1), in turn."""
+    return [(step * cores + i) % total for i in range(cores)]
 
 
 # ---------------------------------------------------------------------------
@@ -146,40 +192,152 @@ def run_reference(args):
     rank, world, _ = _env_rank()
     if rank != 0:
         return 0
+    from paper_2506_00976_b200 import synthetic as S
+
+    cfg = args.config
+    wl = S.WORKLOADS[cfg]
+    total = args.pairs or (45 if cfg == 4 else wl.pairs)
     cores = os.cpu_count() or 1
-    # W warm-up steps on one small pair per worker (import + first-touch), then
-    # K steps, each one pair per core through all four combos of config 3
+    kind, note = cpu_kind()
     ctx = _pool_ctx()
+    # W warm-up steps (one small config-1 pair per worker: imports, first
+    # touch, numba cache load), then K steps of one benched pair per core
+    # through every (kappa, p) combination and all four bounds
     with ctx.Pool(cores) as pool:
         for _ in range(args.warmup):
-            pool.map(_oracle_pair, [(1, 0, ((4, 2.0),))] * cores, chunksize=1)
-        times = []
+            pool.map(_oracle_pair, [(1, 0, ((4, 2.0),), kind)] * cores, chunksize=1)
+        times, per = [], []
         for s in range(args.steps):
             t0 = time.perf_counter()
-            pool.map(_oracle_pair, [(CFG, 1000 + s * cores + i,
-                                     ((4, 1.0), (4, 2.0), (8, 1.0), (8, 2.0)))
-                                    for i in range(cores)], chunksize=1)
+            per += pool.map(_oracle_pair, [(cfg, i, wl.combos, kind)
+                                           for i in _ref_pairs(s, cores, total)], chunksize=1)
             times.append(time.perf_counter() - t0)
     ms = 1000.0 * statistics.mean(times)
     value = cores / (ms / 1000.0)
+    sample = (f"{cores} cfg{cfg} pairs per step (one per core; seeds = the GPU arm's pairs "
+              f"0..{total - 1}), all {len(wl.combos)} (kappa, p) x 4 bounds; "
+              f"{statistics.mean(per):.1f} s per pair per core")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg3: 128x128 smooth random fields, kappa{4,8} x p{1,2}, "
-                               "4 quantization bounds", "pairs_per_step": cores,
-                   "parallelism": f"{cores} host processes"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{cores} cfg3 pairs per step (one per core), all 4 combos"},
+        "impl": "reference", "metric": _metric(cfg, wl), "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": _workload(cfg, wl, total), "pairs_per_step": cores,
+                   "parallelism": f"{cores} host processes", "same_config": True},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample, "source": note},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def _metric(cfg, wl):
+    if cfg == 3:
+        return METRIC
+    return (f"pairs/sec for the four quantization bounds, BASELINE config {cfg} "
+            f"({'x'.join(map(str, wl.dims))}, combos {list(wl.combos)})")
+
+
+def _workload(cfg, wl, ppr):
+    if cfg == 3:
+        return ("cfg3: 45 pairs/GPU of 128x128 smooth random fields; kappa in {4,8} x p in "
+                "{1,2}; 4 quantization bounds; " + wl.precision + " mode")
+    return (f"cfg{cfg}: {ppr} pairs/GPU of {wl.kind} on {'x'.join(map(str, wl.dims))}; "
+            f"{wl.precision} mode; max_iter {wl.max_iter}")
+
+
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
+
+
+def run_e2e(args, torch, dist, G, S, wl, prec, combos, dims, Nf, ppr, rank, world, mus_h, nus_h):
+    """The same job through the public API, from pinned host buffers, host LPs
+    included.  One call per step for all (kappa, p) combinations
+    (quantized_bounds_many: masses uploaded once, every combination's coarse
+    LPs on one host thread pool).  Under torchrun the job is the global batch
+    of ppr * world pairs through distributed_bounds_many: each rank computes
+    its contiguous shard, and one NCCL all_gather collects the per-pair
+    bound records on every rank.  Each rank gets cores // world host threads
+    for its LPs, so the host's LP capacity is the e2e ceiling at any N."""
+    from paper_2506_00976_b200 import distributed as D
+
+    lp_threads = max(1, (os.cpu_count() or 1) // world)
+    total = ppr * world
+    lo, hi = rank * ppr, (rank + 1) * ppr
+    if world > 1:
+        # global host arrays; this rank fills (and reads) its own shard only
+        g_mu = torch.zeros((total, Nf), dtype=torch.float64).pin_memory()
+        g_nu = torch.zeros((total, Nf), dtype=torch.float64).pin_memory()
+        g_mu[lo:hi] = torch.from_numpy(mus_h)
+        g_nu[lo:hi] = torch.from_numpy(nus_h)
+        assert D.shard_range(total, rank, world) == (lo, hi)
+    else:
+        g_mu = torch.from_numpy(mus_h).pin_memory()
+        g_nu = torch.from_numpy(nus_h).pin_memory()
+    kw = dict(precision=prec, xi=wl.xi, max_iter=wl.max_iter, lp_threads=lp_threads)
+
+    def call(timings=None):
+        if world > 1:
+            return D.distributed_bounds_many(g_mu, g_nu, dims, combos, timings=timings, **kw)
+        res = G.quantized_bounds_many(g_mu, g_nu, dims, combos, timings=timings, **kw)
+        return res, None
+
+    call()  # untimed warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times, parts, table = [], {}, None
+    for _ in range(args.e2e_steps):
+        tm = {}
+        t0 = time.perf_counter()
+        res, table = call(tm)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        for key, val in tm.items():
+            if isinstance(val, float):
+                parts[key] = parts.get(key, 0.0) + val
+    if world == 1:
+        for key in res:
+            assert all(not isinstance(r[m], Exception) for r in res[key] for m in r)
+    e2e_s = statistics.mean(times)
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = 2 * ppr * Nf * 8
+    d2h = sum(ppr * ((Nf // k ** len(dims)) ** 2 * 8 + 2 * (Nf // k ** len(dims)) * 8 + 80)
+              for k, _ in combos)
+    out = {"value": total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "bytes_note": "per rank (its shard's masses up; C-bar, "
+           "coarse masses and per-pair results down)",
+           "s_per_step": e2e_s, "steps": args.e2e_steps,
+           "s_per_step_stats": {"mean": statistics.mean(times), "min": min(times),
+                                "max": max(times),
+                                "stdev": statistics.stdev(times) if len(times) > 1 else 0.0},
+           "host_cores": os.cpu_count(), "lp_threads_per_rank": lp_threads,
+           "breakdown_s": {k: round(v / args.e2e_steps, 4) for k, v in parts.items()},
+           "note": ("distributed_bounds_many: contiguous pair shards, one NCCL all_gather of "
+                    "per-pair records" if world > 1 else "public API quantized_bounds_many") +
+                   " (all combos, one call per step) from pinned host memory; includes 3 host "
+                   "LPs per pair per combo on the rank's host cores"}
+    if world > 1:
+        # the gathered table must equal the table of ONE process computing the
+        # whole global batch (rank 0, all host cores, untimed), bit for bit
+        ok = torch.zeros(1, device="cuda")
+        if rank == 0:
+            a_mu, a_nu = S.batch(CFG, 0, total)
+            whole = G.quantized_bounds_many(a_mu, a_nu, dims, combos, precision=prec, xi=wl.xi,
+                                            max_iter=wl.max_iter)
+            ref = np.stack([D.pack_records(whole[(int(k), float(p))], 0) for k, p in combos])
+            same = np.array_equal(np.delete(ref, D._IDX["wall_time"], axis=2),
+                                  np.delete(table, D._IDX["wall_time"], axis=2), equal_nan=True)
+            ok[0] = 1.0 if same else 0.0
+        dist.broadcast(ok, 0)
+        out["gather_matches_single_process"] = bool(ok.item() == 1.0)
+        out["gathered_pairs"] = int(table.shape[1])
+    return out
 
 
 def run_b200(args):
@@ -189,6 +347,9 @@ def run_b200(args):
     rank, world, local = _env_rank()
     torch.cuda.set_device(local)
     if world > 1:
+        # communicator init lines (rank count, transport) on stderr for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2506_00976_b200 as G
     from paper_2506_00976_b200 import _native as N
@@ -199,6 +360,7 @@ def run_b200(args):
     global CFG
     CFG = args.config
     wl = S.WORKLOADS[CFG]
+    prec = args.precision or wl.precision
     ppr = args.pairs or (45 if CFG == 4 else wl.pairs)  # cfg4: 360 pairs = 45 per GPU x 8
     lo = rank * ppr
     mus_h, nus_h = S.batch(CFG, lo, lo + ppr)
@@ -212,7 +374,7 @@ def run_b200(args):
     stages = []
     t_setup = time.perf_counter()
     for k, p in combos:
-        bt = E.make_batch(mus, nus, dims, k, p, wl.precision)
+        bt = E.make_batch(mus, nus, dims, k, p, prec)
         plans = E.prepare_coarse(bt, E.QUANT_METHODS, lp_threads=0)
         dp = E.DevicePlans(bt, plans, None, wl.xi)
         stages.append((k, p, bt, dp))
@@ -387,22 +549,14 @@ def run_b200(args):
     value = ppr * world / (ms / 1000.0)
 
     # ---- roofline of the dominant kernel --------------------------------
-    sink = torch.empty(1, dtype=torch.float32, device="cuda")
-    iters = 4096
-    blocks = 148 * 8
-    N.check(N.lib().gdt_probe_fp32(blocks, 64, N.ptr(sink), stream()), "probe")
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(cur)
-    N.check(N.lib().gdt_probe_fp32(blocks, iters, N.ptr(sink), stream()), "probe")
-    e1.record(cur)
-    torch.cuda.synchronize()
-    fp32_probe = 2.0 * blocks * 256 * 8 * iters / (e0.elapsed_time(e1) / 1000.0) / 1e12
-    # denominator: the nominal FP32 CUDA-core rate at the SM clock sampled under
-    # load (SMs x 128 FMA lanes x 2 FLOP x f); the FFMA probe is reported beside it
+    probes = measure_peaks(torch, N, stream, cur)
+    fp32_peak = probes["fp32_tflops"]
     sms = torch.cuda.get_device_properties(local).multi_processor_count
-    fp32_peak = sms * 128 * 2.0 * float(clk.get("sm_mhz") or 1965.0) * 1e6 / 1e12
-    peak_src = (f"nominal {sms} SMs x 128 FP32 lanes x 2 at the sampled {clk.get('sm_mhz')} MHz; "
-                f"FFMA probe measured {fp32_probe:.1f} TFLOP/s")
+    nominal = sms * 128 * 2.0 * float(clk.get("sm_mhz") or 1965.0) * 1e6 / 1e12
+    peak_src = (f"measured: max of the FFMA ({probes['ffma_tflops']:.1f}) and packed FFMA2 "
+                f"({probes['ffma2_tflops']:.1f}) probes (gdt_probe_peak, this run, kernel timed "
+                f"alone); nominal {sms} SMs x 128 lanes x 2 at {clk.get('sm_mhz')} MHz = "
+                f"{nominal:.1f}")
     dom = max(stage_ms.items(), key=lambda kv: kv[1])
     (dk, dpow, dname), dms = dom
     n_c = Nf // dk ** len(dims)
@@ -455,11 +609,11 @@ def run_b200(args):
     # every sweep (16 B per cell and sweep; the ncu DRAM traffic is in profiles/).
     ipf_bytes = (48.0 * sweeps + 32.0) * Nf * ppr
     bytes_model = "(48*S + 32) * N^d bytes per pair (SURVEY.md 8(d))"
-    ipf_roof = {"bound": "hbm", "kernel": ("ipf_fast_kernel" if wl.precision == "fp32" else
+    ipf_roof = {"bound": "hbm", "kernel": ("ipf_fast_kernel" if prec == "fp32" else
                                            "ipf_kernel") + " + moments_tv + price (primal stage)",
                 "achieved": ipf_bytes / (prim_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
                 "frac": ipf_bytes / (prim_ms / 1000.0) / 1e9 / hbm,
-                "traffic": traffic("ipf_fast_kernel") if wl.precision == "fp32" else None,
+                "traffic": traffic("ipf_fast_kernel") if prec == "fp32" else None,
                 "traffic_source": tsrc, "sweeps": sweeps,
                 "work": bytes_model + "; stage time includes pricing"}
 
@@ -485,17 +639,15 @@ def run_b200(args):
                                                          "unit": "GB/s", "frac": None,
                                                          "traffic": None}
     line = {
-        "metric": METRIC if CFG == 3 else
-        f"pairs/sec for the four quantization bounds, BASELINE config {CFG} "
-        f"({'x'.join(map(str, dims))}, combos {list(combos)})",
-        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "fp32+f64",
-        "data": "synthetic (seeded smooth random fields, BASELINE.json config 3)",
-        "config": {"workload": ("cfg3: 45 pairs/GPU of 128x128 smooth random fields; "
-                                "kappa in {4,8} x p in {1,2}; 4 quantization bounds; fp32 mode")
-                   if CFG == 3 else f"cfg{CFG}: {ppr} pairs/GPU of {wl.kind} on "
-                   f"{'x'.join(map(str, dims))}; {wl.precision} mode; max_iter {wl.max_iter}",
+        "metric": _metric(CFG, wl),
+        "value": value if streams_match else None, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32+f64" if prec == "fp32" else "f64",
+        "data": f"synthetic (seeded {wl.kind}, BASELINE.json config {CFG})",
+        "config": {"workload": _workload(CFG, wl, ppr).replace(wl.precision + " mode",
+                                                                prec + " mode"),
+                   "precision": prec,
                    "pairs_per_gpu": ppr, "global_pairs": ppr * world, "grid": list(dims),
                    "combos": [list(c) for c in combos],
                    "parallelism": f"dp{world} (pairs sharded, no data-path collective)",
@@ -511,69 +663,36 @@ def run_b200(args):
                    "stage_ms": {f"k{k}_p{p:g}_{nm}": round(v, 4)
                                 for (k, p, nm), v in sorted(stage_ms.items())}},
         "roofline": rl, "roofline_ipf": ipf_roof, "roofline_ctransform": ct_roof, "clocks": clk,
+        "peaks_measured": {k: round(v, 2) for k, v in probes.items()},
         "gpu_launches": launches_per_step * args.steps,
     }
 
     # ---- e2e through the public API with host buffers --------------------
     if not args.no_e2e:
-        # each rank gets its own slice of the host cores for its LPs
-        lp_threads = max(1, (os.cpu_count() or 1) // world)
-        pin_mu = torch.from_numpy(mus_h).pin_memory()
-        pin_nu = torch.from_numpy(nus_h).pin_memory()
-        h2d = d2h = 0
-        # one public-API call per step for all (kappa, p) combinations: the
-        # masses go up once and the coarse LPs of every combination share one
-        # host thread pool (quantized_bounds_many)
-        G.quantized_bounds_many(pin_mu, pin_nu, dims, combos, precision=wl.precision, xi=wl.xi,
-                                max_iter=wl.max_iter, lp_threads=lp_threads)  # untimed warm-up
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        parts = {}
-        for _ in range(args.e2e_steps):
-            tm = {}
-            res = G.quantized_bounds_many(pin_mu, pin_nu, dims, combos, precision=wl.precision,
-                                          xi=wl.xi, max_iter=wl.max_iter, timings=tm,
-                                          lp_threads=lp_threads)
-            for key, val in tm.items():
-                if isinstance(val, float):
-                    parts[key] = parts.get(key, 0.0) + val
-            h2d += 2 * ppr * Nf * 8
-            for k, p in combos:
-                n_c = Nf // k ** len(dims)
-                d2h += ppr * (n_c * n_c * 8 + 2 * n_c * 8 + 8 * 8 + 2 * 8)
-                reps = res[(k, float(p))]
-                assert all(not isinstance(r[m], Exception) for r in reps for m in r)
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        line["e2e"] = {"value": ppr * world / e2e_s, "unit": UNIT,
-                       "h2d_bytes_per_step": h2d // args.e2e_steps,
-                       "d2h_bytes_per_step": d2h // args.e2e_steps,
-                       "s_per_step": e2e_s, "host_cores": os.cpu_count(),
-                       "lp_threads_per_rank": lp_threads,
-                       "breakdown_s": {k: round(v / args.e2e_steps, 4) for k, v in parts.items()},
-                       "note": "public API quantized_bounds_many (all combos, one call per "
-                               "step) from pinned host memory; includes 3 host LPs per pair "
-                               "per combo on the rank's host cores"}
+        line["e2e"] = run_e2e(args, torch, dist, G, S, wl, prec, combos, dims, Nf, ppr, rank,
+                              world, mus_h, nus_h)
 
     # ---- CPU baseline (rank 0, N=1 only) --------------------------------
     if world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        wall, per = cpu_oracle_sample(CFG, cores, cores, first_pair=1000)
+        kind, note = cpu_kind()
+        wall, per = cpu_sample(CFG, _ref_pairs(0, cores, ppr), cores, kind)
         line["cpu_baseline"] = {
-            "value": cores / wall, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{cores} cfg3 pairs (one per core, all 4 combos x 4 bounds); "
+            "value": cores / wall, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{cores} cfg{CFG} pairs = the first {cores} benched pairs (one per core, "
+                      f"all {len(combos)} combos x 4 bounds); "
                       f"{statistics.mean(per):.1f} s per pair per core",
+            "source": note,
         }
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if not streams_match:
+        # a broken stream or graph schedule must not publish a headline number
+        print("bench: concurrent/graph outputs differ from the serial pass; value withheld",
+              file=sys.stderr)
+        return 1
     return 0
 
 
@@ -586,7 +705,9 @@ def main():
     ap.add_argument("--pairs", type=int, default=0, help="pairs per GPU (default: the config's)")
     ap.add_argument("--config", type=int, default=3, choices=(1, 2, 3, 4, 5),
                     help="BASELINE.json config (3 = the headline 128x128 workload)")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--precision", choices=("fp64", "fp32"), default=None,
+                    help="override the config's precision mode (cfg3 default: fp32)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches, no CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")

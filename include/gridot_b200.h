@@ -88,7 +88,7 @@ int gdt_sumpool_f64(const double *fine, double *coarse, int64_t batch, int ndim,
  *   centre_cost   [n, n]       C-tilde (costs.py:121-125), shared by the batch
  *   cost_table    [max_sq+1]   rho^p of integer squared distance, required
  *                              when p is neither 1 nor 2 (NULL otherwise)
- *   out           [batch, n, n], unused [batch, n, n] (uint8)
+ *   out           [batch, n, n], unused [batch, n, n] (uint8; NULL skips the mask)
  * mode GDT_MODE_EXACT reproduces the reference's rounding order exactly;
  * GDT_MODE_FAST uses block moments for p == 2 (fp64) and fp32 FFMA tiles
  * otherwise. */
@@ -218,9 +218,17 @@ int gdt_ctransform_points(const double *xs, const double *xt, int64_t ns, int64_
 int gdt_batched_dot(const double *a, const double *b, int64_t batch, int64_t n,
                     double *out, void *stream);
 
-/* FP32 FMA issue-rate probe: `blocks` CTAs x 256 threads x 8 independent FFMA
- * chains x `iters` steps (2 FLOP each).  Used by bench.py as the measured
- * FP32 CUDA-core peak; `sink` is a 4-byte device buffer. */
+/* CUDA-core peak probes (the measured roofline denominators of bench.py):
+ * `blocks` CTAs x 256 threads x 8 independent FMA chains x 16 unrolled steps
+ * x `iters` loop trips of fma.rn.f32 (GDT_PROBE_FFMA), packed fma.rn.f32x2
+ * (GDT_PROBE_FFMA2) or fma.rn.f64 (GDT_PROBE_DFMA); `sink` is a 4-byte device
+ * buffer.  gdt_probe_flops gives the FLOP count of one such launch. */
+#define GDT_PROBE_FFMA 0
+#define GDT_PROBE_FFMA2 1
+#define GDT_PROBE_DFMA 2
+int gdt_probe_peak(int kind, int64_t blocks, int64_t iters, float *sink, void *stream);
+int64_t gdt_probe_flops(int kind, int64_t blocks, int64_t iters);
+/* = gdt_probe_peak(GDT_PROBE_FFMA, ...) */
 int gdt_probe_fp32(int64_t blocks, int64_t iters, float *sink, void *stream);
 
 /* ---- host coarse LP (stays on the host, _simplex.py) ------------------ */
@@ -246,8 +254,9 @@ int gdt_transport_simplex(const double *C, const double *sup, const double *dem,
  * the reference's pivot sequence; warm_from[q] = w (w < q, same shape) starts
  * from the optimal basis of job w instead (any optimal basis gives the same
  * optimal value; the quantization bounds warm-start the C-bar and C-min LPs
- * from the C-tilde basis on the same marginals).  Jobs chained by warm_from
- * run in order on one worker.  status[q] = GDT_LP_* or GDT_ERR_*. */
+ * from the C-tilde basis on the same marginals); if job w did not reach an
+ * optimum, job q is solved cold from the northwest corner instead.  Jobs
+ * chained by warm_from run in order on one worker.  status[q] = GDT_LP_* or GDT_ERR_*. */
 int gdt_transport_simplex_many(int64_t count, const uint64_t *C, const uint64_t *table,
                                const int32_t *grid_ndim, const int64_t *grid_dims,
                                const uint64_t *sup, const uint64_t *dem, const int64_t *ns,

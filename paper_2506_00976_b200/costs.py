@@ -182,8 +182,9 @@ def min_cost_matrix(grid: GridSpec, coarsening: CoarseningSpec, p: float) -> Coa
 
 
 def weighted_cost_batch(mu_pad, nu_pad, mu_c, nu_c, padded_dims, kappa, p, mode, ctil_dev=None,
-                        table_dev=None):
-    """Device C-bar for a batch: returns (values [B,n,n] f64, unused [B,n,n] u8)."""
+                        table_dev=None, want_unused=True):
+    """Device C-bar for a batch: returns (values [B,n,n] f64, unused [B,n,n] u8
+    or None when ``want_unused`` is False -- the kernels then skip the mask)."""
     t = torch()
     B = mu_pad.shape[0]
     n = mu_c.shape[1]
@@ -193,7 +194,7 @@ def weighted_cost_batch(mu_pad, nu_pad, mu_c, nu_c, padded_dims, kappa, p, mode,
     if table_dev is None and p not in (1.0, 2.0):
         table_dev = to_dev(cost_table(ms, float(p)))
     out = t.empty((B, n, n), dtype=t.float64, device=mu_pad.device)
-    unused = t.empty((B, n, n), dtype=t.uint8, device=mu_pad.device)
+    unused = t.empty((B, n, n), dtype=t.uint8, device=mu_pad.device) if want_unused else None
     N.check(N.lib().gdt_weighted_cost(
         N.ptr(mu_pad), N.ptr(nu_pad), N.ptr(mu_c), N.ptr(nu_c), N.ptr(ctil_dev), N.ptr(table_dev),
         ms, N.ptr(out), N.ptr(unused), B, len(padded_dims), N.i64s(padded_dims), kappa, float(p),

@@ -26,7 +26,7 @@ NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "
 # files whose arithmetic restates the reference's rounding order: no FMA
 NO_FMA = {"grid_kernels.cu", "primal.cu", "cbar.cu", "entropic.cu"}
 CU = ["grid_kernels.cu", "cbar.cu", "cbar_fast.cu", "cbar_diag.cu", "primal.cu", "ctransform.cu",
-      "ctransform_pruned.cu", "entropic.cu"]
+      "ctransform_pruned.cu", "entropic.cu", "probes.cu"]
 CPP = ["simplex.cpp"]
 HEADERS = ["common.cuh", os.path.join("..", "..", "include", "gridot_b200.h")]
 

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256) cbar_tile_kernel(
         const int64_t oi = (b * n + k) * n + l;
         const bool un = denom == 0.0;
         out[oi] = un ? Ccentre[k * n + l] : __ddiv_rn(numer, denom);
-        unused[oi] = un ? 1 : 0;
+        if (unused) unused[oi] = un ? 1 : 0;
     }
 }
 
@@ -296,11 +296,13 @@ __global__ void __launch_bounds__(256) cbar_moments_kernel(
         if (vec) {
             reinterpret_cast<double2 *>(out + orow + l0)[0] = make_double2(vals[0], vals[1]);
             reinterpret_cast<double2 *>(out + orow + l0)[1] = make_double2(vals[2], vals[3]);
-            *reinterpret_cast<uchar4 *>(unused + orow + l0) = make_uchar4(un[0], un[1], un[2], un[3]);
+            if (unused)
+                *reinterpret_cast<uchar4 *>(unused + orow + l0) =
+                    make_uchar4(un[0], un[1], un[2], un[3]);
         } else {
             for (int q = 0; q < 4 && l0 + q < n; ++q) {
                 out[orow + l0 + q] = vals[q];
-                unused[orow + l0 + q] = un[q];
+                if (unused) unused[orow + l0 + q] = un[q];
             }
         }
     }

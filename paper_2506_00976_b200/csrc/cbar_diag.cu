@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 4) cbar_diag_kernel(
             const int64_t kb = kbase + j, oi = kb * n + l;
             const bool un = __dmul_rn(mu_c[kb], nu_c[b * n + l]) == 0.0;
             out[oi] = un ? Ccentre[(kb - b * n) * n + l] : (double)snum[i] * rmu[kb] * rnu[b * n + l];
-            unused[oi] = un ? 1 : 0;
+            if (unused) unused[oi] = un ? 1 : 0;
         }
     } else {  // row by row, two consecutive l per thread
         const double *nub_c = nu_c + b * n, *rnub = rnu + b * n;
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 4) cbar_diag_kernel(
             const double mk = mu_c[kb], rk = rmu[kb];
             const float *sj = snum + j * n;
             double *oj = out + kb * n;
-            uint8_t *uj = unused + kb * n;
+            uint8_t *uj = unused ? unused + kb * n : nullptr;
             const double *cj = Ccentre + (kb - (int64_t)b * n) * n;
             for (int l = 2 * threadIdx.x; l < n; l += 2 * nthreads) {
                 const double2 nl = *reinterpret_cast<const double2 *>(nub_c + l);
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(DG_MAX_THREADS, 4) cbar_diag_kernel(
                 o.x = u0 ? cj[l] : (double)sn.x * rk * rl.x;
                 o.y = u1 ? cj[l + 1] : (double)sn.y * rk * rl.y;
                 *reinterpret_cast<double2 *>(oj + l) = o;
-                *reinterpret_cast<uchar2 *>(uj + l) = make_uchar2(u0 ? 1 : 0, u1 ? 1 : 0);
+                if (uj) *reinterpret_cast<uchar2 *>(uj + l) = make_uchar2(u0 ? 1 : 0, u1 ? 1 : 0);
             }
         }
     }

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(CF_THREADS, 2) cbar_toeplitz_kernel(
         const int64_t oi = (b * n + k) * n + l;
         const bool un = denom == 0.0;
         out[oi] = un ? Ccentre[k * n + l] : numer[i] / denom;
-        unused[oi] = un ? 1 : 0;
+        if (unused) unused[oi] = un ? 1 : 0;
     }
 }
 

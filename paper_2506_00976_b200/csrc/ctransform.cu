@@ -541,31 +541,3 @@ extern "C" int gdt_ctransform_points(const double *xs, const double *xt, int64_t
         points_ct_kernel<<<grid_size(ns, 128), 128, 0, st>>>(xs, xt, ns, nt, ndim, p, v, out);
     return cuda_status("gdt_ctransform_points");
 }
-
-// ---------------------------------------------------------------------------
-// FP32 CUDA-core issue-rate probe: independent FFMA chains, used by bench.py
-// as the live denominator of the c-transform / C-bar rooflines.
-// ---------------------------------------------------------------------------
-namespace gdt {
-__global__ void __launch_bounds__(256) ffma_probe_kernel(float *sink, int64_t iters, float seed) {
-    float a[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = seed + threadIdx.x * 1e-7f + q;
-    const float m = 0.9999999f, c = 1e-7f;
-    for (int64_t it = 0; it < iters; ++it) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) a[q] = fmaf(a[q], m, c);
-    }
-    float s = 0.f;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) s += a[q];
-    if (s == 12345.678f) sink[0] = s;  // never true; keeps the chains alive
-}
-}  // namespace gdt
-
-extern "C" int gdt_probe_fp32(int64_t blocks, int64_t iters, float *sink, void *stream) {
-    GDT_CHECK_ARG(blocks >= 1 && iters >= 1, "gdt_probe_fp32: bad sizes");
-    gdt::ffma_probe_kernel<<<(unsigned)blocks, 256, 0, gdt::as_stream(stream)>>>(sink, iters,
-                                                                               1.0f);
-    return gdt::cuda_status("gdt_probe_fp32");
-}

@@ -759,8 +759,9 @@ extern "C" int gdt_transport_simplex_many_flags(
             status[q] = solve_job(q, true);
         } else if (w >= 0) {
             if (status[w] != GDT_LP_OPTIMAL) {
-                status[q] = status[w] < 0 ? status[w] : GDT_ERR_ARG;
-                pivots[q] = 0;
+                // no usable start basis: solve this LP on its own from the
+                // northwest corner, as the reference solves every LP
+                status[q] = solve_job(q, false);
             } else {
                 std::memcpy(P(bi[q]), P(bi[w]), sizeof(int64_t) * nbq);
                 std::memcpy(P(bj[q]), P(bj[w]), sizeof(int64_t) * nbq);

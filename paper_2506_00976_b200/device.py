@@ -57,38 +57,24 @@ def to_host(t):
     return t.detach().cpu().numpy()
 
 
-_PINNED = {}
-
-
-def pinned_empty(shape, slot: str, dtype=None):
-    """A page-locked host buffer of `shape` (float64 by default), reused per
-    `slot`; returns (torch view, numpy view) aliasing it."""
+def pinned_empty(shape, dtype=None):
+    """A fresh page-locked host buffer of `shape` (float64 by default) from
+    torch's caching host allocator; returns (torch view, numpy view) aliasing
+    it.  The numpy view keeps the buffer alive; nothing is shared between
+    callers."""
     tt = torch()
-    dtype = dtype or tt.float64
-    n = int(np.prod(shape))
-    buf = _PINNED.get(slot)
-    if buf is None or buf.numel() < n or buf.dtype != dtype:
-        buf = tt.empty(n, dtype=dtype, pin_memory=True)
-        _PINNED[slot] = buf
-    view = buf[:n].view(tuple(shape))
-    return view, view.numpy()
+    buf = tt.empty(tuple(shape), dtype=dtype or tt.float64, pin_memory=True)
+    return buf, buf.numpy()
 
 
-def to_host_pinned(t, slot: str = "default"):
-    """D2H through a reused page-locked buffer (full PCIe/NVLink-C2C rate).
-
-    The returned numpy array aliases the buffer: it is valid until the next
-    call with the same ``slot``."""
+def to_host_pinned(t):
+    """D2H through a fresh page-locked buffer (full PCIe/NVLink-C2C rate);
+    returns a numpy array that owns (keeps alive) the buffer."""
     tt = torch()
-    n = t.numel()
-    buf = _PINNED.get(slot)
-    if buf is None or buf.numel() < n or buf.dtype != t.dtype:
-        buf = tt.empty(n, dtype=t.dtype, pin_memory=True)
-        _PINNED[slot] = buf
-    view = buf[:n].view(t.shape)
-    view.copy_(t.detach(), non_blocking=True)
+    buf, arr = pinned_empty(t.shape, t.dtype)
+    buf.copy_(t.detach(), non_blocking=True)
     tt.cuda.current_stream(t.device).synchronize()
-    return view.numpy()
+    return arr
 
 
 def stream() -> int:

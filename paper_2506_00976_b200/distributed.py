@@ -13,11 +13,11 @@ import math
 
 import numpy as np
 
-from .engine import QUANT_METHODS, quantized_bounds
+from .engine import QUANT_METHODS, quantized_bounds, quantized_bounds_many
 from .reports import BoundReport
 
 __all__ = ["shard_range", "RECORD_FIELDS", "pack_records", "unpack_records", "gather_records",
-           "distributed_bounds"]
+           "gather_records_rows", "distributed_bounds", "distributed_bounds_many"]
 
 RECORD_FIELDS = (
     "pair", "status", "wc_value", "mc_raw", "pu_value", "pu_transport", "pu_delta_mu",
@@ -51,10 +51,12 @@ def pack_records(reports, first_pair: int) -> np.ndarray:
         row[_IDX["status"]] = status
         get = lambda m: rep.get(m) if not isinstance(rep.get(m), Exception) else None  # noqa
         wc, mc, pu, du = (get(m) for m in QUANT_METHODS)
+        first = next((r for r in (wc, mc, pu, du) if r is not None), None)
+        if first is not None:  # shared by every method of the pair
+            row[_IDX["coarse_size"]] = np.nan if first.coarse_size is None else first.coarse_size
+            row[_IDX["wall_time"]] = first.wall_time
         if wc is not None:
             row[_IDX["wc_value"]] = wc.value
-            row[_IDX["coarse_size"]] = wc.coarse_size
-            row[_IDX["wall_time"]] = wc.wall_time
         if mc is not None:
             row[_IDX["mc_raw"]] = mc.raw_value
         if pu is not None:
@@ -109,11 +111,66 @@ def gather_records(local: np.ndarray, total: int, group=None, device=None) -> np
 
     Shards are padded to the largest shard so one all_gather_into_tensor (NCCL)
     or all_gather (gloo) suffices."""
+    return gather_records_rows(local, total, 1, group, device)
+
+
+def _gather_device(group):
+    import torch
+    import torch.distributed as dist
+
+    return torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else None
+
+
+def distributed_bounds(mus, nus, dims, kappa, p, group=None, *, compute=None, **kw):
+    """Shard the pairs over the process group, compute, gather records on every rank.
+
+    ``compute(mus, nus, dims, kappa, p, **kw)`` defaults to
+    :func:`quantized_bounds` (the CPU tests substitute a host stand-in)."""
+    import torch.distributed as dist
+
+    compute = compute or quantized_bounds
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    total = int(mus.shape[0])
+    lo, hi = shard_range(total, rank, world)
+    reps = compute(mus[lo:hi], nus[lo:hi], dims, kappa, p, **kw) if hi > lo else []
+    local = pack_records(reps, lo)
+    return unpack_records(gather_records(local, total, group, _gather_device(group)))
+
+
+def distributed_bounds_many(mus, nus, dims, combos, group=None, *, compute=None, **kw):
+    """:func:`distributed_bounds` for several (kappa, p) combinations: each rank
+    runs ONE ``quantized_bounds_many`` call on its contiguous shard (its LPs on
+    its own host threads), then one all_gather of [pairs x combos, F] records.
+
+    Returns ({(kappa, p): [unpacked record per pair]}, records [combos, total, F])."""
+    import torch.distributed as dist
+
+    compute = compute or quantized_bounds_many
+    combos = [(int(k), float(p)) for k, p in combos]
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    total = int(mus.shape[0])
+    lo, hi = shard_range(total, rank, world)
+    res = compute(mus[lo:hi], nus[lo:hi], dims, combos, **kw) if hi > lo else \
+        {key: [] for key in combos}
+    # records of pair-major rows, combination-minor: [n_r * C, F], gathered in
+    # pair order as (total * C) rows
+    C = len(combos)
+    local = np.stack([pack_records(res[key], lo) for key in combos], axis=1) \
+        if hi > lo else np.zeros((0, C, F))
+    flat = gather_records_rows(local.reshape(-1, F), total, C, group, _gather_device(group))
+    table = flat.reshape(total, C, F).transpose(1, 0, 2).copy()
+    return {key: unpack_records(table[j]) for j, key in enumerate(combos)}, table
+
+
+def gather_records_rows(local: np.ndarray, total: int, per_pair: int, group=None,
+                        device=None) -> np.ndarray:
+    """gather_records for shards holding `per_pair` consecutive rows per pair."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    width = -(-total // world)
+    width = -(-total // world) * per_pair
     buf = np.full((width, F), np.nan)
     buf[:local.shape[0]] = local
     t = torch.from_numpy(buf)
@@ -129,20 +186,5 @@ def gather_records(local: np.ndarray, total: int, group=None, device=None) -> np
     rows = []
     for r, part in enumerate(parts):
         lo, hi = shard_range(total, r, world)
-        rows.append(part[:hi - lo].cpu().numpy())
+        rows.append(part[:(hi - lo) * per_pair].cpu().numpy())
     return np.concatenate(rows, axis=0)
-
-
-def distributed_bounds(mus, nus, dims, kappa, p, group=None, **kw):
-    """Shard the pairs over the process group, compute, gather records on every rank."""
-    import torch
-    import torch.distributed as dist
-
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    total = int(mus.shape[0])
-    lo, hi = shard_range(total, rank, world)
-    reps = quantized_bounds(mus[lo:hi], nus[lo:hi], dims, kappa, p, **kw) if hi > lo else []
-    local = pack_records(reps, lo)
-    dev = torch.device("cuda", torch.cuda.current_device()) \
-        if dist.get_backend(group) == "nccl" else None
-    return unpack_records(gather_records(local, total, group, dev))

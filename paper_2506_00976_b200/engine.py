@@ -116,7 +116,7 @@ def _cbar(bt: _Batch):
     # reference-order fp64 kernel (fp64 mode) or the fp32 FFMA2 kernel
     mode = 1 if bt.p == 2.0 else bt.mode
     return weighted_cost_batch(bt.mu_pad, bt.nu_pad, bt.mu_c, bt.nu_c, bt.pdims, bt.kappa, bt.p,
-                               mode, bt.ctil_dev, bt.table_dev)
+                               mode, bt.ctil_dev, bt.table_dev, want_unused=False)
 
 
 @dataclass
@@ -131,7 +131,7 @@ class _LPJob:
     cbar_host: object = None  # keeps the pinned C-bar alive until the solve
 
 
-def coarse_problems(bt: _Batch, methods, pin_slot: str = "cbar") -> _LPJob:
+def coarse_problems(bt: _Batch, methods) -> _LPJob:
     """SumPool + C-bar on the device and every coarse LP the methods need."""
     need_ctil = "primal_upscaling" in methods or "dual_upscaling" in methods
     need_cbar = "weighted_cost" in methods
@@ -140,7 +140,7 @@ def coarse_problems(bt: _Batch, methods, pin_slot: str = "cbar") -> _LPJob:
     tc = time.perf_counter()
     if need_cbar:
         vals, _ = _cbar(bt)
-        cbar_host = to_host_pinned(vals, pin_slot)
+        cbar_host = to_host_pinned(vals)
     mu_c = to_host(bt.mu_c)
     nu_c = to_host(bt.nu_c)
     plans = CoarsePlans(n=bt.n)
@@ -297,7 +297,10 @@ def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
         ctil = centre_cost_table(bt.pdims, bt.kappa, bt.p) if need_ctil else None
         cmin = min_cost_table(bt.pdims, bt.kappa, bt.p) if need_cmin else None
         if need_cbar:
-            pinned[i] = pinned_empty((bt.B, bt.n, bt.n), f"cbar{i}")
+            # page-locked C-bar for the host LPs: owned by this call (torch's
+            # caching host allocator makes the allocation cheap), released
+            # when the call returns, so concurrent calls never share it
+            pinned[i] = pinned_empty((bt.B, bt.n, bt.n))
         for b in range(bt.B):
             full = bool((masses[i][0][b] > 0).all() and (masses[i][1][b] > 0).all())
             prev = -1
@@ -450,8 +453,9 @@ def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
         plans[i].solve_seconds = t4 - t1
         plans[i].cbar_seconds = t2 - t1
     if timings is not None:
-        timings.update(lp_build=t1 - t0, cbar=t2 - t1, device_overlapped=t_dev,
-                       lp_tail_wait=t4 - t3, lp_late_and_values=t5 - t4)
+        for key, val in (("lp_build", t1 - t0), ("cbar", t2 - t1), ("device_overlapped", t_dev),
+                         ("lp_tail_wait", t4 - t3), ("lp_late_and_values", t5 - t4)):
+            timings[key] = timings.get(key, 0.0) + val
     return plans, dev
 
 
@@ -730,39 +734,78 @@ def _reports(bt: _Batch, plans: CoarsePlans, prim, dual, methods, xi, max_iter, 
     return reports
 
 
+# page-locked C-bar held for the host LPs of one pipeline run; larger batches
+# are processed in consecutive chunks of pairs (each a full pipeline run)
+PINNED_BUDGET_BYTES = 4 << 30
+
+
+def _chunks(B, dims, combos, methods, max_chunk_pairs):
+    """[lo, hi) pair ranges: each keeps the C-bar of all combinations under
+    PINNED_BUDGET_BYTES (pinned host) unless max_chunk_pairs says otherwise."""
+    if max_chunk_pairs is None:
+        per_pair = 0
+        if "weighted_cost" in methods:
+            for k, _ in combos:
+                n = int(np.prod([-(-x // int(k)) for x in dims]))
+                per_pair += 8 * n * n
+        max_chunk_pairs = max(1, PINNED_BUDGET_BYTES // max(per_pair, 1))
+    step = max(1, int(max_chunk_pairs))
+    return [(lo, min(B, lo + step)) for lo in range(0, B, step)] or [(0, 0)]
+
+
+def _export_plans(plans_out, key, plans: CoarsePlans):
+    if plans_out is None:
+        return
+    dst = plans_out.setdefault(key, [])
+    for b in range(len(plans.ctil_arcs)):
+        arcs, duals = plans.ctil_arcs[b], plans.ctil_duals[b]
+        dst.append(None if arcs is None else (arcs[0], arcs[1], arcs[2], duals[0], duals[1]))
+
+
 def quantized_bounds(mus, nus, dims, kappa, p, *, precision="fp64", xi=None, max_iter=10_000,
                      kernel=None, methods=QUANT_METHODS, dual_method="multilinear",
-                     lp_threads=0, return_exceptions=True, timings=None):
+                     lp_threads=0, return_exceptions=True, timings=None, max_chunk_pairs=None,
+                     plans_out=None):
     """All requested quantization bounds for a batch of pairs on one grid.
 
     mus, nus: [B, prod(dims)] float64 (numpy, pinned or device tensors).
     Returns a list (one per pair) of {method: BoundReport | exception}.
+    Pairs are processed in chunks (``max_chunk_pairs``, default: as many as
+    keep the page-locked C-bar under PINNED_BUDGET_BYTES); ``plans_out``
+    (a dict) receives, under key (kappa, p), each pair's C-tilde plan
+    (full coarse rows, cols, masses, dual g, its support index) or None.
     """
     _check_args(precision, methods)
     t_start = time.perf_counter()
     mu, nu = _device_masses(mus, nus, dims)
-    bt = _Batch(mu, nu, dims, kappa, p, precision)
-    paired = _kernel_pairs(bt, kernel)
-    t0 = time.perf_counter()
-    plans, dev = _pipeline([bt], methods, lp_threads,
-                           lambda i, pl: _run_device(bt, pl, paired, xi, max_iter, methods,
-                                                     dual_method), timings)
-    plans = plans[0]
-    prim, dual, _ = dev[0]
-    t2 = time.perf_counter()
-    if timings is not None:
-        timings.update(prepare=t0 - t_start, coarse_and_gpu=t2 - t0)
-    wall = (t2 - t_start) / max(bt.B, 1)
-    reports = _reports(bt, plans, prim, dual, methods, xi, max_iter, wall, return_exceptions,
-                       timings)
-    if timings is not None:
-        timings["finish"] = time.perf_counter() - t2
+    reports = []
+    for lo, hi in _chunks(mu.shape[0], dims, [(kappa, p)], methods, max_chunk_pairs):
+        tc = time.perf_counter()
+        bt = _Batch(mu[lo:hi], nu[lo:hi], dims, kappa, p, precision)
+        paired = _kernel_pairs(bt, kernel)
+        t0 = time.perf_counter()
+        plans, dev = _pipeline([bt], methods, lp_threads,
+                               lambda i, pl: _run_device(bt, pl, paired, xi, max_iter, methods,
+                                                         dual_method), timings)
+        plans = plans[0]
+        prim, dual, _ = dev[0]
+        t2 = time.perf_counter()
+        if timings is not None:
+            timings["prepare"] = timings.get("prepare", 0.0) + t0 - tc
+            timings["coarse_and_gpu"] = timings.get("coarse_and_gpu", 0.0) + t2 - t0
+        wall = (t2 - (t_start if lo == 0 else tc)) / max(bt.B, 1)
+        _export_plans(plans_out, (int(kappa), float(p)), plans)
+        reports += _reports(bt, plans, prim, dual, methods, xi, max_iter, wall,
+                            return_exceptions, timings)
+        if timings is not None:
+            timings["finish"] = timings.get("finish", 0.0) + time.perf_counter() - t2
     return reports
 
 
 def quantized_bounds_many(mus, nus, dims, combos, *, precision="fp64", xi=None,
                           max_iter=10_000, methods=QUANT_METHODS, dual_method="multilinear",
-                          lp_threads=0, return_exceptions=True, timings=None):
+                          lp_threads=0, return_exceptions=True, timings=None,
+                          max_chunk_pairs=None, plans_out=None):
     """:func:`quantized_bounds` for several (kappa, p) combinations of the same
     batch at once: the masses are uploaded once, and the coarse LPs of ALL
     combinations run as one host batch on one thread pool (the expensive
@@ -770,7 +813,8 @@ def quantized_bounds_many(mus, nus, dims, combos, *, precision="fp64", xi=None,
     combination leaves the tail of each wave idle.  Results and their values
     are those of one ``quantized_bounds`` call per combination (the same LPs,
     pivot paths and device kernels); ``BoundReport.wall_time`` is the whole
-    call's wall time per pair and combination.
+    call's wall time per pair and combination.  ``max_chunk_pairs`` and
+    ``plans_out`` as in :func:`quantized_bounds`.
 
     Returns {(kappa, p): [per-pair {method: BoundReport | exception}]}.
     """
@@ -778,22 +822,26 @@ def quantized_bounds_many(mus, nus, dims, combos, *, precision="fp64", xi=None,
     t_start = time.perf_counter()
     mu, nu = _device_masses(mus, nus, dims)
     combos = [(int(k), float(p)) for k, p in combos]
-    batches = [_Batch(mu, nu, dims, k, p, precision) for k, p in combos]
-    t0 = time.perf_counter()
-    plans, dev = _pipeline(batches, methods, lp_threads,
-                           lambda i, pl: _run_device(batches[i], pl, None, xi, max_iter, methods,
-                                                     dual_method), timings)
-    t3 = time.perf_counter()
-    nb = max(batches[0].B, 1) if batches else 1
-    wall = (t3 - t_start) / nb / max(len(combos), 1)
-    out = {}
-    for i, key in enumerate(combos):
-        prim, dual, _ = dev[i]
-        out[key] = _reports(batches[i], plans[i], prim, dual, methods, xi, max_iter, wall,
-                            return_exceptions, timings)
-    if timings is not None:
-        timings.update(prepare=t0 - t_start, coarse_and_gpu=t3 - t0,
-                       finish=time.perf_counter() - t3)
+    out = {key: [] for key in combos}
+    for lo, hi in _chunks(mu.shape[0], dims, combos, methods, max_chunk_pairs):
+        tc = time.perf_counter()
+        batches = [_Batch(mu[lo:hi], nu[lo:hi], dims, k, p, precision) for k, p in combos]
+        t0 = time.perf_counter()
+        plans, dev = _pipeline(batches, methods, lp_threads,
+                               lambda i, pl: _run_device(batches[i], pl, None, xi, max_iter,
+                                                         methods, dual_method), timings)
+        t3 = time.perf_counter()
+        nb = max(hi - lo, 1)
+        wall = (t3 - (t_start if lo == 0 else tc)) / nb / max(len(combos), 1)
+        for i, key in enumerate(combos):
+            prim, dual, _ = dev[i]
+            _export_plans(plans_out, key, plans[i])
+            out[key] += _reports(batches[i], plans[i], prim, dual, methods, xi, max_iter, wall,
+                                 return_exceptions, timings)
+        if timings is not None:
+            timings["prepare"] = timings.get("prepare", 0.0) + t0 - tc
+            timings["coarse_and_gpu"] = timings.get("coarse_and_gpu", 0.0) + t3 - t0
+            timings["finish"] = timings.get("finish", 0.0) + time.perf_counter() - t3
     return out
 
 

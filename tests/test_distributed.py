@@ -80,6 +80,74 @@ def test_gloo_gather_matches_single_rank(total):
         assert np.array_equal(got[r], expect, equal_nan=True)
 
 
+COMBOS = ((4, 1.0), (4, 2.0), (8, 1.0))
+
+
+def _fake_many(mus, nus, dims, combos, **kw):
+    """Host stand-in for quantized_bounds_many: values depend on the pair's
+    global index (mus[:, 0]) and the combination, so a misplaced row cannot
+    go unnoticed."""
+    out = {}
+    for k, p in combos:
+        rows = []
+        for m in mus:
+            i = int(m[0])
+            rep = _fake_reports(i, i + 1)[0]
+            rows.append({key: (BoundReport(r.method, r.value + k + p, r.raw_value + k + p,
+                                           r.components, r.wall_time, r.iterations,
+                                           r.coarse_size)
+                               if isinstance(r, BoundReport) else r)
+                         for key, r in rep.items()})
+        out[(k, p)] = rows
+    return out
+
+
+def _many_worker(rank, world, port, total, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mus = np.arange(total, dtype=np.float64)[:, None] * np.ones((1, 4))
+    _, table = D.distributed_bounds_many(mus, mus, (2, 2), COMBOS, compute=_fake_many)
+    q.put((rank, table))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total", [7, 2, 1])
+def test_gloo_distributed_bounds_many_matches_single_rank(total):
+    """The multi-combination path: one compute call per rank on its shard,
+    one all_gather of pair-major records, same table as one rank alone."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_many_worker, args=(r, world, port, total, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    mus = np.arange(total, dtype=np.float64)[:, None] * np.ones((1, 4))
+    single = _fake_many(mus, mus, (2, 2), COMBOS)
+    expect = np.stack([D.pack_records(single[key], 0) for key in COMBOS])
+    for r in range(world):
+        assert got[r].shape == (len(COMBOS), total, D.F)
+        assert np.array_equal(got[r], expect, equal_nan=True)
+
+
+def test_record_keeps_coarse_size_without_weighted_cost():
+    reps = _fake_reports(0, 3)
+    for rep in reps:
+        del rep["weighted_cost"]
+    back = D.unpack_records(D.pack_records(reps, 0))
+    for b in back:
+        for r in b["reports"].values():
+            assert r.coarse_size == 1024 and r.wall_time == 0.5
+
+
 def test_shard_range_partitions_exactly():
     for total in (0, 1, 7, 45, 360):
         for world in (1, 2, 3, 8):

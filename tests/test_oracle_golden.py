@@ -112,3 +112,23 @@ def test_sumpool_restatement_matches_add_at():
         out = np.zeros(int(np.prod(P.coarse_dims(dims, k))))
         np.add.at(out, P.block_ids(dims, k), m)
         assert out.tobytes() == P.sumpool(m, dims, k).tobytes()
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_batch_golden_pins_the_generator(cfg):
+    """tests/golden/batch_cfg*.npz (reference values for every benched pair)
+    were made from these exact masses: the GPU box regenerates them from seeds."""
+    import json
+
+    from conftest import GOLDEN
+
+    z = np.load(os.path.join(GOLDEN, f"batch_cfg{cfg}.npz"), allow_pickle=False)
+    meta = json.loads(str(z["meta"]))
+    assert meta["pairs"] == (64 if cfg == 5 else 45)
+    assert [tuple(c) for c in meta["combos"]] == [(int(k), float(p))
+                                                  for k, p in S.WORKLOADS[cfg].combos]
+    for b in range(0, meta["pairs"], 11):
+        for side, key in ((0, "mu_sha"), (1, "nu_sha")):
+            m = S.measure(cfg, b, side)
+            assert hashlib.sha256(np.ascontiguousarray(m).tobytes()).hexdigest() == \
+                str(z[key][b])
