@@ -78,6 +78,14 @@ int gdt_pad_f64(const double *in, double *out, int64_t batch, int ndim,
 int gdt_sumpool_f64(const double *fine, double *coarse, int64_t batch, int ndim,
                     const int64_t *dims, int kappa, void *stream);
 
+/* gdt_sumpool_f64 plus per-block statistics of the same pass:
+ * stats [batch, n, 3] = {smallest positive mass, largest positive mass,
+ * number of positive cells} (+inf, -inf, 0 without support); stats may be
+ * NULL.  The coarse-level primal stage reads them (scale-range checks,
+ * b = 1 on the target support, the default xi). */
+int gdt_sumpool_stats_f64(const double *fine, double *coarse, double *stats, int64_t batch,
+                          int ndim, const int64_t *dims, int kappa, void *stream);
+
 /* ---- K2: marginally weighted coarse cost C-bar ------------------------ */
 
 /* C-bar_kl = sum_{x in X_k, y in Y_l} rho(x,y)^p mu_x nu_y / (mu~_k nu~_l);
@@ -106,6 +114,20 @@ int gdt_weighted_cost(const double *mu, const double *nu, const double *mu_c,
  * sinkhorn.py:101-142, over the upscaled coupling of upscale_coupling,
  * quantized.py:119-159 -- the fine coupling is never materialised.
  *   mu, nu        [batch, N] fine masses (padded grid)
+ *   mu_c, nu_c    [batch, n] their SumPool (gdt_sumpool_f64); nullable
+ *   stats         [2, batch, n, 3] block statistics of mu then nu
+ *                 (gdt_sumpool_stats_f64); nullable
+ *   cbar          [batch, n, n] C-bar of the batch (gdt_weighted_cost); nullable.
+ *                 With mu_c, nu_c, stats, cbar, tv_w and bmap, GDT_MODE_FAST
+ *                 and a uniform kernel, the stage runs at the coarse level:
+ *                 every scaling is a per-block quotient of the masses, so a
+ *                 sweep is O(arcs); transport^p = the fitted coarse plan priced
+ *                 by C-bar (whose numerator is sum mu_t nu_s C_ts); one fine
+ *                 pass: the weighted TV
+ *   tv_w          [N] tv_weights of the padded grid (measures.py:289-296); nullable
+ *   bmap          [N] int32 coarse block of each padded cell (block_index_map,
+ *                 measures.py:248-254); nullable.  Without any of these the
+ *                 fine-level kernels run.
  *   arc_off       [batch+1]  pair b owns arcs [arc_off[b], arc_off[b+1])
  *   row_ptr       [batch, n+1]  per pair CSR over coarse rows (offsets
  *                 relative to arc_off[b]); arcs sorted by (row, col)
@@ -131,7 +153,9 @@ int gdt_weighted_cost(const double *mu, const double *nu, const double *mu_c,
  *   scratch       device workspace of gdt_primal_scratch_bytes() bytes */
 int64_t gdt_primal_scratch_bytes(int64_t batch, int ndim, const int64_t *dims,
                                  int kappa, int kernel_uniform);
-int gdt_primal_upscale(const double *mu, const double *nu, const int64_t *arc_off,
+int gdt_primal_upscale(const double *mu, const double *nu, const double *mu_c,
+                       const double *nu_c, const double *stats, const double *cbar,
+                       const double *tv_w, const int32_t *bmap, const int64_t *arc_off,
                        const int32_t *row_ptr, const int32_t *row_arc_col,
                        const double *row_arc_mass, const int32_t *col_ptr,
                        const int32_t *col_arc_row, const double *col_arc_mass,

@@ -15,7 +15,9 @@ import numpy as np
 from .errors import GridotError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "csrc", "libgridot_b200.so")
+# GRIDOT_B200_LIB selects another build of the same library (debug / trace
+# builds from scripts/); the default is the in-tree release build
+LIB_PATH = os.environ.get("GRIDOT_B200_LIB") or os.path.join(_HERE, "csrc", "libgridot_b200.so")
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64
@@ -28,10 +30,11 @@ _SIGNATURES = {
     "gdt_last_error": (ctypes.c_char_p, []),
     "gdt_pad_f64": (I32, [P, P, I64, I32, P, I32, P]),
     "gdt_sumpool_f64": (I32, [P, P, I64, I32, P, I32, P]),
+    "gdt_sumpool_stats_f64": (I32, [P, P, P, I64, I32, P, I32, P]),
     "gdt_weighted_cost": (I32, [P, P, P, P, P, P, I64, P, P, I64, I32, P, I32, D, I32, P]),
     "gdt_primal_scratch_bytes": (I64, [I64, I32, P, I32, I32]),
-    "gdt_primal_upscale": (I32, [P, P, P, P, P, P, P, P, P, P, I32, P, I64, D, I64, I32, P, I32,
-                                 P, I64, I32, P, P, P, P]),
+    "gdt_primal_upscale": (I32, [P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I32, P, I64, D,
+                                 I64, I32, P, I32, P, I64, I32, P, P, P, P]),
     "gdt_ipf_csr": (I32, [P, P, P, P, P, P, P, P, I64, I64, D, I64, P, P, P, P, P, P, P]),
     "gdt_price_coo": (I32, [P, P, P, I64, P, P, P, I64, D, I32, P, P, P]),
     "gdt_weighted_tv_inner": (I32, [P, P, I64, I32, P, D, P, P, P]),

@@ -50,23 +50,29 @@ def _run(cmd, log):
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     hdrs = [os.path.join(HERE, h) for h in HEADERS]
-    objs = []
+    objs, jobs = [], []
     for f in CU:
         src = os.path.join(HERE, f)
         obj = os.path.join(OBJ, f + ".o")
         objs.append(obj)
         if force or _newer([src] + hdrs + [__file__], obj):
             flags = NVFLAGS + (["--fmad=false"] if f in NO_FMA else [])
-            _run([NVCC] + flags + ["-c", src, "-o", obj], os.path.join(OBJ, f + ".log"))
-            if verbose:
-                print("built", f)
+            jobs.append((f, [NVCC] + flags + ["-c", src, "-o", obj]))
     for f in CPP:
         src = os.path.join(HERE, f)
         obj = os.path.join(OBJ, f + ".o")
         objs.append(obj)
         if force or _newer([src] + hdrs + [__file__], obj):
-            _run([CXX, "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
-                  "-pthread", "-c", src, "-o", obj], os.path.join(OBJ, f + ".log"))
+            jobs.append((f, [CXX, "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off",
+                             "-fno-fast-math", "-pthread", "-c", src, "-o", obj]))
+    # translation units compile in parallel (the slowest, primal.cu, first)
+    from concurrent.futures import ThreadPoolExecutor
+
+    jobs.sort(key=lambda j: j[0] != "primal.cu")
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f, _ in zip([j[0] for j in jobs],
+                        list(ex.map(lambda j: _run(j[1], os.path.join(OBJ, j[0] + ".log")),
+                                    jobs))):
             if verbose:
                 print("built", f)
     if force or _newer(objs, LIB):

@@ -68,8 +68,13 @@ __global__ void pad_kernel(const double *__restrict__ in, double *__restrict__ o
 // K1 SumPool: one thread per (pair, block); offsets visited in ascending fine
 // flat order, accumulator starts at 0.0 (np.add.at order, measures.py:266).
 // ---------------------------------------------------------------------------
+// With `stats`, the same pass also records per block the smallest and largest
+// positive mass and the number of positive cells ([batch, n, 3]; +inf / -inf /
+// 0 for a block without support) -- the block statistics of the coarse-level
+// primal stage (primal.cu), at no extra read of the fine masses.
 __global__ void sumpool_kernel(const double *__restrict__ fine, double *__restrict__ coarse,
-                               int64_t batch, Grid f, Grid c, int kappa) {
+                               int64_t batch, Grid f, Grid c, int kappa,
+                               double *__restrict__ stats) {
     const int64_t total = batch * c.cells;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -83,14 +88,27 @@ __global__ void sumpool_kernel(const double *__restrict__ fine, double *__restri
         }
         const double *src = fine + b * f.cells + origin;
         const int K3 = c.nd > 3 ? kappa : 1, K2 = c.nd > 2 ? kappa : 1, K1 = c.nd > 1 ? kappa : 1;
-        double acc = 0.0;
+        double acc = 0.0, lo = INFINITY, hi = -INFINITY, cnt = 0.0;
         for (int o3 = 0; o3 < K3; ++o3)
             for (int o2 = 0; o2 < K2; ++o2)
                 for (int o1 = 0; o1 < K1; ++o1) {
                     const double *row = src + o3 * f.stride[3] + o2 * f.stride[2] + o1 * f.stride[1];
-                    for (int o0 = 0; o0 < kappa; ++o0) acc = __dadd_rn(acc, row[o0]);
+                    for (int o0 = 0; o0 < kappa; ++o0) {
+                        const double x = row[o0];
+                        acc = __dadd_rn(acc, x);
+                        if (x > 0.0) {
+                            lo = fmin(lo, x);
+                            hi = fmax(hi, x);
+                            cnt += 1.0;
+                        }
+                    }
                 }
         coarse[idx] = acc;
+        if (stats) {
+            stats[3 * idx] = lo;
+            stats[3 * idx + 1] = hi;
+            stats[3 * idx + 2] = cnt;
+        }
     }
 }
 
@@ -368,13 +386,18 @@ int gdt_pad_f64(const double *in, double *out, int64_t batch, int ndim, const in
 
 int gdt_sumpool_f64(const double *fine, double *coarse, int64_t batch, int ndim,
                     const int64_t *dims, int kappa, void *stream) {
+    return gdt_sumpool_stats_f64(fine, coarse, nullptr, batch, ndim, dims, kappa, stream);
+}
+
+int gdt_sumpool_stats_f64(const double *fine, double *coarse, double *stats, int64_t batch,
+                          int ndim, const int64_t *dims, int kappa, void *stream) {
     Grid f, c;
     GDT_CHECK_ARG(make_grid(f, ndim, dims) && make_coarse(c, f, kappa) && batch >= 0,
                   "gdt_sumpool_f64: dims must be positive multiples of kappa");
     if (batch == 0) return GDT_OK;
     const int64_t work = batch * c.cells;
     sumpool_kernel<<<grid_size(work, 128), 128, 0, as_stream(stream)>>>(fine, coarse, batch, f, c,
-                                                                        kappa);
+                                                                        kappa, stats);
     return cuda_status("gdt_sumpool_f64");
 }
 

@@ -154,16 +154,41 @@ struct PairPtrs {
     // [q * K1, (q + 1) * K1), K1 = kappa^(d-1) (run_list_kernel)
     const int32_t *rrc, *crc;
     const double *rrf, *crf;
+    int pf;  // the gathered vector is in global memory: prefetch runs into L1
 };
+
+constexpr int PF_RUNS = 8;  // runs prefetched ahead of the exact-order adds
+
+#ifdef GDT_IPF_TRACE
+// debug builds: SM clock at the phase boundaries of sweep 10 of pair 0
+__device__ long long g_ex_trace[16];
+#define EX_TRACE(slot_)                                                   \
+    do {                                                                  \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && it == 10) g_ex_trace[(slot_)] = clock64(); \
+    } while (0)
+#else
+#define EX_TRACE(slot_) \
+    do {                \
+    } while (0)
+#endif
+
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 
 // Exact-order run sum of one unit from its precomputed run list: runs are
 // consumed in order, the next run's loads issued before the current run's
 // adds (they do not depend on acc), every term rounded as accumulate_run does.
 template <int KAP>
 __device__ __forceinline__ double run_list_sum(const int32_t *cells, const double *coefs, int nr,
-                                               const double *x) {
+                                               const double *x, int pf) {
     double acc = 0.0;
     if (nr <= 0) return acc;
+    // global-memory vector: the unit is a chain of dependent adds whose loads
+    // are known in advance, so the next PF_RUNS runs are pulled into L1 first
+    // (their latency then overlaps the adds; no register cost)
+    if (pf)
+        for (int r = 0; r < nr && r < PF_RUNS; ++r) prefetch_l1(x + cells[r]);
     double xc[KAP], cc = coefs[0];
     {
         const double *p0 = x + cells[0];
@@ -172,6 +197,7 @@ __device__ __forceinline__ double run_list_sum(const int32_t *cells, const doubl
     }
     for (int r = 0; r < nr; ++r) {
         double xn[KAP], cn = 0.0;
+        if (pf && r + PF_RUNS < nr) prefetch_l1(x + cells[r + PF_RUNS]);
         if (r + 1 < nr) {
             const double *pn = x + cells[r + 1];
             cn = coefs[r + 1];
@@ -188,10 +214,10 @@ __device__ __forceinline__ double run_list_sum(const int32_t *cells, const doubl
 }
 
 __device__ __forceinline__ double run_list_sum_any(const int32_t *cells, const double *coefs,
-                                                   int nr, const double *x, int kappa) {
+                                                   int nr, const double *x, int kappa, int pf) {
     switch (kappa) {
-        case 2: return run_list_sum<2>(cells, coefs, nr, x);
-        case 4: return run_list_sum<4>(cells, coefs, nr, x);
+        case 2: return run_list_sum<2>(cells, coefs, nr, x, pf);
+        case 4: return run_list_sum<4>(cells, coefs, nr, x, pf);
         default: {
             double acc = 0.0;
             for (int r = 0; r < nr; ++r) {
@@ -352,7 +378,8 @@ __device__ __forceinline__ void row_unit(int u, const PairPtrs &P, const G32 &c,
     const int lo = P.rptr[k], hi = P.rptr[k + 1];
     if (UNIFORM && kappa <= 8) {  // cells handled by cell_pass_row (all threads, all cells)
         const int K1 = m / kappa;
-        P.kb[u] = run_list_sum_any(P.rrc + lo * K1, P.rrf + lo * K1, (hi - lo) * K1, bsrc, kappa);
+        P.kb[u] = run_list_sum_any(P.rrc + lo * K1, P.rrf + lo * K1, (hi - lo) * K1, bsrc, kappa,
+                                   P.pf);
         return;
     }
     const int64_t *ids = P.rpc + lo;
@@ -392,7 +419,8 @@ __device__ __forceinline__ void col_unit(int u, const PairPtrs &P, const G32 &c,
     const int lo = P.cptr[l], hi = P.cptr[l + 1];
     if (UNIFORM && kappa <= 8) {  // cells handled by cell_pass_col
         const int K1 = m / kappa;
-        P.kta[u] = run_list_sum_any(P.crc + lo * K1, P.crf + lo * K1, (hi - lo) * K1, asrc, kappa);
+        P.kta[u] = run_list_sum_any(P.crc + lo * K1, P.crf + lo * K1, (hi - lo) * K1, asrc, kappa,
+                                    P.pf);
         return;
     }
     const int64_t *ids = P.cpc + lo;
@@ -551,6 +579,7 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
         P.crc = cl_cells ? cl_cells + a0 * K1 : nullptr;
         P.crf = cl_coef ? cl_coef + a0 * K1 : nullptr;
     }
+    P.pf = !use_smem;
     double *ws = scratch + b * stride_pair;
     P.aA = ws;
     P.aB = ws + N;
@@ -608,26 +637,36 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     bool converged = false;
     while (st == GDT_PAIR_OK && it < max_iter) {
         ++it;
+        EX_TRACE(0);
         Red rc = red_init();
         const double *as = stage(a_cur);
+        EX_TRACE(1);
         for (int u = threadIdx.x; u < U; u += PT)
             col_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, a_cur, rc, as);
+        EX_TRACE(2);
         if (UNIFORM) {
             finish_units(P.kta, rcp_buf);
+            EX_TRACE(3);
             cell_pass_col(P, f, bmap, rc, P.kta, rcp_buf);
         }
         if (__syncthreads_or(rc.zcol)) {  // before anything reads b
             st = GDT_PAIR_ZERO_DENOM_COL;
             break;
         }
+        EX_TRACE(4);
         const double *bsw = stage(P.b);
+        EX_TRACE(5);
         for (int u = threadIdx.x; u < U; u += PT)
             row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, false, a_cur, a_nxt, rc, bsw);
+        EX_TRACE(6);
         if (UNIFORM) {
             finish_units(P.kb, rcp_buf);
+            EX_TRACE(7);
             cell_pass_row(P, f, bmap, false, a_cur, a_nxt, rc, P.kb, rcp_buf);
         }
+        EX_TRACE(8);
         block_reduce_red(rc, sh);
+        EX_TRACE(9);
         // _check_scale_range(a), then (b) (sinkhorn.py:137-138)
         const bool bad_a = rc.amin <= rc.amax &&
                            (rc.amin < 1e-100 || rc.amax > 1e100 || !isfinite(rc.amax));
@@ -1515,7 +1554,8 @@ __global__ void finish_kernel(const double *__restrict__ tv_part, int tv_ctas,
         tmu += tv_part[(b * tv_ctas + i) * 2];
         tnu += tv_part[(b * tv_ctas + i) * 2 + 1];
     }
-    for (int i = lane; i < pr_ctas; i += 32) pr += pr_part[b * pr_ctas + i];
+    if (pr_part)
+        for (int i = lane; i < pr_ctas; i += 32) pr += pr_part[b * pr_ctas + i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         tmu += __shfl_xor_sync(0xffffffffu, tmu, o);
@@ -1523,7 +1563,7 @@ __global__ void finish_kernel(const double *__restrict__ tv_part, int tv_ctas,
         pr += __shfl_xor_sync(0xffffffffu, pr, o);
     }
     if (lane == 0) {
-        out[b * 8 + 0] = pr;
+        if (pr_part) out[b * 8 + 0] = pr;  // else the caller's kernel priced already
         out[b * 8 + 1] = tmu;
         out[b * 8 + 2] = tnu;
     }
@@ -1650,6 +1690,382 @@ __global__ void sum_parts_kernel(const double *__restrict__ part, int count, dou
     }
 }
 
+// ---------------------------------------------------------------------------
+// Coarse-level primal stage (fp32 mode, uniform kernel, C-bar supplied).
+//
+// With W_ts = W for every cell pair of an arc, every scaling is a per-block
+// quotient of the masses (a_t = mu_t / KB_k, b_s = nu_s / KTA_l), so the
+// sweep of sinkhorn.py:124-141 closes on the coarse plan:
+//   KTA_l = sum_{k -> l} m_kl W S_k,   S_k = sum_{t in X_k} a_t = mu~_k / KB_k,
+//   KB_k  = sum_{l <- k} m_kl W B_l,   B_l = sum_{s in Y_l} b_s = nu~_l / KTA_l,
+// b = 1 on the target support at the start (B_l = its count).  A sweep costs
+// O(arcs) instead of O(cells); the reference's checks keep their order: zero
+// row (top of a sweep), zero column, scale range of a then b (from each
+// block's extreme positive masses: correctly rounded division by a positive
+// constant is monotone), then the gap -- here the coarse residual
+// |S_k KB'_k - mu~_k| + |nu~_l - B_l KTA_l| (the fine one up to rounding).
+// Pricing needs no fine pass:
+//   sum_{t in X_k, s in Y_l} a_t b_s C_ts = G_kl / (KB_k KTA_l) = C-bar_kl S_k B_l
+// with G_kl = sum mu_t nu_s C_ts the numerator of C-bar (costs.py:128-171),
+// which the weighted-cost bound computes anyway: transport^p is the fitted
+// coarse plan priced by C-bar.  The block statistics come from the SumPool
+// pass (gdt_sumpool_stats_f64); the only fine pass left is the weighted TV of
+// the fitted marginals, cell by cell with the reference's arithmetic
+// (tv_pass_kernel, grid-wide).  Summation orders differ from scipy's (the
+// fp32-mode contract is 1e-5 on the bounds); C-bar for p != 2 carries the
+// fp32 kernel's rounding (<= 3.8e-6 relative per entry), for p = 2 it comes
+// from fp64 block moments (~1e-14).
+//
+// primal_coarse_kernel: one CTA per pair, the plan in shared memory.  Block
+// sums over arcs run one thread per block, except blocks with more than
+// CB_HEAVY arcs (skewed plans): those are summed by a warp (lane-strided,
+// fixed butterfly: deterministic) so no thread serialises a long arc list.
+// ---------------------------------------------------------------------------
+constexpr int CT = 512;       // threads of primal_coarse_kernel
+constexpr int CB_HEAVY = 16;  // arcs above which a block's sum goes to a warp
+enum { CB_MLO, CB_MHI, CB_NLO, CB_NHI, CB_CMU, CB_CNU, CB_S, CB_B, CB_K0, CB_K1, CB_KTA, CB_RK,
+       CB_NF };
+
+struct CoarsePlan {
+    int rp, cp, rcol, rcoef, crow, ccoef, arow, heavy, blk, total;
+};
+
+__host__ __device__ inline CoarsePlan coarse_plan(int n) {
+    CoarsePlan m;
+    const int cap = 2 * n;
+    int o = 0;
+    m.rp = o;
+    o = fp_al(o + 4 * (n + 1));
+    m.cp = o;
+    o = fp_al(o + 4 * (n + 1));
+    m.rcol = o;
+    o = fp_al(o + 4 * cap);
+    m.rcoef = o;
+    o = fp_al(o + 8 * cap);
+    m.crow = o;
+    o = fp_al(o + 4 * cap);
+    m.ccoef = o;
+    o = fp_al(o + 8 * cap);
+    m.arow = o;
+    o = fp_al(o + 4 * cap);
+    m.heavy = o;  // heavy row blocks, then heavy column blocks
+    o = fp_al(o + 4 * 2 * n);
+    m.blk = o;
+    o = fp_al(o + 8 * CB_NF * n);
+    m.total = o;
+    return m;
+}
+
+struct CoarseRed {
+    double gap, alo, ahi, blo, bhi;
+    int flags;  // 1 zero row (next sweep), 2 zero column, 4 non-finite
+};
+
+__device__ __forceinline__ CoarseRed cr_init() {
+    return CoarseRed{0.0, INFINITY, -INFINITY, INFINITY, -INFINITY, 0};
+}
+
+// deterministic CTA reduction: xor butterflies per warp, then warp 0 folds
+// the per-warp records in warp order; every thread gets the result
+__device__ CoarseRed cr_reduce(CoarseRed r, CoarseRed *sh) {
+    auto fold = [](CoarseRed &x) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            x.gap += __shfl_xor_sync(0xffffffffu, x.gap, o);
+            x.alo = fmin(x.alo, __shfl_xor_sync(0xffffffffu, x.alo, o));
+            x.ahi = fmax(x.ahi, __shfl_xor_sync(0xffffffffu, x.ahi, o));
+            x.blo = fmin(x.blo, __shfl_xor_sync(0xffffffffu, x.blo, o));
+            x.bhi = fmax(x.bhi, __shfl_xor_sync(0xffffffffu, x.bhi, o));
+            x.flags |= __shfl_xor_sync(0xffffffffu, x.flags, o);
+        }
+    };
+    fold(r);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) sh[w] = r;
+    __syncthreads();
+    if (w == 0) {
+        CoarseRed o = lane < CT / 32 ? sh[lane] : cr_init();
+        fold(o);
+        if (lane == 0) sh[CT / 32] = o;
+    }
+    __syncthreads();
+    const CoarseRed out = sh[CT / 32];
+    __syncthreads();
+    return out;
+}
+
+__device__ __forceinline__ double cr_sum(double v, double *sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        double x = lane < CT / 32 ? sh[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) sh[CT / 32] = x;
+    }
+    __syncthreads();
+    const double out = sh[CT / 32];
+    __syncthreads();
+    return out;
+}
+
+// out[u] = sum_{e in [ptr[u], ptr[u+1])} coef[e] * x[idx[e]] for every block u:
+// light blocks one thread each, heavy ones (listed in `heavy`) one warp each
+__device__ __forceinline__ void coarse_matvec(const int *ptr, const int *idx, const double *coef,
+                                              const double *x, double *out, int n,
+                                              const int *heavy, int nheavy) {
+    for (int u = threadIdx.x; u < n; u += CT) {
+        const int e0 = ptr[u], e1 = ptr[u + 1];
+        if (e1 - e0 > CB_HEAVY) continue;
+        double s = 0.0;
+        for (int e = e0; e < e1; ++e) s += coef[e] * x[idx[e]];
+        out[u] = s;
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int h = w; h < nheavy; h += CT / 32) {
+        const int u = heavy[h], e0 = ptr[u], e1 = ptr[u + 1];
+        double s = 0.0;
+        for (int e = e0 + lane; e < e1; e += 32) s += coef[e] * x[idx[e]];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) out[u] = s;
+    }
+}
+
+__global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
+    const double *__restrict__ mu_c, const double *__restrict__ nu_c,
+    const double *__restrict__ stats, const double *__restrict__ cbar,
+    const int64_t *__restrict__ arc_off, const int32_t *__restrict__ row_ptr,
+    const int32_t *__restrict__ row_arc_col, const double *__restrict__ row_arc_mass,
+    const int32_t *__restrict__ col_ptr, const int32_t *__restrict__ col_arc_row,
+    const double *__restrict__ col_arc_mass, const double *__restrict__ W,
+    const double *__restrict__ xi_in, int64_t max_iter, int n, int64_t batch,
+    double *__restrict__ blk_out, double *__restrict__ out, int32_t *__restrict__ status) {
+    __shared__ CoarseRed shr[CT / 32 + 1];
+    __shared__ double shd[CT / 32 + 1];
+    __shared__ int nheavy_s[2];
+    extern __shared__ __align__(16) unsigned char csm[];
+    const int64_t b = blockIdx.x;
+    const double Wu = W[0];
+    const double *mcb = mu_c + b * n, *ncb = nu_c + b * n;
+    const double *smu = stats + b * n * 3, *snu = stats + (batch + b) * n * 3;
+    const int64_t a0 = arc_off[b];
+    const int A = (int)(arc_off[b + 1] - a0);
+    const CoarsePlan L = coarse_plan(n);
+    int *rp = reinterpret_cast<int *>(csm + L.rp), *cp = reinterpret_cast<int *>(csm + L.cp);
+    int *rcol = reinterpret_cast<int *>(csm + L.rcol), *crow = reinterpret_cast<int *>(csm + L.crow);
+    int *arow = reinterpret_cast<int *>(csm + L.arow);
+    int *hrow = reinterpret_cast<int *>(csm + L.heavy), *hcol = hrow + n;
+    double *rcoef = reinterpret_cast<double *>(csm + L.rcoef);
+    double *ccoef = reinterpret_cast<double *>(csm + L.ccoef);
+    double *blk = reinterpret_cast<double *>(csm + L.blk);
+    double *Bmlo = blk + CB_MLO * n, *Bmhi = blk + CB_MHI * n, *Bnlo = blk + CB_NLO * n,
+           *Bnhi = blk + CB_NHI * n, *Bcmu = blk + CB_CMU * n, *Bcnu = blk + CB_CNU * n,
+           *BS = blk + CB_S * n, *BB = blk + CB_B * n, *KTA = blk + CB_KTA * n,
+           *RK = blk + CB_RK * n;
+    double *Kcur = blk + CB_K0 * n, *Knext = blk + CB_K1 * n;
+
+    // ---- the pair's coarse plan and block statistics into shared memory
+    if (threadIdx.x < 2) nheavy_s[threadIdx.x] = 0;
+    for (int i = threadIdx.x; i <= n; i += CT) {
+        rp[i] = row_ptr[b * (n + 1) + i];
+        cp[i] = col_ptr[b * (n + 1) + i];
+    }
+    for (int e = threadIdx.x; e < A; e += CT) {
+        rcol[e] = row_arc_col[a0 + e];
+        rcoef[e] = __dmul_rn(row_arc_mass[a0 + e], Wu);
+        crow[e] = col_arc_row[a0 + e];
+        ccoef[e] = __dmul_rn(col_arc_mass[a0 + e], Wu);
+    }
+    double cnt = 0.0;
+    for (int k = threadIdx.x; k < n; k += CT) {
+        Bmlo[k] = smu[3 * k];
+        Bmhi[k] = smu[3 * k + 1];
+        Bcmu[k] = smu[3 * k + 2];
+        Bnlo[k] = snu[3 * k];
+        Bnhi[k] = snu[3 * k + 1];
+        Bcnu[k] = snu[3 * k + 2];
+        cnt += Bcmu[k] + Bcnu[k];
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < n; k += CT) {
+        for (int e = rp[k]; e < rp[k + 1]; ++e) arow[e] = k;
+        if (rp[k + 1] - rp[k] > CB_HEAVY) hrow[atomicAdd(&nheavy_s[0], 1)] = k;
+        if (cp[k + 1] - cp[k] > CB_HEAVY) hcol[atomicAdd(&nheavy_s[1], 1)] = k;
+    }
+    cnt = cr_sum(cnt, shd);  // (its barriers also publish the tables above)
+    const int nhr = nheavy_s[0], nhc = nheavy_s[1];
+    // the heavy lists are sets: their order only decides which warp sums a block
+    const double xi = xi_in[b] < 0.0 ? 1e-9 * cnt : xi_in[b];
+
+    // ---- kb = K b with b = 1 on the target support (sinkhorn.py:119-120)
+    coarse_matvec(rp, rcol, rcoef, Bcnu, Kcur, n, hrow, nhr);
+    __syncthreads();
+    int zrow = 0;
+    for (int k = threadIdx.x; k < n; k += CT)
+        if (Bcmu[k] > 0.0 && Kcur[k] <= 0.0) zrow = 1;
+    int st = __syncthreads_or(zrow) ? GDT_PAIR_ZERO_DENOM_ROW : GDT_PAIR_OK;
+    int64_t it = 0;
+    double gap = INFINITY;
+    bool converged = false;
+    while (st == GDT_PAIR_OK && it < max_iter) {
+        ++it;
+        // a = mu / kb: block sums S_k (quotients correctly rounded: div_shared,
+        // Markstein from one reciprocal per denominator)
+        for (int k = threadIdx.x; k < n; k += CT) {
+            const double den = Kcur[k];
+            const double rk = fp_rcp(den);
+            RK[k] = rk;
+            BS[k] = (Bcmu[k] > 0.0 && den > 0.0) ? div_shared(mcb[k], den, rk) : 0.0;
+        }
+        __syncthreads();
+        // kta = K^T a
+        coarse_matvec(cp, crow, ccoef, BS, KTA, n, hcol, nhc);
+        __syncthreads();
+        // zero-column check, b = nu / kta: block sums B_l, column residual, range(b)
+        CoarseRed r = cr_init();
+        for (int l = threadIdx.x; l < n; l += CT) {
+            const double s = KTA[l];
+            double bl = 0.0;
+            if (Bcnu[l] > 0.0) {
+                if (s <= 0.0) {
+                    r.flags |= 2;
+                } else {
+                    const double rs = __drcp_rn(s);
+                    bl = div_shared(ncb[l], s, rs);
+                    r.gap += fabs(__dsub_rn(ncb[l], __dmul_rn(bl, s)));
+                    const double lo = div_shared(Bnlo[l], s, rs), hi = div_shared(Bnhi[l], s, rs);
+                    if (isnan(lo) || isnan(hi) || !isfinite(hi)) r.flags |= 4;
+                    if (lo > 0.0) r.blo = fmin(r.blo, lo);
+                    if (hi > 0.0) r.bhi = fmax(r.bhi, hi);
+                }
+            }
+            BB[l] = bl;
+        }
+        __syncthreads();
+        // kb' = K b
+        coarse_matvec(rp, rcol, rcoef, BB, Knext, n, hrow, nhr);
+        __syncthreads();
+        // range of a (from kb), the row residual, the next sweep's zero-row check
+        for (int k = threadIdx.x; k < n; k += CT) {
+            if (Bcmu[k] > 0.0) {
+                const double den = Kcur[k], rk = RK[k], s = Knext[k];
+                if (den > 0.0) {
+                    const double lo = div_shared(Bmlo[k], den, rk), hi = div_shared(Bmhi[k], den, rk);
+                    if (isnan(lo) || isnan(hi) || !isfinite(hi)) r.flags |= 4;
+                    if (lo > 0.0) r.alo = fmin(r.alo, lo);
+                    if (hi > 0.0) r.ahi = fmax(r.ahi, hi);
+                }
+                r.gap += fabs(__dsub_rn(__dmul_rn(BS[k], s), mcb[k]));
+                if (s <= 0.0) r.flags |= 1;
+            }
+        }
+        const CoarseRed q = cr_reduce(r, shr);
+        if (q.flags & 2) {
+            st = GDT_PAIR_ZERO_DENOM_COL;
+            break;
+        }
+        if (fp_bad(q.alo, q.ahi) || fp_bad(q.blo, q.bhi) || (q.flags & 4)) {
+            st = GDT_PAIR_OVERFLOW;
+            break;
+        }
+        gap = q.gap;
+        if (gap < xi) {
+            converged = true;
+            break;
+        }
+        if (it >= max_iter) break;
+        if (q.flags & 1) {  // the check at the top of the next sweep
+            st = GDT_PAIR_ZERO_DENOM_ROW;
+            break;
+        }
+        double *t = Kcur;  // kb' defines a of the next sweep
+        Kcur = Knext;
+        Knext = t;
+    }
+    // ---- pricing: the fitted coarse plan S_k (m W) B_l against C-bar (flat
+    //      over the arcs: balanced; per-thread partials in a fixed order)
+    double price = 0.0;
+    const bool ok = st == GDT_PAIR_OK && it >= 1;
+    if (ok)
+        for (int e = threadIdx.x; e < A; e += CT) {
+            const int k = arow[e], l = rcol[e];
+            price += __dmul_rn(__dmul_rn(BS[k], rcoef[e]), BB[l]) *
+                     __ldg(cbar + ((int64_t)b * n + k) * n + l);
+        }
+    price = cr_sum(price, shd);
+    // per-block denominators of the final a (kb), of the plan's row marginal
+    // (kb') and of b (kta), for the weighted-TV pass
+    double *bo = blk_out + b * 3 * n;
+    for (int k = threadIdx.x; k < n; k += CT) {
+        bo[k] = ok ? Kcur[k] : 0.0;
+        bo[n + k] = ok ? Knext[k] : 0.0;
+        bo[2 * n + k] = ok ? KTA[k] : 0.0;
+    }
+    if (threadIdx.x == 0) {
+        status[b] = st;
+        double *o = out + b * 8;
+        o[0] = price;
+        o[1] = 0.0;
+        o[2] = 0.0;
+        o[3] = gap;
+        o[4] = (double)it;
+        o[5] = converged ? 1.0 : 0.0;
+        o[6] = cnt;
+        o[7] = 0.0;
+    }
+}
+
+// Weighted TV of the fitted plan's marginals (quantized.py:357-363):
+//   mu^ = a (K b) = a KB'_k, nu^ = b (K^T a) = b KTA_l, a = mu / KB_k, b = nu / KTA_l,
+// inner sums sum_i w_i |mu^_i - mu_i| and sum_i w_i |nu^_i - nu_i| with the
+// reference's per-cell arithmetic (correctly rounded quotients; w = tv_weights
+// of the padded grid, measures.py:289-296).  Grid-wide, coalesced; one
+// partial pair per CTA (fixed order: deterministic).
+constexpr int TVT = 256, TV_CELLS = 16;  // threads, cells per thread of tv_pass_kernel
+
+__global__ void __launch_bounds__(TVT) tv_pass_kernel(
+    const double *__restrict__ mu, const double *__restrict__ nu,
+    const double *__restrict__ blk, const int32_t *__restrict__ status,
+    const double *__restrict__ tv_w, const int32_t *__restrict__ bmap, int N, int n,
+    double *__restrict__ part) {
+    __shared__ double sh[32];
+    const int64_t b = blockIdx.y;
+    double tmu = 0.0, tnu = 0.0;
+    if (status[b] == GDT_PAIR_OK) {
+        const double *mub = mu + b * N, *nub = nu + b * N;
+        const double *k0 = blk + b * 3 * n, *k1 = k0 + n, *kt = k0 + 2 * n;
+        const int base = blockIdx.x * TVT * TV_CELLS + threadIdx.x;
+#pragma unroll 4
+        for (int q = 0; q < TV_CELLS; ++q) {
+            const int i = base + q * TVT;
+            if (i >= N) break;
+            const double mi = mub[i], ni = nub[i], w = __ldg(tv_w + i);
+            const int k = __ldg(bmap + i);
+            if (mi > 0.0) {
+                const double den = __ldg(k0 + k);
+                const double ai = fp_scale(mi, den, fp_rcp(den));
+                tmu += w * fabs(__dsub_rn(__dmul_rn(ai, __ldg(k1 + k)), mi));
+            }
+            if (ni > 0.0) {
+                const double den = __ldg(kt + k);
+                const double bi = fp_scale(ni, den, fp_rcp(den));
+                tnu += w * fabs(__dsub_rn(__dmul_rn(bi, den), ni));
+            }
+        }
+    }
+    tmu = block_sum<TVT>(tmu, sh);
+    tnu = block_sum<TVT>(tnu, sh);
+    if (threadIdx.x == 0) {
+        double *pp = part + ((int64_t)b * gridDim.x + blockIdx.x) * 2;
+        pp[0] = tmu;
+        pp[1] = tnu;
+    }
+}
+
 // scratch layout per pair: [aA N][aB N][b N][kb U][kta U]; then, after all
 // pairs: moments [B, n, MW], tv partials [B, tv_ctas, 2], price partials
 // [B, pr_ctas]
@@ -1706,7 +2122,10 @@ extern "C" int64_t gdt_primal_scratch_bytes(int64_t batch, int ndim, const int64
     return (int64_t)sizeof(double) * L.total;
 }
 
-extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int64_t *arc_off,
+extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const double *mu_c,
+                                  const double *nu_c, const double *stats, const double *cbar,
+                                  const double *tv_w, const int32_t *bmap_in,
+                                  const int64_t *arc_off,
                                   const int32_t *row_ptr, const int32_t *row_arc_col,
                                   const double *row_arc_mass, const int32_t *col_ptr,
                                   const int32_t *col_arc_row, const double *col_arc_mass,
@@ -1733,6 +2152,29 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const int6
     GDT_CHECK_ARG(c.n[0] < 65536 && c.n[1] < 65536 && c.n[2] < 65536 && c.n[3] < 65536,
                   "gdt_primal_upscale: coarse axes must be < 65536");
     const bool fast_ipf = uni && mode == GDT_MODE_FAST;
+    if (fast_ipf && cbar != nullptr && mu_c != nullptr && nu_c != nullptr && stats != nullptr &&
+        tv_w != nullptr && bmap_in != nullptr) {
+        const CoarsePlan plan = coarse_plan((int)c.cells);
+        if (plan.total <= 200 * 1024) {
+            // the whole primal stage at the coarse level: sweeps + pricing
+            // (one CTA per pair), the weighted-TV pass (grid-wide), the fold
+            const int n = (int)c.cells;
+            double *blk = ws;                             // [batch, 3, n]
+            double *tvp = ws + batch * 3 * c.cells;       // [batch, tv_ctas, 2]
+            const int tv_ctas = (int)((f.cells + TVT * TV_CELLS - 1) / (TVT * TV_CELLS));
+            if (plan.total > 48 * 1024)
+                cudaFuncSetAttribute(primal_coarse_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, plan.total);
+            primal_coarse_kernel<<<(unsigned)batch, CT, plan.total, st>>>(
+                mu_c, nu_c, stats, cbar, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr,
+                col_arc_row, col_arc_mass, kernel_w, xi, max_iter, n, batch, blk, out, status);
+            tv_pass_kernel<<<dim3((unsigned)tv_ctas, (unsigned)batch), TVT, 0, st>>>(
+                mu, nu, blk, status, tv_w, bmap_in, (int)f.cells, n, tvp);
+            finish_kernel<<<grid_size(batch * 32, 128), 128, 0, st>>>(tvp, tv_ctas, nullptr, 0,
+                                                                     status, out, batch);
+            return cuda_status("gdt_primal_upscale (coarse)");
+        }
+    }
     int64_t *rpc = reinterpret_cast<int64_t *>(ws + L.pc_off);
     int64_t *cpc = rpc + batch * 2 * c.cells;
     const int64_t per_pair = 2 * c.cells;
@@ -1882,6 +2324,12 @@ extern "C" int gdt_price_coo(const int64_t *row, const int64_t *col, const doubl
 
 
 #ifdef GDT_IPF_TRACE
+extern "C" int gdt_debug_ex_trace(long long *host) {
+    return cudaMemcpyFromSymbol(host, gdt::g_ex_trace, sizeof(long long) * 16) == cudaSuccess
+               ? 0
+               : -1;
+}
+
 extern "C" int gdt_debug_ipf_trace(unsigned long long *host) {
     return cudaMemcpyFromSymbol(host, gdt::g_ipf_trace, sizeof(unsigned long long) * 128) ==
                    cudaSuccess

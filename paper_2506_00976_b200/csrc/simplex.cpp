@@ -58,6 +58,20 @@ struct DenseCost {
     void runs(int64_t i, int64_t j0, int64_t j1, F &&fn) const {
         fn(C + i * nt + j0, j0, j1 - j0);
     }
+    // lambda-free run iteration (the AVX-512 loops inline their run kernels)
+    struct Cursor {
+        const double *row;
+        int64_t j, j1;
+    };
+    Cursor begin(int64_t i, int64_t j0, int64_t j1) const { return Cursor{C + i * nt, j0, j1}; }
+    bool next(Cursor &c, const double *&cs, int64_t &js, int64_t &len) const {
+        if (c.j >= c.j1) return false;
+        cs = c.row + c.j;
+        js = c.j;
+        len = c.j1 - c.j;
+        c.j = c.j1;
+        return true;
+    }
 };
 
 // cost(i, j) = T[sum_a (x_j,a - x_i,a + cd_a - 1) * tstride_a] on a full grid
@@ -99,6 +113,36 @@ struct GridCost {
                 ++xj[a + 1];
             }
         }
+    }
+    struct Cursor {
+        int64_t xj[GDT_MAX_DIM];
+        int64_t off, j, j1;
+    };
+    Cursor begin(int64_t i, int64_t j0, int64_t j1) const {
+        Cursor c;
+        int64_t xi[GDT_MAX_DIM];
+        coords(i, xi);
+        coords(j0, c.xj);
+        c.off = 0;
+        for (int a = 0; a < nd; ++a) c.off += (c.xj[a] - xi[a] + cd[a] - 1) * tstride[a];
+        c.j = j0;
+        c.j1 = j1;
+        return c;
+    }
+    bool next(Cursor &c, const double *&cs, int64_t &js, int64_t &len) const {
+        if (c.j >= c.j1) return false;
+        len = std::min<int64_t>(cd[0] - c.xj[0], c.j1 - c.j);
+        cs = T + c.off;
+        js = c.j;
+        c.j += len;
+        c.xj[0] += len;
+        c.off += len;
+        for (int a = 0; a < nd - 1 && c.xj[a] >= cd[a]; ++a) {
+            c.xj[a] -= cd[a];
+            c.off += tstride[a + 1] - cd[a] * tstride[a];
+            ++c.xj[a + 1];
+        }
+        return true;
     }
 };
 
@@ -178,7 +222,7 @@ __attribute__((target("avx512f"))) inline __m512d run_acc_avx512(__m512d acc, co
 // reduced cost equals the block minimum; given that minimum (computed with the
 // same arithmetic), an equality search finds the same arc.
 
-__attribute__((target("avx512f"))) int64_t run_find_avx512(const double *cs, const double *vs,
+__attribute__((target("avx512f"))) inline int64_t run_find_avx512(const double *cs, const double *vs,
                                                            int64_t len, double ui, double m) {
     const __m512d uu = _mm512_set1_pd(ui), mm = _mm512_set1_pd(m);
     int64_t t = 0;
@@ -319,14 +363,39 @@ struct Solver {
         while (a < hi) {
             const int64_t j1 = std::min<int64_t>(nt, j + (hi - a));
             const __m512d uu = _mm512_set1_pd(pot[i]);
-            cost.runs(i, j, j1, [&](const double *cs, int64_t js, int64_t len) {
-                acc = run_acc_avx512(acc, cs, v_ + js, len, uu);
-            });
+            // explicit run loop: a lambda here would not inherit the avx512
+            // target and would call the run kernel out of line, passing zmm
+            // arguments through memory
+            auto cur = cost.begin(i, j, j1);
+            const double *cs;
+            int64_t js, len;
+            while (cost.next(cur, cs, js, len)) acc = run_acc_avx512(acc, cs, v_ + js, len, uu);
             a += j1 - j;
             j = 0;
             ++i;
         }
         return _mm512_reduce_min_pd(acc);
+    }
+
+    __attribute__((target("avx512f"))) int64_t find_first_avx512(int64_t a, int64_t hi,
+                                                                  double m) const {
+        const double *v_ = pot.data() + ns;
+        int64_t i = a / nt, j = a - i * nt;
+        while (a < hi) {
+            const int64_t j1 = std::min<int64_t>(nt, j + (hi - a));
+            const double ui = pot[i];
+            auto cur = cost.begin(i, j, j1);
+            const double *cs;
+            int64_t js, len;
+            while (cost.next(cur, cs, js, len)) {
+                const int64_t t = run_find_avx512(cs, v_ + js, len, ui, m);
+                if (t >= 0) return i * nt + js + t;
+            }
+            a += j1 - j;
+            j = 0;
+            ++i;
+        }
+        return -1;
     }
 
     double block_min(int64_t a, int64_t hi) const {
@@ -349,6 +418,7 @@ struct Solver {
     // first arc of [a, hi) whose reduced cost equals m (the block minimum):
     // the arc the reference's strict-< scan ends on
     int64_t find_first(int64_t a, int64_t hi, double m) const {
+        if (simd == 2) return find_first_avx512(a, hi, m);
         const double *v_ = pot.data() + ns;
         int64_t i = a / nt, j = a - i * nt, found = -1;
         while (a < hi && found < 0) {
@@ -408,15 +478,40 @@ struct Solver {
         // sizes between the two cycle sides and the join
         for (int32_t w = hv[u_out].par; w != join; w = hv[w].par) sz[w] -= S;
         for (int32_t w = p_root; w != join; w = hv[w].par) sz[w] += S;
+        // reverse the stem first, so the relabel below can run while T's new
+        // preorder is collected (every node's new parent precedes it)
+        for (int i = k - 1; i >= 1; --i) {
+            hv[stem[i]].par = stem[i - 1];
+            nd[stem[i]].pslot = stem_slot[i - 1];
+            hv[stem[i]].ck = sl[stem_slot[i - 1]].ck;
+            sz[stem[i]] = S - stem_sz[i - 1];
+        }
+        hv[q_root].par = p_root;
+        nd[q_root].pslot = in_slot;
+        hv[q_root].ck = sl[in_slot].ck;
+        sz[q_root] = S;
         // T's new preorder: subtree(s_0), then for each s_i its old subtree
-        // minus subtree(s_{i-1}) (s_i first), which is two contiguous pieces
+        // minus subtree(s_{i-1}) (s_i first), which is two contiguous pieces;
+        // each node is relabelled as it is collected: its potential recomputed
+        // from its (new) parent along its tree arc (_simplex.py:284-330; the
+        // values do not depend on the visiting order, parents come first)
         int32_t *t = tmp.data();
         int32_t m = 0;
-        for (int32_t i = stem_pos[0]; i < stem_pos[0] + stem_sz[0]; ++i) t[m++] = pre[i];
+        double *P = pot.data();
+        Hot *H = hv.data();
+        const int32_t *pr = pre.data();
+        auto emit = [&](int32_t lo, int32_t hi) {
+            for (int32_t x = lo; x < hi; ++x) {
+                const int32_t w = pr[x];
+                t[m++] = w;
+                const Hot &h = H[w];
+                P[w] = h.ck - P[h.par];
+            }
+        };
+        emit(stem_pos[0], stem_pos[0] + stem_sz[0]);
         for (int i = 1; i < k; ++i) {
-            for (int32_t x = stem_pos[i]; x < stem_pos[i - 1]; ++x) t[m++] = pre[x];
-            for (int32_t x = stem_pos[i - 1] + stem_sz[i - 1]; x < stem_pos[i] + stem_sz[i]; ++x)
-                t[m++] = pre[x];
+            emit(stem_pos[i], stem_pos[i - 1]);
+            emit(stem_pos[i - 1] + stem_sz[i - 1], stem_pos[i] + stem_sz[i]);
         }
         // T becomes a child subtree of p_root: its block goes right after p_root
         // or right after p_root's subtree, whichever moves fewer entries (the
@@ -428,36 +523,16 @@ struct Solver {
         int32_t start;
         if (x >= a + S) {  // [a + S, x) moves left by S
             std::memmove(&pre[a], &pre[a + S], sizeof(int32_t) * (x - a - S));
-            for (int32_t i = a; i < x - S; ++i) hv[pre[i]].pos = i;
+            for (int32_t i = a; i < x - S; ++i) H[pre[i]].pos = i;
             start = x - S;
         } else {  // [x, a) moves right by S
             std::memmove(&pre[x + S], &pre[x], sizeof(int32_t) * (a - x));
-            for (int32_t i = x + S; i < a + S; ++i) hv[pre[i]].pos = i;
+            for (int32_t i = x + S; i < a + S; ++i) H[pre[i]].pos = i;
             start = x;
         }
-        // reverse the stem
-        for (int i = k - 1; i >= 1; --i) {
-            hv[stem[i]].par = stem[i - 1];
-            nd[stem[i]].pslot = stem_slot[i - 1];
-            hv[stem[i]].ck = sl[stem_slot[i - 1]].ck;
-            sz[stem[i]] = S - stem_sz[i - 1];
-        }
-        hv[q_root].par = p_root;
-        nd[q_root].pslot = in_slot;
-        hv[q_root].ck = sl[in_slot].ck;
-        sz[q_root] = S;
-        // place and relabel T in preorder: every potential recomputed from its
-        // (new) parent along its tree arc
-        double *P = pot.data();
-        Hot *H = hv.data();
-        int32_t *pre_ = pre.data() + start;
-        for (int32_t i = 0; i < S; ++i) {
-            const int32_t w = t[i];
-            Hot &h = H[w];
-            pre_[i] = w;
-            h.pos = start + i;
-            P[w] = h.ck - P[h.par];
-        }
+        // place T
+        std::memcpy(&pre[start], t, sizeof(int32_t) * S);
+        for (int32_t i = 0; i < S; ++i) H[t[i]].pos = start + i;
     }
 
     // warm = true: (bi, bj, bf) already hold a feasible spanning-tree basis

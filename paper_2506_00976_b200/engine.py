@@ -33,7 +33,8 @@ from .device import device, pinned_empty, stream, to_dev, to_host, to_host_pinne
 from .errors import DimensionMismatchError, GridotError, NumericOverflowError, \
     ZeroDenominatorError
 from .exact import LPBatch, TransportProblem, build_transport_problem, solve_transport_many
-from .measures import CoarseningSpec, GridSpec, coarsen_grid, pad_batch, sumpool_batch
+from .measures import (CoarseningSpec, GridSpec, block_index_map, coarsen_grid, pad_batch,
+                       sumpool_batch, tv_weights)
 from .reports import BoundReport, signed_root
 
 __all__ = ["QUANT_METHODS", "CoarsePlans", "DevicePlans", "quantized_bounds", "prepare_coarse",
@@ -91,6 +92,7 @@ class _Batch:
         self.ctil_dev = to_dev(self.ctil)
         self.table_dev = None
         self.max_sq = 0
+        self.cbar_dev = None  # C-bar of the batch once _cbar ran
         if self.p != 2.0:
             self.max_sq = max(max_sq_of(self.pdims), max_sq_of(self.dims))
             self.table_dev = to_dev(cost_table(self.max_sq, self.p))
@@ -100,8 +102,12 @@ class _Batch:
         """Zero padding + SumPool (K1) of both sides; re-run per step by the bench."""
         self.mu_pad, _ = pad_batch(self.mu, self.dims, self.kappa)
         self.nu_pad, _ = pad_batch(self.nu, self.dims, self.kappa)
-        self.mu_c = sumpool_batch(self.mu_pad, self.pdims, self.kappa)
-        self.nu_c = sumpool_batch(self.nu_pad, self.pdims, self.kappa)
+        # block statistics of both sides from the same pass (mu then nu): the
+        # fp32-mode primal stage works on them instead of the fine masses
+        t = self.t
+        self.stats = t.empty((2, self.B, self.n, 3), dtype=t.float64, device=self.dev)
+        self.mu_c = sumpool_batch(self.mu_pad, self.pdims, self.kappa, self.stats[0])
+        self.nu_c = sumpool_batch(self.nu_pad, self.pdims, self.kappa, self.stats[1])
 
 
 # ---------------------------------------------------------------------------
@@ -115,8 +121,10 @@ def _cbar(bt: _Batch):
     # summation, far inside fp64 mode's 1e-9 bound contract); p != 2: the
     # reference-order fp64 kernel (fp64 mode) or the fp32 FFMA2 kernel
     mode = 1 if bt.p == 2.0 else bt.mode
-    return weighted_cost_batch(bt.mu_pad, bt.nu_pad, bt.mu_c, bt.nu_c, bt.pdims, bt.kappa, bt.p,
-                               mode, bt.ctil_dev, bt.table_dev, want_unused=False)
+    out = weighted_cost_batch(bt.mu_pad, bt.nu_pad, bt.mu_c, bt.nu_c, bt.pdims, bt.kappa, bt.p,
+                              mode, bt.ctil_dev, bt.table_dev, want_unused=False)
+    bt.cbar_dev = out[0]  # kept: the fp32-mode primal stage prices the fitted plan with it
+    return out
 
 
 @dataclass
@@ -540,9 +548,36 @@ class DevicePlans:
         self.prim_status = t.empty(bt.B, dtype=t.int32, device=bt.dev)
 
 
+_GRID_TABLES = {}
+_GRID_LOCK = threading.Lock()
+
+
+def _grid_tables(pdims, kappa, p):
+    """Device copies of the padded grid's tv_weights (the reference's own
+    formula, measures.py:289-296) and its cell -> coarse block map, cached per
+    (device, grid, kappa, p)."""
+    key = (torch().cuda.current_device(), tuple(pdims), int(kappa), float(p))
+    with _GRID_LOCK:
+        hit = _GRID_TABLES.get(key)
+        if hit is None:
+            grid = GridSpec(tuple(pdims))
+            hit = (to_dev(tv_weights(grid, float(p))),
+                   to_dev(block_index_map(grid, CoarseningSpec(int(kappa))).astype(np.int32)))
+            _GRID_TABLES[key] = hit
+    return hit
+
+
 def launch_primal(bt: _Batch, dp: DevicePlans, max_iter):
+    # fp32 mode with C-bar at hand (the weighted-cost bound computed it): the
+    # coarse-level primal stage, priced by C-bar (primal.cu primal_coarse_kernel)
+    cbar = bt.cbar_dev if (bt.mode == 1 and dp.uniform) else None
+    tv_w = bmap = None
+    if cbar is not None:
+        tv_w, bmap = _grid_tables(bt.pdims, bt.kappa, bt.p)
     N.check(N.lib().gdt_primal_upscale(
-        N.ptr(bt.mu_pad), N.ptr(bt.nu_pad), N.ptr(dp.arc_off), N.ptr(dp.row_ptr), N.ptr(dp.rcol),
+        N.ptr(bt.mu_pad), N.ptr(bt.nu_pad), N.ptr(bt.mu_c), N.ptr(bt.nu_c), N.ptr(bt.stats),
+        N.ptr(cbar), N.ptr(tv_w), N.ptr(bmap), N.ptr(dp.arc_off), N.ptr(dp.row_ptr),
+        N.ptr(dp.rcol),
         N.ptr(dp.rmass), N.ptr(dp.col_ptr), N.ptr(dp.crow), N.ptr(dp.cmass), N.ptr(dp.W),
         int(dp.uniform), N.ptr(dp.xi), int(max_iter), bt.p, bt.B, bt.d, N.i64s(bt.pdims),
         bt.kappa, N.ptr(bt.table_dev), bt.max_sq, bt.mode, N.ptr(dp.prim_out),

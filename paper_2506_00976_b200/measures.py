@@ -234,13 +234,18 @@ def pad_batch(x, dims, kappa):
     return out, pd
 
 
-def sumpool_batch(x, dims, kappa):
-    """[B, prod(dims)] -> [B, n_coarse] block sums on the device (bit-exact order)."""
+def sumpool_batch(x, dims, kappa, stats=None):
+    """[B, prod(dims)] -> [B, n_coarse] block sums on the device (bit-exact order).
+
+    ``stats`` (a [B, n_coarse, 3] float64 device tensor) also receives each
+    block's smallest / largest positive mass and positive-cell count from the
+    same pass (gdt_sumpool_stats_f64)."""
     xp, pd = pad_batch(x, dims, kappa)
     nc = int(np.prod(pd)) // kappa ** len(dims)
     out = torch().empty((x.shape[0], nc), dtype=torch().float64, device=x.device)
-    N.check(N.lib().gdt_sumpool_f64(N.ptr(xp), N.ptr(out), x.shape[0], len(dims), N.i64s(pd),
-                                    kappa, stream()), "gdt_sumpool_f64")
+    N.check(N.lib().gdt_sumpool_stats_f64(N.ptr(xp), N.ptr(out), N.ptr(stats), x.shape[0],
+                                          len(dims), N.i64s(pd), kappa, stream()),
+            "gdt_sumpool_stats_f64")
     return out
 
 

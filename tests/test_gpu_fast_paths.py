@@ -218,3 +218,54 @@ def test_fp32_separable_ctransform_bit_exact_emulation(dims):
                               "fp32")
     ref_g = _f32_separable_ct(v.astype(np.float32), dims)
     assert np.array_equal(to_host(g)[0], ref_g)
+
+
+def _all_methods(mus, nus, dims, k, p, precision, **kw):
+    return G.quantized_bounds(mus, nus, dims, k, p, precision=precision, **kw)
+
+
+def test_coarse_primal_matches_exact_small_cases(small_cases):
+    """fp32 mode with the weighted-cost bound requested runs the coarse-level
+    primal stage (primal_coarse_kernel, priced by C-bar); against the exact
+    scipy-order path: same status / exception type, same sweep count, bound
+    within the fp32-mode contract -- on the reference's own small inputs,
+    including partial supports (zero-denominator -> ring fallback), padded
+    grids, 1-D and 3-D."""
+    for c in small_cases:
+        if "kernel" in c:
+            continue
+        mu, nu = inputs_for(c)
+        dims, k, p = c["dims"], c["kappa"], c["p"]
+        e = _all_methods(mu[None], nu[None], dims, k, p, "fp64")[0]["primal_upscaling"]
+        f = _all_methods(mu[None], nu[None], dims, k, p, "fp32")[0]["primal_upscaling"]
+        assert type(e) is type(f), c["tag"]
+        if not isinstance(e, Exception):
+            assert e.iterations == f.iterations, c["tag"]
+            assert e.components["converged"] == f.components["converged"], c["tag"]
+            assert abs(e.value - f.value) <= 1e-5 * abs(e.value), (c["tag"], e.value, f.value)
+
+
+@pytest.mark.parametrize("cfg,k,p,max_iter", [(2, 4, 2.0, 40), (3, 4, 1.0, 7), (3, 8, 1.0, 7),
+                                              (3, 8, 2.0, 30), (4, 8, 2.0, 25),
+                                              (5, 4, 2.0, 9)])
+def test_coarse_primal_fixed_sweeps_tracks_exact(cfg, k, p, max_iter):
+    """Fixed sweep counts (xi = 0): the coarse recursion runs every sweep;
+    transport within 1e-5 (p != 2: C-bar's fp32 rounding) / 1e-12 (p = 2:
+    C-bar from fp64 moments), TV terms at rounding level."""
+    from paper_2506_00976_b200 import synthetic as S
+
+    wl = S.WORKLOADS[cfg]
+    B = 5
+    mus, nus = S.batch(cfg, 0, B)
+    kw = dict(xi=0.0, max_iter=max_iter, return_exceptions=False)
+    ex = _all_methods(mus, nus, wl.dims, k, p, "fp64", **kw)
+    fa = _all_methods(mus, nus, wl.dims, k, p, "fp32", **kw)
+    ttol = 1e-12 if p == 2.0 else 1e-5
+    for b in range(B):
+        e, f = ex[b]["primal_upscaling"], fa[b]["primal_upscaling"]
+        assert e.iterations == f.iterations == max_iter
+        assert abs(e.components["transport"] - f.components["transport"]) <= \
+            ttol * e.components["transport"], (b, e.components, f.components)
+        for key in ("delta_mu", "delta_nu"):
+            assert abs(e.components[key] - f.components[key]) <= 1e-6 * max(1.0, e.value)
+        assert abs(e.value - f.value) <= 1e-5 * abs(e.value), (b, e.value, f.value)
