@@ -602,20 +602,29 @@ def run_b200(args):
     prim_ms = statistics.mean(stage_ms[(k, p, "primal")] for k, p, _, _ in stages)
     sweeps = statistics.mean(
         float(np.mean(E.to_host(dp.prim_out)[:, 4])) for _, _, _, dp in stages)
-    # algorithmic bytes: 48 B per cell and executed sweep
-    # (read b, mu, write a; read a, nu, write b) + 32 B per cell for TV and
-    # pricing.  ipf_fast_kernel (fp32 mode) moves fewer: it recomputes a and
-    # b from mu, nu and the per-block denominators instead of storing them
-    # every sweep (16 B per cell and sweep; the ncu DRAM traffic is in profiles/).
-    ipf_bytes = (48.0 * sweeps + 32.0) * Nf * ppr
-    bytes_model = "(48*S + 32) * N^d bytes per pair (SURVEY.md 8(d))"
-    ipf_roof = {"bound": "hbm", "kernel": ("ipf_fast_kernel" if prec == "fp32" else
-                                           "ipf_kernel") + " + moments_tv + price (primal stage)",
-                "achieved": ipf_bytes / (prim_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
-                "frac": ipf_bytes / (prim_ms / 1000.0) / 1e9 / hbm,
-                "traffic": traffic("ipf_fast_kernel") if prec == "fp32" else None,
-                "traffic_source": tsrc, "sweeps": sweeps,
-                "work": bytes_model + "; stage time includes pricing"}
+    coarse = prec == "fp32" and all(bt.cbar_dev is not None for _, _, bt, _ in stages)
+    if coarse:
+        # fp32 mode: the sweeps run on the coarse plan in shared memory
+        # (O(arcs) per sweep, latency-bound, not a bandwidth stage); the one
+        # fine pass is the weighted TV: read mu and nu once, 16 B per cell
+        # (the TV weights and block map are per-grid tables shared by the batch)
+        ipf_bytes = 16.0 * Nf * ppr
+        ipf_roof = {"bound": "hbm",
+                    "kernel": "tv_pass_kernel + primal_coarse_kernel (fp32 primal stage)",
+                    "work": "16 * N^d bytes per pair (one read of mu, nu by the weighted-TV "
+                            "pass); stage time includes the coarse sweeps and the fold"}
+    else:
+        # fp64 mode, exact order: 48 B per cell and executed
+        # sweep (read b, mu, write a; read a, nu, write b) + 32 B per cell for
+        # TV and pricing
+        ipf_bytes = (48.0 * sweeps + 32.0) * Nf * ppr
+        ipf_roof = {"bound": "hbm", "kernel": "ipf_kernel + moments_tv + price (primal stage)",
+                    "work": "(48*S + 32) * N^d bytes per pair (SURVEY.md 8(d)); stage time "
+                            "includes pricing"}
+    ipf_roof.update({"achieved": ipf_bytes / (prim_ms / 1000.0) / 1e9, "peak": hbm,
+                     "unit": "GB/s", "frac": ipf_bytes / (prim_ms / 1000.0) / 1e9 / hbm,
+                     "traffic": traffic("tv_pass_kernel" if coarse else "ipf_kernel"),
+                     "traffic_source": tsrc, "sweeps": sweeps, "stage_ms": round(prim_ms, 4)})
 
     ct_roofs = {}
     for (k, p_, nm), v in stage_ms.items():
@@ -624,15 +633,27 @@ def run_b200(args):
             ct_roofs[f"k{k}_p{p_:g}_{nm}"] = round(eff, 3)
     ct_roof = None
     if ct_roofs:
-        best = max(ct_roofs.values())
-        ct_roof = {"bound": "fp32", "kernel": "pruned_ct_kernel (fp32, p != 2)",
+        best_key = max(ct_roofs, key=ct_roofs.get)
+        best = ct_roofs[best_key]
+        ct_roof = {"bound": "fp32", "kernel": "pruned_ct_tab_kernel (fp32, p = 1)",
                    "achieved": best, "peak": fp32_peak, "unit": "TFLOP/s",
                    "frac": best / fp32_peak, "traffic": traffic("pruned_ct_tab_kernel"),
                    "traffic_source": tsrc, "per_launch": ct_roofs,
                    "peak_source": peak_src,
-                   "work": "brute-force count 2*N^4 per transform per pair (the reference's "
-                           "algorithm); tile pruning evaluates a subset exactly, so this is an "
-                           "effective rate"}
+                   "work": "brute-force-equivalent count 2*N^4 per transform per pair (the "
+                           "reference's algorithm); tile pruning evaluates a subset exactly, so "
+                           "achieved/frac are effective rates"}
+        # executed-candidate rate: the evaluated fraction of source tiles,
+        # counted by the trace build (scripts/ct_trace.py) on this workload
+        try:
+            tiles = json.load(open(os.path.join(HERE, "profiles", "r02_ct_tiles.json")))
+            fr = tiles[best_key.split("_ct")[0]]["evaluated_fraction"]
+            ct_roof.update({"evaluated_fraction": fr, "achieved_executed": best * fr,
+                            "frac_executed": best * fr / fp32_peak,
+                            "executed_source": "profiles/r02_ct_tiles.json (scripts/ct_trace.py, "
+                                               "trace build, same 45 cfg3 pairs)"})
+        except (OSError, ValueError, KeyError):
+            pass
     if rl is None:
         rl = dict(ipf_roof) if dname == "primal" else {"bound": "hbm", "kernel": dname,
                                                          "achieved": None, "peak": hbm,

@@ -267,6 +267,11 @@ __device__ __forceinline__ void pair_sync(int id) {
 
 constexpr int CT_TAB_TILES = 256;  // (128 / 8)^2 source tiles at most
 
+#ifdef GDT_IPF_TRACE
+// debug builds: source tiles evaluated exactly / visited by the table kernel
+__device__ unsigned long long g_ct_tiles[2];
+#endif
+
 __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
     const float *__restrict__ v, const float *__restrict__ tmax, float *__restrict__ out,
     int64_t batch, Grid g, unsigned long long *__restrict__ counter) {
@@ -380,6 +385,10 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
             const int g0 = max(0, max(t0 * 8 - (X0 + 15), X0 - (t0 * 8 + 7)));
             const int g1 = max(0, max(t1 * 8 - (Y0 + 15), Y0 - (t1 * 8 + 7)));
             const float lb = ct_tab[g1 * CT_TAB_W + g0 + 7] - tm[t];
+#ifdef GDT_IPF_TRACE
+            if (lane == 0) atomicAdd(&g_ct_tiles[1], 1ull);
+            if (lane == 0 && !(lb >= ub)) atomicAdd(&g_ct_tiles[0], 1ull);
+#endif
             if (lb >= ub) continue;
             const int sx0 = t0 * 8, off = sx0 - xj0;
             const int base = off >= 0 ? off : -off;
@@ -508,3 +517,16 @@ int64_t ct_pruned_tiles(const Grid &g) {
 }
 
 }  // namespace gdt
+
+#ifdef GDT_IPF_TRACE
+extern "C" int gdt_debug_ct_tiles(unsigned long long *host, int reset) {
+    if (reset) {
+        const unsigned long long z[2] = {0, 0};
+        return cudaMemcpyToSymbol(gdt::g_ct_tiles, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+    }
+    return cudaMemcpyFromSymbol(host, gdt::g_ct_tiles, sizeof(unsigned long long) * 2) ==
+                   cudaSuccess
+               ? 0
+               : -1;
+}
+#endif

@@ -35,7 +35,7 @@
 
 namespace gdt {
 
-constexpr int PT = 1024;  // threads of the per-pair IPF CTA
+constexpr int PT = 512;  // threads of the per-pair IPF CTA (128 registers each)
 
 struct G32 {  // int32 grid description (cells < 2^31)
     int nd;
@@ -226,6 +226,121 @@ __device__ __forceinline__ double run_list_sum_any(const int32_t *cells, const d
             }
             return acc;
         }
+    }
+}
+
+// Uniform kernel, kappa <= 8: the unit sums in two phases.  (1) Every
+// product coef * x of every run of every unit, in parallel over the runs,
+// written in chain order into a contiguous buffer; (2) one sequential fp64
+// sum per unit over its contiguous products.  The products and the order of
+// the adds are those of run_list_sum (= scipy's CSR/CSC matvec order), so the
+// sums are bit-identical -- but the dependent chain of a long unit now only
+// waits for adds, not for a gather per run.
+template <int KAP>
+__device__ __forceinline__ void run_products(const int32_t *__restrict__ cells,
+                                             const double *__restrict__ coefs, int nruns,
+                                             const double *__restrict__ x,
+                                             double *__restrict__ prod, int kappa) {
+    for (int r = threadIdx.x; r < nruns; r += PT) {
+        const double cf = coefs[r];
+        const double *xp = x + cells[r];
+        if constexpr (KAP >= 2) {
+            double *pp = prod + (int64_t)r * KAP;
+#pragma unroll
+            for (int i = 0; i < KAP; i += 2)
+                *reinterpret_cast<double2 *>(pp + i) =
+                    make_double2(__dmul_rn(cf, xp[i]), __dmul_rn(cf, xp[i + 1]));
+        } else {
+            double *pp = prod + (int64_t)r * kappa;
+            for (int i = 0; i < kappa; ++i) pp[i] = __dmul_rn(cf, xp[i]);
+        }
+    }
+}
+
+// acc = (((0 + p0) + p1) + ...) over `len` contiguous products in shared
+// memory (16-byte aligned when `vec`).  Software-pipelined: the next 8
+// products are loaded while the current 8 are added, so the chain waits only
+// on the adds.
+__device__ __forceinline__ double chain_sum(const double *__restrict__ p, int len, bool vec) {
+    double acc = 0.0;
+    int j = 0;
+    if (vec && len >= 8) {
+        const double2 *q = reinterpret_cast<const double2 *>(p);
+        double2 c0 = q[0], c1 = q[1], c2 = q[2], c3 = q[3];
+        for (; j + 16 <= len; j += 8) {
+            const double2 *qn = reinterpret_cast<const double2 *>(p + j + 8);
+            const double2 n0 = qn[0], n1 = qn[1], n2 = qn[2], n3 = qn[3];
+            acc = __dadd_rn(acc, c0.x);
+            acc = __dadd_rn(acc, c0.y);
+            acc = __dadd_rn(acc, c1.x);
+            acc = __dadd_rn(acc, c1.y);
+            acc = __dadd_rn(acc, c2.x);
+            acc = __dadd_rn(acc, c2.y);
+            acc = __dadd_rn(acc, c3.x);
+            acc = __dadd_rn(acc, c3.y);
+            c0 = n0;
+            c1 = n1;
+            c2 = n2;
+            c3 = n3;
+        }
+        acc = __dadd_rn(acc, c0.x);
+        acc = __dadd_rn(acc, c0.y);
+        acc = __dadd_rn(acc, c1.x);
+        acc = __dadd_rn(acc, c1.y);
+        acc = __dadd_rn(acc, c2.x);
+        acc = __dadd_rn(acc, c2.y);
+        acc = __dadd_rn(acc, c3.x);
+        acc = __dadd_rn(acc, c3.y);
+        j += 8;
+    }
+    for (; j < len; ++j) acc = __dadd_rn(acc, p[j]);
+    return acc;
+}
+
+// out[u] = the exact-order sum of unit u for every unit of the pair.  The
+// products of consecutive units are staged batch by batch (at most `cap`
+// doubles of shared memory per batch); a unit whose products alone exceed
+// `cap` is summed straight from its run list.
+__device__ __noinline__ void unit_sums(const int32_t *cells, const double *coefs,
+                                       const int32_t *ptr, int U, int K1, int kappa,
+                                       const double *x, double *prod, double *out, int cap,
+                                       int pf) {
+    const int per = K1 * kappa;  // products per arc
+    const bool vec = (per & 1) == 0;
+    int u0 = 0;
+    while (u0 < U) {
+        // the batch [u0, u1): as many whole units as fit (every thread computes
+        // the same boundary); an oversized unit forms a batch of its own
+        const int a0 = ptr[u0];
+        int lo = u0 + 1, hi = U;  // largest u1 in [u0 + 1, U] whose products fit
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((int64_t)(ptr[mid] - a0) * per <= cap) lo = mid;
+            else hi = mid - 1;
+        }
+        const int u1 = lo;
+        const bool staged = (int64_t)(ptr[u1] - a0) * per <= cap;
+        if (staged) {
+            const int nruns = (ptr[u1] - a0) * K1;
+            const int32_t *bc = cells + (int64_t)a0 * K1;
+            const double *bf = coefs + (int64_t)a0 * K1;
+            switch (kappa) {
+                case 2: run_products<2>(bc, bf, nruns, x, prod, kappa); break;
+                case 4: run_products<4>(bc, bf, nruns, x, prod, kappa); break;
+                case 8: run_products<8>(bc, bf, nruns, x, prod, kappa); break;
+                default: run_products<0>(bc, bf, nruns, x, prod, kappa); break;
+            }
+            __syncthreads();
+            for (int u = u0 + (int)threadIdx.x; u < u1; u += PT) {
+                const int64_t lo = (int64_t)(ptr[u] - a0) * per, hi = (int64_t)(ptr[u + 1] - a0) * per;
+                out[u] = chain_sum(prod + lo, (int)(hi - lo), vec);
+            }
+            __syncthreads();  // before the next batch overwrites the products
+        } else if (threadIdx.x == 0) {
+            const int lo = ptr[u0] * K1, hi = ptr[u0 + 1] * K1;
+            out[u0] = run_list_sum_any(cells + lo, coefs + lo, hi - lo, x, kappa, pf);
+        }
+        u0 = u1;
     }
 }
 
@@ -467,43 +582,82 @@ __global__ void block_map_kernel(G32 f, G32 c, int kappa, int32_t *__restrict__ 
 // Uniform kernel, phase R cell work spread over every thread: with the
 // block sums kb[] complete, a_next = mu / kb, the gap / range terms of the
 // current a and the zero-row check (same arithmetic as row_unit's cell loop).
+// (cells in groups of CP_U per thread: every independent load of a group is
+// issued before its dependent gathers and arithmetic)
+constexpr int CP_U = 4;
+
 __device__ __forceinline__ void cell_pass_row(const PairPtrs &P, const G32 &f,
                                               const int32_t *__restrict__ bmap, bool init, const double *a_cur,
                                               double *a_next, Red &r, const double *kbs,
                                               const double *rcps) {
-    for (int i = threadIdx.x; i < f.cells; i += PT) {
-        const int k = bmap[i];
-        const double acc = kbs[k];
-        const double mui = P.mu[i];
-        if (!init) {
-            const double ai = a_cur[i];
-            range_acc(ai, r.amin, r.amax, r.nonfinite);
-            if (mui > 0.0) r.gap += fabs(__dsub_rn(__dmul_rn(ai, acc), mui));
+    for (int i0 = threadIdx.x; i0 < f.cells; i0 += PT * CP_U) {
+        int kk[CP_U];
+        double mu_[CP_U], ai_[CP_U], acc_[CP_U], rc_[CP_U];
+#pragma unroll
+        for (int q = 0; q < CP_U; ++q) {
+            const int i = i0 + q * PT;
+            const bool in = i < f.cells;
+            kk[q] = in ? bmap[i] : 0;
+            mu_[q] = in ? P.mu[i] : 0.0;
+            ai_[q] = (in && !init) ? a_cur[i] : 0.0;
         }
-        double an = 0.0;
-        if (mui > 0.0) {
-            if (acc <= 0.0) r.zrow = 1;
-            else an = div_shared(mui, acc, rcps[k]);
+#pragma unroll
+        for (int q = 0; q < CP_U; ++q) {
+            acc_[q] = kbs[kk[q]];
+            rc_[q] = rcps[kk[q]];
         }
-        a_next[i] = an;
+#pragma unroll
+        for (int q = 0; q < CP_U; ++q) {
+            const int i = i0 + q * PT;
+            if (i >= f.cells) break;
+            const double acc = acc_[q], mui = mu_[q];
+            if (!init) {
+                const double ai = ai_[q];
+                range_acc(ai, r.amin, r.amax, r.nonfinite);
+                if (mui > 0.0) r.gap += fabs(__dsub_rn(__dmul_rn(ai, acc), mui));
+            }
+            double an = 0.0;
+            if (mui > 0.0) {
+                if (acc <= 0.0) r.zrow = 1;
+                else an = div_shared(mui, acc, rc_[q]);
+            }
+            a_next[i] = an;
+        }
     }
 }
 
 __device__ __forceinline__ void cell_pass_col(const PairPtrs &P, const G32 &f,
                                               const int32_t *__restrict__ bmap, Red &r, const double *ktas,
                                               const double *rcps) {
-    for (int j = threadIdx.x; j < f.cells; j += PT) {
-        const int l = bmap[j];
-        const double acc = ktas[l];
-        const double nuj = P.nu[j];
-        double bj = 0.0;
-        if (nuj > 0.0) {
-            if (acc <= 0.0) r.zcol = 1;
-            else bj = div_shared(nuj, acc, rcps[l]);
-            range_acc(bj, r.bmin, r.bmax, r.nonfinite);
-            r.gap += fabs(__dsub_rn(nuj, __dmul_rn(bj, acc)));
+    for (int j0 = threadIdx.x; j0 < f.cells; j0 += PT * CP_U) {
+        int ll[CP_U];
+        double nu_[CP_U], acc_[CP_U], rc_[CP_U];
+#pragma unroll
+        for (int q = 0; q < CP_U; ++q) {
+            const int j = j0 + q * PT;
+            const bool in = j < f.cells;
+            ll[q] = in ? bmap[j] : 0;
+            nu_[q] = in ? P.nu[j] : 0.0;
         }
-        P.b[j] = bj;
+#pragma unroll
+        for (int q = 0; q < CP_U; ++q) {
+            acc_[q] = ktas[ll[q]];
+            rc_[q] = rcps[ll[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < CP_U; ++q) {
+            const int j = j0 + q * PT;
+            if (j >= f.cells) break;
+            const double acc = acc_[q], nuj = nu_[q];
+            double bj = 0.0;
+            if (nuj > 0.0) {
+                if (acc <= 0.0) r.zcol = 1;
+                else bj = div_shared(nuj, acc, rc_[q]);
+                range_acc(bj, r.bmin, r.bmax, r.nonfinite);
+                r.gap += fabs(__dsub_rn(nuj, __dmul_rn(bj, acc)));
+            }
+            P.b[j] = bj;
+        }
     }
 }
 
@@ -552,7 +706,7 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     double *__restrict__ scratch, int64_t stride_pair, const int64_t *__restrict__ rpc,
     const int64_t *__restrict__ cpc, int use_smem, const int32_t *__restrict__ bmap,
     const int32_t *__restrict__ rl_cells, const double *__restrict__ rl_coef,
-    const int32_t *__restrict__ cl_cells, const double *__restrict__ cl_coef) {
+    const int32_t *__restrict__ cl_cells, const double *__restrict__ cl_coef, int prod_smem) {
     __shared__ double sh[(PT / 32 + 1) * 6];
     const int64_t b = blockIdx.x;
     const int N = f.cells, n = c.cells;
@@ -623,9 +777,21 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
         __syncthreads();
     };
     double *rcp_buf = P.kta + U;  // scratch after kta (U doubles, see primal_layout)
+    // two-phase unit sums (uniform kernel, kappa <= 8)
+    // (products in shared memory after the staged vector, when the host sized
+    // the dynamic shared memory for them: prod_smem != 0)
+    const int K1 = UNIFORM ? (int)ipow(kappa, f.nd - 1) : 0;
+    // prod_smem = doubles of shared memory for the products (0: off); they
+    // follow the staged vector when it is staged, else start at offset 0
+    double *prod = (UNIFORM && prod_smem > 0) ? sx + (use_smem ? ((N + 1) & ~1) : 0) : nullptr;
+    const bool two_phase = UNIFORM && kappa <= 8 && prod != nullptr;
     const double *bs = stage(P.b);
-    for (int u = threadIdx.x; u < U; u += PT)
-        row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, true, nullptr, a_cur, r, bs);
+    if (two_phase) {
+        unit_sums(P.rrc, P.rrf, P.rptr, U, K1, kappa, bs, prod, P.kb, prod_smem, P.pf);
+    } else {
+        for (int u = threadIdx.x; u < U; u += PT)
+            row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, true, nullptr, a_cur, r, bs);
+    }
     if (UNIFORM) {
         finish_units(P.kb, rcp_buf);
         cell_pass_row(P, f, bmap, true, nullptr, a_cur, r, P.kb, rcp_buf);
@@ -641,8 +807,10 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
         Red rc = red_init();
         const double *as = stage(a_cur);
         EX_TRACE(1);
-        for (int u = threadIdx.x; u < U; u += PT)
-            col_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, a_cur, rc, as);
+        if (two_phase) unit_sums(P.crc, P.crf, P.cptr, U, K1, kappa, as, prod, P.kta, prod_smem, P.pf);
+        else
+            for (int u = threadIdx.x; u < U; u += PT)
+                col_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, a_cur, rc, as);
         EX_TRACE(2);
         if (UNIFORM) {
             finish_units(P.kta, rcp_buf);
@@ -656,8 +824,13 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
         EX_TRACE(4);
         const double *bsw = stage(P.b);
         EX_TRACE(5);
-        for (int u = threadIdx.x; u < U; u += PT)
-            row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, false, a_cur, a_nxt, rc, bsw);
+        if (two_phase) {
+            __syncthreads();  // the column sums are done reading the product buffer
+            unit_sums(P.rrc, P.rrf, P.rptr, U, K1, kappa, bsw, prod, P.kb, prod_smem, P.pf);
+        } else {
+            for (int u = threadIdx.x; u < U; u += PT)
+                row_unit<UNIFORM>(u, P, c, f, kappa, m, W, Wu, false, a_cur, a_nxt, rc, bsw);
+        }
         EX_TRACE(6);
         if (UNIFORM) {
             finish_units(P.kb, rcp_buf);
@@ -1722,12 +1895,12 @@ __global__ void sum_parts_kernel(const double *__restrict__ part, int count, dou
 // fixed butterfly: deterministic) so no thread serialises a long arc list.
 // ---------------------------------------------------------------------------
 constexpr int CT = 512;       // threads of primal_coarse_kernel
-constexpr int CB_HEAVY = 16;  // arcs above which a block's sum goes to a warp
+constexpr int CB_HEAVY = 8;  // arcs above which a block's sum goes to a warp
 enum { CB_MLO, CB_MHI, CB_NLO, CB_NHI, CB_CMU, CB_CNU, CB_S, CB_B, CB_K0, CB_K1, CB_KTA, CB_RK,
        CB_NF };
 
 struct CoarsePlan {
-    int rp, cp, rcol, rcoef, crow, ccoef, arow, heavy, blk, total;
+    int rp, cp, rcol, rcoef, crow, ccoef, arow, heavy, perm, blk, total;
 };
 
 __host__ __device__ inline CoarsePlan coarse_plan(int n) {
@@ -1749,6 +1922,8 @@ __host__ __device__ inline CoarsePlan coarse_plan(int n) {
     m.arow = o;
     o = fp_al(o + 4 * cap);
     m.heavy = o;  // heavy row blocks, then heavy column blocks
+    o = fp_al(o + 4 * 2 * n);
+    m.perm = o;  // light row blocks, then light column blocks, by descending degree
     o = fp_al(o + 4 * 2 * n);
     m.blk = o;
     o = fp_al(o + 8 * CB_NF * n);
@@ -1813,13 +1988,15 @@ __device__ __forceinline__ double cr_sum(double v, double *sh) {
 }
 
 // out[u] = sum_{e in [ptr[u], ptr[u+1])} coef[e] * x[idx[e]] for every block u:
-// light blocks one thread each, heavy ones (listed in `heavy`) one warp each
+// light blocks one thread each, visited in descending degree (`perm`, so the
+// lanes of a warp run near-equal trip counts), heavy ones (listed in `heavy`)
+// one warp each.  Each block's sum runs in its own fixed arc order.
 __device__ __forceinline__ void coarse_matvec(const int *ptr, const int *idx, const double *coef,
-                                              const double *x, double *out, int n,
-                                              const int *heavy, int nheavy) {
-    for (int u = threadIdx.x; u < n; u += CT) {
+                                              const double *x, double *out, const int *perm,
+                                              int nlight, const int *heavy, int nheavy) {
+    for (int j = threadIdx.x; j < nlight; j += CT) {
+        const int u = perm[j];
         const int e0 = ptr[u], e1 = ptr[u + 1];
-        if (e1 - e0 > CB_HEAVY) continue;
         double s = 0.0;
         for (int e = e0; e < e1; ++e) s += coef[e] * x[idx[e]];
         out[u] = s;
@@ -1847,6 +2024,7 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
     __shared__ CoarseRed shr[CT / 32 + 1];
     __shared__ double shd[CT / 32 + 1];
     __shared__ int nheavy_s[2];
+    __shared__ int dcnt[2][CB_HEAVY + 2];
     extern __shared__ __align__(16) unsigned char csm[];
     const int64_t b = blockIdx.x;
     const double Wu = W[0];
@@ -1859,6 +2037,7 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
     int *rcol = reinterpret_cast<int *>(csm + L.rcol), *crow = reinterpret_cast<int *>(csm + L.crow);
     int *arow = reinterpret_cast<int *>(csm + L.arow);
     int *hrow = reinterpret_cast<int *>(csm + L.heavy), *hcol = hrow + n;
+    int *prow = reinterpret_cast<int *>(csm + L.perm), *pcol = prow + n;
     double *rcoef = reinterpret_cast<double *>(csm + L.rcoef);
     double *ccoef = reinterpret_cast<double *>(csm + L.ccoef);
     double *blk = reinterpret_cast<double *>(csm + L.blk);
@@ -1870,6 +2049,7 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
 
     // ---- the pair's coarse plan and block statistics into shared memory
     if (threadIdx.x < 2) nheavy_s[threadIdx.x] = 0;
+    if (threadIdx.x < 2 * (CB_HEAVY + 2)) (&dcnt[0][0])[threadIdx.x] = 0;
     for (int i = threadIdx.x; i <= n; i += CT) {
         rp[i] = row_ptr[b * (n + 1) + i];
         cp[i] = col_ptr[b * (n + 1) + i];
@@ -1891,18 +2071,41 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
         cnt += Bcmu[k] + Bcnu[k];
     }
     __syncthreads();
+    // heavy blocks (> CB_HEAVY arcs) per side; the light ones bucketed by
+    // degree (counting sort, descending) for the thread-per-block sums
     for (int k = threadIdx.x; k < n; k += CT) {
         for (int e = rp[k]; e < rp[k + 1]; ++e) arow[e] = k;
-        if (rp[k + 1] - rp[k] > CB_HEAVY) hrow[atomicAdd(&nheavy_s[0], 1)] = k;
-        if (cp[k + 1] - cp[k] > CB_HEAVY) hcol[atomicAdd(&nheavy_s[1], 1)] = k;
+        const int dr = rp[k + 1] - rp[k], dc = cp[k + 1] - cp[k];
+        if (dr > CB_HEAVY) hrow[atomicAdd(&nheavy_s[0], 1)] = k;
+        else atomicAdd(&dcnt[0][CB_HEAVY - dr], 1);
+        if (dc > CB_HEAVY) hcol[atomicAdd(&nheavy_s[1], 1)] = k;
+        else atomicAdd(&dcnt[1][CB_HEAVY - dc], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {  // exclusive scan of the degree buckets
+        int acc = 0;
+        for (int q = 0; q <= CB_HEAVY; ++q) {
+            const int c = dcnt[threadIdx.x][q];
+            dcnt[threadIdx.x][q] = acc;
+            acc += c;
+        }
+        dcnt[threadIdx.x][CB_HEAVY + 1] = acc;  // number of light blocks
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < n; k += CT) {
+        const int dr = rp[k + 1] - rp[k], dc = cp[k + 1] - cp[k];
+        if (dr <= CB_HEAVY) prow[atomicAdd(&dcnt[0][CB_HEAVY - dr], 1)] = k;
+        if (dc <= CB_HEAVY) pcol[atomicAdd(&dcnt[1][CB_HEAVY - dc], 1)] = k;
     }
     cnt = cr_sum(cnt, shd);  // (its barriers also publish the tables above)
     const int nhr = nheavy_s[0], nhc = nheavy_s[1];
-    // the heavy lists are sets: their order only decides which warp sums a block
+    const int nlr = n - nhr, nlc = n - nhc;
+    // the heavy lists and the buckets are sets: their order only decides which
+    // thread or warp sums a block, never the order of a block's own sum
     const double xi = xi_in[b] < 0.0 ? 1e-9 * cnt : xi_in[b];
 
     // ---- kb = K b with b = 1 on the target support (sinkhorn.py:119-120)
-    coarse_matvec(rp, rcol, rcoef, Bcnu, Kcur, n, hrow, nhr);
+    coarse_matvec(rp, rcol, rcoef, Bcnu, Kcur, prow, nlr, hrow, nhr);
     __syncthreads();
     int zrow = 0;
     for (int k = threadIdx.x; k < n; k += CT)
@@ -1923,7 +2126,7 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
         }
         __syncthreads();
         // kta = K^T a
-        coarse_matvec(cp, crow, ccoef, BS, KTA, n, hcol, nhc);
+        coarse_matvec(cp, crow, ccoef, BS, KTA, pcol, nlc, hcol, nhc);
         __syncthreads();
         // zero-column check, b = nu / kta: block sums B_l, column residual, range(b)
         CoarseRed r = cr_init();
@@ -1947,7 +2150,7 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
         }
         __syncthreads();
         // kb' = K b
-        coarse_matvec(rp, rcol, rcoef, BB, Knext, n, hrow, nhr);
+        coarse_matvec(rp, rcol, rcoef, BB, Knext, prow, nlr, hrow, nhr);
         __syncthreads();
         // range of a (from kb), the row residual, the next sweep's zero-row check
         for (int k = threadIdx.x; k < n; k += CT) {
@@ -2025,7 +2228,7 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
 // reference's per-cell arithmetic (correctly rounded quotients; w = tv_weights
 // of the padded grid, measures.py:289-296).  Grid-wide, coalesced; one
 // partial pair per CTA (fixed order: deterministic).
-constexpr int TVT = 256, TV_CELLS = 16;  // threads, cells per thread of tv_pass_kernel
+constexpr int TVT = 256, TV_CELLS = 8;  // threads, cells per thread of tv_pass_kernel
 
 __global__ void __launch_bounds__(TVT) tv_pass_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu,
@@ -2039,21 +2242,35 @@ __global__ void __launch_bounds__(TVT) tv_pass_kernel(
         const double *mub = mu + b * N, *nub = nu + b * N;
         const double *k0 = blk + b * 3 * n, *k1 = k0 + n, *kt = k0 + 2 * n;
         const int base = blockIdx.x * TVT * TV_CELLS + threadIdx.x;
-#pragma unroll 4
+        // every independent load first (masses, weights, block ids), then the
+        // per-block denominators, then the arithmetic
+        double mv[TV_CELLS], nv[TV_CELLS], wv[TV_CELLS];
+        int kv[TV_CELLS];
+#pragma unroll
         for (int q = 0; q < TV_CELLS; ++q) {
             const int i = base + q * TVT;
-            if (i >= N) break;
-            const double mi = mub[i], ni = nub[i], w = __ldg(tv_w + i);
-            const int k = __ldg(bmap + i);
-            if (mi > 0.0) {
-                const double den = __ldg(k0 + k);
-                const double ai = fp_scale(mi, den, fp_rcp(den));
-                tmu += w * fabs(__dsub_rn(__dmul_rn(ai, __ldg(k1 + k)), mi));
+            const bool in = i < N;
+            mv[q] = in ? mub[i] : 0.0;
+            nv[q] = in ? nub[i] : 0.0;
+            wv[q] = in ? __ldg(tv_w + i) : 0.0;
+            kv[q] = in ? __ldg(bmap + i) : 0;
+        }
+        double d0[TV_CELLS], d1[TV_CELLS], dt[TV_CELLS];
+#pragma unroll
+        for (int q = 0; q < TV_CELLS; ++q) {
+            d0[q] = __ldg(k0 + kv[q]);
+            d1[q] = __ldg(k1 + kv[q]);
+            dt[q] = __ldg(kt + kv[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < TV_CELLS; ++q) {
+            if (mv[q] > 0.0) {
+                const double ai = fp_scale(mv[q], d0[q], fp_rcp(d0[q]));
+                tmu += wv[q] * fabs(__dsub_rn(__dmul_rn(ai, d1[q]), mv[q]));
             }
-            if (ni > 0.0) {
-                const double den = __ldg(kt + k);
-                const double bi = fp_scale(ni, den, fp_rcp(den));
-                tnu += w * fabs(__dsub_rn(__dmul_rn(bi, den), ni));
+            if (nv[q] > 0.0) {
+                const double bi = fp_scale(nv[q], dt[q], fp_rcp(dt[q]));
+                tnu += wv[q] * fabs(__dsub_rn(__dmul_rn(bi, dt[q]), nv[q]));
             }
         }
     }
@@ -2079,7 +2296,8 @@ inline int tv_lanes(const Grid &f, const Grid &c) {
 }
 
 struct PrimalLayout {
-    int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, bm_off, fp_off, ar_off, rl_off, total,
+    int64_t stride_pair, mom_off, tv_off, pr_off, pc_off, bm_off, fp_off, ar_off, rl_off, prod_off,
+        total,
         tv_ctas, pr_ctas, runs;
 };
 
@@ -2104,6 +2322,7 @@ inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, b
     // uniform exact IPF: run lists per direction, coefficients (f64) then cells (int32)
     const int64_t kap = f.n[0] / c.n[0];
     L.runs = uniform ? batch * max_arcs * (f.cells / c.cells / kap) : 0;
+    L.prod_off = 0;  // (two-phase products live in shared memory)
     L.total = L.rl_off + 2 * L.runs + L.runs;
     return L;
 }
@@ -2188,7 +2407,22 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
     }
     const size_t sxb = sizeof(double) * f.cells;
     const int use_smem = sxb <= 160 * 1024;
-    const size_t dyn = use_smem ? sxb : 0;
+    size_t dyn = use_smem ? sxb : 0;
+    // exact-order unit sums in two phases (products, then the chains) when the
+    // staged vector and one direction's products fit in shared memory
+    int prod_smem = 0;
+    if (uni) {
+        // all of one direction's products when they fit beside the staged
+        // vector, else batches of up to 20480 (160 KB)
+        const int64_t prods = 2 * c.cells * (f.cells / c.cells);
+        const int64_t base = use_smem ? ((f.cells + 1) & ~1ll) : 0;
+        const int64_t room = (200 * 1024) / (int64_t)sizeof(double) - base;
+        const int64_t capd = std::min<int64_t>(prods, std::min<int64_t>(room, 20480));
+        if (capd >= std::min<int64_t>(prods, 4096)) {
+            prod_smem = (int)(capd & ~1ll);
+            dyn = sizeof(double) * (base + prod_smem);
+        }
+    }
     if (fast_ipf) {
         // one cluster of ceil(units / FT) <= 8 CTAs per pair; a unit is one
         // fine row of a block for kappa in {2, 4, 8} with kappa^(d-1) <= 32
@@ -2244,10 +2478,13 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
         if (dyn > 48 * 1024)
             cudaFuncSetAttribute(ipf_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)dyn);
+        // chains gathering from global memory: as much L1 as the SM offers
+        cudaFuncSetAttribute(ipf_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             use_smem ? -1 : 0);
         ipf_kernel<true><<<(unsigned)batch, PT, dyn, st>>>(
             mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
             col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair,
-            rpc, cpc, use_smem, bmap, rl_cells, rl_coef, cl_cells, cl_coef);
+            rpc, cpc, use_smem, bmap, rl_cells, rl_coef, cl_cells, cl_coef, prod_smem);
     } else {
         if (dyn > 48 * 1024)
             cudaFuncSetAttribute(ipf_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2255,7 +2492,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
         ipf_kernel<false><<<(unsigned)batch, PT, dyn, st>>>(
             mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
             col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair,
-            rpc, cpc, use_smem, nullptr, nullptr, nullptr, nullptr, nullptr);
+            rpc, cpc, use_smem, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
     }
     const int closed = uni && p == 2.0;
     int32_t *arc_row = reinterpret_cast<int32_t *>(ws + L.ar_off);

@@ -1,0 +1,13 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 1800 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+for C in 3 4 2 5 1; do
+  timeout 600 python bench.py --config $C --no-cpu-baseline --no-e2e > gpurun_out/bench_cfg$C.json 2> gpurun_out/bench_cfg$C.err; echo "exit $?" >> gpurun_out/bench_cfg$C.err
+done
+for C in 1 5; do
+  GRIDOT_B200_LIB=paper_2506_00976_b200/csrc/_trace/libgridot_b200.so timeout 300 python scripts/ipf_trace.py $C >> gpurun_out/ipf_trace.txt 2>&1
+done
+GRIDOT_B200_LIB=paper_2506_00976_b200/csrc/_trace/libgridot_b200.so timeout 300 python scripts/ct_trace.py > gpurun_out/ct_trace.json 2>&1
+timeout 600 bash scripts/gpu_prof_k.sh 4 "primal_coarse" cfg4_coarse 1 > gpurun_out/prof_cfg4c.log 2>&1
+timeout 600 bash scripts/gpu_prof_k.sh 5 "ipf_kernel|unit_sums" cfg5_ipf 1 > gpurun_out/prof_cfg5.log 2>&1
+timeout 600 bash scripts/gpu_prof_k.sh 1 "ipf_kernel" cfg1_ipf 1 > gpurun_out/prof_cfg1.log 2>&1
