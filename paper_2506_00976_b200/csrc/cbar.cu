@@ -15,6 +15,8 @@
 // moments about the block centres, O(N^d + n^2d) instead of O(N^2d) -- and
 // other p use the same tiling as exact mode in fp32 FFMA with an fp64 block
 // sum.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace gdt {
@@ -153,6 +155,179 @@ __global__ void __launch_bounds__(256) cbar_tile_kernel(
         const int64_t oi = (b * n + k) * n + l;
         const bool un = denom == 0.0;
         out[oi] = un ? Ccentre[k * n + l] : __ddiv_rn(numer, denom);
+        if (unused) unused[oi] = un ? 1 : 0;
+    }
+}
+
+// ---- exact mode, p != 2, 2-D / 3-D grids: one row block per CTA ----------
+// The same arithmetic as cbar_tile_kernel<true> (the reference's order:
+// s_kc = sequential over t of (C_tc * mu_t) * nu_c, then the numpy pairwise
+// sum over c in Y_l), organised for throughput: a CTA owns ONE row block k
+// (its mu_t in shared memory) and a chunk of target blocks; each thread runs
+// the chain of one target cell at a time with the cost read from the
+// reference-exact table by integer squared distance (incremental offsets, no
+// divisions in the loop), and the chains of a chunk land in shared memory in
+// fine order for the pairwise block sums.
+constexpr int CE_THREADS = 256;
+constexpr int CE_CELLS = 2048;  // target cells per CTA (chunk of whole blocks)
+
+template <int KAPPA, int ND>
+__global__ void __launch_bounds__(CE_THREADS) cbar_exact_kernel(
+    const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ mu_c,
+    const double *__restrict__ nu_c, const double *__restrict__ Ccentre,
+    const double *__restrict__ table, double p, double *__restrict__ out,
+    uint8_t *__restrict__ unused, Grid f, Grid c, int LT) {
+    constexpr int M = ND == 2 ? KAPPA * KAPPA : KAPPA * KAPPA * KAPPA;
+    __shared__ double mus[M];
+    extern __shared__ double S[];  // [LT][M] chains of the chunk, fine order per block
+    const int64_t b = blockIdx.z;
+    const int64_t n = c.cells;
+    const int64_t k = blockIdx.x;
+    const int64_t l0 = (int64_t)blockIdx.y * LT;
+    const int lt = (int)(n - l0 < LT ? n - l0 : LT);
+    const double *mub = mu + b * f.cells, *nub = nu + b * f.cells;
+    // row block k: origin and its masses in the reference's order (t = tx + K ty (+ K^2 tz))
+    int kx[3] = {0, 0, 0};
+    {
+        int64_t rem = k;
+        for (int a = ND - 1; a >= 0; --a) {
+            kx[a] = (int)(rem / c.stride[a]);
+            rem -= (int64_t)kx[a] * c.stride[a];
+        }
+    }
+    for (int t = threadIdx.x; t < M; t += CE_THREADS) {
+        const int tx = t % KAPPA, ty = (t / KAPPA) % KAPPA, tz = t / (KAPPA * KAPPA);
+        int64_t off = (int64_t)(kx[0] * KAPPA + tx) + (int64_t)(kx[1] * KAPPA + ty) * f.stride[1];
+        if (ND == 3) off += (int64_t)(kx[2] * KAPPA + tz) * f.stride[2];
+        mus[t] = mub[off];
+    }
+    __syncthreads();
+    const int cells = lt * M;
+    for (int i = threadIdx.x; i < cells; i += CE_THREADS) {
+        const int ll = i / M, sidx = i - ll * M;  // target block (chunk-local), cell in it
+        int64_t lrem = l0 + ll;
+        int lc[3] = {0, 0, 0};
+        for (int a = ND - 1; a >= 0; --a) {
+            lc[a] = (int)(lrem / c.stride[a]);
+            lrem -= (int64_t)lc[a] * c.stride[a];
+        }
+        const int sx = sidx % KAPPA, sy = (sidx / KAPPA) % KAPPA, sz = sidx / (KAPPA * KAPPA);
+        const int cx = lc[0] * KAPPA + sx, cy = lc[1] * KAPPA + sy, cz = ND == 3 ? lc[2] * KAPPA + sz : 0;
+        const double nuc = nub[cx + (int64_t)cy * f.stride[1] + (ND == 3 ? (int64_t)cz * f.stride[2] : 0)];
+        // offsets of the row block's cells from c: dx = kx0 + tx - cx, ...
+        const int dx0 = kx[0] * KAPPA - cx, dy0 = kx[1] * KAPPA - cy,
+                  dz0 = ND == 3 ? kx[2] * KAPPA - cz : 0;
+        double acc = 0.0;
+#pragma unroll 1
+        for (int tz = 0; tz < (ND == 3 ? KAPPA : 1); ++tz) {
+            const int dz = dz0 + tz;
+#pragma unroll 1
+            for (int ty = 0; ty < KAPPA; ++ty) {
+                const int dy = dy0 + ty;
+                const int h = dy * dy + dz * dz;
+                const double *mrow = mus + (tz * KAPPA + ty) * KAPPA;
+                double cst[KAPPA];
+#pragma unroll
+                for (int tx = 0; tx < KAPPA; ++tx) {
+                    const int dx = dx0 + tx;
+                    const int sq = h + dx * dx;
+                    cst[tx] = table ? __ldg(table + sq) : (p == 1.0 ? __dsqrt_rn((double)sq) : (double)sq);
+                }
+#pragma unroll
+                for (int tx = 0; tx < KAPPA; ++tx) {
+                    const double term = __dmul_rn(__dmul_rn(cst[tx], mrow[tx]), nuc);
+                    acc = (tz == 0 && ty == 0 && tx == 0) ? term : __dadd_rn(acc, term);
+                }
+            }
+        }
+        S[i] = acc;
+    }
+    __syncthreads();
+    for (int ll = threadIdx.x; ll < lt; ll += CE_THREADS) {
+        const int64_t l = l0 + ll;
+        const double *row = S + ll * M;
+        const double numer = np_pairwise([&](int64_t i) { return row[i]; }, M);
+        const double denom = __dmul_rn(mu_c[b * n + k], nu_c[b * n + l]);
+        const int64_t oi = (b * n + k) * n + l;
+        const bool un = denom == 0.0;
+        out[oi] = un ? Ccentre[k * n + l] : __ddiv_rn(numer, denom);
+        if (unused) unused[oi] = un ? 1 : 0;
+    }
+}
+
+// 2-D grids: the same chains with the CTA's target cells taken in fine-row
+// order (a warp = 32 consecutive cells of one fine row), so the costs a warp
+// needs for one source cell are consecutive entries of a 2-D table
+// T2[|dy|][|dx|] = cost(dx^2 + dy^2) -- the same doubles as the 1-D table --
+// and its loads coalesce instead of scattering over the squared distances.
+__global__ void cost2d_kernel(const double *__restrict__ table, double p, int W, int H,
+                              double *__restrict__ t2) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < W * H; i += gridDim.x * blockDim.x) {
+        const int a = i / W, bx = i - a * W;
+        const int64_t sq = (int64_t)a * a + (int64_t)bx * bx;
+        t2[i] = table ? table[sq] : (p == 1.0 ? __dsqrt_rn((double)sq) : (double)sq);
+    }
+}
+
+template <int KAPPA>
+__global__ void __launch_bounds__(CE_THREADS) cbar_exact2d_kernel(
+    const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ mu_c,
+    const double *__restrict__ nu_c, const double *__restrict__ Ccentre,
+    const double *__restrict__ t2, int W, double *__restrict__ out, uint8_t *__restrict__ unused,
+    Grid f, Grid c, int BR) {
+    constexpr int M = KAPPA * KAPPA;
+    __shared__ double mus[M];
+    extern __shared__ double S[];  // [chunk blocks][M], fine order per block
+    const int64_t b = blockIdx.z;
+    const int64_t n = c.cells;
+    const int n0 = (int)c.n[0], N0 = (int)f.n[0];
+    const int k = blockIdx.x;
+    const int br0 = blockIdx.y * BR;                       // first block-row of the chunk
+    const int brs = min(BR, (int)c.n[1] - br0);            // block-rows in the chunk
+    const int64_t l0 = (int64_t)br0 * n0;
+    const double *mub = mu + b * f.cells, *nub = nu + b * f.cells;
+    const int kx = k % n0, ky = k / n0;
+    for (int t = threadIdx.x; t < M; t += CE_THREADS) {
+        const int tx = t % KAPPA, ty = t / KAPPA;
+        mus[t] = mub[(kx * KAPPA + tx) + (int64_t)(ky * KAPPA + ty) * N0];
+    }
+    __syncthreads();
+    const int cells = brs * KAPPA * N0;
+    for (int i = threadIdx.x; i < cells; i += CE_THREADS) {
+        const int cyl = i / N0, cx = i - cyl * N0;
+        const int cy = br0 * KAPPA + cyl;
+        const double nuc = nub[cx + (int64_t)cy * N0];
+        const int dx0 = kx * KAPPA - cx, dy0 = ky * KAPPA - cy;
+        double acc = 0.0;
+#pragma unroll
+        for (int ty = 0; ty < KAPPA; ++ty) {
+            const int dy = dy0 + ty;
+            const double *row = t2 + (int64_t)(dy < 0 ? -dy : dy) * W;
+            double cst[KAPPA];
+#pragma unroll
+            for (int tx = 0; tx < KAPPA; ++tx) {
+                const int dx = dx0 + tx;
+                cst[tx] = __ldg(row + (dx < 0 ? -dx : dx));
+            }
+#pragma unroll
+            for (int tx = 0; tx < KAPPA; ++tx) {
+                const double term = __dmul_rn(__dmul_rn(cst[tx], mus[ty * KAPPA + tx]), nuc);
+                acc = (ty == 0 && tx == 0) ? term : __dadd_rn(acc, term);
+            }
+        }
+        // staged at (block, cell in block) for the pairwise block sums
+        const int ll = (cyl / KAPPA) * n0 + cx / KAPPA;
+        S[ll * M + (cx % KAPPA) + KAPPA * (cyl % KAPPA)] = acc;
+    }
+    __syncthreads();
+    for (int ll = threadIdx.x; ll < brs * n0; ll += CE_THREADS) {
+        const int64_t l = l0 + ll;
+        const double *rowp = S + ll * M;
+        const double numer = np_pairwise([&](int64_t i) { return rowp[i]; }, M);
+        const double denom = __dmul_rn(mu_c[b * n + k], nu_c[b * n + l]);
+        const int64_t oi = (b * n + k) * n + l;
+        const bool un = denom == 0.0;
+        out[oi] = un ? Ccentre[(int64_t)k * n + l] : __ddiv_rn(numer, denom);
         if (unused) unused[oi] = un ? 1 : 0;
     }
 }
@@ -358,6 +533,57 @@ extern "C" int gdt_weighted_cost(const double *mu, const double *nu, const doubl
                                           unused, batch, f, c, kappa, p, st);
         if (rc == GDT_OK) return cuda_status("gdt_weighted_cost(toeplitz)");
         // outside the fp32 kernel's envelope: fall through to the exact fp64 kernel
+    }
+    if (ndim == 2 && (kappa == 2 || kappa == 4 || kappa == 8) && f.n[0] * kappa <= CE_CELLS &&
+        (p == 1.0 || p == 2.0 || cost_table != nullptr)) {
+        // exact order, 2-D: one row block per CTA, target cells in fine-row
+        // order, costs from a 2-D table (cbar_exact2d_kernel)
+        const int W = (int)std::max(f.n[0], f.n[1]);
+        double *t2 = nullptr;
+        if (malloc_async(reinterpret_cast<void **>(&t2), sizeof(double) * W * W, st) != cudaSuccess)
+            return cuda_status("gdt_weighted_cost: workspace");
+        cost2d_kernel<<<grid_size((int64_t)W * W, 256), 256, 0, st>>>(
+            p == 2.0 ? nullptr : cost_table, p, W, W, t2);
+        const int BR = (int)std::max<int64_t>(1, CE_CELLS / (f.n[0] * kappa));
+        const int brows = (int)((c.n[1] + BR - 1) / BR);
+        const size_t sb = sizeof(double) * (size_t)BR * c.n[0] * m;
+        dim3 grid((unsigned)n, (unsigned)brows, (unsigned)batch);
+        auto go = [&](auto kern) {
+            if (sb > 48 * 1024)
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+            kern<<<grid, CE_THREADS, sb, st>>>(mu, nu, mu_c, nu_c, centre_cost, t2, W, out,
+                                               unused, f, c, BR);
+        };
+        if (kappa == 2) go(cbar_exact2d_kernel<2>);
+        else if (kappa == 4) go(cbar_exact2d_kernel<4>);
+        else go(cbar_exact2d_kernel<8>);
+        cudaFreeAsync(t2, st);
+        return cuda_status("gdt_weighted_cost(exact 2-D)");
+    }
+    if ((ndim == 2 || ndim == 3) && (kappa == 2 || kappa == 4 || kappa == 8) && m <= CE_CELLS &&
+        (p == 1.0 || p == 2.0 || cost_table != nullptr)) {
+        // exact order, one row block per CTA (cbar_exact_kernel)
+        const int LT = (int)std::min<int64_t>(n, CE_CELLS / m);
+        const size_t sb = sizeof(double) * LT * m;
+        dim3 grid((unsigned)n, (unsigned)((n + LT - 1) / LT), (unsigned)batch);
+        auto go = [&](auto kern) {
+            if (sb > 48 * 1024)
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+            // p in {1, 2} without a table: IEEE sqrt of / the integer squared distance
+            kern<<<grid, CE_THREADS, sb, st>>>(mu, nu, mu_c, nu_c, centre_cost,
+                                               p == 2.0 ? nullptr : cost_table, p, out, unused, f,
+                                               c, LT);
+        };
+        if (ndim == 2) {
+            if (kappa == 2) go(cbar_exact_kernel<2, 2>);
+            else if (kappa == 4) go(cbar_exact_kernel<4, 2>);
+            else go(cbar_exact_kernel<8, 2>);
+        } else {
+            if (kappa == 2) go(cbar_exact_kernel<2, 3>);
+            else if (kappa == 4) go(cbar_exact_kernel<4, 3>);
+            else go(cbar_exact_kernel<8, 3>);
+        }
+        return cuda_status("gdt_weighted_cost(exact)");
     }
     // tile shape: ~256 columns per CTA, KT row blocks per CTA
     int LT = m >= 256 ? 1 : 256 / m;

@@ -254,15 +254,34 @@ __global__ void __launch_bounds__(64) pruned_ct_kernel(const T *__restrict__ v,
 // starting at sx0, off = sx0 - xj0 is a multiple of 8 and the lane's costs are
 // T[off + q] (off >= 0) or T[-off + 14 - q] (off < 0), q = 0..14 -- 16 aligned
 // floats, four LDS.128.  Row stride 140 floats (12 mod 32 banks) makes the
-// 16-byte reads of 8 lanes on 8 different rows conflict-free.  Eight regions
-// (16 warps) per CTA amortise the table; the pruning bound of a tile uses the
-// same table values, so no lowering is needed.
+// 16-byte reads of 8 lanes on 8 different rows conflict-free.
+//
+// Work distribution (round 2): a region is shared by CT_TAB_WPR warps that
+// take its ring-ordered tiles from one cursor, and their per-output minima
+// live in one shared array (atomicMin on order-preserving integer keys), so
+// every warp prunes against the region's best known bound, not only its own.
+// Many warps per region finish a region fast; with ~1.2 regions per warp pair
+// (the round-1 mapping) the SMs idled behind the slowest regions (ncu: SM
+// active ~42%).  Regions come from a global counter (persistent CTAs).  The
+// result equals the brute force bit for bit: a tile is skipped only when its
+// lower bound reaches the largest current best of the region.
 constexpr int CT_TAB_W = 140;      // row stride (floats)
 constexpr int CT_TAB_ROWS = 128;   // |dy| <= 127
-constexpr int CT_TAB_REG = 8;      // regions per CTA (2 warps each)
+constexpr int CT_TAB_WPR = 4;      // warps per region
+constexpr int CT_TAB_REG = 4;      // regions per CTA
+constexpr int CT_TAB_GT = 32 * CT_TAB_WPR;  // threads of a region group
 
-__device__ __forceinline__ void pair_sync(int id) {
-    asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+__device__ __forceinline__ void group_sync(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(CT_TAB_GT) : "memory");
+}
+
+// float <-> int key with the same order (for atomicMin on shared memory)
+__device__ __forceinline__ int ord_key(float x) {
+    const int i = __float_as_int(x);
+    return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float ord_val(int k) {
+    return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff);
 }
 
 constexpr int CT_TAB_TILES = 256;  // (128 / 8)^2 source tiles at most
@@ -272,23 +291,22 @@ constexpr int CT_TAB_TILES = 256;  // (128 / 8)^2 source tiles at most
 __device__ unsigned long long g_ct_tiles[2];
 #endif
 
-__global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
+__global__ void __launch_bounds__(CT_TAB_GT * CT_TAB_REG, 2) pruned_ct_tab_kernel(
     const float *__restrict__ v, const float *__restrict__ tmax, float *__restrict__ out,
     int64_t batch, Grid g, unsigned long long *__restrict__ counter) {
     extern __shared__ __align__(16) float ct_tab[];  // [CT_TAB_ROWS][CT_TAB_W]
-    __shared__ float other[CT_TAB_REG][32][8];
+    __shared__ int sbest[CT_TAB_REG][256];           // region minima (ord_key)
     __shared__ long long next_region[CT_TAB_REG];
-    // per warp pair: the region's tiles in Chebyshev-ring order, packed
-    // (ring << 16) | tile, and the cursor both warps take tiles from
+    // per region group: the region's tiles in Chebyshev-ring order, packed
+    // (ring << 16) | tile, and the cursor its warps take tiles from
     __shared__ unsigned tiles_s[CT_TAB_REG][CT_TAB_TILES];
     __shared__ int ring_cnt[CT_TAB_REG][17];
     __shared__ int cursor[CT_TAB_REG];
     const int lane = threadIdx.x & 31;
     const int warp_in_cta = threadIdx.x >> 5;
-    const int half = warp_in_cta & 1;
-    const int slot = warp_in_cta >> 1;
-    const int pt = threadIdx.x & 63;  // thread index inside the pair
-    const int bar_id = 1 + slot;      // named barrier of this warp pair
+    const int slot = warp_in_cta / CT_TAB_WPR;
+    const int pt = threadIdx.x % CT_TAB_GT;  // thread index inside the group
+    const int bar_id = 1 + slot;             // named barrier of this group
     const int N0 = (int)g.n[0], N1 = (int)g.n[1];
     // table: row dy, column i -> sqrt((i - 7)^2 + dy^2), correctly rounded
     for (int e = threadIdx.x; e < CT_TAB_ROWS * CT_TAB_W; e += blockDim.x) {
@@ -302,13 +320,12 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
     const int64_t regions = (int64_t)nr0 * nr1;
     const int64_t total = batch * regions;
     const int nt0 = N0 / 8, nt1 = N1 / 8, ntiles = nt0 * nt1;
-    // persistent warp pairs: each pair takes the next region from a global
-    // counter (pruned work per region is uneven); inside a region the two
-    // warps take ring-ordered tiles from a shared cursor
+    constexpr int PER = (CT_TAB_TILES + CT_TAB_GT - 1) / CT_TAB_GT;  // tiles per thread (sort)
     for (;;) {
         if (pt == 0) next_region[slot] = (long long)atomicAdd(counter, 1ull);
         if (pt < 17) ring_cnt[slot][pt] = 0;
-        pair_sync(bar_id);
+        for (int i = pt; i < 256; i += CT_TAB_GT) sbest[slot][i] = ord_key(INFINITY);
+        group_sync(bar_id);
         const int64_t region = next_region[slot];
         if (region >= total) break;
         const int64_t b = region / regions;
@@ -317,10 +334,10 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
         const int X0 = rx * 16, Y0 = ry * 16;
         const int h0lo = X0 / 8, h0hi = h0lo + 1, h1lo = Y0 / 8, h1hi = h1lo + 1;
         // ring of every tile, counting sort into ring order
-        int my_ring[CT_TAB_TILES / 64];
+        int my_ring[PER];
 #pragma unroll
-        for (int q = 0; q < CT_TAB_TILES / 64; ++q) {
-            const int t = pt + 64 * q;
+        for (int q = 0; q < PER; ++q) {
+            const int t = pt + CT_TAB_GT * q;
             my_ring[q] = -1;
             if (t < ntiles) {
                 const int t0 = t % nt0, t1 = t / nt0;
@@ -330,7 +347,7 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
                 atomicAdd(&ring_cnt[slot][my_ring[q]], 1);
             }
         }
-        pair_sync(bar_id);
+        group_sync(bar_id);
         if (pt == 0) {
             int acc = 0;
             for (int r = 0; r < 17; ++r) {
@@ -340,17 +357,17 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
             }
             cursor[slot] = 0;
         }
-        pair_sync(bar_id);
+        group_sync(bar_id);
 #pragma unroll
-        for (int q = 0; q < CT_TAB_TILES / 64; ++q) {
-            const int t = pt + 64 * q;
+        for (int q = 0; q < PER; ++q) {
+            const int t = pt + CT_TAB_GT * q;
             if (my_ring[q] >= 0) {
                 const int pos = atomicAdd(&ring_cnt[slot][my_ring[q]], 1);
                 tiles_s[slot][pos] = ((unsigned)my_ring[q] << 16) |
                                      ((unsigned)(t / nt0) << 8) | (unsigned)(t % nt0);
             }
         }
-        pair_sync(bar_id);
+        group_sync(bar_id);
 
         float best[8];
 #pragma unroll
@@ -360,6 +377,7 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
         // row stride of 12 mod 32 banks their 16-byte reads do not conflict)
         const int xj0 = X0 + 8 * (lane >> 4);
         const int yj = Y0 + (lane & 15);
+        int *sb = sbest[slot] + (lane & 15) * 16 + 8 * (lane >> 4);  // this lane's 8 outputs
         const float *vb = v + b * g.cells;
         const float *tm = tmax + b * (int64_t)ntiles;
         float vall = -INFINITY;
@@ -417,28 +435,26 @@ __global__ void __launch_bounds__(64 * CT_TAB_REG, 2) pruned_ct_tab_kernel(
                 if (off >= 0) minplus_row8<false, true>(L, vs, best);
                 else minplus_row8<true, true>(L, vs, best);
             }
-            float m = best[0];
+            // publish to the region's minima, take the others' back, and
+            // refresh this warp's bound: the largest best of the region
+            float m = -INFINITY;
 #pragma unroll
-            for (int r8 = 1; r8 < 8; ++r8) m = fmaxf(m, best[r8]);
+            for (int r8 = 0; r8 < 8; ++r8) {
+                const int got = atomicMin(sb + r8, ord_key(best[r8]));
+                best[r8] = fminf(best[r8], ord_val(got));
+                m = fmaxf(m, best[r8]);
+            }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
             ub = m;
         }
-        // merge the two warps' minima
-        if (half == 1) {
-#pragma unroll
-            for (int r8 = 0; r8 < 8; ++r8) other[slot][lane][r8] = best[r8];
-        }
-        pair_sync(bar_id);
-        if (half == 0) {
+        group_sync(bar_id);  // every warp's minima are in sbest
+        if (warp_in_cta % CT_TAB_WPR == 0) {
             float *ob = out + b * g.cells + (int64_t)yj * N0 + xj0;
 #pragma unroll
-            for (int r8 = 0; r8 < 8; ++r8) {
-                const float o = other[slot][lane][r8];
-                ob[r8] = o < best[r8] ? o : best[r8];
-            }
+            for (int r8 = 0; r8 < 8; ++r8) ob[r8] = ord_val(sb[r8]);
         }
-        pair_sync(bar_id);  // the pair's shared lists are reused by the next region
+        group_sync(bar_id);  // the group's shared lists are reused by the next region
     }
 }
 
@@ -484,7 +500,7 @@ static int run_pruned(const T *v, T *out, T *tmax, int64_t batch, const Grid &g,
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev2);
             const int64_t need = (warps + CT_TAB_REG - 1) / CT_TAB_REG;
             const unsigned tctas = (unsigned)std::min<int64_t>(need, 2 * nsm);  // persistent
-            pruned_ct_tab_kernel<<<tctas, 64 * CT_TAB_REG, tb, st>>>(
+            pruned_ct_tab_kernel<<<tctas, CT_TAB_GT * CT_TAB_REG, tb, st>>>(
                 reinterpret_cast<const float *>(v), reinterpret_cast<const float *>(tmax),
                 reinterpret_cast<float *>(out), batch, g, counter);
             return GDT_OK;

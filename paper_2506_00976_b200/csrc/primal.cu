@@ -241,18 +241,48 @@ __device__ __forceinline__ void run_products(const int32_t *__restrict__ cells,
                                              const double *__restrict__ coefs, int nruns,
                                              const double *__restrict__ x,
                                              double *__restrict__ prod, int kappa) {
-    for (int r = threadIdx.x; r < nruns; r += PT) {
-        const double cf = coefs[r];
-        const double *xp = x + cells[r];
-        if constexpr (KAP >= 2) {
-            double *pp = prod + (int64_t)r * KAP;
+    if constexpr (KAP >= 2 && KAP <= 4) {
+        // RU runs per thread at a time: run descriptors, then the gathers, then
+        // the products (the loads of a group are all in flight together)
+        constexpr int RU = 4;
+        for (int r0 = threadIdx.x; r0 < nruns; r0 += PT * RU) {
+            int cl[RU];
+            double cf[RU], xv[RU][KAP];
 #pragma unroll
-            for (int i = 0; i < KAP; i += 2)
-                *reinterpret_cast<double2 *>(pp + i) =
-                    make_double2(__dmul_rn(cf, xp[i]), __dmul_rn(cf, xp[i + 1]));
-        } else {
-            double *pp = prod + (int64_t)r * kappa;
-            for (int i = 0; i < kappa; ++i) pp[i] = __dmul_rn(cf, xp[i]);
+            for (int q = 0; q < RU; ++q) {
+                const int r = r0 + q * PT;
+                cl[q] = r < nruns ? cells[r] : 0;
+                cf[q] = r < nruns ? coefs[r] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < RU; ++q)
+#pragma unroll
+                for (int i = 0; i < KAP; ++i) xv[q][i] = r0 + q * PT < nruns ? x[cl[q] + i] : 0.0;
+#pragma unroll
+            for (int q = 0; q < RU; ++q) {
+                const int r = r0 + q * PT;
+                if (r >= nruns) break;
+                double *pp = prod + (int64_t)r * KAP;
+#pragma unroll
+                for (int i = 0; i < KAP; i += 2)
+                    *reinterpret_cast<double2 *>(pp + i) =
+                        make_double2(__dmul_rn(cf[q], xv[q][i]), __dmul_rn(cf[q], xv[q][i + 1]));
+            }
+        }
+    } else {
+        for (int r = threadIdx.x; r < nruns; r += PT) {
+            const double cf = coefs[r];
+            const double *xp = x + cells[r];
+            if constexpr (KAP >= 2) {
+                double *pp = prod + (int64_t)r * KAP;
+#pragma unroll
+                for (int i = 0; i < KAP; i += 2)
+                    *reinterpret_cast<double2 *>(pp + i) =
+                        make_double2(__dmul_rn(cf, xp[i]), __dmul_rn(cf, xp[i + 1]));
+            } else {
+                double *pp = prod + (int64_t)r * kappa;
+                for (int i = 0; i < kappa; ++i) pp[i] = __dmul_rn(cf, xp[i]);
+            }
         }
     }
 }
@@ -584,7 +614,7 @@ __global__ void block_map_kernel(G32 f, G32 c, int kappa, int32_t *__restrict__ 
 // current a and the zero-row check (same arithmetic as row_unit's cell loop).
 // (cells in groups of CP_U per thread: every independent load of a group is
 // issued before its dependent gathers and arithmetic)
-constexpr int CP_U = 4;
+constexpr int CP_U = 8;
 
 __device__ __forceinline__ void cell_pass_row(const PairPtrs &P, const G32 &f,
                                               const int32_t *__restrict__ bmap, bool init, const double *a_cur,
