@@ -64,6 +64,38 @@ class NativeError(GridotError):
     """A C-ABI call failed (bad arguments or a CUDA error)."""
 
 
+TORCH_EXT_PATH = os.path.join(_HERE, "csrc", "libgridot_torch.so")
+_torch_ops = False
+
+
+def load_torch_extension() -> bool:
+    """Load the PyTorch extension (csrc/torch_ops.cpp): it brings in
+    libgridot_b200.so as its linked dependency and registers
+    torch.ops.gridot_b200.{version, sumpool, weighted_cost}.  Skipped when
+    GRIDOT_B200_LIB selects another build of the C library."""
+    global _torch_ops
+    if _torch_ops or os.environ.get("GRIDOT_B200_LIB"):
+        return _torch_ops
+    if not os.path.exists(TORCH_EXT_PATH):
+        raise NativeError(f"{TORCH_EXT_PATH} is missing; build it with "
+                          "`python -m paper_2506_00976_b200.csrc.build`")
+    import torch
+
+    torch.ops.load_library(TORCH_EXT_PATH)
+    _torch_ops = True
+    return True
+
+
+def torch_ops():
+    """torch.ops.gridot_b200 (None under a GRIDOT_B200_LIB override)."""
+    lib()
+    if not _torch_ops:
+        return None
+    import torch
+
+    return torch.ops.gridot_b200
+
+
 def lib() -> ctypes.CDLL:
     global _lib
     if _lib is None:
@@ -71,6 +103,10 @@ def lib() -> ctypes.CDLL:
             raise NativeError(
                 f"{LIB_PATH} is missing; build it with "
                 "`python -m paper_2506_00976_b200.csrc.build` (there is no CPU fallback)")
+        # the C library is loaded through the PyTorch extension (its linked
+        # dependency); ctypes then binds the remaining entry points on the
+        # same, already loaded library
+        load_torch_extension()
         handle = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in _SIGNATURES.items():
             fn = getattr(handle, name)

@@ -193,6 +193,11 @@ def weighted_cost_batch(mu_pad, nu_pad, mu_c, nu_c, padded_dims, kappa, p, mode,
     ms = max_sq_of(padded_dims)
     if table_dev is None and p not in (1.0, 2.0):
         table_dev = to_dev(cost_table(ms, float(p)))
+    ops = N.torch_ops()
+    if ops is not None and not want_unused:  # the PyTorch extension's operator
+        out = ops.weighted_cost(mu_pad, nu_pad, mu_c, nu_c, ctil_dev, table_dev, int(ms),
+                                [int(d) for d in padded_dims], int(kappa), float(p), int(mode))
+        return out, None
     out = t.empty((B, n, n), dtype=t.float64, device=mu_pad.device)
     unused = t.empty((B, n, n), dtype=t.uint8, device=mu_pad.device) if want_unused else None
     N.check(N.lib().gdt_weighted_cost(

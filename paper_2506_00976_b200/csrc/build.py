@@ -80,7 +80,40 @@ def build(force: bool = False, verbose: bool = False) -> str:
              os.path.join(OBJ, "link.log"))
         if verbose:
             print("linked", LIB)
+    build_torch_ext(force, verbose)
     return LIB
+
+
+TORCH_EXT = os.path.join(HERE, "libgridot_torch.so")
+
+
+def build_torch_ext(force: bool = False, verbose: bool = False) -> str | None:
+    """The PyTorch extension (torch_ops.cpp) that loads libgridot_b200.so as a
+    linked dependency and registers torch.ops.gridot_b200.*; g++ against the
+    installed torch headers, rpath $ORIGIN so the two libraries travel together."""
+    src = os.path.join(HERE, "torch_ops.cpp")
+    hdr = os.path.join(REPO, "include", "gridot_b200.h")
+    if not (force or _newer([src, hdr, LIB, __file__], TORCH_EXT)):
+        return TORCH_EXT
+    try:
+        import torch
+        from torch.utils import cpp_extension
+    except Exception:  # pragma: no cover - torch is part of the image
+        return None
+    inc = []
+    for pth in cpp_extension.include_paths():
+        inc += ["-I", pth]
+    cuda_home = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    libdir = os.path.join(os.path.dirname(torch.__file__), "lib")
+    abi = int(torch._C._GLIBCXX_USE_CXX11_ABI)
+    _run([CXX, "-O2", "-std=c++17", "-fPIC", "-shared", src] + inc +
+         ["-I", os.path.join(cuda_home, "include"), f"-D_GLIBCXX_USE_CXX11_ABI={abi}",
+          "-L", libdir, "-ltorch", "-ltorch_cpu", "-lc10", "-lc10_cuda", "-ltorch_cuda",
+          "-L", HERE, "-lgridot_b200", "-Wl,-rpath,$ORIGIN", "-o", TORCH_EXT],
+         os.path.join(OBJ, "torch_ops.log"))
+    if verbose:
+        print("built", TORCH_EXT)
+    return TORCH_EXT
 
 
 if __name__ == "__main__":

@@ -815,6 +815,16 @@ __global__ void __launch_bounds__(PT) ipf_kernel(
     // follow the staged vector when it is staged, else start at offset 0
     double *prod = (UNIFORM && prod_smem > 0) ? sx + (use_smem ? ((N + 1) & ~1) : 0) : nullptr;
     const bool two_phase = UNIFORM && kappa <= 8 && prod != nullptr;
+    if (two_phase) {  // the pair's CSR / CSC pointers in shared memory (after the products)
+        int32_t *sp = reinterpret_cast<int32_t *>(prod + prod_smem);
+        for (int i = threadIdx.x; i <= U; i += PT) {
+            sp[i] = P.rptr[i];
+            sp[U + 1 + i] = P.cptr[i];
+        }
+        P.rptr = sp;
+        P.cptr = sp + U + 1;
+        __syncthreads();
+    }
     const double *bs = stage(P.b);
     if (two_phase) {
         unit_sums(P.rrc, P.rrf, P.rptr, U, K1, kappa, bs, prod, P.kb, prod_smem, P.pf);
@@ -2450,7 +2460,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
         const int64_t capd = std::min<int64_t>(prods, std::min<int64_t>(room, 20480));
         if (capd >= std::min<int64_t>(prods, 4096)) {
             prod_smem = (int)(capd & ~1ll);
-            dyn = sizeof(double) * (base + prod_smem);
+            dyn = sizeof(double) * (base + prod_smem) + sizeof(int32_t) * 2 * (c.cells + 1);
         }
     }
     if (fast_ipf) {

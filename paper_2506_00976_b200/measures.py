@@ -241,6 +241,9 @@ def sumpool_batch(x, dims, kappa, stats=None):
     block's smallest / largest positive mass and positive-cell count from the
     same pass (gdt_sumpool_stats_f64)."""
     xp, pd = pad_batch(x, dims, kappa)
+    ops = N.torch_ops()
+    if ops is not None:  # the PyTorch extension's operator (same C entry point)
+        return ops.sumpool(xp.contiguous(), [int(d) for d in pd], int(kappa), stats)
     nc = int(np.prod(pd)) // kappa ** len(dims)
     out = torch().empty((x.shape[0], nc), dtype=torch().float64, device=x.device)
     N.check(N.lib().gdt_sumpool_stats_f64(N.ptr(xp), N.ptr(out), N.ptr(stats), x.shape[0],

@@ -271,3 +271,18 @@ def test_exact_module_helpers():
     with pytest.raises(G.DimensionMismatchError):
         m2 = G.GridMeasure(G.GridSpec((2, 2)), np.full(4, 0.25))
         G.wasserstein_1d(m2, m2, 1.0)
+
+
+def test_torch_extension_loads_the_c_abi():
+    """The C library is loaded through the PyTorch extension (its linked
+    dependency): torch.ops.gridot_b200 exists, calls into the same library,
+    and its device operators are registered for CUDA tensors."""
+    import torch
+
+    _native.lib()
+    ops = _native.torch_ops()
+    assert ops is not None
+    assert ops.version() == _native.lib().gdt_version().decode()
+    for name in ("sumpool", "weighted_cost"):
+        assert hasattr(ops, name)
+    assert torch._C._dispatch_has_kernel_for_dispatch_key("gridot_b200::sumpool", "CUDA")
