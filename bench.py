@@ -263,19 +263,23 @@ def run_e2e(args, torch, dist, G, S, wl, prec, combos, dims, Nf, ppr, rank, worl
     for its LPs, so the host's LP capacity is the e2e ceiling at any N."""
     from paper_2506_00976_b200 import distributed as D
 
+    cuda = torch.cuda.is_available()  # (the CPU test of this path runs it under gloo)
+    dev = torch.device("cuda", torch.cuda.current_device()) if cuda else torch.device("cpu")
+    sync = torch.cuda.synchronize if cuda else (lambda: None)
+    pin = (lambda t: t.pin_memory()) if cuda else (lambda t: t)
     lp_threads = max(1, (os.cpu_count() or 1) // world)
     total = ppr * world
     lo, hi = rank * ppr, (rank + 1) * ppr
     if world > 1:
         # global host arrays; this rank fills (and reads) its own shard only
-        g_mu = torch.zeros((total, Nf), dtype=torch.float64).pin_memory()
-        g_nu = torch.zeros((total, Nf), dtype=torch.float64).pin_memory()
+        g_mu = pin(torch.zeros((total, Nf), dtype=torch.float64))
+        g_nu = pin(torch.zeros((total, Nf), dtype=torch.float64))
         g_mu[lo:hi] = torch.from_numpy(mus_h)
         g_nu[lo:hi] = torch.from_numpy(nus_h)
         assert D.shard_range(total, rank, world) == (lo, hi)
     else:
-        g_mu = torch.from_numpy(mus_h).pin_memory()
-        g_nu = torch.from_numpy(nus_h).pin_memory()
+        g_mu = pin(torch.from_numpy(mus_h))
+        g_nu = pin(torch.from_numpy(nus_h))
     kw = dict(precision=prec, xi=wl.xi, max_iter=wl.max_iter, lp_threads=lp_threads)
 
     def call(timings=None):
@@ -285,7 +289,7 @@ def run_e2e(args, torch, dist, G, S, wl, prec, combos, dims, Nf, ppr, rank, worl
         return res, None
 
     call()  # untimed warm-up
-    torch.cuda.synchronize()
+    sync()
     if world > 1:
         dist.barrier()
     times, parts, table = [], {}, None
@@ -293,7 +297,7 @@ def run_e2e(args, torch, dist, G, S, wl, prec, combos, dims, Nf, ppr, rank, worl
         tm = {}
         t0 = time.perf_counter()
         res, table = call(tm)
-        torch.cuda.synchronize()
+        sync()
         times.append(time.perf_counter() - t0)
         for key, val in tm.items():
             if isinstance(val, float):
@@ -303,7 +307,7 @@ def run_e2e(args, torch, dist, G, S, wl, prec, combos, dims, Nf, ppr, rank, worl
             assert all(not isinstance(r[m], Exception) for r in res[key] for m in r)
     e2e_s = statistics.mean(times)
     if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     h2d = 2 * ppr * Nf * 8
@@ -325,7 +329,7 @@ def run_e2e(args, torch, dist, G, S, wl, prec, combos, dims, Nf, ppr, rank, worl
     if world > 1:
         # the gathered table must equal the table of ONE process computing the
         # whole global batch (rank 0, all host cores, untimed), bit for bit
-        ok = torch.zeros(1, device="cuda")
+        ok = torch.zeros(1, device=dev)
         if rank == 0:
             a_mu, a_nu = S.batch(CFG, 0, total)
             whole = G.quantized_bounds_many(a_mu, a_nu, dims, combos, precision=prec, xi=wl.xi,

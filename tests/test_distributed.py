@@ -171,3 +171,74 @@ def test_pack_unpack_roundtrip():
             assert "primal_upscaling" not in b["reports"] and b["status"] & 4
         else:
             assert b["reports"]["primal_upscaling"].components == a["primal_upscaling"].components
+
+
+def _bench_e2e_worker(rank, world, port, q):
+    """bench.run_e2e under torchrun semantics (world 2, gloo), with a host
+    stand-in for the device computation: sharding, the gather of records,
+    the max-over-ranks time and the single-process check of the gathered table."""
+    import argparse
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_2506_00976_b200 import synthetic as S
+
+    def fake(mus, nus, dims, combos, **kw):
+        mus = np.asarray(mus)
+        out = {}
+        for k, p in combos:
+            rows = []
+            for m in mus:
+                v = float(m[0] * 1e6) + k + p
+                pu = BoundReport("primal_upscaling", v, v,
+                                 {"transport": v, "delta_mu": 0.0, "delta_nu": 0.0,
+                                  "marginal_gap": 0.0, "converged": 1.0}, 0.1, 1, 64)
+                du = BoundReport("dual_upscaling", v, v, {"dual_value": v * v}, 0.1, None, 64)
+                wc = BoundReport("weighted_cost", v, v, {"transport": v}, 0.1, None, 64)
+                rows.append({"weighted_cost": wc, "min_cost": wc, "primal_upscaling": pu,
+                             "dual_upscaling": du})
+            out[(int(k), float(p))] = rows
+        return out
+
+    class G:  # the public API the single-process check calls
+        quantized_bounds_many = staticmethod(fake)
+
+    D.quantized_bounds_many = fake  # the per-rank compute of distributed_bounds_many
+    bench.CFG = 3
+    wl = S.WORKLOADS[3]
+    ppr = 2
+    lo = rank * ppr
+    mus_h, nus_h = S.batch(3, lo, lo + ppr)
+    Nf = mus_h.shape[1]
+    args = argparse.Namespace(e2e_steps=2)
+    out = bench.run_e2e(args, torch, dist, G, S, wl, "fp32", list(wl.combos), wl.dims, Nf, ppr,
+                        rank, world, mus_h, nus_h)
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_e2e_distributed_leg_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_e2e_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert got[r]["gather_matches_single_process"] is True
+        assert got[r]["gathered_pairs"] == 4
+        assert got[r]["value"] > 0 and got[r]["steps"] == 2
+    assert got[0]["s_per_step"] == got[1]["s_per_step"]  # max over ranks
