@@ -35,3 +35,4 @@ $CMD64 > gpurun_out/prof_fp64_plain.json 2> gpurun_out/prof_fp64_plain.err && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cbar_exact2d|pruned_ct_kernel" -c 2 \
     -o gpurun_out/prof_fp64 $CMD64 > gpurun_out/ncu_fp64.log 2>&1
 echo "fp64 exit $?" >> gpurun_out/ncu_fp64.log
+bash scripts/ncu_export.sh

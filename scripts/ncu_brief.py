@@ -4,8 +4,17 @@ import csv
 import subprocess
 import sys
 
+
+def raw_page(path):
+    """Raw-page CSV text of a report; a ready-made *.raw.csv (scripts/ncu_export.sh) is read as is."""
+    if path.endswith(".csv"):
+        return open(path).read()
+    return subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                          text=True).stdout
+
+
 rep = sys.argv[1]
-out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+out = raw_page(rep)
 rows = list(csv.reader(out.splitlines()))
 h = rows[0]
 KEYS = ["sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",

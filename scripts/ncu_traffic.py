@@ -13,13 +13,21 @@ import os
 import subprocess
 import sys
 
+
+def raw_page(path):
+    """Raw-page CSV text of a report; a ready-made *.raw.csv (scripts/ncu_export.sh) is read as is."""
+    if path.endswith(".csv"):
+        return open(path).read()
+    return subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                          text=True).stdout
+
+
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 out_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
                         f"ncu_traffic_cfg{sys.argv[1]}.json")
 res = {}
 for rep in sys.argv[2:]:
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    txt = raw_page(rep)
     rows = list(csv.reader(txt.splitlines()))
     hdr, units = rows[0], rows[1]
     for r in rows[2:]:

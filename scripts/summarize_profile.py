@@ -19,6 +19,15 @@ import subprocess
 import sys
 
 
+def raw_page(path):
+    """Raw-page CSV text of a report; a ready-made *.raw.csv (scripts/ncu_export.sh) is read as is."""
+    if path.endswith(".csv"):
+        return open(path).read()
+    return subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                          text=True).stdout
+
+
+
 def launches(path):
     rows = list(csv.reader(open(path)))
     hdr, data = None, []
@@ -60,8 +69,7 @@ RAW = {
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    out = raw_page(path)
     rows = list(csv.reader(out.splitlines()))
     if len(rows) < 3:
         return []
