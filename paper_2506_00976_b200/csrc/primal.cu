@@ -31,6 +31,8 @@
 //     from the moments when p == 2 with the uniform kernel (the cost is a
 //     quadratic), by direct summation with tabulated costs otherwise;
 //   finish_kernel: fixed-order reduction of the per-CTA partials.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace gdt {
@@ -719,6 +721,84 @@ __global__ void run_list_kernel(const int64_t *__restrict__ arc_off,
             ++r;
         };
         walk_blocks(pc + a0 + lo, hi - lo, c, f, kappa, fn);
+    }
+}
+
+// The same run lists without the serial walk, one thread per ARC: the
+// position of run (arc q, offsets s_{d-1..1}) in its unit's walk order follows
+// from the coordinate groups q belongs to (per level the walk visits the
+// groups of equal coarse coordinate in order and, inside a group, the kappa
+// fine offsets one after the other), so a thread finds its arc's groups once
+// (a scan over the unit's arcs) and then writes its K1 runs.  Output
+// identical to run_list_kernel.
+__global__ void __launch_bounds__(128) run_list_par_kernel(
+    const int64_t *__restrict__ arc_off, const int32_t *__restrict__ ptr,
+    const int64_t *__restrict__ pc, const double *__restrict__ mass,
+    const double *__restrict__ W, int64_t batch, G32 f, G32 c, int kappa,
+    int32_t *__restrict__ cells, double *__restrict__ coefs) {
+    const int n = c.cells, nd = f.nd;
+    const int K1 = (int)ipow(kappa, nd - 1);
+    const double Wu = W[0];
+    const int64_t total = arc_off[batch];
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        // pair of arc g: last b with arc_off[b] <= g
+        int64_t blo = 0, bhi = batch - 1;
+        while (blo < bhi) {
+            const int64_t mid = (blo + bhi + 1) >> 1;
+            if (arc_off[mid] <= g) blo = mid;
+            else bhi = mid - 1;
+        }
+        const int64_t b = blo, a0 = arc_off[b];
+        const int qa = (int)(g - a0);  // arc index inside the pair
+        const int32_t *pp = ptr + b * (n + 1);
+        if (qa >= pp[n]) continue;
+        int ulo = 0, uhi = n - 1;  // unit of the arc: last u with ptr[u] <= qa
+        while (ulo < uhi) {
+            const int mid = (ulo + uhi + 1) >> 1;
+            if (pp[mid] <= qa) ulo = mid;
+            else uhi = mid - 1;
+        }
+        const int lo0 = pp[ulo], cnt = pp[ulo + 1] - lo0, q = qa - lo0;
+        const int64_t *up = pc + a0 + lo0;
+        int32_t *oc = cells + (a0 + lo0) * K1;
+        double *of = coefs + (a0 + lo0) * K1;
+        const double cf = __dmul_rn(mass[a0 + qa], Wu);
+        const int64_t w = up[q];
+        // per level (d-1 .. 1): runs before the arc's group, the group's size,
+        // the cell offset of the arc's coarse coordinate
+        int before[GDT_MAX_DIM], gsize[GDT_MAX_DIM], cbase[GDT_MAX_DIM];
+        int lo = 0, hi = cnt, kp = K1, pos0 = 0;
+#pragma unroll
+        for (int level = GDT_MAX_DIM - 1; level >= 1; --level) {
+            if (level > nd - 1) continue;
+            const int cr = pc_coord(w, level);
+            int gs = q, ge = q + 1;
+            while (gs > lo && pc_coord(up[gs - 1], level) == cr) --gs;
+            while (ge < hi && pc_coord(up[ge], level) == cr) ++ge;
+            pos0 += (gs - lo) * kp;
+            kp /= kappa;  // runs per arc below this level
+            before[level] = kp;
+            gsize[level] = ge - gs;
+            cbase[level] = cr * kappa;
+            lo = gs;
+            hi = ge;
+        }
+        pos0 += q - lo;
+        const int cell0 = pc_coord(w, 0) * kappa;
+        for (int r = 0; r < K1; ++r) {
+            int rem = r, pos = pos0, cell = cell0;
+#pragma unroll
+            for (int level = GDT_MAX_DIM - 1; level >= 1; --level) {
+                if (level > nd - 1) continue;
+                const int sa = rem / before[level];
+                rem -= sa * before[level];
+                pos += sa * gsize[level] * before[level];
+                cell += (cbase[level] + sa) * f.stride[level];
+            }
+            oc[pos] = cell;
+            of[pos] = cf;
+        }
     }
 }
 
@@ -1543,12 +1623,18 @@ constexpr int MT = 128;  // threads of the moments/price kernels
 
 // Per block: TV partials (per CTA) and moments of a and b about the block
 // centre: mom[(b*n + k)*MW + {A0, A1[d], A2, B0, B1[d], B2}].
-template <bool UNIFORM>
+// ND / KAP > 0: compile-time dimension and pooling factor (the cell index
+// arithmetic becomes shifts, the moment arrays stay in registers); 0 = runtime.
+// tv_w: the padded grid's tv_weights table (host-computed with the
+// reference's formula, measures.py:289-296) or NULL (computed per cell).
+template <bool UNIFORM, int ND, int KAP>
 __global__ void __launch_bounds__(MT) moments_tv_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu, const double *__restrict__ out,
     const int32_t *__restrict__ status, double *__restrict__ scratch, int64_t stride_pair,
-    double *__restrict__ mom, double *__restrict__ part, G32 f, G32 c, int kappa, double p,
-    int want_moments, int lb) {
+    double *__restrict__ mom, double *__restrict__ part, G32 f, G32 c, int kappa_rt, double p,
+    int want_moments, int lb, const double *__restrict__ tv_w) {
+    const int kappa = KAP ? KAP : kappa_rt;
+    const int nd = ND ? ND : f.nd;
     // one group of `lb` consecutive lanes per coarse block (tv_lanes: a power
     // of two dividing kappa^d): lane j of the group takes the block's cells
     // j, j + lb, ...; moments fold over the group by shuffles, TV partials
@@ -1556,9 +1642,9 @@ __global__ void __launch_bounds__(MT) moments_tv_kernel(
     __shared__ double sh[32];
     const int64_t b = blockIdx.y;
     const int N = f.cells, n = c.cells;
-    const int m = (int)ipow(kappa, f.nd);
+    const int m = (int)ipow(kappa, nd);
     const int U = UNIFORM ? n : N;
-    const int MW = 2 * (f.nd + 2);
+    const int MW = 2 * (nd + 2);
     const int gid = blockIdx.x * MT + threadIdx.x;
     const int k = gid / lb, j = gid - k * lb;
     double tmu = 0.0, tnu = 0.0;
@@ -1574,14 +1660,16 @@ __global__ void __launch_bounds__(MT) moments_tv_kernel(
         for (int t = j; t < m; t += lb) {
             int i = origin, rem = t;
             double dl[GDT_MAX_DIM], r2 = 0.0;
-            for (int q = 0; q < f.nd; ++q) {
+#pragma unroll
+            for (int q = 0; q < (ND ? ND : GDT_MAX_DIM); ++q) {
+                if (q >= nd) break;
                 const int o = rem % kappa;
                 rem /= kappa;
                 i += o * f.stride[q];
                 dl[q] = (double)o - ctr;
                 r2 += dl[q] * dl[q];
             }
-            const double w = tv_weight(i, f, p);
+            const double w = tv_w ? __ldg(tv_w + i) : tv_weight(i, f, p);
             const double kbu = kb[UNIFORM ? k : k * m + t];
             const double ktu = kta[UNIFORM ? k : k * m + t];
             const double ai = a[i], bi = bv[i];
@@ -1590,29 +1678,37 @@ __global__ void __launch_bounds__(MT) moments_tv_kernel(
             tmu += w * fabs(__dsub_rn(mh, mub[i]));
             tnu += w * fabs(__dsub_rn(nh, nub[i]));
             if (want_moments) {
-                for (int q = 0; q < f.nd; ++q) {
+#pragma unroll
+                for (int q = 0; q < (ND ? ND : GDT_MAX_DIM); ++q) {
+                    if (q >= nd) break;
                     A[1 + q] += ai * dl[q];
                     Bm[1 + q] += bi * dl[q];
                 }
                 A[0] += ai;
                 Bm[0] += bi;
-                A[1 + f.nd] += ai * r2;
-                Bm[1 + f.nd] += bi * r2;
+                A[1 + GDT_MAX_DIM] += ai * r2;
+                Bm[1 + GDT_MAX_DIM] += bi * r2;
             }
         }
     }
     if (want_moments) {  // uniform across the CTA: every lane takes part in the shuffles
-        for (int q = 0; q < f.nd + 2; ++q)
+#pragma unroll
+        for (int q = 0; q < 2 + GDT_MAX_DIM; ++q)
             for (int o = 1; o < lb; o <<= 1) {
                 A[q] += __shfl_xor_sync(0xffffffffu, A[q], o, lb);
                 Bm[q] += __shfl_xor_sync(0xffffffffu, Bm[q], o, lb);
             }
         if (live && j == 0) {
             double *o = mom + ((int64_t)b * n + k) * MW;
-            for (int q = 0; q < f.nd + 2; ++q) {
+            // slots: A0, A1[nd], A2, then B likewise (second moments kept in the last register slot)
+#pragma unroll
+            for (int q = 0; q < 1 + GDT_MAX_DIM; ++q) {
+                if (q > nd) break;
                 o[q] = A[q];
-                o[f.nd + 2 + q] = Bm[q];
+                o[nd + 2 + q] = Bm[q];
             }
+            o[nd + 1] = A[1 + GDT_MAX_DIM];
+            o[2 * nd + 3] = Bm[1 + GDT_MAX_DIM];
         }
     }
     tmu = block_sum<MT>(tmu, sh);
@@ -1779,6 +1875,399 @@ __global__ void finish_kernel(const double *__restrict__ tv_part, int tv_ctas,
         if (pr_part) out[b * 8 + 0] = pr;  // else the caller's kernel priced already
         out[b * 8 + 1] = tmu;
         out[b * 8 + 2] = tnu;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ipf_cluster_kernel: the exact-order IPF of ipf_kernel<true> (uniform kernel,
+// two-phase unit sums) with one thread-block CLUSTER per pair.
+//
+// One CTA per pair left most of the GPU idle at the benchmark batch sizes
+// (64 CTAs at cfg5, 45 at cfg3) and forced the products of a direction through
+// several shared-memory batches, whose longest chains then ran one after the
+// other.  Here rank r of the cluster owns a contiguous range of row units and
+// of column units (balanced by arc count) and a contiguous slice of the fine
+// cells.  Every unit is still summed by ONE thread over its products in the
+// reference's order -- the bits of kb / kta, a and b do not depend on the
+// cluster size -- only units and cells are spread over more SMs.  The vectors
+// a, b, kb, kta live in global memory (L2); four cluster barriers per sweep
+// order the phases (release/acquire at cluster scope, so plain loads after a
+// barrier see the other CTAs' stores):
+//     col sums | B | col cells (b, zero-column flag) | C | row sums | D |
+//     row cells (next a, gap / range partials) | A: fold of the per-CTA
+//     records in rank order, the reference's checks (sinkhorn.py:125-141)
+// Every CTA takes the same decisions from the same folded record.
+// ---------------------------------------------------------------------------
+
+// loads of data another CTA of the cluster wrote before the last barrier:
+// explicit ld.global (never the non-coherent path), issue order kept
+__device__ __forceinline__ double ld_gl(const double *p) {
+    double v;
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ld_gl2(const double *p) {
+    double2 v;
+    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
+// products of `nruns` runs (KAP cells each) in chain order into shared memory;
+// RU runs per thread in flight (descriptors, then gathers, then products)
+template <int KAP>
+__device__ __forceinline__ void cl_products(const int32_t *__restrict__ cells,
+                                            const double *__restrict__ coefs, int nruns,
+                                            const double *x, double *prod) {
+    constexpr int RU = KAP <= 4 ? 4 : 2;
+    for (int r0 = threadIdx.x; r0 < nruns; r0 += PT * RU) {
+        int cl[RU];
+        double cf[RU], xv[RU][KAP];
+#pragma unroll
+        for (int q = 0; q < RU; ++q) {
+            const int r = r0 + q * PT;
+            cl[q] = r < nruns ? __ldg(cells + r) : 0;
+            cf[q] = r < nruns ? __ldg(coefs + r) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < RU; ++q) {
+            if (r0 + q * PT < nruns) {
+#pragma unroll
+                for (int i = 0; i < KAP; i += 2) {
+                    const double2 t = ld_gl2(x + cl[q] + i);
+                    xv[q][i] = t.x;
+                    xv[q][i + 1] = t.y;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < RU; ++q) {
+            const int r = r0 + q * PT;
+            if (r >= nruns) break;
+            double *pp = prod + (int64_t)r * KAP;
+#pragma unroll
+            for (int i = 0; i < KAP; i += 2)
+                *reinterpret_cast<double2 *>(pp + i) =
+                    make_double2(__dmul_rn(cf[q], xv[q][i]), __dmul_rn(cf[q], xv[q][i + 1]));
+        }
+    }
+}
+
+// sums (and reciprocals) of units [ua, ub) of one direction: batches of whole
+// units whose products fit `cap` doubles; a unit larger than `cap` is summed
+// straight from its run list by one thread
+__device__ __noinline__ void cl_unit_sums(const int32_t *__restrict__ cells,
+                                          const double *__restrict__ coefs,
+                                          const int32_t *__restrict__ ptr, int ua, int ub, int K1,
+                                          int kappa, const double *x, double *prod,
+                                          double *out_sum, double *out_rcp, int cap) {
+    const int per = K1 * kappa;
+    int u0 = ua;
+    while (u0 < ub) {
+        const int a0 = ptr[u0];
+        int lo = u0 + 1, hi = ub;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((int64_t)(ptr[mid] - a0) * per <= cap) lo = mid;
+            else hi = mid - 1;
+        }
+        const int u1 = lo;
+        if ((int64_t)(ptr[u1] - a0) * per <= cap) {
+            const int nruns = (ptr[u1] - a0) * K1;
+            const int32_t *bc = cells + (int64_t)a0 * K1;
+            const double *bf = coefs + (int64_t)a0 * K1;
+            switch (kappa) {
+                case 2: cl_products<2>(bc, bf, nruns, x, prod); break;
+                case 4: cl_products<4>(bc, bf, nruns, x, prod); break;
+                default: cl_products<8>(bc, bf, nruns, x, prod); break;
+            }
+            __syncthreads();
+            for (int u = u0 + (int)threadIdx.x; u < u1; u += PT) {
+                const int64_t plo = (int64_t)(ptr[u] - a0) * per, phi = (int64_t)(ptr[u + 1] - a0) * per;
+                const double v = chain_sum(prod + plo, (int)(phi - plo), true);
+                out_sum[u] = v;
+                out_rcp[u] = v > 0.0 ? __drcp_rn(v) : 0.0;
+            }
+            __syncthreads();
+        } else if (threadIdx.x == 0) {
+            const int rlo = ptr[u0] * K1, rhi = ptr[u0 + 1] * K1;
+            const double v = run_list_sum_any(cells + rlo, coefs + rlo, rhi - rlo, x, kappa, 0);
+            out_sum[u0] = v;
+            out_rcp[u0] = v > 0.0 ? __drcp_rn(v) : 0.0;
+        }
+        u0 = u1;
+    }
+}
+
+constexpr int CL_U = 4;  // cells per thread in flight in the cluster kernel's cell passes
+
+// the cell passes of ipf_kernel on the cell slice [c0, c1) of this CTA
+__device__ __forceinline__ void cl_cells_row(const double *__restrict__ mu, int c0, int c1,
+                                             const int32_t *__restrict__ bmap, bool init,
+                                             const double *a_cur, double *a_next, Red &r,
+                                             const double *kbs, const double *rcps) {
+    for (int i0 = c0 + (int)threadIdx.x; i0 < c1; i0 += PT * CL_U) {
+        int kk[CL_U];
+        double mu_[CL_U], ai_[CL_U], acc_[CL_U], rc_[CL_U];
+#pragma unroll
+        for (int q = 0; q < CL_U; ++q) {
+            const int i = i0 + q * PT;
+            const bool in = i < c1;
+            kk[q] = in ? __ldg(bmap + i) : 0;
+            mu_[q] = in ? __ldg(mu + i) : 0.0;
+            ai_[q] = (in && !init) ? a_cur[i] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < CL_U; ++q) {
+            acc_[q] = ld_gl(kbs + kk[q]);
+            rc_[q] = ld_gl(rcps + kk[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < CL_U; ++q) {
+            const int i = i0 + q * PT;
+            if (i >= c1) break;
+            const double acc = acc_[q], mui = mu_[q];
+            if (!init) {
+                const double ai = ai_[q];
+                range_acc(ai, r.amin, r.amax, r.nonfinite);
+                if (mui > 0.0) r.gap += fabs(__dsub_rn(__dmul_rn(ai, acc), mui));
+            }
+            double an = 0.0;
+            if (mui > 0.0) {
+                if (acc <= 0.0) r.zrow = 1;
+                else an = div_shared(mui, acc, rc_[q]);
+            }
+            a_next[i] = an;
+        }
+    }
+}
+
+__device__ __forceinline__ void cl_cells_col(const double *__restrict__ nu, int c0, int c1,
+                                             const int32_t *__restrict__ bmap, double *bvec, Red &r,
+                                             const double *ktas, const double *rcps) {
+    for (int j0 = c0 + (int)threadIdx.x; j0 < c1; j0 += PT * CL_U) {
+        int ll[CL_U];
+        double nu_[CL_U], acc_[CL_U], rc_[CL_U];
+#pragma unroll
+        for (int q = 0; q < CL_U; ++q) {
+            const int j = j0 + q * PT;
+            const bool in = j < c1;
+            ll[q] = in ? __ldg(bmap + j) : 0;
+            nu_[q] = in ? __ldg(nu + j) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < CL_U; ++q) {
+            acc_[q] = ld_gl(ktas + ll[q]);
+            rc_[q] = ld_gl(rcps + ll[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < CL_U; ++q) {
+            const int j = j0 + q * PT;
+            if (j >= c1) break;
+            const double acc = acc_[q], nuj = nu_[q];
+            double bj = 0.0;
+            if (nuj > 0.0) {
+                if (acc <= 0.0) r.zcol = 1;
+                else bj = div_shared(nuj, acc, rc_[q]);
+                range_acc(bj, r.bmin, r.bmax, r.nonfinite);
+                r.gap += fabs(__dsub_rn(nuj, __dmul_rn(bj, acc)));
+            }
+            bvec[j] = bj;
+        }
+    }
+}
+
+// CTA reduction, then the cluster's records combined in rank order (includes
+// one cluster barrier; every CTA ends with the same record)
+__device__ void cl_reduce_red(Red &r, double *sh, double *xch, unsigned rank, unsigned cs) {
+    block_reduce_red(r, sh);
+    if (threadIdx.x == 0) {
+        double *o = xch + rank * 8;
+        o[0] = r.gap;
+        o[1] = r.amin;
+        o[2] = r.amax;
+        o[3] = r.bmin;
+        o[4] = r.bmax;
+        o[5] = (double)(r.zrow | (r.zcol << 1) | (r.nonfinite << 2));
+    }
+    cluster_sync_all();
+    if (threadIdx.x < cs * 8) sh[threadIdx.x] = ld_gl(xch + threadIdx.x);
+    __syncthreads();
+    Red o = red_init();
+    for (unsigned q = 0; q < cs; ++q) {
+        const double *s = sh + q * 8;
+        o.gap += s[0];
+        o.amin = fmin(o.amin, s[1]);
+        o.amax = fmax(o.amax, s[2]);
+        o.bmin = fmin(o.bmin, s[3]);
+        o.bmax = fmax(o.bmax, s[4]);
+        const int fl = (int)s[5];
+        o.zrow |= fl & 1;
+        o.zcol |= (fl >> 1) & 1;
+        o.nonfinite |= (fl >> 2) & 1;
+    }
+    __syncthreads();
+    r = o;
+}
+
+constexpr int CL_MAX = 8;       // largest cluster
+constexpr int CL_MIN_UNITS = 128;  // the 4th per-pair block of U doubles holds the exchange area
+
+__global__ void __launch_bounds__(PT) ipf_cluster_kernel(
+    const double *__restrict__ mu, const double *__restrict__ nu,
+    const int64_t *__restrict__ arc_off, const int32_t *__restrict__ row_ptr,
+    const int32_t *__restrict__ col_ptr, const double *__restrict__ xi_in, int64_t max_iter,
+    int N, int U, int kappa, int K1, double *__restrict__ out, int32_t *__restrict__ status,
+    double *scratch, int64_t stride_pair, const int32_t *__restrict__ bmap,
+    const int32_t *__restrict__ rl_cells, const double *__restrict__ rl_coef,
+    const int32_t *__restrict__ cl_cells, const double *__restrict__ cl_coef, int cap) {
+    extern __shared__ double prod[];  // [cap] products of one batch
+    __shared__ double sh[(PT / 32 + 1) * 6 > CL_MAX * 8 ? (PT / 32 + 1) * 6 : CL_MAX * 8];
+    __shared__ int part[4];
+    const unsigned cs = cluster_size(), rank = cluster_rank_id();
+    const int64_t b = blockIdx.x / cs;
+    const double *mub = mu + b * N, *nub = nu + b * N;
+    const int64_t a0 = arc_off[b];
+    const int32_t *rptr = row_ptr + b * (U + 1), *cptr = col_ptr + b * (U + 1);  // (moved to shared memory below)
+    const int32_t *rrc = rl_cells + a0 * K1, *crc = cl_cells + a0 * K1;
+    const double *rrf = rl_coef + a0 * K1, *crf = cl_coef + a0 * K1;
+    double *ws = scratch + b * stride_pair;
+    double *aA = ws, *aB = ws + N, *bv = ws + 2 * (int64_t)N;
+    double *kb = ws + 3 * (int64_t)N, *kta = kb + U, *rcp = kta + U, *xch = rcp + U;
+    // xch: [0, 64) reduction records, [64, 72) zero-column flags, [80, 88) support counts
+
+    // unit ranges balanced by arc count: rank r takes the units whose first
+    // arc lies in [A r / cs, A (r + 1) / cs)
+    if (threadIdx.x < 4) {
+        const int32_t *ptr = threadIdx.x < 2 ? rptr : cptr;
+        const unsigned edge = rank + (threadIdx.x & 1);
+        int res;
+        if (edge == 0) res = 0;
+        else if (edge == cs) res = U;
+        else {
+            const int64_t target = (int64_t)ptr[U] * edge / cs;
+            int lo = 0, hi = U;  // first u with ptr[u] >= target
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (ptr[mid] >= target) hi = mid;
+                else lo = mid + 1;
+            }
+            res = lo;
+        }
+        part[threadIdx.x] = res;
+    }
+    const int cper = ((N + (int)cs - 1) / (int)cs + 7) & ~7;
+    const int c0 = min(N, (int)rank * cper), c1 = min(N, c0 + cper);
+    // the pair's CSR / CSC pointers in shared memory (after the products):
+    // the batch searches of cl_unit_sums then stay on chip
+    {
+        int32_t *sp = reinterpret_cast<int32_t *>(prod + cap);
+        for (int i = threadIdx.x; i <= U; i += PT) {
+            sp[i] = rptr[i];
+            sp[U + 1 + i] = cptr[i];
+        }
+        rptr = sp;
+        cptr = sp + U + 1;
+    }
+
+    // supports, b = ones over the target support, the default xi (quantized.py:317-320)
+    double cnt = 0.0;
+    for (int i0 = c0 + (int)threadIdx.x; i0 < c1; i0 += PT * 4) {
+        double mi[4], ni[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q * PT;
+            mi[q] = i < c1 ? __ldg(mub + i) : 0.0;
+            ni[q] = i < c1 ? __ldg(nub + i) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q * PT;
+            if (i >= c1) break;
+            cnt += (mi[q] > 0.0 ? 1.0 : 0.0) + (ni[q] > 0.0 ? 1.0 : 0.0);
+            bv[i] = ni[q] > 0.0 ? 1.0 : 0.0;
+        }
+    }
+    cnt = block_sum<PT>(cnt, sh);
+    if (threadIdx.x == 0) xch[80 + rank] = cnt;
+    cluster_sync_all();
+    cnt = 0.0;
+    for (unsigned q = 0; q < cs; ++q) cnt += ld_gl(xch + 80 + q);  // integers: exact in any order
+    const double xi = xi_in[b] < 0.0 ? 1e-9 * cnt : xi_in[b];
+    const int ru0 = part[0], ru1 = part[1], cu0 = part[2], cu1 = part[3];
+
+    Red r = red_init();
+    double *a_cur = aA, *a_nxt = aB;
+    cl_unit_sums(rrc, rrf, rptr, ru0, ru1, K1, kappa, bv, prod, kb, rcp, cap);
+    cluster_sync_all();
+    cl_cells_row(mub, c0, c1, bmap, true, nullptr, a_cur, r, kb, rcp);
+    cl_reduce_red(r, sh, xch, rank, cs);
+    int st = r.zrow ? GDT_PAIR_ZERO_DENOM_ROW : GDT_PAIR_OK;
+    int64_t it = 0;
+    double gap = INFINITY;
+    bool converged = false;
+    while (st == GDT_PAIR_OK && it < max_iter) {
+        ++it;
+        EX_TRACE(0);
+        Red rc = red_init();
+        cl_unit_sums(crc, crf, cptr, cu0, cu1, K1, kappa, a_cur, prod, kta, rcp, cap);
+        EX_TRACE(1);
+        cluster_sync_all();  // B
+        EX_TRACE(2);
+        cl_cells_col(nub, c0, c1, bmap, bv, rc, kta, rcp);
+        EX_TRACE(3);
+        const int zc = __syncthreads_or(rc.zcol);
+        if (threadIdx.x == 0) xch[64 + rank] = (double)zc;
+        cluster_sync_all();  // C: b complete, flags visible
+        {
+            int any = 0;
+            for (unsigned q = 0; q < cs; ++q) any |= ld_gl(xch + 64 + q) != 0.0;
+            if (any) {  // before anything reads b
+                st = GDT_PAIR_ZERO_DENOM_COL;
+                break;
+            }
+        }
+        EX_TRACE(4);
+        cl_unit_sums(rrc, rrf, rptr, ru0, ru1, K1, kappa, bv, prod, kb, rcp, cap);
+        EX_TRACE(5);
+        cluster_sync_all();  // D
+        EX_TRACE(6);
+        cl_cells_row(mub, c0, c1, bmap, false, a_cur, a_nxt, rc, kb, rcp);
+        EX_TRACE(7);
+        cl_reduce_red(rc, sh, xch, rank, cs);  // A
+        EX_TRACE(8);
+        const bool bad_a = rc.amin <= rc.amax &&
+                           (rc.amin < 1e-100 || rc.amax > 1e100 || !isfinite(rc.amax));
+        const bool bad_b = rc.bmin <= rc.bmax &&
+                           (rc.bmin < 1e-100 || rc.bmax > 1e100 || !isfinite(rc.bmax));
+        if (bad_a || bad_b || rc.nonfinite) {
+            st = GDT_PAIR_OVERFLOW;
+            break;
+        }
+        gap = rc.gap;
+        if (gap < xi) {
+            converged = true;
+            break;
+        }
+        if (it >= max_iter) break;
+        if (rc.zrow) {
+            st = GDT_PAIR_ZERO_DENOM_ROW;
+            break;
+        }
+        double *tmp = a_cur;
+        a_cur = a_nxt;
+        a_nxt = tmp;
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+        status[b] = st;
+        double *o = out + b * 8;
+        o[0] = 0.0;
+        o[1] = 0.0;
+        o[2] = 0.0;
+        o[3] = gap;
+        o[4] = (double)it;
+        o[5] = converged ? 1.0 : 0.0;
+        o[6] = cnt;
+        o[7] = a_cur == aA ? 0.0 : 1.0;
     }
 }
 
@@ -2511,10 +3000,59 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
     } else if (uni) {
         double *rl_coef = ws + L.rl_off, *cl_coef = rl_coef + L.runs;
         int32_t *rl_cells = reinterpret_cast<int32_t *>(cl_coef + L.runs), *cl_cells = rl_cells + L.runs;
-        run_list_kernel<<<grid_size(batch * c.cells, 128), 128, 0, st>>>(
+        run_list_par_kernel<<<grid_size(batch * 2 * c.cells, 128), 128, 0, st>>>(
             arc_off, row_ptr, rpc, row_arc_mass, kernel_w, batch, f32, c32, kappa, rl_cells, rl_coef);
-        run_list_kernel<<<grid_size(batch * c.cells, 128), 128, 0, st>>>(
+        run_list_par_kernel<<<grid_size(batch * 2 * c.cells, 128), 128, 0, st>>>(
             arc_off, col_ptr, cpc, col_arc_mass, kernel_w, batch, f32, c32, kappa, cl_cells, cl_coef);
+        // one cluster per pair when that puts more SMs to work (see
+        // ipf_cluster_kernel); GRIDOT_IPF_CLUSTER=<n> forces the cluster size
+        // (1 = the single-CTA kernel), for tests and measurements
+        int csz = 1;
+        if (prod_smem > 0 && c.cells >= CL_MIN_UNITS && (kappa == 2 || kappa == 4 || kappa == 8)) {
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            csz = (int)std::max<int64_t>(1, std::min<int64_t>(CL_MAX, sms / batch));
+            if (const char *e = std::getenv("GRIDOT_IPF_CLUSTER")) {
+                const int v = std::atoi(e);
+                if (v >= 1 && v <= CL_MAX) csz = v;
+            }
+        }
+        bool launched = false;
+        while (csz > 1 && !launched) {
+            // products of one CTA's units in one batch when they fit 160 KB
+            const int64_t prods = 2 * c.cells * (f.cells / c.cells);
+            const int cap = (int)std::min<int64_t>(20480, ((prods / csz + 4095) / 2048) * 2048);
+            const size_t cdyn = sizeof(double) * (size_t)cap + sizeof(int32_t) * 2 * (c.cells + 1);
+            cudaFuncSetAttribute(ipf_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)cdyn);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(batch * csz));
+            cfg.blockDim = dim3(PT);
+            cfg.dynamicSmemBytes = cdyn;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)csz;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            const int K1 = (int)(f.cells / c.cells / kappa);
+            const cudaError_t e = cudaLaunchKernelEx(
+                &cfg, ipf_cluster_kernel, mu, nu, arc_off, row_ptr, col_ptr, xi, max_iter,
+                (int)f.cells, (int)c.cells, kappa, K1, out, status, ws, L.stride_pair,
+                (const int32_t *)bmap, (const int32_t *)rl_cells, (const double *)rl_coef,
+                (const int32_t *)cl_cells, (const double *)cl_coef, cap);
+            if (e == cudaSuccess) launched = true;
+            else {
+                cudaGetLastError();  // this cluster size is not schedulable here: try a smaller one
+                --csz;
+            }
+        }
+        if (launched) {
+            // (pricing and TV below read the same per-pair layout)
+        } else {
         if (dyn > 48 * 1024)
             cudaFuncSetAttribute(ipf_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)dyn);
@@ -2525,6 +3063,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
             mu, nu, arc_off, row_ptr, row_arc_col, row_arc_mass, col_ptr, col_arc_row,
             col_arc_mass, kernel_w, xi, max_iter, f32, c32, kappa, out, status, ws, L.stride_pair,
             rpc, cpc, use_smem, bmap, rl_cells, rl_coef, cl_cells, cl_coef, prod_smem);
+        }
     } else {
         if (dyn > 48 * 1024)
             cudaFuncSetAttribute(ipf_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2541,18 +3080,27 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
                                                                          (int)c.cells, arc_row);
     dim3 gtv((unsigned)L.tv_ctas, (unsigned)batch), gpr((unsigned)L.pr_ctas, (unsigned)batch);
     if (uni) {
-        moments_tv_kernel<true><<<gtv, MT, 0, st>>>(mu, nu, out, status, ws, L.stride_pair,
-                                                    ws + L.mom_off, ws + L.tv_off, f32, c32,
-                                                    kappa, p, closed, tv_lanes(f, c));
+        auto mtv = [&](auto kern) {
+            kern<<<gtv, MT, 0, st>>>(mu, nu, out, status, ws, L.stride_pair, ws + L.mom_off,
+                                     ws + L.tv_off, f32, c32, kappa, p, closed, tv_lanes(f, c),
+                                     tv_w);
+        };
+        if (ndim == 2 && kappa == 4) mtv(moments_tv_kernel<true, 2, 4>);
+        else if (ndim == 2 && kappa == 8) mtv(moments_tv_kernel<true, 2, 8>);
+        else if (ndim == 3 && kappa == 4) mtv(moments_tv_kernel<true, 3, 4>);
+        else if (ndim == 2 && kappa == 2) mtv(moments_tv_kernel<true, 2, 2>);
+        else if (ndim == 3 && kappa == 2) mtv(moments_tv_kernel<true, 3, 2>);
+        else mtv(moments_tv_kernel<true, 0, 0>);
         price_kernel<true><<<gpr, MT, 0, st>>>(arc_off, row_ptr, row_arc_col, row_arc_mass,
                                                kernel_w, out, status, ws, L.stride_pair,
                                                ws + L.mom_off, ws + L.pr_off, f32, c32, kappa, p,
                                                cost_table, closed, mode == GDT_MODE_FAST,
                                                closed ? nullptr : arc_row);
     } else {
-        moments_tv_kernel<false><<<gtv, MT, 0, st>>>(mu, nu, out, status, ws, L.stride_pair,
-                                                     ws + L.mom_off, ws + L.tv_off, f32, c32,
-                                                     kappa, p, 0, tv_lanes(f, c));
+        moments_tv_kernel<false, 0, 0><<<gtv, MT, 0, st>>>(mu, nu, out, status, ws,
+                                                           L.stride_pair, ws + L.mom_off,
+                                                           ws + L.tv_off, f32, c32, kappa, p, 0,
+                                                           tv_lanes(f, c), tv_w);
         price_kernel<false><<<gpr, MT, 0, st>>>(arc_off, row_ptr, row_arc_col, row_arc_mass,
                                                 kernel_w, out, status, ws, L.stride_pair,
                                                 ws + L.mom_off, ws + L.pr_off, f32, c32, kappa, p,

@@ -571,9 +571,10 @@ def launch_primal(bt: _Batch, dp: DevicePlans, max_iter):
     # fp32 mode with C-bar at hand (the weighted-cost bound computed it): the
     # coarse-level primal stage, priced by C-bar (primal.cu primal_coarse_kernel)
     cbar = bt.cbar_dev if (bt.mode == 1 and dp.uniform) else None
-    tv_w = bmap = None
-    if cbar is not None:
-        tv_w, bmap = _grid_tables(bt.pdims, bt.kappa, bt.p)
+    # the padded grid's tv_weights (the reference's formula, host-computed) and
+    # cell -> block map: the coarse-level stage needs both, the fine-level
+    # kernels read the weights instead of recomputing them per cell
+    tv_w, bmap = _grid_tables(bt.pdims, bt.kappa, bt.p)
     N.check(N.lib().gdt_primal_upscale(
         N.ptr(bt.mu_pad), N.ptr(bt.nu_pad), N.ptr(bt.mu_c), N.ptr(bt.nu_c), N.ptr(bt.stats),
         N.ptr(cbar), N.ptr(tv_w), N.ptr(bmap), N.ptr(dp.arc_off), N.ptr(dp.row_ptr),

@@ -87,3 +87,33 @@ def test_many_combos_equal_single_calls():
         for b in range(6):
             for m in G.QUANT_METHODS:
                 assert many[(k, p)][b][m].raw_value == one[b][m].raw_value, (k, p, b, m)
+
+
+@pytest.mark.parametrize("cfg,pairs", [(2, 4), (3, 3), (4, 2), (5, 4)])
+def test_exact_ipf_cluster_size_invariance(cfg, pairs, monkeypatch):
+    """The exact-order fp64 IPF spreads a pair over a thread-block cluster
+    (ipf_cluster_kernel); every unit is still summed by one thread in the
+    reference's order, so the primal bound, its components and the iteration
+    count do not depend on the cluster size (1 = the single-CTA ipf_kernel)."""
+    wl = S.WORKLOADS[cfg]
+    mus, nus = S.batch(cfg, 0, pairs)
+    k, p = wl.combos[0]
+    max_iter = min(wl.max_iter, 40)
+    ref = None
+    for csz in (1, 2, 3, 4, 8):
+        monkeypatch.setenv("GRIDOT_IPF_CLUSTER", str(csz))
+        out = G.quantized_bounds(mus, nus, wl.dims, k, p, xi=0.0, max_iter=max_iter,
+                                 precision="fp64", methods=("primal_upscaling",),
+                                 return_exceptions=False)
+        rec = [(r["primal_upscaling"].raw_value, r["primal_upscaling"].iterations,
+                tuple(sorted((a, b) for a, b in r["primal_upscaling"].components.items()
+                             if a != "marginal_gap")))
+               for r in out]
+        gaps = [r["primal_upscaling"].components.get("marginal_gap") for r in out]
+        if ref is None:
+            ref, ref_gaps = rec, gaps
+        else:
+            assert rec == ref, (cfg, csz)
+            for g0, g1 in zip(ref_gaps, gaps):  # the gap folds per-CTA partials: rounding only
+                if g0 is not None:
+                    assert rel_close(g0, g1, 1e-12)
