@@ -254,6 +254,12 @@ int gdt_probe_peak(int kind, int64_t blocks, int64_t iters, float *sink, void *s
 int64_t gdt_probe_flops(int kind, int64_t blocks, int64_t iters);
 /* = gdt_probe_peak(GDT_PROBE_FFMA, ...) */
 int gdt_probe_fp32(int64_t blocks, int64_t iters, float *sink, void *stream);
+/* Dependent-add latency of the FP64 pipe: one warp adds `adds` doubles from
+ * shared memory into one accumulator, ((0 + p0) + p1) + ... -- the chain of
+ * an exact-order IPF unit sum (sinkhorn.py:120-136) -- and reports the SM
+ * cycles it took in cycles[0] (device buffer, 8 bytes).  The latency floor of
+ * a sweep of the exact IPF is this figure x the longest unit. */
+int gdt_probe_dadd_chain(int64_t adds, long long *cycles, void *stream);
 
 /* ---- host coarse LP (stays on the host, _simplex.py) ------------------ */
 

@@ -45,6 +45,7 @@ _SIGNATURES = {
     "gdt_ctransform_points": (I32, [P, P, I64, I64, I32, D, P, I32, P, P]),
     "gdt_batched_dot": (I32, [P, P, I64, I64, P, P]),
     "gdt_probe_fp32": (I32, [I64, I64, P, P]),
+    "gdt_probe_dadd_chain": (I32, [I64, P, P]),
     "gdt_probe_peak": (I32, [I32, I64, I64, P, P]),
     "gdt_probe_flops": (I64, [I32, I64, I64]),
     "gdt_entropic_scratch_bytes": (I64, [I64, I64]),

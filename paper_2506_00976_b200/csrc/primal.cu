@@ -38,6 +38,7 @@
 namespace gdt {
 
 constexpr int PT = 512;  // threads of the per-pair IPF CTA (128 registers each)
+constexpr int CL_SKEW = 2;  // doubles of shared-memory skew per unit (ipf_cluster_kernel products)
 
 struct G32 {  // int32 grid description (cells < 2^31)
     int nd;
@@ -731,11 +732,25 @@ __global__ void run_list_kernel(const int64_t *__restrict__ arc_off,
 // fine offsets one after the other), so a thread finds its arc's groups once
 // (a scan over the unit's arcs) and then writes its K1 runs.  Output
 // identical to run_list_kernel.
+struct RunListArgs {  // one direction: CSR (rows) or CSC (columns) of the coarse plans
+    const int32_t *ptr;
+    const int64_t *pc;
+    const double *mass;
+    int32_t *cells;
+    double *coefs;
+    int32_t *dst;
+};
+
 __global__ void __launch_bounds__(128) run_list_par_kernel(
-    const int64_t *__restrict__ arc_off, const int32_t *__restrict__ ptr,
-    const int64_t *__restrict__ pc, const double *__restrict__ mass,
-    const double *__restrict__ W, int64_t batch, G32 f, G32 c, int kappa,
-    int32_t *__restrict__ cells, double *__restrict__ coefs) {
+    const int64_t *__restrict__ arc_off, RunListArgs rows, RunListArgs cols,
+    const double *__restrict__ W, int64_t batch, G32 f, G32 c, int kappa) {
+    const RunListArgs &A = blockIdx.y == 0 ? rows : cols;
+    const int32_t *__restrict__ ptr = A.ptr;
+    const int64_t *__restrict__ pc = A.pc;
+    const double *__restrict__ mass = A.mass;
+    int32_t *__restrict__ cells = A.cells;
+    double *__restrict__ coefs = A.coefs;
+    int32_t *__restrict__ dst = A.dst;
     const int n = c.cells, nd = f.nd;
     const int K1 = (int)ipow(kappa, nd - 1);
     const double Wu = W[0];
@@ -763,6 +778,12 @@ __global__ void __launch_bounds__(128) run_list_par_kernel(
         const int64_t *up = pc + a0 + lo0;
         int32_t *oc = cells + (a0 + lo0) * K1;
         double *of = coefs + (a0 + lo0) * K1;
+        int32_t *od = dst + (a0 + lo0) * K1;
+        // product slot of run `pos` of this unit in the cluster kernel's shared
+        // buffer: chain order, each unit shifted by 2 doubles more than the one
+        // before (CL_SKEW) so that the lanes of a warp, one chain each, read
+        // different banks (unit sizes are multiples of 128 bytes)
+        const int dbase = lo0 * K1 * kappa + CL_SKEW * ulo;
         const double cf = __dmul_rn(mass[a0 + qa], Wu);
         const int64_t w = up[q];
         // per level (d-1 .. 1): runs before the arc's group, the group's size,
@@ -798,6 +819,7 @@ __global__ void __launch_bounds__(128) run_list_par_kernel(
             }
             oc[pos] = cell;
             of[pos] = cf;
+            od[pos] = dbase + pos * kappa;
         }
     }
 }
@@ -1912,167 +1934,260 @@ __device__ __forceinline__ double2 ld_gl2(const double *p) {
     return v;
 }
 
+#ifdef GDT_IPF_TRACE
+// debug builds: clocks inside the first unit-sum batch of the traced sweep (CTA 0)
+__device__ int g_cl_on;
+#define CL_TRACE(slot_)                                                                   \
+    do {                                                                                  \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && g_cl_on == 1 && u0 == ua)              \
+            g_ex_trace[8 + (slot_)] = clock64();                                          \
+    } while (0)
+#else
+#define CL_TRACE(slot_) \
+    do {                \
+    } while (0)
+#endif
+
 // products of `nruns` runs (KAP cells each) in chain order into shared memory;
 // RU runs per thread in flight (descriptors, then gathers, then products)
+// The gathers go through cp.async (16-byte copies global -> shared, L2 path:
+// coherent with the other CTAs' stores, and no register or scoreboard holds a
+// copy in flight), so a thread keeps all its runs' gathers outstanding at
+// once; the per-SM count of loads in flight, not the chains, bounded the
+// register-staged version.  Each thread then scales the runs it fetched by
+// their coefficients in place (same products, same slots).
+__device__ __forceinline__ void cp_async16(double *smem_dst, const double *gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
 template <int KAP>
 __device__ __forceinline__ void cl_products(const int32_t *__restrict__ cells,
-                                            const double *__restrict__ coefs, int nruns,
+                                            const double *__restrict__ coefs,
+                                            const int32_t *__restrict__ dst, int dbase, int nruns,
                                             const double *x, double *prod) {
-    constexpr int RU = KAP <= 4 ? 4 : 2;
-    for (int r0 = threadIdx.x; r0 < nruns; r0 += PT * RU) {
-        int cl[RU];
-        double cf[RU], xv[RU][KAP];
+    // an item is one 16-byte chunk (2 cells) of a run; consecutive threads take
+    // consecutive chunks, so the KAP / 2 copies of a run sit in adjacent lanes
+    // and share their cache line
+    constexpr int CH = KAP / 2, IU = 8;
+    const int nitems = nruns * CH;
+    for (int t0 = threadIdx.x; t0 < nitems; t0 += PT * IU) {
+        int cl[IU], ds[IU];
 #pragma unroll
-        for (int q = 0; q < RU; ++q) {
-            const int r = r0 + q * PT;
-            cl[q] = r < nruns ? __ldg(cells + r) : 0;
-            cf[q] = r < nruns ? __ldg(coefs + r) : 0.0;
+        for (int q = 0; q < IU; ++q) {
+            const int t = t0 + q * PT, r = t / CH;
+            cl[q] = t < nitems ? __ldg(cells + r) + 2 * (t - r * CH) : 0;
+            ds[q] = t < nitems ? __ldg(dst + r) - dbase + 2 * (t - r * CH) : 0;
         }
 #pragma unroll
-        for (int q = 0; q < RU; ++q) {
-            if (r0 + q * PT < nruns) {
+        for (int q = 0; q < IU; ++q)
+            if (t0 + q * PT < nitems) cp_async16(prod + ds[q], x + cl[q]);
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    // (16 items per thread in one pass -- descriptors, coefficients and copies
+    // all in flight together -- was measured slower: 37k vs 16k cycles per batch)
+    for (int t0 = threadIdx.x; t0 < nitems; t0 += PT * IU) {
+        int ds[IU];
+        double cf[IU];
 #pragma unroll
-                for (int i = 0; i < KAP; i += 2) {
-                    const double2 t = ld_gl2(x + cl[q] + i);
-                    xv[q][i] = t.x;
-                    xv[q][i + 1] = t.y;
-                }
-            }
+        for (int q = 0; q < IU; ++q) {
+            const int t = t0 + q * PT, r = t / CH;
+            cf[q] = t < nitems ? __ldg(coefs + r) : 0.0;
+            ds[q] = t < nitems ? __ldg(dst + r) - dbase + 2 * (t - r * CH) : 0;
         }
 #pragma unroll
-        for (int q = 0; q < RU; ++q) {
-            const int r = r0 + q * PT;
-            if (r >= nruns) break;
-            double *pp = prod + (int64_t)r * KAP;
-#pragma unroll
-            for (int i = 0; i < KAP; i += 2)
-                *reinterpret_cast<double2 *>(pp + i) =
-                    make_double2(__dmul_rn(cf[q], xv[q][i]), __dmul_rn(cf[q], xv[q][i + 1]));
+        for (int q = 0; q < IU; ++q) {
+            if (t0 + q * PT >= nitems) break;
+            double2 *pp = reinterpret_cast<double2 *>(prod + ds[q]);
+            const double2 v = *pp;
+            *pp = make_double2(__dmul_rn(cf[q], v.x), __dmul_rn(cf[q], v.y));
         }
     }
 }
 
 // sums (and reciprocals) of units [ua, ub) of one direction: batches of whole
 // units whose products fit `cap` doubles; a unit larger than `cap` is summed
-// straight from its run list by one thread
+// straight from its run list by one thread.  Results go to shared memory
+// (s_sum / s_rcp, indexed u - ua) for the CTA's own cell pass and to global
+// memory (the TV / pricing kernels read the final sums).
 __device__ __noinline__ void cl_unit_sums(const int32_t *__restrict__ cells,
                                           const double *__restrict__ coefs,
+                                          const int32_t *__restrict__ dst,
                                           const int32_t *__restrict__ ptr, int ua, int ub, int K1,
                                           int kappa, const double *x, double *prod,
-                                          double *out_sum, double *out_rcp, int cap) {
+                                          double *out_sum, double *s_sum, double *s_rcp, int cap) {
     const int per = K1 * kappa;
     int u0 = ua;
     while (u0 < ub) {
         const int a0 = ptr[u0];
+        // a batch [u0, u1) needs its products plus CL_SKEW doubles per unit
         int lo = u0 + 1, hi = ub;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if ((int64_t)(ptr[mid] - a0) * per <= cap) lo = mid;
+            if ((int64_t)(ptr[mid] - a0) * per + CL_SKEW * (mid - u0) <= cap) lo = mid;
             else hi = mid - 1;
         }
         const int u1 = lo;
-        if ((int64_t)(ptr[u1] - a0) * per <= cap) {
+        if ((int64_t)(ptr[u1] - a0) * per + CL_SKEW * (u1 - u0) <= cap) {
             const int nruns = (ptr[u1] - a0) * K1;
             const int32_t *bc = cells + (int64_t)a0 * K1;
             const double *bf = coefs + (int64_t)a0 * K1;
+            const int32_t *bd = dst + (int64_t)a0 * K1;
+            const int dbase = a0 * per + CL_SKEW * u0;
+            CL_TRACE(0);
             switch (kappa) {
-                case 2: cl_products<2>(bc, bf, nruns, x, prod); break;
-                case 4: cl_products<4>(bc, bf, nruns, x, prod); break;
-                default: cl_products<8>(bc, bf, nruns, x, prod); break;
+                case 2: cl_products<2>(bc, bf, bd, dbase, nruns, x, prod); break;
+                case 4: cl_products<4>(bc, bf, bd, dbase, nruns, x, prod); break;
+                default: cl_products<8>(bc, bf, bd, dbase, nruns, x, prod); break;
             }
+            CL_TRACE(1);
             __syncthreads();
+            CL_TRACE(2);
             for (int u = u0 + (int)threadIdx.x; u < u1; u += PT) {
-                const int64_t plo = (int64_t)(ptr[u] - a0) * per, phi = (int64_t)(ptr[u + 1] - a0) * per;
-                const double v = chain_sum(prod + plo, (int)(phi - plo), true);
+                const int plo = (ptr[u] - a0) * per + CL_SKEW * (u - u0);
+                const double v = chain_sum(prod + plo, (ptr[u + 1] - ptr[u]) * per, true);
                 out_sum[u] = v;
-                out_rcp[u] = v > 0.0 ? __drcp_rn(v) : 0.0;
+                s_sum[u - ua] = v;
+                s_rcp[u - ua] = v > 0.0 ? __drcp_rn(v) : 0.0;
+            }
+            CL_TRACE(3);
+            __syncthreads();
+            CL_TRACE(4);
+        } else {
+            if (threadIdx.x == 0) {
+                const int rlo = ptr[u0] * K1, rhi = ptr[u0 + 1] * K1;
+                const double v = run_list_sum_any(cells + rlo, coefs + rlo, rhi - rlo, x, kappa, 0);
+                out_sum[u0] = v;
+                s_sum[u0 - ua] = v;
+                s_rcp[u0 - ua] = v > 0.0 ? __drcp_rn(v) : 0.0;
             }
             __syncthreads();
-        } else if (threadIdx.x == 0) {
-            const int rlo = ptr[u0] * K1, rhi = ptr[u0 + 1] * K1;
-            const double v = run_list_sum_any(cells + rlo, coefs + rlo, rhi - rlo, x, kappa, 0);
-            out_sum[u0] = v;
-            out_rcp[u0] = v > 0.0 ? __drcp_rn(v) : 0.0;
         }
         u0 = u1;
     }
 }
 
-constexpr int CL_U = 4;  // cells per thread in flight in the cluster kernel's cell passes
+// Cell passes of ipf_kernel over the blocks [ua, ub) this CTA just summed: an
+// item is one fine row (KAP cells along axis 0) of one block, its sum and
+// reciprocal come from shared memory, so every load of an item is independent
+// (no block-map gather) and no cluster barrier separates sums from cells.
+struct ClGeom {
+    int nd, lk;                 // dimensions, log2(kappa)
+    int fs[GDT_MAX_DIM];        // fine strides
+    int cn[GDT_MAX_DIM];        // coarse extents
+};
 
-// the cell passes of ipf_kernel on the cell slice [c0, c1) of this CTA
-__device__ __forceinline__ void cl_cells_row(const double *__restrict__ mu, int c0, int c1,
-                                             const int32_t *__restrict__ bmap, bool init,
-                                             const double *a_cur, double *a_next, Red &r,
-                                             const double *kbs, const double *rcps) {
-    for (int i0 = c0 + (int)threadIdx.x; i0 < c1; i0 += PT * CL_U) {
-        int kk[CL_U];
-        double mu_[CL_U], ai_[CL_U], acc_[CL_U], rc_[CL_U];
+__device__ __forceinline__ int cl_block_origin(int k, const ClGeom &g) {
+    int off = 0;
 #pragma unroll
-        for (int q = 0; q < CL_U; ++q) {
-            const int i = i0 + q * PT;
-            const bool in = i < c1;
-            kk[q] = in ? __ldg(bmap + i) : 0;
-            mu_[q] = in ? __ldg(mu + i) : 0.0;
-            ai_[q] = (in && !init) ? a_cur[i] : 0.0;
-        }
-#pragma unroll
-        for (int q = 0; q < CL_U; ++q) {
-            acc_[q] = ld_gl(kbs + kk[q]);
-            rc_[q] = ld_gl(rcps + kk[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < CL_U; ++q) {
-            const int i = i0 + q * PT;
-            if (i >= c1) break;
-            const double acc = acc_[q], mui = mu_[q];
-            if (!init) {
-                const double ai = ai_[q];
-                range_acc(ai, r.amin, r.amax, r.nonfinite);
-                if (mui > 0.0) r.gap += fabs(__dsub_rn(__dmul_rn(ai, acc), mui));
-            }
-            double an = 0.0;
-            if (mui > 0.0) {
-                if (acc <= 0.0) r.zrow = 1;
-                else an = div_shared(mui, acc, rc_[q]);
-            }
-            a_next[i] = an;
-        }
+    for (int a = 0; a < GDT_MAX_DIM; ++a) {
+        if (a >= g.nd) break;
+        const int ka = k % g.cn[a];
+        k /= g.cn[a];
+        off += (ka << g.lk) * g.fs[a];
     }
+    return off;
 }
 
-__device__ __forceinline__ void cl_cells_col(const double *__restrict__ nu, int c0, int c1,
-                                             const int32_t *__restrict__ bmap, double *bvec, Red &r,
-                                             const double *ktas, const double *rcps) {
-    for (int j0 = c0 + (int)threadIdx.x; j0 < c1; j0 += PT * CL_U) {
-        int ll[CL_U];
-        double nu_[CL_U], acc_[CL_U], rc_[CL_U];
+// fine offset of row r (digits s_1 .. s_{d-1} in base kappa) inside a block
+__device__ __forceinline__ int cl_row_offset(int r, const ClGeom &g) {
+    int off = 0;
 #pragma unroll
-        for (int q = 0; q < CL_U; ++q) {
-            const int j = j0 + q * PT;
-            const bool in = j < c1;
-            ll[q] = in ? __ldg(bmap + j) : 0;
-            nu_[q] = in ? __ldg(nu + j) : 0.0;
-        }
+    for (int a = 1; a < GDT_MAX_DIM; ++a) {
+        if (a >= g.nd) break;
+        off += (r & ((1 << g.lk) - 1)) * g.fs[a];
+        r >>= g.lk;
+    }
+    return off;
+}
+
+
+template <int KAP, bool ROW>
+__device__ __forceinline__ void cl_cells(const double *__restrict__ mass, int ua, int ub, int K1,
+                                         int lk1, const ClGeom &g, const int *org, bool init,
+                                         const double *cur, double *nxt, Red &r_io,
+                                         const double *s_sum, const double *s_rcp) {
+    // (a local copy: the stores to `nxt` could alias a record reached by reference,
+    // which would force its fields through memory on every cell)
+    constexpr int CL_IU = KAP <= 4 ? 2 : 1;  // items per thread in flight
+    Red r = r_io;
+    const int nitems = (ub - ua) * K1;
+    for (int it0 = threadIdx.x; it0 < nitems; it0 += PT * CL_IU) {
+        double ms[CL_IU][KAP], cv[CL_IU][KAP], sm[CL_IU], rc[CL_IU];
+        int st[CL_IU];
 #pragma unroll
-        for (int q = 0; q < CL_U; ++q) {
-            acc_[q] = ld_gl(ktas + ll[q]);
-            rc_[q] = ld_gl(rcps + ll[q]);
-        }
+        for (int q = 0; q < CL_IU; ++q) {
+            const int item = it0 + q * PT;
+            const bool in = item < nitems;
+            const int lu = in ? item >> lk1 : 0, row = item & (K1 - 1);
+            st[q] = org[lu] + cl_row_offset(row, g);
+            sm[q] = s_sum[lu];
+            rc[q] = s_rcp[lu];
 #pragma unroll
-        for (int q = 0; q < CL_U; ++q) {
-            const int j = j0 + q * PT;
-            if (j >= c1) break;
-            const double acc = acc_[q], nuj = nu_[q];
-            double bj = 0.0;
-            if (nuj > 0.0) {
-                if (acc <= 0.0) r.zcol = 1;
-                else bj = div_shared(nuj, acc, rc_[q]);
-                range_acc(bj, r.bmin, r.bmax, r.nonfinite);
-                r.gap += fabs(__dsub_rn(nuj, __dmul_rn(bj, acc)));
+            for (int i = 0; i < KAP; i += 2) {
+                const double2 t = in ? __ldg(reinterpret_cast<const double2 *>(mass + st[q] + i))
+                                     : make_double2(0.0, 0.0);
+                ms[q][i] = t.x;
+                ms[q][i + 1] = t.y;
+                if (ROW) {
+                    const double2 c2 = (in && !init)
+                                           ? *reinterpret_cast<const double2 *>(cur + st[q] + i)
+                                           : make_double2(0.0, 0.0);
+                    cv[q][i] = c2.x;
+                    cv[q][i + 1] = c2.y;
+                }
             }
-            bvec[j] = bj;
         }
+#pragma unroll
+        for (int q = 0; q < CL_IU; ++q) {
+            if (it0 + q * PT >= nitems) break;
+            const double acc = sm[q];
+            double res[KAP];
+#pragma unroll
+            for (int i = 0; i < KAP; ++i) {
+                const double mi = ms[q][i];
+                if (ROW) {
+                    if (!init) {
+                        const double ai = cv[q][i];
+                        range_acc(ai, r.amin, r.amax, r.nonfinite);
+                        if (mi > 0.0) r.gap += fabs(__dsub_rn(__dmul_rn(ai, acc), mi));
+                    }
+                    double an = 0.0;
+                    if (mi > 0.0) {
+                        if (acc <= 0.0) r.zrow = 1;
+                        else an = div_shared(mi, acc, rc[q]);
+                    }
+                    res[i] = an;
+                } else {
+                    double bj = 0.0;
+                    if (mi > 0.0) {
+                        if (acc <= 0.0) r.zcol = 1;
+                        else bj = div_shared(mi, acc, rc[q]);
+                        range_acc(bj, r.bmin, r.bmax, r.nonfinite);
+                        r.gap += fabs(__dsub_rn(mi, __dmul_rn(bj, acc)));
+                    }
+                    res[i] = bj;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < KAP; i += 2)
+                *reinterpret_cast<double2 *>(nxt + st[q] + i) = make_double2(res[i], res[i + 1]);
+        }
+    }
+    r_io = r;
+}
+
+template <bool ROW>
+__device__ __forceinline__ void cl_cells_any(int kappa, const double *mass, int ua, int ub, int K1,
+                                          int lk1, const ClGeom &g, int *org, bool init,
+                                          const double *cur, double *nxt, Red &r,
+                                          const double *s_sum, const double *s_rcp) {
+    for (int u = ua + (int)threadIdx.x; u < ub; u += PT) org[u - ua] = cl_block_origin(u, g);
+    __syncthreads();
+    switch (kappa) {
+        case 2: cl_cells<2, ROW>(mass, ua, ub, K1, lk1, g, org, init, cur, nxt, r, s_sum, s_rcp); break;
+        case 4: cl_cells<4, ROW>(mass, ua, ub, K1, lk1, g, org, init, cur, nxt, r, s_sum, s_rcp); break;
+        default: cl_cells<8, ROW>(mass, ua, ub, K1, lk1, g, org, init, cur, nxt, r, s_sum, s_rcp); break;
     }
 }
 
@@ -2116,24 +2231,36 @@ __global__ void __launch_bounds__(PT) ipf_cluster_kernel(
     const double *__restrict__ mu, const double *__restrict__ nu,
     const int64_t *__restrict__ arc_off, const int32_t *__restrict__ row_ptr,
     const int32_t *__restrict__ col_ptr, const double *__restrict__ xi_in, int64_t max_iter,
-    int N, int U, int kappa, int K1, double *__restrict__ out, int32_t *__restrict__ status,
-    double *scratch, int64_t stride_pair, const int32_t *__restrict__ bmap,
-    const int32_t *__restrict__ rl_cells, const double *__restrict__ rl_coef,
-    const int32_t *__restrict__ cl_cells, const double *__restrict__ cl_coef, int cap) {
-    extern __shared__ double prod[];  // [cap] products of one batch
+    G32 f, G32 c, int kappa, int K1, double *__restrict__ out, int32_t *__restrict__ status,
+    double *scratch, int64_t stride_pair, const int32_t *__restrict__ rl_cells,
+    const double *__restrict__ rl_coef, const int32_t *__restrict__ cl_cells_,
+    const double *__restrict__ cl_coef, const int32_t *__restrict__ rl_dst,
+    const int32_t *__restrict__ cl_dst, int cap) {
+    extern __shared__ double prod[];  // [cap] products | CSR/CSC pointers | sums, reciprocals, origins
     __shared__ double sh[(PT / 32 + 1) * 6 > CL_MAX * 8 ? (PT / 32 + 1) * 6 : CL_MAX * 8];
     __shared__ int part[4];
     const unsigned cs = cluster_size(), rank = cluster_rank_id();
     const int64_t b = blockIdx.x / cs;
+    const int N = f.cells, U = c.cells;
     const double *mub = mu + b * N, *nub = nu + b * N;
     const int64_t a0 = arc_off[b];
-    const int32_t *rptr = row_ptr + b * (U + 1), *cptr = col_ptr + b * (U + 1);  // (moved to shared memory below)
-    const int32_t *rrc = rl_cells + a0 * K1, *crc = cl_cells + a0 * K1;
+    const int32_t *rptr = row_ptr + b * (U + 1), *cptr = col_ptr + b * (U + 1);
+    const int32_t *rrc = rl_cells + a0 * K1, *crc = cl_cells_ + a0 * K1;
     const double *rrf = rl_coef + a0 * K1, *crf = cl_coef + a0 * K1;
+    const int32_t *rrd = rl_dst + a0 * K1, *crd = cl_dst + a0 * K1;
     double *ws = scratch + b * stride_pair;
     double *aA = ws, *aB = ws + N, *bv = ws + 2 * (int64_t)N;
-    double *kb = ws + 3 * (int64_t)N, *kta = kb + U, *rcp = kta + U, *xch = rcp + U;
+    double *kb = ws + 3 * (int64_t)N, *kta = kb + U, *xch = kta + 2 * (int64_t)U;
     // xch: [0, 64) reduction records, [64, 72) zero-column flags, [80, 88) support counts
+    ClGeom g;
+    g.nd = f.nd;
+    g.lk = kappa == 2 ? 1 : (kappa == 4 ? 2 : 3);
+#pragma unroll
+    for (int a = 0; a < GDT_MAX_DIM; ++a) {
+        g.fs[a] = f.stride[a];
+        g.cn[a] = c.n[a];
+    }
+    const int lk1 = g.lk * (f.nd - 1);  // K1 = 1 << lk1
 
     // unit ranges balanced by arc count: rank r takes the units whose first
     // arc lies in [A r / cs, A (r + 1) / cs)
@@ -2157,17 +2284,19 @@ __global__ void __launch_bounds__(PT) ipf_cluster_kernel(
     }
     const int cper = ((N + (int)cs - 1) / (int)cs + 7) & ~7;
     const int c0 = min(N, (int)rank * cper), c1 = min(N, c0 + cper);
-    // the pair's CSR / CSC pointers in shared memory (after the products):
-    // the batch searches of cl_unit_sums then stay on chip
-    {
-        int32_t *sp = reinterpret_cast<int32_t *>(prod + cap);
-        for (int i = threadIdx.x; i <= U; i += PT) {
-            sp[i] = rptr[i];
-            sp[U + 1 + i] = cptr[i];
-        }
-        rptr = sp;
-        cptr = sp + U + 1;
+    // the pair's CSR / CSC pointers in shared memory (after the products): the
+    // batch searches of cl_unit_sums stay on chip; then this CTA's unit sums,
+    // their reciprocals and block origins
+    int32_t *sp = reinterpret_cast<int32_t *>(prod + cap);
+    for (int i = threadIdx.x; i <= U; i += PT) {
+        sp[i] = rptr[i];
+        sp[U + 1 + i] = cptr[i];
     }
+    rptr = sp;
+    cptr = sp + U + 1;
+    double *s_sum = prod + cap + (U + 2);  // 2 (U + 1) ints = U + 1 doubles, rounded up
+    double *s_rcp = s_sum + U;
+    int *org = reinterpret_cast<int *>(s_rcp + U);
 
     // supports, b = ones over the target support, the default xi (quantized.py:317-320)
     double cnt = 0.0;
@@ -2197,9 +2326,8 @@ __global__ void __launch_bounds__(PT) ipf_cluster_kernel(
 
     Red r = red_init();
     double *a_cur = aA, *a_nxt = aB;
-    cl_unit_sums(rrc, rrf, rptr, ru0, ru1, K1, kappa, bv, prod, kb, rcp, cap);
-    cluster_sync_all();
-    cl_cells_row(mub, c0, c1, bmap, true, nullptr, a_cur, r, kb, rcp);
+    cl_unit_sums(rrc, rrf, rrd, rptr, ru0, ru1, K1, kappa, bv, prod, kb, s_sum, s_rcp, cap);
+    cl_cells_any<true>(kappa, mub, ru0, ru1, K1, lk1, g, org, true, nullptr, a_cur, r, s_sum, s_rcp);
     cl_reduce_red(r, sh, xch, rank, cs);
     int st = r.zrow ? GDT_PAIR_ZERO_DENOM_ROW : GDT_PAIR_OK;
     int64_t it = 0;
@@ -2208,16 +2336,21 @@ __global__ void __launch_bounds__(PT) ipf_cluster_kernel(
     while (st == GDT_PAIR_OK && it < max_iter) {
         ++it;
         EX_TRACE(0);
+#ifdef GDT_IPF_TRACE
+        if (blockIdx.x == 0 && threadIdx.x == 0) g_cl_on = it == 10 ? 1 : 0;
+#endif
         Red rc = red_init();
-        cl_unit_sums(crc, crf, cptr, cu0, cu1, K1, kappa, a_cur, prod, kta, rcp, cap);
+        cl_unit_sums(crc, crf, crd, cptr, cu0, cu1, K1, kappa, a_cur, prod, kta, s_sum, s_rcp, cap);
         EX_TRACE(1);
-        cluster_sync_all();  // B
+#ifdef GDT_IPF_TRACE
+        if (blockIdx.x == 0 && threadIdx.x == 0) g_cl_on = 0;
+#endif
+        cl_cells_any<false>(kappa, nub, cu0, cu1, K1, lk1, g, org, false, nullptr, bv, rc, s_sum, s_rcp);
         EX_TRACE(2);
-        cl_cells_col(nub, c0, c1, bmap, bv, rc, kta, rcp);
-        EX_TRACE(3);
         const int zc = __syncthreads_or(rc.zcol);
         if (threadIdx.x == 0) xch[64 + rank] = (double)zc;
         cluster_sync_all();  // C: b complete, flags visible
+        EX_TRACE(3);
         {
             int any = 0;
             for (unsigned q = 0; q < cs; ++q) any |= ld_gl(xch + 64 + q) != 0.0;
@@ -2226,15 +2359,12 @@ __global__ void __launch_bounds__(PT) ipf_cluster_kernel(
                 break;
             }
         }
+        cl_unit_sums(rrc, rrf, rrd, rptr, ru0, ru1, K1, kappa, bv, prod, kb, s_sum, s_rcp, cap);
         EX_TRACE(4);
-        cl_unit_sums(rrc, rrf, rptr, ru0, ru1, K1, kappa, bv, prod, kb, rcp, cap);
+        cl_cells_any<true>(kappa, mub, ru0, ru1, K1, lk1, g, org, false, a_cur, a_nxt, rc, s_sum, s_rcp);
         EX_TRACE(5);
-        cluster_sync_all();  // D
+        cl_reduce_red(rc, sh, xch, rank, cs);  // A: next a complete, records folded
         EX_TRACE(6);
-        cl_cells_row(mub, c0, c1, bmap, false, a_cur, a_nxt, rc, kb, rcp);
-        EX_TRACE(7);
-        cl_reduce_red(rc, sh, xch, rank, cs);  // A
-        EX_TRACE(8);
         const bool bad_a = rc.amin <= rc.amax &&
                            (rc.amin < 1e-100 || rc.amax > 1e100 || !isfinite(rc.amax));
         const bool bad_b = rc.bmin <= rc.bmax &&
@@ -2852,7 +2982,8 @@ inline PrimalLayout primal_layout(int64_t batch, const Grid &f, const Grid &c, b
     const int64_t kap = f.n[0] / c.n[0];
     L.runs = uniform ? batch * max_arcs * (f.cells / c.cells / kap) : 0;
     L.prod_off = 0;  // (two-phase products live in shared memory)
-    L.total = L.rl_off + 2 * L.runs + L.runs;
+    // (+ the product slots of the cluster kernel, int32 per run and direction)
+    L.total = L.rl_off + 2 * L.runs + L.runs + L.runs;
     return L;
 }
 
@@ -3000,10 +3131,11 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
     } else if (uni) {
         double *rl_coef = ws + L.rl_off, *cl_coef = rl_coef + L.runs;
         int32_t *rl_cells = reinterpret_cast<int32_t *>(cl_coef + L.runs), *cl_cells = rl_cells + L.runs;
-        run_list_par_kernel<<<grid_size(batch * 2 * c.cells, 128), 128, 0, st>>>(
-            arc_off, row_ptr, rpc, row_arc_mass, kernel_w, batch, f32, c32, kappa, rl_cells, rl_coef);
-        run_list_par_kernel<<<grid_size(batch * 2 * c.cells, 128), 128, 0, st>>>(
-            arc_off, col_ptr, cpc, col_arc_mass, kernel_w, batch, f32, c32, kappa, cl_cells, cl_coef);
+        int32_t *rl_dst = cl_cells + L.runs, *cl_dst = rl_dst + L.runs;
+        const RunListArgs rla{row_ptr, rpc, row_arc_mass, rl_cells, rl_coef, rl_dst};
+        const RunListArgs cla{col_ptr, cpc, col_arc_mass, cl_cells, cl_coef, cl_dst};
+        run_list_par_kernel<<<dim3(grid_size(batch * 2 * c.cells, 128), 2), 128, 0, st>>>(
+            arc_off, rla, cla, kernel_w, batch, f32, c32, kappa);
         // one cluster per pair when that puts more SMs to work (see
         // ipf_cluster_kernel); GRIDOT_IPF_CLUSTER=<n> forces the cluster size
         // (1 = the single-CTA kernel), for tests and measurements
@@ -3022,8 +3154,16 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
         while (csz > 1 && !launched) {
             // products of one CTA's units in one batch when they fit 160 KB
             const int64_t prods = 2 * c.cells * (f.cells / c.cells);
-            const int cap = (int)std::min<int64_t>(20480, ((prods / csz + 4095) / 2048) * 2048);
-            const size_t cdyn = sizeof(double) * (size_t)cap + sizeof(int32_t) * 2 * (c.cells + 1);
+            // (shared memory also holds 3.5 U + 2 doubles of pointers, sums and origins)
+            const int64_t room = (200 * 1024) / 8 - (3 * c.cells + 2 + (c.cells + 1) / 2);
+            const int cap = (int)(std::min<int64_t>(
+                                      room, std::min<int64_t>(20480, ((prods / csz + 4095) / 2048) * 2048 +
+                                                                         CL_SKEW * c.cells)) &
+                                  ~1ll);
+            if (cap < 2048) break;  // coarse grid too large for this layout: single-CTA kernel
+            // products | CSR + CSC pointers | unit sums, reciprocals (f64) | block origins (i32)
+            const size_t cdyn = sizeof(double) * (size_t)(cap + (c.cells + 2) + 2 * c.cells) +
+                                sizeof(int32_t) * (size_t)c.cells;
             cudaFuncSetAttribute(ipf_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)cdyn);
             cudaLaunchConfig_t cfg = {};
@@ -3040,10 +3180,10 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
             cfg.numAttrs = 1;
             const int K1 = (int)(f.cells / c.cells / kappa);
             const cudaError_t e = cudaLaunchKernelEx(
-                &cfg, ipf_cluster_kernel, mu, nu, arc_off, row_ptr, col_ptr, xi, max_iter,
-                (int)f.cells, (int)c.cells, kappa, K1, out, status, ws, L.stride_pair,
-                (const int32_t *)bmap, (const int32_t *)rl_cells, (const double *)rl_coef,
-                (const int32_t *)cl_cells, (const double *)cl_coef, cap);
+                &cfg, ipf_cluster_kernel, mu, nu, arc_off, row_ptr, col_ptr, xi, max_iter, f32,
+                c32, kappa, K1, out, status, ws, L.stride_pair, (const int32_t *)rl_cells,
+                (const double *)rl_coef, (const int32_t *)cl_cells, (const double *)cl_coef,
+                (const int32_t *)rl_dst, (const int32_t *)cl_dst, cap);
             if (e == cudaSuccess) launched = true;
             else {
                 cudaGetLastError();  // this cluster size is not schedulable here: try a smaller one

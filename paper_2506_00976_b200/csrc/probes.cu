@@ -77,8 +77,41 @@ __global__ void __launch_bounds__(256) dfma_probe(float *sink, int64_t iters, do
     if (s == 12345.678) sink[0] = (float)s;
 }
 
+// one warp, one dependent chain of DADDs over shared-memory operands (the
+// loop shape of chain_sum in primal.cu: 8 operands loaded ahead of 8 adds)
+__global__ void __launch_bounds__(32) dadd_chain_probe(long long *cycles, int64_t adds, double seed) {
+    __shared__ double ops[1024];
+    for (int i = threadIdx.x; i < 1024; i += 32) ops[i] = seed * (1.0 + i * 1e-9);
+    __syncwarp();
+    double acc = 0.0;
+    const long long t0 = clock64();
+    for (int64_t j = 0; j + 8 <= adds; j += 8) {
+        const double2 *q = reinterpret_cast<const double2 *>(ops + (j & 1016));
+        const double2 c0 = q[0], c1 = q[1], c2 = q[2], c3 = q[3];
+        acc = __dadd_rn(acc, c0.x);
+        acc = __dadd_rn(acc, c0.y);
+        acc = __dadd_rn(acc, c1.x);
+        acc = __dadd_rn(acc, c1.y);
+        acc = __dadd_rn(acc, c2.x);
+        acc = __dadd_rn(acc, c2.y);
+        acc = __dadd_rn(acc, c3.x);
+        acc = __dadd_rn(acc, c3.y);
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) {
+        cycles[0] = t1 - t0;
+        if (acc == 12345.678) cycles[0] = 0;  // keeps the chain alive
+    }
+}
+
 }  // namespace
 }  // namespace gdt
+
+extern "C" int gdt_probe_dadd_chain(int64_t adds, long long *cycles, void *stream) {
+    GDT_CHECK_ARG(adds >= 8 && cycles != nullptr, "gdt_probe_dadd_chain: bad arguments");
+    gdt::dadd_chain_probe<<<1, 32, 0, gdt::as_stream(stream)>>>(cycles, adds, 1.0);
+    return gdt::cuda_status("gdt_probe_dadd_chain");
+}
 
 extern "C" int gdt_probe_peak(int kind, int64_t blocks, int64_t iters, float *sink,
                               void *stream) {

@@ -16,6 +16,7 @@ for n in ("cfg5","cfg1","cfg3_fp64"):
         d=json.loads(l[-1]); print(n, round(d["value"],1), round(d["ms_per_step"],4), {k:v for k,v in d["config"]["stage_ms"].items() if "primal" in k})
     except Exception as e: print(n, "failed", e)
 PY
+python scripts/probe_dadd.py
 for A in "5 64 2" "5 64 1" "3 45 3" "3 45 2"; do
-  GRIDOT_B200_LIB=paper_2506_00976_b200/csrc/_trace/libgridot_b200.so timeout 300 python scripts/ipf_cl_trace.py $A 2>&1 | tail -1
+  GRIDOT_B200_LIB=paper_2506_00976_b200/csrc/_trace/libgridot_b200.so timeout 300 python scripts/ipf_cl_trace.py $A 2>&1 | tail -2
 done

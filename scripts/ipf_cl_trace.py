@@ -23,14 +23,17 @@ from paper_2506_00976_b200 import synthetic as S  # noqa: E402
 
 wl = S.WORKLOADS[cfg]
 mus, nus = S.batch(cfg, 0, pairs)
-names = ["col units", "barrier B", "col cells", "flags + barrier C", "row units", "barrier D",
-         "row cells", "reduce + barrier A"]
+names = ["col units", "col cells", "flags + barrier C", "row units", "row cells",
+         "reduce + barrier A"]
 for rep in range(2):
     G.quantized_bounds(mus, nus, wl.dims, wl.combos[0][0], wl.combos[0][1], precision="fp64",
                        xi=0.0, max_iter=20, methods=("primal_upscaling",))
     buf = (ctypes.c_longlong * 16)()
     N.lib().gdt_debug_ex_trace(buf)
-    t = np.array(buf[:9], dtype=np.int64)
+    t = np.array(buf[:7], dtype=np.int64)
     d = np.diff(t)
     print(f"cfg{cfg} x{pairs} cluster {os.environ.get('GRIDOT_IPF_CLUSTER', 'auto')}: sweep "
-          f"{t[8] - t[0]} cycles: " + ", ".join(f"{n} {int(x)}" for n, x in zip(names, d)))
+          f"{t[6] - t[0]} cycles: " + ", ".join(f"{n} {int(x)}" for n, x in zip(names, d)))
+    u = np.array(buf[8:13], dtype=np.int64)
+    print("   first col batch: " + ", ".join(f"{n} {int(x)}" for n, x in zip(
+        ["products", "barrier", "chains (thread 0)", "barrier"], np.diff(u))))
