@@ -280,6 +280,7 @@ constexpr int CT_TAB_W = 140;      // row stride (floats)
 constexpr int CT_TAB_ROWS = 128;   // |dy| <= 127
 constexpr int CT_TAB_WPR = 4;      // warps per region
 constexpr int CT_TAB_REG = 4;      // regions per CTA
+constexpr int CT_TAB_CH = 8;       // tiles a warp takes from the region's cursor at a time
 constexpr int CT_TAB_GT = 32 * CT_TAB_WPR;  // threads of a region group
 
 __device__ __forceinline__ void group_sync(int id) {
@@ -396,29 +397,46 @@ __global__ void __launch_bounds__(CT_TAB_GT * CT_TAB_REG, 2) pruned_ct_tab_kerne
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) vall = fmaxf(vall, __shfl_xor_sync(0xffffffffu, vall, o));
         float ub = INFINITY;
-        int cur_ring = 0;
-        for (;;) {
+        // Tiles are taken CT_TAB_CH at a time: lane l of the warp examines tile
+        // idx + l (its pruning bound and its ring's bound, all in one pass),
+        // then the warp walks the chunk in ring order with the bound it keeps
+        // tightening.  One cursor atomic and one round of table / tile-max loads
+        // per chunk instead of per tile.
+        bool done = false;
+        while (!done) {
             int idx = 0;
-            if (lane == 0) idx = atomicAdd(&cursor[slot], 1);
+            if (lane == 0) idx = atomicAdd(&cursor[slot], CT_TAB_CH);
             idx = __shfl_sync(0xffffffffu, idx, 0);
             if (idx >= ntiles) break;
-            const unsigned e = tiles_s[slot][idx];
-            const int r = (int)(e >> 16), t1 = (int)((e >> 8) & 0xffu), t0 = (int)(e & 0xffu);
-            const int t = t1 * nt0 + t0;
-            if (r != cur_ring) {  // entering ring r: the ring bound may end this warp
-                cur_ring = r;
-                const int gap = (r - 1) * 8 + 1;
-                const float cmin = gap + 7 < CT_TAB_W ? ct_tab[gap + 7] : sqrtf((float)gap * gap);
-                if (cmin - vall >= ub) break;
+            unsigned e_l = 0xffffffffu;
+            float lb_l = INFINITY, rb_l = -INFINITY;
+            if (lane < CT_TAB_CH && idx + lane < ntiles) {
+                e_l = tiles_s[slot][idx + lane];
+                const int r = (int)(e_l >> 16), t1 = (int)((e_l >> 8) & 0xffu), t0 = (int)(e_l & 0xffu);
+                if (r >= 1) {  // smallest cost any tile of ring r can have, minus max v
+                    const int gap = (r - 1) * 8 + 1;
+                    rb_l = (gap + 7 < CT_TAB_W ? ct_tab[gap + 7] : sqrtf((float)gap * gap)) - vall;
+                }
+                const int g0 = max(0, max(t0 * 8 - (X0 + 15), X0 - (t0 * 8 + 7)));
+                const int g1 = max(0, max(t1 * 8 - (Y0 + 15), Y0 - (t1 * 8 + 7)));
+                lb_l = ct_tab[g1 * CT_TAB_W + g0 + 7] - tm[t1 * nt0 + t0];
             }
-            const int g0 = max(0, max(t0 * 8 - (X0 + 15), X0 - (t0 * 8 + 7)));
-            const int g1 = max(0, max(t1 * 8 - (Y0 + 15), Y0 - (t1 * 8 + 7)));
-            const float lb = ct_tab[g1 * CT_TAB_W + g0 + 7] - tm[t];
+#pragma unroll 1
+            for (int k = 0; k < CT_TAB_CH; ++k) {
+                const unsigned e = __shfl_sync(0xffffffffu, e_l, k);
+                if (e == 0xffffffffu) break;  // past the last tile
+                const float rb = __shfl_sync(0xffffffffu, rb_l, k);
+                if (rb >= ub) {  // no tile of this ring or a later one can improve the region
+                    done = true;
+                    break;
+                }
+                const float lb = __shfl_sync(0xffffffffu, lb_l, k);
+                const int t1 = (int)((e >> 8) & 0xffu), t0 = (int)(e & 0xffu);
 #ifdef GDT_IPF_TRACE
-            if (lane == 0) atomicAdd(&g_ct_tiles[1], 1ull);
-            if (lane == 0 && !(lb >= ub)) atomicAdd(&g_ct_tiles[0], 1ull);
+                if (lane == 0) atomicAdd(&g_ct_tiles[1], 1ull);
+                if (lane == 0 && !(lb >= ub)) atomicAdd(&g_ct_tiles[0], 1ull);
 #endif
-            if (lb >= ub) continue;
+                if (lb >= ub) continue;
             const int sx0 = t0 * 8, off = sx0 - xj0;
             const int base = off >= 0 ? off : -off;
             const float *vrow = vb + (int64_t)(t1 * 8) * N0 + sx0;
@@ -458,6 +476,7 @@ __global__ void __launch_bounds__(CT_TAB_GT * CT_TAB_REG, 2) pruned_ct_tab_kerne
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
             ub = m;
+            }
         }
         group_sync(bar_id);  // every warp's minima are in sbest
         if (warp_in_cta % CT_TAB_WPR == 0) {

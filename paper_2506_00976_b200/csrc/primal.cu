@@ -2556,7 +2556,7 @@ __global__ void sum_parts_kernel(const double *__restrict__ part, int count, dou
 constexpr int CT = 512;       // threads of primal_coarse_kernel
 constexpr int CB_HEAVY = 8;  // arcs above which a block's sum goes to a warp
 enum { CB_MLO, CB_MHI, CB_NLO, CB_NHI, CB_CMU, CB_CNU, CB_S, CB_B, CB_K0, CB_K1, CB_KTA, CB_RK,
-       CB_NF };
+       CB_S1, CB_RK1, CB_NF };
 
 struct CoarsePlan {
     int rp, cp, rcol, rcoef, crow, ccoef, arow, heavy, perm, blk, total;
@@ -2671,6 +2671,24 @@ __device__ __forceinline__ void coarse_matvec(const int *ptr, const int *idx, co
     }
 }
 
+// Smallest / largest scaling of a block (extreme masses over one denominator)
+// folded into the running range.  The range is only ever compared with 1e-100
+// and 1e100 (_check_scale_range, sinkhorn.py:137-138), so the quotients come
+// from one multiplication by the correctly rounded reciprocal (relative error
+// < 2^-51) unless that lands within 1e-7 of a threshold or is not a positive
+// finite number -- then the correctly rounded divisions decide, as before.
+__device__ __forceinline__ void coarse_range(double mlo, double mhi, double den, double rk,
+                                             double &rlo, double &rhi, int &flags) {
+    double lo = __dmul_rn(mlo, rk), hi = __dmul_rn(mhi, rk);
+    if (!(lo > 1.0000001e-100 && hi < 0.9999999e100)) {
+        lo = div_shared(mlo, den, rk);
+        hi = div_shared(mhi, den, rk);
+    }
+    if (isnan(lo) || isnan(hi) || !isfinite(hi)) flags |= 4;
+    if (lo > 0.0) rlo = fmin(rlo, lo);
+    if (hi > 0.0) rhi = fmax(rhi, hi);
+}
+
 __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
     const double *__restrict__ mu_c, const double *__restrict__ nu_c,
     const double *__restrict__ stats, const double *__restrict__ cbar,
@@ -2702,8 +2720,10 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
     double *blk = reinterpret_cast<double *>(csm + L.blk);
     double *Bmlo = blk + CB_MLO * n, *Bmhi = blk + CB_MHI * n, *Bnlo = blk + CB_NLO * n,
            *Bnhi = blk + CB_NHI * n, *Bcmu = blk + CB_CMU * n, *Bcnu = blk + CB_CNU * n,
-           *BS = blk + CB_S * n, *BB = blk + CB_B * n, *KTA = blk + CB_KTA * n,
-           *RK = blk + CB_RK * n;
+           *BB = blk + CB_B * n, *KTA = blk + CB_KTA * n;
+    // S_k and 1 / kb of the current sweep and, written by the row pass, of the next
+    double *BS = blk + CB_S * n, *RK = blk + CB_RK * n;
+    double *BSn = blk + CB_S1 * n, *RKn = blk + CB_RK1 * n;
     double *Kcur = blk + CB_K0 * n, *Knext = blk + CB_K1 * n;
 
     // ---- the pair's coarse plan and block statistics into shared memory
@@ -2773,20 +2793,24 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
     int64_t it = 0;
     double gap = INFINITY;
     bool converged = false;
+    // a = mu / kb: block sums S_k (quotients correctly rounded: div_shared,
+    // Markstein from one reciprocal per denominator); later sweeps get theirs
+    // from the row pass of the sweep before
+    for (int k = threadIdx.x; k < n; k += CT) {
+        const double den = Kcur[k];
+        const double rk = fp_rcp(den);
+        RK[k] = rk;
+        BS[k] = (Bcmu[k] > 0.0 && den > 0.0) ? div_shared(mcb[k], den, rk) : 0.0;
+    }
+    __syncthreads();
     while (st == GDT_PAIR_OK && it < max_iter) {
         ++it;
-        // a = mu / kb: block sums S_k (quotients correctly rounded: div_shared,
-        // Markstein from one reciprocal per denominator)
-        for (int k = threadIdx.x; k < n; k += CT) {
-            const double den = Kcur[k];
-            const double rk = fp_rcp(den);
-            RK[k] = rk;
-            BS[k] = (Bcmu[k] > 0.0 && den > 0.0) ? div_shared(mcb[k], den, rk) : 0.0;
-        }
-        __syncthreads();
+        EX_TRACE(0);
+        EX_TRACE(1);
         // kta = K^T a
         coarse_matvec(cp, crow, ccoef, BS, KTA, pcol, nlc, hcol, nhc);
         __syncthreads();
+        EX_TRACE(2);
         // zero-column check, b = nu / kta: block sums B_l, column residual, range(b)
         CoarseRed r = cr_init();
         for (int l = threadIdx.x; l < n; l += CT) {
@@ -2799,33 +2823,35 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
                     const double rs = __drcp_rn(s);
                     bl = div_shared(ncb[l], s, rs);
                     r.gap += fabs(__dsub_rn(ncb[l], __dmul_rn(bl, s)));
-                    const double lo = div_shared(Bnlo[l], s, rs), hi = div_shared(Bnhi[l], s, rs);
-                    if (isnan(lo) || isnan(hi) || !isfinite(hi)) r.flags |= 4;
-                    if (lo > 0.0) r.blo = fmin(r.blo, lo);
-                    if (hi > 0.0) r.bhi = fmax(r.bhi, hi);
+                    coarse_range(Bnlo[l], Bnhi[l], s, rs, r.blo, r.bhi, r.flags);
                 }
             }
             BB[l] = bl;
         }
         __syncthreads();
+        EX_TRACE(3);
         // kb' = K b
         coarse_matvec(rp, rcol, rcoef, BB, Knext, prow, nlr, hrow, nhr);
         __syncthreads();
+        EX_TRACE(4);
         // range of a (from kb), the row residual, the next sweep's zero-row check
         for (int k = threadIdx.x; k < n; k += CT) {
+            const double s = Knext[k];
+            const double rn = fp_rcp(s);
+            double sn = 0.0;
             if (Bcmu[k] > 0.0) {
-                const double den = Kcur[k], rk = RK[k], s = Knext[k];
-                if (den > 0.0) {
-                    const double lo = div_shared(Bmlo[k], den, rk), hi = div_shared(Bmhi[k], den, rk);
-                    if (isnan(lo) || isnan(hi) || !isfinite(hi)) r.flags |= 4;
-                    if (lo > 0.0) r.alo = fmin(r.alo, lo);
-                    if (hi > 0.0) r.ahi = fmax(r.ahi, hi);
-                }
+                const double den = Kcur[k];
+                if (den > 0.0) coarse_range(Bmlo[k], Bmhi[k], den, RK[k], r.alo, r.ahi, r.flags);
                 r.gap += fabs(__dsub_rn(__dmul_rn(BS[k], s), mcb[k]));
                 if (s <= 0.0) r.flags |= 1;
+                else sn = div_shared(mcb[k], s, rn);
             }
+            RKn[k] = rn;  // the next sweep's a = mu / kb'
+            BSn[k] = sn;
         }
+        EX_TRACE(5);
         const CoarseRed q = cr_reduce(r, shr);
+        EX_TRACE(6);
         if (q.flags & 2) {
             st = GDT_PAIR_ZERO_DENOM_COL;
             break;
@@ -2847,6 +2873,12 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
         double *t = Kcur;  // kb' defines a of the next sweep
         Kcur = Knext;
         Knext = t;
+        t = BS;
+        BS = BSn;
+        BSn = t;
+        t = RK;
+        RK = RKn;
+        RKn = t;
     }
     // ---- pricing: the fitted coarse plan S_k (m W) B_l against C-bar (flat
     //      over the arcs: balanced; per-thread partials in a fixed order)
