@@ -49,6 +49,8 @@ __device__ __forceinline__ float fmin3f(float a, float b, float c) {
 
 constexpr int SEPT = 256;  // threads per CTA of sep_tile_kernel
 constexpr int SEP_SPLIT = 2;  // lanes sharing one (line, 8 outputs) tile (2: measured best)
+template <typename TO>
+__host__ __device__ constexpr int SEP_PAD() { return 16 / (int)sizeof(TO); }  // elements of line padding
 
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ in,
@@ -58,13 +60,17 @@ __global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ i
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tpl = L / 8;
     TO *sq = reinterpret_cast<TO *>(smem_raw);          // [2L + 16]: sq[k] = (k - L - 7)^2
-    TO *lines = sq + ((2 * L + 16 + 3) & ~3);            // [lpc][L]
+    // [lpc][LP]: lines padded by 16 bytes, so that the 16-byte reads of lanes on
+    // consecutive lines (same source offset) fall into different banks -- a line
+    // stride of L elements is a multiple of 128 bytes and made them all collide
+    const int LP = L + SEP_PAD<TO>();
+    TO *lines = sq + ((2 * L + 16 + 3) & ~3);
     const int64_t lines_per_pair = cells / L;
     const int64_t total_lines = batch * lines_per_pair;
     const int64_t line0 = (int64_t)blockIdx.x * lpc;
     // element offset of each of the CTA's lines (the 64-bit index arithmetic
     // once per line, not per element); -1 past the last line
-    int64_t *lbase = reinterpret_cast<int64_t *>(lines + lpc * L);
+    int64_t *lbase = reinterpret_cast<int64_t *>(lines + lpc * LP);
     for (int k = threadIdx.x; k < 2 * L + 16; k += blockDim.x) {
         const int d = k - L - 7;
         sq[k] = (TO)(d * d);
@@ -91,7 +97,7 @@ __global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ i
             v = (TO)in[off + (int64_t)i * S];
             if (negate) v = -v;
         }
-        lines[li * L + i] = v;
+        lines[li * LP + i] = v;
     }
     __syncthreads();
     // SEP_SPLIT consecutive lanes split the source range of a (line, 8
@@ -101,7 +107,7 @@ __global__ void __launch_bounds__(SEPT) sep_tile_kernel(const TI *__restrict__ i
     const int li = t % lpc, tl = t / lpc;
     const bool live = tl < tpl;
     const int64_t lid = line0 + li;
-    const TO *line = lines + li * L;
+    const TO *line = lines + li * LP;
     const int j0 = 8 * (live ? tl : 0);
     TO best[8];
 #pragma unroll
@@ -452,8 +458,8 @@ extern "C" int gdt_ctransform_grid(const void *v, void *out, int64_t batch, int 
                 while (lpc > 1 && (lines + lpc - 1) / lpc < 2 * nsm) lpc >>= 1;
                 const int thr = ((SEP_SPLIT * lpc * tpl + 31) / 32) * 32;
                 const unsigned ctas = (unsigned)((lines + lpc - 1) / lpc);
-                const size_t sh = el * (((2 * L + 16 + 3) & ~3) + (size_t)lpc * L) +
-                                  sizeof(int64_t) * lpc;  // + line offsets
+                const size_t sh = el * (((2 * L + 16 + 3) & ~3) + (size_t)lpc * (L + 16 / el)) +
+                                  sizeof(int64_t) * lpc;  // padded lines + line offsets
                 if (dtype == 0)
                     sep_tile_kernel<double, double><<<ctas, thr, sh, st>>>(
                         (const double *)src, (double *)o, batch, g.cells, (int)L, g.stride[ax], ax == 0, lpc);
