@@ -334,10 +334,16 @@ __global__ void __launch_bounds__(CE_THREADS) cbar_exact2d_kernel(
 
 // ---- fast p == 2: block moments ------------------------------------------
 // mom layout per (pair, block): [M1_0 .. M1_{d-1}, M2] about the block centre.
+// ND / KAP > 0: compile-time dimension and pooling factor -- the cell loop is
+// fully unrolled (all loads of a block in flight, offsets by shifts) with the
+// same left-to-right summation order as the runtime version (ND = KAP = 0).
+template <int ND, int KAP>
 __global__ void moments_kernel(const double *__restrict__ fine, double *__restrict__ mom,
-                               int64_t batch, Grid f, Grid c, int kappa) {
+                               int64_t batch, Grid f, Grid c, int kappa_rt) {
+    const int kappa = KAP ? KAP : kappa_rt;
+    const int nd = ND ? ND : f.nd;
     const int64_t total = batch * c.cells;
-    const int W = f.nd + 1;
+    const int W = nd + 1;
     const double ctr = (kappa - 1) / 2.0;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -345,27 +351,53 @@ __global__ void moments_kernel(const double *__restrict__ fine, double *__restri
         int64_t kc[GDT_MAX_DIM];
         unravel_block(k, c, kc);
         int64_t origin = b * f.cells;
-        for (int a = 0; a < f.nd; ++a) origin += kc[a] * kappa * f.stride[a];
+        for (int a = 0; a < nd; ++a) origin += kc[a] * kappa * f.stride[a];
         double m1[GDT_MAX_DIM] = {0, 0, 0, 0}, m2 = 0.0;
-        const int m = (int)ipow(kappa, f.nd);
-        for (int t = 0; t < m; ++t) {
-            int rem = t;
-            int64_t off = 0;
-            double r2 = 0.0, dl[GDT_MAX_DIM];
-            for (int a = 0; a < f.nd; ++a) {
-                const int o = rem % kappa;
-                rem /= kappa;
-                off += o * f.stride[a];
-                dl[a] = o - ctr;
-                r2 += dl[a] * dl[a];
+        if constexpr (ND > 0 && KAP > 0) {
+            constexpr int M = ND == 1 ? KAP : (ND == 2 ? KAP * KAP : KAP * KAP * KAP);
+            static_assert(ND <= 3, "compile-time blocks up to 3-D");
+            const double *base = fine + origin;
+            const int64_t s1 = f.stride[1], s2 = f.stride[2];
+            double wv[M];
+#pragma unroll
+            for (int t = 0; t < M; ++t) {
+                const int o0 = t % KAP, o1 = (t / KAP) % KAP, o2 = t / (KAP * KAP);
+                wv[t] = __ldg(base + o0 + (ND > 1 ? o1 * s1 : 0) + (ND > 2 ? o2 * s2 : 0));
             }
-            const double w = fine[origin + off];
-            for (int a = 0; a < f.nd; ++a) m1[a] += w * dl[a];
-            m2 += w * r2;
+#pragma unroll
+            for (int t = 0; t < M; ++t) {
+                const int o[3] = {t % KAP, (t / KAP) % KAP, t / (KAP * KAP)};
+                double r2 = 0.0, dl[3];
+#pragma unroll
+                for (int a = 0; a < ND; ++a) {
+                    dl[a] = o[a] - ctr;
+                    r2 += dl[a] * dl[a];
+                }
+#pragma unroll
+                for (int a = 0; a < ND; ++a) m1[a] += wv[t] * dl[a];
+                m2 += wv[t] * r2;
+            }
+        } else {
+            const int m = (int)ipow(kappa, nd);
+            for (int t = 0; t < m; ++t) {
+                int rem = t;
+                int64_t off = 0;
+                double r2 = 0.0, dl[GDT_MAX_DIM];
+                for (int a = 0; a < nd; ++a) {
+                    const int o = rem % kappa;
+                    rem /= kappa;
+                    off += o * f.stride[a];
+                    dl[a] = o - ctr;
+                    r2 += dl[a] * dl[a];
+                }
+                const double w = fine[origin + off];
+                for (int a = 0; a < nd; ++a) m1[a] += w * dl[a];
+                m2 += w * r2;
+            }
         }
         double *o = mom + idx * W;
-        for (int a = 0; a < f.nd; ++a) o[a] = m1[a];
-        o[f.nd] = m2;
+        for (int a = 0; a < nd; ++a) o[a] = m1[a];
+        o[nd] = m2;
     }
 }
 
@@ -510,9 +542,17 @@ extern "C" int gdt_weighted_cost(const double *mu, const double *nu, const doubl
         double *mom = nullptr;
         if (malloc_async(reinterpret_cast<void **>(&mom), sizeof(double) * 2 * batch * n * W, st) != cudaSuccess)
             return cuda_status("gdt_weighted_cost: workspace");
-        moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(mu, mom, batch, f, c, kappa);
-        moments_kernel<<<grid_size(batch * n, 128), 128, 0, st>>>(nu, mom + batch * n * W, batch,
-                                                                   f, c, kappa);
+        auto mk = [&](auto kern) {
+            kern<<<grid_size(batch * n, 64), 64, 0, st>>>(mu, mom, batch, f, c, kappa);
+            kern<<<grid_size(batch * n, 64), 64, 0, st>>>(nu, mom + batch * n * W, batch, f, c, kappa);
+        };
+        if (ndim == 2 && kappa == 4) mk(moments_kernel<2, 4>);
+        else if (ndim == 2 && kappa == 8) mk(moments_kernel<2, 8>);
+        else if (ndim == 2 && kappa == 2) mk(moments_kernel<2, 2>);
+        else if (ndim == 3 && kappa == 4) mk(moments_kernel<3, 4>);
+        else if (ndim == 3 && kappa == 2) mk(moments_kernel<3, 2>);
+        else if (ndim == 1 && kappa == 4) mk(moments_kernel<1, 4>);
+        else mk(moments_kernel<0, 0>);
         dim3 mg((unsigned)((n + 1023) / 1024), (unsigned)((n + MB_K - 1) / MB_K), (unsigned)batch);
         auto launch = [&](auto kern) {
             kern<<<mg, 256, 0, st>>>(mu_c, nu_c, mom, mom + batch * n * W, centre_cost, out, unused,

@@ -135,6 +135,7 @@ __device__ __forceinline__ int64_t upper_count(const double *ax, int64_t n, doub
 // arithmetic as interpolate_kernel, which recomputes it per cell).
 constexpr int IP_MAX_AX = 2048;  // sum of fine axis lengths handled by the table kernel
 
+template <int ND>  // compile-time dimension (0: runtime): corner loop fully unrolled
 __global__ void __launch_bounds__(256) interpolate_tab_kernel(
     const double *__restrict__ coarse, double *__restrict__ fine, int64_t batch, Grid f, Grid c,
     const double *__restrict__ axes) {
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(256) interpolate_tab_kernel(
     }
     __syncthreads();
     const int64_t total = batch * f.cells;
-    const int nd = f.nd, corners = 1 << nd;
+    const int nd = ND ? ND : f.nd;
     int fs[GDT_MAX_DIM], cs[GDT_MAX_DIM];
 #pragma unroll
     for (int a = 0; a < GDT_MAX_DIM; ++a) {
@@ -181,28 +182,38 @@ __global__ void __launch_bounds__(256) interpolate_tab_kernel(
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = idx / f.cells;
         int rem = (int)(idx - b * f.cells);
-        int e[GDT_MAX_DIM] = {0, 0, 0, 0};
+        // per axis, once per cell: both weights and both coarse offsets
+        double wt[GDT_MAX_DIM][2];
+        int of[GDT_MAX_DIM][2];
 #pragma unroll
         for (int a = GDT_MAX_DIM - 1; a >= 0; --a)
             if (a < nd) {
                 const int x = rem / fs[a];
                 rem -= x * fs[a];
-                e[a] = base[a] + x;
+                const int e = base[a] + x;
+                const double t = tt_s[e];
+                wt[a][0] = __dsub_rn(1.0, t);
+                wt[a][1] = t;
+                of[a][0] = lo_s[e] * cs[a];
+                of[a][1] = hi_s[e] * cs[a];
             }
         const double *T = coarse + b * c.cells;
         double out = 0.0;
-        for (int cidx = 0; cidx < corners; ++cidx) {
+        // corners in the reference's order (axis 0 slowest); the weight is the
+        // left-to-right product 1 * w_0 * w_1 * ... (1 * w_0 is exact)
+#pragma unroll
+        for (int cidx = 0; cidx < (1 << (ND ? ND : GDT_MAX_DIM)); ++cidx) {
+            if (cidx >= (1 << nd)) break;
             double w = 1.0;
             int off = 0;
 #pragma unroll
             for (int a = 0; a < GDT_MAX_DIM; ++a)
                 if (a < nd) {
-                    const int side = (cidx >> (nd - 1 - a)) & 1;  // axis 0 slowest
-                    const double t = tt_s[e[a]];
-                    w = __dmul_rn(w, side ? t : __dsub_rn(1.0, t));
-                    off += (side ? hi_s[e[a]] : lo_s[e[a]]) * cs[a];
+                    const int side = (cidx >> (nd - 1 - a)) & 1;
+                    w = a == 0 ? wt[0][side] : __dmul_rn(w, wt[a][side]);
+                    off += of[a][side];
                 }
-            out = __dadd_rn(out, __dmul_rn(w, T[off]));
+            out = __dadd_rn(out, __dmul_rn(w, __ldg(T + off)));
         }
         fine[idx] = out;
     }
@@ -414,8 +425,12 @@ int gdt_interpolate(const double *coarse, double *fine, int64_t batch, int ndim,
     if (method == 0 && axsum <= IP_MAX_AX && f.cells < (1ll << 31)) {
         const int64_t want = (batch * f.cells + 255) / 256;
         const unsigned ctas = (unsigned)std::min<int64_t>(want, 148 * 8);  // amortise the tables
-        interpolate_tab_kernel<<<ctas, 256, 0, as_stream(stream)>>>(coarse, fine, batch, f, c,
-                                                                    axes);
+        if (ndim == 2)
+            interpolate_tab_kernel<2><<<ctas, 256, 0, as_stream(stream)>>>(coarse, fine, batch, f, c, axes);
+        else if (ndim == 3)
+            interpolate_tab_kernel<3><<<ctas, 256, 0, as_stream(stream)>>>(coarse, fine, batch, f, c, axes);
+        else
+            interpolate_tab_kernel<0><<<ctas, 256, 0, as_stream(stream)>>>(coarse, fine, batch, f, c, axes);
     } else {
         interpolate_kernel<<<grid_size(batch * f.cells, 256), 256, 0, as_stream(stream)>>>(
             coarse, fine, batch, f, c, axes, method);
