@@ -117,3 +117,37 @@ def test_exact_ipf_cluster_size_invariance(cfg, pairs, monkeypatch):
             for g0, g1 in zip(ref_gaps, gaps):  # the gap folds per-CTA partials: rounding only
                 if g0 is not None:
                     assert rel_close(g0, g1, 1e-12)
+
+
+def test_exact_ipf_cluster_sparse_supports(monkeypatch):
+    """Cluster and single-CTA exact IPF agree on measures with large empty
+    regions (coarse blocks without mass, units without arcs) and on failures:
+    same values or the same exception type for every pair."""
+    rng = np.random.default_rng(20260)
+    dims, kappa, B = (64, 64), 4, 6
+    N = dims[0] * dims[1]
+    mus, nus = np.zeros((B, N)), np.zeros((B, N))
+    for b in range(B):
+        for arr, shift in ((mus, 0), (nus, 17)):
+            img = np.zeros(dims)
+            # a few rectangular patches of mass; everything else exactly zero
+            for _ in range(3 + b % 3):
+                x0, y0 = rng.integers(0, 48, 2)
+                w, h = rng.integers(3, 16, 2)
+                img[x0:x0 + w, y0:y0 + h] += rng.random((min(w, 64 - x0), min(h, 64 - y0)))
+            img = np.roll(img, shift, axis=b % 2)
+            arr[b] = (img / img.sum()).reshape(-1, order="F")
+    outs = {}
+    for csz in (1, 2, 4):
+        monkeypatch.setenv("GRIDOT_IPF_CLUSTER", str(csz))
+        outs[csz] = G.quantized_bounds(mus, nus, dims, kappa, 2.0, xi=0.0, max_iter=30,
+                                       precision="fp64", methods=("primal_upscaling",),
+                                       return_exceptions=True)
+    for csz in (2, 4):
+        for b in range(B):
+            r0, r1 = outs[1][b]["primal_upscaling"], outs[csz][b]["primal_upscaling"]
+            if isinstance(r0, Exception):
+                assert type(r1) is type(r0), (csz, b, r0, r1)
+            else:
+                assert not isinstance(r1, Exception), (csz, b, r1)
+                assert r1.raw_value == r0.raw_value and r1.iterations == r0.iterations, (csz, b)
