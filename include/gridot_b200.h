@@ -125,6 +125,8 @@ int gdt_weighted_cost(const double *mu, const double *nu, const double *mu_c,
  *                 by C-bar (whose numerator is sum mu_t nu_s C_ts); one fine
  *                 pass: the weighted TV
  *   tv_w          [N] tv_weights of the padded grid (measures.py:289-296); nullable
+ *                 (the fine-level TV kernel reads it when given, else computes
+ *                 the weights per cell with the same formula)
  *   bmap          [N] int32 coarse block of each padded cell (block_index_map,
  *                 measures.py:248-254); nullable.  Without any of these the
  *                 fine-level kernels run.
@@ -142,6 +144,12 @@ int gdt_weighted_cost(const double *mu, const double *nu, const double *mu_c,
  *   max_iter      sweep cap (>= 1)
  *   cost_table    [max_sq+1] rho^p by integer squared distance for pricing
  *                 (required when p is neither 1 nor 2, else may be NULL)
+ *                 GDT_MODE_EXACT with a uniform kernel spreads each pair over a
+ *                 thread-block cluster of floor(SMs / batch) <= 8 CTAs when the
+ *                 coarse grid has >= 128 blocks and kappa is 2, 4 or 8 (every
+ *                 unit sum still runs in the reference's order: results do not
+ *                 depend on the cluster size); the environment variable
+ *                 GRIDOT_IPF_CLUSTER=<1..8> forces the size (1: one CTA per pair)
  *   mode          GDT_MODE_EXACT: IPF in the reference's order, fp64 pricing
  *                 costs; GDT_MODE_FAST: same IPF, p = 1 pricing costs from
  *                 fp32 sqrt (transport term within ~1e-7)
