@@ -269,3 +269,20 @@ def test_coarse_primal_fixed_sweeps_tracks_exact(cfg, k, p, max_iter):
         for key in ("delta_mu", "delta_nu"):
             assert abs(e.components[key] - f.components[key]) <= 1e-6 * max(1.0, e.value)
         assert abs(e.value - f.value) <= 1e-5 * abs(e.value), (b, e.value, f.value)
+
+
+def test_dadd_chain_probe_reports_a_latency():
+    """gdt_probe_dadd_chain (the latency denominator of the exact IPF's unit
+    sums): cycles per dependent fp64 add of one warp, a few cycles at least
+    and far below a memory round trip."""
+    torch = pytest.importorskip("torch")
+    from paper_2506_00976_b200 import _native as N
+
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        N.check(N.lib().gdt_probe_dadd_chain(4096, N.ptr(out), None), "probe")
+        torch.cuda.synchronize()
+    per_add = int(out[0]) / 4096.0
+    assert 2.0 < per_add < 64.0, per_add
+    with pytest.raises(Exception):
+        N.check(N.lib().gdt_probe_dadd_chain(4, N.ptr(out), None), "probe")
