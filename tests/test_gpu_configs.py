@@ -151,3 +151,4 @@ def test_exact_ipf_cluster_sparse_supports(monkeypatch):
             else:
                 assert not isinstance(r1, Exception), (csz, b, r1)
                 assert r1.raw_value == r0.raw_value and r1.iterations == r0.iterations, (csz, b)
+
