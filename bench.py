@@ -399,6 +399,15 @@ def run_b200(args):
     # stream, forked from and joined back into the current one, so the
     # latency-bound small kernels of one overlap the big ones of another
     streams = [torch.cuda.Stream() for _ in stages]
+    # C-bar of a coarser level is pooled from a finer level's (same p, fp32
+    # mode, nested blocks: engine.cbar_parent), as quantized_bounds_many does:
+    # that combination's stream waits for its parent's C-bar
+    parents = []
+    for ci, (_, _, bt, _) in enumerate(stages):
+        par = E.cbar_parent(bt, [st_[2] for st_ in stages[:ci]], computed=False)
+        parents.append(None if par is None else
+                       next(j for j, st_ in enumerate(stages) if st_[2] is par))
+    cbar_done = [torch.cuda.Event() for _ in stages]
 
     def step(events, concurrent=len(stages) > 1):  # one combination: nothing to overlap
         nonlocal launches_per_step
@@ -432,9 +441,15 @@ def run_b200(args):
             bt.pool()
             launches += 2 + (0 if bt.pdims == bt.dims else 2)
             ev[1].record(sc)
-            E._cbar(bt)
-            # moments x2 + C-bar (p = 2); fp32 diag C-bar: nu pad, 2 reciprocals + C-bar
-            launches += 3 if bt.p == 2.0 else (4 if bt.mode == 1 else 1)
+            if parents[ci] is not None:
+                sc.wait_event(cbar_done[parents[ci]])
+                E._cbar(bt, stages[parents[ci]][2])
+                launches += 1  # the pooling kernel
+            else:
+                E._cbar(bt)
+                # moments x2 + C-bar (p = 2); fp32 diag C-bar: nu pad, 2 reciprocals + C-bar
+                launches += 3 if bt.p == 2.0 else (4 if bt.mode == 1 else 1)
+            cbar_done[ci].record(sc)
             ev[2].record(sc)
             E.launch_primal(bt, dp, wl.max_iter)
             # ipf_fast + TV/moments + pricing + finish (fp32 mode); the exact
@@ -695,6 +710,10 @@ def run_b200(args):
                                "joined into the timed stream; stage_ms from a serial pass")
                               if len(stages) > 1 else "one stream",
                    "graph": graph_note,
+                   "cbar_pooled": {f"k{stages[ci][0]}_p{stages[ci][1]:g}":
+                                   f"from k{stages[pj][0]}_p{stages[pj][1]:g} (nested blocks: the "
+                                   "numerator is additive; gdt_weighted_cost_pool)"
+                                   for ci, pj in enumerate(parents) if pj is not None},
                    "serial_ms_per_step": round(serial_ms, 4),
                    "streams_match_serial": streams_match,
                    "stage_ms": {f"k{k}_p{p:g}_{nm}": round(v, 4)

@@ -106,6 +106,22 @@ int gdt_weighted_cost(const double *mu, const double *nu, const double *mu_c,
                       uint8_t *unused, int64_t batch, int ndim, const int64_t *dims,
                       int kappa, double p, int mode, void *stream);
 
+/* C-bar at pooling factor kappa_c = factor * kappa_f from the C-bar at
+ * kappa_f (same padded grid): the numerator of costs.py:128-171 is additive
+ * over the factor^d fine-level blocks of each coarse block,
+ *   C-bar_KL = sum_{k in K, l in L} C-bar_kl mu~_k nu~_l / (mu~_K nu~_L),
+ * so a second O(N^2) pass over the fine cells is not needed when both levels
+ * are requested (fp64 arithmetic; the result carries the rounding of
+ * cbar_fine, so the engine uses it in fp32 mode only).
+ *   cbar_fine [batch, nf, nf], mu_cf, nu_cf [batch, nf]: level kappa_f
+ *   mu_c, nu_c [batch, n], centre_cost [n, n], out [batch, n, n],
+ *   unused [batch, n, n] (uint8, nullable): level kappa_c
+ *   cdims_fine [ndim]: coarse grid of level kappa_f (multiples of factor) */
+int gdt_weighted_cost_pool(const double *cbar_fine, const double *mu_cf, const double *nu_cf,
+                           const double *mu_c, const double *nu_c, const double *centre_cost,
+                           double *out, uint8_t *unused, int64_t batch, int ndim,
+                           const int64_t *cdims_fine, int factor, void *stream);
+
 /* ---- K5/K6: primal upscaling (IPF + pricing + TV) --------------------- */
 
 /* Block-sparse primal upscaling of a coarse plan, refit by IPF to the fine

@@ -32,6 +32,7 @@ _SIGNATURES = {
     "gdt_sumpool_f64": (I32, [P, P, I64, I32, P, I32, P]),
     "gdt_sumpool_stats_f64": (I32, [P, P, P, I64, I32, P, I32, P]),
     "gdt_weighted_cost": (I32, [P, P, P, P, P, P, I64, P, P, I64, I32, P, I32, D, I32, P]),
+    "gdt_weighted_cost_pool": (I32, [P, P, P, P, P, P, P, P, I64, I32, P, I32, P]),
     "gdt_primal_scratch_bytes": (I64, [I64, I32, P, I32, I32]),
     "gdt_primal_upscale": (I32, [P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I32, P, I64, D,
                                  I64, I32, P, I32, P, I64, I32, P, P, P, P]),

@@ -641,3 +641,104 @@ extern "C" int gdt_weighted_cost(const double *mu, const double *nu, const doubl
                                                       out, unused, f, c, kappa, m, p, KT, LT);
     return cuda_status("gdt_weighted_cost");
 }
+
+// ---------------------------------------------------------------------------
+// C-bar of a coarser level from the C-bar of a finer one (nested blocks).
+//
+// With kappa_c = factor * kappa_f every coarse block K is the union of
+// factor^d fine-level blocks k, and the numerator of C-bar (costs.py:128-171)
+// is additive over them:
+//   sum_{x in X_K, y in Y_L} C mu_x nu_y = sum_{k in K, l in L} C-bar_kl mu~_k nu~_l,
+// so C-bar at kappa_c follows from C-bar at kappa_f in O(n_f^2) instead of a
+// second O(N^2) pass over the fine cells.  One thread per (K, L): the
+// children in ascending fine-coarse order (fixed: deterministic), fp64.
+// Entries with mu~_K nu~_L == 0 take the centre cost, as in gdt_weighted_cost.
+// ---------------------------------------------------------------------------
+namespace gdt {
+
+template <int ND>
+__global__ void __launch_bounds__(256) cbar_pool_kernel(
+    const double *__restrict__ cf, const double *__restrict__ mu_cf,
+    const double *__restrict__ nu_cf, const double *__restrict__ mu_c,
+    const double *__restrict__ nu_c, const double *__restrict__ centre,
+    double *__restrict__ out, uint8_t *__restrict__ unused, int64_t batch, Grid gf, Grid gc,
+    int factor) {
+    const int64_t n = gc.cells, nf = gf.cells;
+    const int64_t total = batch * n * n;
+    const int kids = (int)ipow(factor, ND);
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = idx / (n * n);
+        const int64_t r = idx - b * n * n;
+        const int64_t K = r / n, L = r - K * n;
+        // origins (fine-coarse flat index of the first child) of K and L
+        int64_t ko = 0, lo = 0;
+        {
+            int64_t kk = K, ll = L;
+#pragma unroll
+            for (int a = 0; a < ND; ++a) {
+                ko += (kk % gc.n[a]) * factor * gf.stride[a];
+                lo += (ll % gc.n[a]) * factor * gf.stride[a];
+                kk /= gc.n[a];
+                ll /= gc.n[a];
+            }
+        }
+        const double *cb = cf + b * nf * nf;
+        const double *mf = mu_cf + b * nf, *vf = nu_cf + b * nf;
+        double acc = 0.0;
+        for (int ci = 0; ci < kids; ++ci) {
+            int64_t k = ko;
+            {
+                int rem = ci;
+#pragma unroll
+                for (int a = 0; a < ND; ++a) {
+                    k += (rem % factor) * gf.stride[a];
+                    rem /= factor;
+                }
+            }
+            const double mk = mf[k];
+            if (mk == 0.0) continue;  // weight zero: the entry is the centre cost, unused
+            const double *row = cb + k * nf;
+            for (int cj = 0; cj < kids; ++cj) {
+                int64_t l = lo;
+                int rem = cj;
+#pragma unroll
+                for (int a = 0; a < ND; ++a) {
+                    l += (rem % factor) * gf.stride[a];
+                    rem /= factor;
+                }
+                acc += __ldg(row + l) * (mk * vf[l]);
+            }
+        }
+        const double den = __dmul_rn(mu_c[b * n + K], nu_c[b * n + L]);
+        const bool un = den == 0.0;
+        out[idx] = un ? centre[K * n + L] : acc / den;
+        if (unused) unused[idx] = un ? 1 : 0;
+    }
+}
+
+}  // namespace gdt
+
+extern "C" int gdt_weighted_cost_pool(const double *cbar_fine, const double *mu_cf,
+                                      const double *nu_cf, const double *mu_c,
+                                      const double *nu_c, const double *centre_cost,
+                                      double *out, uint8_t *unused, int64_t batch, int ndim,
+                                      const int64_t *cdims_fine, int factor, void *stream) {
+    Grid gf, gc;
+    GDT_CHECK_ARG(factor >= 2 && make_grid(gf, ndim, cdims_fine) && make_coarse(gc, gf, factor),
+                  "gdt_weighted_cost_pool: fine-level coarse dims must be positive multiples of factor");
+    GDT_CHECK_ARG(batch >= 0 && cbar_fine && mu_cf && nu_cf && mu_c && nu_c && centre_cost && out,
+                  "gdt_weighted_cost_pool: null argument");
+    if (batch == 0) return GDT_OK;
+    cudaStream_t st = as_stream(stream);
+    const unsigned ctas = grid_size(batch * gc.cells * gc.cells, 256);
+    auto go = [&](auto kern) {
+        kern<<<ctas, 256, 0, st>>>(cbar_fine, mu_cf, nu_cf, mu_c, nu_c, centre_cost, out, unused,
+                                   batch, gf, gc, factor);
+    };
+    if (ndim == 1) go(cbar_pool_kernel<1>);
+    else if (ndim == 2) go(cbar_pool_kernel<2>);
+    else if (ndim == 3) go(cbar_pool_kernel<3>);
+    else go(cbar_pool_kernel<4>);
+    return cuda_status("gdt_weighted_cost_pool");
+}

@@ -115,7 +115,35 @@ class _Batch:
 # ---------------------------------------------------------------------------
 
 
-def _cbar(bt: _Batch):
+def cbar_parent(bt: "_Batch", done, computed: bool = True):
+    """A batch among `done` (their C-bar already computed, same masses) whose
+    C-bar can be pooled into bt's: fp32 mode, p != 2 (the O(N^2) fp32 kernel),
+    the same padded grid and a pooling factor dividing bt's -- the largest such
+    factor.  None otherwise."""
+    if bt.mode != 1 or bt.p == 2.0:
+        return None
+    best = None
+    for o in done:
+        if (o is not bt and (o.cbar_dev is not None or not computed) and o.mode == 1
+                and o.p == bt.p
+                and o.pdims == bt.pdims and o.B == bt.B and o.kappa < bt.kappa
+                and bt.kappa % o.kappa == 0 and (best is None or o.kappa > best.kappa)):
+            best = o
+    return best
+
+
+def _cbar(bt: _Batch, parent: "_Batch | None" = None):
+    if parent is not None:
+        # nested blocks: the numerator of C-bar is additive over the parent's
+        # blocks (costs.py:128-171), no second pass over the fine cells
+        t = bt.t
+        out = t.empty((bt.B, bt.n, bt.n), dtype=t.float64, device=bt.dev)
+        N.check(N.lib().gdt_weighted_cost_pool(
+            N.ptr(parent.cbar_dev), N.ptr(parent.mu_c), N.ptr(parent.nu_c), N.ptr(bt.mu_c),
+            N.ptr(bt.nu_c), N.ptr(bt.ctil_dev), N.ptr(out), None, bt.B, bt.d,
+            N.i64s(parent.cdims), bt.kappa // parent.kappa, stream()), "gdt_weighted_cost_pool")
+        bt.cbar_dev = out
+        return out, None
     # p == 2: C-bar from fp64 block moments in both precisions (the quadratic
     # cost factorises; <= ~1e-14 relative per entry against the reference's
     # summation, far inside fp64 mode's 1e-9 bound contract); p != 2: the
@@ -351,7 +379,7 @@ def _pipeline(batches, methods, lp_threads, device_fn, timings=None):
         for i in order:
             if not need_cbar:
                 break
-            vals, _ = _cbar(batches[i])
+            vals, _ = _cbar(batches[i], cbar_parent(batches[i], [batches[j] for j in order]))
             pinned[i][0].copy_(vals, non_blocking=True)
             torch().cuda.current_stream(vals.device).synchronize()
             qs = [slot[(i, b, "cbar")] for b in range(batches[i].B)
@@ -848,7 +876,11 @@ def quantized_bounds_many(mus, nus, dims, combos, *, precision="fp64", xi=None,
     combinations' LPs first), which keeps every core busy where one batch per
     combination leaves the tail of each wave idle.  Results and their values
     are those of one ``quantized_bounds`` call per combination (the same LPs,
-    pivot paths and device kernels); ``BoundReport.wall_time`` is the whole
+    pivot paths and device kernels), with one exception in fp32 mode: for
+    p != 2, C-bar at a pooling factor that is a multiple of another requested
+    one on the same padded grid is pooled from that finer C-bar (the numerator
+    is additive over nested blocks) instead of a second pass over the fine
+    cells -- equal to rounding, inside the fp32 contract; ``BoundReport.wall_time`` is the whole
     call's wall time per pair and combination.  ``max_chunk_pairs`` and
     ``plans_out`` as in :func:`quantized_bounds`.
 

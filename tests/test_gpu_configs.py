@@ -84,9 +84,19 @@ def test_many_combos_equal_single_calls():
     for k, p in wl.combos:
         one = G.quantized_bounds(mus, nus, wl.dims, k, p, precision="fp32",
                                  return_exceptions=False)
+        # (8, p != 2): the many-call pools C-bar from the kappa = 4 C-bar of
+        # the same call (nested blocks; gdt_weighted_cost_pool), the single
+        # call runs the fp32 kernel on the fine cells: both inside the fp32
+        # contract, not bit-equal.  C-bar prices the weighted-cost bound and
+        # the fp32-mode primal transport term.
+        pooled = k == 8 and p != 2.0
         for b in range(6):
             for m in G.QUANT_METHODS:
-                assert many[(k, p)][b][m].raw_value == one[b][m].raw_value, (k, p, b, m)
+                a_, b_ = many[(k, p)][b][m].raw_value, one[b][m].raw_value
+                if pooled and m in ("weighted_cost", "primal_upscaling"):
+                    assert rel_close(a_, b_, 4e-6), (k, p, b, m, a_, b_)
+                else:
+                    assert a_ == b_, (k, p, b, m)
 
 
 @pytest.mark.parametrize("cfg,pairs", [(2, 4), (3, 3), (4, 2), (5, 4)])

@@ -286,3 +286,38 @@ def test_dadd_chain_probe_reports_a_latency():
     assert 2.0 < per_add < 64.0, per_add
     with pytest.raises(Exception):
         N.check(N.lib().gdt_probe_dadd_chain(4, N.ptr(out), None), "probe")
+
+
+@pytest.mark.parametrize("dims,kf,kc,p", [((64, 64), 4, 8, 1.0), ((32, 32), 2, 8, 1.5),
+                                           ((16, 16, 16), 2, 4, 1.0)])
+def test_cbar_pooled_from_finer_level(dims, kf, kc, p):
+    """gdt_weighted_cost_pool: C-bar at kappa_c from the C-bar at kappa_f (the
+    numerator is additive over nested blocks).  From the exact fp64 C-bar it
+    reproduces the exact C-bar at kappa_c to rounding; from the fp32-mode C-bar
+    it stays inside the fp32 contract; empty blocks take the centre cost."""
+    import paper_2506_00976_b200.engine as E
+
+    rng = np.random.default_rng(7)
+    N_ = int(np.prod(dims))
+    mus, nus = rng.random((3, N_)), rng.random((3, N_))
+    mus[0, : N_ // 3] = 0.0  # a pair with empty blocks on the source side
+    nus[0, -(N_ // 4):] = 0.0
+    mus /= mus.sum(1, keepdims=True)
+    nus /= nus.sum(1, keepdims=True)
+    for precision, tol in (("fp64", 1e-12), ("fp32", 1e-5)):
+        fine = E.make_batch(mus, nus, dims, kf, p, precision=precision)
+        coarse = E.make_batch(mus, nus, dims, kc, p, precision=precision)
+        E._cbar(fine)
+        direct = to_host(E._cbar(E.make_batch(mus, nus, dims, kc, p, precision="fp64"))[0])
+        pooled = to_host(E._cbar(coarse, fine)[0])
+        assert np.all(np.isfinite(pooled))
+        err = np.abs(pooled - direct) / np.maximum(np.abs(direct), 1e-300)
+        assert err.max() <= tol, (precision, err.max())
+    # the engine picks the parent only in fp32 mode, for p != 2
+    f32 = E.make_batch(mus, nus, dims, kf, p, precision="fp32")
+    c32 = E.make_batch(mus, nus, dims, kc, p, precision="fp32")
+    assert E.cbar_parent(c32, [f32]) is None  # not computed yet
+    E._cbar(f32)
+    assert E.cbar_parent(c32, [f32]) is f32
+    assert E.cbar_parent(E.make_batch(mus, nus, dims, kc, p, precision="fp64"), [f32]) is None
+    assert E.cbar_parent(E.make_batch(mus, nus, dims, kc, 2.0, precision="fp32"), [f32]) is None
