@@ -663,58 +663,68 @@ __global__ void __launch_bounds__(256) cbar_pool_kernel(
     const double *__restrict__ nu_c, const double *__restrict__ centre,
     double *__restrict__ out, uint8_t *__restrict__ unused, int64_t batch, Grid gf, Grid gc,
     int factor) {
-    const int64_t n = gc.cells, nf = gf.cells;
-    const int64_t total = batch * n * n;
+    // grid: y = (pair, coarse row K), x * 256 + thread = coarse column L
+    // (32-bit index arithmetic; consecutive threads read adjacent children)
+    __shared__ int koff[64];    // flat fine-coarse offsets of the children of a block
+    __shared__ double mks[64];  // mu~ of the children of K
+    const int n = (int)gc.cells, nf = (int)gf.cells;
     const int kids = (int)ipow(factor, ND);
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = idx / (n * n);
-        const int64_t r = idx - b * n * n;
-        const int64_t K = r / n, L = r - K * n;
-        // origins (fine-coarse flat index of the first child) of K and L
-        int64_t ko = 0, lo = 0;
-        {
-            int64_t kk = K, ll = L;
+    const int64_t b = blockIdx.y / n;
+    const int K = (int)(blockIdx.y - b * n);
+    int cn[ND], fs[ND];
 #pragma unroll
-            for (int a = 0; a < ND; ++a) {
-                ko += (kk % gc.n[a]) * factor * gf.stride[a];
-                lo += (ll % gc.n[a]) * factor * gf.stride[a];
-                kk /= gc.n[a];
-                ll /= gc.n[a];
-            }
-        }
-        const double *cb = cf + b * nf * nf;
-        const double *mf = mu_cf + b * nf, *vf = nu_cf + b * nf;
-        double acc = 0.0;
-        for (int ci = 0; ci < kids; ++ci) {
-            int64_t k = ko;
-            {
-                int rem = ci;
-#pragma unroll
-                for (int a = 0; a < ND; ++a) {
-                    k += (rem % factor) * gf.stride[a];
-                    rem /= factor;
-                }
-            }
-            const double mk = mf[k];
-            if (mk == 0.0) continue;  // weight zero: the entry is the centre cost, unused
-            const double *row = cb + k * nf;
-            for (int cj = 0; cj < kids; ++cj) {
-                int64_t l = lo;
-                int rem = cj;
-#pragma unroll
-                for (int a = 0; a < ND; ++a) {
-                    l += (rem % factor) * gf.stride[a];
-                    rem /= factor;
-                }
-                acc += __ldg(row + l) * (mk * vf[l]);
-            }
-        }
-        const double den = __dmul_rn(mu_c[b * n + K], nu_c[b * n + L]);
-        const bool un = den == 0.0;
-        out[idx] = un ? centre[K * n + L] : acc / den;
-        if (unused) unused[idx] = un ? 1 : 0;
+    for (int a = 0; a < ND; ++a) {
+        cn[a] = (int)gc.n[a];
+        fs[a] = (int)gf.stride[a];
     }
+    int ko = 0;
+    {
+        int kk = K;
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+            ko += (kk % cn[a]) * factor * fs[a];
+            kk /= cn[a];
+        }
+    }
+    for (int ci = threadIdx.x; ci < kids; ci += blockDim.x) {
+        int off = 0, rem = ci;
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+            off += (rem % factor) * fs[a];
+            rem /= factor;
+        }
+        koff[ci] = off;
+        mks[ci] = mu_cf[b * nf + ko + off];
+    }
+    __syncthreads();
+    const int L = blockIdx.x * blockDim.x + threadIdx.x;
+    if (L >= n) return;
+    int lo = 0;
+    {
+        int ll = L;
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+            lo += (ll % cn[a]) * factor * fs[a];
+            ll /= cn[a];
+        }
+    }
+    const double *cb = cf + b * (int64_t)nf * nf;
+    const double *vf = nu_cf + b * nf + lo;
+    double acc = 0.0;
+    for (int ci = 0; ci < kids; ++ci) {
+        const double mk = mks[ci];
+        if (mk == 0.0) continue;  // weight zero: the entry is the centre cost, unused
+        const double *row = cb + (int64_t)(ko + koff[ci]) * nf + lo;
+        for (int cj = 0; cj < kids; ++cj) {
+            const int o = koff[cj];
+            acc += __ldg(row + o) * (mk * __ldg(vf + o));
+        }
+    }
+    const int64_t idx = (b * n + K) * (int64_t)n + L;
+    const double den = __dmul_rn(mu_c[b * n + K], nu_c[b * n + L]);
+    const bool un = den == 0.0;
+    out[idx] = un ? centre[(int64_t)K * n + L] : acc / den;
+    if (unused) unused[idx] = un ? 1 : 0;
 }
 
 }  // namespace gdt
@@ -731,9 +741,13 @@ extern "C" int gdt_weighted_cost_pool(const double *cbar_fine, const double *mu_
                   "gdt_weighted_cost_pool: null argument");
     if (batch == 0) return GDT_OK;
     cudaStream_t st = as_stream(stream);
-    const unsigned ctas = grid_size(batch * gc.cells * gc.cells, 256);
+    GDT_CHECK_ARG(ipow(factor, ndim) <= 64 && gf.cells < (1ll << 31) &&
+                      batch * gc.cells < (1ll << 31),
+                  "gdt_weighted_cost_pool: factor^ndim must be <= 64, grids below 2^31 blocks");
+    const int thr = gc.cells >= 256 ? 256 : (int)((gc.cells + 31) / 32 * 32);
+    const dim3 grid((unsigned)((gc.cells + thr - 1) / thr), (unsigned)(batch * gc.cells));
     auto go = [&](auto kern) {
-        kern<<<ctas, 256, 0, st>>>(cbar_fine, mu_cf, nu_cf, mu_c, nu_c, centre_cost, out, unused,
+        kern<<<grid, thr, 0, st>>>(cbar_fine, mu_cf, nu_cf, mu_c, nu_c, centre_cost, out, unused,
                                    batch, gf, gc, factor);
     };
     if (ndim == 1) go(cbar_pool_kernel<1>);
