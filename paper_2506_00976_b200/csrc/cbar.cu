@@ -663,14 +663,14 @@ __global__ void __launch_bounds__(256) cbar_pool_kernel(
     const double *__restrict__ nu_c, const double *__restrict__ centre,
     double *__restrict__ out, uint8_t *__restrict__ unused, int64_t batch, Grid gf, Grid gc,
     int factor) {
-    // grid: y = (pair, coarse row K), x * 256 + thread = coarse column L
+    // grid: x = (pair, coarse row K), y * blockDim + thread = coarse column L
     // (32-bit index arithmetic; consecutive threads read adjacent children)
     __shared__ int koff[64];    // flat fine-coarse offsets of the children of a block
     __shared__ double mks[64];  // mu~ of the children of K
     const int n = (int)gc.cells, nf = (int)gf.cells;
     const int kids = (int)ipow(factor, ND);
-    const int64_t b = blockIdx.y / n;
-    const int K = (int)(blockIdx.y - b * n);
+    const int64_t b = blockIdx.x / n;
+    const int K = (int)(blockIdx.x - b * n);
     int cn[ND], fs[ND];
 #pragma unroll
     for (int a = 0; a < ND; ++a) {
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(256) cbar_pool_kernel(
         mks[ci] = mu_cf[b * nf + ko + off];
     }
     __syncthreads();
-    const int L = blockIdx.x * blockDim.x + threadIdx.x;
+    const int L = blockIdx.y * blockDim.x + threadIdx.x;
     if (L >= n) return;
     int lo = 0;
     {
@@ -745,7 +745,8 @@ extern "C" int gdt_weighted_cost_pool(const double *cbar_fine, const double *mu_
                       batch * gc.cells < (1ll << 31),
                   "gdt_weighted_cost_pool: factor^ndim must be <= 64, grids below 2^31 blocks");
     const int thr = gc.cells >= 256 ? 256 : (int)((gc.cells + 31) / 32 * 32);
-    const dim3 grid((unsigned)((gc.cells + thr - 1) / thr), (unsigned)(batch * gc.cells));
+    const dim3 grid((unsigned)(batch * gc.cells), (unsigned)((gc.cells + thr - 1) / thr));
+    GDT_CHECK_ARG(grid.y <= 65535u, "gdt_weighted_cost_pool: coarse grid too large");
     auto go = [&](auto kern) {
         kern<<<grid, thr, 0, st>>>(cbar_fine, mu_cf, nu_cf, mu_c, nu_c, centre_cost, out, unused,
                                    batch, gf, gc, factor);

@@ -2556,7 +2556,7 @@ __global__ void sum_parts_kernel(const double *__restrict__ part, int count, dou
 constexpr int CT = 512;       // threads of primal_coarse_kernel
 constexpr int CB_HEAVY = 8;  // arcs above which a block's sum goes to a warp
 enum { CB_MLO, CB_MHI, CB_NLO, CB_NHI, CB_CMU, CB_CNU, CB_S, CB_B, CB_K0, CB_K1, CB_KTA, CB_RK,
-       CB_S1, CB_RK1, CB_NF };
+       CB_S1, CB_NF };
 
 struct CoarsePlan {
     int rp, cp, rcol, rcoef, crow, ccoef, arow, heavy, perm, blk, total;
@@ -2721,9 +2721,10 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
     double *Bmlo = blk + CB_MLO * n, *Bmhi = blk + CB_MHI * n, *Bnlo = blk + CB_NLO * n,
            *Bnhi = blk + CB_NHI * n, *Bcmu = blk + CB_CMU * n, *Bcnu = blk + CB_CNU * n,
            *BB = blk + CB_B * n, *KTA = blk + CB_KTA * n;
-    // S_k and 1 / kb of the current sweep and, written by the row pass, of the next
+    // S_k of the current sweep and, written by the row pass, of the next; 1 / kb
+    // is read and replaced by the same thread of the row pass (no second buffer)
     double *BS = blk + CB_S * n, *RK = blk + CB_RK * n;
-    double *BSn = blk + CB_S1 * n, *RKn = blk + CB_RK1 * n;
+    double *BSn = blk + CB_S1 * n;
     double *Kcur = blk + CB_K0 * n, *Knext = blk + CB_K1 * n;
 
     // ---- the pair's coarse plan and block statistics into shared memory
@@ -2846,7 +2847,7 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
                 if (s <= 0.0) r.flags |= 1;
                 else sn = div_shared(mcb[k], s, rn);
             }
-            RKn[k] = rn;  // the next sweep's a = mu / kb'
+            RK[k] = rn;  // the next sweep's a = mu / kb'
             BSn[k] = sn;
         }
         EX_TRACE(5);
@@ -2876,9 +2877,6 @@ __global__ void __launch_bounds__(CT, 1) primal_coarse_kernel(
         t = BS;
         BS = BSn;
         BSn = t;
-        t = RK;
-        RK = RKn;
-        RKn = t;
     }
     // ---- pricing: the fitted coarse plan S_k (m W) B_l against C-bar (flat
     //      over the arcs: balanced; per-thread partials in a fixed order)
