@@ -3064,7 +3064,9 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
     if (fast_ipf && cbar != nullptr && mu_c != nullptr && nu_c != nullptr && stats != nullptr &&
         tv_w != nullptr && bmap_in != nullptr) {
         const CoarsePlan plan = coarse_plan((int)c.cells);
-        if (plan.total <= 200 * 1024) {
+        // (<= 190 KB of dynamic shared memory: Nsight Compute reserves part of an SM's
+        // shared memory, a 194 KB launch failed under its graph replay)
+        if (plan.total <= 190 * 1024) {
             // the whole primal stage at the coarse level: sweeps + pricing
             // (one CTA per pair), the weighted-TV pass (grid-wide), the fold
             const int n = (int)c.cells;
@@ -3106,7 +3108,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
         // vector, else batches of up to 20480 (160 KB)
         const int64_t prods = 2 * c.cells * (f.cells / c.cells);
         const int64_t base = use_smem ? ((f.cells + 1) & ~1ll) : 0;
-        const int64_t room = (200 * 1024) / (int64_t)sizeof(double) - base;
+        const int64_t room = (184 * 1024) / (int64_t)sizeof(double) - base;  // see the 190 KB note above
         const int64_t capd = std::min<int64_t>(prods, std::min<int64_t>(room, 20480));
         if (capd >= std::min<int64_t>(prods, 4096)) {
             prod_smem = (int)(capd & ~1ll);
@@ -3185,7 +3187,7 @@ extern "C" int gdt_primal_upscale(const double *mu, const double *nu, const doub
             // products of one CTA's units in one batch when they fit 160 KB
             const int64_t prods = 2 * c.cells * (f.cells / c.cells);
             // (shared memory also holds 3.5 U + 2 doubles of pointers, sums and origins)
-            const int64_t room = (200 * 1024) / 8 - (3 * c.cells + 2 + (c.cells + 1) / 2);
+            const int64_t room = (184 * 1024) / 8 - (3 * c.cells + 2 + (c.cells + 1) / 2);
             const int cap = (int)(std::min<int64_t>(
                                       room, std::min<int64_t>(20480, ((prods / csz + 4095) / 2048) * 2048 +
                                                                          CL_SKEW * c.cells)) &

@@ -29,7 +29,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 echo "launches exit $?" >> gpurun_out/ncu_launches.log
 timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:"cbar_diag|pruned_ct_tab|primal_coarse|tv_pass|sep_tile|cbar_moments|interpolate_tab" -c 14 \
+    -k regex:"cbar_diag|pruned_ct_tab|primal_coarse|tv_pass|sep_tile|cbar_moments|interpolate_tab|cbar_pool" -c 16 \
     -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full exit $?" >> gpurun_out/ncu_full.log
 timeout 600 bash scripts/gpu_prof_k.sh 5 "ipf_cluster|moments_tv|run_list_par|sep_tile" cfg5_ipf 4 > gpurun_out/prof_cfg5.log 2>&1
