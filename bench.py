@@ -534,7 +534,7 @@ def run_b200(args):
         step(ev, concurrent=False)
         serial_events.append(ev)
     torch.cuda.synchronize()
-    serial_ms = statistics.mean(ev[-1][0].elapsed_time(ev[-1][1]) for ev in serial_events)
+    serial_ms = statistics.median(ev[-1][0].elapsed_time(ev[-1][1]) for ev in serial_events)
     # the concurrent schedule must not change a single bit of the outputs
     streams_match = all(torch.equal(a, dp.prim_out) and torch.equal(b, dp.dots)
                         for (a, b), (_, _, _, dp) in zip(conc_out, stages))
@@ -561,10 +561,14 @@ def run_b200(args):
         print(f"launch count: profiler unavailable ({exc}); using the hand count",
               file=sys.stderr)
     step_ms = [ev[-1][0].elapsed_time(ev[-1][1]) for ev in all_events]
-    stage_ms = {}  # (combo, stage) -> mean ms
+    # (combo, stage) -> ms: the MEDIAN over the serial steps -- the first
+    # kernel after the L2 flush sometimes runs into the flush's write-back
+    # (one step of five at 0.9 ms instead of 0.65 ms), which a mean carries
+    # into the roofline fractions
+    stage_ms = {}
     for ci, (k, p, _, _) in enumerate(stages):
         for si, nm in enumerate(names):
-            stage_ms[(k, p, nm)] = statistics.mean(
+            stage_ms[(k, p, nm)] = statistics.median(
                 ev[ci][si].elapsed_time(ev[ci][si + 1]) for ev in serial_events)
     ms = statistics.mean(step_ms)
     if world > 1:
@@ -707,7 +711,7 @@ def run_b200(args):
                    "lp": "coarse LP plans precomputed on the host (timed in e2e)",
                    "setup_s": t_setup,
                    "streams": ("one CUDA stream per (kappa, p) combination, forked from and "
-                               "joined into the timed stream; stage_ms from a serial pass")
+                               "joined into the timed stream; stage_ms = median over a serial pass")
                               if len(stages) > 1 else "one stream",
                    "graph": graph_note,
                    "cbar_pooled": {f"k{stages[ci][0]}_p{stages[ci][1]:g}":
