@@ -661,6 +661,22 @@ def run_b200(args):
                      (traffic("ipf_cluster_kernel") or traffic("ipf_kernel")),
                      "traffic_source": tsrc, "sweeps": sweeps, "stage_ms": round(prim_ms, 4)})
 
+    # the pooled C-bar (nested levels): a pure streaming pass, against HBM
+    pool_roof = None
+    for ci, pj in enumerate(parents):
+        if pj is None:
+            continue
+        kc, pc, btc, _ = stages[ci]
+        btf = stages[pj][2]
+        nbytes = 8.0 * ppr * (btf.n * btf.n + btc.n * btc.n + 2 * btf.n + 2 * btc.n) + 8.0 * btc.n ** 2
+        t_ms = stage_ms[(kc, pc, "cbar")]
+        pool_roof = {"bound": "hbm", "kernel": f"cbar_pool_kernel (C-bar kappa={kc} from kappa={stages[pj][0]}, p={pc:g})",
+                     "achieved": nbytes / (t_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+                     "frac": nbytes / (t_ms / 1000.0) / 1e9 / hbm,
+                     "traffic": traffic("cbar_pool_kernel"), "traffic_source": tsrc,
+                     "work": "8 (n_f^2 + n^2) bytes per pair: the finer C-bar read once, the "
+                             "coarser one written (plus the coarse masses and centre costs)",
+                     "stage_ms": round(t_ms, 4)}
     ct_roofs = {}
     for (k, p_, nm), v in stage_ms.items():
         if nm in ("ct_target", "ct_source") and p_ != 2.0:
@@ -722,7 +738,8 @@ def run_b200(args):
                    "streams_match_serial": streams_match,
                    "stage_ms": {f"k{k}_p{p:g}_{nm}": round(v, 4)
                                 for (k, p, nm), v in sorted(stage_ms.items())}},
-        "roofline": rl, "roofline_ipf": ipf_roof, "roofline_ctransform": ct_roof, "clocks": clk,
+        "roofline": rl, "roofline_ipf": ipf_roof, "roofline_ctransform": ct_roof,
+        "roofline_cbar_pool": pool_roof, "clocks": clk,
         "peaks_measured": {k: round(v, 2) for k, v in probes.items()},
         "gpu_launches": launches_per_step * args.steps,
     }

@@ -11,7 +11,7 @@ PY
 cp $G/launches.csv $P/r02_cfg3_launches.csv
 python -c "import json,sys; d=json.loads(open('$G/ct_trace.json').read().strip().splitlines()[-1]); json.dump(d, open('$P/r02_ct_tiles.json','w'))" || echo 'ct_trace.json invalid: profiles/r02_ct_tiles.json kept'
 python scripts/summarize_profile.py $G/launches.csv $G/prof_full.raw.csv $P/r02_cfg3_ncu.md $P/r02_bench_cfg3.json >/dev/null
-python scripts/ncu_traffic.py 3 $G/prof_full.raw.csv > /dev/null
+python scripts/ncu_traffic.py 3 $G/prof_full.raw.csv $G/prof_cfg3_pool.raw.csv > /dev/null
 python scripts/ncu_traffic.py 1 $G/prof_cfg1_ipf.raw.csv > /dev/null
 python scripts/ncu_traffic.py 4 $G/prof_cfg4_coarse.raw.csv >/dev/null
 python scripts/ncu_traffic.py 5 $G/prof_cfg5_ipf.raw.csv > /dev/null

@@ -35,6 +35,7 @@ echo "full exit $?" >> gpurun_out/ncu_full.log
 timeout 600 bash scripts/gpu_prof_k.sh 5 "ipf_cluster|moments_tv|run_list_par|sep_tile" cfg5_ipf 4 > gpurun_out/prof_cfg5.log 2>&1
 timeout 600 bash scripts/gpu_prof_k.sh 1 "ipf_kernel" cfg1_ipf 1 > gpurun_out/prof_cfg1.log 2>&1
 timeout 600 bash scripts/gpu_prof_k.sh 4 "primal_coarse|tv_pass" cfg4_coarse 2 > gpurun_out/prof_cfg4.log 2>&1
+timeout 600 bash scripts/gpu_prof_k.sh 3 "cbar_pool" cfg3_pool 2 > gpurun_out/prof_cfg3_pool.log 2>&1
 CMD64="python bench.py --precision fp64 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD64 > gpurun_out/prof_fp64_plain.json 2> gpurun_out/prof_fp64_plain.err && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cbar_exact2d|pruned_ct_kernel" -c 2 \
