@@ -154,7 +154,7 @@ struct PairPtrs {
     double *aA, *aB, *b, *kb, *kta;
     // uniform kernel: the walk of every unit precomputed once per launch as
     // runs (first cell, coefficient mass * W), arc q owning runs
-    // [q * K1, (q + 1) * K1), K1 = kappa^(d-1) (run_list_kernel)
+    // [q * K1, (q + 1) * K1), K1 = kappa^(d-1) (run_list_par_kernel)
     const int32_t *rrc, *crc;
     const double *rrf, *crf;
     int pf;  // the gathered vector is in global memory: prefetch runs into L1
@@ -695,43 +695,14 @@ __device__ __forceinline__ void cell_pass_col(const PairPtrs &P, const G32 &f,
 }
 
 // The uniform kernel's walk of every row / column unit, once per launch:
-// run r of arc q (CSR order) -> first fine cell and coefficient mass * W.
-// One thread per (pair, unit); dir 0 = row units, 1 = column units.
-__global__ void run_list_kernel(const int64_t *__restrict__ arc_off,
-                                const int32_t *__restrict__ ptr, const int64_t *__restrict__ pc,
-                                const double *__restrict__ mass, const double *__restrict__ W,
-                                int64_t batch, G32 f, G32 c, int kappa,
-                                int32_t *__restrict__ cells, double *__restrict__ coefs) {
-    const int n = c.cells;
-    const int K1 = (int)ipow(kappa, f.nd - 1);
-    const double Wu = W[0];
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < batch * n;
-         g += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = g / n;
-        const int u = (int)(g - b * n);
-        const int64_t a0 = arc_off[b];
-        const int32_t *pp = ptr + b * (n + 1);
-        const int lo = pp[u], hi = pp[u + 1];
-        int32_t *oc = cells + (a0 + lo) * K1;
-        double *of = coefs + (a0 + lo) * K1;
-        const double *ms = mass + a0 + lo;
-        int r = 0;
-        auto fn = [&](int q, int cell, int) {
-            oc[r] = cell;
-            of[r] = __dmul_rn(ms[q], Wu);
-            ++r;
-        };
-        walk_blocks(pc + a0 + lo, hi - lo, c, f, kappa, fn);
-    }
-}
-
-// The same run lists without the serial walk, one thread per ARC: the
+// run r of arc q (CSR order) -> first fine cell, coefficient mass * W and
+// product slot, one thread per ARC: the
 // position of run (arc q, offsets s_{d-1..1}) in its unit's walk order follows
 // from the coordinate groups q belongs to (per level the walk visits the
 // groups of equal coarse coordinate in order and, inside a group, the kappa
 // fine offsets one after the other), so a thread finds its arc's groups once
-// (a scan over the unit's arcs) and then writes its K1 runs.  Output
-// identical to run_list_kernel.
+// (a scan over the unit's arcs) and then writes its K1 runs (the order
+// `walk` enumerates: lexicographic over (l_{d-1}, s_{d-1}, ..., l_0)).
 struct RunListArgs {  // one direction: CSR (rows) or CSC (columns) of the coarse plans
     const int32_t *ptr;
     const int64_t *pc;
