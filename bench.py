@@ -22,6 +22,7 @@ oracle/_ref/ by build()) on all host cores, on the same seeded pairs.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -408,8 +409,20 @@ def run_b200(args):
         parents.append(None if par is None else
                        next(j for j, st_ in enumerate(stages) if st_[2] is par))
     cbar_done = [torch.cuda.Event() for _ in stages]
+    # inside a combination the dual chain (f_ext, interpolation, the two
+    # c-transforms) needs only the plans and the masses, not C-bar or the
+    # primal stage: it runs on a second stream of the combination, forked
+    # after the SumPool (at cfg4 the 45-CTA IPF kernel then overlaps the
+    # c-transforms instead of idling 100 SMs)
+    # Measured: cfg4 1.79 -> 1.59 ms, cfg5 0.685 -> 0.553 ms; with four
+    # combinations already on four streams the extra streams only add
+    # contention (cfg3 2.22 -> 2.27 ms), so the split is used for
+    # single-combination configs.
+    split_dual = len(stages) == 1
+    dual_streams = [torch.cuda.Stream() if split_dual else None for _ in stages]
+    pool_done = [torch.cuda.Event() for _ in stages]
 
-    def step(events, concurrent=len(stages) > 1):  # one combination: nothing to overlap
+    def step(events, concurrent=True):
         nonlocal launches_per_step
         launches = 0
         base = torch.cuda.current_stream()  # the capture stream under graph capture
@@ -417,13 +430,13 @@ def run_b200(args):
         for ci, (k, p, bt, dp) in enumerate(stages):
             ev = events[ci]
             if not concurrent:  # stage timing pass: everything on one stream
-                launches += combo(ci, k, p, bt, dp, ev, base)
+                launches += combo(ci, k, p, bt, dp, ev, base, None)
                 continue
             sc = streams[ci]
             sc.wait_stream(base)
             with torch.cuda.stream(sc):
-                launches += combo(ci, k, p, bt, dp, ev, sc)
-        for sc in streams if concurrent else ():
+                launches += combo(ci, k, p, bt, dp, ev, sc, dual_streams[ci])
+        for sc in (streams + [x for x in dual_streams if x is not None]) if concurrent else ():
             base.wait_stream(sc)
         events[-1][1].record(base)  # step end
         launches_per_step = launches
@@ -434,13 +447,15 @@ def run_b200(args):
 
     no_events = [[_NoEvent()] * 7 for _ in stages] + [[_NoEvent()] * 2]
 
-    def combo(ci, k, p, bt, dp, ev, sc):
+    def combo(ci, k, p, bt, dp, ev, sc, sd):
         launches = 0
         if True:
             ev[0].record(sc)
             bt.pool()
             launches += 2 + (0 if bt.pdims == bt.dims else 2)
             ev[1].record(sc)
+            if sd is not None:
+                pool_done[ci].record(sc)
             if parents[ci] is not None:
                 sc.wait_event(cbar_done[parents[ci]])
                 E._cbar(bt, stages[parents[ci]][2])
@@ -456,13 +471,17 @@ def run_b200(args):
             # path adds two arc-coordinate packs and the block map
             launches += (4 if bt.mode == 1 else 7) + (0 if bt.p == 2.0 else 1)  # + arc rows
             ev[3].record(sc)
-            E.launch_dual_prep(bt, dp)
-            launches += 2
-            ev[4].record(sc)
-            E.launch_ctransform(bt, dp, 0)
-            ev[5].record(sc)
-            E.launch_ctransform(bt, dp, 1)
-            ev[6].record(sc)
+            if sd is not None:
+                sd.wait_event(pool_done[ci])
+            with (torch.cuda.stream(sd) if sd is not None else contextlib.nullcontext()):
+                sx = sd if sd is not None else sc
+                E.launch_dual_prep(bt, dp)
+                launches += 2
+                ev[4].record(sx)
+                E.launch_ctransform(bt, dp, 0)
+                ev[5].record(sx)
+                E.launch_ctransform(bt, dp, 1)
+                ev[6].record(sx)
             # separable passes + dot (p = 2); fp32 pruned: cost table, tile max,
             # pruned kernel, dot, plus one f64->f32 conversion of f_hat
             per_ct = (bt.d + 1) if bt.p == 2.0 else (4 if dp.dt == 1 else 2)
@@ -726,9 +745,11 @@ def run_b200(args):
                    "l2": "flushed (256 MB write) between timed steps",
                    "lp": "coarse LP plans precomputed on the host (timed in e2e)",
                    "setup_s": t_setup,
-                   "streams": ("one CUDA stream per (kappa, p) combination, forked from and "
-                               "joined into the timed stream; stage_ms = median over a serial pass")
-                              if len(stages) > 1 else "one stream",
+                   "streams": (("two CUDA streams (SumPool, C-bar, primal | dual chain, forked after "
+                                "the SumPool)" if split_dual else
+                                "one CUDA stream per (kappa, p) combination") +
+                               ", forked from and joined into the timed stream; stage_ms = median "
+                               "over a serial pass"),
                    "graph": graph_note,
                    "cbar_pooled": {f"k{stages[ci][0]}_p{stages[ci][1]:g}":
                                    f"from k{stages[pj][0]}_p{stages[pj][1]:g} (nested blocks: the "
