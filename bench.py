@@ -417,7 +417,9 @@ def run_b200(args):
     # Measured: cfg4 1.79 -> 1.59 ms, cfg5 0.685 -> 0.553 ms; with four
     # combinations already on four streams the extra streams only add
     # contention (cfg3 2.22 -> 2.27 ms), so the split is used for
-    # single-combination configs.
+    # single-combination configs.  (fp64 mode, C-bar moved to the dual stream
+    # too -- the primal stage does not price with it there: cfg5 0.553 -> 0.567
+    # ms, not kept.)
     split_dual = len(stages) == 1
     dual_streams = [torch.cuda.Stream() if split_dual else None for _ in stages]
     pool_done = [torch.cuda.Event() for _ in stages]
