@@ -424,10 +424,13 @@ def run_b200(args):
     dual_streams = [torch.cuda.Stream() if split_dual else None for _ in stages]
     pool_done = [torch.cuda.Event() for _ in stages]
 
+    base_stream = [None]
+
     def step(events, concurrent=True):
         nonlocal launches_per_step
         launches = 0
         base = torch.cuda.current_stream()  # the capture stream under graph capture
+        base_stream[0] = base
         events[-1][0].record(base)  # step start
         for ci, (k, p, bt, dp) in enumerate(stages):
             ev = events[ci]
@@ -451,34 +454,40 @@ def run_b200(args):
 
     def combo(ci, k, p, bt, dp, ev, sc, sd):
         launches = 0
-        if True:
-            ev[0].record(sc)
-            bt.pool()
-            launches += 2 + (0 if bt.pdims == bt.dims else 2)
-            ev[1].record(sc)
-            if sd is not None:
-                pool_done[ci].record(sc)
+        ev[0].record(sc)
+        bt.pool()
+        launches += 2 + (0 if bt.pdims == bt.dims else 2)
+        ev[1].record(sc)
+        if sd is not None:
+            pool_done[ci].record(sc)
+
+        def upper():  # C-bar, then the primal stage (fp32 mode prices with C-bar)
+            n_l = 0
             if parents[ci] is not None:
                 sc.wait_event(cbar_done[parents[ci]])
                 E._cbar(bt, stages[parents[ci]][2])
-                launches += 1  # the pooling kernel
+                n_l += 1  # the pooling kernel
             else:
                 E._cbar(bt)
                 # moments x2 + C-bar (p = 2); fp32 diag C-bar: nu pad, 2 reciprocals + C-bar
-                launches += 3 if bt.p == 2.0 else (4 if bt.mode == 1 else 1)
+                n_l += 3 if bt.p == 2.0 else (4 if bt.mode == 1 else 1)
             cbar_done[ci].record(sc)
             ev[2].record(sc)
             E.launch_primal(bt, dp, wl.max_iter)
             # ipf_fast + TV/moments + pricing + finish (fp32 mode); the exact
             # path adds two arc-coordinate packs and the block map
-            launches += (4 if bt.mode == 1 else 7) + (0 if bt.p == 2.0 else 1)  # + arc rows
+            n_l += (4 if bt.mode == 1 else 7) + (0 if bt.p == 2.0 else 1)  # + arc rows
             ev[3].record(sc)
+            return n_l
+
+        def lower():  # the dual chain: needs the plans and the masses only
+            n_l = 0
             if sd is not None:
                 sd.wait_event(pool_done[ci])
             with (torch.cuda.stream(sd) if sd is not None else contextlib.nullcontext()):
                 sx = sd if sd is not None else sc
                 E.launch_dual_prep(bt, dp)
-                launches += 2
+                n_l += 2
                 ev[4].record(sx)
                 E.launch_ctransform(bt, dp, 0)
                 ev[5].record(sx)
@@ -487,7 +496,15 @@ def run_b200(args):
             # separable passes + dot (p = 2); fp32 pruned: cost table, tile max,
             # pruned kernel, dot, plus one f64->f32 conversion of f_hat
             per_ct = (bt.d + 1) if bt.p == 2.0 else (4 if dp.dt == 1 else 2)
-            launches += 2 * per_ct + (1 if bt.p != 2.0 and dp.dt == 1 else 0)
+            return n_l + 2 * per_ct + (1 if bt.p != 2.0 and dp.dt == 1 else 0)
+
+        # a combination whose C-bar is pooled from another one's runs its dual
+        # chain first instead of waiting for the parent's C-bar (concurrent
+        # schedule only: the serial stage-timing pass keeps the stage order)
+        if parents[ci] is not None and sc is not base_stream[0]:
+            launches += lower() + upper()
+        else:
+            launches += upper() + lower()
         return launches
 
     def new_events():
