@@ -162,3 +162,34 @@ def test_exact_ipf_cluster_sparse_supports(monkeypatch):
                 assert not isinstance(r1, Exception), (csz, b, r1)
                 assert r1.raw_value == r0.raw_value and r1.iterations == r0.iterations, (csz, b)
 
+
+
+@pytest.mark.parametrize("dims,kappa,p", [((48, 40), 2, 2.0), ((24, 24, 24), 2, 1.0),
+                                          ((96, 96), 8, 1.0), ((50, 46), 4, 2.0),
+                                          ((64, 32), 2, 1.5)])
+def test_exact_ipf_cluster_random_grids(dims, kappa, p, monkeypatch):
+    """Cluster sizes 1 (single-CTA kernel), 2 and 5 on grids outside the
+    benchmark shapes: kappa = 2 and 8, three dimensions, rectangular and
+    non-divisible (zero-padded) grids, default xi (early convergence) -- the
+    primal bound, its components and the sweep count must not depend on the
+    cluster size."""
+    rng = np.random.default_rng(sum(dims) * 7 + kappa)
+    N_ = int(np.prod(dims))
+    mus = rng.random((3, N_)) ** 3 + 1e-9
+    nus = rng.random((3, N_)) ** 3 + 1e-9
+    mus /= mus.sum(1, keepdims=True)
+    nus /= nus.sum(1, keepdims=True)
+    ref = None
+    for csz in (1, 2, 5):
+        monkeypatch.setenv("GRIDOT_IPF_CLUSTER", str(csz))
+        out = G.quantized_bounds(mus, nus, dims, kappa, p, max_iter=60, precision="fp64",
+                                 methods=("primal_upscaling",), return_exceptions=False)
+        rec = [(r["primal_upscaling"].raw_value, r["primal_upscaling"].iterations,
+                r["primal_upscaling"].components["transport"],
+                r["primal_upscaling"].components["delta_mu"],
+                r["primal_upscaling"].components["delta_nu"],
+                r["primal_upscaling"].components["converged"]) for r in out]
+        if ref is None:
+            ref = rec
+        else:
+            assert rec == ref, (dims, kappa, p, csz)
